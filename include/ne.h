@@ -1,0 +1,250 @@
+/*
+ * ne.h — C ABI of the B200 numerical-entanglement hot path (libne.so).
+ *
+ * Method: Anam & Andreopoulos, "Reliable Linear, Sesquilinear and Bijective
+ * Operations on Integer Data Streams via Numerical Entanglement",
+ * arXiv 1604.04740.  "P:L" cites line L of the paper text; the
+ * readings of garbled passages (R1..R17) are listed in DESIGN.md.
+ *
+ * Pipeline (Fig. 3):  c --entangle--> eps --LSB op--> delta
+ *                                  --disentangle + check / recover--> d_hat
+ *
+ * Conventions for every call
+ * --------------------------
+ * Ownership  All element pointers are DEVICE pointers allocated and owned by
+ *            the caller (PyTorch in this repo).  libne never allocates, frees
+ *            or synchronises; every call only enqueues kernels on `stream`
+ *            and returns.  Workspaces are sized by a query call and owned by
+ *            the caller.
+ * Layout     SoA: a stream set is an array of M device pointers, one
+ *            contiguous stream each (ne_streams / ne_cstreams /
+ *            ne_cstreams32, passed BY VALUE, M <= NE_MAX_M).  "AoS" buffers
+ *            interleave the M streams position-major: x[n*M + m].  Matrices
+ *            are row-major and dense.  Every stream pointer must be 16-byte
+ *            aligned (128-bit vector access) or the call returns NE_EINVAL.
+ * Words      w = 64 only: entangled and output values are int64 held in
+ *            64-bit two's-complement containers; plain
+ *            inputs are int32.  LSB ops wrap mod 2^64, which is exact for
+ *            every certified (in-range) result (reading R9).
+ * Errors     Two channels.  (1) The returned ne_status, synchronous: argument
+ *            and configuration errors, and CUDA launch errors
+ *            (cudaGetLastError) as NE_ECUDA.  (2) Data-dependent outcomes —
+ *            range violations of the inputs and positions flagged
+ *            by the reliability check — are
+ *            accumulated into a caller-owned DEVICE struct ne_diag, read by
+ *            the caller after synchronising.  Reset it with ne_diag_reset.
+ * Threading  No global mutable state; all calls are re-entrant.
+ */
+#ifndef NE_H
+#define NE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NE_MAX_M 32
+
+typedef struct cudaStream_st* ne_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+/* (M, w, l, k): M streams, w-bit words, shift l, guard k (Eq. 12). */
+typedef struct {
+  int32_t M, w, l, k;
+} ne_config;
+
+typedef enum {
+  NE_OK = 0,
+  NE_EINVAL = 1,          /* bad pointer, alignment, size or stream count          */
+  NE_ECONFIG = 2,         /* infeasible or unsupported (M, w, l, k)               */
+  NE_ERANGE = 3,          /* certification: the op's output bound exceeds range  */
+  NE_EINDEX = 4,          /* excluded stream r outside [0, M)                     */
+  NE_EUNRECOVERABLE = 5,  /* more than one stream absent for recovery             */
+  NE_ECUDA = 6,           /* a CUDA launch failed                                 */
+  NE_ENOTSUP = 7          /* shape not supported by the selected kernel           */
+} ne_status;
+
+typedef struct { int64_t* s[NE_MAX_M]; } ne_streams;
+typedef struct { const int64_t* s[NE_MAX_M]; } ne_cstreams;
+typedef struct { const int32_t* s[NE_MAX_M]; } ne_cstreams32;
+
+/* Device-resident diagnostics (SPEC error list: range error naming (m,n),
+ * fault positions).  first_* are INT64_MAX when nothing was recorded. */
+typedef struct {
+  unsigned long long range_violations; /* inputs with |c| > hi (a0)              */
+  long long first_bad;                 /* min flat index m*n_total + n of those  */
+  unsigned long long fault_positions;  /* positions flagged by the check (a5)    */
+  long long first_fault;               /* min flagged position                   */
+} ne_diag;
+
+typedef enum { NE_GEMM_TC_I8 = 0, NE_GEMM_IMAD64 = 1 } ne_gemm_algo;
+typedef enum { NE_OP_SCALE = 0, NE_OP_ADD = 1, NE_OP_LINEAR = 2, NE_OP_PERMUTE = 3 } ne_op_kind;
+
+/* ======================================================== a0: host only === */
+
+/* (l, k) maximising (M-2)l + k subject to (M-1)l + k <= w and 1 <= k <= l
+ * (Eq. 12; Table II); ties -> larger l (reading R5).
+ * Errors: NE_ECONFIG if M < 3, M > NE_MAX_M or infeasible; NE_EINVAL if out NULL. */
+ne_status ne_config_for(int32_t M, int32_t w, ne_config* out);
+
+/* Admissible output range [-hi, hi]: min(Eq. 13, Eq. 11
+ * when M = 3) (reading R6).  Errors: NE_ECONFIG for an invalid config. */
+ne_status ne_dynamic_range(const ne_config* cfg, int64_t* hi);
+
+/* Worst-case output bound of one LSB op on inputs bounded by in_bound
+ * (Remark 2): SCALE -> in*|s|, ADD -> in + max|g|, LINEAR
+ * (inner/conv/gemm row) -> in * ||g||_1, PERMUTE -> in.  *out_bound gets the
+ * bound; returns NE_ERANGE if it exceeds the dynamic range (chain ops by
+ * feeding out_bound back in). */
+ne_status ne_certify(const ne_config* cfg, ne_op_kind op, int64_t in_bound, int64_t operand,
+                     int64_t* out_bound);
+
+/* Number of balanced signed base-2^8 limbs that represent every entangled
+ * value (2^l + 1) * in_bound exactly (the GEMM operand split). */
+int32_t ne_gemm_limbs_for(const ne_config* cfg, int64_t in_bound);
+
+/* Fill a device ne_diag with {0, INT64_MAX, 0, INT64_MAX}. */
+ne_status ne_diag_reset(ne_diag* diag, ne_stream_t stream);
+
+/* ============================================== a1/a2: entanglement ====== */
+
+/* Eq. 15 with the circulant operator of Eq. 14 (Eq. 7 for M = 3):
+ *   eps_m[n] = c_m[n] + S_l{ c_{(m-1) mod M}[n] },  0 <= n < n_total.
+ * c: M int32 streams (read once each).  eps: M int64 streams (may NOT alias c).
+ * Fused range assertion (a0): every |c_m[n]| <= hi, else diag.range_violations
+ * is incremented and diag.first_bad = min(m*n_total + n).  diag may be NULL. */
+ne_status ne_entangle(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, ne_streams eps,
+                      ne_diag* diag, ne_stream_t stream);
+
+/* Same values, written position-major ("AoS"): eps_aos[n*M + m] — M int64 of
+ * one position share DRAM sectors, so a gather by a permutation touches one
+ * sector per position for M = 4.  eps_aos: 16-B aligned. */
+ne_status ne_entangle_aos(const ne_config* cfg, ne_cstreams32 c, int64_t n_total,
+                          int64_t* eps_aos, ne_diag* diag, ne_stream_t stream);
+
+/* Same values, written as L balanced signed base-2^8 digit planes (the int8
+ * operand of the tensor-core GEMM): planes[((m*L) + i)*n_total + n] = d_i with
+ * eps = sum_i 2^(8i) d_i, d_i in [-128, 127].  A value that L digits cannot
+ * represent counts as a range violation.  n_total must be a multiple of 16. */
+ne_status ne_entangle_limbs(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t L,
+                            int8_t* planes, ne_diag* diag, ne_stream_t stream);
+
+/* One stream only (the per-GPU entanglement of the one-stream-per-GPU layout,
+ * P:608-611): eps_m[n] = c_m[n] + S_l{ c_prev[n] } with c_prev = c_{(m-1) mod M}.
+ * Range check covers c_m only (first_bad = m*n_total + n). */
+ne_status ne_entangle_stream(const ne_config* cfg, int32_t m, const int32_t* c_m,
+                             const int32_t* c_prev, int64_t* eps_m, int64_t n_total,
+                             ne_diag* diag, ne_stream_t stream);
+
+/* Footnote P:507-511: the shared operand of +/- self-entangled,
+ * g_ent[n] = S_l{g[n]} + g[n]. */
+ne_status ne_entangle_shared(const ne_config* cfg, const int32_t* g, int64_t* g_ent,
+                             int64_t n_total, ne_stream_t stream);
+
+/* ========================================= a3: LSB ops on entangled data === */
+/* Eq. 9: delta_m = eps_m op g, the same routine on every stream
+ * (P:380-386).  All arithmetic wraps mod 2^64.                              */
+
+/* Element-wise x (Eq. 2 "x"): x_m[n] *= (g ? g[n] : s), in place. */
+ne_status ne_op_scale(const ne_config* cfg, ne_streams x, int64_t n_total, int64_t s,
+                      const int32_t* g_or_null, ne_stream_t stream);
+
+/* Element-wise +/- (Eq. 2 "+,-"): x_m[n] += sign * a_m[n], in place, with the
+ * addend already entangled (ne_entangle, or ne_entangle_shared broadcast by
+ * passing the same pointer M times) (reading R10).  sign = +1/-1. */
+ne_status ne_op_add(const ne_config* cfg, ne_streams x, ne_cstreams addend, int64_t n_total,
+                    int32_t sign, ne_stream_t stream);
+
+/* Blocked inner product <.,.> (Eq. 2): out_m[b] = sum_{i in block b}
+ * x_m[i] * v[i mod vlen], b < ceil(n_total/block) (ragged last block). */
+ne_status ne_op_inner(const ne_config* cfg, ne_cstreams x, int64_t n_total, const int32_t* v,
+                      int64_t vlen, int64_t block, ne_streams out, ne_stream_t stream);
+
+/* Outer product (x) (Eq. 2): out_m[i*n2 + j] = x_m[i] * h[j]. */
+ne_status ne_op_outer(const ne_config* cfg, ne_cstreams x, int64_t n1, const int32_t* h,
+                      int64_t n2, ne_streams out, ne_stream_t stream);
+
+/* Circular convolution (correlate = 0) / cross-correlation (correlate = 1)
+ * (reading R12): out_m[n] = sum_{j<taps} g[j] x_m[(n -/+ j) mod n_total].
+ * out must not alias x. */
+ne_status ne_op_conv(const ne_config* cfg, ne_cstreams x, int64_t n_total, const int32_t* g,
+                     int32_t taps, int32_t correlate, ne_streams out, ne_stream_t stream);
+
+/* Permutation (bijection I -> G, reading R11), gather:
+ * out_m[i] = x_m[perm[i]].  perm must be a bijection of [0, n_total). */
+ne_status ne_op_permute(const ne_config* cfg, ne_cstreams x, const int32_t* perm,
+                        int64_t n_total, ne_streams out, ne_stream_t stream);
+
+/* Integer matrix product (reading R13): C_m = A_m * B for every
+ * stream m, A_m rows x K (entangled, int64), B K x cols (plain int32, shared
+ * kernel g, unmodified), C_m rows x cols int64.  algo NE_GEMM_IMAD64 runs on
+ * the CUDA cores; NE_GEMM_TC_I8 splits A_m into L balanced int8 limb planes
+ * and B into one int8 plane and runs tcgen05.mma kind::i8 with exact int32
+ * limb accumulators, recombined in int64.  ws: workspace
+ * of ne_gemm_workspace() bytes (TC only).  Entries of B outside [-128,127]
+ * or of A_m outside the L-limb range count in diag.range_violations (TC). */
+ne_status ne_gemm_workspace(const ne_config* cfg, int64_t rows, int64_t cols, int64_t K,
+                            int32_t L, size_t* bytes);
+ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int64_t rows,
+                     int64_t cols, int64_t K, ne_gemm_algo algo, int32_t L, ne_streams C,
+                     void* ws, size_t ws_bytes, ne_diag* diag, ne_stream_t stream);
+
+/* The tensor-core GEMM on operands already in limb form: planes from
+ * ne_entangle_limbs (M*L planes of rows x K int8, K contiguous) and Bt from
+ * ne_gemm_prep_b (cols x K int8, K contiguous).  rows % 128 == 0,
+ * cols % 128 == 0, K % 128 == 0, K <= 131072 (int32 limb sums stay exact). */
+ne_status ne_gemm_prep_b(const int32_t* B, int64_t K, int64_t cols, int8_t* Bt, ne_diag* diag,
+                         ne_stream_t stream);
+ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes, int32_t L,
+                           const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams C,
+                           ne_stream_t stream);
+
+/* ====================================== a4-a6: disentangle, check, recover === */
+
+/* Eqs. 16-19 (readings R1-R3) excluding stream r, then the
+ * reliability check of Eq. 21 (Eq. 20 for M = 3), at every
+ * position, in exact 2w-bit (int128) arithmetic:
+ *   d_out_m[n]  = low 64 bits of the disentangled d_hat_m[n]
+ *   flag[n]     = delta_r[n] != d_hat_r[n] + S_l{ d_hat_{(r-1) mod M}[n] }
+ * bitmap (nullable): bit (n mod 32) of word n/32 = flag[n] (ceil(n_total/32)
+ * words, fully written).  diag (nullable): fault_positions += #flags,
+ * first_fault = min flagged n.  Errors: NE_EINDEX if r outside [0, M). */
+ne_status ne_disentangle_check(const ne_config* cfg, ne_cstreams delta, int64_t n_total,
+                               int32_t r, ne_streams d_out, uint32_t* bitmap, ne_diag* diag,
+                               ne_stream_t stream);
+
+/* Fail-stop recovery (Props 1/3): Eqs. 16-19 excluding
+ * the absent stream r (delta.s[r] == NULL, never read).  Errors:
+ * NE_EUNRECOVERABLE if any other delta.s[m] is NULL. */
+ne_status ne_recover(const ne_config* cfg, ne_cstreams delta, int64_t n_total, int32_t r,
+                     ne_streams d_out, ne_stream_t stream);
+
+/* Fused permutation + blocked inner product + disentangle/check (the C4 hot
+ * path): for block b, delta_m[b] = sum_{i<block} x_m[perm[b*block+i]] * v[i mod vlen]
+ * (perm NULL = identity), then d_out / bitmap / diag exactly as
+ * ne_disentangle_check on delta (r excluded).  x is AoS (x_aos[n*M + m],
+ * aos = 1) or SoA (x.s[m], aos = 0).  delta_out (nullable) receives delta. */
+ne_status ne_op_permute_inner_check(const ne_config* cfg, ne_cstreams x, const int64_t* x_aos,
+                                    int32_t aos, const int32_t* perm, int64_t n_total,
+                                    const int32_t* v, int64_t vlen, int64_t block, int32_t r,
+                                    ne_streams delta_out, ne_streams d_out, uint32_t* bitmap,
+                                    ne_diag* diag, ne_stream_t stream);
+
+/* ============================================== a7: fault injection (test) === */
+
+/* x[idx] ^= mask (one 64-bit word). */
+ne_status ne_inject(int64_t* x, int64_t idx, uint64_t mask, ne_stream_t stream);
+
+/* Exhaustive single-bit sweep over the first `window` (<= 64) positions of
+ * delta: trial t = (s*window + n)*64 + bit flips bit `bit` of delta_s[n] and
+ * re-runs disentangle + check (r excluded) on positions 0..window-1.
+ * flagwords[t] = bit p set iff position p is flagged; dhat[t*M + m] = d_out_m[n].
+ * Both out arrays: M*window*64 entries (dhat: times M). */
+ne_status ne_inject_sweep(const ne_config* cfg, ne_cstreams delta, int64_t window, int32_t r,
+                          uint64_t* flagwords, int64_t* dhat, ne_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NE_H */

@@ -1,0 +1,304 @@
+"""paper_1604_04740_b200 — B200-native numerical entanglement (arXiv 1604.04740).
+
+Thin Python binding of ``libne.so`` (C ABI declared in ``include/ne.h``): the
+functions below carry the C names and only marshal arguments (torch CUDA
+tensors -> device pointers, the current CUDA stream).  Every step of the hot
+path runs in the library's sm_100a kernels.  There is no CPU fallback: if the
+library or a CUDA device is missing, the calls raise.
+
+Layout conventions: a stream set is a list of M 1-D torch tensors (int32 for
+plain inputs, int64 for entangled data / outputs), each contiguous and 16-byte
+aligned; ``diag`` is a device int64 tensor of 4 words (``ne_diag``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Sequence
+
+import torch
+
+from ._build import LIB, build  # noqa: F401  (build() is what __graft_entry__.build calls)
+
+NE_MAX_M = 32
+STATUS = {0: "NE_OK", 1: "NE_EINVAL", 2: "NE_ECONFIG", 3: "NE_ERANGE", 4: "NE_EINDEX",
+          5: "NE_EUNRECOVERABLE", 6: "NE_ECUDA", 7: "NE_ENOTSUP"}
+NE_GEMM_TC_I8, NE_GEMM_IMAD64 = 0, 1
+NE_OP_SCALE, NE_OP_ADD, NE_OP_LINEAR, NE_OP_PERMUTE = 0, 1, 2, 3
+
+# every symbol include/ne.h and include/ne_gendev.h declare (checked by tests)
+EXPORTS = (
+    "ne_config_for", "ne_dynamic_range", "ne_certify", "ne_gemm_limbs_for", "ne_diag_reset",
+    "ne_entangle", "ne_entangle_aos", "ne_entangle_limbs", "ne_entangle_stream", "ne_entangle_shared",
+    "ne_op_scale", "ne_op_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
+    "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
+    "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
+    "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
+)
+
+
+class NeError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        super().__init__(f"{fn} returned {STATUS.get(status, status)}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("M", C.c_int32), ("w", C.c_int32), ("l", C.c_int32), ("k", C.c_int32)]
+
+    def __repr__(self) -> str:
+        return f"ne_config(M={self.M}, w={self.w}, l={self.l}, k={self.k})"
+
+
+class Streams(C.Structure):  # ne_streams / ne_cstreams / ne_cstreams32 (same ABI)
+    _fields_ = [("s", C.c_void_p * NE_MAX_M)]
+
+
+_lib = None
+_PCFG = C.POINTER(Config)
+_VP = C.c_void_p
+_I64, _I32, _U64, _SZ = C.c_int64, C.c_int32, C.c_uint64, C.c_size_t
+
+_SIGS = {
+    "ne_config_for": [_I32, _I32, _PCFG],
+    "ne_dynamic_range": [_PCFG, C.POINTER(_I64)],
+    "ne_certify": [_PCFG, C.c_int, _I64, _I64, C.POINTER(_I64)],
+    "ne_gemm_limbs_for": [_PCFG, _I64],
+    "ne_diag_reset": [_VP, _VP],
+    "ne_entangle": [_PCFG, Streams, _I64, Streams, _VP, _VP],
+    "ne_entangle_aos": [_PCFG, Streams, _I64, _VP, _VP, _VP],
+    "ne_entangle_limbs": [_PCFG, Streams, _I64, _I32, _VP, _VP, _VP],
+    "ne_entangle_stream": [_PCFG, _I32, _VP, _VP, _VP, _I64, _VP, _VP],
+    "ne_entangle_shared": [_PCFG, _VP, _VP, _I64, _VP],
+    "ne_op_scale": [_PCFG, Streams, _I64, _I64, _VP, _VP],
+    "ne_op_add": [_PCFG, Streams, Streams, _I64, _I32, _VP],
+    "ne_op_inner": [_PCFG, Streams, _I64, _VP, _I64, _I64, Streams, _VP],
+    "ne_op_outer": [_PCFG, Streams, _I64, _VP, _I64, Streams, _VP],
+    "ne_op_conv": [_PCFG, Streams, _I64, _VP, _I32, _I32, Streams, _VP],
+    "ne_op_permute": [_PCFG, Streams, _VP, _I64, Streams, _VP],
+    "ne_gemm_workspace": [_PCFG, _I64, _I64, _I64, _I32, C.POINTER(_SZ)],
+    "ne_op_gemm": [_PCFG, Streams, _VP, _I64, _I64, _I64, C.c_int, _I32, Streams, _VP, _SZ, _VP, _VP],
+    "ne_gemm_prep_b": [_VP, _I64, _I64, _VP, _VP, _VP],
+    "ne_op_gemm_limbs": [_PCFG, _VP, _I32, _VP, _I64, _I64, _I64, Streams, _VP],
+    "ne_disentangle_check": [_PCFG, Streams, _I64, _I32, Streams, _VP, _VP, _VP],
+    "ne_recover": [_PCFG, Streams, _I64, _I32, Streams, _VP],
+    "ne_op_permute_inner_check": [_PCFG, Streams, _VP, _I32, _VP, _I64, _VP, _I64, _I64, _I32,
+                                  Streams, Streams, _VP, _VP, _VP],
+    "ne_inject": [_VP, _I64, _U64, _VP],
+    "ne_inject_sweep": [_PCFG, Streams, _I64, _I32, _VP, _VP, _VP],
+    "ne_gen_uniform_i32": [_U64, C.c_uint32, C.c_uint32, _I64, _I64, _I64, _I64, _VP, _VP],
+    "ne_gen_perm_i32": [_U64, C.c_uint32, _I64, _VP, _VP],
+}
+
+
+def lib() -> C.CDLL:
+    """Load libne.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"{LIB} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+        L = C.CDLL(LIB)
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _call(name: str, *args) -> int:
+    st = getattr(lib(), name)(*args)
+    if st != 0:
+        raise NeError(name, st)
+    return st
+
+
+def _stream():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1604_04740_b200 needs a CUDA device (no CPU fallback)")
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None, dtype=None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("device tensors only")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"expected {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError("contiguous tensors only")
+    return C.c_void_p(t.data_ptr())
+
+
+def _streams(ts: Sequence[torch.Tensor | None], dtype) -> Streams:
+    s = Streams()
+    for i, t in enumerate(ts):
+        s.s[i] = None if t is None else _ptr(t, dtype).value
+    return s
+
+
+# ------------------------------------------------------------------ a0 (host)
+def ne_config_for(M: int, w: int = 64) -> Config:
+    cfg = Config()
+    _call("ne_config_for", M, w, C.byref(cfg))
+    return cfg
+
+
+def ne_dynamic_range(cfg: Config) -> int:
+    hi = C.c_int64()
+    _call("ne_dynamic_range", C.byref(cfg), C.byref(hi))
+    return hi.value
+
+
+def ne_certify(cfg: Config, op: int, in_bound: int, operand: int) -> tuple[int, bool]:
+    out = C.c_int64()
+    st = lib().ne_certify(C.byref(cfg), op, in_bound, operand, C.byref(out))
+    if st not in (0, 3):
+        raise NeError("ne_certify", st)
+    return out.value, st == 0
+
+
+def ne_gemm_limbs_for(cfg: Config, in_bound: int) -> int:
+    return int(lib().ne_gemm_limbs_for(C.byref(cfg), in_bound))
+
+
+def diag_new() -> torch.Tensor:
+    d = torch.empty(4, dtype=torch.int64, device="cuda")
+    ne_diag_reset(d)
+    return d
+
+
+def ne_diag_reset(diag: torch.Tensor) -> None:
+    _call("ne_diag_reset", _ptr(diag, torch.int64), _stream())
+
+
+def diag_read(diag: torch.Tensor) -> dict:
+    v = diag.cpu().tolist()
+    big = 2 ** 63 - 1
+    return {"range_violations": v[0], "first_bad": None if v[1] == big else v[1],
+            "fault_positions": v[2], "first_fault": None if v[3] == big else v[3]}
+
+
+# ------------------------------------------------------------------ a1/a2
+def ne_entangle(cfg: Config, c: Sequence[torch.Tensor], eps: Sequence[torch.Tensor], diag=None) -> None:
+    n = c[0].numel()
+    _call("ne_entangle", C.byref(cfg), _streams(c, torch.int32), n, _streams(eps, torch.int64),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_entangle_aos(cfg: Config, c, eps_aos: torch.Tensor, diag=None) -> None:
+    _call("ne_entangle_aos", C.byref(cfg), _streams(c, torch.int32), c[0].numel(),
+          _ptr(eps_aos, torch.int64), _ptr(diag, torch.int64), _stream())
+
+
+def ne_entangle_limbs(cfg: Config, c, L: int, planes: torch.Tensor, diag=None) -> None:
+    _call("ne_entangle_limbs", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), L,
+          _ptr(planes, torch.int8), _ptr(diag, torch.int64), _stream())
+
+
+def ne_entangle_stream(cfg: Config, m: int, c_m, c_prev, eps_m, diag=None) -> None:
+    _call("ne_entangle_stream", C.byref(cfg), m, _ptr(c_m, torch.int32), _ptr(c_prev, torch.int32),
+          _ptr(eps_m, torch.int64), c_m.numel(), _ptr(diag, torch.int64), _stream())
+
+
+def ne_entangle_shared(cfg: Config, g: torch.Tensor, g_ent: torch.Tensor) -> None:
+    _call("ne_entangle_shared", C.byref(cfg), _ptr(g, torch.int32), _ptr(g_ent, torch.int64), g.numel(),
+          _stream())
+
+
+# ------------------------------------------------------------------ a3
+def ne_op_scale(cfg: Config, x, s: int = 1, g: torch.Tensor | None = None) -> None:
+    _call("ne_op_scale", C.byref(cfg), _streams(x, torch.int64), x[0].numel(), int(s), _ptr(g, torch.int32),
+          _stream())
+
+
+def ne_op_add(cfg: Config, x, addend, sign: int = 1) -> None:
+    _call("ne_op_add", C.byref(cfg), _streams(x, torch.int64), _streams(addend, torch.int64), x[0].numel(),
+          int(sign), _stream())
+
+
+def ne_op_inner(cfg: Config, x, v: torch.Tensor, block: int, out) -> None:
+    _call("ne_op_inner", C.byref(cfg), _streams(x, torch.int64), x[0].numel(), _ptr(v, torch.int32), v.numel(),
+          block, _streams(out, torch.int64), _stream())
+
+
+def ne_op_outer(cfg: Config, x, h: torch.Tensor, out) -> None:
+    _call("ne_op_outer", C.byref(cfg), _streams(x, torch.int64), x[0].numel(), _ptr(h, torch.int32), h.numel(),
+          _streams(out, torch.int64), _stream())
+
+
+def ne_op_conv(cfg: Config, x, g: torch.Tensor, out, correlate: bool = False) -> None:
+    _call("ne_op_conv", C.byref(cfg), _streams(x, torch.int64), x[0].numel(), _ptr(g, torch.int32), g.numel(),
+          int(correlate), _streams(out, torch.int64), _stream())
+
+
+def ne_op_permute(cfg: Config, x, perm: torch.Tensor, out) -> None:
+    _call("ne_op_permute", C.byref(cfg), _streams(x, torch.int64), _ptr(perm, torch.int32), x[0].numel(),
+          _streams(out, torch.int64), _stream())
+
+
+def ne_gemm_workspace(cfg: Config, rows: int, cols: int, K: int, L: int) -> int:
+    b = C.c_size_t()
+    _call("ne_gemm_workspace", C.byref(cfg), rows, cols, K, L, C.byref(b))
+    return b.value
+
+
+def ne_op_gemm(cfg: Config, A, B: torch.Tensor, rows: int, cols: int, K: int, out, algo: int = NE_GEMM_TC_I8,
+               L: int = 4, ws: torch.Tensor | None = None, diag=None) -> None:
+    _call("ne_op_gemm", C.byref(cfg), _streams(A, torch.int64), _ptr(B, torch.int32), rows, cols, K, algo, L,
+          _streams(out, torch.int64), _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_gemm_prep_b(B: torch.Tensor, K: int, cols: int, Bt: torch.Tensor, diag=None) -> None:
+    _call("ne_gemm_prep_b", _ptr(B, torch.int32), K, cols, _ptr(Bt, torch.int8), _ptr(diag, torch.int64),
+          _stream())
+
+
+def ne_op_gemm_limbs(cfg: Config, planes: torch.Tensor, L: int, Bt: torch.Tensor, rows: int, cols: int, K: int,
+                     out) -> None:
+    _call("ne_op_gemm_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, _ptr(Bt, torch.int8), rows, cols, K,
+          _streams(out, torch.int64), _stream())
+
+
+# ------------------------------------------------------------------ a4-a7
+def ne_disentangle_check(cfg: Config, delta, r: int, d_out, bitmap: torch.Tensor | None = None, diag=None) -> None:
+    _call("ne_disentangle_check", C.byref(cfg), _streams(delta, torch.int64), delta[0].numel(), r,
+          _streams(d_out, torch.int64), _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _stream())
+
+
+def ne_recover(cfg: Config, delta, r: int, d_out) -> None:
+    n = next(t for t in delta if t is not None).numel()
+    _call("ne_recover", C.byref(cfg), _streams(delta, torch.int64), n, r, _streams(d_out, torch.int64), _stream())
+
+
+def ne_op_permute_inner_check(cfg: Config, v: torch.Tensor, block: int, r: int, d_out, *, x=None,
+                              x_aos: torch.Tensor | None = None, perm: torch.Tensor | None = None,
+                              n: int | None = None, delta_out=None, bitmap=None, diag=None) -> None:
+    if n is None:
+        n = x_aos.numel() // cfg.M if x_aos is not None else x[0].numel()
+    xs = _streams(x if x is not None else [], torch.int64)
+    do = _streams(delta_out if delta_out is not None else [], torch.int64)
+    _call("ne_op_permute_inner_check", C.byref(cfg), xs, _ptr(x_aos, torch.int64), int(x_aos is not None),
+          _ptr(perm, torch.int32), n, _ptr(v, torch.int32), v.numel(), block, r, do, _streams(d_out, torch.int64),
+          _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _stream())
+
+
+def ne_inject(x: torch.Tensor, idx: int, mask: int) -> None:
+    _call("ne_inject", _ptr(x, torch.int64), idx, mask & (2 ** 64 - 1), _stream())
+
+
+def ne_inject_sweep(cfg: Config, delta, window: int, r: int, flagwords: torch.Tensor, dhat: torch.Tensor) -> None:
+    _call("ne_inject_sweep", C.byref(cfg), _streams(delta, torch.int64), window, r, _ptr(flagwords, torch.int64),
+          _ptr(dhat, torch.int64), _stream())
+
+
+# ------------------------------------------------------------------ synthetic inputs (device generator)
+def ne_gen_uniform_i32(seed: int, tag: int, gstream: int, lo: int, hi: int, out: torch.Tensor,
+                       offset: int = 0) -> None:
+    _call("ne_gen_uniform_i32", seed, tag, gstream, lo, hi, offset, out.numel(), _ptr(out, torch.int32), _stream())
+
+
+def ne_gen_perm_i32(seed: int, tag: int, out: torch.Tensor) -> None:
+    _call("ne_gen_perm_i32", seed, tag, out.numel(), _ptr(out, torch.int32), _stream())

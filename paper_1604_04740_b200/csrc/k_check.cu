@@ -1,0 +1,224 @@
+// k_check.cu — a4 disentangle, a5 reliability check, a6 fail-stop recovery,
+// a7 fault injection.  Exact 2w-bit (int128) temporaries on the device
+// (footnote P:717-720; a 64-bit compare is not enough).
+//
+// The host rotates the stream pointers so that the excluded stream r is
+// index 0 (ne::rotate); the kernels then run Eqs. 16-19 / Eq. 21 with r = 0
+// fully unrolled for M in {3, 4, 8} (generic M through local arrays).
+// Streaming layout: every thread owns 2 consecutive positions (one 128-bit
+// load/store per stream), a warp owns 64 positions = two bitmap words built
+// from two __ballot_sync masks.
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "ne_internal.cuh"
+
+namespace ne {
+
+// interleave the low 16 bits of x with zeros: bit i -> bit 2i
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x &= 0xffffu;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+template <int MT, bool CHECK>
+__global__ void __launch_bounds__(kThreads)
+k_disentangle(const __grid_constant__ ne_cstreams e, int M_rt, int l, int64_t n,
+              const __grid_constant__ ne_streams d_out, uint32_t* __restrict__ bitmap,
+              ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  const int64_t npair = (n + 1) / 2;
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  int nflag = 0;
+  long long first = LLONG_MAX;
+  // loop bound rounded up to whole warps so every lane joins the ballots
+  const int64_t npair_w = (npair + 31) & ~(int64_t)31;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < npair_w; v += stride) {
+    const int64_t n0 = 2 * v;
+    bool f0 = false, f1 = false;
+    if (n0 < n) {
+      const bool pair = n0 + 1 < n;
+      int64_t a[MA], b[MA], da[MA], db[MA];
+#pragma unroll
+      for (int j = 0; j < MA; ++j) {
+        if (MT == 0 && j >= M) break;
+        if (j == 0 && !CHECK) {
+          a[0] = b[0] = 0;
+          continue;
+        }
+        const int64_t* p = e.s[j] + n0;
+        if (pair) {
+          longlong2 q = __ldcs(reinterpret_cast<const longlong2*>(p));
+          a[j] = q.x;
+          b[j] = q.y;
+        } else {
+          a[j] = p[0];
+          b[j] = 0;
+        }
+      }
+      f0 = disentangle_rot<MT>(a, M, l, da, CHECK);
+      f1 = disentangle_rot<MT>(b, M, l, db, CHECK) && pair;
+#pragma unroll
+      for (int j = 0; j < MA; ++j) {
+        if (MT == 0 && j >= M) break;
+        int64_t* q = d_out.s[j] + n0;
+        if (pair)
+          __stcs(reinterpret_cast<longlong2*>(q), make_longlong2(da[j], db[j]));
+        else
+          q[0] = da[j];
+      }
+      if (f0) {
+        ++nflag;
+        first = n0 < first ? n0 : first;
+      }
+      if (f1) {
+        ++nflag;
+        first = (n0 + 1) < first ? (n0 + 1) : first;
+      }
+    }
+    if (CHECK && bitmap) {
+      const uint32_t b0 = __ballot_sync(0xffffffffu, f0);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, f1);
+      const int64_t w0 = (v - lane) / 16;  // 64 positions per warp -> 2 words
+      if (lane == 0 && w0 < nwords) bitmap[w0] = spread16(b0) | (spread16(b1) << 1);
+      if (lane == 1 && w0 + 1 < nwords) bitmap[w0 + 1] = spread16(b0 >> 16) | (spread16(b1 >> 16) << 1);
+    }
+  }
+  if (CHECK && diag) diag_add(&diag->fault_positions, &diag->first_fault, nflag, first);
+}
+
+// a7: exhaustive single-bit sweep.  One warp per trial; lane t owns positions
+// 2t, 2t+1 of the window; the flag word is assembled like the bitmap.
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_inject_sweep(const __grid_constant__ ne_cstreams e, int M_rt, int l, int r, int64_t window,
+               uint64_t* __restrict__ flagwords, int64_t* __restrict__ dhat) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  const int64_t trials = (int64_t)M * window * 64;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < trials; t += nwarps) {
+    const int bit = (int)(t & 63);
+    const int64_t pos = (t >> 6) % window;
+    const int s = (int)((t >> 6) / window);      // original stream index
+    const int js = (s - r + M) % M;              // its index in the rotated frame
+    bool fl[2] = {false, false};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t p = 2 * lane + h;
+      if (p < window) {
+        int64_t a[MA], d[MA];
+#pragma unroll
+        for (int j = 0; j < MA; ++j) {
+          if (MT == 0 && j >= M) break;
+          a[j] = e.s[j][p];
+          if (p == pos && j == js) a[j] ^= (int64_t)(1ull << bit);
+        }
+        fl[h] = disentangle_rot<MT>(a, M, l, d, true);
+        if (p == pos) {
+#pragma unroll
+          for (int j = 0; j < MA; ++j) {
+            if (MT == 0 && j >= M) break;
+            dhat[t * M + (r + j) % M] = d[j];
+          }
+        }
+      }
+    }
+    const uint32_t b0 = __ballot_sync(0xffffffffu, fl[0]);
+    const uint32_t b1 = __ballot_sync(0xffffffffu, fl[1]);
+    if (lane == 0) {
+      const uint64_t lo = spread16(b0) | (spread16(b1) << 1);
+      const uint64_t hi = spread16(b0 >> 16) | (spread16(b1 >> 16) << 1);
+      flagwords[t] = lo | (hi << 32);
+    }
+  }
+}
+
+__global__ void k_inject(int64_t* x, int64_t idx, uint64_t mask) { x[idx] ^= (int64_t)mask; }
+
+}  // namespace ne
+
+using namespace ne;
+
+template <typename S>
+static bool streams_ok(const S& c, int M, int skip = -1) {
+  for (int m = 0; m < M; ++m) {
+    if (m == skip) continue;
+    if (!c.s[m] || !aligned16(c.s[m])) return false;
+  }
+  return true;
+}
+
+template <bool CHECK>
+static void launch_disentangle(const ne_config* cfg, const ne_cstreams& er, int64_t n,
+                               const ne_streams& dr, uint32_t* bitmap, ne_diag* diag, cudaStream_t s) {
+  const int grid = grid_for((n + 1) / 2, kThreads);
+  switch (cfg->M) {
+    case 3: k_disentangle<3, CHECK><<<grid, kThreads, 0, s>>>(er, 3, cfg->l, n, dr, bitmap, diag); break;
+    case 4: k_disentangle<4, CHECK><<<grid, kThreads, 0, s>>>(er, 4, cfg->l, n, dr, bitmap, diag); break;
+    case 8: k_disentangle<8, CHECK><<<grid, kThreads, 0, s>>>(er, 8, cfg->l, n, dr, bitmap, diag); break;
+    default: k_disentangle<0, CHECK><<<grid, kThreads, 0, s>>>(er, cfg->M, cfg->l, n, dr, bitmap, diag); break;
+  }
+}
+
+extern "C" ne_status ne_disentangle_check(const ne_config* cfg, ne_cstreams delta, int64_t n_total,
+                                          int32_t r, ne_streams d_out, uint32_t* bitmap, ne_diag* diag,
+                                          ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (r < 0 || r >= cfg->M) return NE_EINDEX;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !streams_ok(delta, cfg->M) || !streams_ok(d_out, cfg->M)) return NE_EINVAL;
+  launch_disentangle<true>(cfg, rotate(delta, cfg->M, r), n_total, rotate(d_out, cfg->M, r), bitmap, diag,
+                           cs(stream));
+  return launch_status();
+}
+
+extern "C" ne_status ne_recover(const ne_config* cfg, ne_cstreams delta, int64_t n_total, int32_t r,
+                                ne_streams d_out, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (r < 0 || r >= cfg->M) return NE_EINDEX;
+  for (int m = 0; m < cfg->M; ++m)
+    if (m != r && !delta.s[m]) return NE_EUNRECOVERABLE;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !streams_ok(delta, cfg->M, r) || !streams_ok(d_out, cfg->M)) return NE_EINVAL;
+  launch_disentangle<false>(cfg, rotate(delta, cfg->M, r), n_total, rotate(d_out, cfg->M, r), nullptr, nullptr,
+                            cs(stream));
+  return launch_status();
+}
+
+extern "C" ne_status ne_inject(int64_t* x, int64_t idx, uint64_t mask, ne_stream_t stream) {
+  if (!x || idx < 0) return NE_EINVAL;
+  k_inject<<<1, 1, 0, cs(stream)>>>(x, idx, mask);
+  return launch_status();
+}
+
+extern "C" ne_status ne_inject_sweep(const ne_config* cfg, ne_cstreams delta, int64_t window, int32_t r,
+                                     uint64_t* flagwords, int64_t* dhat, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (r < 0 || r >= cfg->M) return NE_EINDEX;
+  if (window < 1 || window > 64 || !flagwords || !dhat || !streams_ok(delta, cfg->M)) return NE_EINVAL;
+  const ne_cstreams er = rotate(delta, cfg->M, r);
+  const int64_t trials = (int64_t)cfg->M * window * 64;
+  const int grid = grid_for(trials * 32, kThreads);
+  cudaStream_t s = cs(stream);
+  switch (cfg->M) {
+    case 3: k_inject_sweep<3><<<grid, kThreads, 0, s>>>(er, 3, cfg->l, r, window, flagwords, dhat); break;
+    case 4: k_inject_sweep<4><<<grid, kThreads, 0, s>>>(er, 4, cfg->l, r, window, flagwords, dhat); break;
+    case 8: k_inject_sweep<8><<<grid, kThreads, 0, s>>>(er, 8, cfg->l, r, window, flagwords, dhat); break;
+    default: k_inject_sweep<0><<<grid, kThreads, 0, s>>>(er, cfg->M, cfg->l, r, window, flagwords, dhat); break;
+  }
+  return launch_status();
+}

@@ -1,0 +1,159 @@
+// k_gemm.cu — ne_op_gemm dispatch (IMAD64 CUDA-core path or the tcgen05
+// int8-limb path) and the operand preparation kernels of the limb path.
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "ne_internal.cuh"
+
+namespace ne {
+
+void launch_gemm_imad64(int M, const ne_cstreams& A, const int32_t* B, const ne_streams& C, int64_t rows,
+                        int64_t cols, int64_t K, cudaStream_t s);
+ne_status launch_gemm_tc(int M, int L, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+                         int64_t K, const ne_streams& C, cudaStream_t s);
+
+// int64 entangled A_m -> L balanced int8 digit planes, planes[(m*L+i)*n + idx]
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_split_limbs(const __grid_constant__ ne_cstreams A, int M_rt, int64_t n, int L, int8_t* __restrict__ planes,
+              ne_diag* __restrict__ diag) {
+  const int M = MT > 0 ? MT : M_rt;
+  int bad = 0;
+  long long first = LLONG_MAX;
+  const int64_t nq = n / 4;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+      if (MT == 0 && m >= M) break;
+      const longlong2* p = reinterpret_cast<const longlong2*>(A.s[m] + 4 * q);
+      longlong2 u = __ldcs(p), w = __ldcs(p + 1);
+      int64_t x[4] = {u.x, u.y, w.x, w.y};
+      for (int j = 0; j < L; ++j) {
+        uint32_t packed = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          int8_t d = (int8_t)(x[i] & 0xff);
+          x[i] = (x[i] - d) >> 8;
+          packed |= (uint32_t)(uint8_t)d << (8 * i);
+        }
+        *reinterpret_cast<uint32_t*>(planes + ((int64_t)m * L + j) * n + 4 * q) = packed;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (x[i] != 0) {
+          ++bad;
+          long long idx = (long long)m * n + 4 * q + i;
+          first = idx < first ? idx : first;
+        }
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// B (K x cols int32, row-major) -> Bt (cols x K int8, K contiguous), |B| <= 127..-128
+__global__ void __launch_bounds__(256)
+k_prep_b(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __restrict__ Bt, ne_diag* __restrict__ diag) {
+  __shared__ int8_t tile[32][33 * 4];
+  const int64_t k0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 32;
+  int bad = 0;
+  long long first = LLONG_MAX;
+  // load 128 (k) x 32 (c) int32 coalesced along c
+  for (int t = threadIdx.x; t < 128 * 32; t += 256) {
+    const int kk = t / 32, cc = t % 32;
+    const int64_t k = k0 + kk, c = c0 + cc;
+    int32_t v = 0;
+    if (k < K && c < cols) {
+      v = B[k * cols + c];
+      if (v < -128 || v > 127) {
+        ++bad;
+        long long idx = (long long)(k * cols + c);
+        first = idx < first ? idx : first;
+      }
+    }
+    tile[cc][kk] = (int8_t)v;
+  }
+  __syncthreads();
+  // store 32 (c) rows of 128 (k) int8, 4 bytes per thread
+  for (int t = threadIdx.x; t < 32 * 32; t += 256) {
+    const int cc = t / 32, kq = (t % 32) * 4;
+    const int64_t c = c0 + cc, k = k0 + kq;
+    if (c < cols && k + 3 < K) {
+      uint32_t w = (uint32_t)(uint8_t)tile[cc][kq] | ((uint32_t)(uint8_t)tile[cc][kq + 1] << 8) |
+                   ((uint32_t)(uint8_t)tile[cc][kq + 2] << 16) | ((uint32_t)(uint8_t)tile[cc][kq + 3] << 24);
+      *reinterpret_cast<uint32_t*>(Bt + c * K + k) = w;
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+}  // namespace ne
+
+using namespace ne;
+
+static bool tc_shape_ok(int64_t rows, int64_t cols, int64_t K) {
+  return rows > 0 && cols > 0 && K > 0 && rows % 128 == 0 && cols % 128 == 0 && K % 128 == 0 && K <= 131072;
+}
+
+extern "C" ne_status ne_gemm_workspace(const ne_config* cfg, int64_t rows, int64_t cols, int64_t K, int32_t L,
+                                       size_t* bytes) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (!bytes || L < 1 || L > 8) return NE_EINVAL;
+  *bytes = (size_t)cfg->M * L * rows * K + (size_t)cols * K + 1024;
+  return NE_OK;
+}
+
+extern "C" ne_status ne_gemm_prep_b(const int32_t* B, int64_t K, int64_t cols, int8_t* Bt, ne_diag* diag,
+                                    ne_stream_t stream) {
+  if (!B || !Bt || K <= 0 || cols <= 0 || K % 4 != 0 || !aligned16(Bt)) return NE_EINVAL;
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((K + 127) / 128));
+  k_prep_b<<<grid, 256, 0, cs(stream)>>>(B, K, cols, Bt, diag);
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes, int32_t L, const int8_t* Bt,
+                                      int64_t rows, int64_t cols, int64_t K, ne_streams C, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (!planes || !Bt || L < 1 || L > 4 || !aligned16(planes) || !aligned16(Bt)) return NE_EINVAL;
+  for (int m = 0; m < cfg->M; ++m)
+    if (!C.s[m] || !aligned16(C.s[m])) return NE_EINVAL;
+  if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
+  return launch_gemm_tc(cfg->M, L, planes, Bt, rows, cols, K, C, cs(stream));
+}
+
+extern "C" ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int64_t rows, int64_t cols,
+                                int64_t K, ne_gemm_algo algo, int32_t L, ne_streams C, void* ws, size_t ws_bytes,
+                                ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  const int M = cfg->M;
+  if (!B || rows < 0 || cols < 0 || K < 0) return NE_EINVAL;
+  for (int m = 0; m < M; ++m)
+    if (!A.s[m] || !C.s[m] || !aligned16(A.s[m]) || !aligned16(C.s[m])) return NE_EINVAL;
+  if (rows == 0 || cols == 0) return NE_OK;
+  cudaStream_t s = cs(stream);
+  if (algo == NE_GEMM_IMAD64) {
+    launch_gemm_imad64(M, A, B, C, rows, cols, K, s);
+    return launch_status();
+  }
+  if (algo != NE_GEMM_TC_I8) return NE_EINVAL;
+  if (!tc_shape_ok(rows, cols, K) || L < 1 || L > 4) return NE_ENOTSUP;
+  size_t need = 0;
+  ne_gemm_workspace(cfg, rows, cols, K, L, &need);
+  if (!ws || ws_bytes < need || !aligned16(ws)) return NE_EINVAL;
+  int8_t* planes = static_cast<int8_t*>(ws);
+  int8_t* Bt = planes + (size_t)M * L * rows * K;
+  const int64_t n = rows * K;
+  const int grid = grid_for(n / 4, kThreads);
+  switch (M) {
+    case 3: k_split_limbs<3><<<grid, kThreads, 0, s>>>(A, 3, n, L, planes, diag); break;
+    case 4: k_split_limbs<4><<<grid, kThreads, 0, s>>>(A, 4, n, L, planes, diag); break;
+    case 8: k_split_limbs<8><<<grid, kThreads, 0, s>>>(A, 8, n, L, planes, diag); break;
+    default: k_split_limbs<0><<<grid, kThreads, 0, s>>>(A, M, n, L, planes, diag); break;
+  }
+  if ((st = launch_status()) != NE_OK) return st;
+  if ((st = ne_gemm_prep_b(B, K, cols, Bt, diag, stream)) != NE_OK) return st;
+  return launch_gemm_tc(M, L, planes, Bt, rows, cols, K, C, s);
+}

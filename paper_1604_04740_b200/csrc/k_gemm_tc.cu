@@ -1,0 +1,297 @@
+// k_gemm_tc.cu — the entangled integer GEMM on the 5th-generation tensor
+// cores (tcgen05.mma kind::i8), exact.
+//
+// C_m = E_m B with E_m the entangled rows x K operand (Eq. 9) and
+// B the shared K x cols kernel (unmodified).  E_m is held as L balanced signed
+// base-2^8 digit planes D_{m,i} (ne_entangle_limbs / k_split_limbs), B as one
+// int8 plane (|B| <= 128), so
+//     C_m = sum_i 2^(8i) (D_{m,i} B),
+// every D_{m,i} B is an int8 x int8 -> int32 tensor-core product that is exact
+// while K * 128 * 128 < 2^31 (K <= 131072), and the recombination is done in
+// int64 in the epilogue (wrap mod 2^64, exact for certified results).
+//
+// One CTA computes a 128 x BN tile of one stream m: the L limb accumulators
+// live side by side in TMEM (L * BN <= 512 columns).  Warp roles:
+//   warp 0 lane 0 : TMA producer  (cp.async.bulk.tensor, 128B swizzle, mbarrier complete_tx)
+//   warp 1 lane 0 : MMA issuer    (tcgen05.mma.cta_group::1.kind::i8, commit -> mbarrier)
+//   warp 2        : TMEM allocator (tcgen05.alloc / dealloc)
+//   warps 4..7    : epilogue      (tcgen05.ld 32x32b -> int64 recombine -> st.global)
+// smem: kStages x {L A tiles 128 x 128 B, one B tile BN x 128 B}, 1024-B aligned.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "ne_internal.cuh"
+
+namespace ne {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 128;  // bytes of K per stage = one 128B swizzle atom row
+constexpr int UMMA_K = 32;  // int8: 32 bytes of K per tcgen05.mma
+constexpr int kThreadsTC = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t"
+      "}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t c0,
+                                            int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, 128B swizzle (layout type 2 on sm_100):
+// start >> 4 in [0,14), LBO >> 4 in [16,30) (unused for swizzled K-major: 1),
+// SBO >> 4 in [32,46) (= 1024 B between 8-row groups), version 1 in [46,48).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// instruction descriptor, kind::i8: D s32 (bits 4-5 = 2), A/B signed int8
+// (bits 7-9 = 1, 10-12 = 1), K-major A and B, N >> 3 at bit 17, M >> 4 at bit 24.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+template <int L, int BN, int STAGES>
+struct Cfg {
+  static constexpr int kATile = BM * BK;          // bytes
+  static constexpr int kBTile = BN * BK;
+  static constexpr int kStage = L * kATile + kBTile;
+  static constexpr int kTmemCols = (L * BN <= 32) ? 32 : (L * BN <= 64) ? 64 : (L * BN <= 128) ? 128 : (L * BN <= 256) ? 256 : 512;
+  static constexpr size_t kSmem = (size_t)STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int L, int BN, int STAGES>
+__global__ void __launch_bounds__(kThreadsTC, 1)
+k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+          const __grid_constant__ ne_streams C, int64_t rows, int64_t cols, int64_t K) {
+  using CF = Cfg<L, BN, STAGES>;
+  static_assert(L * BN <= 512, "TMEM holds 512 columns");
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = blockIdx.z;
+  const int64_t row0 = (int64_t)blockIdx.y * BM;
+  const int64_t col0 = (int64_t)blockIdx.x * BN;
+  const int KB = (int)(K / BK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"((uint32_t)CF::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t round = (uint32_t)(kb / STAGES);
+      mbar_wait(&empty[s], (round & 1) ^ 1);
+      unsigned char* st = smem + s * CF::kStage;
+      mbar_expect_tx(&full[s], (uint32_t)CF::kStage);
+#pragma unroll
+      for (int i = 0; i < L; ++i)
+        tma_load_2d(&mapA, &full[s], st + i * CF::kATile, kb * BK, (int32_t)(((int64_t)m * L + i) * rows + row0));
+      tma_load_2d(&mapB, &full[s], st + L * CF::kATile, kb * BK, (int32_t)col0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = idesc_i8(BM, BN);
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t round = (uint32_t)(kb / STAGES);
+      mbar_wait(&full[s], round & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sa = smem_u32(smem + s * CF::kStage);
+      const uint32_t sb = sa + L * CF::kATile;
+#pragma unroll
+      for (int ks = 0; ks < BK / UMMA_K; ++ks) {
+        const uint64_t bdesc = umma_desc_sw128(sb + ks * UMMA_K);
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          const uint64_t adesc = umma_desc_sw128(sa + i * CF::kATile + ks * UMMA_K);
+          mma_i8(tmem_base + i * BN, adesc, bdesc, idesc, (kb | ks) != 0);
+        }
+      }
+      mma_commit(&empty[s]);  // frees the smem stage when these MMAs completed
+    }
+    mma_commit(tmem_full);    // accumulators final
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> int64 recombination -> global
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int64_t row = row0 + 32 * q + lane;
+    int64_t* __restrict__ crow = C.s[m] + row * cols + col0;
+    const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16);
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 16) {
+      uint32_t v[L][16];
+#pragma unroll
+      for (int i = 0; i < L; ++i) tmem_ld16(tl + i * BN + c, v[i]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      uint64_t o[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        uint64_t acc = 0;
+#pragma unroll
+        for (int i = 0; i < L; ++i) acc += (uint64_t)(int64_t)(int32_t)v[i][j] << (8 * i);
+        o[j] = acc;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 2)
+        __stcs(reinterpret_cast<longlong2*>(crow + c + j), make_longlong2((int64_t)o[j], (int64_t)o[j + 1]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)CF::kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D int8 tensor [outer][inner] (inner contiguous), box {BK, box_outer}, 128B swizzle
+static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int L, int BN, int STAGES>
+static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
+                     const ne_streams& C, cudaStream_t s) {
+  using CF = Cfg<L, BN, STAGES>;
+  if (cols % BN != 0) return NE_ENOTSUP;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, planes, (uint64_t)K, (uint64_t)M * L * rows, BM)) return NE_ECUDA;
+  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, BN)) return NE_ECUDA;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(k_gemm_tc<L, BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) !=
+        cudaSuccess)
+      return NE_ECUDA;
+    attr = true;
+  }
+  dim3 grid((unsigned)(cols / BN), (unsigned)(rows / BM), (unsigned)M);
+  k_gemm_tc<L, BN, STAGES><<<grid, kThreadsTC, CF::kSmem, s>>>(ma, mb, C, rows, cols, K);
+  return launch_status();
+}
+
+}  // namespace tc
+
+ne_status launch_gemm_tc(int M, int L, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+                         int64_t K, const ne_streams& C, cudaStream_t s) {
+  switch (L) {
+    case 1: return (cols % 256 == 0) ? tc::run<1, 256, 4>(planes, Bt, rows, cols, K, M, C, s)
+                                     : tc::run<1, 128, 4>(planes, Bt, rows, cols, K, M, C, s);
+    case 2: return (cols % 256 == 0) ? tc::run<2, 256, 3>(planes, Bt, rows, cols, K, M, C, s)
+                                     : tc::run<2, 128, 4>(planes, Bt, rows, cols, K, M, C, s);
+    case 3: return tc::run<3, 128, 3>(planes, Bt, rows, cols, K, M, C, s);
+    case 4: return tc::run<4, 128, 2>(planes, Bt, rows, cols, K, M, C, s);
+    default: return NE_ENOTSUP;
+  }
+}
+
+}  // namespace ne

@@ -1,0 +1,450 @@
+// k_stream.cu — streaming (HBM-bound) kernels of the hot path:
+//   a1 entangle (SoA / AoS / int8 limb planes / one stream), a2 self-entangle,
+//   a3 element-wise ops (scale, add), outer product, permutation gather,
+//   and the device-side seeded input generator (gen/ne_gen.h).
+// Layout and rooflines: DESIGN.md "Kernels".  Every kernel is a grid-stride
+// loop over 128-bit vectors, grid = a multiple of the SM count.
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "../../gen/ne_gen.h"
+#include "../../include/ne_gendev.h"
+#include "ne_internal.cuh"
+
+namespace ne {
+
+// ---------------------------------------------------------------- a1 entangle
+// eps_m[n] = c_m[n] + S_l{c_(m-1) mod M[n]}   (Eq. 15; Eq. 7 for M = 3).
+// One thread handles 4 consecutive positions of ALL M streams, so every c_m is
+// read exactly once (int4) and eps is written as 2 x 128-bit per stream.
+// The a0 range assertion |c| <= hi is fused (warp-aggregated atomics).
+// OUT selects the output layout: 0 = SoA int64, 1 = AoS int64, 2 = int8 limbs.
+template <int MT, int OUT>
+__global__ void __launch_bounds__(kThreads)
+k_entangle(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n,
+           const __grid_constant__ ne_streams eps, int64_t* __restrict__ eps_aos, int8_t* __restrict__ planes,
+           int L, ne_diag* __restrict__ diag) {
+  const int M = MT > 0 ? MT : M_rt;
+  int bad = 0;
+  long long first = LLONG_MAX;
+  const int64_t nvec = (n + 3) / 4;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = v * 4;
+    const bool full = n0 + 4 <= n;
+    int32_t first_c[4], prev[4];
+    // c_{M-1} first: it is the "previous" stream of stream 0 (circulant Eq. 14)
+    {
+      const int32_t* p = c.s[M - 1] + n0;
+      if (full) {
+        int4 q = __ldcs(reinterpret_cast<const int4*>(p));
+        first_c[0] = q.x; first_c[1] = q.y; first_c[2] = q.z; first_c[3] = q.w;
+      } else {
+        for (int i = 0; i < 4; ++i) first_c[i] = (n0 + i < n) ? p[i] : 0;
+      }
+      for (int i = 0; i < 4; ++i) prev[i] = first_c[i];
+    }
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+      if (MT == 0 && m >= M) break;
+      int32_t cur[4];
+      if (m == M - 1) {
+        for (int i = 0; i < 4; ++i) cur[i] = first_c[i];
+      } else {
+        const int32_t* p = c.s[m] + n0;
+        if (full) {
+          int4 q = __ldcs(reinterpret_cast<const int4*>(p));
+          cur[0] = q.x; cur[1] = q.y; cur[2] = q.z; cur[3] = q.w;
+        } else {
+          for (int i = 0; i < 4; ++i) cur[i] = (n0 + i < n) ? p[i] : 0;
+        }
+      }
+      int64_t e[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        e[i] = (int64_t)cur[i] + (int64_t)((uint64_t)(int64_t)prev[i] << l);
+        const int64_t ci = cur[i];
+        if ((ci > hi || ci < -hi) && n0 + i < n) {
+          ++bad;
+          long long idx = (long long)m * n + n0 + i;
+          first = idx < first ? idx : first;
+        }
+      }
+      if (OUT == 0) {
+        int64_t* q = eps.s[m] + n0;
+        if (full) {
+          __stcs(reinterpret_cast<longlong2*>(q), make_longlong2(e[0], e[1]));
+          __stcs(reinterpret_cast<longlong2*>(q) + 1, make_longlong2(e[2], e[3]));
+        } else {
+          for (int i = 0; i < 4; ++i)
+            if (n0 + i < n) q[i] = e[i];
+        }
+      } else if (OUT == 1) {
+        for (int i = 0; i < 4; ++i)
+          if (n0 + i < n) eps_aos[(n0 + i) * M + m] = e[i];
+      } else {
+        // balanced signed base-2^8 digits: d_j = sext8(x_j), x_{j+1} = (x_j - d_j) >> 8
+        int64_t x[4] = {e[0], e[1], e[2], e[3]};
+        for (int j = 0; j < L; ++j) {
+          uint32_t packed = 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            int8_t dgt = (int8_t)(x[i] & 0xff);
+            x[i] = (x[i] - dgt) >> 8;
+            packed |= (uint32_t)(uint8_t)dgt << (8 * i);
+          }
+          // n % 16 == 0 is required by the ABI, so 4-aligned groups are full
+          *reinterpret_cast<uint32_t*>(planes + ((int64_t)m * L + j) * n + n0) = packed;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (x[i] != 0) {  // not representable in L digits
+            ++bad;
+            long long idx = (long long)m * n + n0 + i;
+            first = idx < first ? idx : first;
+          }
+      }
+      for (int i = 0; i < 4; ++i) prev[i] = cur[i];
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// AoS stores above are scalar; for M = 4 use a 2 x 128-bit store per position
+// (one 32-byte sector) — the layout the C4 gather reads.
+__global__ void __launch_bounds__(kThreads)
+k_entangle_aos4(const __grid_constant__ ne_cstreams32 c, int l, int64_t hi, int64_t n,
+                int64_t* __restrict__ eps_aos, ne_diag* __restrict__ diag) {
+  int bad = 0;
+  long long first = LLONG_MAX;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t cv[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      cv[m] = __ldcs(c.s[m] + i);
+      if (cv[m] > hi || cv[m] < -hi) {
+        ++bad;
+        long long idx = (long long)m * n + i;
+        first = idx < first ? idx : first;
+      }
+    }
+    int64_t e[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) e[m] = cv[m] + (int64_t)((uint64_t)cv[(m + 3) & 3] << l);
+    longlong2* q = reinterpret_cast<longlong2*>(eps_aos + i * 4);
+    __stcs(q, make_longlong2(e[0], e[1]));
+    __stcs(q + 1, make_longlong2(e[2], e[3]));
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// one stream: eps_m = c_m + S_l{c_prev}
+__global__ void __launch_bounds__(kThreads)
+k_entangle_stream(const int32_t* __restrict__ cm, const int32_t* __restrict__ cp, int m, int l,
+                  int64_t hi, int64_t n, int64_t* __restrict__ eps, ne_diag* __restrict__ diag) {
+  int bad = 0;
+  long long first = LLONG_MAX;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = __ldcs(cm + i), b = __ldcs(cp + i);
+    if (a > hi || a < -hi) {
+      ++bad;
+      long long idx = (long long)m * n + i;
+      first = idx < first ? idx : first;
+    }
+    __stcs(eps + i, a + (int64_t)((uint64_t)b << l));
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// a2: g_ent = S_l{g} + g (footnote P:507-511)
+__global__ void k_entangle_shared(const int32_t* __restrict__ g, int l, int64_t n,
+                                  int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = g[i];
+    out[i] = (int64_t)((uint64_t)v << l) + v;
+  }
+}
+
+// ---------------------------------------------------------------- a3 element-wise
+// x_m[n] *= (g ? g[n] : s) — 2 positions (128 bits) per thread per stream
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_scale(const __grid_constant__ ne_streams x, int M_rt, int64_t n, int64_t s,
+        const int32_t* __restrict__ g) {
+  const int M = MT > 0 ? MT : M_rt;
+  const int64_t npair = (n + 1) / 2;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < npair;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 2 * v;
+    int64_t f0 = s, f1 = s;
+    if (g) {
+      f0 = g[n0];
+      f1 = (n0 + 1 < n) ? g[n0 + 1] : 0;
+    }
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+      if (MT == 0 && m >= M) break;
+      int64_t* p = x.s[m] + n0;
+      if (n0 + 1 < n) {
+        longlong2 q = __ldcs(reinterpret_cast<const longlong2*>(p));
+        q.x = (int64_t)((uint64_t)q.x * (uint64_t)f0);
+        q.y = (int64_t)((uint64_t)q.y * (uint64_t)f1);
+        __stcs(reinterpret_cast<longlong2*>(p), q);
+      } else {
+        p[0] = (int64_t)((uint64_t)p[0] * (uint64_t)f0);
+      }
+    }
+  }
+}
+
+// x_m[n] += sign * a_m[n]
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_add(const __grid_constant__ ne_streams x, const __grid_constant__ ne_cstreams a, int M_rt,
+      int64_t n, int sign) {
+  const int M = MT > 0 ? MT : M_rt;
+  const int64_t npair = (n + 1) / 2;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < npair;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 2 * v;
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+      if (MT == 0 && m >= M) break;
+      int64_t* p = x.s[m] + n0;
+      const int64_t* q = a.s[m] + n0;
+      if (n0 + 1 < n) {
+        longlong2 u = __ldcs(reinterpret_cast<const longlong2*>(p));
+        longlong2 w = __ldcs(reinterpret_cast<const longlong2*>(q));
+        u.x = sign > 0 ? (int64_t)((uint64_t)u.x + (uint64_t)w.x) : (int64_t)((uint64_t)u.x - (uint64_t)w.x);
+        u.y = sign > 0 ? (int64_t)((uint64_t)u.y + (uint64_t)w.y) : (int64_t)((uint64_t)u.y - (uint64_t)w.y);
+        __stcs(reinterpret_cast<longlong2*>(p), u);
+      } else {
+        p[0] = sign > 0 ? (int64_t)((uint64_t)p[0] + (uint64_t)q[0]) : (int64_t)((uint64_t)p[0] - (uint64_t)q[0]);
+      }
+    }
+  }
+}
+
+// outer product: out_m[i*n2 + j] = x_m[i] * h[j]; write-bound, 2 outputs / thread
+__global__ void __launch_bounds__(kThreads)
+k_outer(const __grid_constant__ ne_cstreams x, const __grid_constant__ ne_streams out, int M,
+        int64_t n1, const int32_t* __restrict__ h, int64_t n2) {
+  const int64_t total = n1 * n2;
+  const int64_t npair = (total + 1) / 2;
+  const bool even = (n2 % 2) == 0;
+  for (int m = 0; m < M; ++m) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < npair;
+         v += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t o = 2 * v;
+      if (even) {
+        const int64_t i = o / n2, j = o - i * n2;
+        const uint64_t xi = (uint64_t)x.s[m][i];
+        __stcs(reinterpret_cast<longlong2*>(out.s[m] + o),
+               make_longlong2((int64_t)(xi * (uint64_t)(int64_t)h[j]), (int64_t)(xi * (uint64_t)(int64_t)h[j + 1])));
+      } else {
+        for (int64_t q = o; q < o + 2 && q < total; ++q) {
+          const int64_t i = q / n2, j = q - i * n2;
+          out.s[m][q] = (int64_t)((uint64_t)x.s[m][i] * (uint64_t)(int64_t)h[j]);
+        }
+      }
+    }
+  }
+}
+
+// permutation gather out_m[i] = x_m[perm[i]] (SoA)
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_permute(const __grid_constant__ ne_cstreams x, const __grid_constant__ ne_streams out,
+          int M_rt, const int32_t* __restrict__ perm, int64_t n) {
+  const int M = MT > 0 ? MT : M_rt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t src = __ldcs(perm + i);
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+      if (MT == 0 && m >= M) break;
+      __stcs(out.s[m] + i, __ldg(x.s[m] + src));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- generator
+__global__ void k_gen_uniform(uint64_t key, int64_t lo, int64_t hi, int64_t offset, int64_t count,
+                              int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)ne_gen_uniform(key, (uint64_t)(offset + i), lo, hi);
+}
+
+__global__ void k_gen_perm(uint64_t key, int64_t n, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)ne_gen_perm(key, (uint64_t)n, (uint64_t)i);
+}
+
+}  // namespace ne
+
+using namespace ne;
+
+#define NE_DISPATCH_M(M, KERNEL, GRID, STREAM, ...)                  \
+  switch (M) {                                                     \
+    case 3: KERNEL<3><<<GRID, kThreads, 0, STREAM>>>(__VA_ARGS__); break;  \
+    case 4: KERNEL<4><<<GRID, kThreads, 0, STREAM>>>(__VA_ARGS__); break;  \
+    case 8: KERNEL<8><<<GRID, kThreads, 0, STREAM>>>(__VA_ARGS__); break;  \
+    default: KERNEL<0><<<GRID, kThreads, 0, STREAM>>>(__VA_ARGS__); break; \
+  }
+
+static bool streams_ok32(const ne_cstreams32& c, int M) {
+  for (int m = 0; m < M; ++m)
+    if (!c.s[m] || !aligned16(c.s[m])) return false;
+  return true;
+}
+template <typename S>
+static bool streams_ok(const S& c, int M) {
+  for (int m = 0; m < M; ++m)
+    if (!c.s[m] || !aligned16(c.s[m])) return false;
+  return true;
+}
+
+template <int OUT>
+static ne_status launch_entangle(const ne_config* cfg, ne_cstreams32 c, int64_t n, ne_streams eps,
+                                 int64_t* aos, int8_t* planes, int L, ne_diag* diag,
+                                 ne_stream_t stream) {
+  const int64_t hi = range_hi(cfg);
+  const int grid = grid_for((n + 3) / 4, kThreads);
+  cudaStream_t s = cs(stream);
+  switch (cfg->M) {
+    case 3: k_entangle<3, OUT><<<grid, kThreads, 0, s>>>(c, 3, cfg->l, hi, n, eps, aos, planes, L, diag); break;
+    case 4: k_entangle<4, OUT><<<grid, kThreads, 0, s>>>(c, 4, cfg->l, hi, n, eps, aos, planes, L, diag); break;
+    case 8: k_entangle<8, OUT><<<grid, kThreads, 0, s>>>(c, 8, cfg->l, hi, n, eps, aos, planes, L, diag); break;
+    default: k_entangle<0, OUT><<<grid, kThreads, 0, s>>>(c, cfg->M, cfg->l, hi, n, eps, aos, planes, L, diag); break;
+  }
+  return launch_status();
+}
+
+extern "C" ne_status ne_entangle(const ne_config* cfg, ne_cstreams32 c, int64_t n_total,
+                                 ne_streams eps, ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !streams_ok32(c, cfg->M) || !streams_ok(eps, cfg->M)) return NE_EINVAL;
+  return launch_entangle<0>(cfg, c, n_total, eps, nullptr, nullptr, 0, diag, stream);
+}
+
+extern "C" ne_status ne_entangle_aos(const ne_config* cfg, ne_cstreams32 c, int64_t n_total,
+                                     int64_t* eps_aos, ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !streams_ok32(c, cfg->M) || !eps_aos || !aligned16(eps_aos)) return NE_EINVAL;
+  if (cfg->M == 4) {
+    k_entangle_aos4<<<grid_for(n_total, kThreads), kThreads, 0, cs(stream)>>>(c, cfg->l, range_hi(cfg), n_total,
+                                                                            eps_aos, diag);
+    return launch_status();
+  }
+  ne_streams none{};
+  return launch_entangle<1>(cfg, c, n_total, none, eps_aos, nullptr, 0, diag, stream);
+}
+
+extern "C" ne_status ne_entangle_limbs(const ne_config* cfg, ne_cstreams32 c, int64_t n_total,
+                                       int32_t L, int8_t* planes, ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || n_total % 16 != 0 || L < 1 || L > 8 || !streams_ok32(c, cfg->M) || !planes ||
+      !aligned16(planes))
+    return NE_EINVAL;
+  ne_streams none{};
+  return launch_entangle<2>(cfg, c, n_total, none, nullptr, planes, L, diag, stream);
+}
+
+extern "C" ne_status ne_entangle_stream(const ne_config* cfg, int32_t m, const int32_t* c_m,
+                                        const int32_t* c_prev, int64_t* eps_m, int64_t n_total,
+                                        ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (m < 0 || m >= cfg->M) return NE_EINDEX;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !c_m || !c_prev || !eps_m || !aligned16(c_m) || !aligned16(c_prev) || !aligned16(eps_m))
+    return NE_EINVAL;
+  k_entangle_stream<<<grid_for(n_total, kThreads), kThreads, 0, cs(stream)>>>(c_m, c_prev, m, cfg->l,
+                                                                            range_hi(cfg), n_total, eps_m, diag);
+  return launch_status();
+}
+
+extern "C" ne_status ne_entangle_shared(const ne_config* cfg, const int32_t* g, int64_t* g_ent,
+                                        int64_t n_total, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !g || !g_ent) return NE_EINVAL;
+  k_entangle_shared<<<grid_for(n_total, kThreads), kThreads, 0, cs(stream)>>>(g, cfg->l, n_total, g_ent);
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_scale(const ne_config* cfg, ne_streams x, int64_t n_total, int64_t s,
+                                 const int32_t* g_or_null, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !streams_ok(x, cfg->M)) return NE_EINVAL;
+  const int grid = grid_for((n_total + 1) / 2, kThreads);
+  NE_DISPATCH_M(cfg->M, k_scale, grid, cs(stream), x, cfg->M, n_total, s, g_or_null);
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_add(const ne_config* cfg, ne_streams x, ne_cstreams addend, int64_t n_total,
+                               int32_t sign, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || (sign != 1 && sign != -1) || !streams_ok(x, cfg->M) || !streams_ok(addend, cfg->M))
+    return NE_EINVAL;
+  const int grid = grid_for((n_total + 1) / 2, kThreads);
+  NE_DISPATCH_M(cfg->M, k_add, grid, cs(stream), x, addend, cfg->M, n_total, sign);
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_outer(const ne_config* cfg, ne_cstreams x, int64_t n1, const int32_t* h,
+                                 int64_t n2, ne_streams out, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n1 < 0 || n2 < 0 || !h || !streams_ok(x, cfg->M) || !streams_ok(out, cfg->M)) return NE_EINVAL;
+  if (n1 == 0 || n2 == 0) return NE_OK;
+  k_outer<<<grid_for((n1 * n2 + 1) / 2, kThreads), kThreads, 0, cs(stream)>>>(x, out, cfg->M, n1, h, n2);
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_permute(const ne_config* cfg, ne_cstreams x, const int32_t* perm,
+                                   int64_t n_total, ne_streams out, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || n_total > INT32_MAX || !perm || !streams_ok(x, cfg->M) || !streams_ok(out, cfg->M))
+    return NE_EINVAL;
+  NE_DISPATCH_M(cfg->M, k_permute, grid_for(n_total, kThreads), cs(stream), x, out, cfg->M, perm, n_total);
+  return launch_status();
+}
+
+extern "C" ne_status ne_gen_uniform_i32(uint64_t seed, uint32_t tag, uint32_t gstream, int64_t lo,
+                                        int64_t hi, int64_t offset, int64_t count, int32_t* out,
+                                        ne_stream_t stream) {
+  if (!out || count < 0 || hi <= lo || hi - lo > (1ll << 32) || lo < INT32_MIN || hi - 1 > INT32_MAX)
+    return NE_EINVAL;
+  if (count == 0) return NE_OK;
+  k_gen_uniform<<<grid_for(count, kThreads), kThreads, 0, cs(stream)>>>(ne_gen_key(seed, tag, gstream), lo, hi,
+                                                                      offset, count, out);
+  return launch_status();
+}
+
+extern "C" ne_status ne_gen_perm_i32(uint64_t seed, uint32_t tag, int64_t n, int32_t* out,
+                                     ne_stream_t stream) {
+  if (!out || n < 0 || n > INT32_MAX) return NE_EINVAL;
+  if (n == 0) return NE_OK;
+  k_gen_perm<<<grid_for(n, kThreads), kThreads, 0, cs(stream)>>>(ne_gen_key(seed, tag, 0), n, out);
+  return launch_status();
+}

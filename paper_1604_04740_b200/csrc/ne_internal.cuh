@@ -1,0 +1,99 @@
+// ne_internal.cuh — shared device/host helpers of libne (the product path).
+// Nothing here is shared with oracle/: this is the CUDA side's own code.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <climits>
+
+#include "../../include/ne.h"
+
+namespace ne {
+
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+constexpr int kThreads = 256;
+
+// ----------------------------------------------------------------- host side
+ne_status validate_cfg(const ne_config* cfg);      // M in [3,32], w = 64, Eq. 12
+int64_t range_hi(const ne_config* cfg);            // Eq. 13 / Eq. 11 (reading R6)
+int num_sms();
+int grid_for(int64_t work_items, int threads, int per_sm = 8);
+ne_status launch_status();
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline cudaStream_t cs(ne_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// rotate a stream set so that stream r becomes index 0 (the disentangling of
+// Eqs. 16-19 depends only on indices relative to r, so the kernels run in the
+// rotated frame with r = 0 and write through rotated output pointers)
+template <typename S>
+inline S rotate(const S& in, int M, int r) {
+  S out{};
+  for (int j = 0; j < M; ++j) out.s[j] = in.s[(r + j) % M];
+  return out;
+}
+
+// ----------------------------------------------------------------- device side
+__device__ __forceinline__ i128 shl128(i128 x, int s) { return (i128)((u128)x << s); }
+
+// Disentangle + check at one position, in the frame rotated so that the
+// excluded stream r is e[0] (Eqs. 16-19 + Eq. 21, readings R1-R4;
+// DESIGN.md "disentangle kernel").  e[1..M-1] are the other streams in the
+// order (r+1) .. (r+M-1) mod M.  d[j] receives the low 64 bits of d_hat for
+// stream (r+j) mod M.  Returns the flag (false when !check).
+//   t    = (-1)^M * sum_{j=0}^{M-2} (-1)^j 2^{(M-2-j)l} e[1+j]     (Eq. 16 x (-1)^M)
+//   d_p  = sext_{(M-1)l}(t)                      p = M-1              (Eq. 17)
+//   d_0  = ((-1)^M (t - d_p)) >> (M-1)l                              (Eq. 18)
+//   d_j  = e[j] - 2^l d_{j-1},  j = 1..M-2                           (Eq. 19)
+//   flag = e[0] != d_0 + 2^l d_p   (exact, 128-bit)                  (Eq. 21)
+template <int MT>
+__device__ __forceinline__ bool disentangle_rot(const int64_t* e, int M_rt, int l, int64_t* d,
+                                                bool check) {
+  const int M = MT > 0 ? MT : M_rt;
+  i128 t = 0;
+#pragma unroll
+  for (int j = 0; j < (MT > 0 ? MT - 1 : NE_MAX_M - 1); ++j) {
+    if (MT == 0 && j > M - 2) break;
+    i128 term = shl128((i128)e[1 + j], (M - 2 - j) * l);
+    t = (j & 1) ? t - term : t + term;
+  }
+  if (M & 1) t = -t;
+  const int b = (M - 1) * l;  // 1 <= b <= 63 for every valid w = 64 config
+  const int64_t dp = (int64_t)((uint64_t)t << (64 - b)) >> (64 - b);
+  i128 num = t - (i128)dp;
+  if (M & 1) num = -num;
+  const i128 dr = num >> b;
+  d[0] = (int64_t)dr;
+  d[M - 1] = dp;
+  i128 prev = dr;
+#pragma unroll
+  for (int j = 1; j < (MT > 0 ? MT - 1 : NE_MAX_M - 1); ++j) {
+    if (MT == 0 && j > M - 2) break;
+    i128 cur = (i128)e[j] - shl128(prev, l);
+    d[j] = (int64_t)cur;
+    prev = cur;
+  }
+  if (!check) return false;
+  return (i128)e[0] != dr + shl128((i128)dp, l);
+}
+
+// warp-aggregated diagnostics: count + min index, one atomic per warp
+__device__ __forceinline__ void diag_add(unsigned long long* count, long long* first, int local_count,
+                                         long long local_first) {
+  unsigned mask = __ballot_sync(0xffffffffu, local_count != 0);
+  if (mask == 0) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    local_count += __shfl_xor_sync(0xffffffffu, local_count, o);
+    long long other = __shfl_xor_sync(0xffffffffu, local_first, o);
+    local_first = other < local_first ? other : local_first;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(count, (unsigned long long)local_count);
+    atomicMin(first, local_first);
+  }
+}
+
+}  // namespace ne

@@ -1,0 +1,99 @@
+"""C-ABI boundary checks that need no GPU: libne.so loads, exports every
+symbol include/*.h declares, and its host-only a0 logic (configuration,
+dynamic range, certification, limb count) agrees with the oracle and with
+Table II.  No compute calls are made here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1604_04740_b200 as ne
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    names = set()
+    for h in ("ne.h", "ne_gendev.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        names |= set(re.findall(r"^\s*(?:ne_status|int32_t)\s+(ne_\w+)\s*\(", src, re.M))
+    return names
+
+
+@pytest.fixture(scope="module")
+def L():
+    ne.build()
+    return ne.lib()
+
+
+def test_every_declared_symbol_is_exported(L):
+    declared = _declared()
+    assert len(declared) >= 25
+    assert declared == set(ne.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+        assert ctypes.cast(getattr(L, name), ctypes.c_void_p).value
+
+
+def test_library_is_sm100a(L):
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {ne.LIB} 2>&1").read()
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("M", [3, 4, 5, 8, 11, 16, 32])
+@pytest.mark.parametrize("w", [32, 64])
+def test_config_for_matches_oracle(O, M, w):
+    a = ne.ne_config_for(M, w)
+    b = O.config_for(M, w)
+    assert (a.l, a.k) == (b.l, b.k)
+
+
+def test_config_errors():
+    with pytest.raises(ne.NeError):
+        ne.ne_config_for(2, 64)
+    with pytest.raises(ne.NeError):
+        ne.ne_config_for(33, 64)
+
+
+@pytest.mark.parametrize("M", [3, 4, 5, 8, 11, 16, 32])
+def test_dynamic_range_matches_oracle(O, M):
+    assert ne.ne_dynamic_range(ne.ne_config_for(M, 64)) == O.dynamic_range(O.config_for(M, 64))
+
+
+def test_w32_rejected_by_gpu_path():
+    """The GPU path implements w = 64 containers only."""
+    with pytest.raises(ne.NeError):
+        ne.ne_dynamic_range(ne.ne_config_for(3, 32))
+
+
+def test_certify_baseline_configs():
+    c3 = ne.ne_config_for(3)
+    b, ok = ne.ne_certify(c3, ne.NE_OP_SCALE, 2 ** 10, 37)
+    b, ok2 = ne.ne_certify(c3, ne.NE_OP_ADD, b, 2 ** 10)
+    assert b == 38912 and ok and ok2
+    assert ne.ne_certify(c3, ne.NE_OP_LINEAR, 128, 64 * 128) == (2 ** 20, True)
+    assert ne.ne_certify(c3, ne.NE_OP_LINEAR, 64, 4096 * 64) == (2 ** 24, True)
+    c4 = ne.ne_config_for(4)
+    assert ne.ne_certify(c4, ne.NE_OP_LINEAR, 2 ** 12, 1024 * 2 ** 12) == (2 ** 34, True)
+    hi = ne.ne_dynamic_range(c3)
+    assert ne.ne_certify(c3, ne.NE_OP_SCALE, hi, 2)[1] is False
+
+
+def test_gemm_limbs_for():
+    """C3: |E| <= 64 (2^22 + 1) < 2^28 needs 4 balanced int8 digits; C5 (M=8,
+    |c| <= 32): |E| <= 8224 needs 2."""
+    assert ne.ne_gemm_limbs_for(ne.ne_config_for(3), 64) == 4
+    assert ne.ne_gemm_limbs_for(ne.ne_config_for(8), 32) == 2
+    assert ne.ne_gemm_limbs_for(ne.ne_config_for(8), 0) == 1
+
+
+def test_no_cpu_fallback():
+    """Compute entry points refuse to run without a CUDA device."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    cfg = ne.ne_config_for(3)
+    with pytest.raises((RuntimeError, ValueError)):
+        ne.ne_op_scale(cfg, [torch.zeros(4, dtype=torch.int64)] * 3, 2)

@@ -1,0 +1,439 @@
+"""GPU parity: every stage of the hot path through the C ABI (libne.so, sm_100a)
+against the CPU oracle on the same seeded inputs, bit-exact (all work is
+integer).  Sizes span several tiles plus ragged tails; edge cases cover empty
+inputs, M = 3..32, every excluded stream, maximal values and faults."""
+import numpy as np
+import pytest
+import torch
+
+import paper_1604_04740_b200 as ne
+from _gpu import bitmap_to_flags, dev, empty_streams, to_np, to_streams
+
+pytestmark = pytest.mark.gpu
+
+MS = [3, 4, 5, 8, 11, 16, 32]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    ne.build()
+    ne.lib()
+    assert torch.cuda.is_available()
+
+
+def gen(O, seed, tag, M, N, lo, hi):
+    return np.stack([O.gen_uniform(seed, tag, m, lo, hi, N) for m in range(M)])
+
+
+# ------------------------------------------------------------------ inputs
+@pytest.mark.parametrize("N", [1, 5, 4096, 100003])
+def test_generator_parity(O, N):
+    out = torch.empty(N, dtype=torch.int32, device="cuda")
+    for (seed, tag, st, lo, hi) in [(0, 1, 2, -1024, 1024), (3, 4, 0, -2 ** 31, 2 ** 31 - 1), (9, 7, 1, 0, 1)]:
+        ne.ne_gen_uniform_i32(seed, tag, st, lo, hi, out)
+        assert (out.cpu().numpy() == O.gen_uniform(seed, tag, st, lo, hi, N)).all()
+    ne.ne_gen_perm_i32(5, 6, out)
+    assert (out.cpu().numpy() == O.gen_perm(5, 6, N)).all()
+
+
+# ------------------------------------------------------------------ a1 / a2
+@pytest.mark.parametrize("M", MS)
+@pytest.mark.parametrize("N", [1, 3, 4, 1029, 65536 + 7])
+def test_entangle_soa(O, M, N):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    hi = O.dynamic_range(ocfg)
+    lim = min(hi, 2 ** 31 - 1)
+    c = gen(O, M, 1, M, N, -lim, lim + 1)
+    eps = empty_streams(M, N)
+    diag = ne.diag_new()
+    ne.ne_entangle(cfg, to_streams(c), eps, diag)
+    assert (to_np(eps) == O.entangle(ocfg, c)).all()
+    d = ne.diag_read(diag)
+    assert d["range_violations"] == O.range_check(c, hi)[0]
+
+
+def test_entangle_range_violation_names_first(O):
+    """a0: values the output format cannot hold are counted and the first is
+    named m*N + n.  With w = 64 every int32 input is inside Eq. 13's
+    range, so the limb format (L = 1 digit: [-128, 127]) exercises the path."""
+    cfg, ocfg = ne.ne_config_for(3), O.config_for(3, 64)
+    N = 1008
+    c = np.zeros((3, N), dtype=np.int64)
+    c[1, 17] = 5000
+    c[2, 3] = -4000
+    planes = torch.empty(3 * N, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_limbs(cfg, to_streams(c), 1, planes, diag)
+    d = ne.diag_read(diag)
+    eps = O.entangle(ocfg, c)
+    bad = np.argwhere((eps > 127) | (eps < -128))
+    assert d["range_violations"] == len(bad) > 0
+    assert d["first_bad"] == min(m * N + n for m, n in bad)
+
+
+@pytest.mark.parametrize("M", [3, 4, 8, 5])
+@pytest.mark.parametrize("N", [1, 7, 4096 + 5])
+def test_entangle_aos(O, M, N):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 11, 1, M, N, -2 ** 12, 2 ** 12)
+    aos = torch.empty(N * M, dtype=torch.int64, device="cuda")
+    ne.ne_entangle_aos(cfg, to_streams(c), aos)
+    assert (aos.cpu().numpy().reshape(N, M).T == O.entangle(ocfg, c)).all()
+
+
+@pytest.mark.parametrize("M,L,B", [(3, 4, 64), (8, 2, 32), (4, 4, 1000), (3, 3, 16), (3, 1, 0)])
+def test_entangle_limbs(O, M, L, B):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    N = 4096 + 16
+    c = gen(O, 2, 4, M, N, -B, B + 1)
+    planes = torch.empty(M * L * N, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_limbs(cfg, to_streams(c), L, planes, diag)
+    p = planes.cpu().numpy().astype(np.int64).reshape(M, L, N)
+    recon = sum(p[:, i, :] * (256 ** i) for i in range(L))
+    assert (recon == O.entangle(ocfg, c)).all()
+    assert p.min() >= -128 and p.max() <= 127
+    assert ne.diag_read(diag)["range_violations"] == 0
+
+
+@pytest.mark.parametrize("M", [3, 8])
+def test_entangle_stream_and_shared(O, M):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    N = 3001
+    c = gen(O, 4, 1, M, N, -32, 32)
+    ref = O.entangle(ocfg, c)
+    cs = to_streams(c)
+    for m in range(M):
+        out = torch.empty(N, dtype=torch.int64, device="cuda")
+        ne.ne_entangle_stream(cfg, m, cs[m], cs[(m - 1) % M], out)
+        assert (out.cpu().numpy() == ref[m]).all()
+    g = O.gen_uniform(1, 2, 0, -1000, 1000, N)
+    ge = torch.empty(N, dtype=torch.int64, device="cuda")
+    ne.ne_entangle_shared(cfg, dev(g, torch.int32), ge)
+    assert (ge.cpu().numpy() == O.entangle_shared(ocfg, g)).all()
+
+
+# ------------------------------------------------------------------ a4 / a5 / a6
+@pytest.mark.parametrize("M", MS)
+@pytest.mark.parametrize("N", [1, 2, 63, 64, 65, 4096 + 33])
+def test_disentangle_check_clean_and_faulty(O, M, N):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    hi = O.dynamic_range(ocfg)
+    rng = np.random.default_rng(M * 1000 + N)
+    c = rng.integers(-hi, hi + 1, size=(M, N))
+    c[:, 0] = hi
+    delta = O.entangle(ocfg, c)
+    # corrupt ~1/8 of positions in one random stream with a random 64-bit mask
+    bad = rng.random(N) < 0.125
+    for n in np.flatnonzero(bad):
+        s = rng.integers(0, M)
+        delta[s, n] ^= np.int64(rng.integers(1, 2 ** 63))
+    for r in sorted({0, M - 1, int(rng.integers(0, M))}):
+        d_out = empty_streams(M, N)
+        bm = torch.full(((N + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        diag = ne.diag_new()
+        ne.ne_disentangle_check(cfg, to_streams(delta, torch.int64), r, d_out, bm, diag)
+        od, oflags, onf = O.disentangle_check(ocfg, delta, r)
+        assert (to_np(d_out) == od).all()
+        assert (bitmap_to_flags(bm, N) == oflags).all()
+        d = ne.diag_read(diag)
+        assert d["fault_positions"] == onf == int(bad.sum())  # every single-stream fault caught
+        assert d["first_fault"] == (int(np.flatnonzero(oflags)[0]) if onf else None)
+
+
+@pytest.mark.parametrize("M", MS)
+def test_recover_every_stream(O, M):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    hi = O.dynamic_range(ocfg)
+    N = 5003
+    rng = np.random.default_rng(M)
+    c = rng.integers(-hi, hi + 1, size=(M, N))
+    delta = O.entangle(ocfg, c)
+    ds = to_streams(delta, torch.int64)
+    for r in range(M):
+        part = [None if m == r else ds[m] for m in range(M)]
+        d_out = empty_streams(M, N)
+        ne.ne_recover(cfg, part, r, d_out)
+        assert (to_np(d_out) == c).all()
+    with pytest.raises(ne.NeError):
+        ne.ne_recover(cfg, [None, None] + ds[2:], 0, empty_streams(M, N))
+
+
+def test_empty_and_bad_args():
+    cfg = ne.ne_config_for(3)
+    z = empty_streams(3, 0)
+    ne.ne_disentangle_check(cfg, z, 0, empty_streams(3, 0))
+    with pytest.raises(ne.NeError):
+        ne.ne_disentangle_check(cfg, empty_streams(3, 8), 3, empty_streams(3, 8))
+    base = torch.empty(9, dtype=torch.int64, device="cuda")
+    with pytest.raises(ne.NeError):  # misaligned stream pointer
+        ne.ne_op_scale(cfg, [base[1:5], base[1:5], base[1:5]], 2)
+
+
+# ------------------------------------------------------------------ C1 (BASELINE configs[0])
+def c1_pipeline_oracle(O, c, a, s=37):
+    ocfg = O.config_for(3, 64)
+    eps = O.entangle(ocfg, c)
+    delta = O.op_add(ocfg, O.op_scale(ocfg, eps, s), O.entangle(ocfg, a), 1)
+    return ocfg, delta
+
+
+def test_c1_full_chain(O):
+    """C1: M=3, N=4096, c,a ~ U[-2^10, 2^10) (seed 0), eps = E c, alpha = E a,
+    delta = 37 eps + alpha, disentangle + check (r = 0), recovery of every r."""
+    M, N = 3, 4096
+    cfg = ne.ne_config_for(M)
+    c_dev = [torch.empty(N, dtype=torch.int32, device="cuda") for _ in range(M)]
+    a_dev = [torch.empty(N, dtype=torch.int32, device="cuda") for _ in range(M)]
+    for m in range(M):
+        ne.ne_gen_uniform_i32(0, 1, m, -1024, 1024, c_dev[m])
+        ne.ne_gen_uniform_i32(0, 2, m, -1024, 1024, a_dev[m])
+    c = gen(O, 0, 1, M, N, -1024, 1024)
+    a = gen(O, 0, 2, M, N, -1024, 1024)
+    assert (to_np(c_dev) == c).all() and (to_np(a_dev) == a).all()
+    eps, alpha = empty_streams(M, N), empty_streams(M, N)
+    diag = ne.diag_new()
+    ne.ne_entangle(cfg, c_dev, eps, diag)
+    ne.ne_entangle(cfg, a_dev, alpha, diag)
+    ne.ne_op_scale(cfg, eps, 37)
+    ne.ne_op_add(cfg, eps, alpha, 1)
+    ocfg, delta = c1_pipeline_oracle(O, c, a)
+    assert (to_np(eps) == delta).all()
+    d_out = empty_streams(M, N)
+    bm = torch.empty(N // 32, dtype=torch.int32, device="cuda")
+    ne.ne_disentangle_check(cfg, eps, 0, d_out, bm, diag)
+    od, oflags, onf = O.disentangle_check(ocfg, delta, 0)
+    assert (to_np(d_out) == od).all() and (od == 37 * c + a).all()
+    assert onf == 0 and (bitmap_to_flags(bm, N) == 0).all()
+    dd = ne.diag_read(diag)
+    assert dd["range_violations"] == 0 and dd["fault_positions"] == 0
+    for r in range(M):
+        part = [None if m == r else eps[m] for m in range(M)]
+        rec = empty_streams(M, N)
+        ne.ne_recover(cfg, part, r, rec)
+        assert (to_np(rec) == od).all()
+
+
+def test_c1_exhaustive_single_bit_injection(O):
+    """C1 a7: all 3 x 64 x 64 = 12 288 single-bit flips of the first 64 outputs;
+    each must flag exactly its own position, and (flag, d_hat) must equal the
+    oracle's for the same corrupted tuple."""
+    M, N, W = 3, 4096, 64
+    cfg = ne.ne_config_for(M)
+    c = gen(O, 0, 1, M, N, -1024, 1024)
+    a = gen(O, 0, 2, M, N, -1024, 1024)
+    ocfg, delta = c1_pipeline_oracle(O, c, a)
+    T = M * W * 64
+    fw = torch.empty(T, dtype=torch.int64, device="cuda")
+    dh = torch.empty(T * M, dtype=torch.int64, device="cuda")
+    ne.ne_inject_sweep(cfg, to_streams(delta, torch.int64), W, 0, fw, dh)
+    fw = fw.cpu().numpy().view(np.uint64)
+    dh = dh.cpu().numpy().reshape(T, M)
+    for t in range(T):
+        s, n, bit = t // (W * 64), (t // 64) % W, t % 64
+        col = delta[:, n].copy()
+        col[s] = np.int64(np.uint64(col[s]) ^ np.uint64(1 << bit))
+        od, of = O.disentangle_one(ocfg, col, 0)
+        assert of == 1
+        assert int(fw[t]) == (1 << n), (s, n, bit)
+        assert (dh[t] == od).all(), (s, n, bit)
+
+
+# ------------------------------------------------------------------ a3 ops
+@pytest.mark.parametrize("M", [3, 4, 8, 5])
+@pytest.mark.parametrize("N", [1, 17, 4096 + 3])
+def test_scale_add_elementwise(O, M, N):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    rng = np.random.default_rng(N + M)
+    x = rng.integers(-2 ** 40, 2 ** 40, size=(M, N))
+    g = rng.integers(-2 ** 31, 2 ** 31, size=N)
+    xs = to_streams(x, torch.int64)
+    ne.ne_op_scale(cfg, xs, -12345)
+    assert (to_np(xs) == O.op_scale(ocfg, x, -12345)).all()
+    ne.ne_op_scale(cfg, xs, 0, dev(g, torch.int32))
+    ref = O.op_scale(ocfg, O.op_scale(ocfg, x, -12345), g=g)
+    assert (to_np(xs) == ref).all()
+    a = rng.integers(-2 ** 62, 2 ** 62, size=(M, N))
+    ne.ne_op_add(cfg, xs, to_streams(a, torch.int64), -1)
+    assert (to_np(xs) == O.op_add(ocfg, ref, a, -1)).all()
+
+
+@pytest.mark.parametrize("N,T", [(65536, 64), (1000, 64), (777, 1), (50, 300), (4099, 2500)])
+@pytest.mark.parametrize("correlate", [False, True])
+def test_conv(O, N, T, correlate):
+    M = 3
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 1, 1, M, N, -128, 128)
+    g = O.gen_uniform(1, 3, 0, -128, 128, T)
+    eps = O.entangle(ocfg, c)
+    out = empty_streams(M, N)
+    ne.ne_op_conv(cfg, to_streams(eps, torch.int64), dev(g, torch.int32), out, correlate)
+    assert (to_np(out) == O.op_conv(ocfg, eps, g, correlate)).all()
+
+
+def test_conv_int64_path(O):
+    """Windows that do not fit int32 take the full 64-bit MAC path."""
+    cfg, ocfg = ne.ne_config_for(3), O.config_for(3, 64)
+    rng = np.random.default_rng(5)
+    x = rng.integers(-2 ** 62, 2 ** 62, size=(3, 3000))
+    g = rng.integers(-2 ** 31, 2 ** 31, size=70)
+    out = empty_streams(3, 3000)
+    ne.ne_op_conv(cfg, to_streams(x, torch.int64), dev(g, torch.int32), out)
+    assert (to_np(out) == O.op_conv(ocfg, x, g)).all()
+
+
+def test_c2_conv_full_pipeline(O):
+    """C2: M=3, N=65536, c ~ U[-128,128) seed 1, 64 taps ~ U[-128,128):
+    entangle -> circular conv -> disentangle + check == plain circular conv."""
+    M, N, T = 3, 65536, 64
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 1, 1, M, N, -128, 128)
+    g = O.gen_uniform(1, 3, 0, -128, 128, T)
+    eps = empty_streams(M, N)
+    ne.ne_entangle(cfg, to_streams(c), eps)
+    out = empty_streams(M, N)
+    ne.ne_op_conv(cfg, eps, dev(g, torch.int32), out)
+    d_out = empty_streams(M, N)
+    diag = ne.diag_new()
+    ne.ne_disentangle_check(cfg, out, 0, d_out, None, diag)
+    assert (to_np(d_out) == O.op_conv(O.config_for(M, 64), c, g)).all()
+    assert ne.diag_read(diag)["fault_positions"] == 0
+
+
+@pytest.mark.parametrize("M", [3, 4, 8, 6])
+@pytest.mark.parametrize("N,block,vlen", [(1024 * 40, 1024, 1024), (5000, 1024, 1024), (1000, 16, 16),
+                                          (3333, 100, 3333), (64, 1024, 1024)])
+def test_inner(O, M, N, block, vlen):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    rng = np.random.default_rng(N)
+    x = rng.integers(-2 ** 40, 2 ** 40, size=(M, N))
+    v = rng.integers(-2 ** 12, 2 ** 12, size=vlen)
+    nb = (N + block - 1) // block
+    out = empty_streams(M, nb)
+    ne.ne_op_inner(cfg, to_streams(x, torch.int64), dev(v, torch.int32), block, out)
+    assert (to_np(out) == O.op_inner(ocfg, x, v, block)).all()
+
+
+@pytest.mark.parametrize("M", [3, 4, 8, 5])
+@pytest.mark.parametrize("aos", [True, False])
+@pytest.mark.parametrize("gather", [True, False])
+def test_permute_inner_check(O, M, aos, gather):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    N, B = 1024 * 37 + 500, 1024
+    c = gen(O, 3, 1, M, N, -2 ** 12, 2 ** 12)
+    perm = O.gen_perm(3, 6, N)
+    v = O.gen_uniform(3, 7, 0, -2 ** 12, 2 ** 12, B)
+    eps = O.entangle(ocfg, c)
+    # inject single-stream faults into a few stored eps values -> those blocks flag
+    nb = (N + B - 1) // B
+    xs = to_streams(eps, torch.int64)
+    x_aos = dev(eps.T.copy(), torch.int64).reshape(-1)
+    d_out, delta = empty_streams(M, nb), empty_streams(M, nb)
+    bm = torch.empty((nb + 31) // 32, dtype=torch.int32, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_op_permute_inner_check(cfg, dev(v, torch.int32), B, 1 % M, d_out,
+                                 x=None if aos else xs, x_aos=x_aos if aos else None,
+                                 perm=dev(perm, torch.int32) if gather else None, n=N,
+                                 delta_out=delta, bitmap=bm, diag=diag)
+    p = perm if gather else np.arange(N)
+    odelta = O.op_inner(ocfg, O.op_permute(eps, p), v, B)
+    assert (to_np(delta) == odelta).all()
+    od, oflags, onf = O.disentangle_check(ocfg, odelta, 1 % M)
+    assert (to_np(d_out) == od).all()
+    assert (od == O.op_inner(O.config_for(M, 64), c[:, p], v, B)).all()
+    assert (bitmap_to_flags(bm, nb) == oflags).all() and onf == 0
+    assert ne.diag_read(diag)["fault_positions"] == 0
+
+
+def test_permute_inner_detects_storage_fault(O):
+    """A fault in one stored eps word (one stream) is caught in its block."""
+    M, N, B = 4, 1024 * 64, 1024
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 3, 1, M, N, -2 ** 12, 2 ** 12)
+    perm = O.gen_perm(3, 6, N)
+    v = O.gen_uniform(3, 7, 0, -2 ** 12, 2 ** 12, B)
+    eps = O.entangle(ocfg, c)
+    x_aos = eps.T.copy()
+    hit = [(5, 2, 1 << 40), (70000 % N, 0, 1), (N - 1, 3, 1 << 63)]
+    for pos, s, mask in hit:
+        x_aos[pos, s] = np.int64(np.uint64(x_aos[pos, s]) ^ np.uint64(mask))
+    nb = N // B
+    d_out = empty_streams(M, nb)
+    bm = torch.empty(nb // 32, dtype=torch.int32, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_op_permute_inner_check(cfg, dev(v, torch.int32), B, 0, d_out, x_aos=dev(x_aos, torch.int64).reshape(-1),
+                                 perm=dev(perm, torch.int32), n=N, bitmap=bm, diag=diag)
+    inv = np.argsort(perm)
+    blocks = sorted({int(inv[pos]) // B for pos, _, _ in hit})
+    flags = bitmap_to_flags(bm, nb)
+    assert list(np.flatnonzero(flags)) == blocks
+    odelta = O.op_inner(ocfg, O.op_permute(np.ascontiguousarray(x_aos.T), perm), v, B)
+    od, oflags, _ = O.disentangle_check(ocfg, odelta, 0)
+    assert (to_np(d_out) == od).all() and (oflags == flags).all()
+    assert ne.diag_read(diag)["fault_positions"] == len(blocks)
+
+
+@pytest.mark.parametrize("M", [3, 8])
+def test_permute_outer(O, M):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    N = 10007
+    rng = np.random.default_rng(2)
+    x = rng.integers(-2 ** 40, 2 ** 40, size=(M, N))
+    perm = O.gen_perm(8, 6, N)
+    out = empty_streams(M, N)
+    ne.ne_op_permute(cfg, to_streams(x, torch.int64), dev(perm, torch.int32), out)
+    assert (to_np(out) == O.op_permute(x, perm)).all()
+    for n1, n2 in [(37, 64), (100, 33), (1, 1)]:
+        h = rng.integers(-2 ** 31, 2 ** 31, size=n2)
+        xs = x[:, :n1].copy()
+        o = empty_streams(M, n1 * n2)
+        ne.ne_op_outer(cfg, to_streams(xs, torch.int64), dev(h, torch.int32), o)
+        assert (to_np(o) == O.op_outer(ocfg, xs, h).reshape(M, -1)).all()
+
+
+# ------------------------------------------------------------------ GEMM
+@pytest.mark.parametrize("rows,cols,K", [(64, 64, 16), (100, 37, 129), (256, 128, 384), (1, 1, 1)])
+def test_gemm_imad64(O, rows, cols, K):
+    M = 3
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    A = np.stack([O.gen_uniform(2, 4, m, -64, 64, rows * K) for m in range(M)])
+    B = O.gen_uniform(2, 5, 0, -64, 64, K * cols)
+    E = O.entangle(ocfg, A)
+    out = empty_streams(M, rows * cols)
+    ne.ne_op_gemm(cfg, to_streams(E, torch.int64), dev(B, torch.int32), rows, cols, K, out, algo=ne.NE_GEMM_IMAD64)
+    ref = O.op_gemm(ocfg, E.reshape(M, rows, K), B.reshape(K, cols)).reshape(M, -1)
+    assert (to_np(out) == ref).all()
+
+
+@pytest.mark.parametrize("M,L,bound,rows,cols,K", [
+    (3, 4, 64, 128, 128, 128), (3, 4, 64, 256, 384, 512), (8, 2, 32, 128, 256, 256),
+    (4, 4, 1000, 128, 128, 1024), (3, 3, 16, 128, 128, 256), (3, 1, 0, 128, 256, 128), (8, 2, 32, 256, 128, 128)])
+def test_gemm_tc_i8(O, M, L, bound, rows, cols, K):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    assert ne.ne_gemm_limbs_for(cfg, bound) <= L
+    A = np.stack([O.gen_uniform(2, 4, m, -bound, bound + 1, rows * K) for m in range(M)])
+    B = O.gen_uniform(2, 5, 0, -64, 64, K * cols)
+    E = O.entangle(ocfg, A)
+    ref = O.op_gemm(ocfg, E.reshape(M, rows, K), B.reshape(K, cols)).reshape(M, -1)
+    # int64 entangled operand path (split in the op)
+    out = empty_streams(M, rows * cols)
+    ws = torch.empty(ne.ne_gemm_workspace(cfg, rows, cols, K, L), dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_op_gemm(cfg, to_streams(E, torch.int64), dev(B, torch.int32), rows, cols, K, out,
+                  algo=ne.NE_GEMM_TC_I8, L=L, ws=ws, diag=diag)
+    torch.cuda.synchronize()
+    assert ne.diag_read(diag)["range_violations"] == 0
+    assert (to_np(out) == ref).all()
+    # limb-plane path fed straight from the entangle kernel
+    planes = torch.empty(M * L * rows * K, dtype=torch.int8, device="cuda")
+    ne.ne_entangle_limbs(cfg, to_streams(A), L, planes)
+    Bt = torch.empty(cols * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, cols, Bt)
+    out2 = empty_streams(M, rows * cols)
+    ne.ne_op_gemm_limbs(cfg, planes, L, Bt, rows, cols, K, out2)
+    assert (to_np(out2) == ref).all()
+    d_out = empty_streams(M, rows * cols)
+    ne.ne_disentangle_check(cfg, out2, 0, d_out, None, diag)
+    plain = (A.reshape(M, rows, K) @ B.reshape(K, cols)).reshape(M, -1)
+    assert (to_np(d_out) == plain).all()
+    assert ne.diag_read(diag)["fault_positions"] == 0
