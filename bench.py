@@ -1,0 +1,779 @@
+#!/usr/bin/env python
+"""bench.py — the entangle -> LSB op -> disentangle + check -> recover hot path
+of arXiv 1604.04740 on B200, through libne.so's C ABI.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c2|c4]
+                    [--impl ours|reference]
+
+One "step" is one pass of every §8(a) stage of the chosen BASELINE.json config
+over one batch of synthetic (seeded, counter-generated) input that is already
+resident in HBM: a0+a1 entangle (range-asserted), a3 the LSB op, a4+a5
+disentangle + reliability check, a6 fail-stop recovery of stream (step mod M).
+Default workload = configs[2] (C3), the largest single-GPU configuration by
+work: the M = 3 entangled 4096^3 integer GEMM on tcgen05 int8 limbs.
+
+Rank 0 prints ONE JSON line (contract in the task statement).  Under torchrun
+(N > 1) every rank runs its own independent instance (weak scaling, no
+data-path collective); timing is max over ranks of CUDA-event time.
+``--impl reference`` times the CPU oracle (oracle/, plain C, 1 core) on a
+bounded sample of the same workload; only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return dict(FALLBACK), "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
+
+
+# ====================================================================== workloads
+class Workload:
+    """A BASELINE.json config: buffers, one step as a list of named stages."""
+
+    name = ""
+    metric_unit = ""
+    launches_per_step = 0
+
+    def stages(self, i):  # -> list of (stage_name, callable)
+        raise NotImplementedError
+
+    def work_per_step(self):  # metric units per step (before /time)
+        raise NotImplementedError
+
+    def stage_info(self):  # stage -> (bound, algorithmic amount per launch, unit)
+        raise NotImplementedError
+
+
+class C3Gemm(Workload):
+    """configs[2]: M=3 entangled GEMM, A_m 4096x4096 int32 in [-64,64), shared B
+    4096x4096 in [-64,64), K = 4096, int64 results; tcgen05 int8 limbs (L = 4)."""
+
+    name = "C3"
+    metric_unit = "Gop/s"
+
+    def __init__(self, rank, n=4096, seed=2, algo="tc"):
+        import torch
+        import paper_1604_04740_b200 as ne
+
+        self.ne, self.torch = ne, torch
+        self.M, self.rows, self.cols, self.K = 3, n, n, n
+        self.seed = seed + 1000 * rank
+        self.cfg = ne.ne_config_for(self.M)
+        self.L = ne.ne_gemm_limbs_for(self.cfg, 64)
+        self.algo = algo
+        M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
+        dev = "cuda"
+        self.A = [torch.empty(R * K, dtype=torch.int32, device=dev) for _ in range(M)]
+        for m in range(M):
+            ne.ne_gen_uniform_i32(self.seed, 4, m, -64, 64, self.A[m])
+        self.B = torch.empty(K * Cc, dtype=torch.int32, device=dev)
+        ne.ne_gen_uniform_i32(self.seed, 5, 0, -64, 64, self.B)
+        self.planes = torch.empty(M * L * R * K, dtype=torch.int8, device=dev)
+        self.Bt = torch.empty(Cc * K, dtype=torch.int8, device=dev)
+        self.delta = [torch.empty(R * Cc, dtype=torch.int64, device=dev) for _ in range(M)]
+        self.dout = [torch.empty(R * Cc, dtype=torch.int64, device=dev) for _ in range(M)]
+        self.drec = [torch.empty(R * Cc, dtype=torch.int64, device=dev) for _ in range(M)]
+        self.bitmap = torch.empty(R * Cc // 32, dtype=torch.int32, device=dev)
+        self.diag = ne.diag_new()
+        if algo == "imad":
+            self.eps = [torch.empty(R * K, dtype=torch.int64, device=dev) for _ in range(M)]
+        self.launches_per_step = 5
+
+    def stages(self, i):
+        ne, cfg, M = self.ne, self.cfg, self.M
+        r = i % M
+        part = [None if m == r else self.delta[m] for m in range(M)]
+        if self.algo == "imad":
+            return [
+                ("entangle", lambda: ne.ne_entangle(cfg, self.A, self.eps, self.diag)),
+                ("gemm", lambda: ne.ne_op_gemm(cfg, self.eps, self.B, self.rows, self.cols, self.K, self.delta,
+                                               algo=ne.NE_GEMM_IMAD64)),
+                ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
+                ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
+            ]
+        return [
+            ("entangle", lambda: ne.ne_entangle_limbs(cfg, self.A, self.L, self.planes, self.diag)),
+            ("prep_b", lambda: ne.ne_gemm_prep_b(self.B, self.K, self.cols, self.Bt, self.diag)),
+            ("gemm", lambda: ne.ne_op_gemm_limbs(cfg, self.planes, self.L, self.Bt, self.rows, self.cols, self.K,
+                                                 self.delta)),
+            ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
+            ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
+        ]
+
+    def work_per_step(self):
+        return 2 * self.M * self.rows * self.cols * self.K / 1e9  # G int64-equivalent ops
+
+    def stage_info(self):
+        M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
+        n = R * Cc
+        gemm = ("tensor", 2 * L * M * R * Cc * K / 1e12, "TOP") if self.algo == "tc" else \
+            ("alu", M * R * Cc * K / 1e12, "TMAC")
+        return {
+            "entangle": ("hbm", M * R * K * (4 + (L if self.algo == "tc" else 8)) / 1e9, "GB"),
+            "prep_b": ("hbm", K * Cc * 5 / 1e9, "GB"),
+            "gemm": gemm,
+            "check": ("hbm", (M * n * 16 + n / 8) / 1e9, "GB"),
+            "recover": ("hbm", ((M - 1) * n * 8 + M * n * 8) / 1e9, "GB"),
+        }
+
+    def config(self):
+        return {"workload": "C3 (BASELINE configs[2]): M=3 entangled GEMM A_m 4096x4096 int32 U[-64,64), "
+                            "shared B 4096x4096 U[-64,64), K=4096, int64 results",
+                "M": self.M, "rows": self.rows, "cols": self.cols, "K": self.K,
+                "limbs_L": self.L if self.algo == "tc" else None, "gemm_algo": self.algo,
+                "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
+                "l2": "working set ~1.9 GB per step >> 126 MB L2 (no flush needed)",
+                "step": "entangle(limbs)+prep_B+GEMM+disentangle/check(r=0)+recover(r=step mod 3)"}
+
+    # ---- end-to-end through host buffers
+    def e2e_setup(self):
+        torch = self.torch
+        self.hA = [a.cpu().pin_memory() for a in self.A]
+        self.hB = self.B.cpu().pin_memory()
+        self.hout = [torch.empty(self.rows * self.cols, dtype=torch.int64).pin_memory() for _ in range(self.M)]
+        self.hdiag = torch.empty(4, dtype=torch.int64).pin_memory()
+        return (sum(a.numel() * 4 for a in self.hA) + self.hB.numel() * 4,
+                sum(o.numel() * 8 for o in self.hout) + 32)
+
+    def e2e_step(self, i):
+        for m in range(self.M):
+            self.A[m].copy_(self.hA[m], non_blocking=True)
+        self.B.copy_(self.hB, non_blocking=True)
+        for _, f in self.stages(i):
+            f()
+        for m in range(self.M):
+            self.hout[m].copy_(self.dout[m], non_blocking=True)
+        self.hdiag.copy_(self.diag, non_blocking=True)
+
+    # ---- plain (unentangled) comparison: the paper's "conventional" routine
+    def plain_times(self, reps=5):
+        """GEMM on plain A: (i) same tcgen05 kernel with the same L limbs,
+        (ii) the narrowest native form (1 int8 limb); ms per call."""
+        torch, ne = self.torch, self.ne
+        if self.algo != "tc":
+            return {}
+        M, R, K = self.M, self.rows, self.K
+        out = {}
+        for tag, L in (("same_kernel_L%d" % self.L, self.L), ("native_L1", 1)):
+            planes = torch.zeros(M * L * R * K, dtype=torch.int8, device="cuda")
+            pv = planes.view(M, L, R * K)
+            for m in range(M):
+                pv[m, 0].copy_(self.A[m].to(torch.int8))  # |A| < 64: one digit, the rest 0
+            ne.ne_op_gemm_limbs(self.cfg, planes, L, self.Bt, R, self.cols, K, self.delta)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                ne.ne_op_gemm_limbs(self.cfg, planes, L, self.Bt, R, self.cols, K, self.delta)
+            e1.record()
+            torch.cuda.synchronize()
+            out[tag] = e0.elapsed_time(e1) / reps
+            del planes
+        return out
+
+    # ---- CPU oracle on a bounded sample (rows of every stream)
+    def oracle_sample(self, rows_sample):
+        import oracle as O
+
+        M, K, Cc = self.M, self.K, self.cols
+        ocfg = O.config_for(M, 64)
+        A = np.stack([O.gen_uniform(self.seed, 4, m, -64, 64, rows_sample * K) for m in range(M)])
+        B = O.gen_uniform(self.seed, 5, 0, -64, 64, K * Cc).reshape(K, Cc)
+        t0 = time.perf_counter()
+        E = O.entangle(ocfg, A)
+        D = O.op_gemm(ocfg, E.reshape(M, rows_sample, K), B).reshape(M, -1)
+        d, flags, nf = O.disentangle_check(ocfg, D, 0)
+        O.recover(ocfg, [None] + [D[m] for m in range(1, M)], 0)
+        dt = time.perf_counter() - t0
+        return dt, 2 * M * rows_sample * Cc * K / 1e9, f"{rows_sample} of {self.rows} rows of each of the " \
+                                                       f"M=3 streams, full K and cols (same seeded inputs)"
+
+
+class C4PermInner(Workload):
+    """configs[3]: M=4 streams of 2^28 int32 U[-2^12, 2^12): permutation by a
+    seeded bijection, then inner products with a shared 1024-vector in blocks
+    of 1024; HBM-bound.  eps at rest in the AoS layout (one 32-B sector per
+    position), gather + inner + disentangle/check fused."""
+
+    name = "C4"
+    metric_unit = "GB/s"
+
+    def __init__(self, rank, n=1 << 28, seed=3):
+        import torch
+        import paper_1604_04740_b200 as ne
+
+        self.ne, self.torch = ne, torch
+        self.M, self.n, self.B = 4, n, 1024
+        self.seed = seed + 1000 * rank
+        self.cfg = ne.ne_config_for(4)
+        dev = "cuda"
+        self.c = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(4)]
+        for m in range(4):
+            ne.ne_gen_uniform_i32(self.seed, 1, m, -(1 << 12), 1 << 12, self.c[m])
+        self.perm = torch.empty(n, dtype=torch.int32, device=dev)
+        ne.ne_gen_perm_i32(self.seed, 6, self.perm)
+        self.v = torch.empty(self.B, dtype=torch.int32, device=dev)
+        ne.ne_gen_uniform_i32(self.seed, 7, 0, -(1 << 12), 1 << 12, self.v)
+        self.eps = torch.empty(n * 4, dtype=torch.int64, device=dev)
+        self.nb = n // self.B
+        self.delta = [torch.empty(self.nb, dtype=torch.int64, device=dev) for _ in range(4)]
+        self.dout = [torch.empty(self.nb, dtype=torch.int64, device=dev) for _ in range(4)]
+        self.drec = [torch.empty(self.nb, dtype=torch.int64, device=dev) for _ in range(4)]
+        self.bitmap = torch.empty((self.nb + 31) // 32, dtype=torch.int32, device=dev)
+        self.diag = ne.diag_new()
+        self.launches_per_step = 3
+
+    def stages(self, i):
+        ne, cfg = self.ne, self.cfg
+        r = i % 4
+        part = [None if m == r else self.delta[m] for m in range(4)]
+        return [
+            ("entangle", lambda: ne.ne_entangle_aos(cfg, self.c, self.eps, self.diag)),
+            ("permute_inner_check", lambda: ne.ne_op_permute_inner_check(
+                cfg, self.v, self.B, 0, self.dout, x_aos=self.eps, perm=self.perm, n=self.n,
+                delta_out=self.delta, bitmap=self.bitmap, diag=self.diag)),
+            ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
+        ]
+
+    def work_per_step(self):  # algorithmic GB per step: entangle 48 B + gather/inner 36 B per position
+        return self.n * (48 + 36) / 1e9
+
+    def stage_info(self):
+        n, nb = self.n, self.nb
+        return {"entangle": ("hbm", n * 48 / 1e9, "GB"),
+                "permute_inner_check": ("hbm", (n * 36 + nb * 4 * 16) / 1e9, "GB"),
+                "recover": ("hbm", nb * 7 * 8 / 1e9, "GB")}
+
+    def config(self):
+        return {"workload": "C4 (BASELINE configs[3]): M=4 streams of 2^28 int32 U[-2^12,2^12), seeded "
+                            "permutation, inner products with a shared 1024-vector in blocks of 1024",
+                "M": 4, "n": self.n, "block": self.B, "layout": "AoS (position-major) entangled int64",
+                "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
+                "l2": "working set ~13 GB >> 126 MB L2 (no flush needed)",
+                "step": "entangle(AoS)+gather/inner/disentangle/check fused(r=0)+recover(r=step mod 4)"}
+
+    def e2e_setup(self):
+        self.hc = [x.cpu().pin_memory() for x in self.c]
+        self.hout = [self.torch.empty(self.nb, dtype=self.torch.int64).pin_memory() for _ in range(4)]
+        return sum(x.numel() * 4 for x in self.hc), sum(o.numel() * 8 for o in self.hout)
+
+    def e2e_step(self, i):
+        for m in range(4):
+            self.c[m].copy_(self.hc[m], non_blocking=True)
+        for _, f in self.stages(i):
+            f()
+        for m in range(4):
+            self.hout[m].copy_(self.dout[m], non_blocking=True)
+
+    def plain_times(self, reps=3):
+        """Same gather + inner kernel on plain (unentangled) data in the same
+        int64 AoS containers, no check: the paper's conventional routine."""
+        torch, ne = self.torch, self.ne
+        plain = torch.stack([x.to(torch.int64) for x in self.c], dim=1).reshape(-1).contiguous()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ne.ne_op_permute_inner_check(self.cfg, self.v, self.B, 0, self.drec, x_aos=plain, perm=self.perm,
+                                     n=self.n, delta_out=self.delta)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            ne.ne_op_permute_inner_check(self.cfg, self.v, self.B, 0, self.drec, x_aos=plain, perm=self.perm,
+                                         n=self.n, delta_out=self.delta)
+        e1.record()
+        torch.cuda.synchronize()
+        del plain
+        return {"same_kernel_plain_int64": e0.elapsed_time(e1) / reps}
+
+    def oracle_sample(self, blocks):
+        import oracle as O
+
+        ocfg = O.config_for(4, 64)
+        n, B = self.n, self.B
+        t0 = time.perf_counter()
+        idx = O.gen_perm(self.seed, 6, n, blocks * B, 0)
+        v = O.gen_uniform(self.seed, 7, 0, -(1 << 12), 1 << 12, B)
+        c = np.stack([np.concatenate([O.gen_uniform(self.seed, 1, m, -(1 << 12), 1 << 12, 1, int(p)) for p in idx])
+                      for m in range(4)])
+        eps = O.entangle(ocfg, c)
+        delta = O.op_inner(ocfg, eps, v, B)
+        O.disentangle_check(ocfg, delta, 0)
+        dt = time.perf_counter() - t0
+        return dt, blocks * B * 84 / 1e9, f"{blocks} output blocks of 1024 gathered positions (of {n // B})"
+
+
+class C2Conv(Workload):
+    """configs[1]: M=3 streams of 65536 int32 U[-128,128), circular convolution
+    with a shared 64-tap kernel U[-128,128), entangled int64."""
+
+    name = "C2"
+    metric_unit = "Gop/s"
+
+    def __init__(self, rank, n=65536, taps=64, seed=1):
+        import torch
+        import paper_1604_04740_b200 as ne
+
+        self.ne, self.torch = ne, torch
+        self.M, self.n, self.T = 3, n, taps
+        self.seed = seed + 1000 * rank
+        self.cfg = ne.ne_config_for(3)
+        self.c = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3)]
+        for m in range(3):
+            ne.ne_gen_uniform_i32(self.seed, 1, m, -128, 128, self.c[m])
+        self.g = torch.empty(taps, dtype=torch.int32, device="cuda")
+        ne.ne_gen_uniform_i32(self.seed, 3, 0, -128, 128, self.g)
+        mk = lambda: [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(3)]  # noqa: E731
+        self.eps, self.delta, self.dout, self.drec = mk(), mk(), mk(), mk()
+        self.bitmap = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+        self.diag = ne.diag_new()
+        self.launches_per_step = 4
+
+    def stages(self, i):
+        ne, cfg = self.ne, self.cfg
+        r = i % 3
+        part = [None if m == r else self.delta[m] for m in range(3)]
+        return [("entangle", lambda: ne.ne_entangle(cfg, self.c, self.eps, self.diag)),
+                ("conv", lambda: ne.ne_op_conv(cfg, self.eps, self.g, self.delta)),
+                ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
+                ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec))]
+
+    def work_per_step(self):
+        return 2 * self.M * self.n * self.T / 1e9
+
+    def stage_info(self):
+        n, M = self.n, self.M
+        return {"entangle": ("hbm", M * n * 12 / 1e9, "GB"),
+                "conv": ("alu", M * n * self.T / 1e12, "TMAC"),
+                "check": ("hbm", M * n * 16 / 1e9, "GB"),
+                "recover": ("hbm", 5 * n * 8 / 1e9, "GB")}
+
+    def config(self):
+        return {"workload": "C2 (BASELINE configs[1]): M=3 streams of 65536 int32 U[-128,128), circular "
+                            "convolution with a shared 64-tap kernel U[-128,128)",
+                "M": 3, "n": self.n, "taps": self.T, "l2": "working set 6 MB fits L2 (launch-latency bound)"}
+
+    def e2e_setup(self):
+        self.hc = [x.cpu().pin_memory() for x in self.c]
+        self.hout = [self.torch.empty(self.n, dtype=self.torch.int64).pin_memory() for _ in range(3)]
+        return self.n * 12, self.n * 24
+
+    def e2e_step(self, i):
+        for m in range(3):
+            self.c[m].copy_(self.hc[m], non_blocking=True)
+        for _, f in self.stages(i):
+            f()
+        for m in range(3):
+            self.hout[m].copy_(self.dout[m], non_blocking=True)
+
+    def plain_times(self, reps=20):
+        return {}
+
+    def oracle_sample(self, reps):
+        import oracle as O
+
+        ocfg = O.config_for(3, 64)
+        c = np.stack([O.gen_uniform(self.seed, 1, m, -128, 128, self.n) for m in range(3)])
+        g = O.gen_uniform(self.seed, 3, 0, -128, 128, self.T)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            eps = O.entangle(ocfg, c)
+            d = O.op_conv(ocfg, eps, g)
+            O.disentangle_check(ocfg, d, 0)
+        dt = time.perf_counter() - t0
+        return dt, reps * self.work_per_step(), f"{reps} full C2 passes"
+
+
+class C1Chain(Workload):
+    """configs[0]: M=3 streams of 4096 int32 U[-2^10,2^10), seed 0; scale by 37
+    then add a second seeded 3-stream set; disentangle + check."""
+
+    name = "C1"
+    metric_unit = "Gpositions/s"
+
+    def __init__(self, rank, n=4096, seed=0):
+        import torch
+        import paper_1604_04740_b200 as ne
+
+        self.ne, self.torch = ne, torch
+        self.M, self.n = 3, n
+        self.seed = seed + 1000 * rank
+        self.cfg = ne.ne_config_for(3)
+        mk32 = lambda: [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3)]  # noqa: E731
+        mk = lambda: [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(3)]  # noqa: E731
+        self.c, self.a = mk32(), mk32()
+        for m in range(3):
+            ne.ne_gen_uniform_i32(self.seed, 1, m, -1024, 1024, self.c[m])
+            ne.ne_gen_uniform_i32(self.seed, 2, m, -1024, 1024, self.a[m])
+        self.eps, self.alpha, self.dout, self.drec = mk(), mk(), mk(), mk()
+        self.bitmap = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+        self.diag = ne.diag_new()
+        self.launches_per_step = 6
+
+    def stages(self, i):
+        ne, cfg = self.ne, self.cfg
+        r = i % 3
+        part = [None if m == r else self.eps[m] for m in range(3)]
+        return [("entangle", lambda: (ne.ne_entangle(cfg, self.c, self.eps, self.diag),
+                                      ne.ne_entangle(cfg, self.a, self.alpha, self.diag))),
+                ("scale_add", lambda: (ne.ne_op_scale(cfg, self.eps, 37), ne.ne_op_add(cfg, self.eps, self.alpha))),
+                ("check", lambda: ne.ne_disentangle_check(cfg, self.eps, 0, self.dout, self.bitmap, self.diag)),
+                ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec))]
+
+    def work_per_step(self):
+        return self.n / 1e9
+
+    def stage_info(self):
+        n = self.n
+        return {"entangle": ("hbm", 2 * 3 * n * 12 / 1e9, "GB"), "scale_add": ("hbm", 3 * n * 40 / 1e9, "GB"),
+                "check": ("hbm", 3 * n * 16 / 1e9, "GB"), "recover": ("hbm", 5 * n * 8 / 1e9, "GB")}
+
+    def config(self):
+        return {"workload": "C1 (BASELINE configs[0]): M=3 streams of 4096 int32 U[-2^10,2^10), seed 0; "
+                            "scale by 37, add a second seeded 3-stream set; disentangle+check",
+                "M": 3, "n": self.n, "l2": "196 KB working set (launch-latency bound)"}
+
+    def e2e_setup(self):
+        self.hc = [x.cpu().pin_memory() for x in self.c + self.a]
+        self.hout = [self.torch.empty(self.n, dtype=self.torch.int64).pin_memory() for _ in range(3)]
+        return self.n * 24, self.n * 24
+
+    def e2e_step(self, i):
+        for d, h in zip(self.c + self.a, self.hc):
+            d.copy_(h, non_blocking=True)
+        for _, f in self.stages(i):
+            f()
+        for m in range(3):
+            self.hout[m].copy_(self.dout[m], non_blocking=True)
+
+    def plain_times(self, reps=20):
+        return {}
+
+    def oracle_sample(self, reps):
+        import oracle as O
+
+        ocfg = O.config_for(3, 64)
+        c = np.stack([O.gen_uniform(self.seed, 1, m, -1024, 1024, self.n) for m in range(3)])
+        a = np.stack([O.gen_uniform(self.seed, 2, m, -1024, 1024, self.n) for m in range(3)])
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            d = O.op_add(ocfg, O.op_scale(ocfg, O.entangle(ocfg, c), 37), O.entangle(ocfg, a))
+            O.disentangle_check(ocfg, d, 0)
+        dt = time.perf_counter() - t0
+        return dt, reps * self.n / 1e9, f"{reps} full C1 passes"
+
+
+WORKLOADS = {"c1": C1Chain, "c2": C2Conv, "c3": C3Gemm, "c4": C4PermInner}
+ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c3": (16, 2), "c4": (64, 8)}  # (cpu_baseline, per ref step)
+METRIC = "entangled LSB Gop/s (or GB/s) at 1/2/4/8 B200, % roofline, % overhead vs plain"
+
+
+# ====================================================================== clocks
+class ClockSampler:
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append((float(f[1]), float(f[2]), f[5], f[6], f[7], f[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [r for r in rows if r[0] > 500] or rows
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in loaded:
+            for nm, v in zip(names, r[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted(reasons), "samples": len(loaded)}
+
+
+# ====================================================================== runs
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1604_04740_b200 as ne
+
+    ne.lib()
+    torch.cuda.set_device(local_rank)
+    W = WORKLOADS[args.workload](rank) if args.workload != "c3" else C3Gemm(rank, algo=args.algo)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    for i in range(args.warmup):
+        for _, f in W.stages(i):
+            f()
+    torch.cuda.synchronize()
+
+    # timed region: per-stage CUDA events on the launching (current) stream
+    names = [nm for nm, _ in W.stages(0)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)] for _ in range(args.steps)]
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.05)
+    barrier()
+    torch.cuda.synchronize()
+    t_host0 = time.perf_counter()
+    for i in range(args.steps):
+        st = W.stages(i)
+        ev[i][0].record()
+        for j, (_, f) in enumerate(st):
+            f()
+            ev[i][j + 1].record()
+    torch.cuda.synchronize()
+    barrier()
+    t_host1 = time.perf_counter()
+    clk.stop()
+
+    total_ms = sum(ev[i][0].elapsed_time(ev[i][-1]) for i in range(args.steps))
+    stage_ms = {nm: sum(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps)) / args.steps
+                for j, nm in enumerate(names)}
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = W.work_per_step() * world / (ms_per_step / 1e3)
+
+    # correctness sentinel of the timed run: no range violation, no flagged position
+    dg = ne.diag_read(W.diag)
+    # recovered outputs of the last step equal the checked ones
+    rec_ok = all(bool(torch.equal(a, b)) for a, b in zip(W.drec, W.dout))
+
+    # end-to-end through host buffers (pinned H2D inputs, D2H outputs, same stream)
+    h2d, d2h = W.e2e_setup()
+    torch.cuda.synchronize()
+    W.e2e_step(0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(3, min(args.steps, 20))
+    barrier()
+    e0.record()
+    for i in range(e2e_steps):
+        W.e2e_step(i)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    plain = W.plain_times()
+    if rank != 0:
+        return None
+
+    peaks, peak_src = load_peaks()
+    info = W.stage_info()
+    dom = max(stage_ms, key=stage_ms.get)
+    bound, amount, unit = info[dom]
+    achieved = amount / (stage_ms[dom] / 1e3)
+    if bound == "hbm":
+        peak, runit = peaks["hbm_gbs"], "GB/s"
+        peak_note = f"HBM copy bandwidth, {peak_src}"
+    elif bound == "tensor":
+        peak, runit = peaks["bf16_tflops"] * 2.0, "TOP/s"
+        peak_note = f"int8 dense = 2 x bf16 burst ({peaks['bf16_tflops']} TFLOP/s, {peak_src}) x nominal 4.5/2.25"
+    else:
+        peak, runit = 64 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, "TMAC/s"
+        peak_note = "IMAD pipe: 64 lanes/clk/SM x 148 SMs x max SM clock (DESIGN.md)"
+    tr = load_traffic().get(f"{W.name}:{dom}")
+    traffic = tr["GB"] if tr else None
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": W.metric_unit,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int64",
+        "data": "synthetic (counter-based splitmix64 generator, gen/ne_gen.h; no dataset)",
+        "config": W.config(),
+        "roofline": {"bound": bound, "kernel": dom, "achieved": round(achieved, 2), "peak": round(peak, 1),
+                     "unit": runit, "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_unit": "GB per launch, ncu dram__bytes_read.sum + dram__bytes_write.sum "
+                                     "(profiles/traffic.json)" if tr else None,
+                     "algorithmic_per_launch": f"{amount:.4g} {unit}", "peak_source": peak_note},
+        "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "e2e": {"value": round(W.work_per_step() * world / (e2e_ms / 1e3), 3), "unit": W.metric_unit,
+                "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": W.launches_per_step * args.steps,
+        "clocks": clk.summary(),
+        "correctness": {"range_violations": dg["range_violations"], "flagged_positions": dg["fault_positions"],
+                        "recover_equals_check": rec_ok},
+    }
+    if plain:
+        line["plain_ms"] = {k: round(v, 4) for k, v in plain.items()}
+        op_stage = "gemm" if "gemm" in stage_ms else dom
+        line["overhead_pct"] = {f"step_vs_{k}": round((ms_per_step / v - 1) * 100, 2) for k, v in plain.items()}
+        line["overhead_pct"]["op_stage"] = op_stage
+    line["timed_host_s"] = round(t_host1 - t_host0, 4)
+    if world == 1:
+        line["cpu_baseline"] = cpu_baseline(args.workload, W)
+    return line
+
+
+def cpu_baseline(workload, W):
+    n, _ = ORACLE_SAMPLE[workload]
+    dt, work, what = W.oracle_sample(n)
+    return {"value": round(work / dt, 6), "unit": W.metric_unit, "cores": 1, "kind": "oracle",
+            "sample": what, "seconds": round(dt, 3), "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+class _HostOnly:
+    """Workload shell for the oracle arm: same config, no device buffers."""
+
+
+def run_reference(args):
+    """The CPU oracle as it stands (plain C, 1 core), each step a bounded sample."""
+    cls = WORKLOADS[args.workload]
+    W = cls.__new__(cls)
+    # the attributes oracle_sample / work_per_step / config need, without CUDA
+    if args.workload == "c3":
+        W.M, W.rows, W.cols, W.K, W.seed, W.algo, W.L = 3, 4096, 4096, 4096, 2, "tc", 4
+
+        class _Cfg:
+            l, k = 22, 20
+        W.cfg = _Cfg
+    elif args.workload == "c4":
+        W.M, W.n, W.B, W.seed = 4, 1 << 28, 1024, 3
+
+        class _Cfg:
+            l, k = 16, 16
+        W.cfg = _Cfg
+    elif args.workload == "c2":
+        W.M, W.n, W.T, W.seed = 3, 65536, 64, 1
+    else:
+        W.M, W.n, W.seed = 3, 4096, 0
+    per_step = ORACLE_SAMPLE[args.workload][1]
+    for _ in range(args.warmup):
+        W.oracle_sample(per_step)
+    tot, work, what = 0.0, 0.0, ""
+    for _ in range(args.steps):
+        dt, wk, what = W.oracle_sample(per_step)
+        tot += dt
+        work += wk
+    value = work / tot
+    cfg = W.config()
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": W.metric_unit,
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (same seeded generator)", "config": cfg,
+            "cpu_baseline": {"value": round(value, 6), "unit": W.metric_unit, "cores": 1, "kind": "oracle",
+                             "sample": what + " per step", "cpu": _cpu_model()},
+            "e2e": {"value": round(value, 6), "unit": W.metric_unit, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--algo", default="tc", choices=["tc", "imad"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, rank, world, local_rank)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
