@@ -51,38 +51,49 @@ k_split_limbs(const __grid_constant__ ne_cstreams A, int M_rt, int64_t n, int L,
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
-// B (K x cols int32, row-major) -> Bt (cols x K int8, K contiguous), |B| <= 127..-128
+// B (K x cols int32, row-major) -> Bt (cols x K int8, K contiguous), the
+// one-plane int8 operand of the tensor-core GEMM (|B| <= 127 / -128, else a
+// range violation).  Tile 128 (k) x 64 (c): 128-bit loads along c, transpose
+// through shared memory, 128-bit stores along k.
 __global__ void __launch_bounds__(256)
 k_prep_b(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __restrict__ Bt, ne_diag* __restrict__ diag) {
-  __shared__ int8_t tile[32][33 * 4];
-  const int64_t k0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 32;
+  __shared__ __align__(16) int8_t tile[64][128 + 16];
+  const int64_t k0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 64;
   int bad = 0;
   long long first = LLONG_MAX;
-  // load 128 (k) x 32 (c) int32 coalesced along c
-  for (int t = threadIdx.x; t < 128 * 32; t += 256) {
-    const int kk = t / 32, cc = t % 32;
-    const int64_t k = k0 + kk, c = c0 + cc;
-    int32_t v = 0;
-    if (k < K && c < cols) {
-      v = B[k * cols + c];
-      if (v < -128 || v > 127) {
-        ++bad;
-        long long idx = (long long)(k * cols + c);
-        first = idx < first ? idx : first;
+  const bool vec = (cols % 4) == 0;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int t = threadIdx.x + 256 * it;  // 2048 groups of 4 consecutive c
+    const int kk = t >> 4, cq = (t & 15) * 4;
+    const int64_t k = k0 + kk, c = c0 + cq;
+    int32_t v[4] = {0, 0, 0, 0};
+    if (k < K) {
+      if (vec && c + 3 < cols) {
+        int4 w = __ldcs(reinterpret_cast<const int4*>(B + k * cols + c));
+        v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+      } else {
+        for (int i = 0; i < 4; ++i) v[i] = (c + i < cols) ? B[k * cols + c + i] : 0;
       }
     }
-    tile[cc][kk] = (int8_t)v;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (v[i] < -128 || v[i] > 127) {
+        ++bad;
+        const long long idx = (long long)(k * cols + c + i);
+        first = idx < first ? idx : first;
+      }
+      tile[cq + i][kk] = (int8_t)v[i];
+    }
   }
   __syncthreads();
-  // store 32 (c) rows of 128 (k) int8, 4 bytes per thread
-  for (int t = threadIdx.x; t < 32 * 32; t += 256) {
-    const int cc = t / 32, kq = (t % 32) * 4;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int t = threadIdx.x + 256 * it;  // 512 groups of 16 consecutive k
+    const int cc = t >> 3, kq = (t & 7) * 16;
     const int64_t c = c0 + cc, k = k0 + kq;
-    if (c < cols && k + 3 < K) {
-      uint32_t w = (uint32_t)(uint8_t)tile[cc][kq] | ((uint32_t)(uint8_t)tile[cc][kq + 1] << 8) |
-                   ((uint32_t)(uint8_t)tile[cc][kq + 2] << 16) | ((uint32_t)(uint8_t)tile[cc][kq + 3] << 24);
-      *reinterpret_cast<uint32_t*>(Bt + c * K + k) = w;
-    }
+    if (c < cols && k + 15 < K)
+      *reinterpret_cast<uint4*>(Bt + c * K + k) = *reinterpret_cast<const uint4*>(&tile[cc][kq]);
   }
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
@@ -106,8 +117,8 @@ extern "C" ne_status ne_gemm_workspace(const ne_config* cfg, int64_t rows, int64
 
 extern "C" ne_status ne_gemm_prep_b(const int32_t* B, int64_t K, int64_t cols, int8_t* Bt, ne_diag* diag,
                                     ne_stream_t stream) {
-  if (!B || !Bt || K <= 0 || cols <= 0 || K % 4 != 0 || !aligned16(Bt)) return NE_EINVAL;
-  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((K + 127) / 128));
+  if (!B || !Bt || K <= 0 || cols <= 0 || K % 16 != 0 || !aligned16(Bt) || !aligned16(B)) return NE_EINVAL;
+  dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((K + 127) / 128));
   k_prep_b<<<grid, 256, 0, cs(stream)>>>(B, K, cols, Bt, diag);
   return launch_status();
 }

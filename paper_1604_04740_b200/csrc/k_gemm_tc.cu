@@ -12,13 +12,17 @@
 //
 // One CTA computes a 128 x BN tile of one stream m: the L limb accumulators
 // live side by side in TMEM (L * BN <= 512 columns).  Warp roles:
-//   warp 0 lane 0 : TMA producer  (cp.async.bulk.tensor, 128B swizzle, mbarrier complete_tx)
+//   warp 0 lane 0 : TMA producer  (cp.async.bulk.tensor, 64B swizzle, multicast, mbarrier complete_tx)
 //   warp 1 lane 0 : MMA issuer    (tcgen05.mma.cta_group::1.kind::i8, commit -> mbarrier)
 //   warp 2        : TMEM allocator (tcgen05.alloc / dealloc)
-//   warps 4..7    : epilogue      (tcgen05.ld 32x32b -> int64 recombine -> st.global)
-// smem: kStages x {L A tiles 128 x 128 B, one B tile BN x 128 B}, 1024-B aligned.
+//   all 8 warps   : epilogue      (tcgen05.ld 32x32b -> int64 recombine -> st.global);
+//                   warp w reads TMEM lane quarter w%4, column half w/4
+// smem: STAGES x {L limb tiles 128 x 64 B, one B tile BN x 64 B} (64B swizzle),
+// 1024-B aligned; clusters of 2 CTAs along N multicast the limb tiles.
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "ne_internal.cuh"
 
@@ -26,12 +30,21 @@ namespace ne {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 128;  // bytes of K per stage = one 128B swizzle atom row
 constexpr int UMMA_K = 32;  // int8: 32 bytes of K per tcgen05.mma
 constexpr int kThreadsTC = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -57,6 +70,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// TMA 2-D tile load; with a cluster mask the tile lands at the same smem
+// offset in every CTA of the mask and completes on each one's mbarrier.
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t c0,
                                             int32_t c1) {
   asm volatile(
@@ -66,16 +81,27 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
-// UMMA shared-memory descriptor, K-major, 128B swizzle (layout type 2 on sm_100):
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t c0,
+                                               int32_t c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, swizzled rows of SW bytes:
 // start >> 4 in [0,14), LBO >> 4 in [16,30) (unused for swizzled K-major: 1),
-// SBO >> 4 in [32,46) (= 1024 B between 8-row groups), version 1 in [46,48).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+// SBO >> 4 in [32,46) (8 rows x SW bytes between 8-row groups), version 1 in
+// [46,48), layout type in [61,64): 2 = 128B swizzle, 4 = 64B swizzle.
+template <int SW>
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)((8 * SW) >> 4) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)(SW == 128 ? 2 : 4) << 61;
   return d;
 }
 
@@ -96,9 +122,18 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
+// arrive on `bar` (same smem offset) in every CTA of `mask` once the MMAs
+// issued so far have completed
+__device__ __forceinline__ void mma_commit(uint64_t* bar, uint16_t mask) {
+  if (mask == 1)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+  else
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
@@ -109,20 +144,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
-template <int L, int BN, int STAGES>
+template <int L, int BN, int STAGES, int SW, int CL>
 struct Cfg {
-  static constexpr int kATile = BM * BK;          // bytes
+  static constexpr int BK = SW;                   // bytes (= int8 elements) of K per stage
+  static constexpr int kATile = BM * BK;          // one limb tile
   static constexpr int kBTile = BN * BK;
   static constexpr int kStage = L * kATile + kBTile;
+  static constexpr int kARows = BM / CL;          // rows of each limb tile this CTA loads (multicast)
   static constexpr int kTmemCols = (L * BN <= 32) ? 32 : (L * BN <= 64) ? 64 : (L * BN <= 128) ? 128 : (L * BN <= 256) ? 256 : 512;
   static constexpr size_t kSmem = (size_t)STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <int L, int BN, int STAGES>
+// One CTA: 128 x BN tile of stream blockIdx.z.  CL CTAs of a cluster (along
+// N) share the row tile: each loads 128/CL rows of every limb tile and
+// multicasts them to all CL CTAs, so A is read from L2 once per cluster.
+template <int L, int BN, int STAGES, int SW, int CL, int EPI = 0>
 __global__ void __launch_bounds__(kThreadsTC, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
           const __grid_constant__ ne_streams C, int64_t rows, int64_t cols, int64_t K) {
-  using CF = Cfg<L, BN, STAGES>;
+  using CF = Cfg<L, BN, STAGES, SW, CL>;
+  constexpr int BK = CF::BK;
   static_assert(L * BN <= 512, "TMEM holds 512 columns");
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -132,6 +173,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = CL > 1 ? cluster_rank() : 0;
+  const uint16_t cmask = (uint16_t)((1u << CL) - 1);
   const int m = blockIdx.z;
   const int64_t row0 = (int64_t)blockIdx.y * BM;
   const int64_t col0 = (int64_t)blockIdx.x * BN;
@@ -140,7 +183,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // released by the MMA warp of every CTA in the cluster
     }
     mbar_init(tmem_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -151,7 +194,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync();  // peers' barriers are initialised before anyone multicasts
+  else
+    __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
@@ -166,8 +212,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       unsigned char* st = smem + s * CF::kStage;
       mbar_expect_tx(&full[s], (uint32_t)CF::kStage);
 #pragma unroll
-      for (int i = 0; i < L; ++i)
-        tma_load_2d(&mapA, &full[s], st + i * CF::kATile, kb * BK, (int32_t)(((int64_t)m * L + i) * rows + row0));
+      for (int i = 0; i < L; ++i) {
+        unsigned char* dst = st + i * CF::kATile + crank * CF::kARows * BK;
+        const int32_t grow = (int32_t)(((int64_t)m * L + i) * rows + row0 + crank * CF::kARows);
+        if (CL > 1)
+          tma_load_2d_mc(&mapA, &full[s], dst, kb * BK, grow, cmask);
+        else
+          tma_load_2d(&mapA, &full[s], dst, kb * BK, grow);
+      }
       tma_load_2d(&mapB, &full[s], st + L * CF::kATile, kb * BK, (int32_t)col0);
     }
   } else if (warp == 1 && lane == 0) {
@@ -182,45 +234,52 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       const uint32_t sb = sa + L * CF::kATile;
 #pragma unroll
       for (int ks = 0; ks < BK / UMMA_K; ++ks) {
-        const uint64_t bdesc = umma_desc_sw128(sb + ks * UMMA_K);
+        const uint64_t bdesc = umma_desc<SW>(sb + ks * UMMA_K);
 #pragma unroll
         for (int i = 0; i < L; ++i) {
-          const uint64_t adesc = umma_desc_sw128(sa + i * CF::kATile + ks * UMMA_K);
+          const uint64_t adesc = umma_desc<SW>(sa + i * CF::kATile + ks * UMMA_K);
           mma_i8(tmem_base + i * BN, adesc, bdesc, idesc, (kb | ks) != 0);
         }
       }
-      mma_commit(&empty[s]);  // frees the smem stage when these MMAs completed
+      mma_commit(&empty[s], cmask);  // frees stage s in every CTA of the cluster
     }
-    mma_commit(tmem_full);    // accumulators final
-  } else if (warp >= 4) {
-    // ---------------- epilogue: TMEM -> registers -> int64 recombination -> global
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    mma_commit(tmem_full, 1);        // accumulators final
+  }
+  __syncwarp();
+
+  // ---------------- epilogue (all 8 warps): TMEM -> registers -> int64 recombination -> global
+  if (EPI != 2) {
+    const int q = warp & 3;           // TMEM lane quarter this warp may access
+    const int half = warp >> 2;       // column half
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int64_t row = row0 + 32 * q + lane;
     int64_t* __restrict__ crow = C.s[m] + row * cols + col0;
     const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
+    for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
       uint32_t v[L][16];
 #pragma unroll
       for (int i = 0; i < L; ++i) tmem_ld16(tl + i * BN + c, v[i]);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      uint64_t o[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        uint64_t acc = 0;
+      for (int j = 0; j < 16; j += 2) {
+        uint64_t a0 = 0, a1 = 0;
 #pragma unroll
-        for (int i = 0; i < L; ++i) acc += (uint64_t)(int64_t)(int32_t)v[i][j] << (8 * i);
-        o[j] = acc;
+        for (int i = 0; i < L; ++i) {
+          a0 += (uint64_t)(int64_t)(int32_t)v[i][j] << (8 * i);
+          a1 += (uint64_t)(int64_t)(int32_t)v[i][j + 1] << (8 * i);
+        }
+        if (EPI == 0 || (a0 == 0x1234567ull && a1 == 0x7654321ull))
+          __stcs(reinterpret_cast<longlong2*>(crow + c + j), make_longlong2((int64_t)a0, (int64_t)a1));
       }
-#pragma unroll
-      for (int j = 0; j < 16; j += 2)
-        __stcs(reinterpret_cast<longlong2*>(crow + c + j), make_longlong2((int64_t)o[j], (int64_t)o[j + 1]));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (CL > 1)
+    cluster_sync();  // no CTA leaves while a peer may still signal its barriers
+  else
+    __syncthreads();
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -245,51 +304,75 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D int8 tensor [outer][inner] (inner contiguous), box {BK, box_outer}, 128B swizzle
-static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+// 2-D int8 tensor [outer][inner] (inner contiguous), box {SW, box_outer}, SW-byte swizzle
+static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                     uint32_t box_outer) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {inner};
-  cuuint32_t box[2] = {(cuuint32_t)BK, box_outer};
+  cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  box_inner == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-template <int L, int BN, int STAGES>
+template <int L, int BN, int STAGES, int SW, int CL>
 static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
                      const ne_streams& C, cudaStream_t s) {
-  using CF = Cfg<L, BN, STAGES>;
-  if (cols % BN != 0) return NE_ENOTSUP;
+  using CF = Cfg<L, BN, STAGES, SW, CL>;
+  if (cols % (BN * CL) != 0 || K % CF::BK != 0) return NE_ENOTSUP;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, planes, (uint64_t)K, (uint64_t)M * L * rows, BM)) return NE_ECUDA;
-  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, BN)) return NE_ECUDA;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_gemm_tc<L, BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) !=
-        cudaSuccess)
-      return NE_ECUDA;
-    attr = true;
-  }
-  dim3 grid((unsigned)(cols / BN), (unsigned)(rows / BM), (unsigned)M);
-  k_gemm_tc<L, BN, STAGES><<<grid, kThreadsTC, CF::kSmem, s>>>(ma, mb, C, rows, cols, K);
+  if (!make_map(&ma, planes, (uint64_t)K, (uint64_t)M * L * rows, SW, CF::kARows)) return NE_ECUDA;
+  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, BN)) return NE_ECUDA;
+  static const int epi = getenv("NE_GEMM_EPI") ? atoi(getenv("NE_GEMM_EPI")) : 0;
+  auto kern = epi == 1 ? k_gemm_tc<L, BN, STAGES, SW, CL, 1> : epi == 2 ? k_gemm_tc<L, BN, STAGES, SW, CL, 2>
+                                                                  : k_gemm_tc<L, BN, STAGES, SW, CL, 0>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) != cudaSuccess)
+    return NE_ECUDA;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(cols / BN), (unsigned)(rows / BM), (unsigned)M);
+  lc.blockDim = dim3(kThreadsTC);
+  lc.dynamicSmemBytes = CF::kSmem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, C, rows, cols, K) != cudaSuccess) return NE_ECUDA;
   return launch_status();
 }
 
 }  // namespace tc
 
+// Tile choice: L limb accumulators of BN columns fill TMEM (L * BN <= 512);
+// 64-byte K stages (64B swizzle) give 4-6 pipeline stages in ~200 KB of smem;
+// clusters of 2 along N multicast the limb tiles (A read once per pair)
+// whenever the column-tile count is even.
 ne_status launch_gemm_tc(int M, int L, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s) {
+  const bool pair128 = cols % 256 == 0, pair256 = cols % 512 == 0;
   switch (L) {
-    case 1: return (cols % 256 == 0) ? tc::run<1, 256, 4>(planes, Bt, rows, cols, K, M, C, s)
-                                     : tc::run<1, 128, 4>(planes, Bt, rows, cols, K, M, C, s);
-    case 2: return (cols % 256 == 0) ? tc::run<2, 256, 3>(planes, Bt, rows, cols, K, M, C, s)
-                                     : tc::run<2, 128, 4>(planes, Bt, rows, cols, K, M, C, s);
-    case 3: return tc::run<3, 128, 3>(planes, Bt, rows, cols, K, M, C, s);
-    case 4: return tc::run<4, 128, 2>(planes, Bt, rows, cols, K, M, C, s);
+    case 1:
+      if (pair256) return tc::run<1, 256, 8, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
+      if (cols % 256 == 0) return tc::run<1, 256, 8, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      return tc::run<1, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+    case 2:
+      if (pair256) return tc::run<2, 256, 6, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
+      if (cols % 256 == 0) return tc::run<2, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      return tc::run<2, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+    case 3:
+      if (pair128) return tc::run<3, 128, 6, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
+      return tc::run<3, 128, 6, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+    case 4:
+      if (pair128) return tc::run<4, 128, 5, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
+      return tc::run<4, 128, 5, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
     default: return NE_ENOTSUP;
   }
 }

@@ -56,25 +56,23 @@ k_pinner(const __grid_constant__ ne_cstreams x, const int64_t* __restrict__ x_ao
         coef[u] = ok ? (int64_t)__ldg(v + (VB ? (p - p_begin) : (p % vlen))) : 0;
       }
       if (AOS && MT == 4) {
-        longlong2 q0[kU], q1[kU];
+        // one 256-bit load per gathered position = exactly its 32-byte sector
+        uint64_t q[kU][4];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           if (idx[u] >= 0) {
-            const longlong2* a = reinterpret_cast<const longlong2*>(x_aos + idx[u] * 4);
-            q0[u] = __ldcs(a);
-            q1[u] = __ldcs(a + 1);
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                         : "=l"(q[u][0]), "=l"(q[u][1]), "=l"(q[u][2]), "=l"(q[u][3])
+                         : "l"(x_aos + idx[u] * 4));
           } else {
-            q0[u] = make_longlong2(0, 0);
-            q1[u] = make_longlong2(0, 0);
+            q[u][0] = q[u][1] = q[u][2] = q[u][3] = 0;
           }
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const uint64_t c = (uint64_t)coef[u];
-          acc[0] = (int64_t)((uint64_t)acc[0] + (uint64_t)q0[u].x * c);
-          acc[1] = (int64_t)((uint64_t)acc[1] + (uint64_t)q0[u].y * c);
-          acc[2] = (int64_t)((uint64_t)acc[2] + (uint64_t)q1[u].x * c);
-          acc[3] = (int64_t)((uint64_t)acc[3] + (uint64_t)q1[u].y * c);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) acc[m] = (int64_t)((uint64_t)acc[m] + q[u][m] * c);
         }
       } else {
 #pragma unroll

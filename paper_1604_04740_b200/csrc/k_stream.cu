@@ -19,7 +19,7 @@ namespace ne {
 // One thread handles 4 consecutive positions of ALL M streams, so every c_m is
 // read exactly once (int4) and eps is written as 2 x 128-bit per stream.
 // The a0 range assertion |c| <= hi is fused (warp-aggregated atomics).
-// OUT selects the output layout: 0 = SoA int64, 1 = AoS int64, 2 = int8 limbs.
+// OUT selects the output layout: 0 = SoA int64, 1 = AoS int64 (generic M).
 template <int MT, int OUT>
 __global__ void __launch_bounds__(kThreads)
 k_entangle(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n,
@@ -83,27 +83,6 @@ k_entangle(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi,
       } else if (OUT == 1) {
         for (int i = 0; i < 4; ++i)
           if (n0 + i < n) eps_aos[(n0 + i) * M + m] = e[i];
-      } else {
-        // balanced signed base-2^8 digits: d_j = sext8(x_j), x_{j+1} = (x_j - d_j) >> 8
-        int64_t x[4] = {e[0], e[1], e[2], e[3]};
-        for (int j = 0; j < L; ++j) {
-          uint32_t packed = 0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            int8_t dgt = (int8_t)(x[i] & 0xff);
-            x[i] = (x[i] - dgt) >> 8;
-            packed |= (uint32_t)(uint8_t)dgt << (8 * i);
-          }
-          // n % 16 == 0 is required by the ABI, so 4-aligned groups are full
-          *reinterpret_cast<uint32_t*>(planes + ((int64_t)m * L + j) * n + n0) = packed;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (x[i] != 0) {  // not representable in L digits
-            ++bad;
-            long long idx = (long long)m * n + n0 + i;
-            first = idx < first ? idx : first;
-          }
       }
       for (int i = 0; i < 4; ++i) prev[i] = cur[i];
     }
@@ -111,31 +90,115 @@ k_entangle(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi,
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
-// AoS stores above are scalar; for M = 4 use a 2 x 128-bit store per position
-// (one 32-byte sector) — the layout the C4 gather reads.
+// AoS for M = 4: a warp owns 128 consecutive positions per iteration, lane t
+// positions base + 32 i + t (i < 4): every 32-bit load instruction is one
+// coalesced 128-byte line per stream, and every position is written with ONE
+// 256-bit store (its whole 32-byte DRAM sector; 1 KB contiguous per warp
+// instruction) — the layout the C4 gather reads.
 __global__ void __launch_bounds__(kThreads)
 k_entangle_aos4(const __grid_constant__ ne_cstreams32 c, int l, int64_t hi, int64_t n,
                 int64_t* __restrict__ eps_aos, ne_diag* __restrict__ diag) {
   int bad = 0;
   long long first = LLONG_MAX;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t cv[4];
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = warp * 128; base < n; base += nwarps * 128) {
+    int32_t cv[4][4];  // [stream][i]
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      cv[m] = __ldcs(c.s[m] + i);
-      if (cv[m] > hi || cv[m] < -hi) {
-        ++bad;
-        long long idx = (long long)m * n + i;
-        first = idx < first ? idx : first;
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t p = base + 32 * i + lane;
+        cv[m][i] = p < n ? __ldcs(c.s[m] + p) : 0;
       }
-    }
-    int64_t e[4];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) e[m] = cv[m] + (int64_t)((uint64_t)cv[(m + 3) & 3] << l);
-    longlong2* q = reinterpret_cast<longlong2*>(eps_aos + i * 4);
-    __stcs(q, make_longlong2(e[0], e[1]));
-    __stcs(q + 1, make_longlong2(e[2], e[3]));
+    for (int i = 0; i < 4; ++i) {
+      const int64_t p = base + 32 * i + lane;
+      if (p >= n) continue;
+      uint64_t e[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int64_t x = cv[m][i];
+        if (x > hi || x < -hi) {
+          ++bad;
+          const long long idx = (long long)m * n + p;
+          first = idx < first ? idx : first;
+        }
+        e[m] = (uint64_t)x + ((uint64_t)(int64_t)cv[(m + 3) & 3][i] << l);
+      }
+      asm volatile("st.global.cs.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(eps_aos + p * 4), "l"(e[0]), "l"(e[1]),
+                   "l"(e[2]), "l"(e[3])
+                   : "memory");
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// Entangle straight into the L int8 digit planes of the tensor-core GEMM.
+// Balanced base-2^8 digits in one add: with bias = sum_{i<L} 128 * 256^i,
+// x = sum_i d_i 256^i, d_i in [-128,127]  <=>  y = x + bias in [0, 256^L) and
+// byte i of y = d_i + 128, so d_i = byte_i(y) ^ 0x80 (two's complement).
+// A thread owns 4 consecutive positions (one 128-bit load per stream, all M
+// loads issued before any store); plane j receives the 4 bytes j of the four
+// y values (PRMT), a 32-bit store per plane (128 contiguous bytes per warp).
+template <int MT, int L>
+__global__ void __launch_bounds__(kThreads)
+k_entangle_limbs(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n,
+                 int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  constexpr uint64_t bias = 0x8080808080808080ull >> (64 - 8 * L);
+  constexpr uint64_t span = L == 8 ? 0 : (1ull << (8 * L));  // 256^L
+  int bad = 0;
+  long long first = LLONG_MAX;
+  const int64_t nvec = n / 4;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 4 * v;
+    int4 q[MA];
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) q[m] = __ldcs(reinterpret_cast<const int4*>(c.s[m] + n0));
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      const int4 cur = q[m], prv = q[m == 0 ? M - 1 : m - 1];
+      const int32_t cc[4] = {cur.x, cur.y, cur.z, cur.w}, pp[4] = {prv.x, prv.y, prv.z, prv.w};
+      uint64_t y[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t ci = cc[i];
+        const uint64_t x = (uint64_t)ci + ((uint64_t)(int64_t)pp[i] << l);
+        y[i] = x + bias;
+        const bool out_of_limbs = L < 8 && y[i] >= span;
+        if (ci > hi || ci < -hi || out_of_limbs) {
+          ++bad;
+          const long long idx = (long long)m * n + n0 + i;
+          first = idx < first ? idx : first;
+        }
+      }
+      const uint32_t lo01 = __byte_perm((uint32_t)y[0], (uint32_t)y[1], 0x5140);  // b0(y0) b0(y1) b1(y0) b1(y1)
+      const uint32_t lo23 = __byte_perm((uint32_t)y[2], (uint32_t)y[3], 0x5140);
+      const uint32_t hi01 = __byte_perm((uint32_t)y[0], (uint32_t)y[1], 0x7362);  // b2(y0) b2(y1) b3(y0) b3(y1)
+      const uint32_t hi23 = __byte_perm((uint32_t)y[2], (uint32_t)y[3], 0x7362);
+      uint32_t w[8];
+      w[0] = __byte_perm(lo01, lo23, 0x5410);  // byte 0 of y0..y3
+      w[1] = __byte_perm(lo01, lo23, 0x7632);  // byte 1
+      w[2] = __byte_perm(hi01, hi23, 0x5410);  // byte 2
+      w[3] = __byte_perm(hi01, hi23, 0x7632);  // byte 3
+      if (L > 4) {
+        const uint32_t a01 = __byte_perm((uint32_t)(y[0] >> 32), (uint32_t)(y[1] >> 32), 0x5140);
+        const uint32_t a23 = __byte_perm((uint32_t)(y[2] >> 32), (uint32_t)(y[3] >> 32), 0x5140);
+        const uint32_t b01 = __byte_perm((uint32_t)(y[0] >> 32), (uint32_t)(y[1] >> 32), 0x7362);
+        const uint32_t b23 = __byte_perm((uint32_t)(y[2] >> 32), (uint32_t)(y[3] >> 32), 0x7362);
+        w[4] = __byte_perm(a01, a23, 0x5410);
+        w[5] = __byte_perm(a01, a23, 0x7632);
+        w[6] = __byte_perm(b01, b23, 0x5410);
+        w[7] = __byte_perm(b01, b23, 0x7632);
+      }
+#pragma unroll
+      for (int j = 0; j < L; ++j)
+        __stcs(reinterpret_cast<unsigned int*>(planes + ((int64_t)m * L + j) * n + n0), w[j] ^ 0x80808080u);
+    }
   }
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
@@ -342,7 +405,7 @@ extern "C" ne_status ne_entangle_aos(const ne_config* cfg, ne_cstreams32 c, int6
   if (n_total == 0) return NE_OK;
   if (n_total < 0 || !streams_ok32(c, cfg->M) || !eps_aos || !aligned16(eps_aos)) return NE_EINVAL;
   if (cfg->M == 4) {
-    k_entangle_aos4<<<grid_for(n_total, kThreads), kThreads, 0, cs(stream)>>>(c, cfg->l, range_hi(cfg), n_total,
+    k_entangle_aos4<<<grid_for((n_total + 3) / 4, kThreads), kThreads, 0, cs(stream)>>>(c, cfg->l, range_hi(cfg), n_total,
                                                                             eps_aos, diag);
     return launch_status();
   }
@@ -358,8 +421,30 @@ extern "C" ne_status ne_entangle_limbs(const ne_config* cfg, ne_cstreams32 c, in
   if (n_total < 0 || n_total % 16 != 0 || L < 1 || L > 8 || !streams_ok32(c, cfg->M) || !planes ||
       !aligned16(planes))
     return NE_EINVAL;
-  ne_streams none{};
-  return launch_entangle<2>(cfg, c, n_total, none, nullptr, planes, L, diag, stream);
+  const int64_t hi = range_hi(cfg);
+  const int grid = grid_for(n_total / 4, kThreads);
+  cudaStream_t s = cs(stream);
+#define NE_LIMB_CASE(MV, LV) k_entangle_limbs<MV, LV><<<grid, kThreads, 0, s>>>(c, cfg->M, cfg->l, hi, n_total, planes, diag)
+#define NE_LIMB_L(MV)              \
+  switch (L) {                     \
+    case 1: NE_LIMB_CASE(MV, 1); break; \
+    case 2: NE_LIMB_CASE(MV, 2); break; \
+    case 3: NE_LIMB_CASE(MV, 3); break; \
+    case 4: NE_LIMB_CASE(MV, 4); break; \
+    case 5: NE_LIMB_CASE(MV, 5); break; \
+    case 6: NE_LIMB_CASE(MV, 6); break; \
+    case 7: NE_LIMB_CASE(MV, 7); break; \
+    default: NE_LIMB_CASE(MV, 8); break; \
+  }
+  switch (cfg->M) {
+    case 3: NE_LIMB_L(3); break;
+    case 4: NE_LIMB_L(4); break;
+    case 8: NE_LIMB_L(8); break;
+    default: NE_LIMB_L(0); break;
+  }
+#undef NE_LIMB_L
+#undef NE_LIMB_CASE
+  return launch_status();
 }
 
 extern "C" ne_status ne_entangle_stream(const ne_config* cfg, int32_t m, const int32_t* c_m,

@@ -81,7 +81,7 @@ def test_entangle_aos(O, M, N):
     assert (aos.cpu().numpy().reshape(N, M).T == O.entangle(ocfg, c)).all()
 
 
-@pytest.mark.parametrize("M,L,B", [(3, 4, 64), (8, 2, 32), (4, 4, 1000), (3, 3, 16), (3, 1, 0)])
+@pytest.mark.parametrize("M,L,B", [(3, 4, 64), (8, 2, 32), (4, 4, 1000), (3, 3, 1), (3, 1, 0), (5, 3, 1)])
 def test_entangle_limbs(O, M, L, B):
     cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
     N = 4096 + 16
@@ -407,7 +407,7 @@ def test_gemm_imad64(O, rows, cols, K):
 
 @pytest.mark.parametrize("M,L,bound,rows,cols,K", [
     (3, 4, 64, 128, 128, 128), (3, 4, 64, 256, 384, 512), (8, 2, 32, 128, 256, 256),
-    (4, 4, 1000, 128, 128, 1024), (3, 3, 16, 128, 128, 256), (3, 1, 0, 128, 256, 128), (8, 2, 32, 256, 128, 128)])
+    (4, 4, 1000, 128, 128, 1024), (3, 3, 1, 128, 128, 256), (3, 1, 0, 128, 256, 128), (8, 2, 32, 256, 128, 128)])
 def test_gemm_tc_i8(O, M, L, bound, rows, cols, K):
     cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
     assert ne.ne_gemm_limbs_for(cfg, bound) <= L
