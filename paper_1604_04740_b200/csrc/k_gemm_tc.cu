@@ -10,19 +10,17 @@
 // while K * 128 * 128 < 2^31 (K <= 131072), and the recombination is done in
 // int64 in the epilogue (wrap mod 2^64, exact for certified results).
 //
-// One CTA computes a 128 x BN tile of one stream m: the L limb accumulators
-// live side by side in TMEM (L * BN <= 512 columns).  Warp roles:
+// A CTA computes 128 x BN tiles of one stream at a time: the L limb
+// accumulators live side by side in TMEM (L * BN <= 512 columns).  Roles:
 //   warp 0 lane 0 : TMA producer  (cp.async.bulk.tensor, 64B swizzle, multicast, mbarrier complete_tx)
 //   warp 1 lane 0 : MMA issuer    (tcgen05.mma.cta_group::1.kind::i8, commit -> mbarrier)
 //   warp 2        : TMEM allocator (tcgen05.alloc / dealloc)
-//   all 8 warps   : epilogue      (tcgen05.ld 32x32b -> int64 recombine -> st.global);
-//                   warp w reads TMEM lane quarter w%4, column half w/4
+//   warps 4..11   : epilogue      (tcgen05.ld 32x32b -> int64 recombine -> swizzled smem -> TMA store);
+//                   warp w reads TMEM lane quarter w%4, column half (w-4)/4
 // smem: STAGES x {L limb tiles 128 x 64 B, one B tile BN x 64 B} (64B swizzle),
 // 1024-B aligned; clusters of 2 CTAs along N multicast the limb tiles.
 #include <cuda.h>
 #include <cuda_runtime.h>
-
-#include <cstdlib>
 
 #include "ne_internal.cuh"
 
@@ -31,7 +29,6 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int UMMA_K = 32;  // int8: 32 bytes of K per tcgen05.mma
-constexpr int kThreadsTC = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -152,33 +149,50 @@ struct Cfg {
   static constexpr int kStage = L * kATile + kBTile;
   static constexpr int kARows = BM / CL;          // rows of each limb tile this CTA loads (multicast)
   static constexpr int kTmemCols = (L * BN <= 32) ? 32 : (L * BN <= 64) ? 64 : (L * BN <= 128) ? 128 : (L * BN <= 256) ? 256 : 512;
-  static constexpr size_t kSmem = (size_t)STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kStageOut = 32 * 16 * 8;  // one epilogue warp's [32 rows x 16 int64] box
+  static constexpr size_t kSmem = (size_t)STAGES * kStage + 2 * 8 * kStageOut + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-// One CTA: 128 x BN tile of stream blockIdx.z.  CL CTAs of a cluster (along
-// N) share the row tile: each loads 128/CL rows of every limb tile and
-// multicasts them to all CL CTAs, so A is read from L2 once per cluster.
-template <int L, int BN, int STAGES, int SW, int CL, int EPI = 0>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+struct OutMaps {
+  CUtensorMap m[8];  // C_m as a 2-D int64 tensor [rows][cols], box {16, 32}, 128B swizzle
+};
+
+// Persistent, warp-specialised kernel.  The grid is one CTA per SM (clusters
+// of CL along N); each cluster walks the work list w = cid, cid + nclusters, ...
+// with w -> (stream m, row tile, column-tile group), CTA rank r taking column
+// tile group*CL + r.  The CL CTAs of a cluster share the row tile: each loads
+// 128/CL rows of every limb tile and multicasts them to all CL CTAs, so A is
+// read from L2 once per cluster.  One accumulator set (L * BN = 512 TMEM
+// columns): the MMA warp waits until the epilogue has drained TMEM
+// (tmem_empty) before the next tile, while the producer already streams the
+// next tile's stages; the epilogue's global stores drain under the next
+// mainloop.
+constexpr int kEpiWarps = 8;
+constexpr int kThreadsP = 128 + 32 * kEpiWarps;  // warps 0-3: roles, 4-11: epilogue
+
+template <int L, int BN, int STAGES, int SW, int CL>
+__global__ void __launch_bounds__(kThreadsP, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-          const __grid_constant__ ne_streams C, int64_t rows, int64_t cols, int64_t K) {
+          const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   constexpr int BK = CF::BK;
   static_assert(L * BN <= 512, "TMEM holds 512 columns");
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::kStage);
+  unsigned char* stage_out = smem + STAGES * CF::kStage;  // 2 x 8 x 4 KB, 1024-B aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + 2 * 8 * CF::kStageOut);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = CL > 1 ? cluster_rank() : 0;
   const uint16_t cmask = (uint16_t)((1u << CL) - 1);
-  const int m = blockIdx.z;
-  const int64_t row0 = (int64_t)blockIdx.y * BM;
-  const int64_t col0 = (int64_t)blockIdx.x * BN;
   const int KB = (int)(K / BK);
+  const int64_t n_rt = rows / BM, n_cg = cols / (BN * CL);
+  const int64_t n_work = (int64_t)M * n_rt * n_cg;
+  const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -186,6 +200,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       mbar_init(&empty[s], CL);  // released by the MMA warp of every CTA in the cluster
     }
     mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, kEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -201,80 +216,121 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
-    for (int kb = 0; kb < KB; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t round = (uint32_t)(kb / STAGES);
-      mbar_wait(&empty[s], (round & 1) ^ 1);
-      unsigned char* st = smem + s * CF::kStage;
-      mbar_expect_tx(&full[s], (uint32_t)CF::kStage);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+      uint32_t it = 0;
+      for (int64_t w = cid; w < n_work; w += ncl) {
+        const int m = (int)(w / (n_rt * n_cg));
+        const int64_t rem = w % (n_rt * n_cg);
+        const int64_t row0 = (rem / n_cg) * BM;
+        const int64_t col0 = ((rem % n_cg) * CL + crank) * BN;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          unsigned char* st = smem + s * CF::kStage;
+          mbar_expect_tx(&full[s], (uint32_t)CF::kStage);
 #pragma unroll
-      for (int i = 0; i < L; ++i) {
-        unsigned char* dst = st + i * CF::kATile + crank * CF::kARows * BK;
-        const int32_t grow = (int32_t)(((int64_t)m * L + i) * rows + row0 + crank * CF::kARows);
-        if (CL > 1)
-          tma_load_2d_mc(&mapA, &full[s], dst, kb * BK, grow, cmask);
-        else
-          tma_load_2d(&mapA, &full[s], dst, kb * BK, grow);
-      }
-      tma_load_2d(&mapB, &full[s], st + L * CF::kATile, kb * BK, (int32_t)col0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
-    constexpr uint32_t idesc = idesc_i8(BM, BN);
-    for (int kb = 0; kb < KB; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t round = (uint32_t)(kb / STAGES);
-      mbar_wait(&full[s], round & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t sa = smem_u32(smem + s * CF::kStage);
-      const uint32_t sb = sa + L * CF::kATile;
-#pragma unroll
-      for (int ks = 0; ks < BK / UMMA_K; ++ks) {
-        const uint64_t bdesc = umma_desc<SW>(sb + ks * UMMA_K);
-#pragma unroll
-        for (int i = 0; i < L; ++i) {
-          const uint64_t adesc = umma_desc<SW>(sa + i * CF::kATile + ks * UMMA_K);
-          mma_i8(tmem_base + i * BN, adesc, bdesc, idesc, (kb | ks) != 0);
+          for (int i = 0; i < L; ++i) {
+            unsigned char* dst = st + i * CF::kATile + crank * CF::kARows * BK;
+            const int32_t grow = (int32_t)(((int64_t)m * L + i) * rows + row0 + crank * CF::kARows);
+            if (CL > 1)
+              tma_load_2d_mc(&mapA, &full[s], dst, kb * BK, grow, cmask);
+            else
+              tma_load_2d(&mapA, &full[s], dst, kb * BK, grow);
+          }
+          tma_load_2d(&mapB, &full[s], st + L * CF::kATile, kb * BK, (int32_t)col0);
         }
       }
-      mma_commit(&empty[s], cmask);  // frees stage s in every CTA of the cluster
     }
-    mma_commit(tmem_full, 1);        // accumulators final
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_i8(BM, BN);
+      uint32_t it = 0, tile = 0;
+      for (int64_t w = cid; w < n_work; w += ncl, ++tile) {
+        mbar_wait(tmem_empty, (tile & 1) ^ 1);  // epilogue drained the accumulators
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + s * CF::kStage);
+          const uint32_t sb = sa + L * CF::kATile;
+#pragma unroll
+          for (int ks = 0; ks < BK / UMMA_K; ++ks) {
+            const uint64_t bdesc = umma_desc<SW>(sb + ks * UMMA_K);
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+              const uint64_t adesc = umma_desc<SW>(sa + i * CF::kATile + ks * UMMA_K);
+              mma_i8(tmem_base + i * BN, adesc, bdesc, idesc, (kb | ks) != 0);
+            }
+          }
+          mma_commit(&empty[s], cmask);  // frees stage s in every CTA of the cluster
+        }
+        mma_commit(tmem_full, 1);        // this tile's accumulators are final
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> int64 recombination ->
+    // 128B-swizzled smem box -> TMA bulk tensor store (double-buffered per warp)
+    const int ew = warp - 4;
+    const int q = warp & 3;          // TMEM lane quarter this warp may access (warp id mod 4)
+    const int half = ew >> 2;        // column half
+    const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16);
+    unsigned char* my_out = stage_out + ew * 2 * CF::kStageOut;
+    uint32_t tile = 0, buf = 0;
+    for (int64_t w = cid; w < n_work; w += ncl, ++tile) {
+      const int m = (int)(w / (n_rt * n_cg));
+      const int64_t rem = w % (n_rt * n_cg);
+      const int64_t row0 = (rem / n_cg) * BM;
+      const int64_t col0 = ((rem % n_cg) * CL + crank) * BN;
+      mbar_wait(tmem_full, tile & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16, buf ^= 1) {
+        uint32_t v[L][16];
+#pragma unroll
+        for (int i = 0; i < L; ++i) tmem_ld16(tl + i * BN + c, v[i]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c + 16 == (half + 1) * (BN / 2)) {
+          // last TMEM read of this tile for this warp: release the accumulators
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tmem_empty)) : "memory");
+        }
+        // the TMA store that last read this buffer (two chunks ago) must be done
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        unsigned char* box = my_out + buf * CF::kStageOut;
+        // row `lane` of the box, 16-byte chunk k stored at chunk k ^ (row & 7) (128B swizzle)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+          for (int i = 0; i < L; ++i) {
+            a0 += (uint64_t)(int64_t)(int32_t)v[i][2 * k] << (8 * i);
+            a1 += (uint64_t)(int64_t)(int32_t)v[i][2 * k + 1] << (8 * i);
+          }
+          *reinterpret_cast<ulonglong2*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) = make_ulonglong2(a0, a1);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  reinterpret_cast<uint64_t>(&outm.m[m])),
+              "r"((int32_t)(col0 + c)), "r"((int32_t)(row0 + 32 * q)), "r"(smem_u32(box))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   __syncwarp();
-
-  // ---------------- epilogue (all 8 warps): TMEM -> registers -> int64 recombination -> global
-  if (EPI != 2) {
-    const int q = warp & 3;           // TMEM lane quarter this warp may access
-    const int half = warp >> 2;       // column half
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int64_t row = row0 + 32 * q + lane;
-    int64_t* __restrict__ crow = C.s[m] + row * cols + col0;
-    const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16);
-#pragma unroll 1
-    for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
-      uint32_t v[L][16];
-#pragma unroll
-      for (int i = 0; i < L; ++i) tmem_ld16(tl + i * BN + c, v[i]);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        uint64_t a0 = 0, a1 = 0;
-#pragma unroll
-        for (int i = 0; i < L; ++i) {
-          a0 += (uint64_t)(int64_t)(int32_t)v[i][j] << (8 * i);
-          a1 += (uint64_t)(int64_t)(int32_t)v[i][j + 1] << (8 * i);
-        }
-        if (EPI == 0 || (a0 == 0x1234567ull && a1 == 0x7654321ull))
-          __stcs(reinterpret_cast<longlong2*>(crow + c + j), make_longlong2((int64_t)a0, (int64_t)a1));
-      }
-    }
-  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if (CL > 1)
     cluster_sync();  // no CTA leaves while a peer may still signal its barriers
@@ -305,6 +361,18 @@ static EncodeTiledFn encode_fn() {
 }
 
 // 2-D int8 tensor [outer][inner] (inner contiguous), box {SW, box_outer}, SW-byte swizzle
+static bool make_out_map(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 8};
+  cuuint32_t box[2] = {16, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
                      uint32_t box_outer) {
   EncodeTiledFn fn = encode_fn();
@@ -328,14 +396,19 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   CUtensorMap ma, mb;
   if (!make_map(&ma, planes, (uint64_t)K, (uint64_t)M * L * rows, SW, CF::kARows)) return NE_ECUDA;
   if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, BN)) return NE_ECUDA;
-  static const int epi = getenv("NE_GEMM_EPI") ? atoi(getenv("NE_GEMM_EPI")) : 0;
-  auto kern = epi == 1 ? k_gemm_tc<L, BN, STAGES, SW, CL, 1> : epi == 2 ? k_gemm_tc<L, BN, STAGES, SW, CL, 2>
-                                                                  : k_gemm_tc<L, BN, STAGES, SW, CL, 0>;
+  if (M > 8) return NE_ENOTSUP;
+  OutMaps om;
+  for (int m = 0; m < M; ++m)
+    if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)rows)) return NE_ECUDA;
+  auto kern = k_gemm_tc<L, BN, STAGES, SW, CL>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) != cudaSuccess)
     return NE_ECUDA;
+  const int64_t n_work = (int64_t)M * (rows / BM) * (cols / (BN * CL));
+  int64_t nclusters = num_sms() / CL;
+  if (nclusters > n_work) nclusters = n_work;
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)(cols / BN), (unsigned)(rows / BM), (unsigned)M);
-  lc.blockDim = dim3(kThreadsTC);
+  lc.gridDim = dim3((unsigned)(nclusters * CL));
+  lc.blockDim = dim3(kThreadsP);
   lc.dynamicSmemBytes = CF::kSmem;
   lc.stream = s;
   cudaLaunchAttribute at[1];
@@ -345,7 +418,7 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  if (cudaLaunchKernelEx(&lc, kern, ma, mb, C, rows, cols, K) != cudaSuccess) return NE_ECUDA;
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M) != cudaSuccess) return NE_ECUDA;
   return launch_status();
 }
 
@@ -360,19 +433,19 @@ ne_status launch_gemm_tc(int M, int L, const int8_t* planes, const int8_t* Bt, i
   const bool pair128 = cols % 256 == 0, pair256 = cols % 512 == 0;
   switch (L) {
     case 1:
-      if (pair256) return tc::run<1, 256, 8, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
-      if (cols % 256 == 0) return tc::run<1, 256, 8, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      if (pair256) return tc::run<1, 256, 6, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
+      if (cols % 256 == 0) return tc::run<1, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
       return tc::run<1, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
     case 2:
-      if (pair256) return tc::run<2, 256, 6, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
-      if (cols % 256 == 0) return tc::run<2, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
-      return tc::run<2, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      if (pair256) return tc::run<2, 256, 5, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
+      if (cols % 256 == 0) return tc::run<2, 256, 5, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      return tc::run<2, 128, 6, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
     case 3:
-      if (pair128) return tc::run<3, 128, 6, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
-      return tc::run<3, 128, 6, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      if (pair128) return tc::run<3, 128, 5, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
+      return tc::run<3, 128, 5, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
     case 4:
-      if (pair128) return tc::run<4, 128, 5, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
-      return tc::run<4, 128, 5, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      if (pair128) return tc::run<4, 128, 4, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
+      return tc::run<4, 128, 4, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
     default: return NE_ENOTSUP;
   }
 }
