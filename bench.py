@@ -483,8 +483,8 @@ class C1Chain(Workload):
         return dt, reps * self.n / 1e9, f"{reps} full C1 passes"
 
 
-WORKLOADS = {"c1": C1Chain, "c2": C2Conv, "c3": C3Gemm, "c4": C4PermInner}
-ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c3": (16, 2), "c4": (64, 8)}  # (cpu_baseline, per ref step)
+WORKLOADS = {"c1": C1Chain, "c2": C2Conv, "c3": C3Gemm, "c4": C4PermInner, "c5": None}
+ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c3": (16, 2), "c4": (64, 8), "c5": (4096, 512)}  # (cpu_baseline, per ref step)
 METRIC = "entangled LSB Gop/s (or GB/s) at 1/2/4/8 B200, % roofline, % overhead vs plain"
 
 
@@ -542,6 +542,104 @@ class ClockSampler:
 
 
 # ====================================================================== runs
+def c5_oracle_sample(plan, ncols):
+    """Row 0 of every stream, the first `ncols` output columns, through the
+    oracle: entangle, GEMM, disentangle + check, recovery without plan.kill."""
+    import oracle as O
+
+    M, K, b = plan.M, plan.K, plan.bound
+    ocfg = O.config_for(M, 64)
+    A0 = np.stack([O.gen_uniform(plan.seed, 4, m, -b, b, K) for m in range(M)])  # row 0 of each block
+    B = O.gen_uniform(plan.seed, 5, 0, -b, b, K * plan.cols).reshape(K, plan.cols)[:, :ncols].copy()
+    t0 = time.perf_counter()
+    E = O.entangle(ocfg, A0)
+    D = O.op_gemm(ocfg, E.reshape(M, 1, K), B).reshape(M, -1)
+    O.disentangle_check(ocfg, D, 0)
+    O.recover(ocfg, [None if m == (plan.kill or 0) else D[m] for m in range(M)], plan.kill or 0)
+    dt = time.perf_counter() - t0
+    return dt, 2 * M * ncols * K / 1e9, f"row 0 of each of the {M} stream blocks, first {ncols} of {plan.cols} columns"
+
+
+def run_c5(args, rank, world, local_rank):
+    """configs[4]: M = 8 entangled streams (one per GPU when N = 8; stream m on
+    rank m mod N otherwise), GEMM 16384^3 int32 U[-32,32) rows sharded, position-
+    major all_to_all + check, kill stream 3, survivors recover (NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1604_04740_b200.dist import C5Plan, GpuBackend, c5_setup, c5_step, make_survivor_groups
+
+    torch.cuda.set_device(local_rank)
+    plan = C5Plan()
+    be = GpuBackend(plan.M, plan.bound)
+    groups = make_survivor_groups(world, plan.M)
+    inp = c5_setup(be, plan)
+    for _ in range(args.warmup):
+        c5_step(be, plan, inp, groups)
+        be.stage_ms()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stage_tot, ok, flagged = {}, True, 0
+    clk = ClockSampler(local_rank)
+    clk.start()
+    time.sleep(0.05)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        res = c5_step(be, plan, inp, groups, verify=False)
+        flagged += res["flagged"]
+    e1.record()
+    torch.cuda.synchronize()
+    clk.stop()
+    for k, v in be.stage_ms().items():
+        stage_tot[k] = stage_tot.get(k, 0.0) + v
+    # untimed verification step: recovered outputs == checked outputs (checksums)
+    res = c5_step(be, plan, inp, groups, verify=True)
+    be.stage_ms()
+    ok = res.get("checksum_ok") in (True, None)
+    total_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    if rank != 0:
+        return None
+    stage_ms = {k: v / args.steps for k, v in stage_tot.items()}
+    peaks, peak_src = load_peaks()
+    per_rank_streams = len([m for m in range(plan.M) if m % world == rank])
+    tops = 2 * be.L * per_rank_streams * plan.rows * plan.cols * plan.K / 1e12
+    achieved = tops / (stage_ms["entangle_gemm"] / 1e3)
+    peak = peaks["bf16_tflops"] * 2.0
+    line = {
+        "metric": METRIC, "value": round(2 * plan.M * plan.rows * plan.cols * plan.K / 1e9 / (ms / 1e3), 3),
+        "unit": "Gop/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (counter-based splitmix64 generator, gen/ne_gen.h; no dataset)",
+        "config": {"workload": "C5 (BASELINE configs[4]): M=8 entangled streams, stream m on rank m mod N; GEMM "
+                               "16384x16384x16384 int32 U[-32,32), row block m of A per stream; kill stream 3, "
+                               "recover from the other 7",
+                   "M": plan.M, "rows_per_stream": plan.rows, "cols": plan.cols, "K": plan.K, "limbs_L": be.L,
+                   "kill": plan.kill, "exchange": "NCCL all_to_all (torch.distributed)" if world > 1 else
+                   "single GPU: all 8 streams local, exchange is a local copy"},
+        "roofline": {"bound": "tensor", "kernel": "entangle_gemm (k_entangle_limbs_stream + k_gemm_tc)",
+                     "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TOP/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak_source": f"int8 dense = 2 x bf16 burst ({peak_src})"},
+        "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "gpu_launches": None,
+        "clocks": clk.summary(),
+        "correctness": {"flagged_positions": flagged, "recovery_checksum_equal": ok},
+    }
+    if world == 1:
+        n = ORACLE_SAMPLE["c5"][0]
+        dt, work, what = c5_oracle_sample(plan, n)
+        line["cpu_baseline"] = {"value": round(work / dt, 6), "unit": "Gop/s", "cores": 1, "kind": "oracle",
+                                "sample": what, "seconds": round(dt, 3), "cpu": _cpu_model()}
+    return line
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -698,7 +796,7 @@ class _HostOnly:
 
 def run_reference(args):
     """The CPU oracle as it stands (plain C, 1 core), each step a bounded sample."""
-    cls = WORKLOADS[args.workload]
+    cls = WORKLOADS[args.workload] or C3Gemm
     W = cls.__new__(cls)
     # the attributes oracle_sample / work_per_step / config need, without CUDA
     if args.workload == "c3":
@@ -713,6 +811,25 @@ def run_reference(args):
         class _Cfg:
             l, k = 16, 16
         W.cfg = _Cfg
+    elif args.workload == "c5":
+        from paper_1604_04740_b200.dist import C5Plan
+
+        plan = C5Plan()
+        per_step = ORACLE_SAMPLE["c5"][1]
+        for _ in range(args.warmup):
+            c5_oracle_sample(plan, per_step)
+        tot = work = 0.0
+        for _ in range(args.steps):
+            dt, wk, what = c5_oracle_sample(plan, per_step)
+            tot, work = tot + dt, work + wk
+        value = work / tot
+        return {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Gop/s", "n_gpus": 1,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+                "data": "synthetic (same seeded generator)", "config": {"workload": "C5 (BASELINE configs[4])"},
+                "cpu_baseline": {"value": round(value, 6), "unit": "Gop/s", "cores": 1, "kind": "oracle",
+                                 "sample": what + " per step", "cpu": _cpu_model()},
+                "e2e": {"value": round(value, 6), "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     elif args.workload == "c2":
         W.M, W.n, W.T, W.seed = 3, 65536, 64, 1
     else:
@@ -765,7 +882,7 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    line = run_ours(args, rank, world, local_rank)
+    line = run_c5(args, rank, world, local_rank) if args.workload == "c5" else run_ours(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -137,6 +137,13 @@ ne_status ne_entangle_stream(const ne_config* cfg, int32_t m, const int32_t* c_m
                              const int32_t* c_prev, int64_t* eps_m, int64_t n_total,
                              ne_diag* diag, ne_stream_t stream);
 
+/* One stream, in the int8 digit-plane format of ne_entangle_limbs:
+ * planes_m[i*n_total + n] = digit i of c_m[n] + S_l{c_prev[n]}.  n_total % 16 == 0.
+ * Range violations (|c_m| > hi or not representable in L digits) name m*n_total + n. */
+ne_status ne_entangle_limbs_stream(const ne_config* cfg, int32_t m, const int32_t* c_m,
+                                   const int32_t* c_prev, int64_t n_total, int32_t L, int8_t* planes_m,
+                                   ne_diag* diag, ne_stream_t stream);
+
 /* Footnote P:507-511: the shared operand of +/- self-entangled,
  * g_ent[n] = S_l{g[n]} + g[n]. */
 ne_status ne_entangle_shared(const ne_config* cfg, const int32_t* g, int64_t* g_ent,
@@ -199,6 +206,12 @@ ne_status ne_gemm_prep_b(const int32_t* B, int64_t K, int64_t cols, int8_t* Bt, 
 ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes, int32_t L,
                            const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams C,
                            ne_stream_t stream);
+
+/* One stream of ne_op_gemm_limbs (the per-GPU GEMM of the one-stream-per-GPU
+ * layout): C_m = sum_i 2^(8i) D_{m,i} B from planes_m (L planes). */
+ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t* planes_m, int32_t L,
+                                  const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int64_t* C_m,
+                                  ne_stream_t stream);
 
 /* ====================================== a4-a6: disentangle, check, recover === */
 

@@ -30,6 +30,7 @@ NE_OP_SCALE, NE_OP_ADD, NE_OP_LINEAR, NE_OP_PERMUTE = 0, 1, 2, 3
 EXPORTS = (
     "ne_config_for", "ne_dynamic_range", "ne_certify", "ne_gemm_limbs_for", "ne_diag_reset",
     "ne_entangle", "ne_entangle_aos", "ne_entangle_limbs", "ne_entangle_stream", "ne_entangle_shared",
+    "ne_entangle_limbs_stream", "ne_op_gemm_limbs_stream",
     "ne_op_scale", "ne_op_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
     "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
@@ -70,6 +71,8 @@ _SIGS = {
     "ne_entangle_limbs": [_PCFG, Streams, _I64, _I32, _VP, _VP, _VP],
     "ne_entangle_stream": [_PCFG, _I32, _VP, _VP, _VP, _I64, _VP, _VP],
     "ne_entangle_shared": [_PCFG, _VP, _VP, _I64, _VP],
+    "ne_entangle_limbs_stream": [_PCFG, _I32, _VP, _VP, _I64, _I32, _VP, _VP, _VP],
+    "ne_op_gemm_limbs_stream": [_PCFG, _VP, _I32, _VP, _I64, _I64, _I64, _VP, _VP],
     "ne_op_scale": [_PCFG, Streams, _I64, _I64, _VP, _VP],
     "ne_op_add": [_PCFG, Streams, Streams, _I64, _I32, _VP],
     "ne_op_inner": [_PCFG, Streams, _I64, _VP, _I64, _I64, Streams, _VP],
@@ -200,6 +203,16 @@ def ne_entangle_limbs(cfg: Config, c, L: int, planes: torch.Tensor, diag=None) -
 def ne_entangle_stream(cfg: Config, m: int, c_m, c_prev, eps_m, diag=None) -> None:
     _call("ne_entangle_stream", C.byref(cfg), m, _ptr(c_m, torch.int32), _ptr(c_prev, torch.int32),
           _ptr(eps_m, torch.int64), c_m.numel(), _ptr(diag, torch.int64), _stream())
+
+
+def ne_entangle_limbs_stream(cfg: Config, m: int, c_m, c_prev, L: int, planes_m, diag=None) -> None:
+    _call("ne_entangle_limbs_stream", C.byref(cfg), m, _ptr(c_m, torch.int32), _ptr(c_prev, torch.int32),
+          c_m.numel(), L, _ptr(planes_m, torch.int8), _ptr(diag, torch.int64), _stream())
+
+
+def ne_op_gemm_limbs_stream(cfg: Config, planes_m, L: int, Bt, rows: int, cols: int, K: int, C_m) -> None:
+    _call("ne_op_gemm_limbs_stream", C.byref(cfg), _ptr(planes_m, torch.int8), L, _ptr(Bt, torch.int8), rows, cols,
+          K, _ptr(C_m, torch.int64), _stream())
 
 
 def ne_entangle_shared(cfg: Config, g: torch.Tensor, g_ent: torch.Tensor) -> None:

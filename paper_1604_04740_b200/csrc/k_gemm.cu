@@ -134,6 +134,19 @@ extern "C" ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes
   return launch_gemm_tc(cfg->M, L, planes, Bt, rows, cols, K, C, cs(stream));
 }
 
+extern "C" ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t* planes_m, int32_t L,
+                                             const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int64_t* C_m,
+                                             ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (!planes_m || !Bt || !C_m || L < 1 || L > 4 || !aligned16(planes_m) || !aligned16(Bt) || !aligned16(C_m))
+    return NE_EINVAL;
+  if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
+  ne_streams C{};
+  C.s[0] = C_m;
+  return launch_gemm_tc(1, L, planes_m, Bt, rows, cols, K, C, cs(stream));
+}
+
 extern "C" ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int64_t rows, int64_t cols,
                                 int64_t K, ne_gemm_algo algo, int32_t L, ne_streams C, void* ws, size_t ws_bytes,
                                 ne_diag* diag, ne_stream_t stream) {

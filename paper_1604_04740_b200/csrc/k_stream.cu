@@ -203,6 +203,41 @@ k_entangle_limbs(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
+// one stream into L digit planes (same digit trick as k_entangle_limbs)
+template <int L>
+__global__ void __launch_bounds__(kThreads)
+k_entangle_limbs_stream(const int32_t* __restrict__ cm, const int32_t* __restrict__ cp, int m, int l, int64_t hi,
+                        int64_t n, int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
+  constexpr uint64_t bias = 0x8080808080808080ull >> (64 - 8 * L);
+  constexpr uint64_t span = L == 8 ? 0 : (1ull << (8 * L));
+  int bad = 0;
+  long long first = LLONG_MAX;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n / 4; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 4 * v;
+    const int4 a = __ldcs(reinterpret_cast<const int4*>(cm + n0)), b = __ldcs(reinterpret_cast<const int4*>(cp + n0));
+    const int32_t cc[4] = {a.x, a.y, a.z, a.w}, pp[4] = {b.x, b.y, b.z, b.w};
+    uint64_t y[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t ci = cc[i];
+      y[i] = (uint64_t)ci + ((uint64_t)(int64_t)pp[i] << l) + bias;
+      if (ci > hi || ci < -hi || (L < 8 && y[i] >= span)) {
+        ++bad;
+        const long long idx = (long long)m * n + n0 + i;
+        first = idx < first ? idx : first;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      uint32_t w = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w |= (uint32_t)((y[i] >> (8 * j)) & 0xff) << (8 * i);
+      __stcs(reinterpret_cast<unsigned int*>(planes + (int64_t)j * n + n0), w ^ 0x80808080u);
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
 // one stream: eps_m = c_m + S_l{c_prev}
 __global__ void __launch_bounds__(kThreads)
 k_entangle_stream(const int32_t* __restrict__ cm, const int32_t* __restrict__ cp, int m, int l,
@@ -458,6 +493,29 @@ extern "C" ne_status ne_entangle_stream(const ne_config* cfg, int32_t m, const i
     return NE_EINVAL;
   k_entangle_stream<<<grid_for(n_total, kThreads), kThreads, 0, cs(stream)>>>(c_m, c_prev, m, cfg->l,
                                                                             range_hi(cfg), n_total, eps_m, diag);
+  return launch_status();
+}
+
+extern "C" ne_status ne_entangle_limbs_stream(const ne_config* cfg, int32_t m, const int32_t* c_m,
+                                              const int32_t* c_prev, int64_t n_total, int32_t L, int8_t* planes_m,
+                                              ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (m < 0 || m >= cfg->M) return NE_EINDEX;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || n_total % 16 != 0 || L < 1 || L > 8 || !c_m || !c_prev || !planes_m || !aligned16(c_m) ||
+      !aligned16(c_prev) || !aligned16(planes_m))
+    return NE_EINVAL;
+  const int grid = grid_for(n_total / 4, kThreads);
+  const int64_t hi = range_hi(cfg);
+  cudaStream_t s = cs(stream);
+  switch (L) {
+    case 1: k_entangle_limbs_stream<1><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
+    case 2: k_entangle_limbs_stream<2><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
+    case 3: k_entangle_limbs_stream<3><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
+    case 4: k_entangle_limbs_stream<4><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
+    default: k_entangle_limbs_stream<8><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
+  }
   return launch_status();
 }
 

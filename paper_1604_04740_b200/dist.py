@@ -1,0 +1,293 @@
+"""Multi-GPU orchestration of the hot path (BASELINE configs[4]).
+
+C5 — "M = 8 streams, one per GPU on 8xB200: entangled GEMM 16384^3 int32 in
+[-32, 32), rows sharded; kill one rank's output, recover all streams from the
+other 7 via NCCL".  The paper's fault-isolation unit is "a separate processor
+core for each of the M streams" (Props 1/3): here stream
+m lives on rank m mod world (one stream per GPU when world == M).
+
+Per rank, for each owned stream m (reading R13: stream m = row block m of A):
+  1. A_m and A_{m-1} are generated locally from the seed (counter-based, so no
+     ring exchange is needed for Eq. 15's c_{m-1}); B is generated locally.
+  2. entangle into int8 digit planes (ne_entangle_limbs_stream, a0 + a1),
+  3. Delta_m = E_m B on tcgen05 (ne_op_gemm_limbs_stream, a3),
+  4. position-major all_to_all: every rank receives all M streams of 1/world of
+     the output positions (the only data-path exchange of the check),
+  5. disentangle + check on that slice (ne_disentangle_check, a4 + a5),
+  6. simulated fail-stop of stream r (its rank's Delta is dropped): the
+     survivors exchange again (subgroup all_to_all) and recover every stream
+     from the other M-1 (ne_recover, a6),
+  7. (verify=True) an order-independent checksum of the checked and the
+     recovered outputs, summed over ranks, must agree (bit-exact recovery).
+
+The compute backend is injected: ``GpuBackend`` (libne.so kernels) is the
+product; the CPU tests drive the same orchestration with a test-only backend
+over gloo so the host logic (partitioning, exchange layout, recovery routing)
+is exercised without GPUs.  No code here falls back to the CPU by itself.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Sequence
+
+import torch
+import torch.distributed as dist
+
+
+@dataclasses.dataclass
+class C5Plan:
+    M: int = 8
+    rows_total: int = 16384
+    cols: int = 16384
+    K: int = 16384
+    seed: int = 4
+    bound: int = 32          # A, B uniform in [-bound, bound)
+    kill: int | None = 3     # stream whose output is lost (None: no fail-stop)
+
+    @property
+    def rows(self) -> int:   # rows per stream (row block of A)
+        return self.rows_total // self.M
+
+
+class GpuBackend:
+    """The product backend: every call is one libne.so entry point on the
+    current CUDA stream."""
+
+    def __init__(self, M: int, bound: int):
+        import paper_1604_04740_b200 as ne
+
+        self.ne = ne
+        self.cfg = ne.ne_config_for(M)
+        self.L = ne.ne_gemm_limbs_for(self.cfg, bound)
+        self.diag = ne.diag_new()
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.marks = []
+
+    def gen(self, seed, tag, stream, lo, hi, n):
+        out = torch.empty(n, dtype=torch.int32, device=self.device)
+        self.ne.ne_gen_uniform_i32(seed, tag, stream, lo, hi, out)
+        return out
+
+    def prep_b(self, B, K, cols):
+        Bt = torch.empty(cols * K, dtype=torch.int8, device=self.device)
+        self.ne.ne_gemm_prep_b(B, K, cols, Bt, self.diag)
+        return Bt
+
+    def entangled_gemm(self, m, A_m, A_prev, Bt, rows, cols, K):
+        planes = torch.empty(self.L * rows * K, dtype=torch.int8, device=self.device)
+        self.ne.ne_entangle_limbs_stream(self.cfg, m, A_m, A_prev, self.L, planes, self.diag)
+        out = torch.empty(rows * cols, dtype=torch.int64, device=self.device)
+        self.ne.ne_op_gemm_limbs_stream(self.cfg, planes, self.L, Bt, rows, cols, K, out)
+        return out
+
+    def check(self, deltas: Sequence[torch.Tensor], r: int):
+        n = deltas[0].numel()
+        out = [torch.empty(n, dtype=torch.int64, device=self.device) for _ in deltas]
+        d = self.ne.diag_new()
+        self.ne.ne_disentangle_check(self.cfg, list(deltas), r, out, None, d)
+        return out, int(self.ne.diag_read(d)["fault_positions"])
+
+    def recover(self, deltas: Sequence[torch.Tensor | None], r: int):
+        n = next(t for t in deltas if t is not None).numel()
+        out = [torch.empty(n, dtype=torch.int64, device=self.device) for _ in deltas]
+        self.ne.ne_recover(self.cfg, list(deltas), r, out)
+        return out
+
+    def sync(self):
+        torch.cuda.synchronize()
+
+    def mark(self, name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.marks.append((name, ev))
+
+    def stage_ms(self):
+        """Elapsed ms between consecutive marks (after a synchronize)."""
+        torch.cuda.synchronize()
+        out = {}
+        for (_, e0), (name, e1) in zip(self.marks, self.marks[1:]):
+            if name not in ("kill", "start"):
+                out[name] = out.get(name, 0.0) + e0.elapsed_time(e1)
+        self.marks = []
+        return out
+
+
+# ---------------------------------------------------------------- host logic
+def owned_streams(M: int, world: int, rank: int) -> list[int]:
+    """Stream m lives on rank m mod world (one stream per GPU when world == M)."""
+    return [m for m in range(M) if m % world == rank]
+
+
+def chunk_bounds(n: int, parts: int) -> list[tuple[int, int]]:
+    """Contiguous near-equal position chunks [lo, hi) of [0, n)."""
+    return [(j * n // parts, (j + 1) * n // parts) for j in range(parts)]
+
+
+def position_major_exchange(local: dict[int, torch.Tensor], M: int, members: list[int], me: int,
+                            group=None) -> dict[int, torch.Tensor]:
+    """all_to_all so that member j ends with every stream's slice j of the
+    positions.  `local` maps stream id -> this rank's full output of that
+    stream; every member sends its streams (ascending id) chunk by chunk.
+    Returns stream id -> this rank's slice of it."""
+    parts = len(members)
+    if parts == 1:  # a single rank holds every stream: nothing to move
+        return dict(local)
+    n = next(iter(local.values())).numel() if local else 0
+    n = _bcast_len(n, group)
+    bounds = chunk_bounds(n, parts)
+    mine = sorted(local)
+    send_chunks, send_sizes = [], []
+    for (lo, hi) in bounds:
+        for m in mine:
+            send_chunks.append(local[m][lo:hi])
+        send_sizes.append((hi - lo) * len(mine))
+    # who owns which streams among the members (static: m mod world over the full world)
+    counts = _allgather_counts(len(mine), group)
+    ids = _allgather_ids(mine, M, group)
+    lo, hi = bounds[members.index(me)]
+    recv_sizes = [(hi - lo) * c for c in counts]
+    dev = next(iter(local.values())).device if local else _dev(group)
+    send = torch.cat(send_chunks) if send_chunks else torch.empty(0, dtype=torch.int64, device=dev)
+    recv = torch.empty(sum(recv_sizes), dtype=torch.int64, device=dev)
+    dist.all_to_all_single(recv, send, recv_sizes, send_sizes, group=group)
+    out, off = {}, 0
+    for src_ids, c in zip(ids, counts):
+        for m in src_ids[:c]:
+            out[m] = recv[off:off + (hi - lo)]
+            off += hi - lo
+    return out
+
+
+def _bcast_len(n, group):
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return n
+    t = torch.tensor([n], dtype=torch.int64, device=_dev(group))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return int(t.item())
+
+
+def _dev(group):
+    if dist.is_initialized() and dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def _allgather_counts(c, group):
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return [c]
+    t = torch.tensor([c], dtype=torch.int64, device=_dev(group))
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, t, group=group)
+    return [int(x.item()) for x in out]
+
+
+def _allgather_ids(ids, M, group):
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return [list(ids)]
+    t = torch.full((M,), -1, dtype=torch.int64, device=_dev(group))
+    if ids:
+        t[: len(ids)] = torch.tensor(ids, dtype=torch.int64)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(out, t, group=group)
+    return [[int(v) for v in x.tolist() if v >= 0] for x in out]
+
+
+def position_checksum(d: Sequence[torch.Tensor], lo: int) -> int:
+    """Order-independent checksum of outputs d[m][i] at positions lo + i:
+    sum over (m, position) of a 64-bit mix of (value, m, position), wrapping."""
+    acc = 0
+    for m, t in enumerate(d):
+        if t.numel() == 0:
+            continue
+        pos = torch.arange(lo, lo + t.numel(), dtype=torch.int64, device=t.device)
+        z = t * 0x2545F4914F6CDD1D + (pos * 64 + m) * 0x9E3779B97F4A7C15
+        z = z ^ (z >> 29)
+        acc = (acc + int(z.sum().item())) & (2 ** 64 - 1)
+    return acc
+
+
+def _sum_u64(x: int, group) -> int:
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return x
+    # two 32-bit halves so the sum cannot overflow int64 for <= 2^31 ranks
+    t = torch.tensor([x & 0xFFFFFFFF, x >> 32], dtype=torch.int64, device=_dev(group))
+    dist.all_reduce(t, group=group)
+    return (int(t[0].item()) + (int(t[1].item()) << 32)) & (2 ** 64 - 1)
+
+
+def make_survivor_groups(world: int, M: int):
+    """One subgroup per possible dead rank (created collectively up front)."""
+    if world < M or world == 1:
+        return {}
+    return {r: dist.new_group([i for i in range(world) if i != r]) for r in range(world)}
+
+
+def c5_setup(backend, plan: C5Plan) -> dict:
+    """Generate this rank's inputs (outside any timed region): B, and A_m,
+    A_{m-1} for every owned stream m, from the counter-based generator."""
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    M, rows, cols, K, b = plan.M, plan.rows, plan.cols, plan.K, plan.bound
+    inp = {"B": backend.gen(plan.seed, 5, 0, -b, b, K * cols), "A": {}}
+    for m in owned_streams(M, world, rank):
+        inp["A"][m] = (backend.gen(plan.seed, 4, m, -b, b, rows * K),
+                       backend.gen(plan.seed, 4, (m - 1) % M, -b, b, rows * K))
+    backend.sync()
+    return inp
+
+
+def c5_step(backend, plan: C5Plan, inp: dict, survivor_groups=None, verify: bool = True) -> dict:
+    """One C5 step on this rank: entangle + GEMM of the owned streams, exchange,
+    check, simulated fail-stop of stream plan.kill and recovery (module doc).
+    Stage boundaries are marked with backend.mark(name) (CUDA events on GPU)."""
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    M, rows, cols, K = plan.M, plan.rows, plan.cols, plan.K
+    mine = owned_streams(M, world, rank)
+
+    backend.mark("start")
+    Bt = backend.prep_b(inp["B"], K, cols)
+    deltas = {m: backend.entangled_gemm(m, inp["A"][m][0], inp["A"][m][1], Bt, rows, cols, K) for m in mine}
+    backend.mark("entangle_gemm")
+
+    # position-major exchange over all ranks, then the reliability check (r = 0)
+    members = list(range(world))
+    sl = position_major_exchange(deltas, M, members, rank, group=None)
+    lo, _ = chunk_bounds(rows * cols, world)[rank]
+    d_chk, flagged = backend.check([sl[m] for m in range(M)], 0)
+    backend.mark("exchange_check")
+    total_flags = int(_sum_u64(flagged, None))
+    cks_check = _sum_u64(position_checksum(d_chk, lo), None) if verify else None
+
+    result = {"flagged": total_flags, "streams": mine, "check_slice": (lo, d_chk)}
+    if plan.kill is None:
+        return result
+
+    # simulated fail-stop of stream r: its output never leaves the dead rank
+    r = plan.kill
+    dead_rank = r % world
+    if world == M and world > 1:
+        # the whole rank is lost: survivors alone exchange and recover
+        if rank == dead_rank:
+            result["checksum_ok"] = None  # this rank is the failed one: it takes no further part
+            return result
+        group = survivor_groups[dead_rank]
+        members = [i for i in range(world) if i != dead_rank]
+    else:
+        group = None
+        members = list(range(world))
+    backend.mark("kill")
+    surviving = {m: v for m, v in deltas.items() if m != r}
+    sl2 = position_major_exchange(surviving, M, members, rank, group=group)
+    lo2, _ = chunk_bounds(rows * cols, len(members))[members.index(rank)]
+    d_rec = backend.recover([None if m == r else sl2[m] for m in range(M)], r)
+    backend.mark("exchange_recover")
+    if verify:
+        cks_rec = _sum_u64(position_checksum(d_rec, lo2), group)
+        result["checksum_ok"] = cks_rec == cks_check
+    result["recover_slice"] = (lo2, d_rec)
+    return result
+
+
+def c5_run(backend, plan: C5Plan, survivor_groups=None) -> dict:
+    return c5_step(backend, plan, c5_setup(backend, plan), survivor_groups)

@@ -437,3 +437,41 @@ def test_gemm_tc_i8(O, M, L, bound, rows, cols, K):
     plain = (A.reshape(M, rows, K) @ B.reshape(K, cols)).reshape(M, -1)
     assert (to_np(d_out) == plain).all()
     assert ne.diag_read(diag)["fault_positions"] == 0
+
+
+# ------------------------------------------------------------------ one-stream-per-GPU entry points (C5)
+@pytest.mark.parametrize("M,L,bound", [(8, 2, 32), (3, 4, 64)])
+def test_entangle_limbs_stream_and_gemm_stream(O, M, L, bound):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    R, Cc, K = 128, 256, 384
+    A = gen(O, 4, 4, M, R * K, -bound, bound)
+    B = O.gen_uniform(4, 5, 0, -bound, bound, K * Cc)
+    E = O.entangle(ocfg, A)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    As = to_streams(A)
+    for m in (0, M - 1):
+        planes = torch.empty(L * R * K, dtype=torch.int8, device="cuda")
+        ne.ne_entangle_limbs_stream(cfg, m, As[m], As[(m - 1) % M], L, planes)
+        p = planes.cpu().numpy().astype(np.int64).reshape(L, -1)
+        assert (sum(p[i] * 256 ** i for i in range(L)) == E[m]).all()
+        out = torch.empty(R * Cc, dtype=torch.int64, device="cuda")
+        ne.ne_op_gemm_limbs_stream(cfg, planes, L, Bt, R, Cc, K, out)
+        ref = O.op_gemm(ocfg, E[m].reshape(R, K), B.reshape(K, Cc)).reshape(-1)
+        assert (out.cpu().numpy() == ref).all()
+
+
+def test_c5_orchestration_single_gpu(O):
+    """C5's host path on one GPU (world = 1: all 8 streams local), reduced size:
+    entangle + tcgen05 GEMM per stream, check, kill stream 3, recover."""
+    from paper_1604_04740_b200.dist import C5Plan, GpuBackend, c5_run
+
+    plan = C5Plan(M=8, rows_total=8 * 128, cols=256, K=512, seed=4, bound=32, kill=3)
+    res = c5_run(GpuBackend(plan.M, plan.bound), plan)
+    assert res["flagged"] == 0 and res["checksum_ok"] is True
+    B = O.gen_uniform(plan.seed, 5, 0, -32, 32, plan.K * plan.cols).reshape(plan.K, plan.cols)
+    lo, d = res["check_slice"]
+    lo2, d2 = res["recover_slice"]
+    for m in range(plan.M):
+        plain = (O.gen_uniform(plan.seed, 4, m, -32, 32, plan.rows * plan.K).reshape(plan.rows, plan.K) @ B).reshape(-1)
+        assert (d[m].cpu().numpy() == plain).all() and (d2[m].cpu().numpy() == plain).all()
