@@ -679,11 +679,35 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
     t_host1 = time.perf_counter()
-    clk.stop()
 
     total_ms = sum(ev[i][0].elapsed_time(ev[i][-1]) for i in range(args.steps))
     stage_ms = {nm: sum(ev[i][j].elapsed_time(ev[i][j + 1]) for i in range(args.steps)) / args.steps
                 for j, nm in enumerate(names)}
+    eager_ms = total_ms / args.steps
+    if args.graph:
+        # the same steps captured once per recovered stream r and replayed: removes
+        # the per-call host launch overhead of launch-bound configs (C1, C2)
+        graphs = []
+        nrot = getattr(W, "M", 1)
+        for i in range(nrot):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _, f in W.stages(i):
+                    f()
+            graphs.append(g)
+        for i in range(args.warmup):
+            graphs[i % nrot].replay()
+        torch.cuda.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        for i in range(args.steps):
+            graphs[i % nrot].replay()
+        g1.record()
+        torch.cuda.synchronize()
+        barrier()
+        total_ms = g0.elapsed_time(g1)
+    clk.stop()
     if world > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -755,6 +779,8 @@ def run_ours(args, rank, world, local_rank):
                                      "(profiles/traffic.json)" if tr else None,
                      "algorithmic_per_launch": f"{amount:.4g} {unit}", "peak_source": peak_note},
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "launch": "CUDA graph replay (one graph per recovered stream r)" if args.graph else "eager",
+        "eager_ms_per_step": round(eager_ms, 4),
         "e2e": {"value": round(W.work_per_step() * world / (e2e_ms / 1e3), 3), "unit": W.metric_unit,
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": W.launches_per_step * args.steps,
@@ -863,6 +889,7 @@ def main():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--algo", default="tc", choices=["tc", "imad"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
