@@ -475,3 +475,104 @@ def test_c5_orchestration_single_gpu(O):
     for m in range(plan.M):
         plain = (O.gen_uniform(plan.seed, 4, m, -32, 32, plan.rows * plan.K).reshape(plan.rows, plan.K) @ B).reshape(-1)
         assert (d[m].cpu().numpy() == plain).all() and (d2[m].cpu().numpy() == plain).all()
+
+
+# ------------------------------------------------------------------ BASELINE full sizes, bench launch config
+def test_c3_full_size_sampled(O):
+    """C3 at full size through the exact calls bench.py times: sampled rows vs
+    the oracle (delta, d_hat, recovery), every position unflagged, and a
+    Freivalds identity d_hat x == A (B x) over the whole output (exact in int64)."""
+    M, n = 3, 4096
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L = ne.ne_gemm_limbs_for(cfg, 64)
+    A = [torch.empty(n * n, dtype=torch.int32, device="cuda") for _ in range(M)]
+    for m in range(M):
+        ne.ne_gen_uniform_i32(2, 4, m, -64, 64, A[m])
+    B = torch.empty(n * n, dtype=torch.int32, device="cuda")
+    ne.ne_gen_uniform_i32(2, 5, 0, -64, 64, B)
+    planes = torch.empty(M * L * n * n, dtype=torch.int8, device="cuda")
+    Bt = torch.empty(n * n, dtype=torch.int8, device="cuda")
+    delta, dout, drec = empty_streams(M, n * n), empty_streams(M, n * n), empty_streams(M, n * n)
+    diag = ne.diag_new()
+    ne.ne_entangle_limbs(cfg, A, L, planes, diag)
+    ne.ne_gemm_prep_b(B, n, n, Bt, diag)
+    ne.ne_op_gemm_limbs(cfg, planes, L, Bt, n, n, n, delta)
+    ne.ne_disentangle_check(cfg, delta, 0, dout, None, diag)
+    ne.ne_recover(cfg, [delta[0], None, delta[2]], 1, drec)
+    d = ne.diag_read(diag)
+    assert d["range_violations"] == 0 and d["fault_positions"] == 0
+    Bh = O.gen_uniform(2, 5, 0, -64, 64, n * n).reshape(n, n)
+    for row in (0, 1, 2047, 4095):
+        Arow = np.stack([O.gen_uniform(2, 4, m, -64, 64, n, row * n) for m in range(M)])
+        E = O.entangle(ocfg, Arow)
+        dref = O.op_gemm(ocfg, E.reshape(M, 1, n), Bh).reshape(M, n)
+        sl = slice(row * n, (row + 1) * n)
+        assert (np.stack([t[sl].cpu().numpy() for t in delta]) == dref).all()
+        plain = O.op_gemm(ocfg, Arow.reshape(M, 1, n), Bh).reshape(M, n)
+        assert (np.stack([t[sl].cpu().numpy() for t in dout]) == plain).all()
+        assert (np.stack([t[sl].cpu().numpy() for t in drec]) == plain).all()
+    rng = np.random.default_rng(0)
+    x = rng.integers(-2 ** 20, 2 ** 20, size=n)
+    Bx = Bh @ x
+    for m in range(M):
+        Am = torch.stack([A[m]]).cpu().numpy().astype(np.int64).reshape(n, n)
+        assert (dout[m].cpu().numpy().reshape(n, n) @ x == Am @ Bx).all()
+
+
+def test_c4_full_size_sampled(O):
+    """C4 at full size (M = 4, 2^28 positions): sampled output blocks vs the
+    oracle recomputed from the generator at the permuted positions."""
+    M, n, Bk = 4, 1 << 28, 1024
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(M)]
+    for m in range(M):
+        ne.ne_gen_uniform_i32(3, 1, m, -(1 << 12), 1 << 12, c[m])
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    ne.ne_gen_perm_i32(3, 6, perm)
+    v = torch.empty(Bk, dtype=torch.int32, device="cuda")
+    ne.ne_gen_uniform_i32(3, 7, 0, -(1 << 12), 1 << 12, v)
+    eps = torch.empty(n * M, dtype=torch.int64, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_aos(cfg, c, eps, diag)
+    del c
+    nb = n // Bk
+    delta, dout = empty_streams(M, nb), empty_streams(M, nb)
+    bm = torch.empty(nb // 32, dtype=torch.int32, device="cuda")
+    ne.ne_op_permute_inner_check(cfg, v, Bk, 0, dout, x_aos=eps, perm=perm, n=n, delta_out=delta, bitmap=bm,
+                                 diag=diag)
+    drec = empty_streams(M, nb)
+    ne.ne_recover(cfg, [delta[0], delta[1], None, delta[3]], 2, drec)
+    d = ne.diag_read(diag)
+    assert d["range_violations"] == 0 and d["fault_positions"] == 0 and int(bm.abs().sum()) == 0
+    assert all(torch.equal(a, b) for a, b in zip(dout, drec))
+    vh = O.gen_uniform(3, 7, 0, -(1 << 12), 1 << 12, Bk)
+    D, DH = to_np(delta), to_np(dout)
+    for b in (0, 1, 12345, nb // 2 + 7, nb - 1):
+        idx = O.gen_perm(3, 6, n, Bk, b * Bk)
+        assert (perm[b * Bk:(b + 1) * Bk].cpu().numpy() == idx).all()
+        cb = np.stack([np.array([O.gen_uniform(3, 1, m, -(1 << 12), 1 << 12, 1, int(p))[0] for p in idx])
+                       for m in range(M)])
+        e = O.entangle(ocfg, cb)
+        dref = O.op_inner(ocfg, e, vh, Bk)[:, 0]
+        assert (D[:, b] == dref).all()
+        assert (DH[:, b] == O.op_inner(ocfg, cb, vh, Bk)[:, 0]).all()
+
+
+def test_c5_full_size_single_gpu_sampled(O):
+    """C5 at full size on one GPU (8 streams local): no flags, recovery of
+    stream 3 equals the checked outputs, sampled entries vs the oracle."""
+    from paper_1604_04740_b200.dist import C5Plan, GpuBackend, c5_run
+
+    plan = C5Plan()
+    res = c5_run(GpuBackend(plan.M, plan.bound), plan)
+    assert res["flagged"] == 0 and res["checksum_ok"] is True
+    _, d = res["check_slice"]
+    M, K, cols = plan.M, plan.K, plan.cols
+    cols_s = np.array([0, 1, 777, 8191, 16383])
+    Bs = np.stack([O.gen_uniform(plan.seed, 5, 0, -32, 32, 1, int(k) * cols + int(j)) [0]
+                   for k in range(K) for j in cols_s]).reshape(K, len(cols_s))
+    for row in (0, plan.rows - 1):
+        Arow = np.stack([O.gen_uniform(plan.seed, 4, m, -32, 32, K, row * K) for m in range(M)])
+        plain = O.op_gemm(O.config_for(M, 64), Arow.reshape(M, 1, K), Bs).reshape(M, -1)
+        got = np.stack([d[m][row * cols + cols_s].cpu().numpy() for m in range(M)])
+        assert (got == plain).all()
