@@ -74,7 +74,7 @@ class C3Gemm(Workload):
     name = "C3"
     metric_unit = "Gop/s"
 
-    def __init__(self, rank, n=4096, seed=2, algo="tc"):
+    def __init__(self, rank, n=4096, seed=2, algo="tc", scheme="entangled", limbs="plan"):
         import torch
         import paper_1604_04740_b200 as ne
 
@@ -82,8 +82,12 @@ class C3Gemm(Workload):
         self.M, self.rows, self.cols, self.K = 3, n, n, n
         self.seed = seed + 1000 * rank
         self.cfg = ne.ne_config_for(self.M)
-        self.L = ne.ne_gemm_limbs_for(self.cfg, 64)
+        if limbs == "base256":
+            self.L, self.limb_bits = ne.ne_gemm_limbs_for(self.cfg, 64), 8
+        else:  # the cheapest exact plan: base 2^l, 2 limbs (|A| < 128)
+            self.L, self.limb_bits = ne.ne_gemm_limb_plan(self.cfg, 64)
         self.algo = algo
+        self.scheme = scheme
         M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
         dev = "cuda"
         self.A = [torch.empty(R * K, dtype=torch.int32, device=dev) for _ in range(M)]
@@ -101,11 +105,34 @@ class C3Gemm(Workload):
         if algo == "imad":
             self.eps = [torch.empty(R * K, dtype=torch.int64, device=dev) for _ in range(M)]
         self.launches_per_step = 5
+        if scheme == "abft":
+            # the paper's comparison method on the same kernels: plain data (1 int8
+            # limb), one checksum stream (Eq. 4; |sum| <= 192 -> 2 limbs)
+            self.Asum = torch.empty(R * K, dtype=torch.int32, device=dev)
+            self.pdata = torch.empty(M * R * K, dtype=torch.int8, device=dev)
+            self.psum = torch.empty(2 * R * K, dtype=torch.int8, device=dev)
+            self.e = torch.empty(R * Cc, dtype=torch.int64, device=dev)
+            self.launches_per_step = 8
+            del self.planes
 
     def stages(self, i):
         ne, cfg, M = self.ne, self.cfg, self.M
         r = i % M
         part = [None if m == r else self.delta[m] for m in range(M)]
+        if self.scheme == "abft":
+            rr = [None if m == r else self.delta[m] for m in range(M)]
+            return [
+                ("encode", lambda: (ne.ne_abft_encode(cfg, self.A, self.Asum, self.diag),
+                                    ne.ne_to_limbs(self.A, 1, self.pdata, self.diag),
+                                    ne.ne_to_limbs([self.Asum], 2, self.psum, self.diag))),
+                ("prep_b", lambda: ne.ne_gemm_prep_b(self.B, self.K, self.cols, self.Bt, self.diag)),
+                ("gemm", lambda: (ne.ne_op_gemm_limbs(cfg, self.pdata, 1, self.Bt, self.rows, self.cols, self.K,
+                                                      self.delta),
+                                  ne.ne_op_gemm_limbs_stream(cfg, self.psum, 2, self.Bt, self.rows, self.cols,
+                                                             self.K, self.e))),
+                ("check", lambda: ne.ne_abft_check(cfg, self.delta, self.e, self.bitmap, self.diag)),
+                ("recover", lambda: ne.ne_abft_recover(cfg, rr, self.e, r, self.drec[r])),
+            ]
         if self.algo == "imad":
             return [
                 ("entangle", lambda: ne.ne_entangle(cfg, self.A, self.eps, self.diag)),
@@ -115,10 +142,10 @@ class C3Gemm(Workload):
                 ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
             ]
         return [
-            ("entangle", lambda: ne.ne_entangle_limbs(cfg, self.A, self.L, self.planes, self.diag)),
+            ("entangle", lambda: ne.ne_entangle_limbs(cfg, self.A, self.L, self.planes, self.diag, self.limb_bits)),
             ("prep_b", lambda: ne.ne_gemm_prep_b(self.B, self.K, self.cols, self.Bt, self.diag)),
             ("gemm", lambda: ne.ne_op_gemm_limbs(cfg, self.planes, self.L, self.Bt, self.rows, self.cols, self.K,
-                                                 self.delta)),
+                                                 self.delta, self.limb_bits)),
             ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
             ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
         ]
@@ -129,6 +156,12 @@ class C3Gemm(Workload):
     def stage_info(self):
         M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
         n = R * Cc
+        if self.scheme == "abft":
+            return {"encode": ("hbm", R * K * (M * 4 + 4 + M + 4 + 2) / 1e9, "GB"),
+                    "prep_b": ("hbm", K * Cc * 5 / 1e9, "GB"),
+                    "gemm": ("tensor", 2 * (M + 2) * R * Cc * K / 1e12, "TOP"),
+                    "check": ("hbm", (M + 1) * n * 8 / 1e9, "GB"),
+                    "recover": ("hbm", (M + 1) * n * 8 / 1e9, "GB")}
         gemm = ("tensor", 2 * L * M * R * Cc * K / 1e12, "TOP") if self.algo == "tc" else \
             ("alu", M * R * Cc * K / 1e12, "TMAC")
         return {
@@ -144,6 +177,9 @@ class C3Gemm(Workload):
                             "shared B 4096x4096 U[-64,64), K=4096, int64 results",
                 "M": self.M, "rows": self.rows, "cols": self.cols, "K": self.K,
                 "limbs_L": self.L if self.algo == "tc" else None, "gemm_algo": self.algo,
+                "limb_base_bits": self.limb_bits if self.algo == "tc" else None,
+                "scheme": self.scheme + (" (ABFT single checksum stream, Eqs. 3-6: the paper's comparison method)"
+                                         if self.scheme == "abft" else " (numerical entanglement)"),
                 "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
                 "l2": "working set ~1.9 GB per step >> 126 MB L2 (no flush needed)",
                 "step": "entangle(limbs)+prep_B+GEMM+disentangle/check(r=0)+recover(r=step mod 3)"}
@@ -173,11 +209,11 @@ class C3Gemm(Workload):
         """GEMM on plain A: (i) same tcgen05 kernel with the same L limbs,
         (ii) the narrowest native form (1 int8 limb); ms per call."""
         torch, ne = self.torch, self.ne
-        if self.algo != "tc":
+        if self.algo != "tc" or self.scheme != "entangled":
             return {}
         M, R, K = self.M, self.rows, self.K
         out = {}
-        for tag, L in (("same_kernel_L%d" % self.L, self.L), ("native_L1", 1)):
+        for tag, L in (("same_kernel_L%d" % self.L, self.L), ("native_L1", 1)):  # plain A: digit 0 = A, rest 0
             planes = torch.zeros(M * L * R * K, dtype=torch.int8, device="cuda")
             pv = planes.view(M, L, R * K)
             for m in range(M):
@@ -648,7 +684,8 @@ def run_ours(args, rank, world, local_rank):
 
     ne.lib()
     torch.cuda.set_device(local_rank)
-    W = WORKLOADS[args.workload](rank) if args.workload != "c3" else C3Gemm(rank, algo=args.algo)
+    W = WORKLOADS[args.workload](rank) if args.workload != "c3" else \
+        C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs)
     torch.cuda.synchronize()
 
     def barrier():
@@ -718,7 +755,11 @@ def run_ours(args, rank, world, local_rank):
     # correctness sentinel of the timed run: no range violation, no flagged position
     dg = ne.diag_read(W.diag)
     # recovered outputs of the last step equal the checked ones
-    rec_ok = all(bool(torch.equal(a, b)) for a, b in zip(W.drec, W.dout))
+    if getattr(W, "scheme", "entangled") == "abft":
+        r_last = (args.steps - 1) % W.M
+        rec_ok = bool(torch.equal(W.drec[r_last], W.delta[r_last]))
+    else:
+        rec_ok = all(bool(torch.equal(a, b)) for a, b in zip(W.drec, W.dout))
 
     # end-to-end through host buffers (pinned H2D inputs, D2H outputs, same stream)
     h2d, d2h = W.e2e_setup()
@@ -826,7 +867,8 @@ def run_reference(args):
     W = cls.__new__(cls)
     # the attributes oracle_sample / work_per_step / config need, without CUDA
     if args.workload == "c3":
-        W.M, W.rows, W.cols, W.K, W.seed, W.algo, W.L = 3, 4096, 4096, 4096, 2, "tc", 4
+        W.M, W.rows, W.cols, W.K, W.seed, W.algo, W.L, W.limb_bits, W.scheme = \
+            3, 4096, 4096, 4096, 2, "tc", 2, 22, "entangled"
 
         class _Cfg:
             l, k = 22, 20
@@ -888,6 +930,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--algo", default="tc", choices=["tc", "imad"])
+    ap.add_argument("--limbs", default="plan", choices=["plan", "base256"],
+                    help="c3: GEMM operand digits: cheapest exact plan (default) or balanced base 256")
+    ap.add_argument("--scheme", default="entangled", choices=["entangled", "abft"],
+                    help="c3 only: numerical entanglement (default) or the paper's ABFT comparison method")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
     args = ap.parse_args()

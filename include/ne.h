@@ -104,6 +104,12 @@ ne_status ne_certify(const ne_config* cfg, ne_op_kind op, int64_t in_bound, int6
  * value (2^l + 1) * in_bound exactly (the GEMM operand split). */
 int32_t ne_gemm_limbs_for(const ne_config* cfg, int64_t in_bound);
 
+/* The cheapest exact digit plan for the GEMM operand: returns L and sets
+ * *limb_bits = b with eps = sum_{i<L} 2^(b i) d_i, every d_i in [-128, 127].
+ * b = l, L = 2 when |c| <= 127 and l >= 8 (an entangled value is then exactly
+ * its two int8 halves c_m, c_{m-1}); else b = 8, L = ne_gemm_limbs_for(). */
+int32_t ne_gemm_limb_plan(const ne_config* cfg, int64_t in_bound, int32_t* limb_bits);
+
 /* Fill a device ne_diag with {0, INT64_MAX, 0, INT64_MAX}. */
 ne_status ne_diag_reset(ne_diag* diag, ne_stream_t stream);
 
@@ -123,12 +129,13 @@ ne_status ne_entangle(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, ne
 ne_status ne_entangle_aos(const ne_config* cfg, ne_cstreams32 c, int64_t n_total,
                           int64_t* eps_aos, ne_diag* diag, ne_stream_t stream);
 
-/* Same values, written as L balanced signed base-2^8 digit planes (the int8
- * operand of the tensor-core GEMM): planes[((m*L) + i)*n_total + n] = d_i with
- * eps = sum_i 2^(8i) d_i, d_i in [-128, 127].  A value that L digits cannot
- * represent counts as a range violation.  n_total must be a multiple of 16. */
+/* Same values, written as L balanced signed base-2^b digit planes, b =
+ * limb_bits (the int8 operand of the tensor-core GEMM):
+ * planes[((m*L) + i)*n_total + n] = d_i with eps = sum_i 2^(b i) d_i,
+ * d_i in [-128, 127].  A value that L such digits cannot represent counts as a
+ * range violation.  n_total must be a multiple of 16; 8 <= limb_bits <= 63. */
 ne_status ne_entangle_limbs(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t L,
-                            int8_t* planes, ne_diag* diag, ne_stream_t stream);
+                            int32_t limb_bits, int8_t* planes, ne_diag* diag, ne_stream_t stream);
 
 /* One stream only (the per-GPU entanglement of the one-stream-per-GPU layout,
  * P:608-611): eps_m[n] = c_m[n] + S_l{ c_prev[n] } with c_prev = c_{(m-1) mod M}.
@@ -141,8 +148,8 @@ ne_status ne_entangle_stream(const ne_config* cfg, int32_t m, const int32_t* c_m
  * planes_m[i*n_total + n] = digit i of c_m[n] + S_l{c_prev[n]}.  n_total % 16 == 0.
  * Range violations (|c_m| > hi or not representable in L digits) name m*n_total + n. */
 ne_status ne_entangle_limbs_stream(const ne_config* cfg, int32_t m, const int32_t* c_m,
-                                   const int32_t* c_prev, int64_t n_total, int32_t L, int8_t* planes_m,
-                                   ne_diag* diag, ne_stream_t stream);
+                                   const int32_t* c_prev, int64_t n_total, int32_t L, int32_t limb_bits,
+                                   int8_t* planes_m, ne_diag* diag, ne_stream_t stream);
 
 /* Footnote P:507-511: the shared operand of +/- self-entangled,
  * g_ent[n] = S_l{g[n]} + g[n]. */
@@ -186,16 +193,17 @@ ne_status ne_op_permute(const ne_config* cfg, ne_cstreams x, const int32_t* perm
 /* Integer matrix product (reading R13): C_m = A_m * B for every
  * stream m, A_m rows x K (entangled, int64), B K x cols (plain int32, shared
  * kernel g, unmodified), C_m rows x cols int64.  algo NE_GEMM_IMAD64 runs on
- * the CUDA cores; NE_GEMM_TC_I8 splits A_m into L balanced int8 limb planes
- * and B into one int8 plane and runs tcgen05.mma kind::i8 with exact int32
- * limb accumulators, recombined in int64.  ws: workspace
+ * the CUDA cores; NE_GEMM_TC_I8 splits A_m into L balanced base-2^limb_bits
+ * int8 digit planes (ne_gemm_limb_plan) and B into one int8 plane and runs
+ * tcgen05.mma kind::i8 with exact int32 limb accumulators, recombined in
+ * int64.  ws: workspace
  * of ne_gemm_workspace() bytes (TC only).  Entries of B outside [-128,127]
  * or of A_m outside the L-limb range count in diag.range_violations (TC). */
 ne_status ne_gemm_workspace(const ne_config* cfg, int64_t rows, int64_t cols, int64_t K,
                             int32_t L, size_t* bytes);
 ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int64_t rows,
-                     int64_t cols, int64_t K, ne_gemm_algo algo, int32_t L, ne_streams C,
-                     void* ws, size_t ws_bytes, ne_diag* diag, ne_stream_t stream);
+                     int64_t cols, int64_t K, ne_gemm_algo algo, int32_t L, int32_t limb_bits,
+                     ne_streams C, void* ws, size_t ws_bytes, ne_diag* diag, ne_stream_t stream);
 
 /* The tensor-core GEMM on operands already in limb form: planes from
  * ne_entangle_limbs (M*L planes of rows x K int8, K contiguous) and Bt from
@@ -203,15 +211,15 @@ ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int6
  * cols % 128 == 0, K % 128 == 0, K <= 131072 (int32 limb sums stay exact). */
 ne_status ne_gemm_prep_b(const int32_t* B, int64_t K, int64_t cols, int8_t* Bt, ne_diag* diag,
                          ne_stream_t stream);
-ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes, int32_t L,
+ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes, int32_t L, int32_t limb_bits,
                            const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams C,
                            ne_stream_t stream);
 
 /* One stream of ne_op_gemm_limbs (the per-GPU GEMM of the one-stream-per-GPU
  * layout): C_m = sum_i 2^(8i) D_{m,i} B from planes_m (L planes). */
 ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t* planes_m, int32_t L,
-                                  const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int64_t* C_m,
-                                  ne_stream_t stream);
+                                  int32_t limb_bits, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K,
+                                  int64_t* C_m, ne_stream_t stream);
 
 /* ====================================== a4-a6: disentangle, check, recover === */
 
@@ -243,6 +251,29 @@ ne_status ne_op_permute_inner_check(const ne_config* cfg, ne_cstreams x, const i
                                     const int32_t* v, int64_t vlen, int64_t block, int32_t r,
                                     ne_streams delta_out, ne_streams d_out, uint32_t* bitmap,
                                     ne_diag* diag, ne_stream_t stream);
+
+/* ====================================== comparison baseline: ABFT (NEXT-1) === */
+/* The paper's comparison method, run on the same hardware so the
+ * overhead of entanglement can be compared with ABFT's at equal fault
+ * tolerance (one faulty stream of M+1 detected, one lost stream recovered).  */
+
+/* Eq. 4: r_out[n] = sum_m c_m[n] (int32; a sum that does not fit
+ * — ABFT's extra ceil(log2 M) bits, Table I — is a range violation naming n). */
+ne_status ne_abft_encode(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t* r_out,
+                         ne_diag* diag, ne_stream_t stream);
+/* Plain int32 streams x[0..count) -> L balanced int8 digit planes
+ * planes[(s*L + i)*n_total + n] (the tensor-core operand of unentangled data;
+ * a value L digits cannot hold is a range violation).  n_total % 16 == 0. */
+ne_status ne_to_limbs(ne_cstreams32 x, int32_t count, int64_t n_total, int32_t L, int8_t* planes,
+                      ne_diag* diag, ne_stream_t stream);
+/* Eq. 6: flag[n] = (sum_m d_m[n] != e[n]) mod 2^64, bitmap/diag as
+ * ne_disentangle_check. */
+ne_status ne_abft_check(const ne_config* cfg, ne_cstreams d, const int64_t* e, int64_t n_total,
+                        uint32_t* bitmap, ne_diag* diag, ne_stream_t stream);
+/* d_r = e - sum_{m != r} d_m (d.s[r] may be NULL; any other NULL ->
+ * NE_EUNRECOVERABLE). */
+ne_status ne_abft_recover(const ne_config* cfg, ne_cstreams d, const int64_t* e, int64_t n_total,
+                          int32_t r, int64_t* d_r, ne_stream_t stream);
 
 /* ============================================== a7: fault injection (test) === */
 

@@ -68,6 +68,9 @@ def lib():
             "or_disentangle_check": (C.c_int64, [_PCFG, _P64, C.c_int64, C.c_int32, _P64, _PU8]),
             "or_recover": (C.c_int32, [_PCFG, C.POINTER(_P64), C.c_int64, C.c_int32, _P64]),
             "or_certify": (C.c_int64, [C.c_int32, C.c_int64, C.c_int64]),
+            "or_abft_encode": (None, [_PCFG, _P64, C.c_int64, _P64]),
+            "or_abft_check": (C.c_int64, [_PCFG, _P64, _P64, C.c_int64, _PU8]),
+            "or_abft_recover": (C.c_int32, [_PCFG, C.POINTER(_P64), _P64, C.c_int64, C.c_int32, _P64]),
             "or_gen_uniform": (None, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_int64, C.c_int64,
                                       C.c_int64, C.c_int64, _P64]),
             "or_gen_perm": (None, [C.c_uint64, C.c_uint32, C.c_int64, C.c_int64, C.c_int64, _P64]),
@@ -247,6 +250,31 @@ def recover(cfg: Config, delta_rows, r: int) -> np.ndarray:
     rc = lib().or_recover(C.byref(cfg), ptrs, N, int(r), _p(out))
     if rc != 0:
         raise ValueError("unrecoverable: more than one stream absent, or the absent stream is not r")
+    return out
+
+
+# ------------------------------------------------------------------ ABFT baseline (Eqs. 3-6)
+def abft_encode(cfg: Config, c) -> np.ndarray:
+    c = _i64(c)
+    out = np.empty(c.shape[1], dtype=np.int64)
+    lib().or_abft_encode(C.byref(cfg), _p(c), c.shape[1], _p(out))
+    return out
+
+
+def abft_check(cfg: Config, d, e):
+    d, e = _i64(d), _i64(e).ravel()
+    flags = np.zeros(e.size, dtype=np.uint8)
+    nf = lib().or_abft_check(C.byref(cfg), _p(d), _p(e), e.size, flags.ctypes.data_as(_PU8))
+    return flags, int(nf)
+
+
+def abft_recover(cfg: Config, d_rows, e, r: int) -> np.ndarray:
+    keep = [None if x is None else _i64(x) for x in d_rows]
+    e = _i64(e).ravel()
+    ptrs = (_P64 * cfg.M)(*[(_P64() if x is None else _p(x)) for x in keep])
+    out = np.empty(e.size, dtype=np.int64)
+    if lib().or_abft_recover(C.byref(cfg), ptrs, _p(e), e.size, int(r), _p(out)) != 0:
+        raise ValueError("unrecoverable: exactly stream r must be absent")
     return out
 
 

@@ -306,6 +306,46 @@ int32_t or_recover(const or_config* cfg, const int64_t* const* delta, int64_t N,
   return 0;
 }
 
+/* ---------------------------------------------------------------- ABFT --- */
+/* The comparison method of §II-A: one extra checksum stream. */
+
+/* Eq. 4: r_n = sum_{m=0}^{M-1} c_{m,n} */
+void or_abft_encode(const or_config* cfg, const int64_t* c, int64_t N, int64_t* r_out) {
+  for (int64_t n = 0; n < N; ++n) {
+    int64_t acc = 0;
+    for (int32_t m = 0; m < cfg->M; ++m) acc = wadd(cfg, acc, c[(int64_t)m * N + n]);
+    r_out[n] = acc;
+  }
+}
+
+/* Eq. 6: a fault in any single stream of the M+1 is flagged where
+ * sum_{m=0}^{M-1} d_{m,n} != e_n */
+int64_t or_abft_check(const or_config* cfg, const int64_t* d, const int64_t* e, int64_t N, uint8_t* flags) {
+  int64_t nflag = 0;
+  for (int64_t n = 0; n < N; ++n) {
+    int64_t acc = 0;
+    for (int32_t m = 0; m < cfg->M; ++m) acc = wadd(cfg, acc, d[(int64_t)m * N + n]);
+    int32_t f = acc != e[n];
+    if (flags) flags[n] = (uint8_t)f;
+    nflag += f;
+  }
+  return nflag;
+}
+
+/* the lost stream r = e - (sum of the remaining output streams) */
+int32_t or_abft_recover(const or_config* cfg, const int64_t* const* d, const int64_t* e, int64_t N, int32_t r,
+                        int64_t* d_r) {
+  for (int32_t m = 0; m < cfg->M; ++m)
+    if ((d[m] == NULL) != (m == r)) return -1;
+  for (int64_t n = 0; n < N; ++n) {
+    int64_t acc = e[n];
+    for (int32_t m = 0; m < cfg->M; ++m)
+      if (m != r) acc = or_wrap(cfg, (int64_t)((uint64_t)acc - (uint64_t)d[m][n]));
+    d_r[n] = acc;
+  }
+  return 0;
+}
+
 /* S:187-195 worst-case bounds */
 int64_t or_certify(int32_t op, int64_t in_bound, int64_t operand) {
   switch (op) {

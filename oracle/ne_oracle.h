@@ -80,6 +80,15 @@ int64_t or_disentangle_check(const or_config* cfg, const int64_t* delta, int64_t
 int32_t or_recover(const or_config* cfg, const int64_t* const* delta, int64_t N,
                    int32_t r, int64_t* dhat);
 
+/* ABFT single-checksum baseline (Eqs. 3-6), w-bit arithmetic:
+ * encode r_n = sum_m c_{m,n} (Eq. 4); check flags n where sum_m d_{m,n} != e_n
+ * (Eq. 6), returns the count; recover d_r = e - sum_{m != r} d_m ("subtracting
+ * the results of all the remaining output streams"). */
+void or_abft_encode(const or_config* cfg, const int64_t* c, int64_t N, int64_t* r_out);
+int64_t or_abft_check(const or_config* cfg, const int64_t* d, const int64_t* e, int64_t N, uint8_t* flags);
+int32_t or_abft_recover(const or_config* cfg, const int64_t* const* d, const int64_t* e, int64_t N, int32_t r,
+                        int64_t* d_r);
+
 /* worst-case output bound of one op: op 0 scale (|s|), 1 add
  * (operand max), 2 inner/conv/gemm (operand l1 norm), 3 permute. */
 int64_t or_certify(int32_t op, int64_t in_bound, int64_t operand);

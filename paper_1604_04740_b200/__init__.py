@@ -28,13 +28,14 @@ NE_OP_SCALE, NE_OP_ADD, NE_OP_LINEAR, NE_OP_PERMUTE = 0, 1, 2, 3
 
 # every symbol include/ne.h and include/ne_gendev.h declare (checked by tests)
 EXPORTS = (
-    "ne_config_for", "ne_dynamic_range", "ne_certify", "ne_gemm_limbs_for", "ne_diag_reset",
+    "ne_config_for", "ne_dynamic_range", "ne_certify", "ne_gemm_limbs_for", "ne_gemm_limb_plan", "ne_diag_reset",
     "ne_entangle", "ne_entangle_aos", "ne_entangle_limbs", "ne_entangle_stream", "ne_entangle_shared",
     "ne_entangle_limbs_stream", "ne_op_gemm_limbs_stream",
     "ne_op_scale", "ne_op_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
     "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
+    "ne_abft_encode", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
 )
 
 
@@ -65,14 +66,15 @@ _SIGS = {
     "ne_dynamic_range": [_PCFG, C.POINTER(_I64)],
     "ne_certify": [_PCFG, C.c_int, _I64, _I64, C.POINTER(_I64)],
     "ne_gemm_limbs_for": [_PCFG, _I64],
+    "ne_gemm_limb_plan": [_PCFG, _I64, C.POINTER(_I32)],
     "ne_diag_reset": [_VP, _VP],
     "ne_entangle": [_PCFG, Streams, _I64, Streams, _VP, _VP],
     "ne_entangle_aos": [_PCFG, Streams, _I64, _VP, _VP, _VP],
-    "ne_entangle_limbs": [_PCFG, Streams, _I64, _I32, _VP, _VP, _VP],
+    "ne_entangle_limbs": [_PCFG, Streams, _I64, _I32, _I32, _VP, _VP, _VP],
     "ne_entangle_stream": [_PCFG, _I32, _VP, _VP, _VP, _I64, _VP, _VP],
     "ne_entangle_shared": [_PCFG, _VP, _VP, _I64, _VP],
-    "ne_entangle_limbs_stream": [_PCFG, _I32, _VP, _VP, _I64, _I32, _VP, _VP, _VP],
-    "ne_op_gemm_limbs_stream": [_PCFG, _VP, _I32, _VP, _I64, _I64, _I64, _VP, _VP],
+    "ne_entangle_limbs_stream": [_PCFG, _I32, _VP, _VP, _I64, _I32, _I32, _VP, _VP, _VP],
+    "ne_op_gemm_limbs_stream": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, _VP, _VP],
     "ne_op_scale": [_PCFG, Streams, _I64, _I64, _VP, _VP],
     "ne_op_add": [_PCFG, Streams, Streams, _I64, _I32, _VP],
     "ne_op_inner": [_PCFG, Streams, _I64, _VP, _I64, _I64, Streams, _VP],
@@ -80,14 +82,18 @@ _SIGS = {
     "ne_op_conv": [_PCFG, Streams, _I64, _VP, _I32, _I32, Streams, _VP],
     "ne_op_permute": [_PCFG, Streams, _VP, _I64, Streams, _VP],
     "ne_gemm_workspace": [_PCFG, _I64, _I64, _I64, _I32, C.POINTER(_SZ)],
-    "ne_op_gemm": [_PCFG, Streams, _VP, _I64, _I64, _I64, C.c_int, _I32, Streams, _VP, _SZ, _VP, _VP],
+    "ne_op_gemm": [_PCFG, Streams, _VP, _I64, _I64, _I64, C.c_int, _I32, _I32, Streams, _VP, _SZ, _VP, _VP],
     "ne_gemm_prep_b": [_VP, _I64, _I64, _VP, _VP, _VP],
-    "ne_op_gemm_limbs": [_PCFG, _VP, _I32, _VP, _I64, _I64, _I64, Streams, _VP],
+    "ne_op_gemm_limbs": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _VP],
     "ne_disentangle_check": [_PCFG, Streams, _I64, _I32, Streams, _VP, _VP, _VP],
     "ne_recover": [_PCFG, Streams, _I64, _I32, Streams, _VP],
     "ne_op_permute_inner_check": [_PCFG, Streams, _VP, _I32, _VP, _I64, _VP, _I64, _I64, _I32,
                                   Streams, Streams, _VP, _VP, _VP],
     "ne_inject": [_VP, _I64, _U64, _VP],
+    "ne_abft_encode": [_PCFG, Streams, _I64, _VP, _VP, _VP],
+    "ne_to_limbs": [Streams, _I32, _I64, _I32, _VP, _VP, _VP],
+    "ne_abft_check": [_PCFG, Streams, _VP, _I64, _VP, _VP, _VP],
+    "ne_abft_recover": [_PCFG, Streams, _VP, _I64, _I32, _VP, _VP],
     "ne_inject_sweep": [_PCFG, Streams, _I64, _I32, _VP, _VP, _VP],
     "ne_gen_uniform_i32": [_U64, C.c_uint32, C.c_uint32, _I64, _I64, _I64, _I64, _VP, _VP],
     "ne_gen_perm_i32": [_U64, C.c_uint32, _I64, _VP, _VP],
@@ -166,6 +172,13 @@ def ne_gemm_limbs_for(cfg: Config, in_bound: int) -> int:
     return int(lib().ne_gemm_limbs_for(C.byref(cfg), in_bound))
 
 
+def ne_gemm_limb_plan(cfg: Config, in_bound: int) -> tuple[int, int]:
+    """(L, limb_bits): the cheapest exact int8 digit plan of the GEMM operand."""
+    b = C.c_int32()
+    L = int(lib().ne_gemm_limb_plan(C.byref(cfg), in_bound, C.byref(b)))
+    return L, b.value
+
+
 def diag_new() -> torch.Tensor:
     d = torch.empty(4, dtype=torch.int64, device="cuda")
     ne_diag_reset(d)
@@ -195,8 +208,8 @@ def ne_entangle_aos(cfg: Config, c, eps_aos: torch.Tensor, diag=None) -> None:
           _ptr(eps_aos, torch.int64), _ptr(diag, torch.int64), _stream())
 
 
-def ne_entangle_limbs(cfg: Config, c, L: int, planes: torch.Tensor, diag=None) -> None:
-    _call("ne_entangle_limbs", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), L,
+def ne_entangle_limbs(cfg: Config, c, L: int, planes: torch.Tensor, diag=None, limb_bits: int = 8) -> None:
+    _call("ne_entangle_limbs", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), L, limb_bits,
           _ptr(planes, torch.int8), _ptr(diag, torch.int64), _stream())
 
 
@@ -205,14 +218,16 @@ def ne_entangle_stream(cfg: Config, m: int, c_m, c_prev, eps_m, diag=None) -> No
           _ptr(eps_m, torch.int64), c_m.numel(), _ptr(diag, torch.int64), _stream())
 
 
-def ne_entangle_limbs_stream(cfg: Config, m: int, c_m, c_prev, L: int, planes_m, diag=None) -> None:
+def ne_entangle_limbs_stream(cfg: Config, m: int, c_m, c_prev, L: int, planes_m, diag=None,
+                             limb_bits: int = 8) -> None:
     _call("ne_entangle_limbs_stream", C.byref(cfg), m, _ptr(c_m, torch.int32), _ptr(c_prev, torch.int32),
-          c_m.numel(), L, _ptr(planes_m, torch.int8), _ptr(diag, torch.int64), _stream())
+          c_m.numel(), L, limb_bits, _ptr(planes_m, torch.int8), _ptr(diag, torch.int64), _stream())
 
 
-def ne_op_gemm_limbs_stream(cfg: Config, planes_m, L: int, Bt, rows: int, cols: int, K: int, C_m) -> None:
-    _call("ne_op_gemm_limbs_stream", C.byref(cfg), _ptr(planes_m, torch.int8), L, _ptr(Bt, torch.int8), rows, cols,
-          K, _ptr(C_m, torch.int64), _stream())
+def ne_op_gemm_limbs_stream(cfg: Config, planes_m, L: int, Bt, rows: int, cols: int, K: int, C_m,
+                            limb_bits: int = 8) -> None:
+    _call("ne_op_gemm_limbs_stream", C.byref(cfg), _ptr(planes_m, torch.int8), L, limb_bits, _ptr(Bt, torch.int8),
+          rows, cols, K, _ptr(C_m, torch.int64), _stream())
 
 
 def ne_entangle_shared(cfg: Config, g: torch.Tensor, g_ent: torch.Tensor) -> None:
@@ -258,8 +273,8 @@ def ne_gemm_workspace(cfg: Config, rows: int, cols: int, K: int, L: int) -> int:
 
 
 def ne_op_gemm(cfg: Config, A, B: torch.Tensor, rows: int, cols: int, K: int, out, algo: int = NE_GEMM_TC_I8,
-               L: int = 4, ws: torch.Tensor | None = None, diag=None) -> None:
-    _call("ne_op_gemm", C.byref(cfg), _streams(A, torch.int64), _ptr(B, torch.int32), rows, cols, K, algo, L,
+               L: int = 4, ws: torch.Tensor | None = None, diag=None, limb_bits: int = 8) -> None:
+    _call("ne_op_gemm", C.byref(cfg), _streams(A, torch.int64), _ptr(B, torch.int32), rows, cols, K, algo, L, limb_bits,
           _streams(out, torch.int64), _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
           _ptr(diag, torch.int64), _stream())
 
@@ -270,9 +285,9 @@ def ne_gemm_prep_b(B: torch.Tensor, K: int, cols: int, Bt: torch.Tensor, diag=No
 
 
 def ne_op_gemm_limbs(cfg: Config, planes: torch.Tensor, L: int, Bt: torch.Tensor, rows: int, cols: int, K: int,
-                     out) -> None:
-    _call("ne_op_gemm_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, _ptr(Bt, torch.int8), rows, cols, K,
-          _streams(out, torch.int64), _stream())
+                     out, limb_bits: int = 8) -> None:
+    _call("ne_op_gemm_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, limb_bits, _ptr(Bt, torch.int8), rows, cols,
+          K, _streams(out, torch.int64), _stream())
 
 
 # ------------------------------------------------------------------ a4-a7
@@ -296,6 +311,27 @@ def ne_op_permute_inner_check(cfg: Config, v: torch.Tensor, block: int, r: int, 
     _call("ne_op_permute_inner_check", C.byref(cfg), xs, _ptr(x_aos, torch.int64), int(x_aos is not None),
           _ptr(perm, torch.int32), n, _ptr(v, torch.int32), v.numel(), block, r, do, _streams(d_out, torch.int64),
           _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _stream())
+
+
+# ------------------------------------------------------------------ ABFT comparison baseline (Eqs. 3-6)
+def ne_abft_encode(cfg: Config, c, r_out: torch.Tensor, diag=None) -> None:
+    _call("ne_abft_encode", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), _ptr(r_out, torch.int32),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_to_limbs(x, L: int, planes: torch.Tensor, diag=None) -> None:
+    _call("ne_to_limbs", _streams(x, torch.int32), len(x), x[0].numel(), L, _ptr(planes, torch.int8),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_abft_check(cfg: Config, d, e: torch.Tensor, bitmap=None, diag=None) -> None:
+    _call("ne_abft_check", C.byref(cfg), _streams(d, torch.int64), _ptr(e, torch.int64), e.numel(),
+          _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _stream())
+
+
+def ne_abft_recover(cfg: Config, d, e: torch.Tensor, r: int, d_r: torch.Tensor) -> None:
+    _call("ne_abft_recover", C.byref(cfg), _streams(d, torch.int64), _ptr(e, torch.int64), e.numel(), r,
+          _ptr(d_r, torch.int64), _stream())
 
 
 def ne_inject(x: torch.Tensor, idx: int, mask: int) -> None:

@@ -10,13 +10,13 @@ namespace ne {
 
 void launch_gemm_imad64(int M, const ne_cstreams& A, const int32_t* B, const ne_streams& C, int64_t rows,
                         int64_t cols, int64_t K, cudaStream_t s);
-ne_status launch_gemm_tc(int M, int L, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s);
 
 // int64 entangled A_m -> L balanced int8 digit planes, planes[(m*L+i)*n + idx]
 template <int MT>
 __global__ void __launch_bounds__(kThreads)
-k_split_limbs(const __grid_constant__ ne_cstreams A, int M_rt, int64_t n, int L, int8_t* __restrict__ planes,
+k_split_limbs(const __grid_constant__ ne_cstreams A, int M_rt, int64_t n, int L, int b, int8_t* __restrict__ planes,
               ne_diag* __restrict__ diag) {
   const int M = MT > 0 ? MT : M_rt;
   int bad = 0;
@@ -28,20 +28,19 @@ k_split_limbs(const __grid_constant__ ne_cstreams A, int M_rt, int64_t n, int L,
       if (MT == 0 && m >= M) break;
       const longlong2* p = reinterpret_cast<const longlong2*>(A.s[m] + 4 * q);
       longlong2 u = __ldcs(p), w = __ldcs(p + 1);
-      int64_t x[4] = {u.x, u.y, w.x, w.y};
-      for (int j = 0; j < L; ++j) {
-        uint32_t packed = 0;
+      const int64_t x[4] = {u.x, u.y, w.x, w.y};
+      uint32_t packed[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      bool ok[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          int8_t d = (int8_t)(x[i] & 0xff);
-          x[i] = (x[i] - d) >> 8;
-          packed |= (uint32_t)(uint8_t)d << (8 * i);
-        }
-        *reinterpret_cast<uint32_t*>(planes + ((int64_t)m * L + j) * n + 4 * q) = packed;
+      for (int i = 0; i < 4; ++i) {
+        int8_t d[8];
+        ok[i] = digits_b(x[i], b, L, d);
+        for (int j = 0; j < L; ++j) packed[j] |= (uint32_t)(uint8_t)d[j] << (8 * i);
       }
+      for (int j = 0; j < L; ++j) *reinterpret_cast<uint32_t*>(planes + ((int64_t)m * L + j) * n + 4 * q) = packed[j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (x[i] != 0) {
+        if (!ok[i]) {
           ++bad;
           long long idx = (long long)m * n + 4 * q + i;
           first = idx < first ? idx : first;
@@ -123,33 +122,36 @@ extern "C" ne_status ne_gemm_prep_b(const int32_t* B, int64_t K, int64_t cols, i
   return launch_status();
 }
 
-extern "C" ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes, int32_t L, const int8_t* Bt,
-                                      int64_t rows, int64_t cols, int64_t K, ne_streams C, ne_stream_t stream) {
+extern "C" ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes, int32_t L, int32_t limb_bits,
+                                      const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams C,
+                                      ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);
   if (st != NE_OK) return st;
-  if (!planes || !Bt || L < 1 || L > 4 || !aligned16(planes) || !aligned16(Bt)) return NE_EINVAL;
+  if (!planes || !Bt || L < 1 || L > 4 || limb_bits < 8 || limb_bits > 63 || !aligned16(planes) || !aligned16(Bt))
+    return NE_EINVAL;
   for (int m = 0; m < cfg->M; ++m)
     if (!C.s[m] || !aligned16(C.s[m])) return NE_EINVAL;
   if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
-  return launch_gemm_tc(cfg->M, L, planes, Bt, rows, cols, K, C, cs(stream));
+  return launch_gemm_tc(cfg->M, L, limb_bits, planes, Bt, rows, cols, K, C, cs(stream));
 }
 
 extern "C" ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t* planes_m, int32_t L,
-                                             const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int64_t* C_m,
-                                             ne_stream_t stream) {
+                                             int32_t limb_bits, const int8_t* Bt, int64_t rows, int64_t cols,
+                                             int64_t K, int64_t* C_m, ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);
   if (st != NE_OK) return st;
-  if (!planes_m || !Bt || !C_m || L < 1 || L > 4 || !aligned16(planes_m) || !aligned16(Bt) || !aligned16(C_m))
+  if (!planes_m || !Bt || !C_m || L < 1 || L > 4 || limb_bits < 8 || limb_bits > 63 || !aligned16(planes_m) ||
+      !aligned16(Bt) || !aligned16(C_m))
     return NE_EINVAL;
   if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
   ne_streams C{};
   C.s[0] = C_m;
-  return launch_gemm_tc(1, L, planes_m, Bt, rows, cols, K, C, cs(stream));
+  return launch_gemm_tc(1, L, limb_bits, planes_m, Bt, rows, cols, K, C, cs(stream));
 }
 
 extern "C" ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int64_t rows, int64_t cols,
-                                int64_t K, ne_gemm_algo algo, int32_t L, ne_streams C, void* ws, size_t ws_bytes,
-                                ne_diag* diag, ne_stream_t stream) {
+                                int64_t K, ne_gemm_algo algo, int32_t L, int32_t limb_bits, ne_streams C, void* ws,
+                                size_t ws_bytes, ne_diag* diag, ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);
   if (st != NE_OK) return st;
   const int M = cfg->M;
@@ -164,6 +166,7 @@ extern "C" ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32
   }
   if (algo != NE_GEMM_TC_I8) return NE_EINVAL;
   if (!tc_shape_ok(rows, cols, K) || L < 1 || L > 4) return NE_ENOTSUP;
+  if (limb_bits < 8 || limb_bits > 63) return NE_EINVAL;
   size_t need = 0;
   ne_gemm_workspace(cfg, rows, cols, K, L, &need);
   if (!ws || ws_bytes < need || !aligned16(ws)) return NE_EINVAL;
@@ -172,12 +175,12 @@ extern "C" ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32
   const int64_t n = rows * K;
   const int grid = grid_for(n / 4, kThreads);
   switch (M) {
-    case 3: k_split_limbs<3><<<grid, kThreads, 0, s>>>(A, 3, n, L, planes, diag); break;
-    case 4: k_split_limbs<4><<<grid, kThreads, 0, s>>>(A, 4, n, L, planes, diag); break;
-    case 8: k_split_limbs<8><<<grid, kThreads, 0, s>>>(A, 8, n, L, planes, diag); break;
-    default: k_split_limbs<0><<<grid, kThreads, 0, s>>>(A, M, n, L, planes, diag); break;
+    case 3: k_split_limbs<3><<<grid, kThreads, 0, s>>>(A, 3, n, L, limb_bits, planes, diag); break;
+    case 4: k_split_limbs<4><<<grid, kThreads, 0, s>>>(A, 4, n, L, limb_bits, planes, diag); break;
+    case 8: k_split_limbs<8><<<grid, kThreads, 0, s>>>(A, 8, n, L, limb_bits, planes, diag); break;
+    default: k_split_limbs<0><<<grid, kThreads, 0, s>>>(A, M, n, L, limb_bits, planes, diag); break;
   }
   if ((st = launch_status()) != NE_OK) return st;
   if ((st = ne_gemm_prep_b(B, K, cols, Bt, diag, stream)) != NE_OK) return st;
-  return launch_gemm_tc(M, L, planes, Bt, rows, cols, K, C, s);
+  return launch_gemm_tc(M, L, limb_bits, planes, Bt, rows, cols, K, C, s);
 }

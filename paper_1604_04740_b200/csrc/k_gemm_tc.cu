@@ -8,7 +8,9 @@
 //     C_m = sum_i 2^(8i) (D_{m,i} B),
 // every D_{m,i} B is an int8 x int8 -> int32 tensor-core product that is exact
 // while K * 128 * 128 < 2^31 (K <= 131072), and the recombination is done in
-// int64 in the epilogue (wrap mod 2^64, exact for certified results).
+// int64 in the epilogue (wrap mod 2^64, exact for certified results).  The
+// digit base 2^b is a launch parameter: b = 8 (any operand) or b = l (an
+// entangled operand c_m + 2^l c_{m-1} whose halves fit int8: 2 limbs).
 //
 // A CTA computes 128 x BN tiles of one stream at a time: the L limb
 // accumulators live side by side in TMEM (L * BN <= 512 columns).  Roles:
@@ -173,7 +175,7 @@ constexpr int kThreadsP = 128 + 32 * kEpiWarps;  // warps 0-3: roles, 4-11: epil
 template <int L, int BN, int STAGES, int SW, int CL>
 __global__ void __launch_bounds__(kThreadsP, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-          const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M) {
+          const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   constexpr int BK = CF::BK;
   static_assert(L * BN <= 512, "TMEM holds 512 columns");
@@ -311,8 +313,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
           uint64_t a0 = 0, a1 = 0;
 #pragma unroll
           for (int i = 0; i < L; ++i) {
-            a0 += (uint64_t)(int64_t)(int32_t)v[i][2 * k] << (8 * i);
-            a1 += (uint64_t)(int64_t)(int32_t)v[i][2 * k + 1] << (8 * i);
+            a0 += (uint64_t)(int64_t)(int32_t)v[i][2 * k] << (limb_bits * i);
+            a1 += (uint64_t)(int64_t)(int32_t)v[i][2 * k + 1] << (limb_bits * i);
           }
           *reinterpret_cast<ulonglong2*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) = make_ulonglong2(a0, a1);
         }
@@ -390,7 +392,7 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
 
 template <int L, int BN, int STAGES, int SW, int CL>
 static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
-                     const ne_streams& C, cudaStream_t s) {
+                     int limb_bits, const ne_streams& C, cudaStream_t s) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   if (cols % (BN * CL) != 0 || K % CF::BK != 0) return NE_ENOTSUP;
   CUtensorMap ma, mb;
@@ -418,7 +420,7 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M) != cudaSuccess) return NE_ECUDA;
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits) != cudaSuccess) return NE_ECUDA;
   return launch_status();
 }
 
@@ -428,24 +430,24 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
 // 64-byte K stages (64B swizzle) give 4-6 pipeline stages in ~200 KB of smem;
 // clusters of 2 along N multicast the limb tiles (A read once per pair)
 // whenever the column-tile count is even.
-ne_status launch_gemm_tc(int M, int L, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s) {
   const bool pair128 = cols % 256 == 0, pair256 = cols % 512 == 0;
   switch (L) {
     case 1:
-      if (pair256) return tc::run<1, 256, 6, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
-      if (cols % 256 == 0) return tc::run<1, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
-      return tc::run<1, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      if (pair256) return tc::run<1, 256, 6, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
+      if (cols % 256 == 0) return tc::run<1, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
+      return tc::run<1, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
     case 2:
-      if (pair256) return tc::run<2, 256, 5, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
-      if (cols % 256 == 0) return tc::run<2, 256, 5, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
-      return tc::run<2, 128, 6, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      if (pair256) return tc::run<2, 256, 5, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
+      if (cols % 256 == 0) return tc::run<2, 256, 5, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
+      return tc::run<2, 128, 6, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
     case 3:
-      if (pair128) return tc::run<3, 128, 5, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
-      return tc::run<3, 128, 5, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      if (pair128) return tc::run<3, 128, 5, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
+      return tc::run<3, 128, 5, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
     case 4:
-      if (pair128) return tc::run<4, 128, 4, 64, 2>(planes, Bt, rows, cols, K, M, C, s);
-      return tc::run<4, 128, 4, 64, 1>(planes, Bt, rows, cols, K, M, C, s);
+      if (pair128) return tc::run<4, 128, 4, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
+      return tc::run<4, 128, 4, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
     default: return NE_ENOTSUP;
   }
 }

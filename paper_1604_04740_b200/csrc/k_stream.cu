@@ -203,37 +203,90 @@ k_entangle_limbs(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
+// Entangle into L digit planes of a general base 2^b (b != 8), 4 positions per
+// thread, all M streams loaded first; digits via digits_b.
+template <int MT, int L>
+__global__ void __launch_bounds__(kThreads)
+k_entangle_digits(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n, int b,
+                  int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  int bad = 0;
+  long long first = LLONG_MAX;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n / 4; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 4 * v;
+    int4 q[MA];
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) q[m] = __ldcs(reinterpret_cast<const int4*>(c.s[m] + n0));
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      const int4 cur = q[m], prv = q[m == 0 ? M - 1 : m - 1];
+      const int32_t cc[4] = {cur.x, cur.y, cur.z, cur.w}, pp[4] = {prv.x, prv.y, prv.z, prv.w};
+      uint32_t w[L];
+#pragma unroll
+      for (int j = 0; j < L; ++j) w[j] = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t ci = cc[i];
+        const int64_t x = (int64_t)((uint64_t)ci + ((uint64_t)(int64_t)pp[i] << l));
+        int8_t d[L];
+        const bool ok = digits_b(x, b, L, d);
+        if (ci > hi || ci < -hi || !ok) {
+          ++bad;
+          const long long idx = (long long)m * n + n0 + i;
+          first = idx < first ? idx : first;
+        }
+#pragma unroll
+        for (int j = 0; j < L; ++j) w[j] |= (uint32_t)(uint8_t)d[j] << (8 * i);
+      }
+#pragma unroll
+      for (int j = 0; j < L; ++j)
+        __stcs(reinterpret_cast<unsigned int*>(planes + ((int64_t)m * L + j) * n + n0), w[j]);
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
 // one stream into L digit planes (same digit trick as k_entangle_limbs)
 template <int L>
 __global__ void __launch_bounds__(kThreads)
 k_entangle_limbs_stream(const int32_t* __restrict__ cm, const int32_t* __restrict__ cp, int m, int l, int64_t hi,
-                        int64_t n, int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
+                        int64_t n, int b, int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
   constexpr uint64_t bias = 0x8080808080808080ull >> (64 - 8 * L);
   constexpr uint64_t span = L == 8 ? 0 : (1ull << (8 * L));
   int bad = 0;
   long long first = LLONG_MAX;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n / 4; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n0 = 4 * v;
-    const int4 a = __ldcs(reinterpret_cast<const int4*>(cm + n0)), b = __ldcs(reinterpret_cast<const int4*>(cp + n0));
-    const int32_t cc[4] = {a.x, a.y, a.z, a.w}, pp[4] = {b.x, b.y, b.z, b.w};
-    uint64_t y[4];
+    const int4 a = __ldcs(reinterpret_cast<const int4*>(cm + n0)), bq = __ldcs(reinterpret_cast<const int4*>(cp + n0));
+    const int32_t cc[4] = {a.x, a.y, a.z, a.w}, pp[4] = {bq.x, bq.y, bq.z, bq.w};
+    uint32_t w[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) w[j] = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t ci = cc[i];
-      y[i] = (uint64_t)ci + ((uint64_t)(int64_t)pp[i] << l) + bias;
-      if (ci > hi || ci < -hi || (L < 8 && y[i] >= span)) {
+      const uint64_t x = (uint64_t)ci + ((uint64_t)(int64_t)pp[i] << l);
+      bool ok;
+      if (b == 8) {
+        const uint64_t y = x + bias;
+        ok = !(L < 8 && y >= span);
+#pragma unroll
+        for (int j = 0; j < L; ++j) w[j] |= (uint32_t)(((y >> (8 * j)) & 0xff) ^ 0x80) << (8 * i);
+      } else {
+        int8_t d[L];
+        ok = digits_b((int64_t)x, b, L, d);
+#pragma unroll
+        for (int j = 0; j < L; ++j) w[j] |= (uint32_t)(uint8_t)d[j] << (8 * i);
+      }
+      if (ci > hi || ci < -hi || !ok) {
         ++bad;
         const long long idx = (long long)m * n + n0 + i;
         first = idx < first ? idx : first;
       }
     }
 #pragma unroll
-    for (int j = 0; j < L; ++j) {
-      uint32_t w = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) w |= (uint32_t)((y[i] >> (8 * j)) & 0xff) << (8 * i);
-      __stcs(reinterpret_cast<unsigned int*>(planes + (int64_t)j * n + n0), w ^ 0x80808080u);
-    }
+    for (int j = 0; j < L; ++j) __stcs(reinterpret_cast<unsigned int*>(planes + (int64_t)j * n + n0), w[j]);
   }
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
@@ -449,13 +502,38 @@ extern "C" ne_status ne_entangle_aos(const ne_config* cfg, ne_cstreams32 c, int6
 }
 
 extern "C" ne_status ne_entangle_limbs(const ne_config* cfg, ne_cstreams32 c, int64_t n_total,
-                                       int32_t L, int8_t* planes, ne_diag* diag, ne_stream_t stream) {
+                                       int32_t L, int32_t limb_bits, int8_t* planes, ne_diag* diag,
+                                       ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);
   if (st != NE_OK) return st;
   if (n_total == 0) return NE_OK;
-  if (n_total < 0 || n_total % 16 != 0 || L < 1 || L > 8 || !streams_ok32(c, cfg->M) || !planes ||
-      !aligned16(planes))
+  if (n_total < 0 || n_total % 16 != 0 || L < 1 || L > 8 || limb_bits < 8 || limb_bits > 63 ||
+      !streams_ok32(c, cfg->M) || !planes || !aligned16(planes))
     return NE_EINVAL;
+  if (limb_bits != 8) {
+    if (L > 4) return NE_EINVAL;  // base-2^b digit planes: L <= 4
+    const int grid = grid_for(n_total / 4, kThreads);
+    cudaStream_t s = cs(stream);
+    const int64_t hi = range_hi(cfg);
+#define NE_DIG(MV, LV) k_entangle_digits<MV, LV><<<grid, kThreads, 0, s>>>(c, cfg->M, cfg->l, hi, n_total, limb_bits, planes, diag)
+#define NE_DIG_L(MV)                                                                   \
+  switch (L) {                                                                         \
+    case 1: NE_DIG(MV, 1); break;                                                      \
+    case 2: NE_DIG(MV, 2); break;                                                      \
+    case 3: NE_DIG(MV, 3); break;                                                      \
+    case 4: NE_DIG(MV, 4); break;                                                      \
+    default: NE_DIG(MV, 4); break;                                                     \
+  }
+    switch (cfg->M) {
+      case 3: NE_DIG_L(3); break;
+      case 4: NE_DIG_L(4); break;
+      case 8: NE_DIG_L(8); break;
+      default: NE_DIG_L(0); break;
+    }
+#undef NE_DIG_L
+#undef NE_DIG
+    return launch_status();
+  }
   const int64_t hi = range_hi(cfg);
   const int grid = grid_for(n_total / 4, kThreads);
   cudaStream_t s = cs(stream);
@@ -497,24 +575,24 @@ extern "C" ne_status ne_entangle_stream(const ne_config* cfg, int32_t m, const i
 }
 
 extern "C" ne_status ne_entangle_limbs_stream(const ne_config* cfg, int32_t m, const int32_t* c_m,
-                                              const int32_t* c_prev, int64_t n_total, int32_t L, int8_t* planes_m,
-                                              ne_diag* diag, ne_stream_t stream) {
+                                              const int32_t* c_prev, int64_t n_total, int32_t L, int32_t limb_bits,
+                                              int8_t* planes_m, ne_diag* diag, ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);
   if (st != NE_OK) return st;
   if (m < 0 || m >= cfg->M) return NE_EINDEX;
   if (n_total == 0) return NE_OK;
-  if (n_total < 0 || n_total % 16 != 0 || L < 1 || L > 8 || !c_m || !c_prev || !planes_m || !aligned16(c_m) ||
-      !aligned16(c_prev) || !aligned16(planes_m))
+  if (n_total < 0 || n_total % 16 != 0 || L < 1 || L > 8 || limb_bits < 8 || limb_bits > 63 || !c_m || !c_prev ||
+      !planes_m || !aligned16(c_m) || !aligned16(c_prev) || !aligned16(planes_m))
     return NE_EINVAL;
   const int grid = grid_for(n_total / 4, kThreads);
   const int64_t hi = range_hi(cfg);
   cudaStream_t s = cs(stream);
   switch (L) {
-    case 1: k_entangle_limbs_stream<1><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
-    case 2: k_entangle_limbs_stream<2><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
-    case 3: k_entangle_limbs_stream<3><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
-    case 4: k_entangle_limbs_stream<4><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
-    default: k_entangle_limbs_stream<8><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, planes_m, diag); break;
+    case 1: k_entangle_limbs_stream<1><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, limb_bits, planes_m, diag); break;
+    case 2: k_entangle_limbs_stream<2><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, limb_bits, planes_m, diag); break;
+    case 3: k_entangle_limbs_stream<3><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, limb_bits, planes_m, diag); break;
+    case 4: k_entangle_limbs_stream<4><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, limb_bits, planes_m, diag); break;
+    default: k_entangle_limbs_stream<8><<<grid, kThreads, 0, s>>>(c_m, c_prev, m, cfg->l, hi, n_total, limb_bits, planes_m, diag); break;
   }
   return launch_status();
 }

@@ -132,6 +132,20 @@ extern "C" int32_t ne_gemm_limbs_for(const ne_config* cfg, int64_t in_bound) {
   return 8;
 }
 
+// Cheapest exact digit plan for the tensor-core GEMM operand:
+// an entangled value c_m + 2^l c_{m-1} with |c| <= 127 and l >= 8 is exactly
+// two int8 digits in base 2^l; otherwise balanced base-256 digits.
+extern "C" int32_t ne_gemm_limb_plan(const ne_config* cfg, int64_t in_bound, int32_t* limb_bits) {
+  if (validate_cfg(cfg) != NE_OK || in_bound < 0 || !limb_bits) return -1;
+  const int32_t L8 = ne_gemm_limbs_for(cfg, in_bound);
+  if (in_bound <= 127 && cfg->l >= 8 && cfg->l <= 63 && L8 > 2) {
+    *limb_bits = cfg->l;
+    return 2;
+  }
+  *limb_bits = 8;
+  return L8;
+}
+
 extern "C" ne_status ne_diag_reset(ne_diag* diag, ne_stream_t stream) {
   if (!diag) return NE_EINVAL;
   k_diag_reset<<<1, 1, 0, cs(stream)>>>(diag);

@@ -79,6 +79,23 @@ __device__ __forceinline__ bool disentangle_rot(const int64_t* e, int M_rt, int 
   return (i128)e[0] != dr + shl128((i128)dp, l);
 }
 
+// Balanced signed base-2^b digits of x, each required to fit int8:
+//   d_j = sext_b(x_j) (low b bits, sign-extended), x_{j+1} = (x_j - d_j) >> b,
+// exact (x = sum_j d_j 2^(b j)) iff every |d_j| fits int8 and x_L == 0.
+// Returns false when x is not representable that way.  (b = 8 is the
+// ordinary base-256 split; b = l splits an entangled value c_m + 2^l c_{m-1}
+// with |c| < 2^7 into its two int8 halves.)
+__device__ __forceinline__ bool digits_b(int64_t x, int b, int L, int8_t* d) {
+  bool ok = true;
+  for (int j = 0; j < L; ++j) {
+    const int64_t dj = (int64_t)((uint64_t)x << (64 - b)) >> (64 - b);
+    ok &= (dj >= -128 && dj <= 127);
+    d[j] = (int8_t)dj;
+    x = (x - dj) >> b;
+  }
+  return ok && x == 0;
+}
+
 // warp-aggregated diagnostics: count + min index, one atomic per warp
 __device__ __forceinline__ void diag_add(unsigned long long* count, long long* first, int local_count,
                                          long long local_first) {

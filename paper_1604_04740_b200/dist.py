@@ -58,10 +58,20 @@ class GpuBackend:
 
         self.ne = ne
         self.cfg = ne.ne_config_for(M)
-        self.L = ne.ne_gemm_limbs_for(self.cfg, bound)
+        self.L, self.limb_bits = ne.ne_gemm_limb_plan(self.cfg, bound)
         self.diag = ne.diag_new()
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.marks = []
+        self._bufs = {}
+
+    def _buf(self, key, n, dtype):
+        """Step buffers are allocated once and reused (results of a step stay
+        valid until the next step that uses the same buffer)."""
+        t = self._bufs.get(key)
+        if t is None or t.numel() != n or t.dtype != dtype:
+            t = torch.empty(n, dtype=dtype, device=self.device)
+            self._bufs[key] = t
+        return t
 
     def gen(self, seed, tag, stream, lo, hi, n):
         out = torch.empty(n, dtype=torch.int32, device=self.device)
@@ -69,27 +79,28 @@ class GpuBackend:
         return out
 
     def prep_b(self, B, K, cols):
-        Bt = torch.empty(cols * K, dtype=torch.int8, device=self.device)
+        Bt = self._buf("Bt", cols * K, torch.int8)
         self.ne.ne_gemm_prep_b(B, K, cols, Bt, self.diag)
         return Bt
 
     def entangled_gemm(self, m, A_m, A_prev, Bt, rows, cols, K):
-        planes = torch.empty(self.L * rows * K, dtype=torch.int8, device=self.device)
-        self.ne.ne_entangle_limbs_stream(self.cfg, m, A_m, A_prev, self.L, planes, self.diag)
-        out = torch.empty(rows * cols, dtype=torch.int64, device=self.device)
-        self.ne.ne_op_gemm_limbs_stream(self.cfg, planes, self.L, Bt, rows, cols, K, out)
+        planes = self._buf("planes", self.L * rows * K, torch.int8)  # stream order: reused per stream
+        self.ne.ne_entangle_limbs_stream(self.cfg, m, A_m, A_prev, self.L, planes, self.diag, self.limb_bits)
+        out = self._buf(("delta", m), rows * cols, torch.int64)
+        self.ne.ne_op_gemm_limbs_stream(self.cfg, planes, self.L, Bt, rows, cols, K, out, self.limb_bits)
         return out
 
     def check(self, deltas: Sequence[torch.Tensor], r: int):
         n = deltas[0].numel()
-        out = [torch.empty(n, dtype=torch.int64, device=self.device) for _ in deltas]
-        d = self.ne.diag_new()
+        out = [self._buf(("chk", i), n, torch.int64) for i in range(len(deltas))]
+        d = self._buf("diag", 4, torch.int64)
+        self.ne.ne_diag_reset(d)
         self.ne.ne_disentangle_check(self.cfg, list(deltas), r, out, None, d)
         return out, int(self.ne.diag_read(d)["fault_positions"])
 
     def recover(self, deltas: Sequence[torch.Tensor | None], r: int):
         n = next(t for t in deltas if t is not None).numel()
-        out = [torch.empty(n, dtype=torch.int64, device=self.device) for _ in deltas]
+        out = [self._buf(("rec", i), n, torch.int64) for i in range(len(deltas))]
         self.ne.ne_recover(self.cfg, list(deltas), r, out)
         return out
 

@@ -97,3 +97,13 @@ def test_no_cpu_fallback():
     cfg = ne.ne_config_for(3)
     with pytest.raises((RuntimeError, ValueError)):
         ne.ne_op_scale(cfg, [torch.zeros(4, dtype=torch.int64)] * 3, 2)
+
+
+def test_gemm_limb_plan():
+    """Base 2^l, two int8 digits, whenever |c| <= 127 (the digits are then the
+    plain halves c_m, c_{m-1} of the entangled value); else base 256."""
+    assert ne.ne_gemm_limb_plan(ne.ne_config_for(3), 64) == (2, 22)
+    assert ne.ne_gemm_limb_plan(ne.ne_config_for(3), 127) == (2, 22)
+    assert ne.ne_gemm_limb_plan(ne.ne_config_for(3), 128) == (4, 8)
+    assert ne.ne_gemm_limb_plan(ne.ne_config_for(8), 32) == (2, 8)
+    assert ne.ne_gemm_limb_plan(ne.ne_config_for(4), 1000) == (4, 8)

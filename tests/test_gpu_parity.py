@@ -576,3 +576,112 @@ def test_c5_full_size_single_gpu_sampled(O):
         plain = O.op_gemm(O.config_for(M, 64), Arow.reshape(M, 1, K), Bs).reshape(M, -1)
         got = np.stack([d[m][row * cols + cols_s].cpu().numpy() for m in range(M)])
         assert (got == plain).all()
+
+
+# ------------------------------------------------------------------ ABFT comparison baseline (NEXT-1)
+@pytest.mark.parametrize("M", [3, 4, 8])
+@pytest.mark.parametrize("N", [16, 4096 + 16])
+def test_abft_encode_check_recover(O, M, N):
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    rng = np.random.default_rng(M + N)
+    c = rng.integers(-2 ** 20, 2 ** 20, size=(M, N))
+    r = torch.empty(N, dtype=torch.int32, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_abft_encode(cfg, to_streams(c), r, diag)
+    assert (r.cpu().numpy() == O.abft_encode(ocfg, c)).all()
+    assert ne.diag_read(diag)["range_violations"] == 0
+    big = np.full((M, N), 2 ** 30)  # the checksum's extra bits overflow int32 -> named range violation
+    ne.ne_abft_encode(cfg, to_streams(big), r, diag)
+    assert ne.diag_read(diag)["range_violations"] == N and ne.diag_read(diag)["first_bad"] == 0
+    d = rng.integers(-2 ** 40, 2 ** 40, size=(M, N))
+    e = d.sum(0)
+    bad = d.copy()
+    hit = rng.random(N) < 0.2
+    for n in np.flatnonzero(hit):
+        bad[rng.integers(0, M), n] ^= np.int64(1 << int(rng.integers(0, 63)))
+    bm = torch.empty((N + 31) // 32, dtype=torch.int32, device="cuda")
+    dg = ne.diag_new()
+    ne.ne_abft_check(cfg, to_streams(bad, torch.int64), dev(e, torch.int64), bm, dg)
+    flags, nf = O.abft_check(ocfg, bad, e)
+    assert (bitmap_to_flags(bm, N) == flags).all() and ne.diag_read(dg)["fault_positions"] == nf == hit.sum()
+    for lost in (0, M - 1):
+        out = torch.empty(N, dtype=torch.int64, device="cuda")
+        ds = to_streams(d, torch.int64)
+        ne.ne_abft_recover(cfg, [None if m == lost else ds[m] for m in range(M)], dev(e, torch.int64), lost, out)
+        assert (out.cpu().numpy() == d[lost]).all()
+
+
+def test_abft_gemm_pipeline(O):
+    """ABFT on tcgen05: plain data 1 int8 limb, checksum 2 limbs (|sum| <= 192),
+    check clean, recovery of a lost stream by subtraction."""
+    M, R, Cc, K = 3, 256, 256, 512
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    A = gen(O, 2, 4, M, R * K, -64, 64)
+    B = O.gen_uniform(2, 5, 0, -64, 64, K * Cc)
+    As = to_streams(A)
+    Asum = torch.empty(R * K, dtype=torch.int32, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_abft_encode(cfg, As, Asum, diag)
+    pd = torch.empty(M * R * K, dtype=torch.int8, device="cuda")
+    ps = torch.empty(2 * R * K, dtype=torch.int8, device="cuda")
+    ne.ne_to_limbs(As, 1, pd, diag)
+    ne.ne_to_limbs([Asum], 2, ps, diag)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt, diag)
+    D = empty_streams(M, R * Cc)
+    e = torch.empty(R * Cc, dtype=torch.int64, device="cuda")
+    ne.ne_op_gemm_limbs(cfg, pd, 1, Bt, R, Cc, K, D)
+    ne.ne_op_gemm_limbs_stream(cfg, ps, 2, Bt, R, Cc, K, e)
+    ne.ne_abft_check(cfg, D, e, None, diag)
+    dd = ne.diag_read(diag)
+    assert dd["range_violations"] == 0 and dd["fault_positions"] == 0
+    plain = (A.reshape(M, R, K) @ B.reshape(K, Cc)).reshape(M, -1)
+    assert (to_np(D) == plain).all() and (e.cpu().numpy() == plain.sum(0)).all()
+    out = torch.empty(R * Cc, dtype=torch.int64, device="cuda")
+    ne.ne_abft_recover(cfg, [D[0], None, D[2]], e, 1, out)
+    assert (out.cpu().numpy() == plain[1]).all()
+
+
+
+# ------------------------------------------------------------------ base-2^l digit plan
+@pytest.mark.parametrize("M,bound", [(3, 64), (3, 127), (4, 100), (5, 127)])
+def test_base_l_digit_plan(O, M, bound):
+    """The GEMM operand as two int8 digits in base 2^l (ne_gemm_limb_plan):
+    entangle into digits, both GEMM entry points and the int64 split of
+    ne_op_gemm agree with the oracle; a value outside the plan is flagged."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L, b = ne.ne_gemm_limb_plan(cfg, bound)
+    assert (L, b) == (2, cfg.l)
+    R, Cc, K = 128, 256, 256
+    A = gen(O, 6, 4, M, R * K, -bound, bound + 1)
+    A[:, 0], A[:, 1] = bound, -bound
+    B = O.gen_uniform(6, 5, 0, -128, 128, K * Cc)
+    E = O.entangle(ocfg, A)
+    planes = torch.empty(M * L * R * K, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_limbs(cfg, to_streams(A), L, planes, diag, limb_bits=b)
+    p = planes.cpu().numpy().astype(np.int64).reshape(M, L, -1)
+    assert (p[:, 0] + p[:, 1] * 2 ** b == E).all() and ne.diag_read(diag)["range_violations"] == 0
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    ref = O.op_gemm(ocfg, E.reshape(M, R, K), B.reshape(K, Cc)).reshape(M, -1)
+    out = empty_streams(M, R * Cc)
+    ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, limb_bits=b)
+    assert (to_np(out) == ref).all()
+    out2 = empty_streams(M, R * Cc)
+    ws = torch.empty(ne.ne_gemm_workspace(cfg, R, Cc, K, L), dtype=torch.int8, device="cuda")
+    ne.ne_op_gemm(cfg, to_streams(E, torch.int64), dev(B, torch.int32), R, Cc, K, out2, L=L, ws=ws, diag=diag,
+                  limb_bits=b)
+    assert (to_np(out2) == ref).all()
+    As = to_streams(A)
+    pm = torch.empty(L * R * K, dtype=torch.int8, device="cuda")
+    ne.ne_entangle_limbs_stream(cfg, 1, As[1], As[0], L, pm, diag, limb_bits=b)
+    o1 = torch.empty(R * Cc, dtype=torch.int64, device="cuda")
+    ne.ne_op_gemm_limbs_stream(cfg, pm, L, Bt, R, Cc, K, o1, limb_bits=b)
+    assert (o1.cpu().numpy() == ref[1]).all()
+    assert ne.diag_read(diag)["range_violations"] == 0
+    big = A.copy()
+    big[2 % M, 5] = 200   # |c| > 127: its two halves no longer fit int8
+    ne.ne_entangle_limbs(cfg, to_streams(big), L, planes, diag, limb_bits=b)
+    dd = ne.diag_read(diag)
+    assert dd["range_violations"] >= 1
