@@ -112,7 +112,7 @@ class C3Gemm(Workload):
             self.pdata = torch.empty(M * R * K, dtype=torch.int8, device=dev)
             self.psum = torch.empty(2 * R * K, dtype=torch.int8, device=dev)
             self.e = torch.empty(R * Cc, dtype=torch.int64, device=dev)
-            self.launches_per_step = 8
+            self.launches_per_step = 6
             del self.planes
 
     def stages(self, i):
@@ -122,9 +122,7 @@ class C3Gemm(Workload):
         if self.scheme == "abft":
             rr = [None if m == r else self.delta[m] for m in range(M)]
             return [
-                ("encode", lambda: (ne.ne_abft_encode(cfg, self.A, self.Asum, self.diag),
-                                    ne.ne_to_limbs(self.A, 1, self.pdata, self.diag),
-                                    ne.ne_to_limbs([self.Asum], 2, self.psum, self.diag))),
+                ("encode", lambda: ne.ne_abft_encode_limbs(cfg, self.A, self.pdata, 2, self.psum, self.diag)),
                 ("prep_b", lambda: ne.ne_gemm_prep_b(self.B, self.K, self.cols, self.Bt, self.diag)),
                 ("gemm", lambda: (ne.ne_op_gemm_limbs(cfg, self.pdata, 1, self.Bt, self.rows, self.cols, self.K,
                                                       self.delta),
@@ -157,7 +155,7 @@ class C3Gemm(Workload):
         M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
         n = R * Cc
         if self.scheme == "abft":
-            return {"encode": ("hbm", R * K * (M * 4 + 4 + M + 4 + 2) / 1e9, "GB"),
+            return {"encode": ("hbm", R * K * (M * 4 + M + 2) / 1e9, "GB"),
                     "prep_b": ("hbm", K * Cc * 5 / 1e9, "GB"),
                     "gemm": ("tensor", 2 * (M + 2) * R * Cc * K / 1e12, "TOP"),
                     "check": ("hbm", (M + 1) * n * 8 / 1e9, "GB"),

@@ -266,6 +266,12 @@ ne_status ne_abft_encode(const ne_config* cfg, ne_cstreams32 c, int64_t n_total,
  * a value L digits cannot hold is a range violation).  n_total % 16 == 0. */
 ne_status ne_to_limbs(ne_cstreams32 x, int32_t count, int64_t n_total, int32_t L, int8_t* planes,
                       ne_diag* diag, ne_stream_t stream);
+/* Eqs. 4-5 in tensor-core form, one pass: pdata[m*n_total + n] = c_m[n] as one
+ * int8 digit, psum[j*n_total + n] = base-256 digit j (Ls digits) of
+ * r = sum_m c_m.  Values that do not fit are range violations (data: m*n + n,
+ * checksum: M*n + n).  n_total % 16 == 0, 1 <= Ls <= 4. */
+ne_status ne_abft_encode_limbs(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int8_t* pdata,
+                               int32_t Ls, int8_t* psum, ne_diag* diag, ne_stream_t stream);
 /* Eq. 6: flag[n] = (sum_m d_m[n] != e[n]) mod 2^64, bitmap/diag as
  * ne_disentangle_check. */
 ne_status ne_abft_check(const ne_config* cfg, ne_cstreams d, const int64_t* e, int64_t n_total,

@@ -35,7 +35,7 @@ EXPORTS = (
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
     "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
-    "ne_abft_encode", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
+    "ne_abft_encode", "ne_abft_encode_limbs", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
 )
 
 
@@ -92,6 +92,7 @@ _SIGS = {
     "ne_inject": [_VP, _I64, _U64, _VP],
     "ne_abft_encode": [_PCFG, Streams, _I64, _VP, _VP, _VP],
     "ne_to_limbs": [Streams, _I32, _I64, _I32, _VP, _VP, _VP],
+    "ne_abft_encode_limbs": [_PCFG, Streams, _I64, _VP, _I32, _VP, _VP, _VP],
     "ne_abft_check": [_PCFG, Streams, _VP, _I64, _VP, _VP, _VP],
     "ne_abft_recover": [_PCFG, Streams, _VP, _I64, _I32, _VP, _VP],
     "ne_inject_sweep": [_PCFG, Streams, _I64, _I32, _VP, _VP, _VP],
@@ -317,6 +318,11 @@ def ne_op_permute_inner_check(cfg: Config, v: torch.Tensor, block: int, r: int, 
 def ne_abft_encode(cfg: Config, c, r_out: torch.Tensor, diag=None) -> None:
     _call("ne_abft_encode", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), _ptr(r_out, torch.int32),
           _ptr(diag, torch.int64), _stream())
+
+
+def ne_abft_encode_limbs(cfg: Config, c, pdata: torch.Tensor, Ls: int, psum: torch.Tensor, diag=None) -> None:
+    _call("ne_abft_encode_limbs", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), _ptr(pdata, torch.int8), Ls,
+          _ptr(psum, torch.int8), _ptr(diag, torch.int64), _stream())
 
 
 def ne_to_limbs(x, L: int, planes: torch.Tensor, diag=None) -> None:

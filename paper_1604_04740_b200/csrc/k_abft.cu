@@ -78,6 +78,62 @@ k_to_limbs(const __grid_constant__ ne_cstreams32 x, int count, int64_t n, int8_t
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
+// encode + digit planes in one pass (the tensor-core form of Eqs. 4-5):
+// data planes[m*n + idx] = c_m (1 int8 digit), sum planes[j*n + idx] = digit j
+// of r = sum_m c_m in base 256 (LS digits).  Values that do not fit are range
+// violations naming m*n + idx (data) or M*n + idx (checksum).
+template <int MT, int LS>
+__global__ void __launch_bounds__(kThreads)
+k_abft_encode_limbs(const __grid_constant__ ne_cstreams32 c, int M_rt, int64_t n, int8_t* __restrict__ pdata,
+                    int8_t* __restrict__ psum, ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  constexpr uint64_t bias = 0x8080808080808080ull >> (64 - 8 * LS);
+  constexpr uint64_t span = LS == 8 ? 0 : (1ull << (8 * LS));
+  int bad = 0;
+  long long first = LLONG_MAX;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n / 4; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 4 * v;
+    int4 q[MA];
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) q[m] = __ldcs(reinterpret_cast<const int4*>(c.s[m] + n0));
+    int64_t acc[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      const int32_t cc[4] = {q[m].x, q[m].y, q[m].z, q[m].w};
+      uint32_t w = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i] += cc[i];
+        if (cc[i] < -128 || cc[i] > 127) {
+          ++bad;
+          const long long idx = (long long)m * n + n0 + i;
+          first = idx < first ? idx : first;
+        }
+        w |= (uint32_t)(uint8_t)(int8_t)cc[i] << (8 * i);
+      }
+      __stcs(reinterpret_cast<unsigned int*>(pdata + (int64_t)m * n + n0), w);
+    }
+    uint32_t ws[LS];
+#pragma unroll
+    for (int j = 0; j < LS; ++j) ws[j] = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t y = (uint64_t)acc[i] + bias;
+      if (LS < 8 && y >= span) {
+        ++bad;
+        const long long idx = (long long)M * n + n0 + i;
+        first = idx < first ? idx : first;
+      }
+#pragma unroll
+      for (int j = 0; j < LS; ++j) ws[j] |= (uint32_t)(((y >> (8 * j)) & 0xff) ^ 0x80) << (8 * i);
+    }
+#pragma unroll
+    for (int j = 0; j < LS; ++j) __stcs(reinterpret_cast<unsigned int*>(psum + (int64_t)j * n + n0), ws[j]);
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
 __device__ __forceinline__ uint32_t spread16b(uint32_t x) {
   x &= 0xffffu;
   x = (x | (x << 8)) & 0x00ff00ffu;
@@ -168,6 +224,37 @@ extern "C" ne_status ne_abft_encode(const ne_config* cfg, ne_cstreams32 c, int64
   for (int m = 0; m < cfg->M; ++m)
     if (!c.s[m] || !aligned16(c.s[m])) return NE_EINVAL;
   k_abft_encode<<<grid_for((n_total + 3) / 4, kThreads), kThreads, 0, cs(stream)>>>(c, cfg->M, n_total, r_out, diag);
+  return launch_status();
+}
+
+extern "C" ne_status ne_abft_encode_limbs(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int8_t* pdata,
+                                          int32_t Ls, int8_t* psum, ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || n_total % 16 != 0 || Ls < 1 || Ls > 4 || !pdata || !psum || !aligned16(pdata) ||
+      !aligned16(psum))
+    return NE_EINVAL;
+  for (int m = 0; m < cfg->M; ++m)
+    if (!c.s[m] || !aligned16(c.s[m])) return NE_EINVAL;
+  const int grid = grid_for(n_total / 4, kThreads);
+  cudaStream_t s = cs(stream);
+#define NE_AE(MV, LV) k_abft_encode_limbs<MV, LV><<<grid, kThreads, 0, s>>>(c, cfg->M, n_total, pdata, psum, diag)
+#define NE_AE_L(MV)                 \
+  switch (Ls) {                     \
+    case 1: NE_AE(MV, 1); break;    \
+    case 2: NE_AE(MV, 2); break;    \
+    case 3: NE_AE(MV, 3); break;    \
+    default: NE_AE(MV, 4); break;   \
+  }
+  switch (cfg->M) {
+    case 3: NE_AE_L(3); break;
+    case 4: NE_AE_L(4); break;
+    case 8: NE_AE_L(8); break;
+    default: NE_AE_L(0); break;
+  }
+#undef NE_AE_L
+#undef NE_AE
   return launch_status();
 }
 

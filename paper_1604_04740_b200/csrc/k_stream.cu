@@ -230,7 +230,16 @@ k_entangle_digits(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int6
         const int64_t ci = cc[i];
         const int64_t x = (int64_t)((uint64_t)ci + ((uint64_t)(int64_t)pp[i] << l));
         int8_t d[L];
-        const bool ok = digits_b(x, b, L, d);
+        bool ok;
+        if (L == 2) {  // the base-2^l plan: two digits, straight-line
+          const int64_t d0 = (int64_t)((uint64_t)x << (64 - b)) >> (64 - b);
+          const int64_t d1 = (x - d0) >> b;
+          ok = (uint64_t)(d0 + 128) < 256u && (uint64_t)(d1 + 128) < 256u;
+          d[0] = (int8_t)d0;
+          d[L - 1] = (int8_t)d1;
+        } else {
+          ok = digits_b(x, b, L, d);
+        }
         if (ci > hi || ci < -hi || !ok) {
           ++bad;
           const long long idx = (long long)m * n + n0 + i;

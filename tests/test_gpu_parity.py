@@ -640,6 +640,10 @@ def test_abft_gemm_pipeline(O):
     out = torch.empty(R * Cc, dtype=torch.int64, device="cuda")
     ne.ne_abft_recover(cfg, [D[0], None, D[2]], e, 1, out)
     assert (out.cpu().numpy() == plain[1]).all()
+    # the one-pass encode produces the same planes
+    pd2, ps2 = torch.empty_like(pd), torch.empty_like(ps)
+    ne.ne_abft_encode_limbs(cfg, As, pd2, 2, ps2, diag)
+    assert torch.equal(pd, pd2) and torch.equal(ps, ps2) and ne.diag_read(diag)["range_violations"] == 0
 
 
 
