@@ -225,28 +225,40 @@ k_entangle_digits(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int6
       uint32_t w[L];
 #pragma unroll
       for (int j = 0; j < L; ++j) w[j] = 0;
+      if (L == 2 && b == l && b <= 31) {
+        // the base-2^l plan in 32-bit arithmetic: x = c + 2^b p has
+        // d0 = sext_b(c) (its low b bits are c's), d1 = p + (c - d0) / 2^b
+        const int sh = 32 - b;
+        int32_t d0[4], d1[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t ci = cc[i];
-        const int64_t x = (int64_t)((uint64_t)ci + ((uint64_t)(int64_t)pp[i] << l));
-        int8_t d[L];
-        bool ok;
-        if (L == 2) {  // the base-2^l plan: two digits, straight-line
-          const int64_t d0 = (int64_t)((uint64_t)x << (64 - b)) >> (64 - b);
-          const int64_t d1 = (x - d0) >> b;
-          ok = (uint64_t)(d0 + 128) < 256u && (uint64_t)(d1 + 128) < 256u;
-          d[0] = (int8_t)d0;
-          d[L - 1] = (int8_t)d1;
-        } else {
-          ok = digits_b(x, b, L, d);
+        for (int i = 0; i < 4; ++i) {
+          d0[i] = (int32_t)((uint32_t)cc[i] << sh) >> sh;
+          const int64_t d1w = (int64_t)pp[i] + (((int64_t)cc[i] - d0[i]) >> b);
+          d1[i] = (int32_t)d1w;
+          const bool ok = (uint32_t)(d0[i] + 128) < 256u && (uint64_t)(d1w + 128) < 256u;
+          if (cc[i] > hi || cc[i] < -hi || !ok) {
+            ++bad;
+            const long long idx = (long long)m * n + n0 + i;
+            first = idx < first ? idx : first;
+          }
         }
-        if (ci > hi || ci < -hi || !ok) {
-          ++bad;
-          const long long idx = (long long)m * n + n0 + i;
-          first = idx < first ? idx : first;
-        }
+        w[0] = __byte_perm(__byte_perm(d0[0], d0[1], 0x0040), __byte_perm(d0[2], d0[3], 0x0040), 0x5410);
+        w[L - 1] = __byte_perm(__byte_perm(d1[0], d1[1], 0x0040), __byte_perm(d1[2], d1[3], 0x0040), 0x5410);
+      } else {
 #pragma unroll
-        for (int j = 0; j < L; ++j) w[j] |= (uint32_t)(uint8_t)d[j] << (8 * i);
+        for (int i = 0; i < 4; ++i) {
+          const int64_t ci = cc[i];
+          const int64_t x = (int64_t)((uint64_t)ci + ((uint64_t)(int64_t)pp[i] << l));
+          int8_t d[L];
+          const bool ok = digits_b(x, b, L, d);
+          if (ci > hi || ci < -hi || !ok) {
+            ++bad;
+            const long long idx = (long long)m * n + n0 + i;
+            first = idx < first ? idx : first;
+          }
+#pragma unroll
+          for (int j = 0; j < L; ++j) w[j] |= (uint32_t)(uint8_t)d[j] << (8 * i);
+        }
       }
 #pragma unroll
       for (int j = 0; j < L; ++j)
