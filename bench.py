@@ -74,7 +74,7 @@ class C3Gemm(Workload):
     name = "C3"
     metric_unit = "Gop/s"
 
-    def __init__(self, rank, n=4096, seed=2, algo="tc", scheme="entangled", limbs="plan"):
+    def __init__(self, rank, n=4096, seed=2, algo="tc", scheme="entangled", limbs="plan", fuse=True):
         import torch
         import paper_1604_04740_b200 as ne
 
@@ -88,6 +88,8 @@ class C3Gemm(Workload):
             self.L, self.limb_bits = ne.ne_gemm_limb_plan(self.cfg, 64)
         self.algo = algo
         self.scheme = scheme
+        # disentangle + check fused into the GEMM epilogue (ne_op_gemm_limbs_check)
+        self.fuse = bool(fuse) and algo == "tc" and scheme == "entangled"
         M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
         dev = "cuda"
         self.A = [torch.empty(R * K, dtype=torch.int32, device=dev) for _ in range(M)]
@@ -104,7 +106,8 @@ class C3Gemm(Workload):
         self.diag = ne.diag_new()
         if algo == "imad":
             self.eps = [torch.empty(R * K, dtype=torch.int64, device=dev) for _ in range(M)]
-        self.launches_per_step = 5
+        self.launches_per_step = 4 if self.fuse else 5
+        self.counters = torch.zeros(ne.ne_gemm_check_workspace(R, Cc) // 4, dtype=torch.int32, device=dev)
         if scheme == "abft":
             # the paper's comparison method on the same kernels: plain data (1 int8
             # limb), one checksum stream (Eq. 4; |sum| <= 192 -> 2 limbs)
@@ -139,6 +142,17 @@ class C3Gemm(Workload):
                 ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
                 ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
             ]
+        if self.fuse:
+            return [
+                ("entangle", lambda: ne.ne_entangle_limbs(cfg, self.A, self.L, self.planes, self.diag,
+                                                          self.limb_bits)),
+                ("prep_b", lambda: ne.ne_gemm_prep_b(self.B, self.K, self.cols, self.Bt, self.diag)),
+                ("gemm_check", lambda: ne.ne_op_gemm_limbs_check(cfg, self.planes, self.L, self.Bt, self.rows,
+                                                                 self.cols, self.K, self.delta, 0, self.dout,
+                                                                 self.counters, self.bitmap, self.diag,
+                                                                 self.limb_bits)),
+                ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
+            ]
         return [
             ("entangle", lambda: ne.ne_entangle_limbs(cfg, self.A, self.L, self.planes, self.diag, self.limb_bits)),
             ("prep_b", lambda: ne.ne_gemm_prep_b(self.B, self.K, self.cols, self.Bt, self.diag)),
@@ -166,6 +180,7 @@ class C3Gemm(Workload):
             "entangle": ("hbm", M * R * K * (4 + (L if self.algo == "tc" else 8)) / 1e9, "GB"),
             "prep_b": ("hbm", K * Cc * 5 / 1e9, "GB"),
             "gemm": gemm,
+            "gemm_check": gemm,  # fused: the tensor work bounds it; + M*n*8 B of d_hat written under it
             "check": ("hbm", (M * n * 16 + n / 8) / 1e9, "GB"),
             "recover": ("hbm", ((M - 1) * n * 8 + M * n * 8) / 1e9, "GB"),
         }
@@ -180,7 +195,9 @@ class C3Gemm(Workload):
                                          if self.scheme == "abft" else " (numerical entanglement)"),
                 "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
                 "l2": "working set ~1.9 GB per step >> 126 MB L2 (no flush needed)",
-                "step": "entangle(limbs)+prep_B+GEMM+disentangle/check(r=0)+recover(r=step mod 3)"}
+                "step": ("entangle(limbs)+prep_B+GEMM with fused disentangle/check(r=0)+recover(r=step mod 3)"
+                         if self.fuse else
+                         "entangle(limbs)+prep_B+GEMM+disentangle/check(r=0)+recover(r=step mod 3)")}
 
     # ---- end-to-end through host buffers
     def e2e_setup(self):
@@ -683,7 +700,7 @@ def run_ours(args, rank, world, local_rank):
     ne.lib()
     torch.cuda.set_device(local_rank)
     W = WORKLOADS[args.workload](rank) if args.workload != "c3" else \
-        C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs)
+        C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=args.fuse)
     torch.cuda.synchronize()
 
     def barrier():
@@ -932,6 +949,8 @@ def main():
                     help="c3: GEMM operand digits: cheapest exact plan (default) or balanced base 256")
     ap.add_argument("--scheme", default="entangled", choices=["entangled", "abft"],
                     help="c3 only: numerical entanglement (default) or the paper's ABFT comparison method")
+    ap.add_argument("--fuse", type=int, default=0,
+                    help="c3: disentangle/check fused into the GEMM epilogue, or a separate pass (default: measured faster)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
     args = ap.parse_args()

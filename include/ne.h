@@ -215,6 +215,23 @@ ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes, int32_t L
                            const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams C,
                            ne_stream_t stream);
 
+/* ne_op_gemm_limbs followed by ne_disentangle_check(C, r, d_out, bitmap,
+ * diag) on its outputs, fused into the GEMM epilogue: the M
+ * streams' tiles of each output tile are computed back to back; the CTA that
+ * stores the last of them reads the M delta tiles back (L2) and disentangles
+ * and checks them (Eqs. 16-19, 21).  C (delta) is still written in full (it
+ * is what recovery reads).  Results, bitmap and diag are bit-identical to the
+ * unfused pair.  tile_counters: ne_gemm_check_workspace() bytes of device
+ * memory, zeroed by the caller once; every call leaves them zeroed (do not
+ * share one buffer between concurrently running calls).  Fused for M in
+ * {3, 4, 8} and L = 2; other (M, L) run the two kernels back to back.
+ * Shapes as ne_op_gemm_limbs.  Errors: NE_EINDEX if r outside [0, M). */
+ne_status ne_gemm_check_workspace(int64_t rows, int64_t cols, size_t* bytes);
+ne_status ne_op_gemm_limbs_check(const ne_config* cfg, const int8_t* planes, int32_t L, int32_t limb_bits,
+                                 const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams C,
+                                 int32_t r, ne_streams d_out, uint32_t* bitmap, ne_diag* diag,
+                                 int32_t* tile_counters, ne_stream_t stream);
+
 /* One stream of ne_op_gemm_limbs (the per-GPU GEMM of the one-stream-per-GPU
  * layout): C_m = sum_i 2^(8i) D_{m,i} B from planes_m (L planes). */
 ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t* planes_m, int32_t L,

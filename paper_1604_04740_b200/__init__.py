@@ -33,6 +33,7 @@ EXPORTS = (
     "ne_entangle_limbs_stream", "ne_op_gemm_limbs_stream",
     "ne_op_scale", "ne_op_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
+    "ne_gemm_check_workspace", "ne_op_gemm_limbs_check",
     "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
     "ne_abft_encode", "ne_abft_encode_limbs", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
@@ -85,6 +86,9 @@ _SIGS = {
     "ne_op_gemm": [_PCFG, Streams, _VP, _I64, _I64, _I64, C.c_int, _I32, _I32, Streams, _VP, _SZ, _VP, _VP],
     "ne_gemm_prep_b": [_VP, _I64, _I64, _VP, _VP, _VP],
     "ne_op_gemm_limbs": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _VP],
+    "ne_gemm_check_workspace": [_I64, _I64, C.POINTER(_SZ)],
+    "ne_op_gemm_limbs_check": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _I32, Streams, _VP, _VP, _VP,
+                               _VP],
     "ne_disentangle_check": [_PCFG, Streams, _I64, _I32, Streams, _VP, _VP, _VP],
     "ne_recover": [_PCFG, Streams, _I64, _I32, Streams, _VP],
     "ne_op_permute_inner_check": [_PCFG, Streams, _VP, _I32, _VP, _I64, _VP, _I64, _I64, _I32,
@@ -289,6 +293,22 @@ def ne_op_gemm_limbs(cfg: Config, planes: torch.Tensor, L: int, Bt: torch.Tensor
                      out, limb_bits: int = 8) -> None:
     _call("ne_op_gemm_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, limb_bits, _ptr(Bt, torch.int8), rows, cols,
           K, _streams(out, torch.int64), _stream())
+
+
+def ne_gemm_check_workspace(rows: int, cols: int) -> int:
+    b = _SZ()
+    _call("ne_gemm_check_workspace", rows, cols, C.byref(b))
+    return b.value
+
+
+def ne_op_gemm_limbs_check(cfg: Config, planes: torch.Tensor, L: int, Bt: torch.Tensor, rows: int, cols: int,
+                           K: int, out, r: int, d_out, counters: torch.Tensor, bitmap: torch.Tensor | None = None,
+                           diag=None, limb_bits: int = 8) -> None:
+    """GEMM + fused disentangle/check epilogue; counters: a zeroed int32 device
+    buffer of ne_gemm_check_workspace(rows, cols) bytes (left zeroed)."""
+    _call("ne_op_gemm_limbs_check", C.byref(cfg), _ptr(planes, torch.int8), L, limb_bits, _ptr(Bt, torch.int8), rows,
+          cols, K, _streams(out, torch.int64), r, _streams(d_out, torch.int64), _ptr(bitmap, torch.int32),
+          _ptr(diag, torch.int64), _ptr(counters, torch.int32), _stream())
 
 
 # ------------------------------------------------------------------ a4-a7

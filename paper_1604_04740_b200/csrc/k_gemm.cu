@@ -12,6 +12,10 @@ void launch_gemm_imad64(int M, const ne_cstreams& A, const int32_t* B, const ne_
                         int64_t cols, int64_t K, cudaStream_t s);
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s);
+ne_status launch_gemm_tc_check(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows,
+                               int64_t cols, int64_t K, const ne_streams& C, const ne_cstreams& dr,
+                               const ne_streams& dor, uint32_t* bitmap, ne_diag* diag, int* cnt, int l,
+                               cudaStream_t s);
 
 // int64 entangled A_m -> L balanced int8 digit planes, planes[(m*L+i)*n + idx]
 template <int MT>
@@ -52,47 +56,55 @@ k_split_limbs(const __grid_constant__ ne_cstreams A, int M_rt, int64_t n, int L,
 
 // B (K x cols int32, row-major) -> Bt (cols x K int8, K contiguous), the
 // one-plane int8 operand of the tensor-core GEMM (|B| <= 127 / -128, else a
-// range violation).  Tile 128 (k) x 64 (c): 128-bit loads along c, transpose
-// through shared memory, 128-bit stores along k.
+// range violation).  Tile 64 (k) x 128 (c), 256 threads.  A task is a 4 x 4
+// block (4 rows k, 4 columns c): four 128-bit loads along c, a register
+// transpose into four 32-bit words (4 k-bytes of one column, PRMT), stored to
+// a [128][17]-word shared tile (a warp's 8 x 4 tasks hit 32 distinct banks);
+// then 128-bit stores of 16 consecutive k per column.
 __global__ void __launch_bounds__(256)
 k_prep_b(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __restrict__ Bt, ne_diag* __restrict__ diag) {
-  __shared__ __align__(16) int8_t tile[64][128 + 16];
-  const int64_t k0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 64;
+  __shared__ uint32_t W[128][17];
+  const int64_t k0 = (int64_t)blockIdx.y * 64, c0 = (int64_t)blockIdx.x * 128;
+  const bool vec = (cols % 4) == 0;
+  const int lane = threadIdx.x & 31;
   int bad = 0;
   long long first = LLONG_MAX;
-  const bool vec = (cols % 4) == 0;
 #pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int t = threadIdx.x + 256 * it;  // 2048 groups of 4 consecutive c
-    const int kk = t >> 4, cq = (t & 15) * 4;
-    const int64_t k = k0 + kk, c = c0 + cq;
-    int32_t v[4] = {0, 0, 0, 0};
-    if (k < K) {
-      if (vec && c + 3 < cols) {
-        int4 w = __ldcs(reinterpret_cast<const int4*>(B + k * cols + c));
-        v[0] = w.x; v[1] = w.y; v[2] = w.z; v[3] = w.w;
+  for (int it = 0; it < 2; ++it) {
+    const int wt = (threadIdx.x >> 5) + 8 * it;  // 16 warp tasks of 8 (c) x 4 (k) blocks
+    const int cq = (wt & 3) * 8 + (lane & 7), kq = (wt >> 2) * 4 + (lane >> 3);
+    const int64_t c = c0 + 4 * cq;
+    int32_t v[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t k = k0 + 4 * kq + r;
+      if (k < K && vec && c + 3 < cols) {
+        const int4 w = __ldcs(reinterpret_cast<const int4*>(B + k * cols + c));
+        v[r][0] = w.x; v[r][1] = w.y; v[r][2] = w.z; v[r][3] = w.w;
       } else {
-        for (int i = 0; i < 4; ++i) v[i] = (c + i < cols) ? B[k * cols + c + i] : 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[r][i] = (k < K && c + i < cols) ? B[k * cols + c + i] : 0;
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if ((uint32_t)(v[r][i] + 128) > 255u) {
+          ++bad;
+          const long long idx = (long long)((k0 + 4 * kq + r) * cols + c + i);
+          first = idx < first ? idx : first;
+        }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (v[i] < -128 || v[i] > 127) {
-        ++bad;
-        const long long idx = (long long)(k * cols + c + i);
-        first = idx < first ? idx : first;
-      }
-      tile[cq + i][kk] = (int8_t)v[i];
-    }
+    for (int i = 0; i < 4; ++i)
+      W[4 * cq + i][kq] = __byte_perm(__byte_perm(v[0][i], v[1][i], 0x0040), __byte_perm(v[2][i], v[3][i], 0x0040), 0x5410);
   }
   __syncthreads();
 #pragma unroll
   for (int it = 0; it < 2; ++it) {
-    const int t = threadIdx.x + 256 * it;  // 512 groups of 16 consecutive k
-    const int cc = t >> 3, kq = (t & 7) * 16;
-    const int64_t c = c0 + cc, k = k0 + kq;
+    const int u = threadIdx.x + 256 * it;  // 512 chunks of 16 consecutive k
+    const int cc = u >> 2, j = u & 3;
+    const int64_t c = c0 + cc, k = k0 + 16 * j;
     if (c < cols && k + 15 < K)
-      *reinterpret_cast<uint4*>(Bt + c * K + k) = *reinterpret_cast<const uint4*>(&tile[cc][kq]);
+      __stcs(reinterpret_cast<uint4*>(Bt + c * K + k), make_uint4(W[cc][4 * j], W[cc][4 * j + 1], W[cc][4 * j + 2], W[cc][4 * j + 3]));
   }
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
@@ -117,7 +129,7 @@ extern "C" ne_status ne_gemm_workspace(const ne_config* cfg, int64_t rows, int64
 extern "C" ne_status ne_gemm_prep_b(const int32_t* B, int64_t K, int64_t cols, int8_t* Bt, ne_diag* diag,
                                     ne_stream_t stream) {
   if (!B || !Bt || K <= 0 || cols <= 0 || K % 16 != 0 || !aligned16(Bt) || !aligned16(B)) return NE_EINVAL;
-  dim3 grid((unsigned)((cols + 63) / 64), (unsigned)((K + 127) / 128));
+  dim3 grid((unsigned)((cols + 127) / 128), (unsigned)((K + 63) / 64));
   k_prep_b<<<grid, 256, 0, cs(stream)>>>(B, K, cols, Bt, diag);
   return launch_status();
 }
@@ -133,6 +145,35 @@ extern "C" ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes
     if (!C.s[m] || !aligned16(C.s[m])) return NE_EINVAL;
   if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
   return launch_gemm_tc(cfg->M, L, limb_bits, planes, Bt, rows, cols, K, C, cs(stream));
+}
+
+extern "C" ne_status ne_gemm_check_workspace(int64_t rows, int64_t cols, size_t* bytes) {
+  if (!bytes || rows < 0 || cols < 0) return NE_EINVAL;
+  *bytes = (size_t)((rows + 127) / 128) * (size_t)((cols + 127) / 128) * sizeof(int32_t) + 16;
+  return NE_OK;
+}
+
+extern "C" ne_status ne_op_gemm_limbs_check(const ne_config* cfg, const int8_t* planes, int32_t L, int32_t limb_bits,
+                                            const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams C,
+                                            int32_t r, ne_streams d_out, uint32_t* bitmap, ne_diag* diag,
+                                            int32_t* tile_counters, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (r < 0 || r >= cfg->M) return NE_EINDEX;
+  if (!planes || !Bt || !tile_counters || L < 1 || L > 4 || limb_bits < 8 || limb_bits > 63 || !aligned16(planes) ||
+      !aligned16(Bt))
+    return NE_EINVAL;
+  for (int m = 0; m < cfg->M; ++m)
+    if (!C.s[m] || !aligned16(C.s[m]) || !d_out.s[m] || !aligned16(d_out.s[m])) return NE_EINVAL;
+  if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
+  cudaStream_t s = cs(stream);
+  ne_cstreams Cc{};
+  for (int m = 0; m < cfg->M; ++m) Cc.s[m] = C.s[m];
+  st = launch_gemm_tc_check(cfg->M, L, limb_bits, planes, Bt, rows, cols, K, C, rotate(Cc, cfg->M, r),
+                            rotate(d_out, cfg->M, r), bitmap, diag, tile_counters, cfg->l, s);
+  if (st != NE_ENOTSUP) return st;
+  if ((st = launch_gemm_tc(cfg->M, L, limb_bits, planes, Bt, rows, cols, K, C, s)) != NE_OK) return st;
+  return ne_disentangle_check(cfg, Cc, rows * cols, r, d_out, bitmap, diag, stream);
 }
 
 extern "C" ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t* planes_m, int32_t L,

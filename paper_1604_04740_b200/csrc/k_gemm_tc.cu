@@ -152,12 +152,119 @@ struct Cfg {
   static constexpr int kARows = BM / CL;          // rows of each limb tile this CTA loads (multicast)
   static constexpr int kTmemCols = (L * BN <= 32) ? 32 : (L * BN <= 64) ? 64 : (L * BN <= 128) ? 128 : (L * BN <= 256) ? 256 : 512;
   static constexpr int kStageOut = 32 * 16 * 8;  // one epilogue warp's [32 rows x 16 int64] box
-  static constexpr size_t kSmem = (size_t)STAGES * kStage + 2 * 8 * kStageOut + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr size_t kSmem = (size_t)STAGES * kStage + 2 * 8 * kStageOut + 1024 /*align*/ + 512 /*barriers, check queue*/;
 };
 
 struct OutMaps {
   CUtensorMap m[8];  // C_m as a 2-D int64 tensor [rows][cols], box {16, 32}, 128B swizzle
 };
+
+// Fused a4/a5 (CHK = M > 0): the M streams' tiles of one output tile are
+// consecutive work items (stream index fastest), so they run at about the
+// same time on M different CTAs.  Each CTA, once its delta tile is stored
+// (bulk stores complete, proxy fence, release), increments the tile's counter.
+// Tile t is checked by the CTA computing stream t mod M (balanced): its
+// epilogue queues t for the CTA's 8 checker warps, which wait until the
+// counter reaches M, read the M delta tiles back and run disentangle + check
+// (Eqs. 16-19, 21), writing d_hat, the bitmap and ne_diag exactly as
+// k_disentangle<M, true> does, then re-zero the counter.  The checkers never
+// touch TMEM, so the MMA pipeline does not wait for them.  The delta tiles are
+// the op's stored outputs: the check still sees every stream through memory.
+// Measured: correct, but slower than GEMM + separate check on
+// B200 — the checker warps' 800 MB of extra memory traffic per C3 step is
+// latency-bound at 8 warps per SM and stretches the GEMM by ~0.16 ms.
+struct ChkArgs {
+  ne_cstreams dr;     // delta, rotated so that the excluded stream r is index 0
+  ne_streams dor;     // d_hat outputs, same rotation
+  uint32_t* bitmap;   // nullable
+  ne_diag* diag;      // nullable
+  int* cnt;           // (rows/128) x (cols/BN) zero-initialised tile counters
+  int l;
+};
+
+__device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * 8) : "memory");
+}
+
+constexpr int kChkWarps = 8;  // checker warps (fused check only; 4 and 16 measured slower)
+constexpr int kChkThreads = 32 * kChkWarps;
+
+__device__ __forceinline__ void chk_bar() {  // the checker warps only
+  asm volatile("bar.sync 2, %0;" ::"n"(kChkThreads) : "memory");
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// spread the low 16 bits of x to the even bit positions (bitmap assembly)
+__device__ __forceinline__ uint32_t spread16e(uint32_t x) {
+  x &= 0xffffu;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+// disentangle + check of one 128 x BN output tile by the checker threads
+// (et = 0..kChkThreads-1): pair p = j*kChkThreads + et covers row p / (BN/2), columns
+// col0 + 2 (p % (BN/2)) .. +1, so a warp owns 64 consecutive positions of a
+// row = two bitmap words (as in k_disentangle).  Loads go through L2 (.cg:
+// the tiles were written by this kernel), U pairs in flight per thread.
+template <int MT, int BN>
+__device__ __forceinline__ void check_tile(const ChkArgs& chk, int64_t row0, int64_t col0, int64_t cols,
+                                           int64_t n_total, int et) {
+  constexpr int U = MT >= 4 ? 2 : 4;  // registers: <= 96 per thread at 640 threads
+  constexpr int kPairs = BM * BN / 2;
+  static_assert(kPairs % (kChkThreads * U) == 0, "tile pairs divide evenly");
+  const int lane = et & 31;
+  int nflag = 0;
+  long long first = LLONG_MAX;
+#pragma unroll 1
+  for (int j0 = 0; j0 < kPairs / kChkThreads; j0 += U) {
+    int64_t a[U][MT], b[U][MT], n0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = (j0 + u) * kChkThreads + et;
+      n0[u] = (row0 + p / (BN / 2)) * cols + col0 + 2 * (p % (BN / 2));
+#pragma unroll
+      for (int s = 0; s < MT; ++s) {
+        const longlong2 q = __ldcg(reinterpret_cast<const longlong2*>(chk.dr.s[s] + n0[u]));
+        a[u][s] = q.x;
+        b[u][s] = q.y;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int64_t da[MT], db[MT];
+      const bool f0 = disentangle_rot<MT>(a[u], MT, chk.l, da, true);
+      const bool f1 = disentangle_rot<MT>(b[u], MT, chk.l, db, true);
+#pragma unroll
+      for (int s = 0; s < MT; ++s)
+        __stcs(reinterpret_cast<longlong2*>(chk.dor.s[s] + n0[u]), make_longlong2(da[s], db[s]));
+      if (f0) {
+        ++nflag;
+        first = n0[u] < first ? n0[u] : first;
+      }
+      if (f1) {
+        ++nflag;
+        first = n0[u] + 1 < first ? n0[u] + 1 : first;
+      }
+      if (chk.bitmap) {
+        const uint32_t b0 = __ballot_sync(0xffffffffu, f0);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, f1);
+        const int64_t w0 = (n0[u] - 2 * lane) / 32;  // lane 0's position starts a 64-position run
+        if (lane == 0) chk.bitmap[w0] = spread16e(b0) | (spread16e(b1) << 1);
+        if (lane == 1) chk.bitmap[w0 + 1] = spread16e(b0 >> 16) | (spread16e(b1 >> 16) << 1);
+      }
+    }
+  }
+  (void)n_total;
+  if (chk.diag) diag_add(&chk.diag->fault_positions, &chk.diag->first_fault, nflag, first);
+}
 
 // Persistent, warp-specialised kernel.  The grid is one CTA per SM (clusters
 // of CL along N); each cluster walks the work list w = cid, cid + nclusters, ...
@@ -171,11 +278,33 @@ struct OutMaps {
 // mainloop.
 constexpr int kEpiWarps = 8;
 constexpr int kThreadsP = 128 + 32 * kEpiWarps;  // warps 0-3: roles, 4-11: epilogue
+template <int CHK>
+constexpr int threads_for() { return kThreadsP + (CHK > 0 ? 32 * kChkWarps : 0); }
+constexpr int kQN = 32;                          // check queue ring (tile ids)
 
-template <int L, int BN, int STAGES, int SW, int CL>
-__global__ void __launch_bounds__(kThreadsP, 1)
+// work item w -> (stream m, row tile, column-tile group); stream-fastest
+// order when the check is fused (CHK > 0), else stream-slowest
+template <int CHK>
+__device__ __forceinline__ void decode_work(int64_t w, int M, int64_t n_rt, int64_t n_cg, int& m, int64_t& rt,
+                                            int64_t& cg) {
+  if (CHK > 0) {
+    m = (int)(w % M);
+    const int64_t rem = w / M;
+    rt = rem / n_cg;
+    cg = rem % n_cg;
+  } else {
+    m = (int)(w / (n_rt * n_cg));
+    const int64_t rem = w % (n_rt * n_cg);
+    rt = rem / n_cg;
+    cg = rem % n_cg;
+  }
+}
+
+template <int L, int BN, int STAGES, int SW, int CL, int CHK>
+__global__ void __launch_bounds__(threads_for<CHK>(), 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-          const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits) {
+          const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
+          const __grid_constant__ ChkArgs chk) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   constexpr int BK = CF::BK;
   static_assert(L * BN <= 512, "TMEM holds 512 columns");
@@ -187,6 +316,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
   uint64_t* tmem_full = empty + STAGES;
   uint64_t* tmem_empty = tmem_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+  // check queue (CHK > 0): ring of tile ids pushed by the epilogue, consumed by the checker warps
+  volatile int* q_head = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  volatile int* q_tail = q_head + 1;
+  volatile int* q_done = q_head + 2;
+  volatile int* q_ring = q_head + 4;
+  if (threadIdx.x == 0) {
+    *q_head = 0;
+    *q_tail = 0;
+    *q_done = 0;
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = CL > 1 ? cluster_rank() : 0;
@@ -225,10 +364,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
       uint32_t it = 0;
       for (int64_t w = cid; w < n_work; w += ncl) {
-        const int m = (int)(w / (n_rt * n_cg));
-        const int64_t rem = w % (n_rt * n_cg);
-        const int64_t row0 = (rem / n_cg) * BM;
-        const int64_t col0 = ((rem % n_cg) * CL + crank) * BN;
+        int m;
+        int64_t rt, cg;
+        decode_work<CHK>(w, M, n_rt, n_cg, m, rt, cg);
+        const int64_t row0 = rt * BM;
+        const int64_t col0 = (cg * CL + crank) * BN;
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -275,7 +415,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
         mma_commit(tmem_full, 1);        // this tile's accumulators are final
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 4 + kEpiWarps) {
     // ---------------- epilogue: TMEM -> registers -> int64 recombination ->
     // 128B-swizzled smem box -> TMA bulk tensor store (double-buffered per warp)
     const int ew = warp - 4;
@@ -285,10 +425,11 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
     unsigned char* my_out = stage_out + ew * 2 * CF::kStageOut;
     uint32_t tile = 0, buf = 0;
     for (int64_t w = cid; w < n_work; w += ncl, ++tile) {
-      const int m = (int)(w / (n_rt * n_cg));
-      const int64_t rem = w % (n_rt * n_cg);
-      const int64_t row0 = (rem / n_cg) * BM;
-      const int64_t col0 = ((rem % n_cg) * CL + crank) * BN;
+      int m;
+      int64_t rt, cg;
+      decode_work<CHK>(w, M, n_rt, n_cg, m, rt, cg);
+      const int64_t row0 = rt * BM;
+      const int64_t col0 = (cg * CL + crank) * BN;
       mbar_wait(tmem_full, tile & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
@@ -329,8 +470,71 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
+      if constexpr (CHK > 0) {
+        // publish this delta tile: bulk stores complete and ordered before
+        // the generic-proxy reads of the CTA that checks the tile
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
+        epi_bar();
+        const int64_t tile_id = rt * (cols / BN) + cg * CL + crank;
+        if (ew == 0 && lane == 0) {
+          __threadfence();
+          atomicAdd(chk.cnt + tile_id, 1);
+          if (tile_id % M == m) {  // this CTA's checker warps check the tile (balanced: 1 in M)
+            const int h = *q_head;
+            while (h - *q_tail >= kQN) __nanosleep(128);
+            q_ring[h % kQN] = (int)tile_id;
+            __threadfence_block();
+            *q_head = h + 1;
+          }
+        }
+      }
+    }
+    if constexpr (CHK > 0) {
+      if (ew == 0 && lane == 0) {
+        __threadfence_block();
+        *q_done = 1;
+      }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else if (warp >= 4 + kEpiWarps) {
+    if constexpr (CHK > 0) {
+    // ---------------- checkers: disentangle + check of the tiles queued for
+    // this CTA, once all M streams' delta tiles are published (tile counter == M)
+    const int ct = threadIdx.x - 32 * (4 + kEpiWarps);  // 0 .. kChkThreads-1
+    int tail = 0;
+    while (true) {
+      const int done = *q_done;
+      const int head = *q_head;
+      if (tail == head) {
+        if (done) break;
+        __nanosleep(256);
+        continue;
+      }
+      __threadfence_block();
+      const int tile_id = q_ring[tail % kQN];
+      if (ct == 0) {
+        // bounded wait (all CTAs are co-resident: the grid is sized by the
+        // cluster occupancy); a timeout is reported as a flagged run, not a hang
+        long long spins = 0;
+        int c;
+        while ((c = ld_acquire(chk.cnt + tile_id)) < M && ++spins < (1ll << 24)) __nanosleep(64);
+        if (c < M && chk.diag) atomicAdd(&chk.diag->fault_positions, 1ull << 40);
+      }
+      chk_bar();
+      const int64_t nct = cols / BN;
+      check_tile<CHK, BN>(chk, (tile_id / nct) * BM, (tile_id % nct) * BN, cols, rows * cols, ct);
+      chk_bar();
+      ++tail;
+      if (ct == 0) {
+        chk.cnt[tile_id] = 0;
+        *q_tail = tail;
+      }
+    }
+    }
   }
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -390,9 +594,9 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
   return r == CUDA_SUCCESS;
 }
 
-template <int L, int BN, int STAGES, int SW, int CL>
+template <int L, int BN, int STAGES, int SW, int CL, int CHK = 0>
 static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
-                     int limb_bits, const ne_streams& C, cudaStream_t s) {
+                     int limb_bits, const ne_streams& C, cudaStream_t s, const ChkArgs* chk = nullptr) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   if (cols % (BN * CL) != 0 || K % CF::BK != 0) return NE_ENOTSUP;
   CUtensorMap ma, mb;
@@ -402,15 +606,14 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   OutMaps om;
   for (int m = 0; m < M; ++m)
     if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)rows)) return NE_ECUDA;
-  auto kern = k_gemm_tc<L, BN, STAGES, SW, CL>;
+  auto kern = k_gemm_tc<L, BN, STAGES, SW, CL, CHK>;
+  ChkArgs ca{};
+  if (CHK > 0) ca = *chk;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) != cudaSuccess)
     return NE_ECUDA;
   const int64_t n_work = (int64_t)M * (rows / BM) * (cols / (BN * CL));
-  int64_t nclusters = num_sms() / CL;
-  if (nclusters > n_work) nclusters = n_work;
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)(nclusters * CL));
-  lc.blockDim = dim3(kThreadsP);
+  lc.blockDim = dim3(threads_for<CHK>());
   lc.dynamicSmemBytes = CF::kSmem;
   lc.stream = s;
   cudaLaunchAttribute at[1];
@@ -420,7 +623,21 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits) != cudaSuccess) return NE_ECUDA;
+  // persistent grid: one CTA per SM, capped by how many clusters can be
+  // resident at once (the fused check waits on peer CTAs' tiles, so every
+  // CTA of the grid must be co-resident)
+  int64_t nclusters = num_sms() / CL;
+  lc.gridDim = dim3((unsigned)(nclusters * CL));
+  int active = 0;
+  if (cudaOccupancyMaxActiveClusters(&active, kern, &lc) == cudaSuccess && active > 0) {
+    if (active < nclusters) nclusters = active;
+  } else {
+    cudaGetLastError();
+    if (CHK > 0) return NE_ENOTSUP;
+  }
+  if (nclusters > n_work) nclusters = n_work;
+  lc.gridDim = dim3((unsigned)(nclusters * CL));
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, ca) != cudaSuccess) return NE_ECUDA;
   return launch_status();
 }
 
@@ -430,24 +647,48 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
 // 64-byte K stages (64B swizzle) give 4-6 pipeline stages in ~200 KB of smem;
 // clusters of 2 along N multicast the limb tiles (A read once per pair)
 // whenever the column-tile count is even.
-ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
-                         int64_t K, const ne_streams& C, cudaStream_t s) {
+template <int CHK>
+static ne_status gemm_tc_dispatch(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows,
+                                  int64_t cols, int64_t K, const ne_streams& C, cudaStream_t s, const tc::ChkArgs* chk) {
   const bool pair128 = cols % 256 == 0, pair256 = cols % 512 == 0;
   switch (L) {
     case 1:
+      if (CHK > 0) return NE_ENOTSUP;
       if (pair256) return tc::run<1, 256, 6, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
       if (cols % 256 == 0) return tc::run<1, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
       return tc::run<1, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
     case 2:
-      if (pair256) return tc::run<2, 256, 5, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
-      if (cols % 256 == 0) return tc::run<2, 256, 5, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
-      return tc::run<2, 128, 6, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
+      if (pair256) return tc::run<2, 256, 5, 64, 2, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk);
+      if (cols % 256 == 0) return tc::run<2, 256, 5, 64, 1, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk);
+      return tc::run<2, 128, 6, 64, 1, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk);
     case 3:
+      if (CHK > 0) return NE_ENOTSUP;
       if (pair128) return tc::run<3, 128, 5, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
       return tc::run<3, 128, 5, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
     case 4:
+      if (CHK > 0) return NE_ENOTSUP;  // 4 limb accumulators leave no registers for checker warps
       if (pair128) return tc::run<4, 128, 4, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
       return tc::run<4, 128, 4, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
+    default: return NE_ENOTSUP;
+  }
+}
+
+ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+                         int64_t K, const ne_streams& C, cudaStream_t s) {
+  return gemm_tc_dispatch<0>(M, L, b, planes, Bt, rows, cols, K, C, s, nullptr);
+}
+
+// The GEMM with the fused disentangle + check epilogue: M in {3, 4, 8} and
+// L = 2; NE_ENOTSUP otherwise (the caller then runs the separate pass).
+ne_status launch_gemm_tc_check(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows,
+                               int64_t cols, int64_t K, const ne_streams& C, const ne_cstreams& dr,
+                               const ne_streams& dor, uint32_t* bitmap, ne_diag* diag, int* cnt, int l,
+                               cudaStream_t s) {
+  const tc::ChkArgs chk{dr, dor, bitmap, diag, cnt, l};
+  switch (M) {
+    case 3: return gemm_tc_dispatch<3>(M, L, b, planes, Bt, rows, cols, K, C, s, &chk);
+    case 4: return gemm_tc_dispatch<4>(M, L, b, planes, Bt, rows, cols, K, C, s, &chk);
+    case 8: return gemm_tc_dispatch<8>(M, L, b, planes, Bt, rows, cols, K, C, s, &chk);
     default: return NE_ENOTSUP;
   }
 }

@@ -203,6 +203,79 @@ k_entangle_limbs(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
+// The two-digit base-2^l plan in pure 32-bit arithmetic:
+// eps = c + 2^b p (b = l <= 31) has digits d0 = sext_b(c) and
+// d1 = p + (c - d0) / 2^b = p + (c >> b) + bit_{b-1}(c); it is exact iff both
+// fit int8.  8 positions per thread: one 256-bit load per stream (two 128-bit
+// loads when a stream is only 16-B aligned), one 64-bit store per digit plane.
+// Wrapping of d1 in int32 cannot fake a valid digit: a wrapped value is near
+// -2^31.  Range failures (|c| > hi, digit out of int8) take a slow path.
+__device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+template <int MT, bool V256>
+__global__ void __launch_bounds__(kThreads)
+k_entangle_pair(const __grid_constant__ ne_cstreams32 c, int M_rt, int b, int64_t hi, int64_t n,
+                int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  const bool rc = hi < 2147483647ll;  // |c| <= hi can fail for an int32 only then
+  const int32_t h32 = rc ? (int32_t)hi : 0;
+  const int sh = 32 - b;
+  int bad = 0;
+  long long first = LLONG_MAX;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n / 8; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 8 * v;
+    int32_t q[MA][8];
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      const int32_t* p = c.s[m] + n0;
+      if (V256) {
+        uint64_t u0, u1, u2, u3;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(u0), "=l"(u1), "=l"(u2), "=l"(u3)
+                     : "l"(p));
+        const uint64_t u[4] = {u0, u1, u2, u3};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          q[m][2 * k] = (int32_t)(uint32_t)u[k];
+          q[m][2 * k + 1] = (int32_t)(uint32_t)(u[k] >> 32);
+        }
+      } else {
+        const int4 a = __ldcs(reinterpret_cast<const int4*>(p));
+        const int4 e = __ldcs(reinterpret_cast<const int4*>(p + 4));
+        q[m][0] = a.x; q[m][1] = a.y; q[m][2] = a.z; q[m][3] = a.w;
+        q[m][4] = e.x; q[m][5] = e.y; q[m][6] = e.z; q[m][7] = e.w;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      const int mp = m == 0 ? M - 1 : m - 1;
+      int32_t d0[8], d1[8];
+      uint32_t badm = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int32_t cc = q[m][i];
+        d0[i] = (int32_t)((uint32_t)cc << sh) >> sh;
+        d1[i] = q[mp][i] + (cc >> b) + ((cc >> (b - 1)) & 1);
+        uint32_t f = ((uint32_t)(d0[i] + 128) | (uint32_t)(d1[i] + 128)) > 255u;
+        if (rc) f |= (cc > h32) | (cc < -h32);
+        badm |= f << i;
+      }
+      if (badm) {
+        bad += __popc(badm);
+        const long long idx = (long long)m * n + n0 + (__ffs(badm) - 1);
+        first = idx < first ? idx : first;
+      }
+      int8_t* p0 = planes + ((int64_t)m * 2) * n + n0;
+      __stcs(reinterpret_cast<uint2*>(p0), make_uint2(pack4(d0[0], d0[1], d0[2], d0[3]), pack4(d0[4], d0[5], d0[6], d0[7])));
+      __stcs(reinterpret_cast<uint2*>(p0 + n), make_uint2(pack4(d1[0], d1[1], d1[2], d1[3]), pack4(d1[4], d1[5], d1[6], d1[7])));
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
 // Entangle into L digit planes of a general base 2^b (b != 8), 4 positions per
 // thread, all M streams loaded first; digits via digits_b.
 template <int MT, int L>
@@ -533,9 +606,27 @@ extern "C" ne_status ne_entangle_limbs(const ne_config* cfg, ne_cstreams32 c, in
     return NE_EINVAL;
   if (limb_bits != 8) {
     if (L > 4) return NE_EINVAL;  // base-2^b digit planes: L <= 4
-    const int grid = grid_for(n_total / 4, kThreads);
     cudaStream_t s = cs(stream);
     const int64_t hi = range_hi(cfg);
+    if (L == 2 && limb_bits == cfg->l && limb_bits <= 31) {
+      bool a32 = true;
+      for (int m = 0; m < cfg->M; ++m) a32 &= (reinterpret_cast<uintptr_t>(c.s[m]) & 31u) == 0;
+      const int g8 = grid_for(n_total / 8, kThreads);
+#define NE_PAIR(MV)                                                                                   \
+  if (a32)                                                                                            \
+    k_entangle_pair<MV, true><<<g8, kThreads, 0, s>>>(c, cfg->M, limb_bits, hi, n_total, planes, diag); \
+  else                                                                                                \
+    k_entangle_pair<MV, false><<<g8, kThreads, 0, s>>>(c, cfg->M, limb_bits, hi, n_total, planes, diag)
+      switch (cfg->M) {
+        case 3: NE_PAIR(3); break;
+        case 4: NE_PAIR(4); break;
+        case 8: NE_PAIR(8); break;
+        default: NE_PAIR(0); break;
+      }
+#undef NE_PAIR
+      return launch_status();
+    }
+    const int grid = grid_for(n_total / 4, kThreads);
 #define NE_DIG(MV, LV) k_entangle_digits<MV, LV><<<grid, kThreads, 0, s>>>(c, cfg->M, cfg->l, hi, n_total, limb_bits, planes, diag)
 #define NE_DIG_L(MV)                                                                   \
   switch (L) {                                                                         \

@@ -689,3 +689,109 @@ def test_base_l_digit_plan(O, M, bound):
     ne.ne_entangle_limbs(cfg, to_streams(big), L, planes, diag, limb_bits=b)
     dd = ne.diag_read(diag)
     assert dd["range_violations"] >= 1
+
+
+@pytest.mark.parametrize("M,align32", [(3, True), (3, False), (4, False), (5, True)])
+def test_pair_digits_extremes_and_alignment(O, M, align32):
+    """k_entangle_pair (the 32-bit two-digit path): digits equal the oracle's
+    entangled value on representable entries; every non-representable entry
+    (extreme int32 values included) is counted and the first one is named;
+    16-B-only aligned streams take the 2 x 128-bit load path."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L, b = 2, cfg.l
+    N = 4096 + 16
+    c = gen(O, 9, 1, M, N, -127, 128)
+    specials = [2**31 - 1, -2**31, 200, -129, 128, -128, 127, 2**b, -(2**b), 2**b + 5, 2**(b - 1), -(2**(b - 1)) - 1]
+    for k, v in enumerate(specials):
+        c[k % M, 37 + 11 * k] = v
+    E = O.entangle(ocfg, c)                        # exact (int64, w = 64)
+    d0 = ((E + 2 ** (b - 1)) % 2 ** b) - 2 ** (b - 1)  # sext_b(E)
+    d1 = (E - d0) >> b
+    ok = (d0 >= -128) & (d0 <= 127) & (d1 >= -128) & (d1 <= 127)
+    off = 0 if align32 else 4                      # int32 elements: 16-B offset
+    streams = []
+    for m in range(M):
+        t = torch.zeros(N + 8, dtype=torch.int32, device="cuda")
+        t[off:off + N] = torch.from_numpy(c[m].astype(np.int32)).cuda()
+        streams.append(t[off:off + N])
+    planes = torch.empty(M * L * N, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_limbs(cfg, streams, L, planes, diag, limb_bits=b)
+    p = planes.cpu().numpy().astype(np.int64).reshape(M, L, N)
+    assert (p[:, 0][ok] == d0[ok]).all() and (p[:, 1][ok] == d1[ok]).all()
+    dd = ne.diag_read(diag)
+    bad = np.flatnonzero((~ok).reshape(-1))
+    assert dd["range_violations"] == len(bad) and len(bad) > 0
+    assert dd["first_bad"] == bad.min()
+
+
+@pytest.mark.parametrize("K,cols", [(64, 128), (192, 260), (16, 5), (4096, 384)])
+def test_prep_b_ragged(O, K, cols):
+    """B (K x cols int32) -> Bt (cols x K int8): partial 64 x 128 tiles,
+    scalar tail columns, and out-of-int8 entries counted with the first named."""
+    B = O.gen_uniform(3, 5, 0, -128, 128, K * cols)
+    B[7 % (K * cols)] = 300
+    B[(K * cols) // 2] = -129
+    Bt = torch.empty(cols * K, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, cols, Bt, diag)
+    ref = B.reshape(K, cols).T.astype(np.int64)
+    got = Bt.cpu().numpy().astype(np.int64).reshape(cols, K)
+    okm = (ref >= -128) & (ref <= 127)
+    assert (got[okm] == ref[okm]).all()
+    dd = ne.diag_read(diag)
+    bad = np.flatnonzero((B < -128) | (B > 127))
+    assert dd["range_violations"] == len(bad) and dd["first_bad"] == bad.min()
+
+
+# ------------------------------------------------------------------ GEMM with the fused check epilogue
+@pytest.mark.parametrize("M,plan,bound,rows,cols,K,r", [
+    (3, "pair", 64, 256, 512, 256, 0), (3, "pair", 127, 384, 256, 128, 2), (3, "b256", 64, 256, 384, 256, 1),
+    (4, "pair", 100, 128, 256, 256, 3), (8, "b256", 32, 256, 256, 128, 5), (5, "pair", 100, 128, 128, 128, 4),
+    (8, "pair", 32, 512, 1024, 256, 6), (3, "pair", 100, 1024, 2048, 256, 1)])
+def test_gemm_limbs_check_fused(O, M, plan, bound, rows, cols, K, r):
+    """ne_op_gemm_limbs_check == oracle GEMM (delta) + oracle disentangle/check
+    (d_hat, flags, count, first) on clean data and with one stream's operand
+    corrupted (a fault inside that stream's computation); the tile counters
+    come back zeroed, and a second call on the same counters agrees.  M = 5
+    exercises the unfused fallback."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    if plan == "pair":
+        L, b = ne.ne_gemm_limb_plan(cfg, bound)
+        assert (L, b) == (2, cfg.l)
+    else:
+        L, b = 4, 8
+    A = np.stack([O.gen_uniform(8, 4, m, -bound, bound + 1, rows * K) for m in range(M)])
+    B = O.gen_uniform(8, 5, 0, -128, 128, K * cols)
+    planes = torch.empty(M * L * rows * K, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_limbs(cfg, to_streams(A), L, planes, diag, limb_bits=b)
+    Bt = torch.empty(cols * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, cols, Bt, diag)
+    cnt = torch.zeros(ne.ne_gemm_check_workspace(rows, cols) // 4, dtype=torch.int32, device="cuda")
+    n = rows * cols
+    for corrupt in (False, True, False):
+        if corrupt:
+            # a fault in stream s's operand: one digit of one row changes
+            s, row, k = (r + 1) % M, rows // 2 + 3, 5
+            planes.view(M, L, rows, K)[s, 0, row, k] += 1
+        pl = planes.cpu().numpy().astype(np.int64).reshape(M, L, rows, K)
+        E = sum(pl[:, i] * (2 ** (b * i)) for i in range(L))          # the operands the GPU consumes
+        delta_ref = O.op_gemm(ocfg, E, B.reshape(K, cols)).reshape(M, -1)
+        d_ref, f_ref, nf_ref = O.disentangle_check(ocfg, delta_ref, r)
+        out, d_out = empty_streams(M, n), empty_streams(M, n)
+        bm = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        dg = ne.diag_new()
+        ne.ne_op_gemm_limbs_check(cfg, planes, L, Bt, rows, cols, K, out, r, d_out, cnt, bm, dg, limb_bits=b)
+        torch.cuda.synchronize()
+        assert (to_np(out) == delta_ref).all()
+        assert (to_np(d_out) == d_ref).all()
+        assert (bitmap_to_flags(bm, n) == f_ref).all()
+        dd = ne.diag_read(dg)
+        assert dd["fault_positions"] == nf_ref
+        assert (nf_ref > 0) == corrupt
+        if corrupt:
+            assert dd["first_fault"] == int(np.flatnonzero(f_ref)[0])
+            planes.view(M, L, rows, K)[s, 0, row, k] -= 1
+        assert int(cnt.abs().sum()) == 0
+    assert ne.diag_read(diag)["range_violations"] == 0
