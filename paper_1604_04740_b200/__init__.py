@@ -34,6 +34,7 @@ EXPORTS = (
     "ne_op_scale", "ne_op_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
     "ne_gemm_check_workspace", "ne_op_gemm_limbs_check",
+    "ne_conv_geometry", "ne_entangle_limbs_conv", "ne_conv_prep_taps", "ne_op_conv_limbs",
     "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
     "ne_abft_encode", "ne_abft_encode_limbs", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
@@ -86,6 +87,10 @@ _SIGS = {
     "ne_op_gemm": [_PCFG, Streams, _VP, _I64, _I64, _I64, C.c_int, _I32, _I32, Streams, _VP, _SZ, _VP, _VP],
     "ne_gemm_prep_b": [_VP, _I64, _I64, _VP, _VP, _VP],
     "ne_op_gemm_limbs": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _VP],
+    "ne_conv_geometry": [_I64, _I32, C.POINTER(_I64), C.POINTER(_I64)],
+    "ne_entangle_limbs_conv": [_PCFG, Streams, _I64, _I32, _I32, _I32, _I32, _VP, _VP, _VP],
+    "ne_conv_prep_taps": [_VP, _I32, _I32, _VP, _VP, _VP],
+    "ne_op_conv_limbs": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I32, _I32, Streams, _VP],
     "ne_gemm_check_workspace": [_I64, _I64, C.POINTER(_SZ)],
     "ne_op_gemm_limbs_check": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _I32, Streams, _VP, _VP, _VP,
                                _VP],
@@ -293,6 +298,30 @@ def ne_op_gemm_limbs(cfg: Config, planes: torch.Tensor, L: int, Bt: torch.Tensor
                      out, limb_bits: int = 8) -> None:
     _call("ne_op_gemm_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, limb_bits, _ptr(Bt, torch.int8), rows, cols,
           K, _streams(out, torch.int64), _stream())
+
+
+def ne_conv_geometry(n: int, taps: int) -> tuple[int, int]:
+    """(Kpad, plane_len) of the tensor-core convolution."""
+    kp, pl = _I64(), _I64()
+    _call("ne_conv_geometry", n, taps, C.byref(kp), C.byref(pl))
+    return kp.value, pl.value
+
+
+def ne_entangle_limbs_conv(cfg: Config, c, taps: int, correlate: int, L: int, planes: torch.Tensor, diag=None,
+                           limb_bits: int = 8) -> None:
+    _call("ne_entangle_limbs_conv", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), taps, correlate, L,
+          limb_bits, _ptr(planes, torch.int8), _ptr(diag, torch.int64), _stream())
+
+
+def ne_conv_prep_taps(g: torch.Tensor, correlate: int, Gt: torch.Tensor, diag=None) -> None:
+    _call("ne_conv_prep_taps", _ptr(g, torch.int32), g.numel(), correlate, _ptr(Gt, torch.int8),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_op_conv_limbs(cfg: Config, planes: torch.Tensor, L: int, Gt: torch.Tensor, n: int, taps: int, correlate: int,
+                     out, limb_bits: int = 8) -> None:
+    _call("ne_op_conv_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, limb_bits, _ptr(Gt, torch.int8), n, taps,
+          correlate, _streams(out, torch.int64), _stream())
 
 
 def ne_gemm_check_workspace(rows: int, cols: int) -> int:

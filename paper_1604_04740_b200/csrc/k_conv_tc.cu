@@ -1,0 +1,201 @@
+// k_conv_tc.cu — circular convolution / cross-correlation of the entangled
+// streams on the tensor cores (NEXT-2 of SURVEY §8(f)): the direct form
+// (reading R12)
+//     out_m[n] = sum_{j<T} g[j] eps_m[(n - j) mod N]        (conv)
+//     out_m[n] = sum_{j<T} g[j] eps_m[(n + j) mod N]        (correlation)
+// written as a Toeplitz GEMM.  Output block b = outputs 128 b .. 128 b + 127:
+//     out_m[128 b + i] = sum_{k<Kpad} W_b[k] G[i][k],
+//     W_b[k] = eps_m[(128 b + k - s0) mod N],   s0 = T - 1 (conv) or 0 (corr),
+//     G[i][k] = g[i + s0 - k] (conv) or g[k - i] (corr), 0 outside [0, T),
+// with Kpad = roundup(T + 127, 64).  eps_m is held as L int8 digit planes
+// (the GEMM's digit plan), circularly extended so that window
+// row b is the contiguous bytes [128 b, 128 b + Kpad) of each plane:
+//     plane_{m,d}[t] = digit d of eps_m[(t - s0) mod N],  0 <= t < plane_len.
+// The GEMM is k_gemm_tc in Toeplitz mode (rows = blocks, cols = 128, K = Kpad,
+// B = G); every D_{m,d} G product is exact in int32 (Kpad * 2^14 < 2^31) and
+// recombined in int64.  The last N mod 128 outputs (a partial block) are
+// computed by k_conv_tail from the same planes.  Redundancy: Kpad / T MACs
+// per useful MAC (3x at T = 64, 1.03x at T = 4500), paid on a pipe ~100x
+// faster than the IMAD path of k_conv.cu.
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "ne_internal.cuh"
+
+namespace ne {
+
+ne_status launch_conv_tc(int M, int L, int b, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
+                         int64_t Kpad, int64_t nblocks, const ne_streams& C, cudaStream_t s);
+
+static int64_t conv_kpad(int64_t taps) { return (taps + 127 + 63) / 64 * 64; }
+static int64_t conv_plane_len(int64_t n, int64_t taps) {
+  const int64_t nb_all = (n + 127) / 128;
+  return (128 * nb_all + conv_kpad(taps) + 127) / 128 * 128;
+}
+
+// a1 into circularly extended digit planes: 4 consecutive t per thread, all M
+// streams (each c_m[n] is read once per t and used by streams m and m+1).
+// The range assertion (a0) counts every position once: t in [s0, s0 + N).
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n, int64_t s0,
+                       int64_t plane_len, int L, int b, int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  int bad = 0;
+  long long first = LLONG_MAX;
+  const int64_t nq = plane_len / 4;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    int32_t cv[MA][4];
+    int64_t pos[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = 4 * q + u;
+      int64_t p = (t - s0) % n;
+      if (p < 0) p += n;
+      pos[u] = p;
+#pragma unroll
+      for (int m = 0; m < (MT > 0 ? MT : M); ++m) cv[m][u] = __ldg(c.s[m] + p);
+    }
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      const int mp = m == 0 ? M - 1 : m - 1;
+      uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t cc = cv[m][u];
+        const int64_t x = (int64_t)((uint64_t)cc + ((uint64_t)(int64_t)cv[mp][u] << l));
+        int8_t d[8];
+        const bool ok = digits_b(x, b, L, d);
+        for (int j = 0; j < L; ++j) w[j] |= (uint32_t)(uint8_t)d[j] << (8 * u);
+        const int64_t t = 4 * q + u;
+        if (t >= s0 && t < s0 + n && (cc > hi || cc < -hi || !ok)) {
+          ++bad;
+          const long long idx = (long long)m * n + pos[u];
+          first = idx < first ? idx : first;
+        }
+      }
+      for (int j = 0; j < L; ++j)
+        __stcs(reinterpret_cast<unsigned int*>(planes + ((int64_t)m * L + j) * plane_len + 4 * q), w[j]);
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// G (128 x Kpad int8, K contiguous): conv G[i][k] = g[i + T - 1 - k],
+// correlation G[i][k] = g[k - i]; taps outside [-128, 127] are range
+// violations (counted once per tap, first_bad = tap index).
+__global__ void __launch_bounds__(kThreads)
+k_conv_prep_taps(const int32_t* __restrict__ g, int64_t T, int correlate, int64_t Kpad, int8_t* __restrict__ Gt,
+                 ne_diag* __restrict__ diag) {
+  int bad = 0;
+  long long first = LLONG_MAX;
+  const int64_t total = 128 * Kpad;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / Kpad, k = e % Kpad;
+    const int64_t j = correlate ? k - i : i + T - 1 - k;
+    const int32_t v = (j >= 0 && j < T) ? __ldg(g + j) : 0;
+    Gt[e] = (int8_t)v;
+    if (i == 0 && e < T) {  // tap e checked once
+      const int32_t ge = __ldg(g + e);
+      if (ge < -128 || ge > 127) {
+        ++bad;
+        first = e < first ? e : first;
+      }
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// the last n - 128 nb outputs of every stream (a partial block): one warp per
+// output, lanes split k, exact int32 digit sums (Kpad 2^14 < 2^31) reduced by
+// shuffles, recombined in int64
+__global__ void __launch_bounds__(kThreads)
+k_conv_tail(const int8_t* __restrict__ planes, int M, int L, int b, int64_t plane_len, const int8_t* __restrict__ Gt,
+            int64_t Kpad, int64_t nb, int64_t n, const __grid_constant__ ne_streams out) {
+  const int64_t tail = n - 128 * nb;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (wid >= (int64_t)M * tail) return;
+  const int m = (int)(wid / tail);
+  const int64_t i = wid % tail;
+  uint64_t acc = 0;
+  for (int d = 0; d < L; ++d) {
+    const int8_t* w = planes + ((int64_t)m * L + d) * plane_len + 128 * nb;
+    int32_t s = 0;
+    for (int64_t k = lane; k < Kpad; k += 32) s += (int32_t)w[k] * (int32_t)Gt[i * Kpad + k];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    acc += (uint64_t)(int64_t)s << (b * d);
+  }
+  if (lane == 0) out.s[m][128 * nb + i] = (int64_t)acc;
+}
+
+}  // namespace ne
+
+using namespace ne;
+
+extern "C" ne_status ne_conv_geometry(int64_t n_total, int32_t taps, int64_t* kpad, int64_t* plane_len) {
+  if (n_total < 1 || taps < 1 || !kpad || !plane_len) return NE_EINVAL;
+  *kpad = conv_kpad(taps);
+  *plane_len = conv_plane_len(n_total, taps);
+  return NE_OK;
+}
+
+extern "C" ne_status ne_entangle_limbs_conv(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t taps,
+                                            int32_t correlate, int32_t L, int32_t limb_bits, int8_t* planes,
+                                            ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total < 1 || taps < 1 || (correlate != 0 && correlate != 1) || L < 1 || L > 4 || limb_bits < 8 ||
+      limb_bits > 63 || !planes || !aligned16(planes))
+    return NE_EINVAL;
+  for (int m = 0; m < cfg->M; ++m)
+    if (!c.s[m]) return NE_EINVAL;
+  const int64_t plen = conv_plane_len(n_total, taps);
+  const int64_t s0 = correlate ? 0 : (int64_t)taps - 1;
+  const int grid = grid_for(plen / 4, kThreads);
+  cudaStream_t s = cs(stream);
+  const int64_t hi = range_hi(cfg);
+  switch (cfg->M) {
+    case 3: k_entangle_conv_planes<3><<<grid, kThreads, 0, s>>>(c, 3, cfg->l, hi, n_total, s0, plen, L, limb_bits, planes, diag); break;
+    case 4: k_entangle_conv_planes<4><<<grid, kThreads, 0, s>>>(c, 4, cfg->l, hi, n_total, s0, plen, L, limb_bits, planes, diag); break;
+    case 8: k_entangle_conv_planes<8><<<grid, kThreads, 0, s>>>(c, 8, cfg->l, hi, n_total, s0, plen, L, limb_bits, planes, diag); break;
+    default: k_entangle_conv_planes<0><<<grid, kThreads, 0, s>>>(c, cfg->M, cfg->l, hi, n_total, s0, plen, L, limb_bits, planes, diag); break;
+  }
+  return launch_status();
+}
+
+extern "C" ne_status ne_conv_prep_taps(const int32_t* g, int32_t taps, int32_t correlate, int8_t* Gt, ne_diag* diag,
+                                       ne_stream_t stream) {
+  if (!g || taps < 1 || (correlate != 0 && correlate != 1) || !Gt || !aligned16(Gt)) return NE_EINVAL;
+  const int64_t kp = conv_kpad(taps);
+  k_conv_prep_taps<<<grid_for(128 * kp, kThreads), kThreads, 0, cs(stream)>>>(g, taps, correlate, kp, Gt, diag);
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_conv_limbs(const ne_config* cfg, const int8_t* planes, int32_t L, int32_t limb_bits,
+                                      const int8_t* Gt, int64_t n_total, int32_t taps, int32_t correlate,
+                                      ne_streams out, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total < 1 || taps < 1 || (correlate != 0 && correlate != 1) || L < 1 || L > 4 || limb_bits < 8 ||
+      limb_bits > 63 || !planes || !Gt || !aligned16(planes) || !aligned16(Gt))
+    return NE_EINVAL;
+  const int64_t kp = conv_kpad(taps);
+  if (kp > 131072) return NE_ENOTSUP;  // int32 digit sums stay exact
+  for (int m = 0; m < cfg->M; ++m)
+    if (!out.s[m] || !aligned16(out.s[m])) return NE_EINVAL;
+  const int64_t plen = conv_plane_len(n_total, taps);
+  const int64_t nb = n_total / 128;
+  cudaStream_t s = cs(stream);
+  if (nb > 0 && (st = launch_conv_tc(cfg->M, L, limb_bits, planes, plen / 128, Gt, kp, nb, out, s)) != NE_OK)
+    return st;
+  const int64_t tail = n_total - 128 * nb;
+  if (tail > 0) {
+    const int64_t warps = (int64_t)cfg->M * tail;
+    k_conv_tail<<<(unsigned)((warps * 32 + kThreads - 1) / kThreads), kThreads, 0, s>>>(planes, cfg->M, L, limb_bits,
+                                                                                       plen, Gt, kp, nb, n_total, out);
+  }
+  return launch_status();
+}

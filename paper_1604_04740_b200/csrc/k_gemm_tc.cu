@@ -182,6 +182,19 @@ struct ChkArgs {
   int l;
 };
 
+// Operand geometry.  GEMM: A is the [M*L*rows][K] stack of limb planes and C_m
+// is [rows][cols].  Toeplitz (circular convolution as a GEMM, k_conv_tc.cu):
+// each limb plane is a circularly extended 1-D stream of a_plane_rows * 128
+// bytes viewed as [a_plane_rows][128]; window row b of K bytes starts at byte
+// 128 b, so the 64-byte K-chunk kb of row b is the chunk (kb & 1) of row
+// b + kb / 2 of that view (no overlapping tensor-map strides needed).  Output
+// rows >= out_rows are clipped by the TMA store (tensor bounds).
+struct Geo {
+  int64_t a_plane_rows;
+  int64_t out_rows;
+  int toeplitz;
+};
+
 __device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps only
   asm volatile("bar.sync 1, %0;" ::"n"(32 * 8) : "memory");
 }
@@ -304,7 +317,7 @@ template <int L, int BN, int STAGES, int SW, int CL, int CHK>
 __global__ void __launch_bounds__(threads_for<CHK>(), 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
           const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
-          const __grid_constant__ ChkArgs chk) {
+          const __grid_constant__ ChkArgs chk, const Geo geo) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   constexpr int BK = CF::BK;
   static_assert(L * BN <= 512, "TMEM holds 512 columns");
@@ -374,14 +387,16 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           unsigned char* st = smem + s * CF::kStage;
           mbar_expect_tx(&full[s], (uint32_t)CF::kStage);
+          const int32_t kc = geo.toeplitz ? ((kb * BK) & 127) : kb * BK;
+          const int64_t radd = geo.toeplitz ? ((int64_t)kb * BK) >> 7 : 0;
 #pragma unroll
           for (int i = 0; i < L; ++i) {
             unsigned char* dst = st + i * CF::kATile + crank * CF::kARows * BK;
-            const int32_t grow = (int32_t)(((int64_t)m * L + i) * rows + row0 + crank * CF::kARows);
+            const int32_t grow = (int32_t)(((int64_t)m * L + i) * geo.a_plane_rows + row0 + crank * CF::kARows + radd);
             if (CL > 1)
-              tma_load_2d_mc(&mapA, &full[s], dst, kb * BK, grow, cmask);
+              tma_load_2d_mc(&mapA, &full[s], dst, kc, grow, cmask);
             else
-              tma_load_2d(&mapA, &full[s], dst, kb * BK, grow);
+              tma_load_2d(&mapA, &full[s], dst, kc, grow);
           }
           tma_load_2d(&mapB, &full[s], st + L * CF::kATile, kb * BK, (int32_t)col0);
         }
@@ -596,16 +611,19 @@ static bool make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_
 
 template <int L, int BN, int STAGES, int SW, int CL, int CHK = 0>
 static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
-                     int limb_bits, const ne_streams& C, cudaStream_t s, const ChkArgs* chk = nullptr) {
+                     int limb_bits, const ne_streams& C, cudaStream_t s, const ChkArgs* chk = nullptr,
+                     const Geo* geo_in = nullptr) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   if (cols % (BN * CL) != 0 || K % CF::BK != 0) return NE_ENOTSUP;
+  const Geo geo = geo_in ? *geo_in : Geo{rows, rows, 0};
   CUtensorMap ma, mb;
-  if (!make_map(&ma, planes, (uint64_t)K, (uint64_t)M * L * rows, SW, CF::kARows)) return NE_ECUDA;
+  if (!make_map(&ma, planes, geo.toeplitz ? 128 : (uint64_t)K, (uint64_t)M * L * geo.a_plane_rows, SW, CF::kARows))
+    return NE_ECUDA;
   if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, BN)) return NE_ECUDA;
   if (M > 8) return NE_ENOTSUP;
   OutMaps om;
   for (int m = 0; m < M; ++m)
-    if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)rows)) return NE_ECUDA;
+    if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)geo.out_rows)) return NE_ECUDA;
   auto kern = k_gemm_tc<L, BN, STAGES, SW, CL, CHK>;
   ChkArgs ca{};
   if (CHK > 0) ca = *chk;
@@ -637,7 +655,7 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   }
   if (nclusters > n_work) nclusters = n_work;
   lc.gridDim = dim3((unsigned)(nclusters * CL));
-  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, ca) != cudaSuccess) return NE_ECUDA;
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, ca, geo) != cudaSuccess) return NE_ECUDA;
   return launch_status();
 }
 
@@ -676,6 +694,23 @@ static ne_status gemm_tc_dispatch(int M, int L, int b, const int8_t* planes, con
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s) {
   return gemm_tc_dispatch<0>(M, L, b, planes, Bt, rows, cols, K, C, s, nullptr);
+}
+
+// Circular convolution / correlation of M entangled streams as a Toeplitz
+// GEMM (k_conv_tc.cu): planes = M*L extended limb planes of plane_rows * 128
+// bytes; Gt = [128][Kpad] int8 tap matrix; C_m = [nblocks][128] int64 (the
+// first 128 * nblocks outputs of stream m).  One 128-output column tile.
+ne_status launch_conv_tc(int M, int L, int b, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
+                         int64_t Kpad, int64_t nblocks, const ne_streams& C, cudaStream_t s) {
+  const tc::Geo geo{plane_rows, nblocks, 1};
+  const int64_t rows = (nblocks + 127) / 128 * 128;
+  switch (L) {
+    case 1: return tc::run<1, 128, 8, 64, 1>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
+    case 2: return tc::run<2, 128, 6, 64, 1>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
+    case 3: return tc::run<3, 128, 5, 64, 1>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
+    case 4: return tc::run<4, 128, 4, 64, 1>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
+    default: return NE_ENOTSUP;
+  }
 }
 
 // The GEMM with the fused disentangle + check epilogue: M in {3, 4, 8} and

@@ -795,3 +795,69 @@ def test_gemm_limbs_check_fused(O, M, plan, bound, rows, cols, K, r):
             planes.view(M, L, rows, K)[s, 0, row, k] -= 1
         assert int(cnt.abs().sum()) == 0
     assert ne.diag_read(diag)["range_violations"] == 0
+
+
+# ------------------------------------------------------------------ tensor-core (Toeplitz) convolution
+@pytest.mark.parametrize("M,N,T,correlate,bound", [
+    (3, 65536, 64, 0, 127), (3, 65536 + 77, 64, 1, 127), (4, 1000, 100, 0, 1000), (8, 5000, 4500, 0, 100),
+    (3, 100, 300, 1, 127), (3, 384, 1, 0, 127), (5, 4096, 64, 1, 100), (3, 20000, 1000, 0, 127)])
+def test_conv_tensor_core(O, M, N, T, correlate, bound):
+    """ne_op_conv_limbs (tcgen05 Toeplitz GEMM + partial-block tail) equals the
+    oracle's circular convolution / correlation of the entangled streams,
+    bit for bit; the extended planes hold digit d of eps[(t - s0) mod N]."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L, b = ne.ne_gemm_limb_plan(cfg, bound)
+    c = gen(O, 11, 1, M, N, -bound, bound + 1)
+    c[:, 0] = bound
+    c[:, -1] = -bound
+    g = O.gen_uniform(11, 3, 0, -128, 128, T)
+    g[0] = -128
+    eps = O.entangle(ocfg, c)
+    kp, plen = ne.ne_conv_geometry(N, T)
+    assert kp % 64 == 0 and kp >= T + 127 and plen % 128 == 0
+    planes = torch.empty(M * L * plen, dtype=torch.int8, device="cuda")
+    Gt = torch.empty(128 * kp, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_limbs_conv(cfg, to_streams(c), T, correlate, L, planes, diag, limb_bits=b)
+    ne.ne_conv_prep_taps(dev(g, torch.int32), correlate, Gt, diag)
+    out = empty_streams(M, N)
+    ne.ne_op_conv_limbs(cfg, planes, L, Gt, N, T, correlate, out, limb_bits=b)
+    torch.cuda.synchronize()
+    assert ne.diag_read(diag)["range_violations"] == 0
+    assert (to_np(out) == O.op_conv(ocfg, eps, g, bool(correlate))).all()
+    pl = planes.cpu().numpy().astype(np.int64).reshape(M, L, plen)
+    rec = sum(pl[:, d] * (2 ** (b * d)) for d in range(L))
+    s0 = 0 if correlate else T - 1
+    idx = (np.arange(plen) - s0) % N
+    assert (rec == eps[:, idx]).all()
+
+
+def test_conv_tensor_core_range_violations(O):
+    """Taps outside int8 and inputs outside the digit plan are counted once
+    each and the first is named (tap index; m*N + n for inputs)."""
+    M, N, T = 3, 3000, 70
+    cfg = ne.ne_config_for(M)
+    L, b = ne.ne_gemm_limb_plan(cfg, 127)
+    c = gen(O, 12, 1, M, N, -100, 100)
+    c[1, 17] = 300      # |c| > 127: not two int8 digits
+    c[2, 5] = -129
+    g = O.gen_uniform(12, 3, 0, -100, 100, T)
+    g[9] = 128
+    g[40] = -300
+    kp, plen = ne.ne_conv_geometry(N, T)
+    planes = torch.empty(M * L * plen, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_limbs_conv(cfg, to_streams(c), T, 0, L, planes, diag, limb_bits=b)
+    d = ne.diag_read(diag)
+    # c[2,5] = -129 alone is still exact (d0 = -129 needs 9 bits: flagged), c[1,17] flagged;
+    # the neighbour stream's digit d1 = c_{m-1} also leaves int8 for stream m+1
+    E = O.entangle(O.config_for(M, 64), c)
+    d0 = ((E + 2 ** (b - 1)) % 2 ** b) - 2 ** (b - 1)
+    d1 = (E - d0) >> b
+    bad = np.flatnonzero((~((d0 >= -128) & (d0 <= 127) & (d1 >= -128) & (d1 <= 127))).reshape(-1))
+    assert d["range_violations"] == len(bad) and d["first_bad"] == bad.min()
+    Gt = torch.empty(128 * kp, dtype=torch.int8, device="cuda")
+    diag2 = ne.diag_new()
+    ne.ne_conv_prep_taps(dev(g, torch.int32), 0, Gt, diag2)
+    d2 = ne.diag_read(diag2)
+    assert d2["range_violations"] == 2 and d2["first_bad"] == 9
