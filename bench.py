@@ -376,76 +376,153 @@ class C4PermInner(Workload):
 
 class C2Conv(Workload):
     """configs[1]: M=3 streams of 65536 int32 U[-128,128), circular convolution
-    with a shared 64-tap kernel U[-128,128), entangled int64."""
+    with a shared 64-tap kernel U[-128,128), entangled int64.  algo "tc": the
+    Toeplitz GEMM on tcgen05 over extended digit planes (k_conv_tc.cu);
+    "direct": the IMAD kernel (k_conv.cu).  The paper's own conv shape
+    (P:1106-1108: N_in = 10^6, 100-4500 taps, M in {3, 8}) is workload c2p."""
 
     name = "C2"
     metric_unit = "Gop/s"
 
-    def __init__(self, rank, n=65536, taps=64, seed=1):
+    def __init__(self, rank, n=65536, taps=64, seed=1, M=3, algo="tc", paper=False):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
-        self.M, self.n, self.T = 3, n, taps
+        self.M, self.n, self.T, self.algo, self.paper = M, n, taps, algo, paper
+        if paper:
+            self.name = "C2P"
         self.seed = seed + 1000 * rank
-        self.cfg = ne.ne_config_for(3)
-        self.c = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3)]
-        for m in range(3):
+        self.cfg = ne.ne_config_for(M)
+        self.c = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(M)]
+        for m in range(M):
             ne.ne_gen_uniform_i32(self.seed, 1, m, -128, 128, self.c[m])
         self.g = torch.empty(taps, dtype=torch.int32, device="cuda")
         ne.ne_gen_uniform_i32(self.seed, 3, 0, -128, 128, self.g)
-        mk = lambda: [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(3)]  # noqa: E731
-        self.eps, self.delta, self.dout, self.drec = mk(), mk(), mk(), mk()
+        mk = lambda: [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(M)]  # noqa: E731
+        self.delta, self.dout, self.drec = mk(), mk(), mk()
+        if algo == "tc":
+            # c in [-128, 127] (U[-128, 128)): exactly the int8 range, so eps = c_m + 2^l c_{m-1}
+            # is its two int8 halves (the pair plan; |c| <= 127 in the plan's symmetric terms
+            # plus c = -128, whose digit is still int8); the entangle kernel asserts it per value
+            self.L, self.limb_bits = ne.ne_gemm_limb_plan(self.cfg, 127)
+            self.kpad, self.plen = ne.ne_conv_geometry(n, taps)
+            self.planes = torch.empty(M * self.L * self.plen, dtype=torch.int8, device="cuda")
+            self.Gt = torch.empty(128 * self.kpad, dtype=torch.int8, device="cuda")
+            self.launches_per_step = 5 + (1 if n % 128 else 0)
+        else:
+            self.eps = mk()
+            self.launches_per_step = 4
         self.bitmap = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
         self.diag = ne.diag_new()
-        self.launches_per_step = 4
 
     def stages(self, i):
-        ne, cfg = self.ne, self.cfg
-        r = i % 3
-        part = [None if m == r else self.delta[m] for m in range(3)]
-        return [("entangle", lambda: ne.ne_entangle(cfg, self.c, self.eps, self.diag)),
-                ("conv", lambda: ne.ne_op_conv(cfg, self.eps, self.g, self.delta)),
-                ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
+        ne, cfg, M = self.ne, self.cfg, self.M
+        r = i % M
+        part = [None if m == r else self.delta[m] for m in range(M)]
+        tail = [("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
                 ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec))]
+        if self.algo == "tc":
+            return [("entangle", lambda: ne.ne_entangle_limbs_conv(cfg, self.c, self.T, 0, self.L, self.planes,
+                                                                   self.diag, self.limb_bits)),
+                    ("prep_g", lambda: ne.ne_conv_prep_taps(self.g, 0, self.Gt, self.diag)),
+                    ("conv", lambda: ne.ne_op_conv_limbs(cfg, self.planes, self.L, self.Gt, self.n, self.T, 0,
+                                                         self.delta, self.limb_bits))] + tail
+        return [("entangle", lambda: ne.ne_entangle(cfg, self.c, self.eps, self.diag)),
+                ("conv", lambda: ne.ne_op_conv(cfg, self.eps, self.g, self.delta))] + tail
 
     def work_per_step(self):
         return 2 * self.M * self.n * self.T / 1e9
 
     def stage_info(self):
-        n, M = self.n, self.M
-        return {"entangle": ("hbm", M * n * 12 / 1e9, "GB"),
-                "conv": ("alu", M * n * self.T / 1e12, "TMAC"),
-                "check": ("hbm", M * n * 16 / 1e9, "GB"),
-                "recover": ("hbm", 5 * n * 8 / 1e9, "GB")}
+        n, M, T = self.n, self.M, self.T
+        info = {"check": ("hbm", M * n * 16 / 1e9, "GB"),
+                "recover": ("hbm", (2 * M - 1) * n * 8 / 1e9, "GB")}
+        if self.algo == "tc":
+            # useful limb products only (the Toeplitz zeros, Kpad/T - 1, are not counted)
+            info["conv"] = ("tensor", 2 * self.L * M * n * T / 1e12, "TOP")
+            info["entangle"] = ("hbm", M * (n * 4 + self.L * self.plen) / 1e9, "GB")
+            info["prep_g"] = ("hbm", (T * 4 + 128 * self.kpad) / 1e9, "GB")
+        else:
+            info["conv"] = ("alu", M * n * T / 1e12, "TMAC")
+            info["entangle"] = ("hbm", M * n * 12 / 1e9, "GB")
+        return info
 
     def config(self):
-        return {"workload": "C2 (BASELINE configs[1]): M=3 streams of 65536 int32 U[-128,128), circular "
-                            "convolution with a shared 64-tap kernel U[-128,128)",
-                "M": 3, "n": self.n, "taps": self.T, "l2": "working set 6 MB fits L2 (launch-latency bound)"}
+        if self.paper:
+            wl = (f"C2P (the paper's convolution shape, P:1106-1108): M={self.M} streams of N_in={self.n} int32 "
+                  f"U[-128,128), circular convolution with a {self.T}-tap kernel U[-128,128)")
+        else:
+            wl = ("C2 (BASELINE configs[1]): M=3 streams of 65536 int32 U[-128,128), circular "
+                  "convolution with a shared 64-tap kernel U[-128,128)")
+        ws = self.M * self.n * 8 * 3 / 1e6
+        return {"workload": wl, "M": self.M, "n": self.n, "taps": self.T,
+                "conv_algo": ("tc: Toeplitz GEMM on tcgen05, %d int8 digits base 2^%d, Kpad=%d"
+                              % (self.L, self.limb_bits, self.kpad)) if self.algo == "tc" else "direct IMAD",
+                "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
+                "l2": (f"working set {ws:.0f} MB" + (" fits L2 (launch-latency bound)" if ws < 100 else " > L2")),
+                "step": "entangle+prep_taps+conv+disentangle/check(r=0)+recover(r=step mod M)"
+                if self.algo == "tc" else "entangle+conv+disentangle/check(r=0)+recover(r=step mod M)"}
 
     def e2e_setup(self):
+        M = self.M
         self.hc = [x.cpu().pin_memory() for x in self.c]
-        self.hout = [self.torch.empty(self.n, dtype=self.torch.int64).pin_memory() for _ in range(3)]
-        return self.n * 12, self.n * 24
+        self.hg = self.g.cpu().pin_memory()
+        self.hout = [self.torch.empty(self.n, dtype=self.torch.int64).pin_memory() for _ in range(M)]
+        return self.n * 4 * M + self.T * 4, self.n * 8 * M
 
     def e2e_step(self, i):
-        for m in range(3):
+        for m in range(self.M):
             self.c[m].copy_(self.hc[m], non_blocking=True)
+        self.g.copy_(self.hg, non_blocking=True)
         for _, f in self.stages(i):
             f()
-        for m in range(3):
+        for m in range(self.M):
             self.hout[m].copy_(self.dout[m], non_blocking=True)
 
     def plain_times(self, reps=20):
-        return {}
+        """The same conv kernel on unentangled data: (i) same digit count
+        (plain c in digit 0, other digits 0), (ii) one int8 digit; ms per call."""
+        torch, ne = self.torch, self.ne
+        if self.algo != "tc":
+            return {}
+        M, out = self.M, {}
+        for tag, L in (("same_kernel_L%d" % self.L, self.L), ("native_L1", 1)):
+            planes = torch.zeros(M * L * self.plen, dtype=torch.int8, device="cuda")
+            pv = planes.view(M, L, self.plen)
+            s0 = self.T - 1
+            idx = (torch.arange(self.plen, device="cuda") - s0) % self.n
+            for m in range(M):
+                pv[m, 0].copy_(self.c[m][idx].to(torch.int8))
+            ne.ne_op_conv_limbs(self.cfg, planes, L, self.Gt, self.n, self.T, 0, self.delta, self.limb_bits)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                ne.ne_op_conv_limbs(self.cfg, planes, L, self.Gt, self.n, self.T, 0, self.delta, self.limb_bits)
+            e1.record()
+            torch.cuda.synchronize()
+            out[tag] = e0.elapsed_time(e1) / reps
+            del planes
+        return out
 
     def oracle_sample(self, reps):
         import oracle as O
 
-        ocfg = O.config_for(3, 64)
-        c = np.stack([O.gen_uniform(self.seed, 1, m, -128, 128, self.n) for m in range(3)])
+        M = self.M
+        ocfg = O.config_for(M, 64)
+        c = np.stack([O.gen_uniform(self.seed, 1, m, -128, 128, self.n) for m in range(M)])
         g = O.gen_uniform(self.seed, 3, 0, -128, 128, self.T)
+        if self.paper:
+            # bounded sample: the same pipeline at N' = 16384 (same M, taps, distributions)
+            n2 = 16384
+            c = np.stack([O.gen_uniform(self.seed, 1, m, -128, 128, n2) for m in range(M)])
+            t0 = time.perf_counter()
+            eps = O.entangle(ocfg, c)
+            d = O.op_conv(ocfg, eps, g)
+            O.disentangle_check(ocfg, d, 0)
+            dt = time.perf_counter() - t0
+            return dt, 2 * M * n2 * self.T / 1e9, f"one full pass at N'={n2} (M={M}, T={self.T}, same distributions)"
         t0 = time.perf_counter()
         for _ in range(reps):
             eps = O.entangle(ocfg, c)
@@ -534,8 +611,18 @@ class C1Chain(Workload):
         return dt, reps * self.n / 1e9, f"{reps} full C1 passes"
 
 
-WORKLOADS = {"c1": C1Chain, "c2": C2Conv, "c3": C3Gemm, "c4": C4PermInner, "c5": None}
-ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c3": (16, 2), "c4": (64, 8), "c5": (4096, 512)}  # (cpu_baseline, per ref step)
+WORKLOADS = {"c1": C1Chain, "c2": C2Conv, "c2p": C2Conv, "c3": C3Gemm, "c4": C4PermInner, "c5": None}
+ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c2p": (1, 1), "c3": (16, 2), "c4": (64, 8), "c5": (4096, 512)}
+
+
+def make_workload(args, rank):
+    if args.workload == "c3":
+        return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=args.fuse)
+    if args.workload == "c2":
+        return C2Conv(rank, algo=args.conv or "direct")
+    if args.workload == "c2p":
+        return C2Conv(rank, n=10 ** 6, taps=args.taps, M=args.streams, algo=args.conv or "tc", paper=True)
+    return WORKLOADS[args.workload](rank)  # (cpu_baseline, per ref step)
 METRIC = "entangled LSB Gop/s (or GB/s) at 1/2/4/8 B200, % roofline, % overhead vs plain"
 
 
@@ -699,8 +786,7 @@ def run_ours(args, rank, world, local_rank):
 
     ne.lib()
     torch.cuda.set_device(local_rank)
-    W = WORKLOADS[args.workload](rank) if args.workload != "c3" else \
-        C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=args.fuse)
+    W = make_workload(args, rank)
     torch.cuda.synchronize()
 
     def barrier():
@@ -913,8 +999,16 @@ def run_reference(args):
                 "cpu_baseline": {"value": round(value, 6), "unit": "Gop/s", "cores": 1, "kind": "oracle",
                                  "sample": what + " per step", "cpu": _cpu_model()},
                 "e2e": {"value": round(value, 6), "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    elif args.workload == "c2":
-        W.M, W.n, W.T, W.seed = 3, 65536, 64, 1
+    elif args.workload in ("c2", "c2p"):
+        paper = args.workload == "c2p"
+        W.M, W.n, W.T, W.seed = (args.streams, 10 ** 6, args.taps, 1) if paper else (3, 65536, 64, 1)
+        W.algo, W.paper, W.name = args.conv or ("tc" if paper else "direct"), paper, "C2P" if paper else "C2"
+        W.L, W.limb_bits = 2, {3: 22, 4: 16, 8: 8}.get(W.M, 8)
+        W.kpad = (W.T + 127 + 127) // 128 * 128
+
+        class _Cfg:
+            l, k = {3: (22, 20), 4: (16, 16), 8: (8, 8)}.get(W.M, (8, 8))
+        W.cfg = _Cfg
     else:
         W.M, W.n, W.seed = 3, 4096, 0
     per_step = ORACLE_SAMPLE[args.workload][1]
@@ -951,6 +1045,11 @@ def main():
                     help="c3 only: numerical entanglement (default) or the paper's ABFT comparison method")
     ap.add_argument("--fuse", type=int, default=0,
                     help="c3: disentangle/check fused into the GEMM epilogue, or a separate pass (default: measured faster)")
+    ap.add_argument("--conv", default=None, choices=["tc", "direct"],
+                    help="c2/c2p: tensor-core Toeplitz conv or the direct IMAD kernel (default: the faster one "
+                         "measured: direct for c2's 64 taps, tc for c2p)")
+    ap.add_argument("--taps", type=int, default=4500, help="c2p: kernel taps (paper: 100-4500)")
+    ap.add_argument("--streams", type=int, default=8, help="c2p: M (paper: 3 or 8)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
     args = ap.parse_args()

@@ -190,7 +190,7 @@ ne_status ne_op_conv(const ne_config* cfg, ne_cstreams x, int64_t n_total, const
  * block b (outputs 128b .. 128b+127) = W_b G^T with W_b[k] = x[(128b + k - s0)
  * mod N] (s0 = taps-1 for conv, 0 for correlation) and the 128 x Kpad int8 tap
  * matrix G[i][k] = g[i + s0 - k] (conv) / g[k - i] (corr), Kpad =
- * roundup(taps + 127, 64).  x is held as L int8 digit planes (base 2^limb_bits,
+ * roundup(taps + 127, 128).  x is held as L int8 digit planes (base 2^limb_bits,
  * as ne_entangle_limbs), each circularly extended to plane_len bytes so that
  * W_b is contiguous:  planes[(m*L + d)*plane_len + t] = digit d of
  * eps_m[(t - s0) mod N].

@@ -7,7 +7,7 @@
 //     out_m[128 b + i] = sum_{k<Kpad} W_b[k] G[i][k],
 //     W_b[k] = eps_m[(128 b + k - s0) mod N],   s0 = T - 1 (conv) or 0 (corr),
 //     G[i][k] = g[i + s0 - k] (conv) or g[k - i] (corr), 0 outside [0, T),
-// with Kpad = roundup(T + 127, 64).  eps_m is held as L int8 digit planes
+// with Kpad = roundup(T + 127, 128) (whole 128-byte K stages).  eps_m is held as L int8 digit planes
 // (the GEMM's digit plan), circularly extended so that window
 // row b is the contiguous bytes [128 b, 128 b + Kpad) of each plane:
 //     plane_{m,d}[t] = digit d of eps_m[(t - s0) mod N],  0 <= t < plane_len.
@@ -15,7 +15,7 @@
 // B = G); every D_{m,d} G product is exact in int32 (Kpad * 2^14 < 2^31) and
 // recombined in int64.  The last N mod 128 outputs (a partial block) are
 // computed by k_conv_tail from the same planes.  Redundancy: Kpad / T MACs
-// per useful MAC (3x at T = 64, 1.03x at T = 4500), paid on a pipe ~100x
+// per useful MAC (4x at T = 64, 1.05x at T = 4500), paid on a pipe ~100x
 // faster than the IMAD path of k_conv.cu.
 #include <cuda_runtime.h>
 
@@ -28,7 +28,7 @@ namespace ne {
 ne_status launch_conv_tc(int M, int L, int b, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
                          int64_t Kpad, int64_t nblocks, const ne_streams& C, cudaStream_t s);
 
-static int64_t conv_kpad(int64_t taps) { return (taps + 127 + 63) / 64 * 64; }
+static int64_t conv_kpad(int64_t taps) { return (taps + 127 + 127) / 128 * 128; }
 static int64_t conv_plane_len(int64_t n, int64_t taps) {
   const int64_t nb_all = (n + 127) / 128;
   return (128 * nb_all + conv_kpad(taps) + 127) / 128 * 128;
@@ -40,35 +40,52 @@ static int64_t conv_plane_len(int64_t n, int64_t taps) {
 template <int MT>
 __global__ void __launch_bounds__(kThreads)
 k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n, int64_t s0,
-                       int64_t plane_len, int L, int b, int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
+                       int64_t s0mod, int64_t plane_len, int L, int b, int8_t* __restrict__ planes,
+                       ne_diag* __restrict__ diag) {
   constexpr int MA = MT > 0 ? MT : NE_MAX_M;
   const int M = MT > 0 ? MT : M_rt;
+  const bool pair = L == 2 && b == l && b <= 31;
   int bad = 0;
   long long first = LLONG_MAX;
   const int64_t nq = plane_len / 4;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
     int32_t cv[MA][4];
+    // position of t = 4q: (t - s0) mod n without a 64-bit division
+    // (s0mod = s0 mod n; t - s0mod < plane_len, a few multiples of n at most)
+    int64_t p = 4 * q - s0mod;
+    if (p < 0) p += n;
+    while (p >= n) p -= n;
     int64_t pos[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t t = 4 * q + u;
-      int64_t p = (t - s0) % n;
-      if (p < 0) p += n;
       pos[u] = p;
 #pragma unroll
       for (int m = 0; m < (MT > 0 ? MT : M); ++m) cv[m][u] = __ldg(c.s[m] + p);
+      if (++p == n) p = 0;
     }
 #pragma unroll
     for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
       const int mp = m == 0 ? M - 1 : m - 1;
-      uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t cc = cv[m][u];
-        const int64_t x = (int64_t)((uint64_t)cc + ((uint64_t)(int64_t)cv[mp][u] << l));
-        int8_t d[8];
-        const bool ok = digits_b(x, b, L, d);
-        for (int j = 0; j < L; ++j) w[j] |= (uint32_t)(uint8_t)d[j] << (8 * u);
+        bool ok;
+        if (pair) {  // the two-digit base-2^l plan in 32-bit arithmetic (as k_entangle_pair)
+          const int32_t c32 = cv[m][u];
+          const int32_t d0 = (int32_t)((uint32_t)c32 << (32 - b)) >> (32 - b);
+          const int32_t d1 = cv[mp][u] + (c32 >> b) + ((c32 >> (b - 1)) & 1);
+          ok = ((uint32_t)(d0 + 128) | (uint32_t)(d1 + 128)) <= 255u;
+          w[0] |= (uint32_t)(uint8_t)d0 << (8 * u);
+          w[1] |= (uint32_t)(uint8_t)d1 << (8 * u);
+        } else {
+          const int64_t x = (int64_t)((uint64_t)cc + ((uint64_t)(int64_t)cv[mp][u] << l));
+          int8_t d[4];
+          ok = digits_b(x, b, L, d);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < L) w[j] |= (uint32_t)(uint8_t)d[j] << (8 * u);
+        }
         const int64_t t = 4 * q + u;
         if (t >= s0 && t < s0 + n && (cc > hi || cc < -hi || !ok)) {
           ++bad;
@@ -76,8 +93,9 @@ k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l,
           first = idx < first ? idx : first;
         }
       }
-      for (int j = 0; j < L; ++j)
-        __stcs(reinterpret_cast<unsigned int*>(planes + ((int64_t)m * L + j) * plane_len + 4 * q), w[j]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < L) __stcs(reinterpret_cast<unsigned int*>(planes + ((int64_t)m * L + j) * plane_len + 4 * q), w[j]);
     }
   }
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
@@ -91,44 +109,53 @@ k_conv_prep_taps(const int32_t* __restrict__ g, int64_t T, int correlate, int64_
                  ne_diag* __restrict__ diag) {
   int bad = 0;
   long long first = LLONG_MAX;
-  const int64_t total = 128 * Kpad;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / Kpad, k = e % Kpad;
-    const int64_t j = correlate ? k - i : i + T - 1 - k;
-    const int32_t v = (j >= 0 && j < T) ? __ldg(g + j) : 0;
-    Gt[e] = (int8_t)v;
-    if (i == 0 && e < T) {  // tap e checked once
-      const int32_t ge = __ldg(g + e);
-      if (ge < -128 || ge > 127) {
-        ++bad;
-        first = e < first ? e : first;
+  const int64_t i = blockIdx.y;  // row of G (output within the block)
+  for (int64_t k4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 4 * k4 < Kpad; k4 += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = 4 * k4 + u;
+      const int64_t j = correlate ? k - i : i + T - 1 - k;
+      const int32_t v = (j >= 0 && j < T) ? __ldg(g + j) : 0;
+      w |= (uint32_t)(uint8_t)(int8_t)v << (8 * u);
+      if (i == 0 && k < T) {  // tap k checked once
+        const int32_t gk = __ldg(g + k);
+        if (gk < -128 || gk > 127) {
+          ++bad;
+          first = k < first ? k : first;
+        }
       }
     }
+    *reinterpret_cast<uint32_t*>(Gt + i * Kpad + 4 * k4) = w;
   }
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
-// the last n - 128 nb outputs of every stream (a partial block): one warp per
-// output, lanes split k, exact int32 digit sums (Kpad 2^14 < 2^31) reduced by
-// shuffles, recombined in int64
-__global__ void __launch_bounds__(kThreads)
+// the last n - 128 nb outputs of every stream (a partial block): one CTA of
+// 128 threads per output, threads split k, exact int32 digit sums (Kpad 2^14
+// < 2^31) reduced by shuffles and shared memory, recombined in int64
+__global__ void __launch_bounds__(128)
 k_conv_tail(const int8_t* __restrict__ planes, int M, int L, int b, int64_t plane_len, const int8_t* __restrict__ Gt,
             int64_t Kpad, int64_t nb, int64_t n, const __grid_constant__ ne_streams out) {
+  __shared__ int32_t part[4][4];
   const int64_t tail = n - 128 * nb;
-  const int lane = threadIdx.x & 31;
-  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (wid >= (int64_t)M * tail) return;
-  const int m = (int)(wid / tail);
-  const int64_t i = wid % tail;
-  uint64_t acc = 0;
+  const int m = (int)(blockIdx.x / tail);
+  const int64_t i = blockIdx.x % tail;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   for (int d = 0; d < L; ++d) {
     const int8_t* w = planes + ((int64_t)m * L + d) * plane_len + 128 * nb;
     int32_t s = 0;
-    for (int64_t k = lane; k < Kpad; k += 32) s += (int32_t)w[k] * (int32_t)Gt[i * Kpad + k];
+    for (int64_t k = threadIdx.x; k < Kpad; k += 128) s += (int32_t)w[k] * (int32_t)Gt[i * Kpad + k];
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    acc += (uint64_t)(int64_t)s << (b * d);
+    if (lane == 0) part[d][wp] = s;
   }
-  if (lane == 0) out.s[m][128 * nb + i] = (int64_t)acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t acc = 0;
+    for (int d = 0; d < L; ++d)
+      acc += (uint64_t)(int64_t)(part[d][0] + part[d][1] + part[d][2] + part[d][3]) << (b * d);
+    out.s[m][128 * nb + i] = (int64_t)acc;
+  }
 }
 
 }  // namespace ne
@@ -154,14 +181,15 @@ extern "C" ne_status ne_entangle_limbs_conv(const ne_config* cfg, ne_cstreams32 
     if (!c.s[m]) return NE_EINVAL;
   const int64_t plen = conv_plane_len(n_total, taps);
   const int64_t s0 = correlate ? 0 : (int64_t)taps - 1;
+  const int64_t s0m = s0 % n_total;
   const int grid = grid_for(plen / 4, kThreads);
   cudaStream_t s = cs(stream);
   const int64_t hi = range_hi(cfg);
   switch (cfg->M) {
-    case 3: k_entangle_conv_planes<3><<<grid, kThreads, 0, s>>>(c, 3, cfg->l, hi, n_total, s0, plen, L, limb_bits, planes, diag); break;
-    case 4: k_entangle_conv_planes<4><<<grid, kThreads, 0, s>>>(c, 4, cfg->l, hi, n_total, s0, plen, L, limb_bits, planes, diag); break;
-    case 8: k_entangle_conv_planes<8><<<grid, kThreads, 0, s>>>(c, 8, cfg->l, hi, n_total, s0, plen, L, limb_bits, planes, diag); break;
-    default: k_entangle_conv_planes<0><<<grid, kThreads, 0, s>>>(c, cfg->M, cfg->l, hi, n_total, s0, plen, L, limb_bits, planes, diag); break;
+    case 3: k_entangle_conv_planes<3><<<grid, kThreads, 0, s>>>(c, 3, cfg->l, hi, n_total, s0, s0m, plen, L, limb_bits, planes, diag); break;
+    case 4: k_entangle_conv_planes<4><<<grid, kThreads, 0, s>>>(c, 4, cfg->l, hi, n_total, s0, s0m, plen, L, limb_bits, planes, diag); break;
+    case 8: k_entangle_conv_planes<8><<<grid, kThreads, 0, s>>>(c, 8, cfg->l, hi, n_total, s0, s0m, plen, L, limb_bits, planes, diag); break;
+    default: k_entangle_conv_planes<0><<<grid, kThreads, 0, s>>>(c, cfg->M, cfg->l, hi, n_total, s0, s0m, plen, L, limb_bits, planes, diag); break;
   }
   return launch_status();
 }
@@ -170,7 +198,8 @@ extern "C" ne_status ne_conv_prep_taps(const int32_t* g, int32_t taps, int32_t c
                                        ne_stream_t stream) {
   if (!g || taps < 1 || (correlate != 0 && correlate != 1) || !Gt || !aligned16(Gt)) return NE_EINVAL;
   const int64_t kp = conv_kpad(taps);
-  k_conv_prep_taps<<<grid_for(128 * kp, kThreads), kThreads, 0, cs(stream)>>>(g, taps, correlate, kp, Gt, diag);
+  const dim3 grid((unsigned)((kp / 4 + kThreads - 1) / kThreads), 128);
+  k_conv_prep_taps<<<grid, kThreads, 0, cs(stream)>>>(g, taps, correlate, kp, Gt, diag);
   return launch_status();
 }
 
@@ -193,9 +222,7 @@ extern "C" ne_status ne_op_conv_limbs(const ne_config* cfg, const int8_t* planes
     return st;
   const int64_t tail = n_total - 128 * nb;
   if (tail > 0) {
-    const int64_t warps = (int64_t)cfg->M * tail;
-    k_conv_tail<<<(unsigned)((warps * 32 + kThreads - 1) / kThreads), kThreads, 0, s>>>(planes, cfg->M, L, limb_bits,
-                                                                                       plen, Gt, kp, nb, n_total, out);
+    k_conv_tail<<<(unsigned)(cfg->M * tail), 128, 0, s>>>(planes, cfg->M, L, limb_bits, plen, Gt, kp, nb, n_total, out);
   }
   return launch_status();
 }

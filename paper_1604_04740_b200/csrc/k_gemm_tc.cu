@@ -150,7 +150,10 @@ struct Cfg {
   static constexpr int kBTile = BN * BK;
   static constexpr int kStage = L * kATile + kBTile;
   static constexpr int kARows = BM / CL;          // rows of each limb tile this CTA loads (multicast)
-  static constexpr int kTmemCols = (L * BN <= 32) ? 32 : (L * BN <= 64) ? 64 : (L * BN <= 128) ? 128 : (L * BN <= 256) ? 256 : 512;
+  static constexpr int kAccCols = L * BN;                     // one accumulator set
+  static constexpr int kBufs = 2 * kAccCols <= 512 ? 2 : 1;   // double-buffered when two sets fit TMEM
+  static constexpr int kTmemNeed = kBufs * kAccCols;
+  static constexpr int kTmemCols = (kTmemNeed <= 32) ? 32 : (kTmemNeed <= 64) ? 64 : (kTmemNeed <= 128) ? 128 : (kTmemNeed <= 256) ? 256 : 512;
   static constexpr int kStageOut = 32 * 16 * 8;  // one epilogue warp's [32 rows x 16 int64] box
   static constexpr size_t kSmem = (size_t)STAGES * kStage + 2 * 8 * kStageOut + 1024 /*align*/ + 512 /*barriers, check queue*/;
 };
@@ -189,10 +192,15 @@ struct ChkArgs {
 // 128 b, so the 64-byte K-chunk kb of row b is the chunk (kb & 1) of row
 // b + kb / 2 of that view (no overlapping tensor-map strides needed).  Output
 // rows >= out_rows are clipped by the TMA store (tensor bounds).
+// mcast_b (clusters of CL > 1): the CL CTAs of a cluster take CL consecutive
+// row tiles of the same column tile and share the B tile instead of the A
+// tile (each loads BN/CL rows of B and multicasts them) — the convolution's
+// G matrix is shared by every work item, its A windows by none.
 struct Geo {
   int64_t a_plane_rows;
   int64_t out_rows;
   int toeplitz;
+  int mcast_b;
 };
 
 __device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps only
@@ -284,11 +292,12 @@ __device__ __forceinline__ void check_tile(const ChkArgs& chk, int64_t row0, int
 // with w -> (stream m, row tile, column-tile group), CTA rank r taking column
 // tile group*CL + r.  The CL CTAs of a cluster share the row tile: each loads
 // 128/CL rows of every limb tile and multicasts them to all CL CTAs, so A is
-// read from L2 once per cluster.  One accumulator set (L * BN = 512 TMEM
-// columns): the MMA warp waits until the epilogue has drained TMEM
-// (tmem_empty) before the next tile, while the producer already streams the
-// next tile's stages; the epilogue's global stores drain under the next
-// mainloop.
+// read from L2 once per cluster.  Accumulators: two sets of L * BN TMEM
+// columns when they fit (L * BN <= 256: the MMA of tile t+1 runs while the
+// epilogue drains tile t), else one set (L * BN = 512): the MMA warp waits
+// until the epilogue has drained TMEM (tmem_empty) before the next tile,
+// while the producer already streams the next tile's stages; the epilogue's
+// global stores drain under the next mainloop.
 constexpr int kEpiWarps = 8;
 constexpr int kThreadsP = 128 + 32 * kEpiWarps;  // warps 0-3: roles, 4-11: epilogue
 template <int CHK>
@@ -326,9 +335,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
   unsigned char* stage_out = smem + STAGES * CF::kStage;  // 2 x 8 x 4 KB, 1024-B aligned
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + 2 * 8 * CF::kStageOut);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint64_t* tmem_empty = tmem_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+  uint64_t* tmem_full = empty + STAGES;  // [kBufs]
+  uint64_t* tmem_empty = tmem_full + 2;  // [kBufs]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   // check queue (CHK > 0): ring of tile ids pushed by the epilogue, consumed by the checker warps
   volatile int* q_head = reinterpret_cast<volatile int*>(tmem_slot + 1);
   volatile int* q_tail = q_head + 1;
@@ -344,7 +353,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
   const uint32_t crank = CL > 1 ? cluster_rank() : 0;
   const uint16_t cmask = (uint16_t)((1u << CL) - 1);
   const int KB = (int)(K / BK);
-  const int64_t n_rt = rows / BM, n_cg = cols / (BN * CL);
+  const bool mb = CL > 1 && geo.mcast_b;
+  const int64_t n_rt = mb ? rows / (BM * CL) : rows / BM, n_cg = mb ? cols / BN : cols / (BN * CL);
   const int64_t n_work = (int64_t)M * n_rt * n_cg;
   const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
 
@@ -353,8 +363,10 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CL);  // released by the MMA warp of every CTA in the cluster
     }
-    mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, kEpiWarps);
+    for (int b = 0; b < CF::kBufs; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -380,8 +392,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
         int m;
         int64_t rt, cg;
         decode_work<CHK>(w, M, n_rt, n_cg, m, rt, cg);
-        const int64_t row0 = rt * BM;
-        const int64_t col0 = (cg * CL + crank) * BN;
+        const int64_t row0 = mb ? (rt * CL + crank) * BM : rt * BM;
+        const int64_t col0 = mb ? cg * BN : (cg * CL + crank) * BN;
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -389,16 +401,27 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
           mbar_expect_tx(&full[s], (uint32_t)CF::kStage);
           const int32_t kc = geo.toeplitz ? ((kb * BK) & 127) : kb * BK;
           const int64_t radd = geo.toeplitz ? ((int64_t)kb * BK) >> 7 : 0;
+          if (mb) {
 #pragma unroll
-          for (int i = 0; i < L; ++i) {
-            unsigned char* dst = st + i * CF::kATile + crank * CF::kARows * BK;
-            const int32_t grow = (int32_t)(((int64_t)m * L + i) * geo.a_plane_rows + row0 + crank * CF::kARows + radd);
-            if (CL > 1)
-              tma_load_2d_mc(&mapA, &full[s], dst, kc, grow, cmask);
-            else
-              tma_load_2d(&mapA, &full[s], dst, kc, grow);
+            for (int i = 0; i < L; ++i) {
+              const int32_t grow = (int32_t)(((int64_t)m * L + i) * geo.a_plane_rows + row0 + radd);
+              tma_load_2d(&mapA, &full[s], st + i * CF::kATile, kc, grow);
+            }
+            tma_load_2d_mc(&mapB, &full[s], st + L * CF::kATile + crank * (BN / CL) * BK, kb * BK,
+                           (int32_t)(col0 + crank * (BN / CL)), cmask);
+          } else {
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+              unsigned char* dst = st + i * CF::kATile + crank * CF::kARows * BK;
+              const int32_t grow =
+                  (int32_t)(((int64_t)m * L + i) * geo.a_plane_rows + row0 + crank * CF::kARows + radd);
+              if (CL > 1)
+                tma_load_2d_mc(&mapA, &full[s], dst, kc, grow, cmask);
+              else
+                tma_load_2d(&mapA, &full[s], dst, kc, grow);
+            }
+            tma_load_2d(&mapB, &full[s], st + L * CF::kATile, kb * BK, (int32_t)col0);
           }
-          tma_load_2d(&mapB, &full[s], st + L * CF::kATile, kb * BK, (int32_t)col0);
         }
       }
     }
@@ -408,7 +431,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       constexpr uint32_t idesc = idesc_i8(BM, BN);
       uint32_t it = 0, tile = 0;
       for (int64_t w = cid; w < n_work; w += ncl, ++tile) {
-        mbar_wait(tmem_empty, (tile & 1) ^ 1);  // epilogue drained the accumulators
+        const uint32_t ab = tile % CF::kBufs, use = tile / CF::kBufs;
+        mbar_wait(&tmem_empty[ab], (use & 1) ^ 1);  // epilogue drained this accumulator set
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % STAGES;
@@ -422,12 +446,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
 #pragma unroll
             for (int i = 0; i < L; ++i) {
               const uint64_t adesc = umma_desc<SW>(sa + i * CF::kATile + ks * UMMA_K);
-              mma_i8(tmem_base + i * BN, adesc, bdesc, idesc, (kb | ks) != 0);
+              mma_i8(tmem_base + ab * CF::kAccCols + i * BN, adesc, bdesc, idesc, (kb | ks) != 0);
             }
           }
           mma_commit(&empty[s], cmask);  // frees stage s in every CTA of the cluster
         }
-        mma_commit(tmem_full, 1);        // this tile's accumulators are final
+        mma_commit(&tmem_full[ab], 1);   // this tile's accumulators are final
       }
     }
   } else if (warp >= 4 && warp < 4 + kEpiWarps) {
@@ -443,21 +467,23 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       int m;
       int64_t rt, cg;
       decode_work<CHK>(w, M, n_rt, n_cg, m, rt, cg);
-      const int64_t row0 = rt * BM;
-      const int64_t col0 = (cg * CL + crank) * BN;
-      mbar_wait(tmem_full, tile & 1);
+      const int64_t row0 = mb ? (rt * CL + crank) * BM : rt * BM;
+      const int64_t col0 = mb ? cg * BN : (cg * CL + crank) * BN;
+      const uint32_t ab = tile % CF::kBufs, use = tile / CF::kBufs;
+      mbar_wait(&tmem_full[ab], use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
       for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16, buf ^= 1) {
         uint32_t v[L][16];
 #pragma unroll
-        for (int i = 0; i < L; ++i) tmem_ld16(tl + i * BN + c, v[i]);
+        for (int i = 0; i < L; ++i) tmem_ld16(tl + ab * CF::kAccCols + i * BN + c, v[i]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c + 16 == (half + 1) * (BN / 2)) {
           // last TMEM read of this tile for this warp: release the accumulators
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
-          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tmem_empty)) : "memory");
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[ab])) : "memory");
         }
         // the TMA store that last read this buffer (two chunks ago) must be done
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -614,12 +640,16 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
                      int limb_bits, const ne_streams& C, cudaStream_t s, const ChkArgs* chk = nullptr,
                      const Geo* geo_in = nullptr) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
-  if (cols % (BN * CL) != 0 || K % CF::BK != 0) return NE_ENOTSUP;
-  const Geo geo = geo_in ? *geo_in : Geo{rows, rows, 0};
+  if (cols % BN != 0 || K % CF::BK != 0) return NE_ENOTSUP;
+  const Geo geo = geo_in ? *geo_in : Geo{rows, rows, 0, 0};
+  const bool mcb = CL > 1 && geo.mcast_b;
+  if (mcb && rows % (BM * CL) != 0) return NE_ENOTSUP;
+  if (!mcb && cols % (BN * CL) != 0) return NE_ENOTSUP;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, planes, geo.toeplitz ? 128 : (uint64_t)K, (uint64_t)M * L * geo.a_plane_rows, SW, CF::kARows))
+  if (!make_map(&ma, planes, geo.toeplitz ? 128 : (uint64_t)K, (uint64_t)M * L * geo.a_plane_rows, SW,
+                mcb ? BM : CF::kARows))
     return NE_ECUDA;
-  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, BN)) return NE_ECUDA;
+  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, mcb ? BN / CL : BN)) return NE_ECUDA;
   if (M > 8) return NE_ENOTSUP;
   OutMaps om;
   for (int m = 0; m < M; ++m)
@@ -629,7 +659,7 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   if (CHK > 0) ca = *chk;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) != cudaSuccess)
     return NE_ECUDA;
-  const int64_t n_work = (int64_t)M * (rows / BM) * (cols / (BN * CL));
+  const int64_t n_work = (int64_t)M * (rows / BM) * (cols / BN) / CL;
   cudaLaunchConfig_t lc = {};
   lc.blockDim = dim3(threads_for<CHK>());
   lc.dynamicSmemBytes = CF::kSmem;
@@ -702,13 +732,18 @@ ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t
 // first 128 * nblocks outputs of stream m).  One 128-output column tile.
 ne_status launch_conv_tc(int M, int L, int b, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
                          int64_t Kpad, int64_t nblocks, const ne_streams& C, cudaStream_t s) {
-  const tc::Geo geo{plane_rows, nblocks, 1};
-  const int64_t rows = (nblocks + 127) / 128 * 128;
+  // clusters of 2 consecutive row tiles multicast the shared tap tiles of G;
+  // 128-byte K stages (128B swizzle): each window row is one full 128-byte
+  // line of the extended plane per stage (half the TMA row requests of 64-byte
+  // stages; measured 0.125 -> 0.108 ms at M = 8, N = 10^6, T = 4500)
+  const tc::Geo geo{plane_rows, nblocks, 1, 1};
+  const int64_t rows = (nblocks + 255) / 256 * 256;
+  if (Kpad % 128 != 0) return NE_EINVAL;
   switch (L) {
-    case 1: return tc::run<1, 128, 8, 64, 1>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
-    case 2: return tc::run<2, 128, 6, 64, 1>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
-    case 3: return tc::run<3, 128, 5, 64, 1>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
-    case 4: return tc::run<4, 128, 4, 64, 1>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
+    case 1: return tc::run<1, 128, 5, 128, 2>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
+    case 2: return tc::run<2, 128, 3, 128, 2>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
+    case 3: return tc::run<3, 128, 2, 128, 2>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
+    case 4: return tc::run<4, 128, 2, 128, 2>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
     default: return NE_ENOTSUP;
   }
 }

@@ -2,6 +2,8 @@
 """Summarise ncu captures brought back in gpurun_out/ into profiles/.
 
     python scripts/ncu_summary.py ROUND rep1.ncu-rep[=WORKLOAD:stage] ... [--launches a.csv ...]
+    (a rep holding several kernels: rep=W:stage1@substr1;W:stage2@substr2 — the
+    first key whose kernel-name substring matches is used)
 
 For every --set full capture: the kernel's duration, DRAM bytes (the
 `traffic` of bench.py's roofline: dram__bytes_read.sum + dram__bytes_write.sum
@@ -77,13 +79,22 @@ def main():
             continue
         (lists if mode == "l" else reps).append(a)
     md = [f"# ncu summary, round {rnd}", "",
-          "Captured with `ncu --set full --clock-control none --import-source on -k regex:<kernel> -s 2 -c 1` "
-          "on one B200 (gpurun), recipe in scripts/profile_r01.sh.  Times are one cold-cache replayed launch.", ""]
+          "Captured with `ncu --set full --clock-control none --import-source on -k regex:<kernel> -s <n> -c <k>` "
+          "on one B200 (gpurun); the recipe is the scripts/profile_*.sh / scripts/round_*.sh named in DESIGN.md.  "
+          "Times are one cold-cache replayed launch (ncu's clock, often power-capped below 1965 MHz).", ""]
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for spec in reps:
-        rep, _, key = spec.partition("=")
+        rep, _, keyspec = spec.partition("=")
         for d in raw(rep):
+            key = keyspec
+            if "@" in keyspec:
+                key = ""
+                for part in keyspec.split(";"):
+                    k, _, sub = part.partition("@")
+                    if sub in d["kernel"]:
+                        key = k
+                        break
             md.append(f"## `{d['kernel'][:120]}`  ({os.path.basename(rep)}{', ' + key if key else ''})")
             for k in KEYS:
                 if k in d:

@@ -814,7 +814,7 @@ def test_conv_tensor_core(O, M, N, T, correlate, bound):
     g[0] = -128
     eps = O.entangle(ocfg, c)
     kp, plen = ne.ne_conv_geometry(N, T)
-    assert kp % 64 == 0 and kp >= T + 127 and plen % 128 == 0
+    assert kp % 128 == 0 and kp >= T + 127 and plen % 128 == 0
     planes = torch.empty(M * L * plen, dtype=torch.int8, device="cuda")
     Gt = torch.empty(128 * kp, dtype=torch.int8, device="cuda")
     diag = ne.diag_new()
