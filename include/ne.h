@@ -22,9 +22,11 @@
  *            interleave the M streams position-major: x[n*M + m].  Matrices
  *            are row-major and dense.  Every stream pointer must be 16-byte
  *            aligned (128-bit vector access) or the call returns NE_EINVAL.
- * Words      w = 64 only: entangled and output values are int64 held in
+ * Words      w = 64: entangled and output values are int64 held in
  *            64-bit two's-complement containers; plain
- *            inputs are int32.  LSB ops wrap mod 2^64, which is exact for
+ *            inputs are int32.  The ne_*_w32 calls are the paper's own w = 32
+ *            instantiation on int32 containers; every other call
+ *            requires cfg->w == 64 (NE_ECONFIG otherwise).  LSB ops wrap mod 2^64, which is exact for
  *            every certified (in-range) result (reading R9).
  * Errors     Two channels.  (1) The returned ne_status, synchronous: argument
  *            and configuration errors, and CUDA launch errors
@@ -68,6 +70,7 @@ typedef enum {
 typedef struct { int64_t* s[NE_MAX_M]; } ne_streams;
 typedef struct { const int64_t* s[NE_MAX_M]; } ne_cstreams;
 typedef struct { const int32_t* s[NE_MAX_M]; } ne_cstreams32;
+typedef struct { int32_t* s[NE_MAX_M]; } ne_streams32;   /* w = 32 containers (ne_*_w32) */
 
 /* Device-resident diagnostics (SPEC error list: range error naming (m,n),
  * fault positions).  first_* are INT64_MAX when nothing was recorded. */
@@ -325,6 +328,29 @@ ne_status ne_abft_check(const ne_config* cfg, ne_cstreams d, const int64_t* e, i
  * NE_EUNRECOVERABLE). */
 ne_status ne_abft_recover(const ne_config* cfg, ne_cstreams d, const int64_t* e, int64_t n_total,
                           int32_t r, int64_t* d_r, ne_stream_t stream);
+
+/* ============================== w = 32 containers (NEXT-3; Table II) === */
+/* The same operations with cfg->w == 32 (e.g. ne_config_for(3, 32) = (l, k) =
+ * (11, 10), dynamic range +-1 046 528): entangled values and results in int32
+ * containers, every op mod 2^32, the 2w-bit temporaries of Eqs. 16-19/21 in
+ * int64 (exact: |t| < 2^63, (M-1) l <= 31).  d_out gets the low 32 bits of the
+ * exact d_hat (reading R17).  Layout, bitmap, diag and errors as the w = 64
+ * calls; NE_ECONFIG unless cfg->w == 32.                                      */
+ne_status ne_entangle_w32(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, ne_streams32 eps,
+                          ne_diag* diag, ne_stream_t stream);
+/* x_m[n] = x_m[n] * (g ? g[n] : s) + sign * addend_m[n] (addend_or_null: a host
+ * pointer to the entangled addend set, or NULL for scale only), in place. */
+ne_status ne_op_scale_add_w32(const ne_config* cfg, ne_streams32 x, int64_t n_total, int32_t s,
+                              const int32_t* g_or_null, const ne_cstreams32* addend_or_null, int32_t sign,
+                              ne_stream_t stream);
+ne_status ne_disentangle_check_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t n_total, int32_t r,
+                                   ne_streams32 d_out, uint32_t* bitmap, ne_diag* diag, ne_stream_t stream);
+ne_status ne_recover_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t n_total, int32_t r,
+                         ne_streams32 d_out, ne_stream_t stream);
+/* as ne_inject_sweep with 32 bits per word: trial t = (s*window + n)*32 + bit;
+ * flagwords / dhat: M*window*32 entries (dhat times M, int32). */
+ne_status ne_inject_sweep_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t window, int32_t r,
+                              uint64_t* flagwords, int32_t* dhat, ne_stream_t stream);
 
 /* ============================================== a7: fault injection (test) === */
 

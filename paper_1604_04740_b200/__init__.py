@@ -35,6 +35,7 @@ EXPORTS = (
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
     "ne_gemm_check_workspace", "ne_op_gemm_limbs_check",
     "ne_conv_geometry", "ne_entangle_limbs_conv", "ne_conv_prep_taps", "ne_op_conv_limbs",
+    "ne_entangle_w32", "ne_op_scale_add_w32", "ne_disentangle_check_w32", "ne_recover_w32", "ne_inject_sweep_w32",
     "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
     "ne_abft_encode", "ne_abft_encode_limbs", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
@@ -87,6 +88,11 @@ _SIGS = {
     "ne_op_gemm": [_PCFG, Streams, _VP, _I64, _I64, _I64, C.c_int, _I32, _I32, Streams, _VP, _SZ, _VP, _VP],
     "ne_gemm_prep_b": [_VP, _I64, _I64, _VP, _VP, _VP],
     "ne_op_gemm_limbs": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _VP],
+    "ne_entangle_w32": [_PCFG, Streams, _I64, Streams, _VP, _VP],
+    "ne_op_scale_add_w32": [_PCFG, Streams, _I64, _I32, _VP, C.POINTER(Streams), _I32, _VP],
+    "ne_disentangle_check_w32": [_PCFG, Streams, _I64, _I32, Streams, _VP, _VP, _VP],
+    "ne_recover_w32": [_PCFG, Streams, _I64, _I32, Streams, _VP],
+    "ne_inject_sweep_w32": [_PCFG, Streams, _I64, _I32, _VP, _VP, _VP],
     "ne_conv_geometry": [_I64, _I32, C.POINTER(_I64), C.POINTER(_I64)],
     "ne_entangle_limbs_conv": [_PCFG, Streams, _I64, _I32, _I32, _I32, _I32, _VP, _VP, _VP],
     "ne_conv_prep_taps": [_VP, _I32, _I32, _VP, _VP, _VP],
@@ -298,6 +304,33 @@ def ne_op_gemm_limbs(cfg: Config, planes: torch.Tensor, L: int, Bt: torch.Tensor
                      out, limb_bits: int = 8) -> None:
     _call("ne_op_gemm_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, limb_bits, _ptr(Bt, torch.int8), rows, cols,
           K, _streams(out, torch.int64), _stream())
+
+
+# ------------------------------------------------------------------ w = 32 containers
+def ne_entangle_w32(cfg: Config, c, eps, diag=None) -> None:
+    _call("ne_entangle_w32", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), _streams(eps, torch.int32),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_op_scale_add_w32(cfg: Config, x, s: int = 1, g: torch.Tensor | None = None, addend=None, sign: int = 1) -> None:
+    a = C.byref(_streams(addend, torch.int32)) if addend is not None else None
+    _call("ne_op_scale_add_w32", C.byref(cfg), _streams(x, torch.int32), x[0].numel(), s, _ptr(g, torch.int32), a,
+          sign, _stream())
+
+
+def ne_disentangle_check_w32(cfg: Config, delta, r: int, d_out, bitmap: torch.Tensor | None = None, diag=None) -> None:
+    _call("ne_disentangle_check_w32", C.byref(cfg), _streams(delta, torch.int32), delta[0].numel(), r,
+          _streams(d_out, torch.int32), _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _stream())
+
+
+def ne_recover_w32(cfg: Config, delta, r: int, d_out) -> None:
+    n = next(t for t in delta if t is not None).numel()
+    _call("ne_recover_w32", C.byref(cfg), _streams(delta, torch.int32), n, r, _streams(d_out, torch.int32), _stream())
+
+
+def ne_inject_sweep_w32(cfg: Config, delta, window: int, r: int, flagwords: torch.Tensor, dhat: torch.Tensor) -> None:
+    _call("ne_inject_sweep_w32", C.byref(cfg), _streams(delta, torch.int32), window, r, _ptr(flagwords, torch.int64),
+          _ptr(dhat, torch.int32), _stream())
 
 
 def ne_conv_geometry(n: int, taps: int) -> tuple[int, int]:

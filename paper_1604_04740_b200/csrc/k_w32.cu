@@ -1,0 +1,371 @@
+// k_w32.cu — the paper's own w = 32 instantiation (NEXT-3 of SURVEY §8(f);
+// P:528-530 "32-bit integers ... l = 11, k = 10" for M = 3, Table II for the
+// rest): entangled streams held in 32-bit containers, which halves the HBM
+// bytes of every bandwidth-bound stage relative to w = 64 wherever the
+// dynamic range allows (Eq. 11/13: +-1 046 528 for M = 3).
+//
+// The 2w-bit temporaries of the disentanglement are
+// native int64 here: with (M-1) l + k = 32,
+//   |t| <= 2^31 sum_j 2^{(M-2-j) l} < 2^63,  b = (M-1) l <= 31,
+// so t, d_p = sext_b(t), d_r = (-1)^M (t - d_p) >> b and the check
+// e_r == d_r + 2^l d_p are exact in int64; the cascade of Eq. 19 is taken mod
+// 2^64 and its low 32 bits stored (the "low w bits" convention, reading R17).
+// Layout and vector widths as the w = 64 kernels: 4 positions per thread, one
+// 128-bit load/store per stream; a warp covers 128 positions = 4 bitmap words.
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "ne_internal.cuh"
+
+namespace ne {
+
+// Eqs. 16-19 + 21 in the rotated frame (excluded stream = e[0]), int64 temporaries.
+template <int MT>
+__device__ __forceinline__ bool disentangle_rot32(const int64_t* e, int M_rt, int l, int32_t* d, bool check) {
+  const int M = MT > 0 ? MT : M_rt;
+  int64_t t = 0;
+#pragma unroll
+  for (int j = 0; j < (MT > 0 ? MT - 1 : NE_MAX_M - 1); ++j) {
+    if (MT == 0 && j > M - 2) break;
+    const int64_t term = (int64_t)((uint64_t)e[1 + j] << ((M - 2 - j) * l));
+    t = (j & 1) ? t - term : t + term;
+  }
+  if (M & 1) t = -t;
+  const int b = (M - 1) * l;  // <= 31
+  const int64_t dp = (int64_t)((uint64_t)t << (64 - b)) >> (64 - b);
+  int64_t num = t - dp;
+  if (M & 1) num = -num;
+  const int64_t dr = num >> b;
+  d[0] = (int32_t)dr;
+  d[M - 1] = (int32_t)dp;
+  uint64_t prev = (uint64_t)dr;
+#pragma unroll
+  for (int j = 1; j < (MT > 0 ? MT - 1 : NE_MAX_M - 1); ++j) {
+    if (MT == 0 && j > M - 2) break;
+    const uint64_t cur = (uint64_t)e[j] - (prev << l);
+    d[j] = (int32_t)(uint32_t)cur;
+    prev = cur;
+  }
+  if (!check) return false;
+  return e[0] != dr + (int64_t)((uint64_t)dp << l);
+}
+
+// bit (4*lane + u) of the warp's 128-position run, from 4 ballots, as word j
+__device__ __forceinline__ uint32_t word_of4(const uint32_t (&bal)[4], int j) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t byte = (bal[u] >> (8 * j)) & 0xffu;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w |= ((byte >> k) & 1u) << (4 * k + u);
+  }
+  return w;
+}
+
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_entangle_w32(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n,
+               const __grid_constant__ ne_streams32 eps, ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  int bad = 0;
+  long long first = LLONG_MAX;
+  const int64_t nv = (n + 3) / 4;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 4 * v;
+    const bool full = n0 + 3 < n;
+    int32_t q[MA][4];
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      if (full) {
+        const int4 a = __ldcs(reinterpret_cast<const int4*>(c.s[m] + n0));
+        q[m][0] = a.x; q[m][1] = a.y; q[m][2] = a.z; q[m][3] = a.w;
+      } else {
+        for (int u = 0; u < 4; ++u) q[m][u] = n0 + u < n ? c.s[m][n0 + u] : 0;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      const int mp = m == 0 ? M - 1 : m - 1;
+      int32_t o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        o[u] = (int32_t)((uint32_t)q[m][u] + ((uint32_t)q[mp][u] << l));  // Eq. 15 mod 2^32
+        if (n0 + u < n && (q[m][u] > hi || q[m][u] < -hi)) {
+          ++bad;
+          const long long idx = (long long)m * n + n0 + u;
+          first = idx < first ? idx : first;
+        }
+      }
+      if (full)
+        __stcs(reinterpret_cast<int4*>(eps.s[m] + n0), make_int4(o[0], o[1], o[2], o[3]));
+      else
+        for (int u = 0; u < 4; ++u)
+          if (n0 + u < n) eps.s[m][n0 + u] = o[u];
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// x_m[n] = x_m[n] * (g ? g[n] : s) + sign * a_m[n] (a nullable), mod 2^32:
+// the C1 chain's scale and add in one pass (either alone when s = 1 / a = NULL)
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_scale_add_w32(const __grid_constant__ ne_streams32 x, int M_rt, int64_t n, int32_t s, const int32_t* __restrict__ g,
+                const __grid_constant__ ne_cstreams32 a, int has_a, int32_t sign) {
+  const int M = MT > 0 ? MT : M_rt;
+  const int64_t nv = (n + 3) / 4;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 4 * v;
+    const bool full = n0 + 3 < n;
+    uint32_t gs[4] = {(uint32_t)s, (uint32_t)s, (uint32_t)s, (uint32_t)s};
+    if (g)
+      for (int u = 0; u < 4; ++u) gs[u] = n0 + u < n ? (uint32_t)g[n0 + u] : 0u;
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      uint32_t xv[4], av[4] = {0, 0, 0, 0};
+      if (full) {
+        const int4 q = *reinterpret_cast<const int4*>(x.s[m] + n0);
+        xv[0] = q.x; xv[1] = q.y; xv[2] = q.z; xv[3] = q.w;
+        if (has_a) {
+          const int4 p = __ldcs(reinterpret_cast<const int4*>(a.s[m] + n0));
+          av[0] = p.x; av[1] = p.y; av[2] = p.z; av[3] = p.w;
+        }
+      } else {
+        for (int u = 0; u < 4; ++u) {
+          xv[u] = n0 + u < n ? (uint32_t)x.s[m][n0 + u] : 0u;
+          if (has_a) av[u] = n0 + u < n ? (uint32_t)a.s[m][n0 + u] : 0u;
+        }
+      }
+      int32_t o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = (int32_t)(xv[u] * gs[u] + (uint32_t)sign * av[u]);
+      if (full)
+        *reinterpret_cast<int4*>(x.s[m] + n0) = make_int4(o[0], o[1], o[2], o[3]);
+      else
+        for (int u = 0; u < 4; ++u)
+          if (n0 + u < n) x.s[m][n0 + u] = o[u];
+    }
+  }
+}
+
+template <int MT, bool CHECK>
+__global__ void __launch_bounds__(kThreads)
+k_disentangle_w32(const __grid_constant__ ne_cstreams32 e, int M_rt, int l, int64_t n,
+                  const __grid_constant__ ne_streams32 d_out, uint32_t* __restrict__ bitmap,
+                  ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  const int64_t nv = (n + 3) / 4;
+  const int64_t nwords = (n + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nv_w = (nv + 31) & ~(int64_t)31;  // whole warps join the ballots
+  int nflag = 0;
+  long long first = LLONG_MAX;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv_w; v += stride) {
+    const int64_t n0 = 4 * v;
+    bool f[4] = {false, false, false, false};
+    if (n0 < n) {
+      const bool full = n0 + 3 < n;
+      int64_t q[4][MA];
+#pragma unroll
+      for (int j = 0; j < MA; ++j) {
+        if (MT == 0 && j >= M) break;
+        if (j == 0 && !CHECK) {
+          q[0][0] = q[1][0] = q[2][0] = q[3][0] = 0;
+          continue;
+        }
+        if (full) {
+          const int4 a = __ldcs(reinterpret_cast<const int4*>(e.s[j] + n0));
+          q[0][j] = a.x; q[1][j] = a.y; q[2][j] = a.z; q[3][j] = a.w;
+        } else {
+          for (int u = 0; u < 4; ++u) q[u][j] = n0 + u < n ? e.s[j][n0 + u] : 0;
+        }
+      }
+      int32_t d[4][MA];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) f[u] = disentangle_rot32<MT>(q[u], M, l, d[u], CHECK) && (n0 + u < n);
+#pragma unroll
+      for (int j = 0; j < MA; ++j) {
+        if (MT == 0 && j >= M) break;
+        if (full)
+          __stcs(reinterpret_cast<int4*>(d_out.s[j] + n0), make_int4(d[0][j], d[1][j], d[2][j], d[3][j]));
+        else
+          for (int u = 0; u < 4; ++u)
+            if (n0 + u < n) d_out.s[j][n0 + u] = d[u][j];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (f[u]) {
+          ++nflag;
+          first = (n0 + u) < first ? (n0 + u) : first;
+        }
+    }
+    if (CHECK && bitmap) {
+      uint32_t bal[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bal[u] = __ballot_sync(0xffffffffu, f[u]);
+      const int64_t w0 = (v - lane) / 8;  // 128 positions per warp -> 4 words
+      if (lane < 4 && w0 + lane < nwords) bitmap[w0 + lane] = word_of4(bal, lane);
+    }
+  }
+  if (CHECK && diag) diag_add(&diag->fault_positions, &diag->first_fault, nflag, first);
+}
+
+// a7 at w = 32: trial t = (s*window + pos)*32 + bit flips bit `bit` of
+// delta_s[pos] and re-runs disentangle + check on positions 0..window-1.
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_inject_sweep_w32(const __grid_constant__ ne_cstreams32 e, int M_rt, int l, int r, int64_t window,
+                   uint64_t* __restrict__ flagwords, int32_t* __restrict__ dhat) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  const int64_t trials = (int64_t)M * window * 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < trials; t += nwarps) {
+    const int bit = (int)(t & 31);
+    const int64_t pos = (t >> 5) % window;
+    const int s = (int)((t >> 5) / window);
+    const int js = (s - r + M) % M;
+    bool fl[2] = {false, false};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t p = 2 * lane + h;
+      if (p < window) {
+        int64_t a[MA];
+        int32_t d[MA];
+#pragma unroll
+        for (int j = 0; j < MA; ++j) {
+          if (MT == 0 && j >= M) break;
+          int32_t v = e.s[j][p];
+          if (p == pos && j == js) v ^= (int32_t)(1u << bit);
+          a[j] = v;
+        }
+        fl[h] = disentangle_rot32<MT>(a, M, l, d, true);
+        if (p == pos) {
+#pragma unroll
+          for (int j = 0; j < MA; ++j) {
+            if (MT == 0 && j >= M) break;
+            dhat[t * M + (r + j) % M] = d[j];
+          }
+        }
+      }
+    }
+    const uint32_t b0 = __ballot_sync(0xffffffffu, fl[0]);
+    const uint32_t b1 = __ballot_sync(0xffffffffu, fl[1]);
+    if (lane == 0) {
+      uint64_t w = 0;
+      for (int k = 0; k < 32; ++k) w |= ((uint64_t)((b0 >> k) & 1u) << (2 * k)) | ((uint64_t)((b1 >> k) & 1u) << (2 * k + 1));
+      flagwords[t] = w;
+    }
+  }
+}
+
+}  // namespace ne
+
+using namespace ne;
+
+static ne_status validate_cfg32(const ne_config* cfg) {
+  if (!cfg) return NE_EINVAL;
+  if (cfg->M < 3 || cfg->M > NE_MAX_M || cfg->w != 32) return NE_ECONFIG;
+  if (cfg->l < 1 || cfg->k < 1 || cfg->k > cfg->l || (cfg->M - 1) * cfg->l + cfg->k > 32) return NE_ECONFIG;
+  return NE_OK;
+}
+
+template <typename S>
+static bool ok32(const S& c, int M, int skip = -1) {
+  for (int m = 0; m < M; ++m) {
+    if (m == skip) continue;
+    if (!c.s[m] || !aligned16(c.s[m])) return false;
+  }
+  return true;
+}
+
+#define NE_W32_M(M, KERNEL, GRID, STREAM, ...)                             \
+  switch (M) {                                                           \
+    case 3: KERNEL<3><<<GRID, kThreads, 0, STREAM>>>(__VA_ARGS__); break; \
+    case 4: KERNEL<4><<<GRID, kThreads, 0, STREAM>>>(__VA_ARGS__); break; \
+    case 8: KERNEL<8><<<GRID, kThreads, 0, STREAM>>>(__VA_ARGS__); break; \
+    default: KERNEL<0><<<GRID, kThreads, 0, STREAM>>>(__VA_ARGS__); break; \
+  }
+
+extern "C" ne_status ne_entangle_w32(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, ne_streams32 eps,
+                                     ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg32(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !ok32(c, cfg->M) || !ok32(eps, cfg->M)) return NE_EINVAL;
+  NE_W32_M(cfg->M, k_entangle_w32, grid_for((n_total + 3) / 4, kThreads), cs(stream), c, cfg->M, cfg->l,
+           range_hi(cfg), n_total, eps, diag);
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_scale_add_w32(const ne_config* cfg, ne_streams32 x, int64_t n_total, int32_t s,
+                                         const int32_t* g_or_null, const ne_cstreams32* addend_or_null, int32_t sign,
+                                         ne_stream_t stream) {
+  ne_status st = validate_cfg32(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || (sign != 1 && sign != -1) || !ok32(x, cfg->M)) return NE_EINVAL;
+  ne_cstreams32 a{};
+  if (addend_or_null) {
+    if (!ok32(*addend_or_null, cfg->M)) return NE_EINVAL;
+    a = *addend_or_null;
+  }
+  NE_W32_M(cfg->M, k_scale_add_w32, grid_for((n_total + 3) / 4, kThreads), cs(stream), x, cfg->M, n_total, s,
+           g_or_null, a, addend_or_null ? 1 : 0, sign);
+  return launch_status();
+}
+
+template <bool CHECK>
+static void launch_dis32(const ne_config* cfg, const ne_cstreams32& er, int64_t n, const ne_streams32& dr,
+                         uint32_t* bitmap, ne_diag* diag, cudaStream_t s) {
+  const int grid = grid_for((n + 3) / 4, kThreads);
+  switch (cfg->M) {
+    case 3: k_disentangle_w32<3, CHECK><<<grid, kThreads, 0, s>>>(er, 3, cfg->l, n, dr, bitmap, diag); break;
+    case 4: k_disentangle_w32<4, CHECK><<<grid, kThreads, 0, s>>>(er, 4, cfg->l, n, dr, bitmap, diag); break;
+    case 8: k_disentangle_w32<8, CHECK><<<grid, kThreads, 0, s>>>(er, 8, cfg->l, n, dr, bitmap, diag); break;
+    default: k_disentangle_w32<0, CHECK><<<grid, kThreads, 0, s>>>(er, cfg->M, cfg->l, n, dr, bitmap, diag); break;
+  }
+}
+
+extern "C" ne_status ne_disentangle_check_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t n_total, int32_t r,
+                                              ne_streams32 d_out, uint32_t* bitmap, ne_diag* diag,
+                                              ne_stream_t stream) {
+  ne_status st = validate_cfg32(cfg);
+  if (st != NE_OK) return st;
+  if (r < 0 || r >= cfg->M) return NE_EINDEX;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !ok32(delta, cfg->M) || !ok32(d_out, cfg->M)) return NE_EINVAL;
+  launch_dis32<true>(cfg, rotate(delta, cfg->M, r), n_total, rotate(d_out, cfg->M, r), bitmap, diag, cs(stream));
+  return launch_status();
+}
+
+extern "C" ne_status ne_recover_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t n_total, int32_t r,
+                                    ne_streams32 d_out, ne_stream_t stream) {
+  ne_status st = validate_cfg32(cfg);
+  if (st != NE_OK) return st;
+  if (r < 0 || r >= cfg->M) return NE_EINDEX;
+  for (int m = 0; m < cfg->M; ++m)
+    if (m != r && !delta.s[m]) return NE_EUNRECOVERABLE;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !ok32(delta, cfg->M, r) || !ok32(d_out, cfg->M)) return NE_EINVAL;
+  launch_dis32<false>(cfg, rotate(delta, cfg->M, r), n_total, rotate(d_out, cfg->M, r), nullptr, nullptr, cs(stream));
+  return launch_status();
+}
+
+extern "C" ne_status ne_inject_sweep_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t window, int32_t r,
+                                         uint64_t* flagwords, int32_t* dhat, ne_stream_t stream) {
+  ne_status st = validate_cfg32(cfg);
+  if (st != NE_OK) return st;
+  if (r < 0 || r >= cfg->M) return NE_EINDEX;
+  if (window < 1 || window > 64 || !flagwords || !dhat || !ok32(delta, cfg->M)) return NE_EINVAL;
+  const int64_t trials = (int64_t)cfg->M * window * 32;
+  NE_W32_M(cfg->M, k_inject_sweep_w32, grid_for(trials * 32, kThreads), cs(stream), rotate(delta, cfg->M, r), cfg->M,
+           cfg->l, r, window, flagwords, dhat);
+  return launch_status();
+}

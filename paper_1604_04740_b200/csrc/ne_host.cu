@@ -91,8 +91,20 @@ extern "C" ne_status ne_config_for(int32_t M, int32_t w, ne_config* out) {
   return NE_OK;
 }
 
+// a0 host calls accept both container widths (w = 32: the ne_*_w32 path)
+static ne_status validate_cfg_host(const ne_config* cfg) {
+  if (!cfg) return NE_EINVAL;
+  if (cfg->w == 32) {
+    if (cfg->M < 3 || cfg->M > NE_MAX_M || cfg->l < 1 || cfg->k < 1 || cfg->k > cfg->l ||
+        (cfg->M - 1) * cfg->l + cfg->k > 32)
+      return NE_ECONFIG;
+    return NE_OK;
+  }
+  return validate_cfg(cfg);
+}
+
 extern "C" ne_status ne_dynamic_range(const ne_config* cfg, int64_t* hi) {
-  ne_status st = validate_cfg(cfg);
+  ne_status st = validate_cfg_host(cfg);
   if (st != NE_OK) return st;
   if (!hi) return NE_EINVAL;
   *hi = range_hi(cfg);
@@ -101,7 +113,7 @@ extern "C" ne_status ne_dynamic_range(const ne_config* cfg, int64_t* hi) {
 
 extern "C" ne_status ne_certify(const ne_config* cfg, ne_op_kind op, int64_t in_bound,
                                 int64_t operand, int64_t* out_bound) {
-  ne_status st = validate_cfg(cfg);
+  ne_status st = validate_cfg_host(cfg);
   if (st != NE_OK) return st;
   if (!out_bound || in_bound < 0 || operand < 0) return NE_EINVAL;
   __int128 b;

@@ -59,12 +59,21 @@ def test_config_errors():
 @pytest.mark.parametrize("M", [3, 4, 5, 8, 11, 16, 32])
 def test_dynamic_range_matches_oracle(O, M):
     assert ne.ne_dynamic_range(ne.ne_config_for(M, 64)) == O.dynamic_range(O.config_for(M, 64))
+    assert ne.ne_dynamic_range(ne.ne_config_for(M, 32)) == O.dynamic_range(O.config_for(M, 32))
 
 
-def test_w32_rejected_by_gpu_path():
-    """The GPU path implements w = 64 containers only."""
-    with pytest.raises(ne.NeError):
-        ne.ne_dynamic_range(ne.ne_config_for(3, 32))
+def test_w32_configs_rejected_by_w64_calls_and_vice_versa():
+    """w = 32 containers only through the ne_*_w32 calls, w = 64 only through
+    the others (argument validation happens before any device work)."""
+    c32, c64 = ne.ne_config_for(3, 32), ne.ne_config_for(3, 64)
+    assert (c32.l, c32.k) == (11, 10)  # P:528-530
+    L = ne.lib()
+    st = ne.Streams()
+    assert L.ne_entangle(ctypes.byref(c32), st, 0, st, None, None) == 2          # NE_ECONFIG
+    assert L.ne_disentangle_check(ctypes.byref(c32), st, 0, 0, st, None, None, None) == 2
+    assert L.ne_entangle_w32(ctypes.byref(c64), st, 0, st, None, None) == 2
+    assert L.ne_recover_w32(ctypes.byref(c64), st, 0, 0, st, None) == 2
+    assert L.ne_disentangle_check_w32(ctypes.byref(c32), st, 0, 3, st, None, None, None) == 4  # NE_EINDEX
 
 
 def test_certify_baseline_configs():

@@ -1,0 +1,160 @@
+"""GPU parity of the w = 32 container path (the paper's own instantiation,
+P:528-530: M = 3, l = 11, k = 10; Table II for other M) against the CPU
+oracle, whose arithmetic is generic in w (values reduced mod 2^w).  All
+integer: bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import paper_1604_04740_b200 as ne
+from _gpu import bitmap_to_flags, to_np, to_streams
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    ne.build()
+    ne.lib()
+    assert torch.cuda.is_available()
+
+
+def gen(O, seed, tag, M, N, lo, hi):
+    return np.stack([O.gen_uniform(seed, tag, m, lo, hi, N) for m in range(M)])
+
+
+def empty32(M, N):
+    return [torch.empty(N, dtype=torch.int32, device="cuda") for _ in range(M)]
+
+
+@pytest.mark.parametrize("N", [4096, 4099, 1, 130])
+def test_w32_c1_chain(O, N):
+    """C1 at w = 32: eps = E c, alpha = E a, delta = 37 eps + alpha (one fused
+    pass), disentangle + check for every excluded r, recovery of every r; the
+    disentangled result equals 37 c + a (Props 1/3)."""
+    M = 3
+    cfg, ocfg = ne.ne_config_for(M, 32), O.config_for(M, 32)
+    assert (cfg.l, cfg.k) == (11, 10)
+    c = gen(O, 0, 1, M, N, -2 ** 10, 2 ** 10)
+    a = gen(O, 0, 2, M, N, -2 ** 10, 2 ** 10)
+    diag = ne.diag_new()
+    eps, alpha = empty32(M, N), empty32(M, N)
+    ne.ne_entangle_w32(cfg, to_streams(c), eps, diag)
+    ne.ne_entangle_w32(cfg, to_streams(a), alpha, diag)
+    E, A = O.entangle(ocfg, c), O.entangle(ocfg, a)
+    assert (to_np(eps) == E).all() and (to_np(alpha) == A).all()
+    ne.ne_op_scale_add_w32(cfg, eps, 37, None, alpha, 1)
+    D = O.op_add(ocfg, O.op_scale(ocfg, E, 37), A, 1)
+    assert (to_np(eps) == D).all()
+    plain = 37 * c + a
+    for r in range(M):
+        d_out = empty32(M, N)
+        bm = torch.full(((N + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        ne.ne_disentangle_check_w32(cfg, eps, r, d_out, bm, diag)
+        ref, flags, nf = O.disentangle_check(ocfg, D, r)
+        assert (to_np(d_out) == ref).all() and (ref == plain).all()
+        assert (bitmap_to_flags(bm, N) == flags).all() and nf == 0
+        rec = empty32(M, N)
+        ne.ne_recover_w32(cfg, [None if m == r else eps[m] for m in range(M)], r, rec)
+        assert (to_np(rec) == plain).all()
+    d = ne.diag_read(diag)
+    assert d["range_violations"] == 0 and d["fault_positions"] == 0
+
+
+@pytest.mark.parametrize("M", [4, 5, 8, 11, 16, 32])
+def test_w32_every_M(O, M):
+    """Table II configurations: entangle, scale by g[n], add, check and recover
+    agree with the oracle at the edges of the dynamic range."""
+    cfg, ocfg = ne.ne_config_for(M, 32), O.config_for(M, 32)
+    hi = ne.ne_dynamic_range(cfg)
+    assert hi == O.dynamic_range(ocfg)
+    N = 1000 + M
+    c = gen(O, 5, 1, M, N, -hi, hi + 1)
+    c[:, 0], c[:, 1] = hi, -hi
+    eps = empty32(M, N)
+    ne.ne_entangle_w32(cfg, to_streams(c), eps)
+    E = O.entangle(ocfg, c)
+    assert (to_np(eps) == E).all()
+    g = np.ones(N, dtype=np.int64)
+    g[::3] = -1
+    ne.ne_op_scale_add_w32(cfg, eps, 1, torch.from_numpy(g.astype(np.int32)).cuda())
+    D = O.op_scale(ocfg, E, 1, g)
+    assert (to_np(eps) == D).all()
+    r = M // 2
+    d_out = empty32(M, N)
+    diag = ne.diag_new()
+    ne.ne_disentangle_check_w32(cfg, eps, r, d_out, None, diag)
+    ref, _, nf = O.disentangle_check(ocfg, D, r)
+    assert (to_np(d_out) == ref).all() and (ref == c * g).all()
+    assert ne.diag_read(diag)["fault_positions"] == nf == 0
+    rec = empty32(M, N)
+    ne.ne_recover_w32(cfg, [None if m == 1 else eps[m] for m in range(M)], 1, rec)
+    assert (to_np(rec) == c * g).all()
+
+
+@pytest.mark.parametrize("M", [3, 4, 8])
+def test_w32_random_faults(O, M):
+    """Random-mask corruptions of random words of single streams: flags, d_hat
+    (low 32 bits of the exact values) and the bitmap equal the oracle's, and
+    every corrupted position is flagged (M l >= w: Props 2/4)."""
+    cfg, ocfg = ne.ne_config_for(M, 32), O.config_for(M, 32)
+    hi = ne.ne_dynamic_range(cfg)
+    N = 4096 + 7
+    c = gen(O, 7, 1, M, N, -hi, hi + 1)
+    D = O.entangle(ocfg, c)
+    rng = np.random.default_rng(M)
+    pos = rng.choice(N, size=300, replace=False)
+    D_f = D.copy()
+    for p in pos:
+        s = rng.integers(M)
+        mask = int(rng.integers(1, 2 ** 32))
+        D_f[s, p] = O.wrap(ocfg, int(D_f[s, p]) ^ mask)
+    d_out = empty32(M, N)
+    bm = torch.empty((N + 31) // 32, dtype=torch.int32, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_disentangle_check_w32(cfg, to_streams(D_f), 0, d_out, bm, diag)
+    ref, flags, nf = O.disentangle_check(ocfg, D_f, 0)
+    assert (to_np(d_out) == ref).all()
+    assert (bitmap_to_flags(bm, N) == flags).all()
+    d = ne.diag_read(diag)
+    assert d["fault_positions"] == nf and nf == len(pos)
+    assert d["first_fault"] == int(pos.min())
+
+
+def test_w32_exhaustive_single_bit_injection(O):
+    """All 3 x 64 x 32 single-bit flips of the C1 (w = 32) outputs in the first
+    64 positions: exactly the injected position is flagged, and d_hat at it
+    equals the oracle's for the same corrupted word."""
+    M, N, W = 3, 4096, 64
+    cfg, ocfg = ne.ne_config_for(M, 32), O.config_for(M, 32)
+    c = gen(O, 0, 1, M, N, -2 ** 10, 2 ** 10)
+    a = gen(O, 0, 2, M, N, -2 ** 10, 2 ** 10)
+    D = O.op_add(ocfg, O.op_scale(ocfg, O.entangle(ocfg, c), 37), O.entangle(ocfg, a), 1)
+    for r in (0, 2):
+        T = M * W * 32
+        fw = torch.empty(T, dtype=torch.int64, device="cuda")
+        dh = torch.empty(T * M, dtype=torch.int32, device="cuda")
+        ne.ne_inject_sweep_w32(cfg, to_streams(D[:, :W]), W, r, fw, dh)
+        fw = fw.cpu().numpy().astype(np.uint64)
+        dh = dh.cpu().numpy().reshape(T, M)
+        for t in range(T):
+            bit, p, s = t & 31, (t >> 5) % W, (t >> 5) // W
+            assert fw[t] == np.uint64(1) << np.uint64(p), (r, s, p, bit)
+            col = D[:, p].copy()
+            col[s] = O.wrap(ocfg, int(col[s]) ^ (1 << bit))
+            out, f = O.disentangle_one(ocfg, col, r)
+            assert f == 1 and (dh[t] == out).all()
+
+
+def test_w32_range_violation_names_first(O):
+    M, N = 3, 5000
+    cfg = ne.ne_config_for(M, 32)
+    hi = ne.ne_dynamic_range(cfg)
+    c = gen(O, 1, 1, M, N, -100, 100)
+    c[2, 4000] = hi + 1
+    c[1, 4001] = -hi - 1
+    c[0, 17] = hi  # at the limit: admissible
+    diag = ne.diag_new()
+    ne.ne_entangle_w32(cfg, to_streams(c), empty32(M, N), diag)
+    d = ne.diag_read(diag)
+    assert d["range_violations"] == 2 and d["first_bad"] == 1 * N + 4001
