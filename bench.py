@@ -534,21 +534,25 @@ class C2Conv(Workload):
 
 class C1Chain(Workload):
     """configs[0]: M=3 streams of 4096 int32 U[-2^10,2^10), seed 0; scale by 37
-    then add a second seeded 3-stream set; disentangle + check."""
+    then add a second seeded 3-stream set; disentangle + check.  w = 64
+    containers (default) or the paper's w = 32 instantiation (l = 11, k = 10,
+    P:528-530; range +-1 046 528 admits C1's bound 38 912).  --n sweeps the
+    stream length (HBM-bound from ~2^20 on)."""
 
     name = "C1"
     metric_unit = "Gpositions/s"
 
-    def __init__(self, rank, n=4096, seed=0):
+    def __init__(self, rank, n=4096, seed=0, w=64):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
-        self.M, self.n = 3, n
+        self.M, self.n, self.w = 3, n, w
         self.seed = seed + 1000 * rank
-        self.cfg = ne.ne_config_for(3)
+        self.cfg = ne.ne_config_for(3, w)
+        dt = torch.int64 if w == 64 else torch.int32
         mk32 = lambda: [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3)]  # noqa: E731
-        mk = lambda: [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(3)]  # noqa: E731
+        mk = lambda: [torch.empty(n, dtype=dt, device="cuda") for _ in range(3)]  # noqa: E731
         self.c, self.a = mk32(), mk32()
         for m in range(3):
             ne.ne_gen_uniform_i32(self.seed, 1, m, -1024, 1024, self.c[m])
@@ -556,15 +560,22 @@ class C1Chain(Workload):
         self.eps, self.alpha, self.dout, self.drec = mk(), mk(), mk(), mk()
         self.bitmap = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
         self.diag = ne.diag_new()
-        self.launches_per_step = 6
+        self.launches_per_step = 5
 
     def stages(self, i):
         ne, cfg = self.ne, self.cfg
         r = i % 3
         part = [None if m == r else self.eps[m] for m in range(3)]
+        if self.w == 32:
+            return [("entangle", lambda: (ne.ne_entangle_w32(cfg, self.c, self.eps, self.diag),
+                                          ne.ne_entangle_w32(cfg, self.a, self.alpha, self.diag))),
+                    ("scale_add", lambda: ne.ne_op_scale_add_w32(cfg, self.eps, 37, None, self.alpha, 1)),
+                    ("check", lambda: ne.ne_disentangle_check_w32(cfg, self.eps, 0, self.dout, self.bitmap,
+                                                                  self.diag)),
+                    ("recover", lambda: ne.ne_recover_w32(cfg, part, r, self.drec))]
         return [("entangle", lambda: (ne.ne_entangle(cfg, self.c, self.eps, self.diag),
                                       ne.ne_entangle(cfg, self.a, self.alpha, self.diag))),
-                ("scale_add", lambda: (ne.ne_op_scale(cfg, self.eps, 37), ne.ne_op_add(cfg, self.eps, self.alpha))),
+                ("scale_add", lambda: ne.ne_op_scale_add(cfg, self.eps, 37, self.alpha)),
                 ("check", lambda: ne.ne_disentangle_check(cfg, self.eps, 0, self.dout, self.bitmap, self.diag)),
                 ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec))]
 
@@ -572,19 +583,24 @@ class C1Chain(Workload):
         return self.n / 1e9
 
     def stage_info(self):
-        n = self.n
-        return {"entangle": ("hbm", 2 * 3 * n * 12 / 1e9, "GB"), "scale_add": ("hbm", 3 * n * 40 / 1e9, "GB"),
-                "check": ("hbm", 3 * n * 16 / 1e9, "GB"), "recover": ("hbm", 5 * n * 8 / 1e9, "GB")}
+        n, B = self.n, self.w // 8
+        sa = 3 * n * 3 * B  # fused scale + add: read eps, alpha, write eps
+        return {"entangle": ("hbm", 2 * 3 * n * (4 + B) / 1e9, "GB"), "scale_add": ("hbm", sa / 1e9, "GB"),
+                "check": ("hbm", 3 * n * 2 * B / 1e9, "GB"), "recover": ("hbm", 5 * n * B / 1e9, "GB")}
 
     def config(self):
-        return {"workload": "C1 (BASELINE configs[0]): M=3 streams of 4096 int32 U[-2^10,2^10), seed 0; "
-                            "scale by 37, add a second seeded 3-stream set; disentangle+check",
-                "M": 3, "n": self.n, "l2": "196 KB working set (launch-latency bound)"}
+        small = self.n * 3 * 4 * 2 < 100e6
+        return {"workload": "C1 (BASELINE configs[0]): M=3 streams of %d int32 U[-2^10,2^10), seed 0; "
+                            "scale by 37, add a second seeded 3-stream set; disentangle+check" % self.n,
+                "M": 3, "n": self.n, "w": self.w, "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": self.w},
+                "l2": ("%.1f MB working set (launch-latency bound)" % (self.n * 3 * (8 + 4 * self.w // 8) / 1e6))
+                if small else "working set >> 126 MB L2 (no flush needed)"}
 
     def e2e_setup(self):
         self.hc = [x.cpu().pin_memory() for x in self.c + self.a]
-        self.hout = [self.torch.empty(self.n, dtype=self.torch.int64).pin_memory() for _ in range(3)]
-        return self.n * 24, self.n * 24
+        dt = self.torch.int64 if self.w == 64 else self.torch.int32
+        self.hout = [self.torch.empty(self.n, dtype=dt).pin_memory() for _ in range(3)]
+        return self.n * 24, self.n * 3 * self.w // 8
 
     def e2e_step(self, i):
         for d, h in zip(self.c + self.a, self.hc):
@@ -600,19 +616,21 @@ class C1Chain(Workload):
     def oracle_sample(self, reps):
         import oracle as O
 
-        ocfg = O.config_for(3, 64)
-        c = np.stack([O.gen_uniform(self.seed, 1, m, -1024, 1024, self.n) for m in range(3)])
-        a = np.stack([O.gen_uniform(self.seed, 2, m, -1024, 1024, self.n) for m in range(3)])
+        ocfg = O.config_for(3, self.w)
+        ns = min(self.n, 1 << 16)
+        c = np.stack([O.gen_uniform(self.seed, 1, m, -1024, 1024, ns) for m in range(3)])
+        a = np.stack([O.gen_uniform(self.seed, 2, m, -1024, 1024, ns) for m in range(3)])
         t0 = time.perf_counter()
         for _ in range(reps):
             d = O.op_add(ocfg, O.op_scale(ocfg, O.entangle(ocfg, c), 37), O.entangle(ocfg, a))
             O.disentangle_check(ocfg, d, 0)
         dt = time.perf_counter() - t0
-        return dt, reps * self.n / 1e9, f"{reps} full C1 passes"
+        return dt, reps * ns / 1e9, f"{reps} full C1 passes (w={self.w})" + ("" if ns == self.n else f" at N'={ns}")
 
 
 WORKLOADS = {"c1": C1Chain, "c2": C2Conv, "c2p": C2Conv, "c3": C3Gemm, "c4": C4PermInner, "c5": None}
-ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c2p": (1, 1), "c3": (16, 2), "c4": (64, 8), "c5": (4096, 512)}
+ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c2p": (1, 1), "c3": (16, 2), "c4": (64, 8),
+                 "c5": (4096, 512)}  # (cpu_baseline, per reference-arm step)
 
 
 def make_workload(args, rank):
@@ -622,7 +640,11 @@ def make_workload(args, rank):
         return C2Conv(rank, algo=args.conv or "direct")
     if args.workload == "c2p":
         return C2Conv(rank, n=10 ** 6, taps=args.taps, M=args.streams, algo=args.conv or "tc", paper=True)
-    return WORKLOADS[args.workload](rank)  # (cpu_baseline, per ref step)
+    if args.workload == "c1":
+        return C1Chain(rank, n=args.n or 4096, w=args.w)
+    return WORKLOADS[args.workload](rank)
+
+
 METRIC = "entangled LSB Gop/s (or GB/s) at 1/2/4/8 B200, % roofline, % overhead vs plain"
 
 
@@ -1010,7 +1032,11 @@ def run_reference(args):
             l, k = {3: (22, 20), 4: (16, 16), 8: (8, 8)}.get(W.M, (8, 8))
         W.cfg = _Cfg
     else:
-        W.M, W.n, W.seed = 3, 4096, 0
+        W.M, W.n, W.seed, W.w = 3, args.n or 4096, 0, args.w
+
+        class _Cfg:
+            l, k = (22, 20) if args.w == 64 else (11, 10)
+        W.cfg = _Cfg
     per_step = ORACLE_SAMPLE[args.workload][1]
     for _ in range(args.warmup):
         W.oracle_sample(per_step)
@@ -1050,6 +1076,8 @@ def main():
                          "measured: direct for c2's 64 taps, tc for c2p)")
     ap.add_argument("--taps", type=int, default=4500, help="c2p: kernel taps (paper: 100-4500)")
     ap.add_argument("--streams", type=int, default=8, help="c2p: M (paper: 3 or 8)")
+    ap.add_argument("--w", type=int, default=64, choices=[64, 32], help="c1: container width (P:528-530)")
+    ap.add_argument("--n", type=int, default=None, help="c1: stream length (default 4096 = configs[0])")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
     args = ap.parse_args()

@@ -173,6 +173,11 @@ ne_status ne_op_scale(const ne_config* cfg, ne_streams x, int64_t n_total, int64
 ne_status ne_op_add(const ne_config* cfg, ne_streams x, ne_cstreams addend, int64_t n_total,
                     int32_t sign, ne_stream_t stream);
 
+/* ne_op_scale then ne_op_add in one pass: x_m[n] = x_m[n] * (g ? g[n] : s)
+ * + sign * addend_m[n] (the C1 chain's two ops; mod 2^64, in place). */
+ne_status ne_op_scale_add(const ne_config* cfg, ne_streams x, int64_t n_total, int64_t s,
+                          const int32_t* g_or_null, ne_cstreams addend, int32_t sign, ne_stream_t stream);
+
 /* Blocked inner product <.,.> (Eq. 2): out_m[b] = sum_{i in block b}
  * x_m[i] * v[i mod vlen], b < ceil(n_total/block) (ragged last block). */
 ne_status ne_op_inner(const ne_config* cfg, ne_cstreams x, int64_t n_total, const int32_t* v,

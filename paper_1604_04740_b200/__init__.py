@@ -31,7 +31,7 @@ EXPORTS = (
     "ne_config_for", "ne_dynamic_range", "ne_certify", "ne_gemm_limbs_for", "ne_gemm_limb_plan", "ne_diag_reset",
     "ne_entangle", "ne_entangle_aos", "ne_entangle_limbs", "ne_entangle_stream", "ne_entangle_shared",
     "ne_entangle_limbs_stream", "ne_op_gemm_limbs_stream",
-    "ne_op_scale", "ne_op_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
+    "ne_op_scale", "ne_op_add", "ne_op_scale_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
     "ne_gemm_check_workspace", "ne_op_gemm_limbs_check",
     "ne_conv_geometry", "ne_entangle_limbs_conv", "ne_conv_prep_taps", "ne_op_conv_limbs",
@@ -80,6 +80,7 @@ _SIGS = {
     "ne_op_gemm_limbs_stream": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, _VP, _VP],
     "ne_op_scale": [_PCFG, Streams, _I64, _I64, _VP, _VP],
     "ne_op_add": [_PCFG, Streams, Streams, _I64, _I32, _VP],
+    "ne_op_scale_add": [_PCFG, Streams, _I64, _I64, _VP, Streams, _I32, _VP],
     "ne_op_inner": [_PCFG, Streams, _I64, _VP, _I64, _I64, Streams, _VP],
     "ne_op_outer": [_PCFG, Streams, _I64, _VP, _I64, Streams, _VP],
     "ne_op_conv": [_PCFG, Streams, _I64, _VP, _I32, _I32, Streams, _VP],
@@ -260,6 +261,11 @@ def ne_op_scale(cfg: Config, x, s: int = 1, g: torch.Tensor | None = None) -> No
 def ne_op_add(cfg: Config, x, addend, sign: int = 1) -> None:
     _call("ne_op_add", C.byref(cfg), _streams(x, torch.int64), _streams(addend, torch.int64), x[0].numel(),
           int(sign), _stream())
+
+
+def ne_op_scale_add(cfg: Config, x, s: int, addend, sign: int = 1, g: torch.Tensor | None = None) -> None:
+    _call("ne_op_scale_add", C.byref(cfg), _streams(x, torch.int64), x[0].numel(), int(s), _ptr(g, torch.int32),
+          _streams(addend, torch.int64), int(sign), _stream())
 
 
 def ne_op_inner(cfg: Config, x, v: torch.Tensor, block: int, out) -> None:

@@ -256,6 +256,13 @@ def test_scale_add_elementwise(O, M, N):
     a = rng.integers(-2 ** 62, 2 ** 62, size=(M, N))
     ne.ne_op_add(cfg, xs, to_streams(a, torch.int64), -1)
     assert (to_np(xs) == O.op_add(ocfg, ref, a, -1)).all()
+    ref2 = O.op_add(ocfg, ref, a, -1)
+    ne.ne_op_scale_add(cfg, xs, -7, to_streams(a, torch.int64), 1)       # fused scale + add
+    ref2 = O.op_add(ocfg, O.op_scale(ocfg, ref2, -7), a, 1)
+    assert (to_np(xs) == ref2).all()
+    gg = rng.integers(-2 ** 31, 2 ** 31, size=N)
+    ne.ne_op_scale_add(cfg, xs, 1, to_streams(a, torch.int64), -1, dev(gg, torch.int32))
+    assert (to_np(xs) == O.op_add(ocfg, O.op_scale(ocfg, ref2, 1, gg), a, -1)).all()
 
 
 @pytest.mark.parametrize("N,T", [(65536, 64), (1000, 64), (777, 1), (50, 300), (4099, 2500)])
