@@ -727,7 +727,8 @@ def run_c5(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_1604_04740_b200.dist import C5Plan, GpuBackend, c5_setup, c5_step, make_survivor_groups
+    from paper_1604_04740_b200.dist import (C5Plan, GpuBackend, c5_setup, c5_step, c5_step_failstop,
+                                            make_survivor_groups, owned_streams)
 
     torch.cuda.set_device(local_rank)
     plan = C5Plan()
@@ -759,11 +760,55 @@ def run_c5(args, rank, world, local_rank):
     be.stage_ms()
     ok = res.get("checksum_ok") in (True, None)
     total_ms = e0.elapsed_time(e1)
+    mine = owned_streams(plan.M, world, rank)
+
+    # end to end: the step's inputs (this rank's A_m, A_{m-1} and B) copied from
+    # pinned host memory, its checked outputs copied back, every step
+    hA = {m: (a.cpu().pin_memory(), b.cpu().pin_memory()) for m, (a, b) in inp["A"].items()}
+    hB = inp["B"].cpu().pin_memory()
+    h2d = sum(a.numel() * 4 + b.numel() * 4 for a, b in hA.values()) + hB.numel() * 4
+    hout = None
+    e2e_steps = max(2, min(args.steps, 5))
     if world > 1:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for i in range(e2e_steps):
+        for m, (a, b) in hA.items():
+            inp["A"][m][0].copy_(a, non_blocking=True)
+            inp["A"][m][1].copy_(b, non_blocking=True)
+        inp["B"].copy_(hB, non_blocking=True)
+        r2 = c5_step(be, plan, inp, groups, verify=False)
+        _, dchk = r2["check_slice"]
+        if hout is None:
+            hout = [torch.empty(t.numel(), dtype=t.dtype).pin_memory() for t in dchk]
+        for h, t in zip(hout, dchk):
+            h.copy_(t, non_blocking=True)
+    f1.record()
+    torch.cuda.synchronize()
+    be.stage_ms()
+    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    d2h = sum(h.numel() * 8 for h in hout)
+    if world > 1:
+        t = torch.tensor([total_ms, e2e_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms, e2e_ms = float(t[0].item()), float(t[1].item())
     ms = total_ms / args.steps
+
+    # real fail-stop (world == M): the rank of stream plan.kill exits its process
+    fs = None
+    if args.failstop == "exit" and world == plan.M and world > 1:
+        be.stage_ms()
+        store = dist.distributed_c10d._get_default_store()
+        t0 = time.perf_counter()
+        rf = c5_step_failstop(be, plan, inp, store, epoch=1, timeout_s=args.failstop_timeout)
+        st = be.stage_ms()
+        fs = {"real": True, "dead_rank": plan.kill, "view": rf["view"],
+              "detect_s_host": round(time.perf_counter() - t0, 3),
+              "stages_ms": {k: round(v, 3) for k, v in st.items()},
+              "recovered_stream": rf.get("recovered_stream"), "new_world": rf.get("new_world")}
+        rank = dist.get_rank()
     if rank != 0:
         return None
     stage_ms = {k: v / args.steps for k, v in stage_tot.items()}
@@ -788,10 +833,16 @@ def run_c5(args, rank, world, local_rank):
                      "frac": round(achieved / peak, 4), "traffic": None,
                      "peak_source": f"int8 dense = 2 x bf16 burst ({peak_src})"},
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
-        "gpu_launches": None,
+        "e2e": {"value": round(2 * plan.M * plan.rows * plan.cols * plan.K / 1e9 / (e2e_ms / 1e3), 3),
+                "unit": "Gop/s", "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        # per rank and step: prep_B, entangle + GEMM per owned stream, diag reset + check, recover
+        "gpu_launches": (1 + 2 * len(mine) + 2 + 1) * args.steps,
         "clocks": clk.summary(),
         "correctness": {"flagged_positions": flagged, "recovery_checksum_equal": ok},
     }
+    if fs is not None:
+        line["failstop"] = fs
     if world == 1:
         n = ORACLE_SAMPLE["c5"][0]
         dt, work, what = c5_oracle_sample(plan, n)
@@ -1078,6 +1129,10 @@ def main():
     ap.add_argument("--streams", type=int, default=8, help="c2p: M (paper: 3 or 8)")
     ap.add_argument("--w", type=int, default=64, choices=[64, 32], help="c1: container width (P:528-530)")
     ap.add_argument("--n", type=int, default=None, help="c1: stream length (default 4096 = configs[0])")
+    ap.add_argument("--failstop", default="simulated", choices=["simulated", "exit"],
+                    help="c5 at N = M = 8: after the timed steps, the rank of stream 3 exits its process and the "
+                         "survivors re-form the world and recover (dist.c5_step_failstop)")
+    ap.add_argument("--failstop-timeout", type=float, default=10.0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
     args = ap.parse_args()

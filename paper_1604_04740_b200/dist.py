@@ -20,6 +20,17 @@ Per rank, for each owned stream m (reading R13: stream m = row block m of A):
   7. (verify=True) an order-independent checksum of the checked and the
      recovered outputs, summed over ranks, must agree (bit-exact recovery).
 
+c5_step_failstop is the REAL fail-stop (NEXT-4, world == M): the rank holding
+stream plan.kill terminates its process right after its GEMM (os._exit), the
+survivors detect it by heartbeat keys in the rendezvous store (a missing key
+after `timeout_s` = a dead rank; the first published view wins via
+compare_set, so every survivor adopts the same one), tear down the old
+communicator (it includes the dead peer), form a new world of the survivors
+on a fresh store prefix, exchange the M-1 surviving outputs there and recover
+all M streams (Props 1/3).  With no failure the same step runs the check.
+The store must outlive any single rank (torchrun's agent store, or a
+TCPStore the launcher hosts); the process that hosts it must not be killed.
+
 The compute backend is injected: ``GpuBackend`` (libne.so kernels) is the
 product; the CPU tests drive the same orchestration with a test-only backend
 over gloo so the host logic (partitioning, exchange layout, recovery routing)
@@ -28,6 +39,9 @@ is exercised without GPUs.  No code here falls back to the CPU by itself.
 from __future__ import annotations
 
 import dataclasses
+import os
+import time
+from datetime import timedelta
 from typing import Sequence
 
 import torch
@@ -302,3 +316,87 @@ def c5_step(backend, plan: C5Plan, inp: dict, survivor_groups=None, verify: bool
 
 def c5_run(backend, plan: C5Plan, survivor_groups=None) -> dict:
     return c5_step(backend, plan, c5_setup(backend, plan), survivor_groups)
+
+
+# ---------------------------------------------------------------- real fail-stop
+def detect_alive(store, epoch: int, world: int, rank: int, timeout_s: float) -> list[int]:
+    """Heartbeat round `epoch`: publish this rank's key, wait up to timeout_s
+    for the others', then agree on one view (the first one published wins)."""
+    store.set(f"ne/alive/{epoch}/{rank}", "1")
+    deadline = time.monotonic() + timeout_s
+    alive = []
+    for r in range(world):
+        key = f"ne/alive/{epoch}/{r}"
+        while True:
+            if store.check([key]):
+                alive.append(r)
+                break
+            if time.monotonic() >= deadline:
+                break
+            time.sleep(0.01)
+    view = ",".join(str(r) for r in alive)
+    agreed = store.compare_set(f"ne/view/{epoch}", "", view)
+    agreed = agreed.decode() if isinstance(agreed, bytes) else agreed
+    return [int(x) for x in agreed.split(",") if x != ""]
+
+
+def reform_world(store, epoch: int, view: list[int], rank: int, backend_name: str) -> None:
+    """Replace the default process group (which includes the dead peer) by a
+    new one over the survivors in `view`, on a fresh store prefix."""
+    if dist.is_initialized():
+        dist.destroy_process_group()
+    prefix = dist.PrefixStore(f"ne/world/{epoch}", store)
+    dist.init_process_group(backend_name, store=prefix, rank=view.index(rank), world_size=len(view),
+                            timeout=timedelta(seconds=120))
+
+
+def c5_step_failstop(backend, plan: C5Plan, inp: dict, store, epoch: int = 0, timeout_s: float = 10.0,
+                     die: bool = True) -> dict:
+    """One C5 step with a real fail-stop (module doc).  world must equal M
+    (one stream per rank: a lost rank is a lost stream).  The rank owning
+    stream plan.kill exits its process after its GEMM when die is True."""
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    M, rows, cols, K = plan.M, plan.rows, plan.cols, plan.K
+    if world != M:
+        raise ValueError("real fail-stop needs one stream per rank (world == M)")
+    backend_name = dist.get_backend()
+    (m,) = owned_streams(M, world, rank)
+    backend.mark("start")
+    Bt = backend.prep_b(inp["B"], K, cols)
+    delta = backend.entangled_gemm(m, inp["A"][m][0], inp["A"][m][1], Bt, rows, cols, K)
+    backend.sync()
+    backend.mark("entangle_gemm")
+    if die and plan.kill is not None and m == plan.kill:
+        os._exit(0)  # fail-stop: the process, its memory and its GPU context are gone
+    view = detect_alive(store, epoch, world, rank, timeout_s)
+    backend.mark("detect")
+    result = {"streams": [m], "view": view}
+    if len(view) == world:
+        sl = position_major_exchange({m: delta}, M, list(range(world)), rank)
+        lo, _ = chunk_bounds(rows * cols, world)[rank]
+        d_chk, flagged = backend.check([sl[j] for j in range(M)], 0)
+        backend.mark("exchange_check")
+        result.update(flagged=int(_sum_u64(flagged, None)), check_slice=(lo, d_chk))
+        return result
+    dead = [r for r in range(world) if r not in view]
+    if len(dead) > 1:
+        raise RuntimeError(f"unrecoverable: {len(dead)} streams lost (S:113)")
+    r = dead[0]  # stream r == rank r
+    reform_world(store, epoch, view, rank, backend_name)
+    backend.mark("reform")
+    members = list(range(len(view)))
+    me = view.index(rank)
+    sl2 = _exchange_survivors({m: delta}, M, view, me)
+    lo2, _ = chunk_bounds(rows * cols, len(view))[me]
+    d_rec = backend.recover([None if j == r else sl2[j] for j in range(M)], r)
+    backend.mark("exchange_recover")
+    result.update(flagged=None, recovered_stream=r, recover_slice=(lo2, d_rec), new_rank=me,
+                  new_world=len(members))
+    return result
+
+
+def _exchange_survivors(local: dict[int, torch.Tensor], M: int, view: list[int], me: int) -> dict[int, torch.Tensor]:
+    """position_major_exchange in the re-formed world (new ranks 0..len(view)-1)."""
+    return position_major_exchange(local, M, list(range(len(view))), me, group=None)
+

@@ -123,3 +123,75 @@ def test_host_partition_helpers():
     assert owned_streams(8, 2, 1) == [1, 3, 5, 7]
     b = chunk_bounds(105, 4)
     assert b[0][0] == 0 and b[-1][1] == 105 and all(b[i][1] == b[i + 1][0] for i in range(3))
+
+
+# ------------------------------------------------------------------ real fail-stop (NEXT-4)
+def _failstop_worker(rank, world, host, port, plan_kw, timeout_s, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from datetime import timedelta
+
+    store = dist.TCPStore(host, port, world, is_master=False, timeout=timedelta(seconds=60))
+    dist.init_process_group("gloo", store=dist.PrefixStore("init", store), rank=rank, world_size=world)
+    import oracle as O
+    from _oracle_backend import OracleBackend
+    from paper_1604_04740_b200.dist import C5Plan, c5_setup, c5_step_failstop
+
+    plan = C5Plan(**plan_kw)
+    be = OracleBackend(plan.M, plan.bound)
+    res = c5_step_failstop(be, plan, c5_setup(be, plan), store, epoch=1, timeout_s=timeout_s)
+    M, R, Cc, K, b = plan.M, plan.rows, plan.cols, plan.K, plan.bound
+    B = O.gen_uniform(plan.seed, 5, 0, -b, b, K * Cc).reshape(K, Cc)
+    plain = np.stack([(O.gen_uniform(plan.seed, 4, m, -b, b, R * K).reshape(R, K) @ B).reshape(-1)
+                      for m in range(M)])
+    key = "recover_slice" if "recover_slice" in res else "check_slice"
+    lo, d = res[key]
+    ok = all((d[m].numpy() == plain[m, lo:lo + d[m].numel()]).all() for m in range(M))
+    covered = (lo, lo + d[0].numel())
+    q.put((rank, key, ok, res["view"], res.get("new_rank"), res.get("flagged"), covered))
+    dist.destroy_process_group()
+
+
+def _run_failstop(world, plan_kw, timeout_s=3.0):
+    from datetime import timedelta
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    # the rendezvous store lives in this (launcher) process, so it outlives any rank
+    store = dist.TCPStore("127.0.0.1", port, world, is_master=True, timeout=timedelta(seconds=60),
+                          wait_for_workers=False)
+    procs = [ctx.Process(target=_failstop_worker, args=(r, world, "127.0.0.1", port, plan_kw, timeout_s, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    alive = world - (1 if plan_kw.get("kill") is not None else 0)
+    out = sorted(q.get(timeout=300) for _ in range(alive))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    del store
+    return out
+
+
+def test_c5_real_failstop_process_exit_world8():
+    """The rank holding stream 3 exits its process after its GEMM; the other 7
+    detect it by heartbeat timeout, agree on the view, re-form a 7-rank world
+    on a fresh store prefix and recover all 8 streams bit-exactly; together
+    their slices cover every output position once."""
+    out = _run_failstop(8, dict(SMALL, kill=3))
+    assert [o[0] for o in out] == [0, 1, 2, 4, 5, 6, 7]
+    spans = []
+    for rank, key, ok, view, new_rank, flagged, covered in out:
+        assert key == "recover_slice" and ok
+        assert view == [0, 1, 2, 4, 5, 6, 7] and new_rank == view.index(rank)
+        spans.append(covered)
+    spans.sort()
+    n = SMALL["rows_total"] // SMALL["M"] * SMALL["cols"]
+    assert spans[0][0] == 0 and spans[-1][1] == n and all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_c5_real_failstop_no_failure_runs_the_check():
+    out = _run_failstop(8, dict(SMALL, kill=None))
+    for rank, key, ok, view, new_rank, flagged, covered in out:
+        assert key == "check_slice" and ok and flagged == 0 and view == list(range(8))
