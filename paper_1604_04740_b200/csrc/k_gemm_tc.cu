@@ -22,7 +22,6 @@
 // smem: STAGES x {L limb tiles 128 x 64 B, one B tile BN x 64 B} (64B swizzle),
 // 1024-B aligned; clusters of 2 CTAs along N multicast the limb tiles.
 #include <cuda.h>
-#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ne_internal.cuh"
@@ -562,15 +561,8 @@ static ne_status gemm_tc_dispatch(int M, int L, int b, const int8_t* planes, con
   }
 }
 
-ne_status launch_gemm_tc2(int M, int L, int b, int bn, const int8_t* planes, const int8_t* Bt, int64_t rows,
-                          int64_t cols, int64_t K, const ne_streams& C, cudaStream_t s);
-
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s) {
-  if (const char* e = getenv("NE_EXP_PAIR")) {
-    const int bn = atoi(e);
-    if (L <= 2 && rows % 256 == 0 && cols % bn == 0) return launch_gemm_tc2(M, L, b, bn, planes, Bt, rows, cols, K, C, s);
-  }
   return gemm_tc_dispatch<0>(M, L, b, planes, Bt, rows, cols, K, C, s, nullptr);
 }
 

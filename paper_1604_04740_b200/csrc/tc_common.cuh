@@ -1,5 +1,4 @@
-// tc_common.cuh — helpers shared by the tcgen05 kernels (k_gemm_tc.cu,
-// k_gemm_tc2.cu): mbarriers, TMA bulk-tensor loads, UMMA shared-memory and
+// tc_common.cuh — helpers of the tcgen05 kernels (k_gemm_tc.cu): mbarriers, TMA bulk-tensor loads, UMMA shared-memory and
 // instruction descriptors for kind::i8, TMEM loads, tensor-map encoding.
 // Part of the product path (libne); nothing here is shared with oracle/.
 #pragma once
