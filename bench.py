@@ -384,12 +384,13 @@ class C2Conv(Workload):
     name = "C2"
     metric_unit = "Gop/s"
 
-    def __init__(self, rank, n=65536, taps=64, seed=1, M=3, algo="tc", paper=False):
+    def __init__(self, rank, n=65536, taps=64, seed=1, M=3, algo="tc", paper=False, fuse=True):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
         self.M, self.n, self.T, self.algo, self.paper = M, n, taps, algo, paper
+        self.fuse = fuse and algo == "direct"  # the direct conv kernel carries the fused check
         if paper:
             self.name = "C2P"
         self.seed = seed + 1000 * rank
@@ -412,7 +413,7 @@ class C2Conv(Workload):
             self.launches_per_step = 5 + (1 if n % 128 else 0)
         else:
             self.eps = mk()
-            self.launches_per_step = 4
+            self.launches_per_step = 3 if self.fuse else 4
         self.bitmap = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
         self.diag = ne.diag_new()
 
@@ -428,6 +429,11 @@ class C2Conv(Workload):
                     ("prep_g", lambda: ne.ne_conv_prep_taps(self.g, 0, self.Gt, self.diag)),
                     ("conv", lambda: ne.ne_op_conv_limbs(cfg, self.planes, self.L, self.Gt, self.n, self.T, 0,
                                                          self.delta, self.limb_bits))] + tail
+        if self.fuse:
+            return [("entangle", lambda: ne.ne_entangle(cfg, self.c, self.eps, self.diag)),
+                    ("conv_check", lambda: ne.ne_op_conv_check(cfg, self.eps, self.g, self.delta, 0, self.dout,
+                                                               self.bitmap, self.diag)),
+                    tail[1]]
         return [("entangle", lambda: ne.ne_entangle(cfg, self.c, self.eps, self.diag)),
                 ("conv", lambda: ne.ne_op_conv(cfg, self.eps, self.g, self.delta))] + tail
 
@@ -445,6 +451,7 @@ class C2Conv(Workload):
             info["prep_g"] = ("hbm", (T * 4 + 128 * self.kpad) / 1e9, "GB")
         else:
             info["conv"] = ("alu", M * n * T / 1e12, "TMAC")
+            info["conv_check"] = ("alu", M * n * T / 1e12, "TMAC")
             info["entangle"] = ("hbm", M * n * 12 / 1e9, "GB")
         return info
 
@@ -462,7 +469,9 @@ class C2Conv(Workload):
                 "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
                 "l2": (f"working set {ws:.0f} MB" + (" fits L2 (launch-latency bound)" if ws < 100 else " > L2")),
                 "step": "entangle+prep_taps+conv+disentangle/check(r=0)+recover(r=step mod M)"
-                if self.algo == "tc" else "entangle+conv+disentangle/check(r=0)+recover(r=step mod M)"}
+                if self.algo == "tc" else ("entangle+conv with fused disentangle/check(r=0)+recover(r=step mod M)"
+                                           if self.fuse else
+                                           "entangle+conv+disentangle/check(r=0)+recover(r=step mod M)")}
 
     def e2e_setup(self):
         M = self.M
@@ -542,12 +551,12 @@ class C1Chain(Workload):
     name = "C1"
     metric_unit = "Gpositions/s"
 
-    def __init__(self, rank, n=4096, seed=0, w=64):
+    def __init__(self, rank, n=4096, seed=0, w=64, fuse=True):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
-        self.M, self.n, self.w = 3, n, w
+        self.M, self.n, self.w, self.fuse = 3, n, w, fuse
         self.seed = seed + 1000 * rank
         self.cfg = ne.ne_config_for(3, w)
         dt = torch.int64 if w == 64 else torch.int32
@@ -560,12 +569,26 @@ class C1Chain(Workload):
         self.eps, self.alpha, self.dout, self.drec = mk(), mk(), mk(), mk()
         self.bitmap = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
         self.diag = ne.diag_new()
-        self.launches_per_step = 5
+        self.launches_per_step = 4 if fuse else 5
 
     def stages(self, i):
         ne, cfg = self.ne, self.cfg
         r = i % 3
         part = [None if m == r else self.eps[m] for m in range(3)]
+        if self.fuse:
+            if self.w == 32:
+                ent = lambda: (ne.ne_entangle_w32(cfg, self.c, self.eps, self.diag),  # noqa: E731
+                               ne.ne_entangle_w32(cfg, self.a, self.alpha, self.diag))
+                opc = lambda: ne.ne_op_scale_add_check_w32(cfg, self.eps, 37, self.alpha, 0, self.dout,  # noqa: E731
+                                                           self.bitmap, self.diag)
+                rec = lambda: ne.ne_recover_w32(cfg, part, r, self.drec)  # noqa: E731
+            else:
+                ent = lambda: (ne.ne_entangle(cfg, self.c, self.eps, self.diag),  # noqa: E731
+                               ne.ne_entangle(cfg, self.a, self.alpha, self.diag))
+                opc = lambda: ne.ne_op_scale_add_check(cfg, self.eps, 37, self.alpha, 0, self.dout,  # noqa: E731
+                                                       self.bitmap, self.diag)
+                rec = lambda: ne.ne_recover(cfg, part, r, self.drec)  # noqa: E731
+            return [("entangle", ent), ("scale_add_check", opc), ("recover", rec)]
         if self.w == 32:
             return [("entangle", lambda: (ne.ne_entangle_w32(cfg, self.c, self.eps, self.diag),
                                           ne.ne_entangle_w32(cfg, self.a, self.alpha, self.diag))),
@@ -586,6 +609,7 @@ class C1Chain(Workload):
         n, B = self.n, self.w // 8
         sa = 3 * n * 3 * B  # fused scale + add: read eps, alpha, write eps
         return {"entangle": ("hbm", 2 * 3 * n * (4 + B) / 1e9, "GB"), "scale_add": ("hbm", sa / 1e9, "GB"),
+                "scale_add_check": ("hbm", (sa + 3 * n * B + n / 8) / 1e9, "GB"),  # + d_hat written
                 "check": ("hbm", 3 * n * 2 * B / 1e9, "GB"), "recover": ("hbm", 5 * n * B / 1e9, "GB")}
 
     def config(self):
@@ -594,7 +618,9 @@ class C1Chain(Workload):
                             "scale by 37, add a second seeded 3-stream set; disentangle+check" % self.n,
                 "M": 3, "n": self.n, "w": self.w, "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": self.w},
                 "l2": ("%.1f MB working set (launch-latency bound)" % (self.n * 3 * (8 + 4 * self.w // 8) / 1e6))
-                if small else "working set >> 126 MB L2 (no flush needed)"}
+                if small else "working set >> 126 MB L2 (no flush needed)",
+                "step": "entangle(c, a) + scale/add with fused disentangle/check(r=0) + recover(r=step mod 3)"
+                if self.fuse else "entangle(c, a) + scale/add + disentangle/check(r=0) + recover(r=step mod 3)"}
 
     def e2e_setup(self):
         self.hc = [x.cpu().pin_memory() for x in self.c + self.a]
@@ -635,13 +661,13 @@ ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c2p": (1, 1), "c3": (16, 2), "
 
 def make_workload(args, rank):
     if args.workload == "c3":
-        return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=args.fuse)
+        return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=bool(args.fuse or 0))
     if args.workload == "c2":
-        return C2Conv(rank, algo=args.conv or "direct")
+        return C2Conv(rank, algo=args.conv or "direct", fuse=bool(args.fuse if args.fuse is not None else 1))
     if args.workload == "c2p":
         return C2Conv(rank, n=10 ** 6, taps=args.taps, M=args.streams, algo=args.conv or "tc", paper=True)
     if args.workload == "c1":
-        return C1Chain(rank, n=args.n or 4096, w=args.w)
+        return C1Chain(rank, n=args.n or 4096, w=args.w, fuse=bool(args.fuse if args.fuse is not None else 1))
     return WORKLOADS[args.workload](rank)
 
 
@@ -1076,6 +1102,7 @@ def run_reference(args):
         paper = args.workload == "c2p"
         W.M, W.n, W.T, W.seed = (args.streams, 10 ** 6, args.taps, 1) if paper else (3, 65536, 64, 1)
         W.algo, W.paper, W.name = args.conv or ("tc" if paper else "direct"), paper, "C2P" if paper else "C2"
+        W.fuse = W.algo == "direct" and bool(args.fuse if args.fuse is not None else 1)
         W.L, W.limb_bits = 2, {3: 22, 4: 16, 8: 8}.get(W.M, 8)
         W.kpad = (W.T + 127 + 127) // 128 * 128
 
@@ -1084,6 +1111,7 @@ def run_reference(args):
         W.cfg = _Cfg
     else:
         W.M, W.n, W.seed, W.w = 3, args.n or 4096, 0, args.w
+        W.fuse = bool(args.fuse if args.fuse is not None else 1)
 
         class _Cfg:
             l, k = (22, 20) if args.w == 64 else (11, 10)
@@ -1120,8 +1148,9 @@ def main():
                     help="c3: GEMM operand digits: cheapest exact plan (default) or balanced base 256")
     ap.add_argument("--scheme", default="entangled", choices=["entangled", "abft"],
                     help="c3 only: numerical entanglement (default) or the paper's ABFT comparison method")
-    ap.add_argument("--fuse", type=int, default=0,
-                    help="c3: disentangle/check fused into the GEMM epilogue, or a separate pass (default: measured faster)")
+    ap.add_argument("--fuse", type=int, default=None,
+                    help="disentangle/check fused into the op kernel (1) or a separate pass (0); default: the "
+                         "measured-faster choice per workload (c1, c2: fused; c3: separate)")
     ap.add_argument("--conv", default=None, choices=["tc", "direct"],
                     help="c2/c2p: tensor-core Toeplitz conv or the direct IMAD kernel (default: the faster one "
                          "measured: direct for c2's 64 taps, tc for c2p)")

@@ -178,6 +178,21 @@ ne_status ne_op_add(const ne_config* cfg, ne_streams x, ne_cstreams addend, int6
 ne_status ne_op_scale_add(const ne_config* cfg, ne_streams x, int64_t n_total, int64_t s,
                           const int32_t* g_or_null, ne_cstreams addend, int32_t sign, ne_stream_t stream);
 
+/* Op + check fused (BASELINE north star: extract and check fused into the
+ * consumer kernel): ne_op_scale_add (resp. ne_op_conv) on every stream, delta
+ * stored to x (resp. out) as the unfused op does, then Eqs. 16-19 + 21 run on
+ * the values the kernel holds: d_out / bitmap / diag exactly as
+ * ne_disentangle_check(delta, r) (bit-identical; tests compare both).  Every
+ * stream's delta comes from that stream's operand only, so a fault in one
+ * stream's computation still corrupts one delta (Props 2/4).  M in {3, 4, 8}
+ * fused; other M run the two calls back to back.  Errors as the two calls. */
+ne_status ne_op_scale_add_check(const ne_config* cfg, ne_streams x, int64_t n_total, int64_t s,
+                                const int32_t* g_or_null, ne_cstreams addend, int32_t sign, int32_t r,
+                                ne_streams d_out, uint32_t* bitmap, ne_diag* diag, ne_stream_t stream);
+ne_status ne_op_conv_check(const ne_config* cfg, ne_cstreams x, int64_t n_total, const int32_t* g,
+                           int32_t taps, int32_t correlate, ne_streams out, int32_t r, ne_streams d_out,
+                           uint32_t* bitmap, ne_diag* diag, ne_stream_t stream);
+
 /* Blocked inner product <.,.> (Eq. 2): out_m[b] = sum_{i in block b}
  * x_m[i] * v[i mod vlen], b < ceil(n_total/block) (ragged last block). */
 ne_status ne_op_inner(const ne_config* cfg, ne_cstreams x, int64_t n_total, const int32_t* v,
@@ -348,6 +363,9 @@ ne_status ne_entangle_w32(const ne_config* cfg, ne_cstreams32 c, int64_t n_total
 ne_status ne_op_scale_add_w32(const ne_config* cfg, ne_streams32 x, int64_t n_total, int32_t s,
                               const int32_t* g_or_null, const ne_cstreams32* addend_or_null, int32_t sign,
                               ne_stream_t stream);
+ne_status ne_op_scale_add_check_w32(const ne_config* cfg, ne_streams32 x, int64_t n_total, int32_t s,
+                                    const int32_t* g_or_null, ne_cstreams32 addend, int32_t sign, int32_t r,
+                                    ne_streams32 d_out, uint32_t* bitmap, ne_diag* diag, ne_stream_t stream);
 ne_status ne_disentangle_check_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t n_total, int32_t r,
                                    ne_streams32 d_out, uint32_t* bitmap, ne_diag* diag, ne_stream_t stream);
 ne_status ne_recover_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t n_total, int32_t r,

@@ -35,6 +35,7 @@ EXPORTS = (
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
     "ne_gemm_check_workspace", "ne_op_gemm_limbs_check",
     "ne_conv_geometry", "ne_entangle_limbs_conv", "ne_conv_prep_taps", "ne_op_conv_limbs",
+    "ne_op_scale_add_check", "ne_op_conv_check", "ne_op_scale_add_check_w32",
     "ne_entangle_w32", "ne_op_scale_add_w32", "ne_disentangle_check_w32", "ne_recover_w32", "ne_inject_sweep_w32",
     "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
@@ -89,6 +90,9 @@ _SIGS = {
     "ne_op_gemm": [_PCFG, Streams, _VP, _I64, _I64, _I64, C.c_int, _I32, _I32, Streams, _VP, _SZ, _VP, _VP],
     "ne_gemm_prep_b": [_VP, _I64, _I64, _VP, _VP, _VP],
     "ne_op_gemm_limbs": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _VP],
+    "ne_op_scale_add_check": [_PCFG, Streams, _I64, _I64, _VP, Streams, _I32, _I32, Streams, _VP, _VP, _VP],
+    "ne_op_conv_check": [_PCFG, Streams, _I64, _VP, _I32, _I32, Streams, _I32, Streams, _VP, _VP, _VP],
+    "ne_op_scale_add_check_w32": [_PCFG, Streams, _I64, _I32, _VP, Streams, _I32, _I32, Streams, _VP, _VP, _VP],
     "ne_entangle_w32": [_PCFG, Streams, _I64, Streams, _VP, _VP],
     "ne_op_scale_add_w32": [_PCFG, Streams, _I64, _I32, _VP, C.POINTER(Streams), _I32, _VP],
     "ne_disentangle_check_w32": [_PCFG, Streams, _I64, _I32, Streams, _VP, _VP, _VP],
@@ -310,6 +314,27 @@ def ne_op_gemm_limbs(cfg: Config, planes: torch.Tensor, L: int, Bt: torch.Tensor
                      out, limb_bits: int = 8) -> None:
     _call("ne_op_gemm_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, limb_bits, _ptr(Bt, torch.int8), rows, cols,
           K, _streams(out, torch.int64), _stream())
+
+
+def ne_op_scale_add_check(cfg: Config, x, s: int, addend, r: int, d_out, bitmap: torch.Tensor | None = None,
+                          diag=None, sign: int = 1, g: torch.Tensor | None = None) -> None:
+    _call("ne_op_scale_add_check", C.byref(cfg), _streams(x, torch.int64), x[0].numel(), int(s), _ptr(g, torch.int32),
+          _streams(addend, torch.int64), int(sign), r, _streams(d_out, torch.int64), _ptr(bitmap, torch.int32),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_op_conv_check(cfg: Config, x, g: torch.Tensor, out, r: int, d_out, bitmap: torch.Tensor | None = None,
+                     diag=None, correlate: bool = False) -> None:
+    _call("ne_op_conv_check", C.byref(cfg), _streams(x, torch.int64), x[0].numel(), _ptr(g, torch.int32), g.numel(),
+          int(correlate), _streams(out, torch.int64), r, _streams(d_out, torch.int64), _ptr(bitmap, torch.int32),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_op_scale_add_check_w32(cfg: Config, x, s: int, addend, r: int, d_out, bitmap: torch.Tensor | None = None,
+                              diag=None, sign: int = 1, g: torch.Tensor | None = None) -> None:
+    _call("ne_op_scale_add_check_w32", C.byref(cfg), _streams(x, torch.int32), x[0].numel(), int(s),
+          _ptr(g, torch.int32), _streams(addend, torch.int32), int(sign), r, _streams(d_out, torch.int32),
+          _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _stream())
 
 
 # ------------------------------------------------------------------ w = 32 containers

@@ -16,15 +16,6 @@
 
 namespace ne {
 
-// interleave the low 16 bits of x with zeros: bit i -> bit 2i
-__device__ __forceinline__ uint32_t spread16(uint32_t x) {
-  x &= 0xffffu;
-  x = (x | (x << 8)) & 0x00ff00ffu;
-  x = (x | (x << 4)) & 0x0f0f0f0fu;
-  x = (x | (x << 2)) & 0x33333333u;
-  x = (x | (x << 1)) & 0x55555555u;
-  return x;
-}
 
 template <int MT, bool CHECK>
 __global__ void __launch_bounds__(kThreads)

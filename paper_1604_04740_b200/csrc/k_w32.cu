@@ -150,11 +150,14 @@ k_scale_add_w32(const __grid_constant__ ne_streams32 x, int M_rt, int64_t n, int
   }
 }
 
-template <int MT, bool CHECK>
+// OP: the C1 op fused in front (delta = x * (g ? g[n] : s) + sign * a, stored
+// back to x, then checked from registers; see k_opcheck.cu)
+template <int MT, bool CHECK, bool OP = false>
 __global__ void __launch_bounds__(kThreads)
 k_disentangle_w32(const __grid_constant__ ne_cstreams32 e, int M_rt, int l, int64_t n,
                   const __grid_constant__ ne_streams32 d_out, uint32_t* __restrict__ bitmap,
-                  ne_diag* __restrict__ diag) {
+                  ne_diag* __restrict__ diag, const __grid_constant__ ne_cstreams32 a = ne_cstreams32{},
+                  int32_t s = 1, const int32_t* __restrict__ g = nullptr, int32_t sign = 1) {
   constexpr int MA = MT > 0 ? MT : NE_MAX_M;
   const int M = MT > 0 ? MT : M_rt;
   const int64_t nv = (n + 3) / 4;
@@ -178,10 +181,33 @@ k_disentangle_w32(const __grid_constant__ ne_cstreams32 e, int M_rt, int l, int6
           continue;
         }
         if (full) {
-          const int4 a = __ldcs(reinterpret_cast<const int4*>(e.s[j] + n0));
-          q[0][j] = a.x; q[1][j] = a.y; q[2][j] = a.z; q[3][j] = a.w;
+          const int4 v4 = __ldcs(reinterpret_cast<const int4*>(e.s[j] + n0));
+          q[0][j] = v4.x; q[1][j] = v4.y; q[2][j] = v4.z; q[3][j] = v4.w;
         } else {
           for (int u = 0; u < 4; ++u) q[u][j] = n0 + u < n ? e.s[j][n0 + u] : 0;
+        }
+        if (OP) {
+          int32_t av[4], gv[4] = {s, s, s, s};
+          if (full) {
+            const int4 w4 = __ldcs(reinterpret_cast<const int4*>(a.s[j] + n0));
+            av[0] = w4.x; av[1] = w4.y; av[2] = w4.z; av[3] = w4.w;
+          } else {
+            for (int u = 0; u < 4; ++u) av[u] = n0 + u < n ? a.s[j][n0 + u] : 0;
+          }
+          if (g)
+            for (int u = 0; u < 4; ++u) gv[u] = n0 + u < n ? g[n0 + u] : 0;
+          int32_t o[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            o[u] = (int32_t)((uint32_t)q[u][j] * (uint32_t)gv[u] + (uint32_t)sign * (uint32_t)av[u]);
+            q[u][j] = o[u];
+          }
+          int32_t* xo = const_cast<int32_t*>(e.s[j]) + n0;
+          if (full)
+            __stcs(reinterpret_cast<int4*>(xo), make_int4(o[0], o[1], o[2], o[3]));
+          else
+            for (int u = 0; u < 4; ++u)
+              if (n0 + u < n) xo[u] = o[u];
         }
       }
       int32_t d[4][MA];
@@ -355,6 +381,31 @@ extern "C" ne_status ne_recover_w32(const ne_config* cfg, ne_cstreams32 delta, i
   if (n_total == 0) return NE_OK;
   if (n_total < 0 || !ok32(delta, cfg->M, r) || !ok32(d_out, cfg->M)) return NE_EINVAL;
   launch_dis32<false>(cfg, rotate(delta, cfg->M, r), n_total, rotate(d_out, cfg->M, r), nullptr, nullptr, cs(stream));
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_scale_add_check_w32(const ne_config* cfg, ne_streams32 x, int64_t n_total, int32_t s,
+                                               const int32_t* g_or_null, ne_cstreams32 addend, int32_t sign, int32_t r,
+                                               ne_streams32 d_out, uint32_t* bitmap, ne_diag* diag,
+                                               ne_stream_t stream) {
+  ne_status st = validate_cfg32(cfg);
+  if (st != NE_OK) return st;
+  if (r < 0 || r >= cfg->M) return NE_EINDEX;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || (sign != 1 && sign != -1) || !ok32(x, cfg->M) || !ok32(addend, cfg->M) || !ok32(d_out, cfg->M))
+    return NE_EINVAL;
+  ne_cstreams32 xc{};
+  for (int m = 0; m < cfg->M; ++m) xc.s[m] = x.s[m];
+  const ne_cstreams32 xr = rotate(xc, cfg->M, r), ar = rotate(addend, cfg->M, r);
+  const ne_streams32 dr = rotate(d_out, cfg->M, r);
+  const int grid = grid_for((n_total + 3) / 4, kThreads);
+  cudaStream_t cst = cs(stream);
+  switch (cfg->M) {
+    case 3: k_disentangle_w32<3, true, true><<<grid, kThreads, 0, cst>>>(xr, 3, cfg->l, n_total, dr, bitmap, diag, ar, s, g_or_null, sign); break;
+    case 4: k_disentangle_w32<4, true, true><<<grid, kThreads, 0, cst>>>(xr, 4, cfg->l, n_total, dr, bitmap, diag, ar, s, g_or_null, sign); break;
+    case 8: k_disentangle_w32<8, true, true><<<grid, kThreads, 0, cst>>>(xr, 8, cfg->l, n_total, dr, bitmap, diag, ar, s, g_or_null, sign); break;
+    default: k_disentangle_w32<0, true, true><<<grid, kThreads, 0, cst>>>(xr, cfg->M, cfg->l, n_total, dr, bitmap, diag, ar, s, g_or_null, sign); break;
+  }
   return launch_status();
 }
 

@@ -141,6 +141,17 @@ __device__ __forceinline__ bool digits_b(int64_t x, int b, int L, int8_t* d) {
   return ok && x == 0;
 }
 
+// interleave the low 16 bits of x with zeros: bit i -> bit 2i (bitmap words
+// of warps that own two consecutive positions per lane)
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x &= 0xffffu;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
 // warp-aggregated diagnostics: count + min index, one atomic per warp
 __device__ __forceinline__ void diag_add(unsigned long long* count, long long* first, int local_count,
                                          long long local_first) {

@@ -868,3 +868,59 @@ def test_conv_tensor_core_range_violations(O):
     ne.ne_conv_prep_taps(dev(g, torch.int32), 0, Gt, diag2)
     d2 = ne.diag_read(diag2)
     assert d2["range_violations"] == 2 and d2["first_bad"] == 9
+
+
+# ------------------------------------------------------------------ op + check fused in one kernel
+@pytest.mark.parametrize("M,N,r", [(3, 4096, 0), (3, 4099, 2), (4, 1001, 3), (8, 777, 5), (5, 300, 1)])
+def test_scale_add_check_fused(O, M, N, r):
+    """ne_op_scale_add_check == oracle scale + add + disentangle/check (delta
+    stored, d_hat, bitmap, count, first) on clean operands and with one
+    stream's stored eps corrupted before the op (a fault in that stream)."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 13, 1, M, N, -2 ** 10, 2 ** 10)
+    a = gen(O, 13, 2, M, N, -2 ** 10, 2 ** 10)
+    E, A = O.entangle(ocfg, c), O.entangle(ocfg, a)
+    for corrupt in (False, True):
+        Ec = E.copy()
+        if corrupt:
+            Ec[(r + 1) % M, N // 3] ^= 1 << 40
+            Ec[r, N - 1] ^= 12345
+        D = O.op_add(ocfg, O.op_scale(ocfg, Ec, 37), A, 1)
+        ref, flags, nf = O.disentangle_check(ocfg, D, r)
+        x = to_streams(Ec, torch.int64)
+        d_out = empty_streams(M, N)
+        bm = torch.full(((N + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        dg = ne.diag_new()
+        ne.ne_op_scale_add_check(cfg, x, 37, to_streams(A, torch.int64), r, d_out, bm, dg)
+        assert (to_np(x) == D).all() and (to_np(d_out) == ref).all()
+        assert (bitmap_to_flags(bm, N) == flags).all()
+        d = ne.diag_read(dg)
+        assert d["fault_positions"] == nf and (nf == 2) == corrupt
+        if corrupt:
+            assert d["first_fault"] == N // 3
+
+
+@pytest.mark.parametrize("M,N,T,correlate,r", [(3, 65536, 64, 0, 0), (3, 1000, 64, 1, 1), (4, 777, 1, 0, 2),
+                                               (8, 5000, 300, 1, 7), (3, 50, 300, 0, 0), (5, 2000, 64, 0, 4)])
+def test_conv_check_fused(O, M, N, T, correlate, r):
+    """ne_op_conv_check == oracle circular conv + disentangle/check, clean and
+    with a corrupted stored eps word (flags exactly where the oracle's are)."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 14, 1, M, N, -128, 128)
+    g = O.gen_uniform(14, 3, 0, -128, 128, T)
+    E = O.entangle(ocfg, c)
+    for corrupt in (False, True):
+        Ec = E.copy()
+        if corrupt:
+            Ec[(r + 2) % M, N // 2] ^= 1 << 7
+        D = O.op_conv(ocfg, Ec, g, bool(correlate))
+        ref, flags, nf = O.disentangle_check(ocfg, D, r)
+        out, d_out = empty_streams(M, N), empty_streams(M, N)
+        bm = torch.full(((N + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        dg = ne.diag_new()
+        ne.ne_op_conv_check(cfg, to_streams(Ec, torch.int64), dev(g, torch.int32), out, r, d_out, bm, dg,
+                            bool(correlate))
+        assert (to_np(out) == D).all() and (to_np(d_out) == ref).all()
+        assert (bitmap_to_flags(bm, N) == flags).all()
+        d = ne.diag_read(dg)
+        assert d["fault_positions"] == nf and (nf > 0) == corrupt

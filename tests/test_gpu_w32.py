@@ -158,3 +158,27 @@ def test_w32_range_violation_names_first(O):
     ne.ne_entangle_w32(cfg, to_streams(c), empty32(M, N), diag)
     d = ne.diag_read(diag)
     assert d["range_violations"] == 2 and d["first_bad"] == 1 * N + 4001
+
+
+@pytest.mark.parametrize("M,N,r", [(3, 4096, 0), (3, 4099, 1), (4, 1003, 3), (8, 515, 2), (5, 129, 4)])
+def test_w32_scale_add_check_fused(O, M, N, r):
+    cfg, ocfg = ne.ne_config_for(M, 32), O.config_for(M, 32)
+    hi = ne.ne_dynamic_range(cfg)
+    b = min(2 ** 10, hi // 40)
+    c = gen(O, 15, 1, M, N, -b, b + 1)
+    a = gen(O, 15, 2, M, N, -b, b + 1)
+    E, A = O.entangle(ocfg, c), O.entangle(ocfg, a)
+    for corrupt in (False, True):
+        Ec = E.copy()
+        if corrupt:
+            Ec[(r + 1) % M, N // 2] = O.wrap(ocfg, int(Ec[(r + 1) % M, N // 2]) ^ (1 << 20))
+        D = O.op_add(ocfg, O.op_scale(ocfg, Ec, 37), A, 1)
+        ref, flags, nf = O.disentangle_check(ocfg, D, r)
+        x = to_streams(Ec)
+        d_out = empty32(M, N)
+        bm = torch.full(((N + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        dg = ne.diag_new()
+        ne.ne_op_scale_add_check_w32(cfg, x, 37, to_streams(A), r, d_out, bm, dg)
+        assert (to_np(x) == D).all() and (to_np(d_out) == ref).all()
+        assert (bitmap_to_flags(bm, N) == flags).all()
+        assert ne.diag_read(dg)["fault_positions"] == nf and (nf == 1) == corrupt
