@@ -60,6 +60,25 @@ class Workload:
     def stages(self, i):  # -> list of (stage_name, callable)
         raise NotImplementedError
 
+    def _time(self, fn, reps):
+        """ms per call of fn, captured once in a CUDA graph and replayed: the
+        same launch path as the timed step, so plain and entangled compare."""
+        torch = self.torch
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
     def work_per_step(self):  # metric units per step (before /time)
         raise NotImplementedError
 
@@ -494,7 +513,9 @@ class C2Conv(Workload):
         (plain c in digit 0, other digits 0), (ii) one int8 digit; ms per call."""
         torch, ne = self.torch, self.ne
         if self.algo != "tc":
-            return {}
+            x64 = [c.to(torch.int64) for c in self.c]
+            o64 = [torch.empty_like(x) for x in x64]
+            return {"same_kernel_plain_int64": self._time(lambda: ne.ne_op_conv(self.cfg, x64, self.g, o64), reps)}
         M, out = self.M, {}
         for tag, L in (("same_kernel_L%d" % self.L, self.L), ("native_L1", 1)):
             planes = torch.zeros(M * L * self.plen, dtype=torch.int8, device="cuda")
@@ -637,7 +658,20 @@ class C1Chain(Workload):
             self.hout[m].copy_(self.dout[m], non_blocking=True)
 
     def plain_times(self, reps=20):
-        return {}
+        """The conventional routine on unentangled data (the paper's comparison,
+        F5): (i) the same scale+add kernel on plain values in the same
+        containers, (ii) the narrowest native form (int32 plain data, the w = 32
+        kernel); ms per call.  overhead_pct = step / plain - 1."""
+        torch, ne = self.torch, self.ne
+        cfg32 = ne.ne_config_for(3, 32)
+        x32 = [c.clone() for c in self.c]
+        native = self._time(lambda: ne.ne_op_scale_add_w32(cfg32, x32, 37, None, self.a, 1), reps)
+        if self.w == 32:
+            return {"same_kernel_plain_int32": native}
+        x64 = [c.to(torch.int64) for c in self.c]
+        a64 = [a.to(torch.int64) for a in self.a]
+        same = self._time(lambda: ne.ne_op_scale_add(self.cfg, x64, 37, a64), reps)
+        return {"same_kernel_plain_int64": same, "native_int32": native}
 
     def oracle_sample(self, reps):
         import oracle as O
