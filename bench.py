@@ -578,6 +578,8 @@ class C1Chain(Workload):
 
         self.ne, self.torch = ne, torch
         self.M, self.n, self.w, self.fuse = 3, n, w, fuse
+        if (n, w) != (4096, 64):
+            self.name = f"C1_w{w}_n{n}"  # traffic.json key of the sweep lines
         self.seed = seed + 1000 * rank
         self.cfg = ne.ne_config_for(3, w)
         dt = torch.int64 if w == 64 else torch.int32
@@ -780,6 +782,14 @@ def c5_oracle_sample(plan, ncols):
     return dt, 2 * M * ncols * K / 1e9, f"row 0 of each of the {M} stream blocks, first {ncols} of {plan.cols} columns"
 
 
+def c5_traffic(streams):
+    t = load_traffic()
+    g, e = t.get("C5:gemm"), t.get("C5:entangle")
+    if not g or not e:
+        return None
+    return round((g["GB"] + e["GB"]) * streams, 4)
+
+
 def run_c5(args, rank, world, local_rank):
     """configs[4]: M = 8 entangled streams (one per GPU when N = 8; stream m on
     rank m mod N otherwise), GEMM 16384^3 int32 U[-32,32) rows sharded, position-
@@ -890,7 +900,9 @@ def run_c5(args, rank, world, local_rank):
                    "single GPU: all 8 streams local, exchange is a local copy"},
         "roofline": {"bound": "tensor", "kernel": "entangle_gemm (k_entangle_limbs_stream + k_gemm_tc)",
                      "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TOP/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": c5_traffic(per_rank_streams),
+                     "traffic_unit": "GB per step and rank: ncu DRAM bytes of one stream's entangle + GEMM launch "
+                                     "(profiles/traffic.json) x streams on the rank",
                      "peak_source": f"int8 dense = 2 x bf16 burst ({peak_src})"},
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "e2e": {"value": round(2 * plan.M * plan.rows * plan.cols * plan.K / 1e9 / (e2e_ms / 1e3), 3),

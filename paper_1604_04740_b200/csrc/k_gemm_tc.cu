@@ -80,11 +80,15 @@ struct ChkArgs {
 // row tiles of the same column tile and share the B tile instead of the A
 // tile (each loads BN/CL rows of B and multicasts them) — the convolution's
 // G matrix is shared by every work item, its A windows by none.
+// raster_rows: row tiles fastest in the work order (consecutive clusters
+// share a column group of B instead of a row tile of A) — chosen when B does
+// not fit L2 next to the A operand, so each B panel is read from DRAM ~once.
 struct Geo {
   int64_t a_plane_rows;
   int64_t out_rows;
   int toeplitz;
   int mcast_b;
+  int raster_rows;
 };
 
 __device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps only
@@ -192,8 +196,13 @@ constexpr int kQN = 32;                          // check queue ring (tile ids)
 // order when the check is fused (CHK > 0), else stream-slowest
 template <int CHK>
 __device__ __forceinline__ void decode_work(int64_t w, int M, int64_t n_rt, int64_t n_cg, int& m, int64_t& rt,
-                                            int64_t& cg) {
-  if (CHK > 0) {
+                                            int64_t& cg, int raster_rows) {
+  if (CHK == 0 && raster_rows) {
+    m = (int)(w / (n_rt * n_cg));
+    const int64_t rem = w % (n_rt * n_cg);
+    cg = rem / n_rt;
+    rt = rem % n_rt;
+  } else if (CHK > 0) {
     m = (int)(w % M);
     const int64_t rem = w / M;
     rt = rem / n_cg;
@@ -275,7 +284,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       for (int64_t w = cid; w < n_work; w += ncl) {
         int m;
         int64_t rt, cg;
-        decode_work<CHK>(w, M, n_rt, n_cg, m, rt, cg);
+        decode_work<CHK>(w, M, n_rt, n_cg, m, rt, cg, geo.raster_rows);
         const int64_t row0 = mb ? (rt * CL + crank) * BM : rt * BM;
         const int64_t col0 = mb ? cg * BN : (cg * CL + crank) * BN;
         for (int kb = 0; kb < KB; ++kb, ++it) {
@@ -350,7 +359,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
     for (int64_t w = cid; w < n_work; w += ncl, ++tile) {
       int m;
       int64_t rt, cg;
-      decode_work<CHK>(w, M, n_rt, n_cg, m, rt, cg);
+      decode_work<CHK>(w, M, n_rt, n_cg, m, rt, cg, geo.raster_rows);
       const int64_t row0 = mb ? (rt * CL + crank) * BM : rt * BM;
       const int64_t col0 = mb ? cg * BN : (cg * CL + crank) * BN;
       const uint32_t ab = tile % CF::kBufs, use = tile / CF::kBufs;
@@ -481,7 +490,9 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
                      const Geo* geo_in = nullptr) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   if (cols % BN != 0 || K % CF::BK != 0) return NE_ENOTSUP;
-  const Geo geo = geo_in ? *geo_in : Geo{rows, rows, 0, 0};
+  // B panel larger than ~1/3 of L2: rasterise along rows (see Geo)
+  const int raster = (CHK == 0 && (uint64_t)cols * (uint64_t)K > (48ull << 20)) ? 1 : 0;
+  const Geo geo = geo_in ? *geo_in : Geo{rows, rows, 0, 0, raster};
   const bool mcb = CL > 1 && geo.mcast_b;
   if (mcb && rows % (BM * CL) != 0) return NE_ENOTSUP;
   if (!mcb && cols % (BN * CL) != 0) return NE_ENOTSUP;
@@ -576,7 +587,7 @@ ne_status launch_conv_tc(int M, int L, int b, const int8_t* planes, int64_t plan
   // 128-byte K stages (128B swizzle): each window row is one full 128-byte
   // line of the extended plane per stage (half the TMA row requests of 64-byte
   // stages; measured 0.125 -> 0.108 ms at M = 8, N = 10^6, T = 4500)
-  const tc::Geo geo{plane_rows, nblocks, 1, 1};
+  const tc::Geo geo{plane_rows, nblocks, 1, 1, 0};
   const int64_t rows = (nblocks + 255) / 256 * 256;
   if (Kpad % 128 != 0) return NE_EINVAL;
   switch (L) {
