@@ -592,22 +592,24 @@ class C1Chain(Workload):
         self.eps, self.alpha, self.dout, self.drec = mk(), mk(), mk(), mk()
         self.bitmap = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
         self.diag = ne.diag_new()
-        self.launches_per_step = 4 if fuse else 5
+        # fused: entangle_sets (1 launch; 2 for w = 64 streams > 2^22) + op/check + recover
+        self.launches_per_step = (3 if (w == 32 or n <= (1 << 22)) else 4) if fuse else 5
 
     def stages(self, i):
         ne, cfg = self.ne, self.cfg
         r = i % 3
         part = [None if m == r else self.eps[m] for m in range(3)]
         if self.fuse:
+            # operand set c and addend set a entangled in one launch (two stream sets)
             if self.w == 32:
-                ent = lambda: (ne.ne_entangle_w32(cfg, self.c, self.eps, self.diag),  # noqa: E731
-                               ne.ne_entangle_w32(cfg, self.a, self.alpha, self.diag))
+                ent = lambda: ne.ne_entangle_sets_w32(cfg, self.c + self.a, 2, self.eps + self.alpha,  # noqa: E731
+                                                      self.diag)
                 opc = lambda: ne.ne_op_scale_add_check_w32(cfg, self.eps, 37, self.alpha, 0, self.dout,  # noqa: E731
                                                            self.bitmap, self.diag)
                 rec = lambda: ne.ne_recover_w32(cfg, part, r, self.drec)  # noqa: E731
             else:
-                ent = lambda: (ne.ne_entangle(cfg, self.c, self.eps, self.diag),  # noqa: E731
-                               ne.ne_entangle(cfg, self.a, self.alpha, self.diag))
+                ent = lambda: ne.ne_entangle_sets(cfg, self.c + self.a, 2, self.eps + self.alpha,  # noqa: E731
+                                                  self.diag)
                 opc = lambda: ne.ne_op_scale_add_check(cfg, self.eps, 37, self.alpha, 0, self.dout,  # noqa: E731
                                                        self.bitmap, self.diag)
                 rec = lambda: ne.ne_recover(cfg, part, r, self.drec)  # noqa: E731
@@ -642,7 +644,8 @@ class C1Chain(Workload):
                 "M": 3, "n": self.n, "w": self.w, "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": self.w},
                 "l2": ("%.1f MB working set (launch-latency bound)" % (self.n * 3 * (8 + 4 * self.w // 8) / 1e6))
                 if small else "working set >> 126 MB L2 (no flush needed)",
-                "step": "entangle(c, a) + scale/add with fused disentangle/check(r=0) + recover(r=step mod 3)"
+                "step": "entangle(c, a: one launch) + scale/add with fused disentangle/check(r=0) + "
+                        "recover(r=step mod 3)"
                 if self.fuse else "entangle(c, a) + scale/add + disentangle/check(r=0) + recover(r=step mod 3)"}
 
     def e2e_setup(self):

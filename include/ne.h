@@ -126,6 +126,13 @@ ne_status ne_diag_reset(ne_diag* diag, ne_stream_t stream);
 ne_status ne_entangle(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, ne_streams eps,
                       ne_diag* diag, ne_stream_t stream);
 
+/* `sets` independent stream sets in one launch: set s is c.s[s*M .. s*M+M-1]
+ * -> eps.s[s*M .. s*M+M-1], each entangled by Eq. 15 on its own (the C1 chain
+ * entangles its operand set and its addend set together); first_bad =
+ * (s*M + m)*n_total + n.  sets*M <= NE_MAX_M. */
+ne_status ne_entangle_sets(const ne_config* cfg, ne_cstreams32 c, int32_t sets, int64_t n_total,
+                           ne_streams eps, ne_diag* diag, ne_stream_t stream);
+
 /* Same values, written position-major ("AoS"): eps_aos[n*M + m] — M int64 of
  * one position share DRAM sectors, so a gather by a permutation touches one
  * sector per position for M = 4.  eps_aos: 16-B aligned. */
@@ -358,6 +365,8 @@ ne_status ne_abft_recover(const ne_config* cfg, ne_cstreams d, const int64_t* e,
  * calls; NE_ECONFIG unless cfg->w == 32.                                      */
 ne_status ne_entangle_w32(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, ne_streams32 eps,
                           ne_diag* diag, ne_stream_t stream);
+ne_status ne_entangle_sets_w32(const ne_config* cfg, ne_cstreams32 c, int32_t sets, int64_t n_total,
+                               ne_streams32 eps, ne_diag* diag, ne_stream_t stream);
 /* x_m[n] = x_m[n] * (g ? g[n] : s) + sign * addend_m[n] (addend_or_null: a host
  * pointer to the entangled addend set, or NULL for scale only), in place. */
 ne_status ne_op_scale_add_w32(const ne_config* cfg, ne_streams32 x, int64_t n_total, int32_t s,

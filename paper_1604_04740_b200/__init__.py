@@ -29,7 +29,7 @@ NE_OP_SCALE, NE_OP_ADD, NE_OP_LINEAR, NE_OP_PERMUTE = 0, 1, 2, 3
 # every symbol include/ne.h and include/ne_gendev.h declare (checked by tests)
 EXPORTS = (
     "ne_config_for", "ne_dynamic_range", "ne_certify", "ne_gemm_limbs_for", "ne_gemm_limb_plan", "ne_diag_reset",
-    "ne_entangle", "ne_entangle_aos", "ne_entangle_limbs", "ne_entangle_stream", "ne_entangle_shared",
+    "ne_entangle", "ne_entangle_sets", "ne_entangle_sets_w32", "ne_entangle_aos", "ne_entangle_limbs", "ne_entangle_stream", "ne_entangle_shared",
     "ne_entangle_limbs_stream", "ne_op_gemm_limbs_stream",
     "ne_op_scale", "ne_op_add", "ne_op_scale_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
@@ -73,6 +73,8 @@ _SIGS = {
     "ne_gemm_limb_plan": [_PCFG, _I64, C.POINTER(_I32)],
     "ne_diag_reset": [_VP, _VP],
     "ne_entangle": [_PCFG, Streams, _I64, Streams, _VP, _VP],
+    "ne_entangle_sets": [_PCFG, Streams, _I32, _I64, Streams, _VP, _VP],
+    "ne_entangle_sets_w32": [_PCFG, Streams, _I32, _I64, Streams, _VP, _VP],
     "ne_entangle_aos": [_PCFG, Streams, _I64, _VP, _VP, _VP],
     "ne_entangle_limbs": [_PCFG, Streams, _I64, _I32, _I32, _VP, _VP, _VP],
     "ne_entangle_stream": [_PCFG, _I32, _VP, _VP, _VP, _I64, _VP, _VP],
@@ -222,6 +224,17 @@ def ne_entangle(cfg: Config, c: Sequence[torch.Tensor], eps: Sequence[torch.Tens
     n = c[0].numel()
     _call("ne_entangle", C.byref(cfg), _streams(c, torch.int32), n, _streams(eps, torch.int64),
           _ptr(diag, torch.int64), _stream())
+
+
+def ne_entangle_sets(cfg: Config, c, sets: int, eps, diag=None) -> None:
+    """c, eps: sets*M tensors (set s = entries s*M .. s*M+M-1)."""
+    _call("ne_entangle_sets", C.byref(cfg), _streams(c, torch.int32), sets, c[0].numel(), _streams(eps, torch.int64),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_entangle_sets_w32(cfg: Config, c, sets: int, eps, diag=None) -> None:
+    _call("ne_entangle_sets_w32", C.byref(cfg), _streams(c, torch.int32), sets, c[0].numel(),
+          _streams(eps, torch.int32), _ptr(diag, torch.int64), _stream())
 
 
 def ne_entangle_aos(cfg: Config, c, eps_aos: torch.Tensor, diag=None) -> None:

@@ -92,11 +92,18 @@ k_scale_add_check(const __grid_constant__ ne_streams x, const __grid_constant__ 
 }
 
 // Direct conv of all MT streams over a tile of 256 * P outputs; taps in chunks
-// of kTC staged in shared memory with the circular window of one stream at a
-// time; the int32-window fast path of k_conv.cu (IMAD.WIDE) when the window
-// fits int32, the full 64-bit MAC otherwise.  Thread t owns outputs
-// n0 + t + 256 p, so a warp's 32 consecutive outputs are one bitmap word.
-constexpr int kTCc = 1024;
+// of kTCc staged in shared memory together with the circular windows of ALL
+// MT streams (one load phase, one barrier per chunk: the windows' L2/DRAM
+// latencies overlap instead of adding up stream by stream); the int32-window
+// fast path of k_conv.cu (IMAD.WIDE) when every window fits int32, the full
+// 64-bit MAC otherwise.  Thread t owns outputs n0 + t + 256 p, so a warp's 32
+// consecutive outputs are one bitmap word.
+constexpr int kTCc = 256;
+
+template <int MT, int P>
+constexpr size_t conv_check_smem() {
+  return (size_t)MT * (256 * P + kTCc) * 12 + (size_t)kTCc * 4;
+}
 
 template <int MT, int P>
 __global__ void __launch_bounds__(256)
@@ -104,10 +111,11 @@ k_conv_check(const __grid_constant__ ne_cstreams x, const __grid_constant__ ne_s
              const int32_t* __restrict__ g, int T, int correlate, int l, const __grid_constant__ ne_streams d_out,
              uint32_t* __restrict__ bitmap, ne_diag* __restrict__ diag) {
   constexpr int TILE = 256 * P;
+  constexpr int WS = TILE + kTCc;  // window slots per stream
   extern __shared__ __align__(16) unsigned char smem[];
-  int64_t* xs = reinterpret_cast<int64_t*>(smem);                  // TILE + kTCc
-  int32_t* xs32 = reinterpret_cast<int32_t*>(xs + TILE + kTCc);    // TILE + kTCc
-  int32_t* gs = xs32 + TILE + kTCc;                                // kTCc
+  int64_t* xs = reinterpret_cast<int64_t*>(smem);            // [MT][WS]
+  int32_t* xs32 = reinterpret_cast<int32_t*>(xs + MT * WS);  // [MT][WS]
+  int32_t* gs = xs32 + MT * WS;                              // [kTCc]
   const int64_t n0 = (int64_t)blockIdx.x * TILE;
   int64_t acc[MT][P];
 #pragma unroll
@@ -119,40 +127,44 @@ k_conv_check(const __grid_constant__ ne_cstreams x, const __grid_constant__ ne_s
     const int tc = T - j0 < kTCc ? T - j0 : kTCc;
     const int wlen = TILE + tc - 1;
     for (int j = threadIdx.x; j < tc; j += 256) gs[j] = __ldg(g + j0 + j);
+    int64_t base = correlate ? (n0 + j0) : (n0 - j0 - (tc - 1));
+    base %= N;
+    if (base < 0) base += N;
+    int fits = 1;
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
-      int64_t base = correlate ? (n0 + j0) : (n0 - j0 - (tc - 1));
-      base %= N;
-      if (base < 0) base += N;
-      int fits = 1;
       for (int q = threadIdx.x; q < wlen; q += 256) {
         int64_t idx = base + q;
-        idx %= N;
+        if (idx >= N) idx %= N;
         const int64_t val = __ldg(x.s[m] + idx);
-        xs[q] = val;
-        xs32[q] = (int32_t)val;
+        xs[m * WS + q] = val;
+        xs32[m * WS + q] = (int32_t)val;
         fits &= (val == (int64_t)(int32_t)val);
       }
-      fits = __syncthreads_and(fits);
-      if (fits) {
-        for (int j = 0; j < tc; ++j) {
-          const int64_t gj = gs[j];
-          const int off = correlate ? j : (tc - 1 - j);
-#pragma unroll
-          for (int p = 0; p < P; ++p)
-            acc[m][p] = (int64_t)((uint64_t)acc[m][p] + (uint64_t)(gj * (int64_t)xs32[threadIdx.x + 256 * p + off]));
-        }
-      } else {
-        for (int j = 0; j < tc; ++j) {
-          const uint64_t gj = (uint64_t)(int64_t)gs[j];
-          const int off = correlate ? j : (tc - 1 - j);
-#pragma unroll
-          for (int p = 0; p < P; ++p)
-            acc[m][p] = (int64_t)((uint64_t)acc[m][p] + gj * (uint64_t)xs[threadIdx.x + 256 * p + off]);
-        }
-      }
-      __syncthreads();
     }
+    fits = __syncthreads_and(fits);
+    if (fits) {
+      for (int j = 0; j < tc; ++j) {
+        const int64_t gj = gs[j];
+        const int off = correlate ? j : (tc - 1 - j);
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int p = 0; p < P; ++p)
+            acc[m][p] = (int64_t)((uint64_t)acc[m][p] + (uint64_t)(gj * (int64_t)xs32[m * WS + threadIdx.x + 256 * p + off]));
+      }
+    } else {
+      for (int j = 0; j < tc; ++j) {
+        const uint64_t gj = (uint64_t)(int64_t)gs[j];
+        const int off = correlate ? j : (tc - 1 - j);
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int p = 0; p < P; ++p)
+            acc[m][p] = (int64_t)((uint64_t)acc[m][p] + gj * (uint64_t)xs[m * WS + threadIdx.x + 256 * p + off]);
+      }
+    }
+    __syncthreads();
   }
   const int lane = threadIdx.x & 31;
   int nflag = 0;
@@ -225,7 +237,8 @@ template <int MT, int P>
 static void launch_conv_check(const ne_config* cfg, const ne_cstreams& xr, int64_t n, const int32_t* g, int taps,
                               int correlate, const ne_streams& outr, const ne_streams& dr, uint32_t* bitmap,
                               ne_diag* diag, cudaStream_t s) {
-  const size_t smem = (size_t)(256 * P + kTCc) * 12 + (size_t)kTCc * 4;
+  constexpr size_t smem = conv_check_smem<MT, P>();
+  cudaFuncSetAttribute(k_conv_check<MT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const unsigned grid = (unsigned)((n + 256 * P - 1) / (256 * P));
   k_conv_check<MT, P><<<grid, 256, smem, s>>>(xr, outr, n, g, taps, correlate, cfg->l, dr, bitmap, diag);
 }

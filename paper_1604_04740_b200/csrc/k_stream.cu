@@ -24,8 +24,9 @@ template <int MT, int OUT>
 __global__ void __launch_bounds__(kThreads)
 k_entangle(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n,
            const __grid_constant__ ne_streams eps, int64_t* __restrict__ eps_aos, int8_t* __restrict__ planes,
-           int L, ne_diag* __restrict__ diag) {
+           int L, ne_diag* __restrict__ diag, int set0 = 0) {
   const int M = MT > 0 ? MT : M_rt;
+  const int so = (blockIdx.y + set0) * M;  // stream-set offset (ne_entangle_sets; 0 otherwise)
   int bad = 0;
   long long first = LLONG_MAX;
   const int64_t nvec = (n + 3) / 4;
@@ -36,7 +37,7 @@ k_entangle(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi,
     int32_t first_c[4], prev[4];
     // c_{M-1} first: it is the "previous" stream of stream 0 (circulant Eq. 14)
     {
-      const int32_t* p = c.s[M - 1] + n0;
+      const int32_t* p = c.s[so + M - 1] + n0;
       if (full) {
         int4 q = __ldcs(reinterpret_cast<const int4*>(p));
         first_c[0] = q.x; first_c[1] = q.y; first_c[2] = q.z; first_c[3] = q.w;
@@ -52,7 +53,7 @@ k_entangle(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi,
       if (m == M - 1) {
         for (int i = 0; i < 4; ++i) cur[i] = first_c[i];
       } else {
-        const int32_t* p = c.s[m] + n0;
+        const int32_t* p = c.s[so + m] + n0;
         if (full) {
           int4 q = __ldcs(reinterpret_cast<const int4*>(p));
           cur[0] = q.x; cur[1] = q.y; cur[2] = q.z; cur[3] = q.w;
@@ -67,12 +68,12 @@ k_entangle(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi,
         const int64_t ci = cur[i];
         if ((ci > hi || ci < -hi) && n0 + i < n) {
           ++bad;
-          long long idx = (long long)m * n + n0 + i;
+          long long idx = (long long)(so + m) * n + n0 + i;
           first = idx < first ? idx : first;
         }
       }
       if (OUT == 0) {
-        int64_t* q = eps.s[m] + n0;
+        int64_t* q = eps.s[so + m] + n0;
         if (full) {
           __stcs(reinterpret_cast<longlong2*>(q), make_longlong2(e[0], e[1]));
           __stcs(reinterpret_cast<longlong2*>(q) + 1, make_longlong2(e[2], e[3]));
@@ -613,6 +614,31 @@ extern "C" ne_status ne_entangle(const ne_config* cfg, ne_cstreams32 c, int64_t 
   if (n_total == 0) return NE_OK;
   if (n_total < 0 || !streams_ok32(c, cfg->M) || !streams_ok(eps, cfg->M)) return NE_EINVAL;
   return launch_entangle<0>(cfg, c, n_total, eps, nullptr, nullptr, 0, diag, stream);
+}
+
+extern "C" ne_status ne_entangle_sets(const ne_config* cfg, ne_cstreams32 c, int32_t sets, int64_t n_total,
+                                      ne_streams eps, ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (sets < 1 || sets * cfg->M > NE_MAX_M) return NE_EINVAL;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !streams_ok32(c, sets * cfg->M) || !streams_ok(eps, sets * cfg->M)) return NE_EINVAL;
+  const int64_t hi = range_hi(cfg);
+  cudaStream_t s = cs(stream);
+  // small streams: all sets in one launch (grid.y = set; launch latency
+  // dominates); large streams: one launch per set (measured faster at 2^27)
+  const bool one = n_total <= (1 << 22);
+  const int ny = one ? sets : 1;
+  const dim3 grid((unsigned)grid_for((n_total + 3) / 4, kThreads, one ? (8 + sets - 1) / sets : 8), (unsigned)ny);
+  for (int s0 = 0; s0 < sets; s0 += ny) {
+    switch (cfg->M) {
+      case 3: k_entangle<3, 0><<<grid, kThreads, 0, s>>>(c, 3, cfg->l, hi, n_total, eps, nullptr, nullptr, 0, diag, s0); break;
+      case 4: k_entangle<4, 0><<<grid, kThreads, 0, s>>>(c, 4, cfg->l, hi, n_total, eps, nullptr, nullptr, 0, diag, s0); break;
+      case 8: k_entangle<8, 0><<<grid, kThreads, 0, s>>>(c, 8, cfg->l, hi, n_total, eps, nullptr, nullptr, 0, diag, s0); break;
+      default: k_entangle<0, 0><<<grid, kThreads, 0, s>>>(c, cfg->M, cfg->l, hi, n_total, eps, nullptr, nullptr, 0, diag, s0); break;
+    }
+  }
+  return launch_status();
 }
 
 extern "C" ne_status ne_entangle_aos(const ne_config* cfg, ne_cstreams32 c, int64_t n_total,

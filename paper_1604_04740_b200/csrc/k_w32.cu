@@ -69,6 +69,7 @@ k_entangle_w32(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t
                const __grid_constant__ ne_streams32 eps, ne_diag* __restrict__ diag) {
   constexpr int MA = MT > 0 ? MT : NE_MAX_M;
   const int M = MT > 0 ? MT : M_rt;
+  const int so = blockIdx.y * M;  // stream-set offset (ne_entangle_sets_w32; 0 otherwise)
   int bad = 0;
   long long first = LLONG_MAX;
   const int64_t nv = (n + 3) / 4;
@@ -79,10 +80,10 @@ k_entangle_w32(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t
 #pragma unroll
     for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
       if (full) {
-        const int4 a = __ldcs(reinterpret_cast<const int4*>(c.s[m] + n0));
+        const int4 a = __ldcs(reinterpret_cast<const int4*>(c.s[so + m] + n0));
         q[m][0] = a.x; q[m][1] = a.y; q[m][2] = a.z; q[m][3] = a.w;
       } else {
-        for (int u = 0; u < 4; ++u) q[m][u] = n0 + u < n ? c.s[m][n0 + u] : 0;
+        for (int u = 0; u < 4; ++u) q[m][u] = n0 + u < n ? c.s[so + m][n0 + u] : 0;
       }
     }
 #pragma unroll
@@ -94,15 +95,15 @@ k_entangle_w32(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t
         o[u] = (int32_t)((uint32_t)q[m][u] + ((uint32_t)q[mp][u] << l));  // Eq. 15 mod 2^32
         if (n0 + u < n && (q[m][u] > hi || q[m][u] < -hi)) {
           ++bad;
-          const long long idx = (long long)m * n + n0 + u;
+          const long long idx = (long long)(so + m) * n + n0 + u;
           first = idx < first ? idx : first;
         }
       }
       if (full)
-        __stcs(reinterpret_cast<int4*>(eps.s[m] + n0), make_int4(o[0], o[1], o[2], o[3]));
+        __stcs(reinterpret_cast<int4*>(eps.s[so + m] + n0), make_int4(o[0], o[1], o[2], o[3]));
       else
         for (int u = 0; u < 4; ++u)
-          if (n0 + u < n) eps.s[m][n0 + u] = o[u];
+          if (n0 + u < n) eps.s[so + m][n0 + u] = o[u];
     }
   }
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
@@ -327,6 +328,18 @@ extern "C" ne_status ne_entangle_w32(const ne_config* cfg, ne_cstreams32 c, int6
   if (n_total < 0 || !ok32(c, cfg->M) || !ok32(eps, cfg->M)) return NE_EINVAL;
   NE_W32_M(cfg->M, k_entangle_w32, grid_for((n_total + 3) / 4, kThreads), cs(stream), c, cfg->M, cfg->l,
            range_hi(cfg), n_total, eps, diag);
+  return launch_status();
+}
+
+extern "C" ne_status ne_entangle_sets_w32(const ne_config* cfg, ne_cstreams32 c, int32_t sets, int64_t n_total,
+                                          ne_streams32 eps, ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg32(cfg);
+  if (st != NE_OK) return st;
+  if (sets < 1 || sets * cfg->M > NE_MAX_M) return NE_EINVAL;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !ok32(c, sets * cfg->M) || !ok32(eps, sets * cfg->M)) return NE_EINVAL;
+  const dim3 grid((unsigned)grid_for((n_total + 3) / 4, kThreads, (8 + sets - 1) / sets), (unsigned)sets);
+  NE_W32_M(cfg->M, k_entangle_w32, grid, cs(stream), c, cfg->M, cfg->l, range_hi(cfg), n_total, eps, diag);
   return launch_status();
 }
 

@@ -924,3 +924,24 @@ def test_conv_check_fused(O, M, N, T, correlate, r):
         assert (bitmap_to_flags(bm, N) == flags).all()
         d = ne.diag_read(dg)
         assert d["fault_positions"] == nf and (nf > 0) == corrupt
+
+
+@pytest.mark.parametrize("M,sets,N", [(3, 2, 4096), (3, 2, 4099), (4, 3, 1001), (8, 4, 130), (5, 2, 77)])
+def test_entangle_sets(O, M, sets, N):
+    """Several independent stream sets in one launch: each set equals the
+    oracle's entangle of that set; a range violation names (s*M + m)*N + n."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = np.concatenate([gen(O, 16 + s, 1, M, N, -1000, 1000) for s in range(sets)])
+    eps = empty_streams(sets * M, N)
+    diag = ne.diag_new()
+    ne.ne_entangle_sets(cfg, to_streams(c), sets, eps, diag)
+    got = to_np(eps)
+    for s in range(sets):
+        assert (got[s * M:(s + 1) * M] == O.entangle(ocfg, c[s * M:(s + 1) * M])).all()
+    assert ne.diag_read(diag)["range_violations"] == 0
+    hi = ne.ne_dynamic_range(cfg)
+    c[(sets - 1) * M + 1, N - 1] = hi + 1 if hi < 2 ** 31 - 1 else c[0, 0]
+    if hi < 2 ** 31 - 1:
+        ne.ne_entangle_sets(cfg, to_streams(c), sets, eps, diag)
+        d = ne.diag_read(diag)
+        assert d["range_violations"] == 1 and d["first_bad"] == ((sets - 1) * M + 1) * N + N - 1

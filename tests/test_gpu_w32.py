@@ -182,3 +182,21 @@ def test_w32_scale_add_check_fused(O, M, N, r):
         assert (to_np(x) == D).all() and (to_np(d_out) == ref).all()
         assert (bitmap_to_flags(bm, N) == flags).all()
         assert ne.diag_read(dg)["fault_positions"] == nf and (nf == 1) == corrupt
+
+
+@pytest.mark.parametrize("M,sets,N", [(3, 2, 4096), (3, 2, 4099), (4, 3, 1001)])
+def test_w32_entangle_sets(O, M, sets, N):
+    cfg, ocfg = ne.ne_config_for(M, 32), O.config_for(M, 32)
+    hi = ne.ne_dynamic_range(cfg)
+    c = np.concatenate([gen(O, 20 + s, 1, M, N, -hi, hi + 1) for s in range(sets)])
+    eps = empty32(sets * M, N)
+    diag = ne.diag_new()
+    ne.ne_entangle_sets_w32(cfg, to_streams(c), sets, eps, diag)
+    got = to_np(eps)
+    for s in range(sets):
+        assert (got[s * M:(s + 1) * M] == O.entangle(ocfg, c[s * M:(s + 1) * M])).all()
+    assert ne.diag_read(diag)["range_violations"] == 0
+    c[M + 2, 7] = hi + 1
+    ne.ne_entangle_sets_w32(cfg, to_streams(c), sets, eps, diag)
+    d = ne.diag_read(diag)
+    assert d["range_violations"] == 1 and d["first_bad"] == (M + 2) * N + 7
