@@ -291,12 +291,14 @@ class C4PermInner(Workload):
     name = "C4"
     metric_unit = "GB/s"
 
-    def __init__(self, rank, n=1 << 28, seed=3):
+    def __init__(self, rank, n=1 << 28, seed=3, layout="aos"):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
-        self.M, self.n, self.B = 4, n, 1024
+        self.M, self.n, self.B, self.layout = 4, n, 1024, layout
+        if layout != "aos":
+            self.name = "C4_soa"
         self.seed = seed + 1000 * rank
         self.cfg = ne.ne_config_for(4)
         dev = "cuda"
@@ -307,7 +309,10 @@ class C4PermInner(Workload):
         ne.ne_gen_perm_i32(self.seed, 6, self.perm)
         self.v = torch.empty(self.B, dtype=torch.int32, device=dev)
         ne.ne_gen_uniform_i32(self.seed, 7, 0, -(1 << 12), 1 << 12, self.v)
-        self.eps = torch.empty(n * 4, dtype=torch.int64, device=dev)
+        if layout == "aos":
+            self.eps = torch.empty(n * 4, dtype=torch.int64, device=dev)
+        else:  # SoA: one int64 stream per m (each gathered position touches 4 sectors)
+            self.eps = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(4)]
         self.nb = n // self.B
         self.delta = [torch.empty(self.nb, dtype=torch.int64, device=dev) for _ in range(4)]
         self.dout = [torch.empty(self.nb, dtype=torch.int64, device=dev) for _ in range(4)]
@@ -320,6 +325,14 @@ class C4PermInner(Workload):
         ne, cfg = self.ne, self.cfg
         r = i % 4
         part = [None if m == r else self.delta[m] for m in range(4)]
+        if self.layout != "aos":
+            return [
+                ("entangle", lambda: ne.ne_entangle(cfg, self.c, self.eps, self.diag)),
+                ("permute_inner_check", lambda: ne.ne_op_permute_inner_check(
+                    cfg, self.v, self.B, 0, self.dout, x=self.eps, perm=self.perm, n=self.n,
+                    delta_out=self.delta, bitmap=self.bitmap, diag=self.diag)),
+                ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
+            ]
         return [
             ("entangle", lambda: ne.ne_entangle_aos(cfg, self.c, self.eps, self.diag)),
             ("permute_inner_check", lambda: ne.ne_op_permute_inner_check(
@@ -340,7 +353,9 @@ class C4PermInner(Workload):
     def config(self):
         return {"workload": "C4 (BASELINE configs[3]): M=4 streams of 2^28 int32 U[-2^12,2^12), seeded "
                             "permutation, inner products with a shared 1024-vector in blocks of 1024",
-                "M": 4, "n": self.n, "block": self.B, "layout": "AoS (position-major) entangled int64",
+                "M": 4, "n": self.n, "block": self.B,
+                "layout": "AoS (position-major) entangled int64" if self.layout == "aos" else
+                          "SoA (one int64 stream per m; 4 random sectors per gathered position)",
                 "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
                 "l2": "working set ~13 GB >> 126 MB L2 (no flush needed)",
                 "step": "entangle(AoS)+gather/inner/disentangle/check fused(r=0)+recover(r=step mod 4)"}
@@ -362,6 +377,8 @@ class C4PermInner(Workload):
         """Same gather + inner kernel on plain (unentangled) data in the same
         int64 AoS containers, no check: the paper's conventional routine."""
         torch, ne = self.torch, self.ne
+        if self.layout != "aos":
+            return {}
         plain = torch.stack([x.to(torch.int64) for x in self.c], dim=1).reshape(-1).contiguous()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ne.ne_op_permute_inner_check(self.cfg, self.v, self.B, 0, self.drec, x_aos=plain, perm=self.perm,
@@ -705,6 +722,8 @@ def make_workload(args, rank):
         return C2Conv(rank, algo=args.conv or "direct", fuse=bool(args.fuse if args.fuse is not None else 1))
     if args.workload == "c2p":
         return C2Conv(rank, n=10 ** 6, taps=args.taps, M=args.streams, algo=args.conv or "tc", paper=True)
+    if args.workload == "c4":
+        return C4PermInner(rank, layout=args.layout)
     if args.workload == "c1":
         return C1Chain(rank, n=args.n or 4096, w=args.w, fuse=bool(args.fuse if args.fuse is not None else 1))
     return WORKLOADS[args.workload](rank)
@@ -1123,7 +1142,7 @@ def run_reference(args):
             l, k = 22, 20
         W.cfg = _Cfg
     elif args.workload == "c4":
-        W.M, W.n, W.B, W.seed = 4, 1 << 28, 1024, 3
+        W.M, W.n, W.B, W.seed, W.layout = 4, 1 << 28, 1024, 3, args.layout
 
         class _Cfg:
             l, k = 16, 16
@@ -1206,6 +1225,7 @@ def main():
     ap.add_argument("--taps", type=int, default=4500, help="c2p: kernel taps (paper: 100-4500)")
     ap.add_argument("--streams", type=int, default=8, help="c2p: M (paper: 3 or 8)")
     ap.add_argument("--w", type=int, default=64, choices=[64, 32], help="c1: container width (P:528-530)")
+    ap.add_argument("--layout", default="aos", choices=["aos", "soa"], help="c4: entangled layout at rest")
     ap.add_argument("--n", type=int, default=None, help="c1: stream length (default 4096 = configs[0])")
     ap.add_argument("--failstop", default="simulated", choices=["simulated", "exit"],
                     help="c5 at N = M = 8: after the timed steps, the rank of stream 3 exits its process and the "
