@@ -443,9 +443,9 @@ class C2Conv(Workload):
             # is its two int8 halves (the pair plan; |c| <= 127 in the plan's symmetric terms
             # plus c = -128, whose digit is still int8); the entangle kernel asserts it per value
             self.L, self.limb_bits = ne.ne_gemm_limb_plan(self.cfg, 127)
-            self.kpad, self.plen = ne.ne_conv_geometry(n, taps)
+            self.block, self.kpad, self.plen = ne.ne_conv_geometry(n, taps, self.L)
             self.planes = torch.empty(M * self.L * self.plen, dtype=torch.int8, device="cuda")
-            self.Gt = torch.empty(128 * self.kpad, dtype=torch.int8, device="cuda")
+            self.Gt = torch.empty(self.block * self.kpad, dtype=torch.int8, device="cuda")
             self.launches_per_step = 5 + (1 if n % 128 else 0)
         else:
             self.eps = mk()
@@ -461,10 +461,10 @@ class C2Conv(Workload):
                 ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec))]
         if self.algo == "tc":
             return [("entangle", lambda: ne.ne_entangle_limbs_conv(cfg, self.c, self.T, 0, self.L, self.planes,
-                                                                   self.diag, self.limb_bits)),
-                    ("prep_g", lambda: ne.ne_conv_prep_taps(self.g, 0, self.Gt, self.diag)),
+                                                                   self.diag, self.limb_bits, self.block)),
+                    ("prep_g", lambda: ne.ne_conv_prep_taps(self.g, 0, self.Gt, self.diag, self.block)),
                     ("conv", lambda: ne.ne_op_conv_limbs(cfg, self.planes, self.L, self.Gt, self.n, self.T, 0,
-                                                         self.delta, self.limb_bits))] + tail
+                                                         self.delta, self.limb_bits, self.block))] + tail
         if self.fuse:
             return [("entangle", lambda: ne.ne_entangle(cfg, self.c, self.eps, self.diag)),
                     ("conv_check", lambda: ne.ne_op_conv_check(cfg, self.eps, self.g, self.delta, 0, self.dout,
@@ -484,7 +484,7 @@ class C2Conv(Workload):
             # useful limb products only (the Toeplitz zeros, Kpad/T - 1, are not counted)
             info["conv"] = ("tensor", 2 * self.L * M * n * T / 1e12, "TOP")
             info["entangle"] = ("hbm", M * (n * 4 + self.L * self.plen) / 1e9, "GB")
-            info["prep_g"] = ("hbm", (T * 4 + 128 * self.kpad) / 1e9, "GB")
+            info["prep_g"] = ("hbm", (T * 4 + self.block * self.kpad) / 1e9, "GB")
         else:
             info["conv"] = ("alu", M * n * T / 1e12, "TMAC")
             info["conv_check"] = ("alu", M * n * T / 1e12, "TMAC")
@@ -500,8 +500,8 @@ class C2Conv(Workload):
                   "convolution with a shared 64-tap kernel U[-128,128)")
         ws = self.M * self.n * 8 * 3 / 1e6
         return {"workload": wl, "M": self.M, "n": self.n, "taps": self.T,
-                "conv_algo": ("tc: Toeplitz GEMM on tcgen05, %d int8 digits base 2^%d, Kpad=%d"
-                              % (self.L, self.limb_bits, self.kpad)) if self.algo == "tc" else "direct IMAD",
+                "conv_algo": ("tc: Toeplitz GEMM on tcgen05, %d int8 digits base 2^%d, %d-output blocks, Kpad=%d"
+                              % (self.L, self.limb_bits, self.block, self.kpad)) if self.algo == "tc" else "direct IMAD",
                 "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
                 "l2": (f"working set {ws:.0f} MB" + (" fits L2 (launch-latency bound)" if ws < 100 else " > L2")),
                 "step": "entangle+prep_taps+conv+disentangle/check(r=0)+recover(r=step mod M)"
@@ -538,15 +538,16 @@ class C2Conv(Workload):
             planes = torch.zeros(M * L * self.plen, dtype=torch.int8, device="cuda")
             pv = planes.view(M, L, self.plen)
             s0 = self.T - 1
-            idx = (torch.arange(self.plen, device="cuda") - s0) % self.n
+            idx = (torch.arange(self.plen, device="cuda") - s0) % self.n  # same extended layout
             for m in range(M):
                 pv[m, 0].copy_(self.c[m][idx].to(torch.int8))
-            ne.ne_op_conv_limbs(self.cfg, planes, L, self.Gt, self.n, self.T, 0, self.delta, self.limb_bits)
+            ne.ne_op_conv_limbs(self.cfg, planes, L, self.Gt, self.n, self.T, 0, self.delta, self.limb_bits, self.block)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(reps):
-                ne.ne_op_conv_limbs(self.cfg, planes, L, self.Gt, self.n, self.T, 0, self.delta, self.limb_bits)
+                ne.ne_op_conv_limbs(self.cfg, planes, L, self.Gt, self.n, self.T, 0, self.delta, self.limb_bits,
+                                    self.block)
             e1.record()
             torch.cuda.synchronize()
             out[tag] = e0.elapsed_time(e1) / reps
@@ -1172,7 +1173,8 @@ def run_reference(args):
         W.algo, W.paper, W.name = args.conv or ("tc" if paper else "direct"), paper, "C2P" if paper else "C2"
         W.fuse = W.algo == "direct" and bool(args.fuse if args.fuse is not None else 1)
         W.L, W.limb_bits = 2, {3: 22, 4: 16, 8: 8}.get(W.M, 8)
-        W.kpad = (W.T + 127 + 127) // 128 * 128
+        W.block = 256 if W.T >= 256 else 128
+        W.kpad = (W.T + W.block - 1 + 127) // 128 * 128
 
         class _Cfg:
             l, k = {3: (22, 20), 4: (16, 16), 8: (8, 8)}.get(W.M, (8, 8))

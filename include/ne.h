@@ -217,30 +217,34 @@ ne_status ne_op_conv(const ne_config* cfg, ne_cstreams x, int64_t n_total, const
 
 /* Tensor-core circular convolution / correlation (NEXT-2; same definition as
  * ne_op_conv): the op as a Toeplitz GEMM on tcgen05.  Output
- * block b (outputs 128b .. 128b+127) = W_b G^T with W_b[k] = x[(128b + k - s0)
- * mod N] (s0 = taps-1 for conv, 0 for correlation) and the 128 x Kpad int8 tap
- * matrix G[i][k] = g[i + s0 - k] (conv) / g[k - i] (corr), Kpad =
- * roundup(taps + 127, 128).  x is held as L int8 digit planes (base 2^limb_bits,
- * as ne_entangle_limbs), each circularly extended to plane_len bytes so that
- * W_b is contiguous:  planes[(m*L + d)*plane_len + t] = digit d of
- * eps_m[(t - s0) mod N].
- *   ne_conv_geometry      -> Kpad and plane_len for (n_total, taps).
+ * block b (outputs W b .. W b + W-1, W = `block` in {128, 256}) = W_b G^T with
+ * W_b[k] = x[(W b + k - s0) mod N] (s0 = taps-1 for conv, 0 for correlation)
+ * and the W x Kpad int8 tap matrix G[i][k] = g[i + s0 - k] (conv) / g[k - i]
+ * (corr), Kpad = roundup(taps + W - 1, 128).  x is held as L int8 digit
+ * planes (base 2^limb_bits, as ne_entangle_limbs), each circularly extended to
+ * plane_len bytes so that W_b is contiguous:
+ *     planes[(m*L + d)*plane_len + t] = digit d of eps_m[(t - s0) mod N].
+ *   ne_conv_geometry      -> the block width for (taps, L) (256 when taps >= 256
+ *                            and L <= 2, else 128), Kpad and plane_len; pass the
+ *                            same block to the three calls below.
  *   ne_entangle_limbs_conv : c (M int32 streams) -> entangled extended digit
  *                            planes (Eq. 15), range assertion as ne_entangle_limbs
  *                            (each position counted once, first_bad = m*N + n).
  *   ne_conv_prep_taps     : g (taps int32, each in [-128, 127], else a range
- *                            violation naming the tap) -> Gt [128][Kpad] int8.
+ *                            violation naming the tap) -> Gt [block][Kpad] int8.
  *   ne_op_conv_limbs      : out_m[n], n < n_total, int64 (wraps mod 2^64).
- * M <= 8, Kpad <= 131072 (exact int32 digit sums), else NE_ENOTSUP.  planes,
- * Gt, out: 16-B aligned device buffers owned by the caller. */
-ne_status ne_conv_geometry(int64_t n_total, int32_t taps, int64_t* kpad, int64_t* plane_len);
+ * M <= 8, Kpad <= 131072 (exact int32 digit sums), block 256 needs L <= 2,
+ * else NE_ENOTSUP.  planes, Gt, out: 16-B aligned device buffers owned by the
+ * caller. */
+ne_status ne_conv_geometry(int64_t n_total, int32_t taps, int32_t L, int32_t* block, int64_t* kpad,
+                           int64_t* plane_len);
 ne_status ne_entangle_limbs_conv(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t taps,
-                                 int32_t correlate, int32_t L, int32_t limb_bits, int8_t* planes,
-                                 ne_diag* diag, ne_stream_t stream);
-ne_status ne_conv_prep_taps(const int32_t* g, int32_t taps, int32_t correlate, int8_t* Gt, ne_diag* diag,
-                            ne_stream_t stream);
+                                 int32_t correlate, int32_t L, int32_t limb_bits, int32_t block,
+                                 int8_t* planes, ne_diag* diag, ne_stream_t stream);
+ne_status ne_conv_prep_taps(const int32_t* g, int32_t taps, int32_t correlate, int32_t block, int8_t* Gt,
+                            ne_diag* diag, ne_stream_t stream);
 ne_status ne_op_conv_limbs(const ne_config* cfg, const int8_t* planes, int32_t L, int32_t limb_bits,
-                           const int8_t* Gt, int64_t n_total, int32_t taps, int32_t correlate,
+                           int32_t block, const int8_t* Gt, int64_t n_total, int32_t taps, int32_t correlate,
                            ne_streams out, ne_stream_t stream);
 
 /* Permutation (bijection I -> G, reading R11), gather:

@@ -100,10 +100,10 @@ _SIGS = {
     "ne_disentangle_check_w32": [_PCFG, Streams, _I64, _I32, Streams, _VP, _VP, _VP],
     "ne_recover_w32": [_PCFG, Streams, _I64, _I32, Streams, _VP],
     "ne_inject_sweep_w32": [_PCFG, Streams, _I64, _I32, _VP, _VP, _VP],
-    "ne_conv_geometry": [_I64, _I32, C.POINTER(_I64), C.POINTER(_I64)],
-    "ne_entangle_limbs_conv": [_PCFG, Streams, _I64, _I32, _I32, _I32, _I32, _VP, _VP, _VP],
-    "ne_conv_prep_taps": [_VP, _I32, _I32, _VP, _VP, _VP],
-    "ne_op_conv_limbs": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I32, _I32, Streams, _VP],
+    "ne_conv_geometry": [_I64, _I32, _I32, C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I64)],
+    "ne_entangle_limbs_conv": [_PCFG, Streams, _I64, _I32, _I32, _I32, _I32, _I32, _VP, _VP, _VP],
+    "ne_conv_prep_taps": [_VP, _I32, _I32, _I32, _VP, _VP, _VP],
+    "ne_op_conv_limbs": [_PCFG, _VP, _I32, _I32, _I32, _VP, _I64, _I32, _I32, Streams, _VP],
     "ne_gemm_check_workspace": [_I64, _I64, C.POINTER(_SZ)],
     "ne_op_gemm_limbs_check": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _I32, Streams, _VP, _VP, _VP,
                                _VP],
@@ -377,28 +377,28 @@ def ne_inject_sweep_w32(cfg: Config, delta, window: int, r: int, flagwords: torc
           _ptr(dhat, torch.int32), _stream())
 
 
-def ne_conv_geometry(n: int, taps: int) -> tuple[int, int]:
-    """(Kpad, plane_len) of the tensor-core convolution."""
-    kp, pl = _I64(), _I64()
-    _call("ne_conv_geometry", n, taps, C.byref(kp), C.byref(pl))
-    return kp.value, pl.value
+def ne_conv_geometry(n: int, taps: int, L: int = 2) -> tuple[int, int, int]:
+    """(block, Kpad, plane_len) of the tensor-core convolution."""
+    bl, kp, pl = _I32(), _I64(), _I64()
+    _call("ne_conv_geometry", n, taps, L, C.byref(bl), C.byref(kp), C.byref(pl))
+    return bl.value, kp.value, pl.value
 
 
 def ne_entangle_limbs_conv(cfg: Config, c, taps: int, correlate: int, L: int, planes: torch.Tensor, diag=None,
-                           limb_bits: int = 8) -> None:
+                           limb_bits: int = 8, block: int = 128) -> None:
     _call("ne_entangle_limbs_conv", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), taps, correlate, L,
-          limb_bits, _ptr(planes, torch.int8), _ptr(diag, torch.int64), _stream())
+          limb_bits, block, _ptr(planes, torch.int8), _ptr(diag, torch.int64), _stream())
 
 
-def ne_conv_prep_taps(g: torch.Tensor, correlate: int, Gt: torch.Tensor, diag=None) -> None:
-    _call("ne_conv_prep_taps", _ptr(g, torch.int32), g.numel(), correlate, _ptr(Gt, torch.int8),
+def ne_conv_prep_taps(g: torch.Tensor, correlate: int, Gt: torch.Tensor, diag=None, block: int = 128) -> None:
+    _call("ne_conv_prep_taps", _ptr(g, torch.int32), g.numel(), correlate, block, _ptr(Gt, torch.int8),
           _ptr(diag, torch.int64), _stream())
 
 
 def ne_op_conv_limbs(cfg: Config, planes: torch.Tensor, L: int, Gt: torch.Tensor, n: int, taps: int, correlate: int,
-                     out, limb_bits: int = 8) -> None:
-    _call("ne_op_conv_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, limb_bits, _ptr(Gt, torch.int8), n, taps,
-          correlate, _streams(out, torch.int64), _stream())
+                     out, limb_bits: int = 8, block: int = 128) -> None:
+    _call("ne_op_conv_limbs", C.byref(cfg), _ptr(planes, torch.int8), L, limb_bits, block, _ptr(Gt, torch.int8), n,
+          taps, correlate, _streams(out, torch.int64), _stream())
 
 
 def ne_gemm_check_workspace(rows: int, cols: int) -> int:

@@ -3,20 +3,21 @@
 // (reading R12)
 //     out_m[n] = sum_{j<T} g[j] eps_m[(n - j) mod N]        (conv)
 //     out_m[n] = sum_{j<T} g[j] eps_m[(n + j) mod N]        (correlation)
-// written as a Toeplitz GEMM.  Output block b = outputs 128 b .. 128 b + 127:
-//     out_m[128 b + i] = sum_{k<Kpad} W_b[k] G[i][k],
-//     W_b[k] = eps_m[(128 b + k - s0) mod N],   s0 = T - 1 (conv) or 0 (corr),
+// written as a Toeplitz GEMM.  Output block b = outputs W b .. W b + W-1
+// (W = 128, or 256 for long kernels with <= 2 digit planes: conv_block):
+//     out_m[W b + i] = sum_{k<Kpad} W_b[k] G[i][k],
+//     W_b[k] = eps_m[(W b + k - s0) mod N],   s0 = T - 1 (conv) or 0 (corr),
 //     G[i][k] = g[i + s0 - k] (conv) or g[k - i] (corr), 0 outside [0, T),
-// with Kpad = roundup(T + 127, 128) (whole 128-byte K stages).  eps_m is held as L int8 digit planes
+// with Kpad = roundup(T + W - 1, 128).  eps_m is held as L int8 digit planes
 // (the GEMM's digit plan), circularly extended so that window
-// row b is the contiguous bytes [128 b, 128 b + Kpad) of each plane:
+// row b is the contiguous bytes [W b, W b + Kpad) of each plane:
 //     plane_{m,d}[t] = digit d of eps_m[(t - s0) mod N],  0 <= t < plane_len.
-// The GEMM is k_gemm_tc in Toeplitz mode (rows = blocks, cols = 128, K = Kpad,
+// The GEMM is k_gemm_tc in Toeplitz mode (rows = blocks, cols = W, K = Kpad,
 // B = G); every D_{m,d} G product is exact in int32 (Kpad * 2^14 < 2^31) and
-// recombined in int64.  The last N mod 128 outputs (a partial block) are
+// recombined in int64.  The last N mod W outputs (a partial block) are
 // computed by k_conv_tail from the same planes.  Redundancy: Kpad / T MACs
-// per useful MAC (4x at T = 64, 1.05x at T = 4500), paid on a pipe ~100x
-// faster than the IMAD path of k_conv.cu.
+// per useful MAC (4x at T = 64, 1.08x at T = 4500 with W = 256), paid on a
+// pipe ~100x faster than the IMAD path of k_conv.cu.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -25,13 +26,17 @@
 
 namespace ne {
 
-ne_status launch_conv_tc(int M, int L, int b, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
+ne_status launch_conv_tc(int M, int L, int b, int W, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
                          int64_t Kpad, int64_t nblocks, const ne_streams& C, cudaStream_t s);
 
-static int64_t conv_kpad(int64_t taps) { return (taps + 127 + 127) / 128 * 128; }
-static int64_t conv_plane_len(int64_t n, int64_t taps) {
-  const int64_t nb_all = (n + 127) / 128;
-  return (128 * nb_all + conv_kpad(taps) + 127) / 128 * 128;
+// output block width W (= GEMM columns): 256 when the taps are long enough
+// that the extra W - 1 window bytes cost little (T >= 256) and TMEM holds the
+// L limb accumulators of a 256-wide tile (L <= 2); 128 otherwise
+static int conv_block(int64_t taps, int L) { return (taps >= 256 && L <= 2) ? 256 : 128; }
+static int64_t conv_kpad(int64_t taps, int W) { return (taps + W - 1 + 127) / 128 * 128; }
+static int64_t conv_plane_len(int64_t n, int64_t taps, int W) {
+  const int64_t nb_all = (n + W - 1) / W;
+  return (W * nb_all + conv_kpad(taps, W) + W - 1) / W * W;
 }
 
 // a1 into circularly extended digit planes: 4 consecutive t per thread, all M
@@ -101,7 +106,7 @@ k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l,
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
-// G (128 x Kpad int8, K contiguous): conv G[i][k] = g[i + T - 1 - k],
+// G (W x Kpad int8, K contiguous): conv G[i][k] = g[i + T - 1 - k],
 // correlation G[i][k] = g[k - i]; taps outside [-128, 127] are range
 // violations (counted once per tap, first_bad = tap index).
 __global__ void __launch_bounds__(kThreads)
@@ -131,19 +136,19 @@ k_conv_prep_taps(const int32_t* __restrict__ g, int64_t T, int correlate, int64_
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
-// the last n - 128 nb outputs of every stream (a partial block): one CTA of
+// the last n - W nb outputs of every stream (a partial block): one CTA of
 // 128 threads per output, threads split k, exact int32 digit sums (Kpad 2^14
 // < 2^31) reduced by shuffles and shared memory, recombined in int64
 __global__ void __launch_bounds__(128)
 k_conv_tail(const int8_t* __restrict__ planes, int M, int L, int b, int64_t plane_len, const int8_t* __restrict__ Gt,
-            int64_t Kpad, int64_t nb, int64_t n, const __grid_constant__ ne_streams out) {
+            int64_t Kpad, int64_t nb, int W, int64_t n, const __grid_constant__ ne_streams out) {
   __shared__ int32_t part[4][4];
-  const int64_t tail = n - 128 * nb;
+  const int64_t tail = n - (int64_t)W * nb;
   const int m = (int)(blockIdx.x / tail);
   const int64_t i = blockIdx.x % tail;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   for (int d = 0; d < L; ++d) {
-    const int8_t* w = planes + ((int64_t)m * L + d) * plane_len + 128 * nb;
+    const int8_t* w = planes + ((int64_t)m * L + d) * plane_len + (int64_t)W * nb;
     int32_t s = 0;
     for (int64_t k = threadIdx.x; k < Kpad; k += 128) s += (int32_t)w[k] * (int32_t)Gt[i * Kpad + k];
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -154,7 +159,7 @@ k_conv_tail(const int8_t* __restrict__ planes, int M, int L, int b, int64_t plan
     uint64_t acc = 0;
     for (int d = 0; d < L; ++d)
       acc += (uint64_t)(int64_t)(part[d][0] + part[d][1] + part[d][2] + part[d][3]) << (b * d);
-    out.s[m][128 * nb + i] = (int64_t)acc;
+    out.s[m][(int64_t)W * nb + i] = (int64_t)acc;
   }
 }
 
@@ -162,24 +167,26 @@ k_conv_tail(const int8_t* __restrict__ planes, int M, int L, int b, int64_t plan
 
 using namespace ne;
 
-extern "C" ne_status ne_conv_geometry(int64_t n_total, int32_t taps, int64_t* kpad, int64_t* plane_len) {
-  if (n_total < 1 || taps < 1 || !kpad || !plane_len) return NE_EINVAL;
-  *kpad = conv_kpad(taps);
-  *plane_len = conv_plane_len(n_total, taps);
+extern "C" ne_status ne_conv_geometry(int64_t n_total, int32_t taps, int32_t L, int32_t* block, int64_t* kpad,
+                                      int64_t* plane_len) {
+  if (n_total < 1 || taps < 1 || L < 1 || L > 4 || !block || !kpad || !plane_len) return NE_EINVAL;
+  *block = conv_block(taps, L);
+  *kpad = conv_kpad(taps, *block);
+  *plane_len = conv_plane_len(n_total, taps, *block);
   return NE_OK;
 }
 
 extern "C" ne_status ne_entangle_limbs_conv(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t taps,
-                                            int32_t correlate, int32_t L, int32_t limb_bits, int8_t* planes,
-                                            ne_diag* diag, ne_stream_t stream) {
+                                            int32_t correlate, int32_t L, int32_t limb_bits, int32_t block,
+                                            int8_t* planes, ne_diag* diag, ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);
   if (st != NE_OK) return st;
   if (n_total < 1 || taps < 1 || (correlate != 0 && correlate != 1) || L < 1 || L > 4 || limb_bits < 8 ||
-      limb_bits > 63 || !planes || !aligned16(planes))
+      limb_bits > 63 || (block != 128 && block != 256) || !planes || !aligned16(planes))
     return NE_EINVAL;
   for (int m = 0; m < cfg->M; ++m)
     if (!c.s[m]) return NE_EINVAL;
-  const int64_t plen = conv_plane_len(n_total, taps);
+  const int64_t plen = conv_plane_len(n_total, taps, block);
   const int64_t s0 = correlate ? 0 : (int64_t)taps - 1;
   const int64_t s0m = s0 % n_total;
   const int grid = grid_for(plen / 4, kThreads);
@@ -194,35 +201,38 @@ extern "C" ne_status ne_entangle_limbs_conv(const ne_config* cfg, ne_cstreams32 
   return launch_status();
 }
 
-extern "C" ne_status ne_conv_prep_taps(const int32_t* g, int32_t taps, int32_t correlate, int8_t* Gt, ne_diag* diag,
-                                       ne_stream_t stream) {
-  if (!g || taps < 1 || (correlate != 0 && correlate != 1) || !Gt || !aligned16(Gt)) return NE_EINVAL;
-  const int64_t kp = conv_kpad(taps);
-  const dim3 grid((unsigned)((kp / 4 + kThreads - 1) / kThreads), 128);
+extern "C" ne_status ne_conv_prep_taps(const int32_t* g, int32_t taps, int32_t correlate, int32_t block, int8_t* Gt,
+                                       ne_diag* diag, ne_stream_t stream) {
+  if (!g || taps < 1 || (correlate != 0 && correlate != 1) || (block != 128 && block != 256) || !Gt ||
+      !aligned16(Gt))
+    return NE_EINVAL;
+  const int64_t kp = conv_kpad(taps, block);
+  const dim3 grid((unsigned)((kp / 4 + kThreads - 1) / kThreads), (unsigned)block);
   k_conv_prep_taps<<<grid, kThreads, 0, cs(stream)>>>(g, taps, correlate, kp, Gt, diag);
   return launch_status();
 }
 
 extern "C" ne_status ne_op_conv_limbs(const ne_config* cfg, const int8_t* planes, int32_t L, int32_t limb_bits,
-                                      const int8_t* Gt, int64_t n_total, int32_t taps, int32_t correlate,
-                                      ne_streams out, ne_stream_t stream) {
+                                      int32_t block, const int8_t* Gt, int64_t n_total, int32_t taps,
+                                      int32_t correlate, ne_streams out, ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);
   if (st != NE_OK) return st;
   if (n_total < 1 || taps < 1 || (correlate != 0 && correlate != 1) || L < 1 || L > 4 || limb_bits < 8 ||
-      limb_bits > 63 || !planes || !Gt || !aligned16(planes) || !aligned16(Gt))
+      limb_bits > 63 || (block != 128 && block != 256) || !planes || !Gt || !aligned16(planes) || !aligned16(Gt))
     return NE_EINVAL;
-  const int64_t kp = conv_kpad(taps);
+  if (block == 256 && L > 2) return NE_ENOTSUP;  // 256-wide tiles hold at most 2 limb accumulators in TMEM
+  const int64_t kp = conv_kpad(taps, block);
   if (kp > 131072) return NE_ENOTSUP;  // int32 digit sums stay exact
   for (int m = 0; m < cfg->M; ++m)
     if (!out.s[m] || !aligned16(out.s[m])) return NE_EINVAL;
-  const int64_t plen = conv_plane_len(n_total, taps);
-  const int64_t nb = n_total / 128;
+  const int64_t plen = conv_plane_len(n_total, taps, block);
+  const int64_t nb = n_total / block;
   cudaStream_t s = cs(stream);
-  if (nb > 0 && (st = launch_conv_tc(cfg->M, L, limb_bits, planes, plen / 128, Gt, kp, nb, out, s)) != NE_OK)
+  if (nb > 0 && (st = launch_conv_tc(cfg->M, L, limb_bits, block, planes, plen / block, Gt, kp, nb, out, s)) != NE_OK)
     return st;
-  const int64_t tail = n_total - 128 * nb;
-  if (tail > 0) {
-    k_conv_tail<<<(unsigned)(cfg->M * tail), 128, 0, s>>>(planes, cfg->M, L, limb_bits, plen, Gt, kp, nb, n_total, out);
-  }
+  const int64_t tail = n_total - (int64_t)block * nb;
+  if (tail > 0)
+    k_conv_tail<<<(unsigned)(cfg->M * tail), 128, 0, s>>>(planes, cfg->M, L, limb_bits, plen, Gt, kp, nb, block,
+                                                          n_total, out);
   return launch_status();
 }

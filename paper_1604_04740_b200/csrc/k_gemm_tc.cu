@@ -70,12 +70,13 @@ struct ChkArgs {
 };
 
 // Operand geometry.  GEMM: A is the [M*L*rows][K] stack of limb planes and C_m
-// is [rows][cols].  Toeplitz (circular convolution as a GEMM, k_conv_tc.cu):
-// each limb plane is a circularly extended 1-D stream of a_plane_rows * 128
-// bytes viewed as [a_plane_rows][128]; window row b of K bytes starts at byte
-// 128 b, so the 64-byte K-chunk kb of row b is the chunk (kb & 1) of row
-// b + kb / 2 of that view (no overlapping tensor-map strides needed).  Output
-// rows >= out_rows are clipped by the TMA store (tensor bounds).
+// is [rows][cols].  Toeplitz (circular convolution as a GEMM, k_conv_tc.cu;
+// toeplitz = the output block width W in {128, 256}): each limb plane is a
+// circularly extended 1-D stream of a_plane_rows * W bytes viewed as
+// [a_plane_rows][W]; window row b of K bytes starts at byte W b, so the K-chunk
+// kb (BK bytes) of row b is column (kb BK) mod W of row b + (kb BK) / W of
+// that view (no overlapping tensor-map strides needed).  Output rows >=
+// out_rows are clipped by the TMA store (tensor bounds).
 // mcast_b (clusters of CL > 1): the CL CTAs of a cluster take CL consecutive
 // row tiles of the same column tile and share the B tile instead of the A
 // tile (each loads BN/CL rows of B and multicasts them) — the convolution's
@@ -86,7 +87,7 @@ struct ChkArgs {
 struct Geo {
   int64_t a_plane_rows;
   int64_t out_rows;
-  int toeplitz;
+  int toeplitz;  // 0, or the Toeplitz output block width W in bytes (= outputs)
   int mcast_b;
   int raster_rows;
 };
@@ -292,8 +293,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
           mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           unsigned char* st = smem + s * CF::kStage;
           mbar_expect_tx(&full[s], (uint32_t)CF::kStage);
-          const int32_t kc = geo.toeplitz ? ((kb * BK) & 127) : kb * BK;
-          const int64_t radd = geo.toeplitz ? ((int64_t)kb * BK) >> 7 : 0;
+          const int32_t kc = geo.toeplitz ? (int32_t)(((int64_t)kb * BK) % geo.toeplitz) : kb * BK;
+          const int64_t radd = geo.toeplitz ? ((int64_t)kb * BK) / geo.toeplitz : 0;
           if (mb) {
 #pragma unroll
             for (int i = 0; i < L; ++i) {
@@ -497,7 +498,7 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   if (mcb && rows % (BM * CL) != 0) return NE_ENOTSUP;
   if (!mcb && cols % (BN * CL) != 0) return NE_ENOTSUP;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, planes, geo.toeplitz ? 128 : (uint64_t)K, (uint64_t)M * L * geo.a_plane_rows, SW,
+  if (!make_map(&ma, planes, geo.toeplitz ? (uint64_t)geo.toeplitz : (uint64_t)K, (uint64_t)M * L * geo.a_plane_rows, SW,
                 mcb ? BM : CF::kARows))
     return NE_ECUDA;
   if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, mcb ? BN / CL : BN)) return NE_ECUDA;
@@ -578,18 +579,28 @@ ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t
 }
 
 // Circular convolution / correlation of M entangled streams as a Toeplitz
-// GEMM (k_conv_tc.cu): planes = M*L extended limb planes of plane_rows * 128
-// bytes; Gt = [128][Kpad] int8 tap matrix; C_m = [nblocks][128] int64 (the
-// first 128 * nblocks outputs of stream m).  One 128-output column tile.
-ne_status launch_conv_tc(int M, int L, int b, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
+// GEMM (k_conv_tc.cu): planes = M*L extended limb planes of plane_rows * W
+// bytes; Gt = [W][Kpad] int8 tap matrix; C_m = [nblocks][W] int64 (the first
+// W * nblocks outputs of stream m).  One W-output column tile.
+//   W = 128: clusters of 2 consecutive row tiles multicast the shared tap
+//     tiles of G; 128-byte K stages (128B swizzle): each window row is one
+//     full 128-byte line of the extended plane per stage; double-buffered
+//     TMEM (L * 128 <= 256)
+//   W = 256 (L <= 2): the C3 GEMM configuration (128 x 256 tiles, 64-byte K
+//     stages, 5 stages) — the A windows are reused by 256 columns instead of
+//     128, halving the A stream per MAC
+ne_status launch_conv_tc(int M, int L, int b, int W, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
                          int64_t Kpad, int64_t nblocks, const ne_streams& C, cudaStream_t s) {
-  // clusters of 2 consecutive row tiles multicast the shared tap tiles of G;
-  // 128-byte K stages (128B swizzle): each window row is one full 128-byte
-  // line of the extended plane per stage (half the TMA row requests of 64-byte
-  // stages; measured 0.125 -> 0.108 ms at M = 8, N = 10^6, T = 4500)
-  const tc::Geo geo{plane_rows, nblocks, 1, 1, 0};
+  const tc::Geo geo{plane_rows, nblocks, W, 1, 0};
   const int64_t rows = (nblocks + 255) / 256 * 256;
   if (Kpad % 128 != 0) return NE_EINVAL;
+  if (W == 256) {
+    switch (L) {
+      case 1: return tc::run<1, 256, 6, 64, 2>(planes, Gt, rows, 256, Kpad, M, b, C, s, nullptr, &geo);
+      case 2: return tc::run<2, 256, 5, 64, 2>(planes, Gt, rows, 256, Kpad, M, b, C, s, nullptr, &geo);
+      default: return NE_ENOTSUP;
+    }
+  }
   switch (L) {
     case 1: return tc::run<1, 128, 5, 128, 2>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);
     case 2: return tc::run<2, 128, 3, 128, 2>(planes, Gt, rows, 128, Kpad, M, b, C, s, nullptr, &geo);

@@ -805,10 +805,12 @@ def test_gemm_limbs_check_fused(O, M, plan, bound, rows, cols, K, r):
 
 
 # ------------------------------------------------------------------ tensor-core (Toeplitz) convolution
-@pytest.mark.parametrize("M,N,T,correlate,bound", [
-    (3, 65536, 64, 0, 127), (3, 65536 + 77, 64, 1, 127), (4, 1000, 100, 0, 1000), (8, 5000, 4500, 0, 100),
-    (3, 100, 300, 1, 127), (3, 384, 1, 0, 127), (5, 4096, 64, 1, 100), (3, 20000, 1000, 0, 127)])
-def test_conv_tensor_core(O, M, N, T, correlate, bound):
+@pytest.mark.parametrize("M,N,T,correlate,bound,block", [
+    (3, 65536, 64, 0, 127, None), (3, 65536 + 77, 64, 1, 127, None), (4, 1000, 100, 0, 1000, None),
+    (8, 5000, 4500, 0, 100, None), (3, 100, 300, 1, 127, None), (3, 384, 1, 0, 127, None),
+    (5, 4096, 64, 1, 100, None), (3, 20000, 1000, 0, 127, None), (8, 70000, 700, 1, 100, 128),
+    (3, 70000 + 5, 64, 0, 127, 256), (4, 600, 300, 1, 100, 256)])
+def test_conv_tensor_core(O, M, N, T, correlate, bound, block):
     """ne_op_conv_limbs (tcgen05 Toeplitz GEMM + partial-block tail) equals the
     oracle's circular convolution / correlation of the entangled streams,
     bit for bit; the extended planes hold digit d of eps[(t - s0) mod N]."""
@@ -820,15 +822,20 @@ def test_conv_tensor_core(O, M, N, T, correlate, bound):
     g = O.gen_uniform(11, 3, 0, -128, 128, T)
     g[0] = -128
     eps = O.entangle(ocfg, c)
-    kp, plen = ne.ne_conv_geometry(N, T)
-    assert kp % 128 == 0 and kp >= T + 127 and plen % 128 == 0
+    bw, kp, plen = ne.ne_conv_geometry(N, T, L)
+    if block is not None:
+        bw = block
+        kp = (T + bw - 1 + 127) // 128 * 128
+        plen = (bw * ((N + bw - 1) // bw) + kp + bw - 1) // bw * bw
+    assert bw == (256 if (T >= 256 and L <= 2) else 128) or block is not None
+    assert kp % 128 == 0 and kp >= T + bw - 1 and plen % bw == 0
     planes = torch.empty(M * L * plen, dtype=torch.int8, device="cuda")
-    Gt = torch.empty(128 * kp, dtype=torch.int8, device="cuda")
+    Gt = torch.empty(bw * kp, dtype=torch.int8, device="cuda")
     diag = ne.diag_new()
-    ne.ne_entangle_limbs_conv(cfg, to_streams(c), T, correlate, L, planes, diag, limb_bits=b)
-    ne.ne_conv_prep_taps(dev(g, torch.int32), correlate, Gt, diag)
+    ne.ne_entangle_limbs_conv(cfg, to_streams(c), T, correlate, L, planes, diag, limb_bits=b, block=bw)
+    ne.ne_conv_prep_taps(dev(g, torch.int32), correlate, Gt, diag, block=bw)
     out = empty_streams(M, N)
-    ne.ne_op_conv_limbs(cfg, planes, L, Gt, N, T, correlate, out, limb_bits=b)
+    ne.ne_op_conv_limbs(cfg, planes, L, Gt, N, T, correlate, out, limb_bits=b, block=bw)
     torch.cuda.synchronize()
     assert ne.diag_read(diag)["range_violations"] == 0
     assert (to_np(out) == O.op_conv(ocfg, eps, g, bool(correlate))).all()
@@ -851,10 +858,10 @@ def test_conv_tensor_core_range_violations(O):
     g = O.gen_uniform(12, 3, 0, -100, 100, T)
     g[9] = 128
     g[40] = -300
-    kp, plen = ne.ne_conv_geometry(N, T)
+    bw, kp, plen = ne.ne_conv_geometry(N, T, L)
     planes = torch.empty(M * L * plen, dtype=torch.int8, device="cuda")
     diag = ne.diag_new()
-    ne.ne_entangle_limbs_conv(cfg, to_streams(c), T, 0, L, planes, diag, limb_bits=b)
+    ne.ne_entangle_limbs_conv(cfg, to_streams(c), T, 0, L, planes, diag, limb_bits=b, block=bw)
     d = ne.diag_read(diag)
     # c[2,5] = -129 alone is still exact (d0 = -129 needs 9 bits: flagged), c[1,17] flagged;
     # the neighbour stream's digit d1 = c_{m-1} also leaves int8 for stream m+1
@@ -863,9 +870,9 @@ def test_conv_tensor_core_range_violations(O):
     d1 = (E - d0) >> b
     bad = np.flatnonzero((~((d0 >= -128) & (d0 <= 127) & (d1 >= -128) & (d1 <= 127))).reshape(-1))
     assert d["range_violations"] == len(bad) and d["first_bad"] == bad.min()
-    Gt = torch.empty(128 * kp, dtype=torch.int8, device="cuda")
+    Gt = torch.empty(bw * kp, dtype=torch.int8, device="cuda")
     diag2 = ne.diag_new()
-    ne.ne_conv_prep_taps(dev(g, torch.int32), 0, Gt, diag2)
+    ne.ne_conv_prep_taps(dev(g, torch.int32), 0, Gt, diag2, block=bw)
     d2 = ne.diag_read(diag2)
     assert d2["range_violations"] == 2 and d2["first_bad"] == 9
 
