@@ -1248,12 +1248,20 @@ def main():
             print(json.dumps(run_reference(args)), flush=True)
         return
 
+    if os.environ.get("NE_BENCH_SHARE_GPU") == "1":
+        # test hook only: exercise the N > 1 code path (barriers, max-over-ranks
+        # timing, rank-0 printing) with every rank on cuda:0 over gloo; the
+        # numbers of such a run are not measurements
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("NE_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_c5(args, rank, world, local_rank) if args.workload == "c5" else run_ours(args, rank, world, local_rank)
     if line is not None:
         print(json.dumps(line), flush=True)
