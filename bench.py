@@ -60,6 +60,103 @@ class Workload:
     def stages(self, i):  # -> list of (stage_name, callable)
         raise NotImplementedError
 
+    # ---- end to end (pinned host inputs -> device -> result -> pinned host),
+    # pipelined across steps: step i's H2D, compute and D2H run on three CUDA
+    # streams over two device buffer slots, so the copies of one step overlap
+    # the compute of another and H2D overlaps D2H (PCIe is full duplex).
+    # Every step still moves all of its inputs and results.
+    E2E_IN: tuple = ()
+    E2E_OUT: tuple = ()
+    def e2e_bytes(self):
+        def flat(v):
+            return list(v) if isinstance(v, (list, tuple)) else [v]
+        return sum(t.numel() * t.element_size() for n in self.E2E_IN + self.E2E_OUT for t in flat(getattr(self, n)))
+
+    @property
+    def E2E_PIPELINE(self):  # pipelining pays once the copies outweigh its per-step enqueue cost
+        return self.e2e_bytes() > (8 << 20)
+
+    def e2e(self, steps):
+        return self.e2e_pipeline(steps) if self.E2E_PIPELINE else self.e2e_serial(steps)
+
+    def e2e_serial(self, steps):
+        """One stream: H2D inputs, the step, D2H results, in order."""
+        torch = self.torch
+
+        def flat(v):
+            return list(v) if isinstance(v, (list, tuple)) else [v]
+
+        dev_in = [t for n in self.E2E_IN for t in flat(getattr(self, n))]
+        dev_out = [t for n in self.E2E_OUT for t in flat(getattr(self, n))]
+        h_in = [t.cpu().pin_memory() for t in dev_in]
+        h_out = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in dev_out]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0.record()
+        for i in range(steps):
+            for d, h in zip(dev_in, h_in):
+                d.copy_(h, non_blocking=True)
+            for _, f in self.stages(i):
+                f()
+            for h, d in zip(h_out, dev_out):
+                h.copy_(d, non_blocking=True)
+        t1.record()
+        torch.cuda.synchronize()
+        return (t0.elapsed_time(t1) / steps, sum(h.numel() * h.element_size() for h in h_in),
+                sum(h.numel() * h.element_size() for h in h_out))
+
+    def e2e_pipeline(self, steps, nslots=2):
+        torch = self.torch
+
+        def flat(v):
+            return list(v) if isinstance(v, (list, tuple)) else [v]
+
+        names = self.E2E_IN + self.E2E_OUT
+        orig = {n: getattr(self, n) for n in names}
+        slots = [orig] + [{n: ([t.clone() for t in orig[n]] if isinstance(orig[n], list) else orig[n].clone())
+                           for n in names} for _ in range(nslots - 1)]
+        h_in = {n: [t.cpu().pin_memory() for t in flat(orig[n])] for n in self.E2E_IN}
+        h_out = [{n: [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in flat(orig[n])]
+                  for n in self.E2E_OUT} for _ in range(nslots)]
+        s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        mk = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        ev_in, ev_cmp, ev_out = [mk() for _ in range(steps)], [mk() for _ in range(steps)], [mk() for _ in range(steps)]
+        t0, t1 = mk(), mk()
+        torch.cuda.synchronize()
+        t0.record(s_in)
+        for i in range(steps):
+            k = i % nslots
+            sl = slots[k]
+            with torch.cuda.stream(s_in):
+                if i >= nslots:
+                    s_in.wait_event(ev_cmp[i - nslots])  # compute i-nslots done reading slot k's inputs
+                for n in self.E2E_IN:
+                    for d, h in zip(flat(sl[n]), h_in[n]):
+                        d.copy_(h, non_blocking=True)
+                ev_in[i].record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in[i])
+                if i >= nslots:
+                    s_cmp.wait_event(ev_out[i - nslots])  # D2H i-nslots done reading slot k's results
+                for n in names:
+                    setattr(self, n, sl[n])
+                for _, f in self.stages(i):
+                    f()
+                ev_cmp[i].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp[i])
+                for n in self.E2E_OUT:
+                    for h, d in zip(h_out[k][n], flat(sl[n])):
+                        h.copy_(d, non_blocking=True)
+                ev_out[i].record(s_out)
+        t1.record(s_out)
+        torch.cuda.synchronize()
+        for n in names:
+            setattr(self, n, orig[n])
+        h2d = sum(h.numel() * h.element_size() for n in self.E2E_IN for h in h_in[n])
+        d2h = sum(h.numel() * h.element_size() for n in self.E2E_OUT for h in h_out[0][n])
+        return t0.elapsed_time(t1) / steps, h2d, d2h
+
     def _time(self, fn, reps):
         """ms per call of fn, captured once in a CUDA graph and replayed: the
         same launch path as the timed step, so plain and entangled compare."""
@@ -92,6 +189,8 @@ class C3Gemm(Workload):
 
     name = "C3"
     metric_unit = "Gop/s"
+    E2E_IN = ("A", "B")
+    E2E_OUT = ("dout",)
 
     def __init__(self, rank, n=4096, seed=2, algo="tc", scheme="entangled", limbs="plan", fuse=True):
         import torch
@@ -218,27 +317,6 @@ class C3Gemm(Workload):
                          if self.fuse else
                          "entangle(limbs)+prep_B+GEMM+disentangle/check(r=0)+recover(r=step mod 3)")}
 
-    # ---- end-to-end through host buffers
-    def e2e_setup(self):
-        torch = self.torch
-        self.hA = [a.cpu().pin_memory() for a in self.A]
-        self.hB = self.B.cpu().pin_memory()
-        self.hout = [torch.empty(self.rows * self.cols, dtype=torch.int64).pin_memory() for _ in range(self.M)]
-        self.hdiag = torch.empty(4, dtype=torch.int64).pin_memory()
-        return (sum(a.numel() * 4 for a in self.hA) + self.hB.numel() * 4,
-                sum(o.numel() * 8 for o in self.hout) + 32)
-
-    def e2e_step(self, i):
-        for m in range(self.M):
-            self.A[m].copy_(self.hA[m], non_blocking=True)
-        self.B.copy_(self.hB, non_blocking=True)
-        for _, f in self.stages(i):
-            f()
-        for m in range(self.M):
-            self.hout[m].copy_(self.dout[m], non_blocking=True)
-        self.hdiag.copy_(self.diag, non_blocking=True)
-
-    # ---- plain (unentangled) comparison: the paper's "conventional" routine
     def plain_times(self, reps=5):
         """GEMM on plain A: (i) same tcgen05 kernel with the same L limbs,
         (ii) the narrowest native form (1 int8 limb); ms per call."""
@@ -290,6 +368,8 @@ class C4PermInner(Workload):
 
     name = "C4"
     metric_unit = "GB/s"
+    E2E_IN = ("c",)
+    E2E_OUT = ("dout",)
 
     def __init__(self, rank, n=1 << 28, seed=3, layout="aos"):
         import torch
@@ -360,19 +440,6 @@ class C4PermInner(Workload):
                 "l2": "working set ~13 GB >> 126 MB L2 (no flush needed)",
                 "step": "entangle(AoS)+gather/inner/disentangle/check fused(r=0)+recover(r=step mod 4)"}
 
-    def e2e_setup(self):
-        self.hc = [x.cpu().pin_memory() for x in self.c]
-        self.hout = [self.torch.empty(self.nb, dtype=self.torch.int64).pin_memory() for _ in range(4)]
-        return sum(x.numel() * 4 for x in self.hc), sum(o.numel() * 8 for o in self.hout)
-
-    def e2e_step(self, i):
-        for m in range(4):
-            self.c[m].copy_(self.hc[m], non_blocking=True)
-        for _, f in self.stages(i):
-            f()
-        for m in range(4):
-            self.hout[m].copy_(self.dout[m], non_blocking=True)
-
     def plain_times(self, reps=3):
         """Same gather + inner kernel on plain (unentangled) data in the same
         int64 AoS containers, no check: the paper's conventional routine."""
@@ -419,6 +486,8 @@ class C2Conv(Workload):
 
     name = "C2"
     metric_unit = "Gop/s"
+    E2E_IN = ("c", "g")
+    E2E_OUT = ("dout",)
 
     def __init__(self, rank, n=65536, taps=64, seed=1, M=3, algo="tc", paper=False, fuse=True):
         import torch
@@ -509,22 +578,6 @@ class C2Conv(Workload):
                                            if self.fuse else
                                            "entangle+conv+disentangle/check(r=0)+recover(r=step mod M)")}
 
-    def e2e_setup(self):
-        M = self.M
-        self.hc = [x.cpu().pin_memory() for x in self.c]
-        self.hg = self.g.cpu().pin_memory()
-        self.hout = [self.torch.empty(self.n, dtype=self.torch.int64).pin_memory() for _ in range(M)]
-        return self.n * 4 * M + self.T * 4, self.n * 8 * M
-
-    def e2e_step(self, i):
-        for m in range(self.M):
-            self.c[m].copy_(self.hc[m], non_blocking=True)
-        self.g.copy_(self.hg, non_blocking=True)
-        for _, f in self.stages(i):
-            f()
-        for m in range(self.M):
-            self.hout[m].copy_(self.dout[m], non_blocking=True)
-
     def plain_times(self, reps=20):
         """The same conv kernel on unentangled data: (i) same digit count
         (plain c in digit 0, other digits 0), (ii) one int8 digit; ms per call."""
@@ -589,6 +642,8 @@ class C1Chain(Workload):
 
     name = "C1"
     metric_unit = "Gpositions/s"
+    E2E_IN = ("c", "a")
+    E2E_OUT = ("dout",)
 
     def __init__(self, rank, n=4096, seed=0, w=64, fuse=True):
         import torch
@@ -665,20 +720,6 @@ class C1Chain(Workload):
                 "step": "entangle(c, a: one launch) + scale/add with fused disentangle/check(r=0) + "
                         "recover(r=step mod 3)"
                 if self.fuse else "entangle(c, a) + scale/add + disentangle/check(r=0) + recover(r=step mod 3)"}
-
-    def e2e_setup(self):
-        self.hc = [x.cpu().pin_memory() for x in self.c + self.a]
-        dt = self.torch.int64 if self.w == 64 else self.torch.int32
-        self.hout = [self.torch.empty(self.n, dtype=dt).pin_memory() for _ in range(3)]
-        return self.n * 24, self.n * 3 * self.w // 8
-
-    def e2e_step(self, i):
-        for d, h in zip(self.c + self.a, self.hc):
-            d.copy_(h, non_blocking=True)
-        for _, f in self.stages(i):
-            f()
-        for m in range(3):
-            self.hout[m].copy_(self.dout[m], non_blocking=True)
 
     def plain_times(self, reps=20):
         """The conventional routine on unentangled data (the paper's comparison,
@@ -1030,20 +1071,12 @@ def run_ours(args, rank, world, local_rank):
     else:
         rec_ok = all(bool(torch.equal(a, b)) for a, b in zip(W.drec, W.dout))
 
-    # end-to-end through host buffers (pinned H2D inputs, D2H outputs, same stream)
-    h2d, d2h = W.e2e_setup()
-    torch.cuda.synchronize()
-    W.e2e_step(0)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(3, min(args.steps, 20))
+    # end to end through host buffers: pinned H2D inputs, D2H results, every
+    # step, pipelined over three CUDA streams (Workload.e2e_pipeline)
+    e2e_steps = max(4, min(args.steps, 20))
+    W.e2e(2)
     barrier()
-    e0.record()
-    for i in range(e2e_steps):
-        W.e2e_step(i)
-    e1.record()
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    e2e_ms, h2d, d2h = W.e2e(e2e_steps)
     if world > 1:
         t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -1092,7 +1125,9 @@ def run_ours(args, rank, world, local_rank):
         "launch": "CUDA graph replay (one graph per recovered stream r)" if args.graph else "eager",
         "eager_ms_per_step": round(eager_ms, 4),
         "e2e": {"value": round(W.work_per_step() * world / (e2e_ms / 1e3), 3), "unit": W.metric_unit,
-                "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "pipelined": "H2D / compute / D2H on three streams, two buffer slots" if W.E2E_PIPELINE
+                else "no (one stream; the step is smaller than the enqueue cost of a pipeline)"},
         "gpu_launches": W.launches_per_step * args.steps,
         "clocks": clk.summary(),
         "correctness": {"range_violations": dg["range_violations"], "flagged_positions": dg["fault_positions"],
