@@ -116,3 +116,35 @@ def test_gemm_limb_plan():
     assert ne.ne_gemm_limb_plan(ne.ne_config_for(3), 128) == (4, 8)
     assert ne.ne_gemm_limb_plan(ne.ne_config_for(8), 32) == (2, 8)
     assert ne.ne_gemm_limb_plan(ne.ne_config_for(4), 1000) == (4, 8)
+
+
+def test_argument_validation_of_the_newer_entry_points(L):
+    """Errors are returned before any device work (fake, 16-B aligned device
+    addresses are never dereferenced): stream-set counts, conv block widths,
+    excluded-stream indices, aliasing, geometry arguments."""
+    cfg = ne.ne_config_for(3)
+    st = ne.Streams()
+    fake = [0x10000 * (i + 1) for i in range(8)]
+    for i in range(6):
+        st.s[i] = fake[i]
+    assert L.ne_entangle_sets(ctypes.byref(cfg), st, 11, 16, st, None, None) == 1    # 11 * 3 > 32 streams
+    assert L.ne_entangle_sets(ctypes.byref(cfg), st, 0, 16, st, None, None) == 1
+    bl, kp, pl = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+    assert L.ne_conv_geometry(1000, 4500, 2, ctypes.byref(bl), ctypes.byref(kp), ctypes.byref(pl)) == 0
+    assert bl.value == 256 and kp.value % 128 == 0 and kp.value >= 4500 + 255 and pl.value % 256 == 0
+    assert L.ne_conv_geometry(1000, 4500, 3, ctypes.byref(bl), ctypes.byref(kp), ctypes.byref(pl)) == 0
+    assert bl.value == 128                                                               # 3 limbs: 128-wide
+    assert L.ne_conv_geometry(0, 64, 2, ctypes.byref(bl), ctypes.byref(kp), ctypes.byref(pl)) == 1
+    assert L.ne_conv_prep_taps(ctypes.c_void_p(fake[0]), 64, 0, 192, ctypes.c_void_p(fake[1]), None, None) == 1
+    assert L.ne_op_conv_limbs(ctypes.byref(cfg), ctypes.c_void_p(fake[0]), 3, 8, 256, ctypes.c_void_p(fake[1]),
+                              1000, 300, 0, st, None) == 7                              # NE_ENOTSUP: L = 3 at W = 256
+    assert L.ne_op_scale_add_check(ctypes.byref(cfg), st, 16, 37, None, st, 1, 3, st, None, None, None) == 4
+    assert L.ne_op_conv_check(ctypes.byref(cfg), st, 16, ctypes.c_void_p(fake[7]), 4, 0, st, 0, st, None, None,
+                              None) == 1                                                # out aliases x
+    assert L.ne_op_gemm_limbs_check(ctypes.byref(cfg), ctypes.c_void_p(fake[0]), 2, 22, ctypes.c_void_p(fake[1]),
+                                    128, 128, 128, st, 5, st, None, None, ctypes.c_void_p(fake[2]), None) == 4
+    b = ctypes.c_size_t()
+    assert L.ne_gemm_check_workspace(256, 512, ctypes.byref(b)) == 0 and b.value >= 2 * 4 * 4
+    c32 = ne.ne_config_for(3, 32)
+    assert L.ne_op_scale_add_check_w32(ctypes.byref(c32), st, 16, 37, None, st, 1, 3, st, None, None, None) == 4
+    assert L.ne_entangle_sets_w32(ctypes.byref(cfg), st, 2, 16, st, None, None) == 2      # w = 64 config
