@@ -86,6 +86,75 @@ k_disentangle(const __grid_constant__ ne_cstreams e, int M_rt, int l, int64_t n,
   if (CHECK && diag) diag_add(&diag->fault_positions, &diag->first_fault, nflag, first);
 }
 
+// Four consecutive positions per thread for M = 3 (the C1 / C3 configs): one
+// 256-bit load and store per stream (32-B aligned streams, n % 4 == 0), the
+// 64-bit M = 3 disentangle of ne_internal.cuh; a warp owns 128 positions =
+// four bitmap words assembled from four ballots.
+__device__ __forceinline__ uint32_t word_of4b(const uint32_t (&bal)[4], int j) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t byte = (bal[u] >> (8 * j)) & 0xffu;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w |= ((byte >> k) & 1u) << (4 * k + u);
+  }
+  return w;
+}
+
+template <bool CHECK>
+__global__ void __launch_bounds__(kThreads)
+k_disentangle3x4(const __grid_constant__ ne_cstreams e, int l, int64_t n, const __grid_constant__ ne_streams d_out,
+                 uint32_t* __restrict__ bitmap, ne_diag* __restrict__ diag) {
+  const int64_t nq = n / 4;
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  int nflag = 0;
+  long long first = LLONG_MAX;
+  const int64_t nq_w = (nq + 31) & ~(int64_t)31;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nq_w; v += stride) {
+    const int64_t n0 = 4 * v;
+    bool f[4] = {false, false, false, false};
+    if (v < nq) {
+      int64_t q[4][3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        if (j == 0 && !CHECK) {
+          q[0][0] = q[1][0] = q[2][0] = q[3][0] = 0;
+          continue;
+        }
+        uint64_t u0, u1, u2, u3;
+        asm volatile("ld.global.cs.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(u0), "=l"(u1), "=l"(u2), "=l"(u3)
+                     : "l"(e.s[j] + n0));
+        q[0][j] = (int64_t)u0; q[1][j] = (int64_t)u1; q[2][j] = (int64_t)u2; q[3][j] = (int64_t)u3;
+      }
+      int64_t d[4][3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) f[u] = disentangle_rot<3>(q[u], 3, l, d[u], CHECK);
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        asm volatile("st.global.cs.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(d_out.s[j] + n0), "l"(d[0][j]), "l"(d[1][j]),
+                     "l"(d[2][j]), "l"(d[3][j])
+                     : "memory");
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (f[u]) {
+          ++nflag;
+          first = (n0 + u) < first ? (n0 + u) : first;
+        }
+    }
+    if (CHECK && bitmap) {
+      uint32_t bal[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bal[u] = __ballot_sync(0xffffffffu, f[u]);
+      const int64_t w0 = (v - lane) / 8;
+      if (lane < 4 && w0 + lane < nwords) bitmap[w0 + lane] = word_of4b(bal, lane);
+    }
+  }
+  if (CHECK && diag) diag_add(&diag->fault_positions, &diag->first_fault, nflag, first);
+}
+
 // a7: exhaustive single-bit sweep.  One warp per trial; lane t owns positions
 // 2t, 2t+1 of the window; the flag word is assembled like the bitmap.
 template <int MT>
@@ -150,9 +219,20 @@ static bool streams_ok(const S& c, int M, int skip = -1) {
   return true;
 }
 
+template <typename S>
+static bool aligned32_all(const S& c, int M, int skip = -1) {
+  for (int m = 0; m < M; ++m)
+    if (m != skip && (reinterpret_cast<uintptr_t>(c.s[m]) & 31u)) return false;
+  return true;
+}
+
 template <bool CHECK>
 static void launch_disentangle(const ne_config* cfg, const ne_cstreams& er, int64_t n,
                                const ne_streams& dr, uint32_t* bitmap, ne_diag* diag, cudaStream_t s) {
+  if (cfg->M == 3 && n % 4 == 0 && aligned32_all(er, 3, CHECK ? -1 : 0) && aligned32_all(dr, 3)) {
+    k_disentangle3x4<CHECK><<<grid_for(n / 4, kThreads), kThreads, 0, s>>>(er, cfg->l, n, dr, bitmap, diag);
+    return;
+  }
   const int grid = grid_for((n + 1) / 2, kThreads);
   switch (cfg->M) {
     case 3: k_disentangle<3, CHECK><<<grid, kThreads, 0, s>>>(er, 3, cfg->l, n, dr, bitmap, diag); break;
