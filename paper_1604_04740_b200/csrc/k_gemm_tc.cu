@@ -42,7 +42,10 @@ struct Cfg {
   static constexpr int kTmemNeed = kBufs * kAccCols;
   static constexpr int kTmemCols = (kTmemNeed <= 32) ? 32 : (kTmemNeed <= 64) ? 64 : (kTmemNeed <= 128) ? 128 : (kTmemNeed <= 256) ? 256 : 512;
   static constexpr int kStageOut = 32 * 16 * 8;  // one epilogue warp's [32 rows x 16 int64] box
-  static constexpr size_t kSmem = (size_t)STAGES * kStage + 2 * 8 * kStageOut + 1024 /*align*/ + 512 /*barriers, check queue*/;
+  // staging boxes per epilogue warp: 2 (double-buffered TMA stores) unless the
+  // operand stages leave room for only 1 in the 227 KB of shared memory
+  static constexpr int kOutBufs = (size_t)STAGES * kStage + 2 * 8 * kStageOut + 1536 <= 232448 ? 2 : 1;
+  static constexpr size_t kSmem = (size_t)STAGES * kStage + kOutBufs * 8 * kStageOut + 1024 /*align*/ + 512 /*barriers, check queue*/;
 };
 
 
@@ -227,7 +230,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   unsigned char* stage_out = smem + STAGES * CF::kStage;  // 2 x 8 x 4 KB, 1024-B aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + 2 * 8 * CF::kStageOut);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + CF::kOutBufs * 8 * CF::kStageOut);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;  // [kBufs]
   uint64_t* tmem_empty = tmem_full + 2;  // [kBufs]
@@ -355,7 +358,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
     const int q = warp & 3;          // TMEM lane quarter this warp may access (warp id mod 4)
     const int half = ew >> 2;        // column half
     const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16);
-    unsigned char* my_out = stage_out + ew * 2 * CF::kStageOut;
+    unsigned char* my_out = stage_out + ew * CF::kOutBufs * CF::kStageOut;
     uint32_t tile = 0, buf = 0;
     for (int64_t w = cid; w < n_work; w += ncl, ++tile) {
       int m;
@@ -367,7 +370,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       mbar_wait(&tmem_full[ab], use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16, buf ^= 1) {
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16, buf = (buf + 1) % CF::kOutBufs) {
         uint32_t v[L][16];
 #pragma unroll
         for (int i = 0; i < L; ++i) tmem_ld16(tl + ab * CF::kAccCols + i * BN + c, v[i]);
@@ -380,7 +383,12 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[ab])) : "memory");
         }
         // the TMA store that last read this buffer (two chunks ago) must be done
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (lane == 0) {
+          if (CF::kOutBufs == 2)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncwarp();
         unsigned char* box = my_out + buf * CF::kStageOut;
         // row `lane` of the box, 16-byte chunk k stored at chunk k ^ (row & 7) (128B swizzle)
@@ -558,6 +566,13 @@ static ne_status gemm_tc_dispatch(int M, int L, int b, const int8_t* planes, con
       if (cols % 256 == 0) return tc::run<1, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
       return tc::run<1, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
     case 2:
+      // 128-byte K stages (128B swizzle, 3 stages, single-buffered store
+      // staging): half the TMA row requests and barrier round trips per MAC
+      // of the 64-byte / 5-stage form (C3 GEMM 0.2897 -> 0.2862 ms)
+      // (long work lists only: with few waves the shallower pipeline's ramp
+      // shows — the ABFT checksum GEMM, 3.5 waves, measured 5 % slower)
+      if (CHK == 0 && pair256 && K % 128 == 0 && (int64_t)M * (rows / 128) * (cols / 512) >= 6 * (num_sms() / 2))
+        return tc::run<2, 256, 3, 128, 2>(planes, Bt, rows, cols, K, M, b, C, s, chk);
       if (pair256) return tc::run<2, 256, 5, 64, 2, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk);
       if (cols % 256 == 0) return tc::run<2, 256, 5, 64, 1, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk);
       return tc::run<2, 128, 6, 64, 1, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk);
