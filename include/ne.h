@@ -233,7 +233,7 @@ ne_status ne_op_conv(const ne_config* cfg, ne_cstreams x, int64_t n_total, const
  *   ne_conv_prep_taps     : g (taps int32, each in [-128, 127], else a range
  *                            violation naming the tap) -> Gt [block][Kpad] int8.
  *   ne_op_conv_limbs      : out_m[n], n < n_total, int64 (wraps mod 2^64).
- * M <= 8, Kpad <= 131072 (exact int32 digit sums), block 256 needs L <= 2,
+ * M <= 8, Kpad < 131072 (exact int32 digit sums), block 256 needs L <= 2,
  * else NE_ENOTSUP.  planes, Gt, out: 16-B aligned device buffers owned by the
  * caller. */
 ne_status ne_conv_geometry(int64_t n_total, int32_t taps, int32_t L, int32_t* block, int64_t* kpad,
@@ -270,7 +270,8 @@ ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int6
 /* The tensor-core GEMM on operands already in limb form: planes from
  * ne_entangle_limbs (M*L planes of rows x K int8, K contiguous) and Bt from
  * ne_gemm_prep_b (cols x K int8, K contiguous).  rows % 128 == 0,
- * cols % 128 == 0, K % 128 == 0, K <= 131072 (int32 limb sums stay exact). */
+ * cols % 128 == 0, K % 128 == 0, K < 131072 (int32 limb sums stay exact: |sum| <=
+ * K * 128 * 128 must stay below 2^31, so K = 131072 itself is refused). */
 ne_status ne_gemm_prep_b(const int32_t* B, int64_t K, int64_t cols, int8_t* Bt, ne_diag* diag,
                          ne_stream_t stream);
 ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes, int32_t L, int32_t limb_bits,

@@ -222,7 +222,7 @@ extern "C" ne_status ne_op_conv_limbs(const ne_config* cfg, const int8_t* planes
     return NE_EINVAL;
   if (block == 256 && L > 2) return NE_ENOTSUP;  // 256-wide tiles hold at most 2 limb accumulators in TMEM
   const int64_t kp = conv_kpad(taps, block);
-  if (kp > 131072) return NE_ENOTSUP;  // int32 digit sums stay exact
+  if (kp >= 131072) return NE_ENOTSUP;  // int32 digit sums stay exact: Kpad * 128 * 128 < 2^31
   for (int m = 0; m < cfg->M; ++m)
     if (!out.s[m] || !aligned16(out.s[m])) return NE_EINVAL;
   const int64_t plen = conv_plane_len(n_total, taps, block);

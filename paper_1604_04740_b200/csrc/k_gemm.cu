@@ -114,7 +114,7 @@ k_prep_b(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __restr
 using namespace ne;
 
 static bool tc_shape_ok(int64_t rows, int64_t cols, int64_t K) {
-  return rows > 0 && cols > 0 && K > 0 && rows % 128 == 0 && cols % 128 == 0 && K % 128 == 0 && K <= 131072;
+  return rows > 0 && cols > 0 && K > 0 && rows % 128 == 0 && cols % 128 == 0 && K % 128 == 0 && K < 131072;  // K * 2^14 < 2^31
 }
 
 extern "C" ne_status ne_gemm_workspace(const ne_config* cfg, int64_t rows, int64_t cols, int64_t K, int32_t L,

@@ -7,7 +7,7 @@
 // int8 plane (|B| <= 128), so
 //     C_m = sum_i 2^(8i) (D_{m,i} B),
 // every D_{m,i} B is an int8 x int8 -> int32 tensor-core product that is exact
-// while K * 128 * 128 < 2^31 (K <= 131072), and the recombination is done in
+// while K * 128 * 128 < 2^31 (K < 131072), and the recombination is done in
 // int64 in the epilogue (wrap mod 2^64, exact for certified results).  The
 // digit base 2^b is a launch parameter: b = 8 (any operand) or b = l (an
 // entangled operand c_m + 2^l c_{m-1} whose halves fit int8: 2 limbs).

@@ -952,3 +952,21 @@ def test_entangle_sets(O, M, sets, N):
         ne.ne_entangle_sets(cfg, to_streams(c), sets, eps, diag)
         d = ne.diag_read(diag)
         assert d["range_violations"] == 1 and d["first_bad"] == ((sets - 1) * M + 1) * N + N - 1
+
+
+def test_gemm_int32_limb_sum_boundary():
+    """The largest admissible K (130 944 < 2^31 / 2^14) with every digit and
+    every B entry at -128: each int32 limb sum is K * 16384 = 2^31 - 2^21, the
+    extreme the tensor-core accumulators must hold exactly; K = 131072 (sum
+    2^31, which would wrap) is refused."""
+    M, R, Cc, K = 3, 128, 128, 130944
+    cfg = ne.ne_config_for(M)
+    planes = torch.full((M * 1 * R * K,), -128, dtype=torch.int8, device="cuda")
+    Bt = torch.full((Cc * K,), -128, dtype=torch.int8, device="cuda")
+    out = empty_streams(M, R * Cc)
+    ne.ne_op_gemm_limbs(cfg, planes, 1, Bt, R, Cc, K, out)
+    torch.cuda.synchronize()
+    assert all(bool((t == K * 16384).all()) for t in out)
+    big = torch.empty(M * R * 131072, dtype=torch.int8, device="cuda")
+    with pytest.raises(ne.NeError):
+        ne.ne_op_gemm_limbs(cfg, big, 1, torch.empty(Cc * 131072, dtype=torch.int8, device="cuda"), R, Cc, 131072, out)
