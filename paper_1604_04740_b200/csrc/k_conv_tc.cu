@@ -40,7 +40,7 @@ static int64_t conv_plane_len(int64_t n, int64_t taps, int W) {
 }
 
 // a1 into circularly extended digit planes: 4 consecutive t per thread, all M
-// streams (each c_m[n] is read once per t and used by streams m and m+1).
+// streams in order (each c_m[n] read once per t, used by streams m and m+1).
 // The range assertion (a0) counts every position once: t in [s0, s0 + N).
 template <int MT>
 __global__ void __launch_bounds__(kThreads)
@@ -50,11 +50,11 @@ k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l,
   constexpr int MA = MT > 0 ? MT : NE_MAX_M;
   const int M = MT > 0 ? MT : M_rt;
   const bool pair = L == 2 && b == l && b <= 31;
+  (void)MA;
   int bad = 0;
   long long first = LLONG_MAX;
   const int64_t nq = plane_len / 4;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
-    int32_t cv[MA][4];
     // position of t = 4q: (t - s0) mod n without a 64-bit division
     // (s0mod = s0 mod n; t - s0mod < plane_len, a few multiples of n at most)
     int64_t p = 4 * q - s0mod;
@@ -64,27 +64,32 @@ k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l,
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       pos[u] = p;
-#pragma unroll
-      for (int m = 0; m < (MT > 0 ? MT : M); ++m) cv[m][u] = __ldg(c.s[m] + p);
       if (++p == n) p = 0;
     }
+    // streams in order with only the previous one live (registers: the M = 8
+    // instantiation stays at full occupancy); c_{M-1} first, the "previous"
+    // stream of stream 0 (circulant Eq. 14)
+    int32_t prv[4], cur[4];
 #pragma unroll
-    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
-      const int mp = m == 0 ? M - 1 : m - 1;
+    for (int u = 0; u < 4; ++u) prv[u] = __ldg(c.s[M - 1] + pos[u]);
+#pragma unroll 1
+    for (int m = 0; m < M; ++m) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cur[u] = __ldg(c.s[m] + pos[u]);
       uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int64_t cc = cv[m][u];
+        const int64_t cc = cur[u];
         bool ok;
         if (pair) {  // the two-digit base-2^l plan in 32-bit arithmetic (as k_entangle_pair)
-          const int32_t c32 = cv[m][u];
+          const int32_t c32 = cur[u];
           const int32_t d0 = (int32_t)((uint32_t)c32 << (32 - b)) >> (32 - b);
-          const int32_t d1 = cv[mp][u] + (c32 >> b) + ((c32 >> (b - 1)) & 1);
+          const int32_t d1 = prv[u] + (c32 >> b) + ((c32 >> (b - 1)) & 1);
           ok = ((uint32_t)(d0 + 128) | (uint32_t)(d1 + 128)) <= 255u;
           w[0] |= (uint32_t)(uint8_t)d0 << (8 * u);
           w[1] |= (uint32_t)(uint8_t)d1 << (8 * u);
         } else {
-          const int64_t x = (int64_t)((uint64_t)cc + ((uint64_t)(int64_t)cv[mp][u] << l));
+          const int64_t x = (int64_t)((uint64_t)cc + ((uint64_t)(int64_t)prv[u] << l));
           int8_t d[4];
           ok = digits_b(x, b, L, d);
 #pragma unroll
@@ -101,6 +106,8 @@ k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l,
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (j < L) __stcs(reinterpret_cast<unsigned int*>(planes + ((int64_t)m * L + j) * plane_len + 4 * q), w[j]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) prv[u] = cur[u];
     }
   }
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
