@@ -192,12 +192,22 @@ class C3Gemm(Workload):
     E2E_IN = ("A", "B")
     E2E_OUT = ("dout",)
 
-    def __init__(self, rank, n=4096, seed=2, algo="tc", scheme="entangled", limbs="plan", fuse=True):
+    def __init__(self, rank, n=4096, seed=2, algo="tc", scheme="entangled", limbs="plan", fuse=True,
+                 paper_shape=None):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
         self.M, self.rows, self.cols, self.K = 3, n, n, n
+        self.true_shape = None
+        if paper_shape is not None:
+            # the paper's GEMM experiment: M subblocks of 2000 x N times N x 1200;
+            # operands zero-padded to the kernel's tile multiples (rows 128, cols 256, K 128),
+            # the metric counts the true shape only
+            Mp, Rt, Ct, Kt = paper_shape
+            self.M, self.true_shape = Mp, (Rt, Ct, Kt)
+            self.rows, self.cols, self.K = -(-Rt // 128) * 128, -(-Ct // 256) * 256, -(-Kt // 128) * 128
+            self.name = f"C3P_M{Mp}_N{Kt}"
         self.seed = seed + 1000 * rank
         self.cfg = ne.ne_config_for(self.M)
         if limbs == "base256":
@@ -210,11 +220,23 @@ class C3Gemm(Workload):
         self.fuse = bool(fuse) and algo == "tc" and scheme == "entangled"
         M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
         dev = "cuda"
-        self.A = [torch.empty(R * K, dtype=torch.int32, device=dev) for _ in range(M)]
-        for m in range(M):
-            ne.ne_gen_uniform_i32(self.seed, 4, m, -64, 64, self.A[m])
-        self.B = torch.empty(K * Cc, dtype=torch.int32, device=dev)
-        ne.ne_gen_uniform_i32(self.seed, 5, 0, -64, 64, self.B)
+        if self.true_shape is None:
+            self.A = [torch.empty(R * K, dtype=torch.int32, device=dev) for _ in range(M)]
+            for m in range(M):
+                ne.ne_gen_uniform_i32(self.seed, 4, m, -64, 64, self.A[m])
+            self.B = torch.empty(K * Cc, dtype=torch.int32, device=dev)
+            ne.ne_gen_uniform_i32(self.seed, 5, 0, -64, 64, self.B)
+        else:
+            Rt, Ct, Kt = self.true_shape
+            self.A = [torch.zeros(R * K, dtype=torch.int32, device=dev) for _ in range(M)]
+            for m in range(M):
+                t = torch.empty(Rt * Kt, dtype=torch.int32, device=dev)
+                ne.ne_gen_uniform_i32(self.seed, 4, m, -64, 64, t)
+                self.A[m].view(R, K)[:Rt, :Kt] = t.view(Rt, Kt)
+            self.B = torch.zeros(K * Cc, dtype=torch.int32, device=dev)
+            t = torch.empty(Kt * Ct, dtype=torch.int32, device=dev)
+            ne.ne_gen_uniform_i32(self.seed, 5, 0, -64, 64, t)
+            self.B.view(K, Cc)[:Kt, :Ct] = t.view(Kt, Ct)
         self.planes = torch.empty(M * L * R * K, dtype=torch.int8, device=dev)
         self.Bt = torch.empty(Cc * K, dtype=torch.int8, device=dev)
         self.delta = [torch.empty(R * Cc, dtype=torch.int64, device=dev) for _ in range(M)]
@@ -281,7 +303,8 @@ class C3Gemm(Workload):
         ]
 
     def work_per_step(self):
-        return 2 * self.M * self.rows * self.cols * self.K / 1e9  # G int64-equivalent ops
+        R, Cc, K = self.true_shape or (self.rows, self.cols, self.K)
+        return 2 * self.M * R * Cc * K / 1e9  # G int64-equivalent ops (true shape)
 
     def stage_info(self):
         M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
@@ -292,8 +315,9 @@ class C3Gemm(Workload):
                     "gemm": ("tensor", 2 * (M + 2) * R * Cc * K / 1e12, "TOP"),
                     "check": ("hbm", (M + 1) * n * 8 / 1e9, "GB"),
                     "recover": ("hbm", (M + 1) * n * 8 / 1e9, "GB")}
-        gemm = ("tensor", 2 * L * M * R * Cc * K / 1e12, "TOP") if self.algo == "tc" else \
-            ("alu", M * R * Cc * K / 1e12, "TMAC")
+        Rt, Ct, Kt = self.true_shape or (R, Cc, K)  # useful work only (the zero padding is not counted)
+        gemm = ("tensor", 2 * L * M * Rt * Ct * Kt / 1e12, "TOP") if self.algo == "tc" else \
+            ("alu", M * Rt * Ct * Kt / 1e12, "TMAC")
         return {
             "entangle": ("hbm", M * R * K * (4 + (L if self.algo == "tc" else 8)) / 1e9, "GB"),
             "prep_b": ("hbm", K * Cc * 5 / 1e9, "GB"),
@@ -304,8 +328,14 @@ class C3Gemm(Workload):
         }
 
     def config(self):
-        return {"workload": "C3 (BASELINE configs[2]): M=3 entangled GEMM A_m 4096x4096 int32 U[-64,64), "
-                            "shared B 4096x4096 U[-64,64), K=4096, int64 results",
+        wl = ("C3 (BASELINE configs[2]): M=3 entangled GEMM A_m 4096x4096 int32 U[-64,64), "
+              "shared B 4096x4096 U[-64,64), K=4096, int64 results")
+        if self.true_shape is not None:
+            Rt, Ct, Kt = self.true_shape
+            wl = (f"C3P (the paper's GEMM shape, P:1119-1121): M={self.M} subblocks of {Rt}x{Kt} int32 "
+                  f"U[-64,64) times a shared {Kt}x{Ct}, int64 results; zero-padded to {self.rows}x{self.K} "
+                  f"x {self.K}x{self.cols} for the tiles, metric on the true shape")
+        return {"workload": wl,
                 "M": self.M, "rows": self.rows, "cols": self.cols, "K": self.K,
                 "limbs_L": self.L if self.algo == "tc" else None, "gemm_algo": self.algo,
                 "limb_base_bits": self.limb_bits if self.algo == "tc" else None,
@@ -347,6 +377,8 @@ class C3Gemm(Workload):
         import oracle as O
 
         M, K, Cc = self.M, self.K, self.cols
+        if self.true_shape is not None:
+            _, Cc, K = self.true_shape
         ocfg = O.config_for(M, 64)
         A = np.stack([O.gen_uniform(self.seed, 4, m, -64, 64, rows_sample * K) for m in range(M)])
         B = O.gen_uniform(self.seed, 5, 0, -64, 64, K * Cc).reshape(K, Cc)
@@ -357,7 +389,7 @@ class C3Gemm(Workload):
         O.recover(ocfg, [None] + [D[m] for m in range(1, M)], 0)
         dt = time.perf_counter() - t0
         return dt, 2 * M * rows_sample * Cc * K / 1e9, f"{rows_sample} of {self.rows} rows of each of the " \
-                                                       f"M=3 streams, full K and cols (same seeded inputs)"
+                                                       f"M={M} streams, full K and cols (same seeded inputs)"
 
 
 class C4PermInner(Workload):
@@ -752,14 +784,17 @@ class C1Chain(Workload):
         return dt, reps * ns / 1e9, f"{reps} full C1 passes (w={self.w})" + ("" if ns == self.n else f" at N'={ns}")
 
 
-WORKLOADS = {"c1": C1Chain, "c2": C2Conv, "c2p": C2Conv, "c3": C3Gemm, "c4": C4PermInner, "c5": None}
-ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c2p": (1, 1), "c3": (16, 2), "c4": (64, 8),
+WORKLOADS = {"c1": C1Chain, "c2": C2Conv, "c2p": C2Conv, "c3": C3Gemm, "c3p": C3Gemm, "c4": C4PermInner, "c5": None}
+ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c2p": (1, 1), "c3": (16, 2), "c3p": (64, 8), "c4": (64, 8),
                  "c5": (4096, 512)}  # (cpu_baseline, per reference-arm step)
 
 
 def make_workload(args, rank):
     if args.workload == "c3":
         return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=bool(args.fuse or 0))
+    if args.workload == "c3p":
+        return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=bool(args.fuse or 0),
+                      paper_shape=(args.streams, 2000, 1200, args.kdim))
     if args.workload == "c2":
         return C2Conv(rank, algo=args.conv or "direct", fuse=bool(args.fuse if args.fuse is not None else 1))
     if args.workload == "c2p":
@@ -1170,9 +1205,14 @@ def run_reference(args):
     cls = WORKLOADS[args.workload] or C3Gemm
     W = cls.__new__(cls)
     # the attributes oracle_sample / work_per_step / config need, without CUDA
-    if args.workload == "c3":
+    if args.workload in ("c3", "c3p"):
         W.M, W.rows, W.cols, W.K, W.seed, W.algo, W.L, W.limb_bits, W.scheme = \
             3, 4096, 4096, 4096, 2, "tc", 2, 22, "entangled"
+        W.true_shape, W.fuse = None, False
+        if args.workload == "c3p":
+            W.M, W.true_shape = args.streams, (2000, 1200, args.kdim)
+            W.rows, W.cols, W.K = 2048, 1280, -(-args.kdim // 128) * 128
+            W.limb_bits = {3: 22, 4: 16, 8: 8}.get(W.M, 8)
 
         class _Cfg:
             l, k = 22, 20
@@ -1260,7 +1300,8 @@ def main():
                     help="c2/c2p: tensor-core Toeplitz conv or the direct IMAD kernel (default: the faster one "
                          "measured: direct for c2's 64 taps, tc for c2p)")
     ap.add_argument("--taps", type=int, default=4500, help="c2p: kernel taps (paper: 100-4500)")
-    ap.add_argument("--streams", type=int, default=8, help="c2p: M (paper: 3 or 8)")
+    ap.add_argument("--streams", type=int, default=8, help="c2p / c3p: M (paper: 3 or 8)")
+    ap.add_argument("--kdim", type=int, default=2000, help="c3p: N, the inner dimension (paper: 200-2000)")
     ap.add_argument("--w", type=int, default=64, choices=[64, 32], help="c1: container width (P:528-530)")
     ap.add_argument("--layout", default="aos", choices=["aos", "soa"], help="c4: entangled layout at rest")
     ap.add_argument("--n", type=int, default=None, help="c1: stream length (default 4096 = configs[0])")

@@ -970,3 +970,35 @@ def test_gemm_int32_limb_sum_boundary():
     big = torch.empty(M * R * 131072, dtype=torch.int8, device="cuda")
     with pytest.raises(ne.NeError):
         ne.ne_op_gemm_limbs(cfg, big, 1, torch.empty(Cc * 131072, dtype=torch.int8, device="cuda"), R, Cc, 131072, out)
+
+
+@pytest.mark.parametrize("M,Rt,Ct,Kt", [(3, 200, 300, 100), (8, 130, 1200, 200)])
+def test_gemm_zero_padded_paper_shape(O, M, Rt, Ct, Kt):
+    """The paper's GEMM shapes (2000 x N by N x 1200) are not tile
+    multiples: operands zero-padded to (128, 256, 128) multiples give, in the
+    true region, exactly the oracle's product of the unpadded operands, and the
+    check on the padded output flags nothing."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    R, Cc, K = -(-Rt // 128) * 128, -(-Ct // 256) * 256, -(-Kt // 128) * 128
+    L, b = ne.ne_gemm_limb_plan(cfg, 64)
+    A = np.stack([O.gen_uniform(21, 4, m, -64, 64, Rt * Kt) for m in range(M)])
+    B = O.gen_uniform(21, 5, 0, -64, 64, Kt * Ct)
+    Ap = np.zeros((M, R, K), dtype=np.int64)
+    Ap[:, :Rt, :Kt] = A.reshape(M, Rt, Kt)
+    Bp = np.zeros((K, Cc), dtype=np.int64)
+    Bp[:Kt, :Ct] = B.reshape(Kt, Ct)
+    planes = torch.empty(M * L * R * K, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_limbs(cfg, to_streams(Ap.reshape(M, -1)), L, planes, diag, limb_bits=b)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(Bp.reshape(-1), torch.int32), K, Cc, Bt, diag)
+    out, d_out = empty_streams(M, R * Cc), empty_streams(M, R * Cc)
+    ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, limb_bits=b)
+    ne.ne_disentangle_check(cfg, out, 0, d_out, None, diag)
+    ref = O.op_gemm(ocfg, O.entangle(ocfg, A).reshape(M, Rt, Kt), B.reshape(Kt, Ct))
+    got = to_np(out).reshape(M, R, Cc)
+    assert (got[:, :Rt, :Ct] == ref).all() and (got[:, Rt:, :] == 0).all() and (got[:, :, Ct:] == 0).all()
+    plain = A.reshape(M, Rt, Kt) @ B.reshape(Kt, Ct)
+    assert (to_np(d_out).reshape(M, R, Cc)[:, :Rt, :Ct] == plain).all()
+    d = ne.diag_read(diag)
+    assert d["range_violations"] == 0 and d["fault_positions"] == 0
