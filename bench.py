@@ -521,12 +521,13 @@ class C2Conv(Workload):
     E2E_IN = ("c", "g")
     E2E_OUT = ("dout",)
 
-    def __init__(self, rank, n=65536, taps=64, seed=1, M=3, algo="tc", paper=False, fuse=True):
+    def __init__(self, rank, n=65536, taps=64, seed=1, M=3, algo="tc", paper=False, fuse=True, scheme="entangled"):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
         self.M, self.n, self.T, self.algo, self.paper = M, n, taps, algo, paper
+        self.scheme = scheme if algo == "tc" else "entangled"
         self.fuse = fuse and algo == "direct"  # the direct conv kernel carries the fused check
         if paper:
             self.name = "C2P"
@@ -546,6 +547,13 @@ class C2Conv(Workload):
             self.L, self.limb_bits = ne.ne_gemm_limb_plan(self.cfg, 127)
             self.block, self.kpad, self.plen = ne.ne_conv_geometry(n, taps, self.L)
             self.planes = torch.empty(M * self.L * self.plen, dtype=torch.int8, device="cuda")
+            if self.scheme == "abft":
+                # the paper's comparison: plain data (one int8 digit per stream) + the checksum
+                # stream (Eq. 4; |sum| <= 128 M -> 2 base-256 digits)
+                self.Ls = 2
+                self.pdata = torch.empty(M * self.plen, dtype=torch.int8, device="cuda")
+                self.psum = torch.empty(self.Ls * self.plen, dtype=torch.int8, device="cuda")
+                self.e = torch.empty(n, dtype=torch.int64, device="cuda")
             self.Gt = torch.empty(self.block * self.kpad, dtype=torch.int8, device="cuda")
             self.launches_per_step = 5 + (1 if n % 128 else 0)
         else:
@@ -560,6 +568,17 @@ class C2Conv(Workload):
         part = [None if m == r else self.delta[m] for m in range(M)]
         tail = [("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
                 ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec))]
+        if self.scheme == "abft":
+            rr = [None if m == r else self.delta[m] for m in range(M)]
+            return [("encode", lambda: ne.ne_abft_encode_conv(cfg, self.c, self.T, 0, self.block, self.pdata, self.Ls,
+                                                              self.psum, self.diag)),
+                    ("prep_g", lambda: ne.ne_conv_prep_taps(self.g, 0, self.Gt, self.diag, self.block)),
+                    ("conv", lambda: (ne.ne_op_conv_limbs_plain(M, self.pdata, 1, self.Gt, self.n, self.T, 0,
+                                                                self.delta, block=self.block),
+                                      ne.ne_op_conv_limbs_plain(1, self.psum, self.Ls, self.Gt, self.n, self.T, 0,
+                                                                [self.e], block=self.block))),
+                    ("check", lambda: ne.ne_abft_check(cfg, self.delta, self.e, self.bitmap, self.diag)),
+                    ("recover", lambda: ne.ne_abft_recover(cfg, rr, self.e, r, self.drec[r]))]
         if self.algo == "tc":
             return [("entangle", lambda: ne.ne_entangle_limbs_conv(cfg, self.c, self.T, 0, self.L, self.planes,
                                                                    self.diag, self.limb_bits, self.block)),
@@ -581,7 +600,13 @@ class C2Conv(Workload):
         n, M, T = self.n, self.M, self.T
         info = {"check": ("hbm", M * n * 16 / 1e9, "GB"),
                 "recover": ("hbm", (2 * M - 1) * n * 8 / 1e9, "GB")}
-        if self.algo == "tc":
+        if self.scheme == "abft":
+            info["conv"] = ("tensor", 2 * (M + self.Ls) * n * T / 1e12, "TOP")
+            info["encode"] = ("hbm", (M * n * 4 + (M + self.Ls) * self.plen) / 1e9, "GB")
+            info["prep_g"] = ("hbm", (T * 4 + self.block * self.kpad) / 1e9, "GB")
+            info["check"] = ("hbm", (M + 1) * n * 8 / 1e9, "GB")
+            info["recover"] = ("hbm", (M + 1) * n * 8 / 1e9, "GB")
+        elif self.algo == "tc":
             # useful limb products only (the Toeplitz zeros, Kpad/T - 1, are not counted)
             info["conv"] = ("tensor", 2 * self.L * M * n * T / 1e12, "TOP")
             info["entangle"] = ("hbm", M * (n * 4 + self.L * self.plen) / 1e9, "GB")
@@ -600,7 +625,9 @@ class C2Conv(Workload):
             wl = ("C2 (BASELINE configs[1]): M=3 streams of 65536 int32 U[-128,128), circular "
                   "convolution with a shared 64-tap kernel U[-128,128)")
         ws = self.M * self.n * 8 * 3 / 1e6
-        return {"workload": wl, "M": self.M, "n": self.n, "taps": self.T,
+        if self.scheme == "abft":
+            wl += "; scheme: ABFT single checksum stream (Eqs. 3-6, the paper's comparison method)"
+        return {"workload": wl, "M": self.M, "n": self.n, "taps": self.T, "scheme": self.scheme,
                 "conv_algo": ("tc: Toeplitz GEMM on tcgen05, %d int8 digits base 2^%d, %d-output blocks, Kpad=%d"
                               % (self.L, self.limb_bits, self.block, self.kpad)) if self.algo == "tc" else "direct IMAD",
                 "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
@@ -614,6 +641,8 @@ class C2Conv(Workload):
         """The same conv kernel on unentangled data: (i) same digit count
         (plain c in digit 0, other digits 0), (ii) one int8 digit; ms per call."""
         torch, ne = self.torch, self.ne
+        if self.scheme == "abft":
+            return {}
         if self.algo != "tc":
             x64 = [c.to(torch.int64) for c in self.c]
             o64 = [torch.empty_like(x) for x in x64]
@@ -798,7 +827,8 @@ def make_workload(args, rank):
     if args.workload == "c2":
         return C2Conv(rank, algo=args.conv or "direct", fuse=bool(args.fuse if args.fuse is not None else 1))
     if args.workload == "c2p":
-        return C2Conv(rank, n=10 ** 6, taps=args.taps, M=args.streams, algo=args.conv or "tc", paper=True)
+        return C2Conv(rank, n=10 ** 6, taps=args.taps, M=args.streams, algo=args.conv or "tc", paper=True,
+                      scheme=args.scheme)
     if args.workload == "c4":
         return C4PermInner(rank, layout=args.layout)
     if args.workload == "c1":
@@ -1247,6 +1277,7 @@ def run_reference(args):
         W.M, W.n, W.T, W.seed = (args.streams, 10 ** 6, args.taps, 1) if paper else (3, 65536, 64, 1)
         W.algo, W.paper, W.name = args.conv or ("tc" if paper else "direct"), paper, "C2P" if paper else "C2"
         W.fuse = W.algo == "direct" and bool(args.fuse if args.fuse is not None else 1)
+        W.scheme = args.scheme if W.algo == "tc" else "entangled"
         W.L, W.limb_bits = 2, {3: 22, 4: 16, 8: 8}.get(W.M, 8)
         W.block = 256 if W.T >= 256 else 128
         W.kpad = (W.T + W.block - 1 + 127) // 128 * 128
@@ -1292,7 +1323,7 @@ def main():
     ap.add_argument("--limbs", default="plan", choices=["plan", "base256"],
                     help="c3: GEMM operand digits: cheapest exact plan (default) or balanced base 256")
     ap.add_argument("--scheme", default="entangled", choices=["entangled", "abft"],
-                    help="c3 only: numerical entanglement (default) or the paper's ABFT comparison method")
+                    help="c3 / c2p: numerical entanglement (default) or the paper's ABFT comparison method")
     ap.add_argument("--fuse", type=int, default=None,
                     help="disentangle/check fused into the op kernel (1) or a separate pass (0); default: the "
                          "measured-faster choice per workload (c1, c2: fused; c3: separate)")

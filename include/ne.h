@@ -352,6 +352,20 @@ ne_status ne_to_limbs(ne_cstreams32 x, int32_t count, int64_t n_total, int32_t L
  * checksum: M*n + n).  n_total % 16 == 0, 1 <= Ls <= 4. */
 ne_status ne_abft_encode_limbs(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int8_t* pdata,
                                int32_t Ls, int8_t* psum, ne_diag* diag, ne_stream_t stream);
+/* ABFT on the tensor-core convolution (the paper's conv comparison, P:1102-
+ * 1116): plain data as one int8 digit plane per stream and the checksum r =
+ * sum_m c_m (Eq. 4) as Ls base-256 digit planes, circularly extended exactly
+ * like ne_entangle_limbs_conv (same block / plane_len); out-of-range values
+ * are range violations (data m*N + n, checksum M*N + n).  Then
+ * ne_op_conv_limbs_plain runs the Toeplitz conv on `count` plane sets of L
+ * digits (count <= 8; no entanglement config involved), and ne_abft_check /
+ * ne_abft_recover finish.  Layout, alignment and limits as the conv calls. */
+ne_status ne_abft_encode_conv(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t taps,
+                              int32_t correlate, int32_t block, int8_t* pdata, int32_t Ls, int8_t* psum,
+                              ne_diag* diag, ne_stream_t stream);
+ne_status ne_op_conv_limbs_plain(int32_t count, const int8_t* planes, int32_t L, int32_t limb_bits,
+                                 int32_t block, const int8_t* Gt, int64_t n_total, int32_t taps,
+                                 int32_t correlate, ne_streams out, ne_stream_t stream);
 /* Eq. 6: flag[n] = (sum_m d_m[n] != e[n]) mod 2^64, bitmap/diag as
  * ne_disentangle_check. */
 ne_status ne_abft_check(const ne_config* cfg, ne_cstreams d, const int64_t* e, int64_t n_total,

@@ -39,7 +39,7 @@ EXPORTS = (
     "ne_entangle_w32", "ne_op_scale_add_w32", "ne_disentangle_check_w32", "ne_recover_w32", "ne_inject_sweep_w32",
     "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
-    "ne_abft_encode", "ne_abft_encode_limbs", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
+    "ne_abft_encode", "ne_abft_encode_limbs", "ne_abft_encode_conv", "ne_op_conv_limbs_plain", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
 )
 
 
@@ -112,6 +112,8 @@ _SIGS = {
     "ne_op_permute_inner_check": [_PCFG, Streams, _VP, _I32, _VP, _I64, _VP, _I64, _I64, _I32,
                                   Streams, Streams, _VP, _VP, _VP],
     "ne_inject": [_VP, _I64, _U64, _VP],
+    "ne_abft_encode_conv": [_PCFG, Streams, _I64, _I32, _I32, _I32, _VP, _I32, _VP, _VP, _VP],
+    "ne_op_conv_limbs_plain": [_I32, _VP, _I32, _I32, _I32, _VP, _I64, _I32, _I32, Streams, _VP],
     "ne_abft_encode": [_PCFG, Streams, _I64, _VP, _VP, _VP],
     "ne_to_limbs": [Streams, _I32, _I64, _I32, _VP, _VP, _VP],
     "ne_abft_encode_limbs": [_PCFG, Streams, _I64, _VP, _I32, _VP, _VP, _VP],
@@ -441,6 +443,18 @@ def ne_op_permute_inner_check(cfg: Config, v: torch.Tensor, block: int, r: int, 
 
 
 # ------------------------------------------------------------------ ABFT comparison baseline (Eqs. 3-6)
+def ne_abft_encode_conv(cfg: Config, c, taps: int, correlate: int, block: int, pdata: torch.Tensor, Ls: int,
+                        psum: torch.Tensor, diag=None) -> None:
+    _call("ne_abft_encode_conv", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), taps, correlate, block,
+          _ptr(pdata, torch.int8), Ls, _ptr(psum, torch.int8), _ptr(diag, torch.int64), _stream())
+
+
+def ne_op_conv_limbs_plain(count: int, planes: torch.Tensor, L: int, Gt: torch.Tensor, n: int, taps: int,
+                           correlate: int, out, limb_bits: int = 8, block: int = 128) -> None:
+    _call("ne_op_conv_limbs_plain", count, _ptr(planes, torch.int8), L, limb_bits, block, _ptr(Gt, torch.int8), n,
+          taps, correlate, _streams(out, torch.int64), _stream())
+
+
 def ne_abft_encode(cfg: Config, c, r_out: torch.Tensor, diag=None) -> None:
     _call("ne_abft_encode", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), _ptr(r_out, torch.int32),
           _ptr(diag, torch.int64), _stream())

@@ -113,6 +113,70 @@ k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l,
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
+// ABFT comparison (NEXT-1 on the conv, Eqs. 3-5): plain data as one int8
+// digit per stream and the checksum stream r = sum_m c_m (Eq. 4) as Ls
+// balanced base-256 digits, in the same circularly extended plane layout, one
+// pass; values that do not fit are range violations (data: m*N + n; checksum:
+// M*N + n), each position counted once.
+template <int MT>
+__global__ void __launch_bounds__(kThreads)
+k_abft_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int64_t n, int64_t s0, int64_t s0mod,
+                   int64_t plane_len, int Ls, int8_t* __restrict__ pdata, int8_t* __restrict__ psum,
+                   ne_diag* __restrict__ diag) {
+  const int M = MT > 0 ? MT : M_rt;
+  int bad = 0;
+  long long first = LLONG_MAX;
+  const int64_t nq = plane_len / 4;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = 4 * q - s0mod;
+    if (p < 0) p += n;
+    while (p >= n) p -= n;
+    int64_t pos[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      pos[u] = p;
+      if (++p == n) p = 0;
+    }
+    int64_t sum[4] = {0, 0, 0, 0};
+#pragma unroll 1
+    for (int m = 0; m < M; ++m) {
+      uint32_t w = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t v = __ldg(c.s[m] + pos[u]);
+        sum[u] += v;
+        w |= (uint32_t)(uint8_t)(int8_t)v << (8 * u);
+        const int64_t t = 4 * q + u;
+        if (t >= s0 && t < s0 + n && (v < -128 || v > 127)) {
+          ++bad;
+          const long long idx = (long long)m * n + pos[u];
+          first = idx < first ? idx : first;
+        }
+      }
+      __stcs(reinterpret_cast<unsigned int*>(pdata + (int64_t)m * plane_len + 4 * q), w);
+    }
+    uint32_t ws[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int8_t d[4];
+      const bool ok = digits_b(sum[u], 8, Ls, d);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < Ls) ws[j] |= (uint32_t)(uint8_t)d[j] << (8 * u);
+      const int64_t t = 4 * q + u;
+      if (t >= s0 && t < s0 + n && !ok) {
+        ++bad;
+        const long long idx = (long long)M * n + pos[u];
+        first = idx < first ? idx : first;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < Ls) __stcs(reinterpret_cast<unsigned int*>(psum + (int64_t)j * plane_len + 4 * q), ws[j]);
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
 // G (W x Kpad int8, K contiguous): conv G[i][k] = g[i + T - 1 - k],
 // correlation G[i][k] = g[k - i]; taps outside [-128, 127] are range
 // violations (counted once per tap, first_bad = tap index).
@@ -243,3 +307,51 @@ extern "C" ne_status ne_op_conv_limbs(const ne_config* cfg, const int8_t* planes
                                                           n_total, out);
   return launch_status();
 }
+
+extern "C" ne_status ne_abft_encode_conv(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t taps,
+                                         int32_t correlate, int32_t block, int8_t* pdata, int32_t Ls, int8_t* psum,
+                                         ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total < 1 || taps < 1 || (correlate != 0 && correlate != 1) || (block != 128 && block != 256) || Ls < 1 ||
+      Ls > 4 || !pdata || !psum || !aligned16(pdata) || !aligned16(psum))
+    return NE_EINVAL;
+  for (int m = 0; m < cfg->M; ++m)
+    if (!c.s[m]) return NE_EINVAL;
+  const int64_t plen = conv_plane_len(n_total, taps, block);
+  const int64_t s0 = correlate ? 0 : (int64_t)taps - 1;
+  const int grid = grid_for(plen / 4, kThreads);
+  cudaStream_t s = cs(stream);
+  switch (cfg->M) {
+    case 3: k_abft_conv_planes<3><<<grid, kThreads, 0, s>>>(c, 3, n_total, s0, s0 % n_total, plen, Ls, pdata, psum, diag); break;
+    case 8: k_abft_conv_planes<8><<<grid, kThreads, 0, s>>>(c, 8, n_total, s0, s0 % n_total, plen, Ls, pdata, psum, diag); break;
+    default: k_abft_conv_planes<0><<<grid, kThreads, 0, s>>>(c, cfg->M, n_total, s0, s0 % n_total, plen, Ls, pdata, psum, diag); break;
+  }
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_conv_limbs_plain(int32_t count, const int8_t* planes, int32_t L, int32_t limb_bits,
+                                            int32_t block, const int8_t* Gt, int64_t n_total, int32_t taps,
+                                            int32_t correlate, ne_streams out, ne_stream_t stream) {
+  if (count < 1 || count > 8 || n_total < 1 || taps < 1 || (correlate != 0 && correlate != 1) || L < 1 || L > 4 ||
+      limb_bits < 8 || limb_bits > 63 || (block != 128 && block != 256) || !planes || !Gt || !aligned16(planes) ||
+      !aligned16(Gt))
+    return NE_EINVAL;
+  if (block == 256 && L > 2) return NE_ENOTSUP;
+  const int64_t kp = conv_kpad(taps, block);
+  if (kp >= 131072) return NE_ENOTSUP;
+  for (int m = 0; m < count; ++m)
+    if (!out.s[m] || !aligned16(out.s[m])) return NE_EINVAL;
+  const int64_t plen = conv_plane_len(n_total, taps, block);
+  const int64_t nb = n_total / block;
+  cudaStream_t s = cs(stream);
+  ne_status st;
+  if (nb > 0 && (st = launch_conv_tc(count, L, limb_bits, block, planes, plen / block, Gt, kp, nb, out, s)) != NE_OK)
+    return st;
+  const int64_t tail = n_total - (int64_t)block * nb;
+  if (tail > 0)
+    k_conv_tail<<<(unsigned)(count * tail), 128, 0, s>>>(planes, count, L, limb_bits, plen, Gt, kp, nb, block, n_total,
+                                                        out);
+  return launch_status();
+}
+

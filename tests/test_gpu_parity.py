@@ -1002,3 +1002,40 @@ def test_gemm_zero_padded_paper_shape(O, M, Rt, Ct, Kt):
     assert (to_np(d_out).reshape(M, R, Cc)[:, :Rt, :Ct] == plain).all()
     d = ne.diag_read(diag)
     assert d["range_violations"] == 0 and d["fault_positions"] == 0
+
+
+@pytest.mark.parametrize("M,N,T,correlate", [(3, 5000, 300, 0), (8, 4099, 64, 1), (3, 100, 257, 0)])
+def test_abft_conv_tensor_core(O, M, N, T, correlate):
+    """The paper's ABFT comparison on the tensor-core conv: data planes (one
+    int8 digit), checksum planes (Eq. 4, base 256) in the extended layout, the
+    plain Toeplitz conv of both, ABFT check (Eq. 6) and recovery ==
+    the oracle's ABFT on the direct conv; a corrupted data output is flagged."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 22, 1, M, N, -128, 128)
+    g = O.gen_uniform(22, 3, 0, -128, 128, T)
+    bw, kp, plen = ne.ne_conv_geometry(N, T, 2)
+    Ls = 2
+    pdata = torch.empty(M * plen, dtype=torch.int8, device="cuda")
+    psum = torch.empty(Ls * plen, dtype=torch.int8, device="cuda")
+    Gt = torch.empty(bw * kp, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_abft_encode_conv(cfg, to_streams(c), T, correlate, bw, pdata, Ls, psum, diag)
+    ne.ne_conv_prep_taps(dev(g, torch.int32), correlate, Gt, diag, block=bw)
+    d, e = empty_streams(M, N), empty_streams(1, N)
+    ne.ne_op_conv_limbs_plain(M, pdata, 1, Gt, N, T, correlate, d, block=bw)
+    ne.ne_op_conv_limbs_plain(1, psum, Ls, Gt, N, T, correlate, e, block=bw)
+    torch.cuda.synchronize()
+    assert ne.diag_read(diag)["range_violations"] == 0
+    dref = O.op_conv(ocfg, c, g, bool(correlate))
+    eref = O.op_conv(ocfg, O.abft_encode(ocfg, c)[None, :], g, bool(correlate))[0]
+    assert (to_np(d) == dref).all() and (e[0].cpu().numpy() == eref).all()
+    d[1][N // 2] += 5
+    bm = torch.empty((N + 31) // 32, dtype=torch.int32, device="cuda")
+    dg = ne.diag_new()
+    ne.ne_abft_check(cfg, d, e[0], bm, dg)
+    fref, nf = O.abft_check(ocfg, to_np(d), eref)
+    assert (bitmap_to_flags(bm, N) == fref).all() and ne.diag_read(dg)["fault_positions"] == nf == 1
+    rec = torch.empty(N, dtype=torch.int64, device="cuda")
+    d[1][N // 2] -= 5
+    ne.ne_abft_recover(cfg, [None if m == 2 else d[m] for m in range(M)], e[0], 2, rec)
+    assert (rec.cpu().numpy() == dref[2]).all()
