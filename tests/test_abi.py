@@ -148,3 +148,13 @@ def test_argument_validation_of_the_newer_entry_points(L):
     c32 = ne.ne_config_for(3, 32)
     assert L.ne_op_scale_add_check_w32(ctypes.byref(c32), st, 16, 37, None, st, 1, 3, st, None, None, None) == 4
     assert L.ne_entangle_sets_w32(ctypes.byref(cfg), st, 2, 16, st, None, None) == 2      # w = 64 config
+
+
+def test_sass_has_tcgen05_tma_and_tmem(L):
+    """The GEMM / conv kernels are real tcgen05 code: the sm_100a SASS of
+    libne.so contains the tensor-core MMA (UTCIMMA), its commit barrier
+    (UTCBAR), TMEM allocation (UTCATOMSWS) and loads (LDTM), and TMA bulk
+    tensor loads / stores (UTMALDG / UTMASTG)."""
+    sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {ne.LIB} 2>/dev/null").read()
+    for op in ("UTCIMMA", "UTCBAR", "UTCATOMSWS", "LDTM", "UTMALDG", "UTMASTG"):
+        assert op in sass, op
