@@ -1039,3 +1039,29 @@ def test_abft_conv_tensor_core(O, M, N, T, correlate):
     d[1][N // 2] -= 5
     ne.ne_abft_recover(cfg, [None if m == 2 else d[m] for m in range(M)], e[0], 2, rec)
     assert (rec.cpu().numpy() == dref[2]).all()
+
+
+@pytest.mark.parametrize("M,r,W", [(4, 3, 32), (8, 5, 16), (5, 2, 24)])
+def test_exhaustive_single_bit_injection_other_M(O, M, r, W):
+    """a7 beyond C1: every single-bit flip of every stream in the first W
+    outputs of a conv (M = 4, 8 and the generic-M kernel at M = 5, excluded
+    stream r != 0) flags exactly its own position (Props 2/4, M l >= w), and
+    d_hat at it equals the oracle's for the same corrupted word."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    N, T = 1024, 17
+    c = gen(O, 23, 1, M, N, -100, 100)
+    g = O.gen_uniform(23, 3, 0, -100, 100, T)
+    delta = O.op_conv(ocfg, O.entangle(ocfg, c), g)
+    trials = M * W * 64
+    fw = torch.empty(trials, dtype=torch.int64, device="cuda")
+    dh = torch.empty(trials * M, dtype=torch.int64, device="cuda")
+    ne.ne_inject_sweep(cfg, to_streams(delta, torch.int64), W, r, fw, dh)
+    fw = fw.cpu().numpy().view(np.uint64)
+    dh = dh.cpu().numpy().reshape(trials, M)
+    for t in range(trials):
+        s, n, bit = t // (W * 64), (t // 64) % W, t % 64
+        col = delta[:, n].copy()
+        col[s] = np.int64(np.uint64(col[s]) ^ np.uint64(1 << bit))
+        od, of = O.disentangle_one(ocfg, col, r)
+        assert of == 1 and int(fw[t]) == (1 << n), (s, n, bit)
+        assert (dh[t] == od).all(), (s, n, bit)
