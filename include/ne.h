@@ -295,6 +295,15 @@ ne_status ne_op_gemm_limbs_check(const ne_config* cfg, const int8_t* planes, int
                                  int32_t r, ne_streams d_out, uint32_t* bitmap, ne_diag* diag,
                                  int32_t* tile_counters, ne_stream_t stream);
 
+/* Debug hook (not on the hot path): every later tensor-core GEMM / Toeplitz
+ * conv launch in this process records, for CTA c and its t-th tile (t < 32),
+ * the %globaltimer value when the tile's accumulators are complete and when
+ * its epilogue has staged the last chunk, at buf[(c * 32 + t) * 2 + {0, 1}]
+ * (device memory of grid x 64 int64, zeroed by the caller).  max_clusters > 0
+ * caps the persistent grid (0: occupancy-sized).  buf = NULL, max_clusters = 0
+ * turn it off.  Not thread-safe; NE_EINVAL if max_clusters < 0. */
+ne_status ne_gemm_trace(long long* buf, int32_t max_clusters);
+
 /* One stream of ne_op_gemm_limbs (the per-GPU GEMM of the one-stream-per-GPU
  * layout): C_m = sum_i 2^(8i) D_{m,i} B from planes_m (L planes). */
 ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t* planes_m, int32_t L,

@@ -12,6 +12,7 @@ void launch_gemm_imad64(int M, const ne_cstreams& A, const int32_t* B, const ne_
                         int64_t cols, int64_t K, cudaStream_t s);
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s);
+void gemm_trace(long long* buf, int max_clusters);
 ne_status launch_gemm_tc_check(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows,
                                int64_t cols, int64_t K, const ne_streams& C, const ne_cstreams& dr,
                                const ne_streams& dor, uint32_t* bitmap, ne_diag* diag, int* cnt, int l,
@@ -145,6 +146,12 @@ extern "C" ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes
     if (!C.s[m] || !aligned16(C.s[m])) return NE_EINVAL;
   if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
   return launch_gemm_tc(cfg->M, L, limb_bits, planes, Bt, rows, cols, K, C, cs(stream));
+}
+
+extern "C" ne_status ne_gemm_trace(long long* buf, int32_t max_clusters) {
+  if (max_clusters < 0) return NE_EINVAL;
+  gemm_trace(buf, max_clusters);
+  return NE_OK;
 }
 
 extern "C" ne_status ne_gemm_check_workspace(int64_t rows, int64_t cols, size_t* bytes) {

@@ -95,6 +95,19 @@ struct Geo {
   int raster_rows;
 };
 
+// Debug hook (ne_gemm_trace): per CTA and tile t < 32, %globaltimer when the
+// tile's accumulators are complete and when its last chunk is staged.
+struct DbgArgs {
+  long long* trace;
+};
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+static long long* g_trace = nullptr;
+static int g_max_clusters = 0;
+
 __device__ __forceinline__ void epi_bar() {  // the 8 epilogue warps only
   asm volatile("bar.sync 1, %0;" ::"n"(32 * 8) : "memory");
 }
@@ -223,7 +236,7 @@ template <int L, int BN, int STAGES, int SW, int CL, int CHK>
 __global__ void __launch_bounds__(threads_for<CHK>(), 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
           const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
-          const __grid_constant__ ChkArgs chk, const Geo geo) {
+          const __grid_constant__ ChkArgs chk, const Geo geo, const DbgArgs dbg) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   constexpr int BK = CF::BK;
   static_assert(L * BN <= 512, "TMEM holds 512 columns");
@@ -331,9 +344,17 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
         const uint32_t ab = tile % CF::kBufs, use = tile / CF::kBufs;
         mbar_wait(&tmem_empty[ab], (use & 1) ^ 1);  // epilogue drained this accumulator set
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        long long t_wait = 0;
+        if (dbg.trace && tile < 32) dbg.trace[(blockIdx.x * 32 + tile) * 4 + 2] = globaltimer();
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % STAGES;
-          mbar_wait(&full[s], (it / STAGES) & 1);
+          if (dbg.trace) {
+            const long long t0 = globaltimer();
+            mbar_wait(&full[s], (it / STAGES) & 1);
+            t_wait += globaltimer() - t0;
+          } else {
+            mbar_wait(&full[s], (it / STAGES) & 1);
+          }
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = smem_u32(smem + s * CF::kStage);
           const uint32_t sb = sa + L * CF::kATile;
@@ -349,6 +370,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
           mma_commit(&empty[s], cmask);  // frees stage s in every CTA of the cluster
         }
         mma_commit(&tmem_full[ab], 1);   // this tile's accumulators are final
+        if (dbg.trace && tile < 32) dbg.trace[(blockIdx.x * 32 + tile) * 4 + 3] = t_wait;
       }
     }
   } else if (warp >= 4 && warp < 4 + kEpiWarps) {
@@ -369,20 +391,17 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
       const uint32_t ab = tile % CF::kBufs, use = tile / CF::kBufs;
       mbar_wait(&tmem_full[ab], use & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll 1
-      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16, buf = (buf + 1) % CF::kOutBufs) {
-        uint32_t v[L][16];
-#pragma unroll
-        for (int i = 0; i < L; ++i) tmem_ld16(tl + ab * CF::kAccCols + i * BN + c, v[i]);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c + 16 == (half + 1) * (BN / 2)) {
-          // last TMEM read of this tile for this warp: release the accumulators
-          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-          __syncwarp();
-          if (lane == 0)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[ab])) : "memory");
-        }
-        // the TMA store that last read this buffer (two chunks ago) must be done
+      if (dbg.trace && ew == 0 && lane == 0 && tile < 32) dbg.trace[(blockIdx.x * 32 + tile) * 4] = globaltimer();
+      // 16-column chunks, kNch per warp; the TMEM load of chunk ci+1 is in
+      // flight while chunk ci is staged (two register sets, plain GEMM only)
+      constexpr int kNch = BN / 2 / 16;
+      constexpr bool kPipe = CHK == 0 && L <= 3;  // (L = 4: 128 registers of limbs would spill)
+      const uint32_t tacc = tl + ab * CF::kAccCols;
+      const int cb = half * (BN / 2);
+      uint32_t vs[kPipe ? 2 : 1][L][16];
+      // stage one chunk: pack the limbs to int64, 128B-swizzled smem box, TMA store
+      auto stage = [&](uint32_t(&v)[L][16], int c) {
+        // the TMA store that last read this buffer must be done
         if (lane == 0) {
           if (CF::kOutBufs == 2)
             asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -392,15 +411,29 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
         __syncwarp();
         unsigned char* box = my_out + buf * CF::kStageOut;
         // row `lane` of the box, 16-byte chunk k stored at chunk k ^ (row & 7) (128B swizzle)
+        if (limb_bits * (L - 1) <= 30) {  // sum_i v_i 2^(b i) as 32 x 32 -> 64-bit multiply-adds
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          uint64_t a0 = 0, a1 = 0;
+          for (int k = 0; k < 8; ++k) {
+            int64_t a0 = (int32_t)v[0][2 * k], a1 = (int32_t)v[0][2 * k + 1];
 #pragma unroll
-          for (int i = 0; i < L; ++i) {
-            a0 += (uint64_t)(int64_t)(int32_t)v[i][2 * k] << (limb_bits * i);
-            a1 += (uint64_t)(int64_t)(int32_t)v[i][2 * k + 1] << (limb_bits * i);
+            for (int i = 1; i < L; ++i) {
+              const int32_t sc = 1 << (limb_bits * i);
+              a0 += (int64_t)(int32_t)v[i][2 * k] * sc;
+              a1 += (int64_t)(int32_t)v[i][2 * k + 1] * sc;
+            }
+            *reinterpret_cast<longlong2*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) = make_longlong2(a0, a1);
           }
-          *reinterpret_cast<ulonglong2*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) = make_ulonglong2(a0, a1);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            uint64_t a0 = 0, a1 = 0;
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+              a0 += (uint64_t)(int64_t)(int32_t)v[i][2 * k] << (limb_bits * i);
+              a1 += (uint64_t)(int64_t)(int32_t)v[i][2 * k + 1] << (limb_bits * i);
+            }
+            *reinterpret_cast<ulonglong2*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) = make_ulonglong2(a0, a1);
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -412,7 +445,36 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
               : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        buf = (buf + 1) % CF::kOutBufs;
+      };
+#pragma unroll
+      for (int i = 0; i < L; ++i) tmem_ld16(tacc + i * BN + cb, vs[0][i]);
+#pragma unroll
+      for (int ci = 0; ci < kNch; ++ci) {
+        uint32_t(&v)[L][16] = vs[kPipe ? (ci & 1) : 0];
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < L; ++i)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(v[i][j]));  // uses stay after the wait
+        if (kPipe && ci + 1 < kNch) {
+#pragma unroll
+          for (int i = 0; i < L; ++i) tmem_ld16(tacc + i * BN + cb + 16 * (ci + 1), vs[(ci + 1) & 1][i]);
+        }
+        if (ci + 1 == kNch) {
+          // last TMEM read of this tile for this warp: release the accumulators
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[ab])) : "memory");
+        }
+        stage(v, cb + 16 * ci);
+        if (!kPipe && ci + 1 < kNch) {
+#pragma unroll
+          for (int i = 0; i < L; ++i) tmem_ld16(tacc + i * BN + cb + 16 * (ci + 1), vs[0][i]);
+        }
       }
+      if (dbg.trace && ew == 0 && lane == 0 && tile < 32) dbg.trace[(blockIdx.x * 32 + tile) * 4 + 1] = globaltimer();
       if constexpr (CHK > 0) {
         // publish this delta tile: bulk stores complete and ordered before
         // the generic-proxy reads of the CTA that checks the tile
@@ -544,8 +606,11 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
     if (CHK > 0) return NE_ENOTSUP;
   }
   if (nclusters > n_work) nclusters = n_work;
+  if (g_max_clusters > 0 && nclusters > g_max_clusters) nclusters = g_max_clusters;
   lc.gridDim = dim3((unsigned)(nclusters * CL));
-  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, ca, geo) != cudaSuccess) return NE_ECUDA;
+  const DbgArgs dbg{g_trace};
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, ca, geo, dbg) != cudaSuccess)
+    return NE_ECUDA;
   return launch_status();
 }
 
@@ -586,6 +651,11 @@ static ne_status gemm_tc_dispatch(int M, int L, int b, const int8_t* planes, con
       return tc::run<4, 128, 4, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
     default: return NE_ENOTSUP;
   }
+}
+
+void gemm_trace(long long* buf, int max_clusters) {
+  tc::g_trace = buf;
+  tc::g_max_clusters = max_clusters;
 }
 
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,

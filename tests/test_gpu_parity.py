@@ -446,6 +446,43 @@ def test_gemm_tc_i8(O, M, L, bound, rows, cols, K):
     assert ne.diag_read(diag)["fault_positions"] == 0
 
 
+@pytest.mark.parametrize("max_clusters", [1, 3])
+def test_gemm_capped_persistent_grid_and_trace(O, max_clusters):
+    """The persistent scheduler with a capped grid (every CTA walks many work
+    items, across both TMEM/stage phases) stays bit-exact; the debug trace
+    (ne_gemm_trace) records, per CTA, accumulator-complete and epilogue-end
+    times that are ordered within and across tiles."""
+    M = 3
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L, b = ne.ne_gemm_limb_plan(cfg, 127)
+    R, Cc, K = 640, 1024, 384
+    A = gen(O, 50, 4, M, R * K, -127, 128)
+    B = O.gen_uniform(50, 5, 0, -128, 128, K * Cc)
+    planes = torch.empty(M * L * R * K, dtype=torch.int8, device="cuda")
+    ne.ne_entangle_limbs(cfg, to_streams(A), L, planes, limb_bits=b)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    tr = torch.zeros(2 * max_clusters * 32 * 4, dtype=torch.int64, device="cuda")
+    out = empty_streams(M, R * Cc)
+    ne.ne_gemm_trace(tr, max_clusters)
+    try:
+        ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, limb_bits=b)
+        torch.cuda.synchronize()
+    finally:
+        ne.ne_gemm_trace(None, 0)
+    ref = O.op_gemm(ocfg, O.entangle(ocfg, A).reshape(M, R, K), B.reshape(K, Cc)).reshape(M, -1)
+    assert (to_np(out) == ref).all()
+    t = tr.view(2 * max_clusters, 32, 4).cpu().numpy()
+    n_items = M * (R // 128) * (Cc // 512)  # cluster work items (CTA pairs, 2 x 256 columns)
+    for cta in range(2 * max_clusters):
+        rows = [r for r in t[cta] if r[0] > 0]
+        assert len(rows) == min(32, -(-(n_items - cta // 2) // max_clusters))
+        for i, r in enumerate(rows):
+            assert r[2] <= r[0] <= r[1]          # MMA start <= accumulators full <= epilogue end
+            if i:
+                assert rows[i - 1][0] <= r[2]   # single TMEM set: next tile starts after the previous is full
+
+
 # ------------------------------------------------------------------ one-stream-per-GPU entry points (C5)
 @pytest.mark.parametrize("M,L,bound", [(8, 2, 32), (3, 4, 64)])
 def test_entangle_limbs_stream_and_gemm_stream(O, M, L, bound):
