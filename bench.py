@@ -927,15 +927,29 @@ def run_c5(args, rank, world, local_rank):
     import torch.distributed as dist
 
     from paper_1604_04740_b200.dist import (C5Plan, GpuBackend, c5_setup, c5_step, c5_step_failstop,
-                                            make_survivor_groups, owned_streams)
+                                            fused_exchange_ok, make_survivor_groups, owned_streams)
 
     torch.cuda.set_device(local_rank)
     plan = C5Plan()
     be = GpuBackend(plan.M, plan.bound)
     groups = make_survivor_groups(world, plan.M)
     inp = c5_setup(be, plan)
+    # exchange: the GEMM epilogue stores each row block into its owner's
+    # symmetric-memory window (fused) when there is something to exchange
+    exchange = args.exchange
+    if exchange == "auto":
+        exchange = "fused" if world > 1 and fused_exchange_ok(plan, world) else "nccl"
+    exchange_note = None
+    if exchange == "fused":
+        try:
+            c5_step(be, plan, inp, groups, exchange="fused")
+            be.stage_ms()
+        except Exception as e:  # symmetric memory unavailable: the all_to_all path (still NCCL over NVLink)
+            if args.exchange == "fused":
+                raise
+            exchange, exchange_note = "nccl", f"fused exchange unavailable ({type(e).__name__}: {e})"[:200]
     for _ in range(args.warmup):
-        c5_step(be, plan, inp, groups)
+        c5_step(be, plan, inp, groups, exchange=exchange)
         be.stage_ms()
     if world > 1:
         dist.barrier()
@@ -947,7 +961,7 @@ def run_c5(args, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        res = c5_step(be, plan, inp, groups, verify=False)
+        res = c5_step(be, plan, inp, groups, verify=False, exchange=exchange)
         flagged += res["flagged"]
     e1.record()
     torch.cuda.synchronize()
@@ -955,7 +969,7 @@ def run_c5(args, rank, world, local_rank):
     for k, v in be.stage_ms().items():
         stage_tot[k] = stage_tot.get(k, 0.0) + v
     # untimed verification step: recovered outputs == checked outputs (checksums)
-    res = c5_step(be, plan, inp, groups, verify=True)
+    res = c5_step(be, plan, inp, groups, verify=True, exchange=exchange)
     be.stage_ms()
     ok = res.get("checksum_ok") in (True, None)
     total_ms = e0.elapsed_time(e1)
@@ -978,7 +992,7 @@ def run_c5(args, rank, world, local_rank):
             inp["A"][m][0].copy_(a, non_blocking=True)
             inp["A"][m][1].copy_(b, non_blocking=True)
         inp["B"].copy_(hB, non_blocking=True)
-        r2 = c5_step(be, plan, inp, groups, verify=False)
+        r2 = c5_step(be, plan, inp, groups, verify=False, exchange=exchange)
         _, dchk = r2["check_slice"]
         if hout is None:
             hout = [torch.empty(t.numel(), dtype=t.dtype).pin_memory() for t in dchk]
@@ -1025,8 +1039,13 @@ def run_c5(args, rank, world, local_rank):
                                "16384x16384x16384 int32 U[-32,32), row block m of A per stream; kill stream 3, "
                                "recover from the other 7",
                    "M": plan.M, "rows_per_stream": plan.rows, "cols": plan.cols, "K": plan.K, "limbs_L": be.L,
-                   "kill": plan.kill, "exchange": "NCCL all_to_all (torch.distributed)" if world > 1 else
-                   "single GPU: all 8 streams local, exchange is a local copy"},
+                   "kill": plan.kill,
+                   "exchange": ("fused: GEMM epilogue TMA-stores each row block into its owner's symmetric-memory "
+                                "window (ne_op_gemm_limbs_scatter), device barrier; recovery exchange NCCL "
+                                "all_to_all among survivors" if exchange == "fused" else
+                                "NCCL all_to_all (torch.distributed)" if world > 1 else
+                                "single GPU: all 8 streams local, nothing to exchange")
+                   + (f"; {exchange_note}" if exchange_note else "")},
         "roofline": {"bound": "tensor", "kernel": "entangle_gemm (k_entangle_limbs_stream + k_gemm_tc)",
                      "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TOP/s",
                      "frac": round(achieved / peak, 4), "traffic": c5_traffic(per_rank_streams),
@@ -1038,7 +1057,7 @@ def run_c5(args, rank, world, local_rank):
                 "unit": "Gop/s", "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         # per rank and step: prep_B, entangle + GEMM per owned stream, diag reset + check, recover
-        "gpu_launches": (1 + 2 * len(mine) + 2 + 1) * args.steps,
+        "gpu_launches": (1 + 2 * len(mine) + 2 + 1) * args.steps,  # (+ the symmetric-memory barrier when fused)
         "clocks": clk.summary(),
         "correctness": {"flagged_positions": flagged, "recovery_checksum_equal": ok},
     }
@@ -1360,6 +1379,9 @@ def main():
                          "survivors re-form the world and recover (dist.c5_step_failstop)")
     ap.add_argument("--failstop-timeout", type=float, default=10.0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--exchange", default="auto", choices=["auto", "fused", "nccl"],
+                    help="c5: position-major exchange fused into the GEMM epilogue (symmetric memory) or an NCCL "
+                         "all_to_all after it; auto = fused when N > 1")
     ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -295,6 +295,25 @@ ne_status ne_op_gemm_limbs_check(const ne_config* cfg, const int8_t* planes, int
                                  int32_t r, ne_streams d_out, uint32_t* bitmap, ne_diag* diag,
                                  int32_t* tile_counters, ne_stream_t stream);
 
+/* ne_op_gemm_limbs_stream with the position-major exchange fused into the
+ * epilogue (C5; one stream per GPU): the output
+ * C_m (rows x cols int64, row-major) is split into ndest row blocks of
+ * rows / ndest rows — exactly the contiguous position chunks j of the check's
+ * all-to-all — and block j is stored by TMA straight into dests.s[j], a
+ * [rows / ndest][cols] int64 region that may live in another GPU's memory
+ * (a peer-mapped / symmetric-memory address reached over NVLink) or locally.
+ * The stores are asynchronous bulk copies issued tile by tile while later
+ * tiles are still being multiplied, so the exchange overlaps the GEMM.  If
+ * C_local is non-NULL the whole C_m is also stored there (rows x cols int64,
+ * local memory): the sender's copy that a recovery exchange among survivors
+ * needs after a fail-stop.  The caller orders the receivers' reads after the
+ * launch (stream order plus a cross-GPU barrier).  ndest in [1, 8],
+ * rows % (128 ndest) == 0 (else NE_ENOTSUP); other shapes and errors as
+ * ne_op_gemm_limbs_stream. */
+ne_status ne_op_gemm_limbs_scatter(const ne_config* cfg, const int8_t* planes_m, int32_t L, int32_t limb_bits,
+                                   const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams dests,
+                                   int32_t ndest, int64_t* C_local, ne_stream_t stream);
+
 /* Debug hook (not on the hot path): every later tensor-core GEMM / Toeplitz
  * conv launch in this process records, for CTA c and its t-th tile (t < 32),
  * the %globaltimer value when the tile's accumulators are complete and when

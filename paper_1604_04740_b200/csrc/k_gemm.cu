@@ -13,6 +13,8 @@ void launch_gemm_imad64(int M, const ne_cstreams& A, const int32_t* B, const ne_
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s);
 void gemm_trace(long long* buf, int max_clusters);
+ne_status launch_gemm_tc_scatter(int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+                                 int64_t K, const ne_streams& dests, int ndest, int64_t* local, cudaStream_t s);
 ne_status launch_gemm_tc_check(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows,
                                int64_t cols, int64_t K, const ne_streams& C, const ne_cstreams& dr,
                                const ne_streams& dor, uint32_t* bitmap, ne_diag* diag, int* cnt, int l,
@@ -195,6 +197,22 @@ extern "C" ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t*
   ne_streams C{};
   C.s[0] = C_m;
   return launch_gemm_tc(1, L, limb_bits, planes_m, Bt, rows, cols, K, C, cs(stream));
+}
+
+extern "C" ne_status ne_op_gemm_limbs_scatter(const ne_config* cfg, const int8_t* planes_m, int32_t L,
+                                              int32_t limb_bits, const int8_t* Bt, int64_t rows, int64_t cols,
+                                              int64_t K, ne_streams dests, int32_t ndest, int64_t* C_local,
+                                              ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (!planes_m || !Bt || L < 1 || L > 4 || limb_bits < 8 || limb_bits > 63 || !aligned16(planes_m) ||
+      !aligned16(Bt) || ndest < 1 || ndest > 8)
+    return NE_EINVAL;
+  for (int j = 0; j < ndest; ++j)
+    if (!dests.s[j] || !aligned16(dests.s[j])) return NE_EINVAL;
+  if (C_local && !aligned16(C_local)) return NE_EINVAL;
+  if (!tc_shape_ok(rows, cols, K) || rows % (128 * (int64_t)ndest) != 0) return NE_ENOTSUP;
+  return launch_gemm_tc_scatter(L, limb_bits, planes_m, Bt, rows, cols, K, dests, ndest, C_local, cs(stream));
 }
 
 extern "C" ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int64_t rows, int64_t cols,

@@ -87,12 +87,20 @@ struct ChkArgs {
 // raster_rows: row tiles fastest in the work order (consecutive clusters
 // share a column group of B instead of a row tile of A) — chosen when B does
 // not fit L2 next to the A operand, so each B panel is read from DRAM ~once.
+// dest_rows (> 0, a multiple of 128; GEMM with M = 1 only): output row block
+// j = row / dest_rows goes to out map j, at row - j * dest_rows — the fused
+// GEMM -> position-major exchange of C5, each map addressing the owner rank's
+// receive buffer (peer memory over NVLink, or local); with dest_local the
+// tile is also stored at its own row through out map 8 (the full local copy
+// that recovery after a fail-stop needs).
 struct Geo {
   int64_t a_plane_rows;
   int64_t out_rows;
   int toeplitz;  // 0, or the Toeplitz output block width W in bytes (= outputs)
   int mcast_b;
   int raster_rows;
+  int64_t dest_rows;
+  int dest_local;
 };
 
 // Debug hook (ne_gemm_trace): per CTA and tile t < 32, %globaltimer when the
@@ -438,11 +446,19 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
+          const int dj = geo.dest_rows > 0 ? (int)(row0 / geo.dest_rows) : m;  // destination map
+          const int64_t drow = geo.dest_rows > 0 ? row0 - dj * geo.dest_rows : row0;
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                  reinterpret_cast<uint64_t>(&outm.m[m])),
-              "r"((int32_t)(col0 + c)), "r"((int32_t)(row0 + 32 * q)), "r"(smem_u32(box))
+                  reinterpret_cast<uint64_t>(&outm.m[dj])),
+              "r"((int32_t)(col0 + c)), "r"((int32_t)(drow + 32 * q)), "r"(smem_u32(box))
               : "memory");
+          if (geo.dest_local)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&outm.m[8])),
+                "r"((int32_t)(col0 + c)), "r"((int32_t)(row0 + 32 * q)), "r"(smem_u32(box))
+                : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         buf = (buf + 1) % CF::kOutBufs;
@@ -574,8 +590,16 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, mcb ? BN / CL : BN)) return NE_ECUDA;
   if (M > 8) return NE_ENOTSUP;
   OutMaps om;
-  for (int m = 0; m < M; ++m)
-    if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)geo.out_rows)) return NE_ECUDA;
+  if (geo.dest_rows > 0) {  // C.s[j]: destination j's [dest_rows][cols] block
+    if (M != 1 || geo.dest_rows % BM != 0 || rows % geo.dest_rows != 0 || rows / geo.dest_rows > 8)
+      return NE_ENOTSUP;
+    for (int j = 0; j < rows / geo.dest_rows; ++j)
+      if (!make_out_map(&om.m[j], C.s[j], (uint64_t)cols, (uint64_t)geo.dest_rows)) return NE_ECUDA;
+    if (geo.dest_local && !make_out_map(&om.m[8], C.s[8], (uint64_t)cols, (uint64_t)rows)) return NE_ECUDA;
+  } else {
+    for (int m = 0; m < M; ++m)
+      if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)geo.out_rows)) return NE_ECUDA;
+  }
   auto kern = k_gemm_tc<L, BN, STAGES, SW, CL, CHK>;
   ChkArgs ca{};
   if (CHK > 0) ca = *chk;
@@ -622,14 +646,15 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
 // whenever the column-tile count is even.
 template <int CHK>
 static ne_status gemm_tc_dispatch(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows,
-                                  int64_t cols, int64_t K, const ne_streams& C, cudaStream_t s, const tc::ChkArgs* chk) {
+                                  int64_t cols, int64_t K, const ne_streams& C, cudaStream_t s, const tc::ChkArgs* chk,
+                                  const tc::Geo* geo = nullptr) {
   const bool pair128 = cols % 256 == 0, pair256 = cols % 512 == 0;
   switch (L) {
     case 1:
       if (CHK > 0) return NE_ENOTSUP;
-      if (pair256) return tc::run<1, 256, 6, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
-      if (cols % 256 == 0) return tc::run<1, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
-      return tc::run<1, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
+      if (pair256) return tc::run<1, 256, 6, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s, nullptr, geo);
+      if (cols % 256 == 0) return tc::run<1, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s, nullptr, geo);
+      return tc::run<1, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s, nullptr, geo);
     case 2:
       // 128-byte K stages (128B swizzle, 3 stages, single-buffered store
       // staging): half the TMA row requests and barrier round trips per MAC
@@ -637,18 +662,18 @@ static ne_status gemm_tc_dispatch(int M, int L, int b, const int8_t* planes, con
       // (long work lists only: with few waves the shallower pipeline's ramp
       // shows — the ABFT checksum GEMM, 3.5 waves, measured 5 % slower)
       if (CHK == 0 && pair256 && K % 128 == 0 && (int64_t)M * (rows / 128) * (cols / 512) >= 6 * (num_sms() / 2))
-        return tc::run<2, 256, 3, 128, 2>(planes, Bt, rows, cols, K, M, b, C, s, chk);
-      if (pair256) return tc::run<2, 256, 5, 64, 2, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk);
-      if (cols % 256 == 0) return tc::run<2, 256, 5, 64, 1, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk);
-      return tc::run<2, 128, 6, 64, 1, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk);
+        return tc::run<2, 256, 3, 128, 2>(planes, Bt, rows, cols, K, M, b, C, s, chk, geo);
+      if (pair256) return tc::run<2, 256, 5, 64, 2, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk, geo);
+      if (cols % 256 == 0) return tc::run<2, 256, 5, 64, 1, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk, geo);
+      return tc::run<2, 128, 6, 64, 1, CHK>(planes, Bt, rows, cols, K, M, b, C, s, chk, geo);
     case 3:
       if (CHK > 0) return NE_ENOTSUP;
-      if (pair128) return tc::run<3, 128, 5, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
-      return tc::run<3, 128, 5, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
+      if (pair128) return tc::run<3, 128, 5, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s, nullptr, geo);
+      return tc::run<3, 128, 5, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s, nullptr, geo);
     case 4:
       if (CHK > 0) return NE_ENOTSUP;  // 4 limb accumulators leave no registers for checker warps
-      if (pair128) return tc::run<4, 128, 4, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s);
-      return tc::run<4, 128, 4, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s);
+      if (pair128) return tc::run<4, 128, 4, 64, 2>(planes, Bt, rows, cols, K, M, b, C, s, nullptr, geo);
+      return tc::run<4, 128, 4, 64, 1>(planes, Bt, rows, cols, K, M, b, C, s, nullptr, geo);
     default: return NE_ENOTSUP;
   }
 }
@@ -661,6 +686,18 @@ void gemm_trace(long long* buf, int max_clusters) {
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s) {
   return gemm_tc_dispatch<0>(M, L, b, planes, Bt, rows, cols, K, C, s, nullptr);
+}
+
+// One stream's GEMM (M = 1) with row block j of the output stored to dests[j]
+// ([rows / ndest][cols] int64 each), and in full to `local` if non-null: the
+// fused GEMM -> exchange of C5.
+ne_status launch_gemm_tc_scatter(int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+                                 int64_t K, const ne_streams& dests, int ndest, int64_t* local, cudaStream_t s) {
+  const int raster = (uint64_t)cols * (uint64_t)K > (48ull << 20) ? 1 : 0;
+  const tc::Geo geo{rows, rows, 0, 0, raster, rows / ndest, local ? 1 : 0};
+  ne_streams d = dests;  // ne_streams holds NE_MAX_M >= 9 pointers
+  d.s[8] = local;
+  return gemm_tc_dispatch<0>(1, L, b, planes, Bt, rows, cols, K, d, s, nullptr, &geo);
 }
 
 // Circular convolution / correlation of M entangled streams as a Toeplitz

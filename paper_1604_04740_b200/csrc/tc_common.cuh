@@ -126,7 +126,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 
 
 struct OutMaps {
-  CUtensorMap m[8];  // C_m as a 2-D int64 tensor [rows][cols], box {16, 32}, 128B swizzle
+  CUtensorMap m[9];  // C_m as a 2-D int64 tensor [rows][cols], box {16, 32}, 128B swizzle
+                     // (scatter mode: m[0..ndest) destinations, m[8] the optional local copy)
 };
 
 // ---------------------------------------------------------------- host side

@@ -77,6 +77,7 @@ class GpuBackend:
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.marks = []
         self._bufs = {}
+        self.symmetric = None  # exchange windows: symmetric memory if world > 1 (None), or forced on/off
 
     def _buf(self, key, n, dtype):
         """Step buffers are allocated once and reused (results of a step stay
@@ -102,6 +103,28 @@ class GpuBackend:
         self.ne.ne_entangle_limbs_stream(self.cfg, m, A_m, A_prev, self.L, planes, self.diag, self.limb_bits)
         out = self._buf(("delta", m), rows * cols, torch.int64)
         self.ne.ne_op_gemm_limbs_stream(self.cfg, planes, self.L, Bt, rows, cols, K, out, self.limb_bits)
+        return out
+
+    def exchange_window(self, n: int) -> "SymmWindow":
+        """Receive window of n int64 per rank in symmetric memory (collective
+        over the world; cached per size)."""
+        key = ("win", n)
+        w = self._bufs.get(key)
+        if w is None:
+            w = SymmWindow(n, self.device, self.symmetric)
+            self._bufs[key] = w
+        return w
+
+    def entangled_gemm_scatter(self, m, A_m, A_prev, Bt, rows, cols, K, dests, keep_local: bool):
+        """Entangle + GEMM of stream m with the position-major exchange fused
+        into the epilogue: row block j of Delta_m is stored straight into
+        dests[j] (receiver j's window, over NVLink); the full Delta_m is also
+        kept locally when a recovery exchange may need it."""
+        planes = self._buf("planes", self.L * rows * K, torch.int8)
+        self.ne.ne_entangle_limbs_stream(self.cfg, m, A_m, A_prev, self.L, planes, self.diag, self.limb_bits)
+        out = self._buf(("delta", m), rows * cols, torch.int64) if keep_local else None
+        self.ne.ne_op_gemm_limbs_scatter(self.cfg, planes, self.L, Bt, rows, cols, K, list(dests), self.limb_bits,
+                                         local=out)
         return out
 
     def check(self, deltas: Sequence[torch.Tensor], r: int):
@@ -135,6 +158,36 @@ class GpuBackend:
                 out[name] = out.get(name, 0.0) + e0.elapsed_time(e1)
         self.marks = []
         return out
+
+
+class SymmWindow:
+    """A per-rank receive window that every rank can store into: torch
+    symmetric memory (peer-mapped over NVLink) when the world has several
+    ranks, a plain local buffer for a single rank.  `peer(j)` is rank j's
+    window as a tensor on this device; `barrier()` is a device-side barrier on
+    the current stream after which every rank's stores into every window are
+    visible."""
+
+    def __init__(self, n: int, device, symmetric: bool | None = None):
+        world = dist.get_world_size() if dist.is_initialized() else 1
+        self.hdl = None
+        if not (symmetric if symmetric is not None else world > 1):
+            self.local = torch.empty(n, dtype=torch.int64, device=device)
+            self.peers = [self.local]
+            return
+        import torch.distributed._symmetric_memory as symm_mem
+
+        group = dist.group.WORLD
+        self.local = symm_mem.empty(n, dtype=torch.int64, device=device)
+        self.hdl = symm_mem.rendezvous(self.local, group.group_name)
+        self.peers = [self.hdl.get_buffer(j, (n,), torch.int64) for j in range(world)]
+
+    def peer(self, j: int) -> torch.Tensor:
+        return self.peers[j]
+
+    def barrier(self):
+        if self.hdl is not None:
+            self.hdl.barrier(channel=0)
 
 
 # ---------------------------------------------------------------- host logic
@@ -261,23 +314,48 @@ def c5_setup(backend, plan: C5Plan) -> dict:
     return inp
 
 
-def c5_step(backend, plan: C5Plan, inp: dict, survivor_groups=None, verify: bool = True) -> dict:
+def fused_exchange_ok(plan: C5Plan, world: int) -> bool:
+    """The fused GEMM -> exchange needs every rank's position chunk to be a
+    whole number of 128-row tiles of each stream's output (and <= 8 ranks)."""
+    return world <= 8 and plan.rows % (128 * world) == 0
+
+
+def c5_step(backend, plan: C5Plan, inp: dict, survivor_groups=None, verify: bool = True,
+            exchange: str = "nccl") -> dict:
     """One C5 step on this rank: entangle + GEMM of the owned streams, exchange,
     check, simulated fail-stop of stream plan.kill and recovery (module doc).
-    Stage boundaries are marked with backend.mark(name) (CUDA events on GPU)."""
+    exchange="fused": the GEMM epilogue stores each row block of Delta_m
+    straight into its owner's receive window (ne_op_gemm_limbs_scatter over
+    symmetric memory) instead of an all_to_all after the GEMM; "nccl": the
+    all_to_all.  Stage boundaries are marked with backend.mark(name) (CUDA
+    events on GPU)."""
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
     M, rows, cols, K = plan.M, plan.rows, plan.cols, plan.K
     mine = owned_streams(M, world, rank)
+    if exchange == "fused" and not fused_exchange_ok(plan, world):
+        raise ValueError(f"fused exchange needs rows per stream ({rows}) divisible by 128 x world ({world})")
 
     backend.mark("start")
     Bt = backend.prep_b(inp["B"], K, cols)
-    deltas = {m: backend.entangled_gemm(m, inp["A"][m][0], inp["A"][m][1], Bt, rows, cols, K) for m in mine}
-    backend.mark("entangle_gemm")
-
-    # position-major exchange over all ranks, then the reliability check (r = 0)
     members = list(range(world))
-    sl = position_major_exchange(deltas, M, members, rank, group=None)
+    if exchange == "fused":
+        # GEMM epilogue -> owner's window: rank j receives [M][chunk] (stream-major)
+        chunk = rows * cols // world
+        win = backend.exchange_window(M * chunk)
+        deltas = {}
+        for m in mine:
+            dests = [win.peer(j)[m * chunk:(m + 1) * chunk] for j in range(world)]
+            deltas[m] = backend.entangled_gemm_scatter(m, inp["A"][m][0], inp["A"][m][1], Bt, rows, cols, K, dests,
+                                                       keep_local=plan.kill is not None)
+        win.barrier()
+        backend.mark("entangle_gemm")
+        sl = {m: win.local[m * chunk:(m + 1) * chunk] for m in range(M)}
+    else:
+        deltas = {m: backend.entangled_gemm(m, inp["A"][m][0], inp["A"][m][1], Bt, rows, cols, K) for m in mine}
+        backend.mark("entangle_gemm")
+        # position-major exchange over all ranks, then the reliability check (r = 0)
+        sl = position_major_exchange(deltas, M, members, rank, group=None)
     lo, _ = chunk_bounds(rows * cols, world)[rank]
     d_chk, flagged = backend.check([sl[m] for m in range(M)], 0)
     backend.mark("exchange_check")
@@ -314,8 +392,8 @@ def c5_step(backend, plan: C5Plan, inp: dict, survivor_groups=None, verify: bool
     return result
 
 
-def c5_run(backend, plan: C5Plan, survivor_groups=None) -> dict:
-    return c5_step(backend, plan, c5_setup(backend, plan), survivor_groups)
+def c5_run(backend, plan: C5Plan, survivor_groups=None, exchange: str = "nccl") -> dict:
+    return c5_step(backend, plan, c5_setup(backend, plan), survivor_groups, exchange=exchange)
 
 
 # ---------------------------------------------------------------- real fail-stop

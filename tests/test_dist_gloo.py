@@ -39,10 +39,12 @@ def _worker(rank, world, port, plans, q):
         results = []
         groups_for = {}
         for plan_kw in plans:
-            plan = C5Plan(**plan_kw)
+            plan = C5Plan(**{k: v for k, v in plan_kw.items() if k != "exchange"})
             if plan.M not in groups_for:
                 groups_for[plan.M] = make_survivor_groups(world, plan.M)
-            res = c5_run(OracleBackend(plan.M, plan.bound), plan, groups_for[plan.M])
+            exchange = plan_kw.get("exchange", "nccl")
+            plan = C5Plan(**{k: v for k, v in plan_kw.items() if k != "exchange"})
+            res = c5_run(OracleBackend(plan.M, plan.bound), plan, groups_for[plan.M], exchange=exchange)
             # expected: plain products A_m B (no entanglement), from the same generator
             M, R, Cc, K, b = plan.M, plan.rows, plan.cols, plan.K, plan.bound
             B = O.gen_uniform(plan.seed, 5, 0, -b, b, K * Cc).reshape(K, Cc)
@@ -114,6 +116,35 @@ def test_c5_ragged_positions_world2(world2):
     and a rank left with no surviving stream after the kill (M = 3, world = 2)."""
     for rank, flagged, cks_ok, ok_check, ok_rec, streams in world2[3]:
         assert flagged == 0 and ok_check and cks_ok is True and ok_rec is True
+
+
+FUSED = dict(M=8, rows_total=8 * 1024, cols=2, K=3, seed=6, bound=32)
+
+
+@pytest.mark.parametrize("world,kill", [(8, 3), (2, 5), (4, None)])
+def test_c5_fused_exchange(world, kill):
+    """exchange="fused": each stream's GEMM stores row block j straight into
+    rank j's receive window (the fused GEMM -> exchange kernel's routing;
+    gloo emulates the peer stores), then check, simulated fail-stop and
+    recovery as in the all_to_all path — every rank's checked and recovered
+    slices equal the plain products."""
+    out = _run(world, [dict(FUSED, kill=kill, exchange="fused")])[0]
+    for rank, flagged, cks_ok, ok_check, ok_rec, streams in out:
+        assert flagged == 0 and ok_check
+        if kill is None:
+            assert cks_ok is None
+        elif world == 8 and rank == kill:
+            assert cks_ok is None and ok_rec is None
+        else:
+            assert cks_ok is True and ok_rec is True
+
+
+def test_fused_exchange_shape_rule():
+    from paper_1604_04740_b200.dist import C5Plan, fused_exchange_ok
+
+    assert fused_exchange_ok(C5Plan(), 8)             # C5: 2048 rows per stream = 8 x 256
+    assert not fused_exchange_ok(C5Plan(rows_total=8 * 384), 8)
+    assert not fused_exchange_ok(C5Plan(), 16)
 
 
 def test_host_partition_helpers():

@@ -505,6 +505,50 @@ def test_entangle_limbs_stream_and_gemm_stream(O, M, L, bound):
         assert (out.cpu().numpy() == ref).all()
 
 
+@pytest.mark.parametrize("M,ndest,R,Cc,K", [(8, 8, 1024, 512, 256), (8, 4, 512, 1024, 384), (3, 2, 256, 768, 128),
+                                           (3, 1, 384, 256, 256), (8, 8, 2048, 1024, 512)])
+def test_gemm_scatter_fused_exchange(O, M, ndest, R, Cc, K):
+    """ne_op_gemm_limbs_scatter: each stream's GEMM stores row block j straight
+    into receiver j's buffer at that stream's slot (the position-major layout
+    the check reads: [M][rows/ndest * cols] per receiver).  Receivers are
+    local buffers here; the kernel only sees addresses (peer memory on a
+    multi-GPU node).  Every receiver slice equals the oracle's product, and so
+    does the optional full local copy."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L, b = ne.ne_gemm_limb_plan(cfg, 32)
+    A = gen(O, 60, 4, M, R * K, -32, 32)
+    B = O.gen_uniform(60, 5, 0, -32, 32, K * Cc)
+    E = O.entangle(ocfg, A)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    chunk = R // ndest * Cc
+    recv = [torch.full((M * chunk,), -7, dtype=torch.int64, device="cuda") for _ in range(ndest)]
+    As = to_streams(A)
+    planes = torch.empty(L * R * K, dtype=torch.int8, device="cuda")
+    local = empty_streams(M, R * Cc)
+    for m in range(M):
+        ne.ne_entangle_limbs_stream(cfg, m, As[m], As[(m - 1) % M], L, planes, limb_bits=b)
+        ne.ne_op_gemm_limbs_scatter(cfg, planes, L, Bt, R, Cc, K, [recv[j][m * chunk:(m + 1) * chunk]
+                                                                  for j in range(ndest)], limb_bits=b,
+                                    local=local[m] if m % 2 else None)
+    ref = O.op_gemm(ocfg, E.reshape(M, R, K), B.reshape(K, Cc)).reshape(M, -1)
+    for m in range(1, M, 2):   # the optional full local copy (what survivors exchange for recovery)
+        assert (local[m].cpu().numpy() == ref[m]).all(), m
+    for j in range(ndest):
+        got = recv[j].view(M, chunk).cpu().numpy()
+        assert (got == ref[:, j * chunk:(j + 1) * chunk]).all(), j
+    # the receiver's slice disentangles and checks clean (what the C5 check runs on)
+    d_out = empty_streams(M, chunk)
+    diag = ne.diag_new()
+    ne.ne_disentangle_check(cfg, [recv[ndest - 1][m * chunk:(m + 1) * chunk] for m in range(M)], 0, d_out, None, diag)
+    plain = (A.reshape(M, R, K) @ B.reshape(K, Cc)).reshape(M, -1)[:, (ndest - 1) * chunk:]
+    assert (to_np(d_out) == plain).all() and ne.diag_read(diag)["fault_positions"] == 0
+    if R % (128 * 2 * ndest) != 0 and 2 * ndest <= 8:
+        with pytest.raises(ne.NeError):   # row blocks that are not whole 128-row tiles: refused
+            ne.ne_op_gemm_limbs_scatter(cfg, planes, L, Bt, R, Cc, K, [recv[0][:chunk // 2]] * (2 * ndest),
+                                        limb_bits=b)
+
+
 def test_c5_orchestration_single_gpu(O):
     """C5's host path on one GPU (world = 1: all 8 streams local), reduced size:
     entangle + tcgen05 GEMM per stream, check, kill stream 3, recover."""
@@ -512,6 +556,46 @@ def test_c5_orchestration_single_gpu(O):
 
     plan = C5Plan(M=8, rows_total=8 * 128, cols=256, K=512, seed=4, bound=32, kill=3)
     res = c5_run(GpuBackend(plan.M, plan.bound), plan)
+    assert res["flagged"] == 0 and res["checksum_ok"] is True
+    B = O.gen_uniform(plan.seed, 5, 0, -32, 32, plan.K * plan.cols).reshape(plan.K, plan.cols)
+    lo, d = res["check_slice"]
+    lo2, d2 = res["recover_slice"]
+    for m in range(plan.M):
+        plain = (O.gen_uniform(plan.seed, 4, m, -32, 32, plan.rows * plan.K).reshape(plan.rows, plan.K) @ B).reshape(-1)
+        assert (d[m].cpu().numpy() == plain).all() and (d2[m].cpu().numpy() == plain).all()
+
+
+@pytest.mark.parametrize("symmetric", [False, True])
+def test_c5_fused_exchange_single_gpu(O, symmetric):
+    """C5 with exchange="fused" on one GPU: each stream's GEMM stores its
+    output through ne_op_gemm_limbs_scatter into the receive window (a plain
+    buffer, or torch symmetric memory rendezvoused over a one-rank NCCL group,
+    the allocation the multi-GPU path stores into over NVLink), keeps the local
+    copy for recovery; check, kill stream 3, recover — all bit-exact."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1604_04740_b200.dist import C5Plan, GpuBackend, c5_run
+
+    own_pg = False
+    if symmetric and not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+        own_pg = True
+    try:
+        plan = C5Plan(M=8, rows_total=8 * 256, cols=512, K=256, seed=4, bound=32, kill=3)
+        be = GpuBackend(plan.M, plan.bound)
+        be.symmetric = symmetric
+        res = c5_run(be, plan, exchange="fused")
+        torch.cuda.synchronize()
+    finally:
+        if own_pg:
+            dist.destroy_process_group()
     assert res["flagged"] == 0 and res["checksum_ok"] is True
     B = O.gen_uniform(plan.seed, 5, 0, -32, 32, plan.K * plan.cols).reshape(plan.K, plan.cols)
     lo, d = res["check_slice"]
