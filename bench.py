@@ -1071,6 +1071,35 @@ def run_c5(args, rank, world, local_rank):
     return line
 
 
+def graph_stage_ms(W, nrot, reps, flush_l2):
+    """Median per-stage device time of the step as a CUDA graph: external
+    event-record nodes between the stages (torch.cuda.Event(external=True))."""
+    import torch
+
+    names = [nm for nm, _ in W.stages(0)]
+    times = {nm: [] for nm in names}
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if flush_l2 else None
+    for i in range(nrot):
+        evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(names) + 1)]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            evs[0].record()
+            for j, (_, f) in enumerate(W.stages(i)):
+                f()
+                evs[j + 1].record()
+        g.replay()
+        torch.cuda.synchronize()
+        for _ in range(reps):
+            if flush is not None:
+                flush.fill_(i & 0xff)
+            g.replay()
+            torch.cuda.synchronize()
+            for j, nm in enumerate(names):
+                times[nm].append(evs[j].elapsed_time(evs[j + 1]))
+        del g
+    return {nm: sorted(v)[len(v) // 2] for nm, v in times.items()}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -1156,6 +1185,13 @@ def run_ours(args, rank, world, local_rank):
             barrier()
             total_ms = g0.elapsed_time(g1)
     clk.stop()
+    eager_stage_ms = stage_ms
+    if args.graph:
+        # per-stage device time inside the replayed step: the same per-r graphs
+        # captured again with event-record nodes between the stages (separate
+        # graphs, so the timed replays above carry no extra nodes); each replay
+        # is synchronised and read, L2 flushed before it when the timed run did
+        stage_ms = graph_stage_ms(W, getattr(W, "M", 1), max(3, min(args.steps, 10)), flush_l2)
     if world > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -1225,6 +1261,9 @@ def run_ours(args, rank, world, local_rank):
                                      "(profiles/traffic.json)" if tr else None,
                      "algorithmic_per_launch": f"{amount:.4g} {unit}", "peak_source": peak_note},
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "stages_timing": ("device time of each stage inside the replayed step graph (event-record nodes, median)"
+                          if args.graph else "eager launches, CUDA events between stages"),
+        "eager_stages_ms": {k: round(v, 4) for k, v in eager_stage_ms.items()},
         "launch": "CUDA graph replay (one graph per recovered stream r)" if args.graph else "eager",
         "eager_ms_per_step": round(eager_ms, 4),
         "e2e": {"value": round(W.work_per_step() * world / (e2e_ms / 1e3), 3), "unit": W.metric_unit,

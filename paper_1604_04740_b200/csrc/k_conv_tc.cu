@@ -208,8 +208,9 @@ k_conv_prep_taps(const int32_t* __restrict__ g, int64_t T, int correlate, int64_
 }
 
 // the last n - W nb outputs of every stream (a partial block): one CTA of
-// 128 threads per output, threads split k, exact int32 digit sums (Kpad 2^14
-// < 2^31) reduced by shuffles and shared memory, recombined in int64
+// 128 threads per output, threads split k in 16-byte pieces (4 dp4a each),
+// exact int32 digit sums (Kpad 2^14 < 2^31) reduced by shuffles and shared
+// memory, recombined in int64
 __global__ void __launch_bounds__(128)
 k_conv_tail(const int8_t* __restrict__ planes, int M, int L, int b, int64_t plane_len, const int8_t* __restrict__ Gt,
             int64_t Kpad, int64_t nb, int W, int64_t n, const __grid_constant__ ne_streams out) {
@@ -218,10 +219,18 @@ k_conv_tail(const int8_t* __restrict__ planes, int M, int L, int b, int64_t plan
   const int m = (int)(blockIdx.x / tail);
   const int64_t i = blockIdx.x % tail;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int4* g = reinterpret_cast<const int4*>(Gt + i * Kpad);  // Kpad % 128 == 0: 16-byte aligned rows
   for (int d = 0; d < L; ++d) {
-    const int8_t* w = planes + ((int64_t)m * L + d) * plane_len + (int64_t)W * nb;
+    const int4* w = reinterpret_cast<const int4*>(planes + ((int64_t)m * L + d) * plane_len + (int64_t)W * nb);
     int32_t s = 0;
-    for (int64_t k = threadIdx.x; k < Kpad; k += 128) s += (int32_t)w[k] * (int32_t)Gt[i * Kpad + k];
+#pragma unroll 4
+    for (int64_t k = threadIdx.x; k < Kpad / 16; k += 128) {
+      const int4 x = __ldg(w + k), y = __ldg(g + k);
+      s = __dp4a(x.x, y.x, s);
+      s = __dp4a(x.y, y.y, s);
+      s = __dp4a(x.z, y.z, s);
+      s = __dp4a(x.w, y.w, s);
+    }
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) part[d][wp] = s;
   }
