@@ -1,3 +1,4 @@
+# Experiment record: the NE_GEMM_TILE hook it drives was removed after the measurement.
 cd $GRAFT_REPO_ROOT
 export PYTHONPATH=.
 for T in 0 1 2; do
