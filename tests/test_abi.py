@@ -148,6 +148,20 @@ def test_argument_validation_of_the_newer_entry_points(L):
     c32 = ne.ne_config_for(3, 32)
     assert L.ne_op_scale_add_check_w32(ctypes.byref(c32), st, 16, 37, None, st, 1, 3, st, None, None, None) == 4
     assert L.ne_entangle_sets_w32(ctypes.byref(cfg), st, 2, 16, st, None, None) == 2      # w = 64 config
+    # fused GEMM -> exchange: destination count, alignment, row blocks of whole tiles
+    P = ctypes.c_void_p
+    assert L.ne_op_gemm_limbs_scatter(ctypes.byref(cfg), P(fake[0]), 2, 22, P(fake[1]), 1024, 256, 256, st, 0,
+                                      None, None) == 1                                  # ndest = 0
+    assert L.ne_op_gemm_limbs_scatter(ctypes.byref(cfg), P(fake[0]), 2, 22, P(fake[1]), 1024, 256, 256, st, 9,
+                                      None, None) == 1                                  # ndest > 8
+    assert L.ne_op_gemm_limbs_scatter(ctypes.byref(cfg), P(fake[0]), 2, 22, P(fake[1]), 1024, 256, 256, st, 7,
+                                      None, None) == 1                                  # dests[6] is NULL
+    assert L.ne_op_gemm_limbs_scatter(ctypes.byref(cfg), P(fake[0]), 2, 22, P(fake[1]), 1024, 256, 256, st, 2,
+                                      P(fake[2] + 8), None) == 1                        # misaligned local copy
+    assert L.ne_op_gemm_limbs_scatter(ctypes.byref(cfg), P(fake[0]), 2, 22, P(fake[1]), 384, 256, 256, st, 2,
+                                      None, None) == 7                                  # 192-row blocks: ENOTSUP
+    assert L.ne_gemm_trace(None, -1) == 1
+    assert L.ne_gemm_trace(None, 0) == 0
 
 
 def test_sass_has_tcgen05_tma_and_tmem(L):
