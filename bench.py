@@ -403,32 +403,39 @@ class C4PermInner(Workload):
     E2E_IN = ("c",)
     E2E_OUT = ("dout",)
 
-    def __init__(self, rank, n=1 << 28, seed=3, layout="aos"):
+    def __init__(self, rank, n=1 << 28, seed=3, layout="aos", w=64):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
-        self.M, self.n, self.B, self.layout = 4, n, 1024, layout
+        self.M, self.n, self.B, self.layout, self.w = 4, n, 1024, layout, w
         if layout != "aos":
             self.name = "C4_soa"
+        # w = 32 containers (NEXT-3): C4's own range (block sums up to 2^34) does
+        # not fit 32 bits, so the w = 32 line uses 7-bit inputs and coefficients
+        # (|block sum| <= 1024 * 64 * 64 = 2^22 < 8 323 072, the M = 4, w = 32 range)
+        self.vr = (1 << 12) if w == 64 else 64
+        if w == 32:
+            self.name = "C4_w32"
         self.seed = seed + 1000 * rank
-        self.cfg = ne.ne_config_for(4)
+        self.cfg = ne.ne_config_for(4, w)
         dev = "cuda"
         self.c = [torch.empty(n, dtype=torch.int32, device=dev) for _ in range(4)]
         for m in range(4):
-            ne.ne_gen_uniform_i32(self.seed, 1, m, -(1 << 12), 1 << 12, self.c[m])
+            ne.ne_gen_uniform_i32(self.seed, 1, m, -self.vr, self.vr, self.c[m])
         self.perm = torch.empty(n, dtype=torch.int32, device=dev)
         ne.ne_gen_perm_i32(self.seed, 6, self.perm)
         self.v = torch.empty(self.B, dtype=torch.int32, device=dev)
-        ne.ne_gen_uniform_i32(self.seed, 7, 0, -(1 << 12), 1 << 12, self.v)
+        ne.ne_gen_uniform_i32(self.seed, 7, 0, -self.vr, self.vr, self.v)
+        wd = torch.int64 if w == 64 else torch.int32
         if layout == "aos":
-            self.eps = torch.empty(n * 4, dtype=torch.int64, device=dev)
+            self.eps = torch.empty(n * 4, dtype=wd, device=dev)
         else:  # SoA: one int64 stream per m (each gathered position touches 4 sectors)
             self.eps = [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(4)]
         self.nb = n // self.B
-        self.delta = [torch.empty(self.nb, dtype=torch.int64, device=dev) for _ in range(4)]
-        self.dout = [torch.empty(self.nb, dtype=torch.int64, device=dev) for _ in range(4)]
-        self.drec = [torch.empty(self.nb, dtype=torch.int64, device=dev) for _ in range(4)]
+        self.delta = [torch.empty(self.nb, dtype=wd, device=dev) for _ in range(4)]
+        self.dout = [torch.empty(self.nb, dtype=wd, device=dev) for _ in range(4)]
+        self.drec = [torch.empty(self.nb, dtype=wd, device=dev) for _ in range(4)]
         self.bitmap = torch.empty((self.nb + 31) // 32, dtype=torch.int32, device=dev)
         self.diag = ne.diag_new()
         self.launches_per_step = 3
@@ -437,6 +444,14 @@ class C4PermInner(Workload):
         ne, cfg = self.ne, self.cfg
         r = i % 4
         part = [None if m == r else self.delta[m] for m in range(4)]
+        if self.w == 32:
+            return [
+                ("entangle", lambda: ne.ne_entangle_aos_w32(cfg, self.c, self.eps, self.diag)),
+                ("permute_inner_check", lambda: ne.ne_op_permute_inner_check_w32(
+                    cfg, self.eps, self.v, self.B, 0, self.dout, perm=self.perm, delta_out=self.delta,
+                    bitmap=self.bitmap, diag=self.diag)),
+                ("recover", lambda: ne.ne_recover_w32(cfg, part, r, self.drec)),
+            ]
         if self.layout != "aos":
             return [
                 ("entangle", lambda: ne.ne_entangle(cfg, self.c, self.eps, self.diag)),
@@ -453,22 +468,34 @@ class C4PermInner(Workload):
             ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
         ]
 
-    def work_per_step(self):  # algorithmic GB per step: entangle 48 B + gather/inner 36 B per position
+    def work_per_step(self):  # algorithmic GB per step: entangle 48 B + gather/inner 36 B per position (w = 64)
+        if self.w == 32:      # entangle 16 + 16 B, gather 16 B + 4 B index
+            return self.n * (32 + 20) / 1e9
         return self.n * (48 + 36) / 1e9
 
     def stage_info(self):
         n, nb = self.n, self.nb
+        if self.w == 32:
+            return {"entangle": ("hbm", n * 32 / 1e9, "GB"),
+                    "permute_inner_check": ("hbm", (n * 20 + nb * 4 * 8) / 1e9, "GB"),
+                    "recover": ("hbm", nb * 7 * 4 / 1e9, "GB")}
         return {"entangle": ("hbm", n * 48 / 1e9, "GB"),
                 "permute_inner_check": ("hbm", (n * 36 + nb * 4 * 16) / 1e9, "GB"),
                 "recover": ("hbm", nb * 7 * 8 / 1e9, "GB")}
 
     def config(self):
-        return {"workload": "C4 (BASELINE configs[3]): M=4 streams of 2^28 int32 U[-2^12,2^12), seeded "
-                            "permutation, inner products with a shared 1024-vector in blocks of 1024",
+        wl = ("C4 (BASELINE configs[3]): M=4 streams of 2^28 int32 U[-2^12,2^12), seeded "
+              "permutation, inner products with a shared 1024-vector in blocks of 1024")
+        if self.w == 32:
+            wl = ("C4 shape at w = 32 (NEXT-3): M=4 streams of 2^28 int32 U[-64,64) (C4's U[-2^12,2^12) "
+                  "does not fit 32-bit containers), seeded permutation, 1024-blocked inner products with a "
+                  "shared U[-64,64) vector")
+        return {"workload": wl,
                 "M": 4, "n": self.n, "block": self.B,
-                "layout": "AoS (position-major) entangled int64" if self.layout == "aos" else
-                          "SoA (one int64 stream per m; 4 random sectors per gathered position)",
-                "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": 64},
+                "layout": ("AoS (position-major) entangled int32 (16 B per position)" if self.w == 32 else
+                           "AoS (position-major) entangled int64" if self.layout == "aos" else
+                           "SoA (one int64 stream per m; 4 random sectors per gathered position)"),
+                "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": self.w},
                 "l2": "working set ~13 GB >> 126 MB L2 (no flush needed)",
                 "step": "entangle(AoS)+gather/inner/disentangle/check fused(r=0)+recover(r=step mod 4)"}
 
@@ -476,7 +503,7 @@ class C4PermInner(Workload):
         """Same gather + inner kernel on plain (unentangled) data in the same
         int64 AoS containers, no check: the paper's conventional routine."""
         torch, ne = self.torch, self.ne
-        if self.layout != "aos":
+        if self.layout != "aos" or self.w != 64:
             return {}
         plain = torch.stack([x.to(torch.int64) for x in self.c], dim=1).reshape(-1).contiguous()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -495,18 +522,19 @@ class C4PermInner(Workload):
     def oracle_sample(self, blocks):
         import oracle as O
 
-        ocfg = O.config_for(4, 64)
-        n, B = self.n, self.B
+        ocfg = O.config_for(4, self.w)
+        n, B, vr = self.n, self.B, self.vr
         t0 = time.perf_counter()
         idx = O.gen_perm(self.seed, 6, n, blocks * B, 0)
-        v = O.gen_uniform(self.seed, 7, 0, -(1 << 12), 1 << 12, B)
-        c = np.stack([np.concatenate([O.gen_uniform(self.seed, 1, m, -(1 << 12), 1 << 12, 1, int(p)) for p in idx])
+        v = O.gen_uniform(self.seed, 7, 0, -vr, vr, B)
+        c = np.stack([np.concatenate([O.gen_uniform(self.seed, 1, m, -vr, vr, 1, int(p)) for p in idx])
                       for m in range(4)])
         eps = O.entangle(ocfg, c)
         delta = O.op_inner(ocfg, eps, v, B)
         O.disentangle_check(ocfg, delta, 0)
         dt = time.perf_counter() - t0
-        return dt, blocks * B * 84 / 1e9, f"{blocks} output blocks of 1024 gathered positions (of {n // B})"
+        return dt, blocks * B * (84 if self.w == 64 else 52) / 1e9, \
+            f"{blocks} output blocks of 1024 gathered positions (of {n // B})"
 
 
 class C2Conv(Workload):
@@ -830,7 +858,7 @@ def make_workload(args, rank):
         return C2Conv(rank, n=10 ** 6, taps=args.taps, M=args.streams, algo=args.conv or "tc", paper=True,
                       scheme=args.scheme)
     if args.workload == "c4":
-        return C4PermInner(rank, layout=args.layout)
+        return C4PermInner(rank, layout=args.layout, w=args.w)
     if args.workload == "c1":
         return C1Chain(rank, n=args.n or 4096, w=args.w, fuse=bool(args.fuse if args.fuse is not None else 1))
     return WORKLOADS[args.workload](rank)
@@ -1250,7 +1278,7 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "int64",
+        "dtype": "int32" if getattr(W, "w", 64) == 32 else "int64",  # the containers' arithmetic (w bits)
         "data": "synthetic (counter-based splitmix64 generator, gen/ne_gen.h; no dataset)",
         "config": dict(W.config(), **({"l2": "working set < L2: a 512 MB write flushes L2 before every timed "
                                                    "step, outside that step's CUDA events (per-step timing)"}
@@ -1325,10 +1353,11 @@ def run_reference(args):
             l, k = 22, 20
         W.cfg = _Cfg
     elif args.workload == "c4":
-        W.M, W.n, W.B, W.seed, W.layout = 4, 1 << 28, 1024, 3, args.layout
+        W.M, W.n, W.B, W.seed, W.layout, W.w = 4, 1 << 28, 1024, 3, args.layout, args.w
+        W.vr = (1 << 12) if args.w == 64 else 64
 
         class _Cfg:
-            l, k = 16, 16
+            l, k = (16, 16) if args.w == 64 else (8, 8)
         W.cfg = _Cfg
     elif args.workload == "c5":
         from paper_1604_04740_b200.dist import C5Plan
@@ -1410,7 +1439,7 @@ def main():
     ap.add_argument("--taps", type=int, default=4500, help="c2p: kernel taps (paper: 100-4500)")
     ap.add_argument("--streams", type=int, default=8, help="c2p / c3p: M (paper: 3 or 8)")
     ap.add_argument("--kdim", type=int, default=2000, help="c3p: N, the inner dimension (paper: 200-2000)")
-    ap.add_argument("--w", type=int, default=64, choices=[64, 32], help="c1: container width (P:528-530)")
+    ap.add_argument("--w", type=int, default=64, choices=[64, 32], help="c1 / c4: container width (P:528-530)")
     ap.add_argument("--layout", default="aos", choices=["aos", "soa"], help="c4: entangled layout at rest")
     ap.add_argument("--n", type=int, default=None, help="c1: stream length (default 4096 = configs[0])")
     ap.add_argument("--failstop", default="simulated", choices=["simulated", "exit"],

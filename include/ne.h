@@ -430,6 +430,22 @@ ne_status ne_recover_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t n_to
  * flagwords / dhat: M*window*32 entries (dhat times M, int32). */
 ne_status ne_inject_sweep_w32(const ne_config* cfg, ne_cstreams32 delta, int64_t window, int32_t r,
                               uint64_t* flagwords, int32_t* dhat, ne_stream_t stream);
+/* The C4 class at w = 32 (permute + inner, where the range
+ * allows: every block sum must lie inside ne_dynamic_range).  AoS containers
+ * x_aos[n*M + m] = eps_m[n] (int32; M = 4: 16 bytes per position, one 128-bit
+ * load in the random gather).  ne_entangle_aos_w32: Eq. 15 mod 2^32, inputs
+ * outside the dynamic range counted as in ne_entangle_w32 (first_bad =
+ * m*N + n).  ne_op_permute_inner_check_w32: for block b,
+ * delta_m[b] = sum_{i<block} x_m[perm[b*block+i]] * v[i mod vlen] mod 2^32
+ * (perm NULL = identity), then d_out / bitmap / diag exactly as
+ * ne_disentangle_check_w32 on delta (r excluded); delta_out (nullable)
+ * receives delta.  n_total <= INT32_MAX; NE_EINDEX if r outside [0, M). */
+ne_status ne_entangle_aos_w32(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t* x_aos,
+                              ne_diag* diag, ne_stream_t stream);
+ne_status ne_op_permute_inner_check_w32(const ne_config* cfg, const int32_t* x_aos, const int32_t* perm,
+                                        int64_t n_total, const int32_t* v, int64_t vlen, int64_t block,
+                                        int32_t r, ne_streams32 delta_out, ne_streams32 d_out,
+                                        uint32_t* bitmap, ne_diag* diag, ne_stream_t stream);
 
 /* ============================================== a7: fault injection (test) === */
 

@@ -37,6 +37,7 @@ EXPORTS = (
     "ne_conv_geometry", "ne_entangle_limbs_conv", "ne_conv_prep_taps", "ne_op_conv_limbs",
     "ne_op_scale_add_check", "ne_op_conv_check", "ne_op_scale_add_check_w32",
     "ne_entangle_w32", "ne_op_scale_add_w32", "ne_disentangle_check_w32", "ne_recover_w32", "ne_inject_sweep_w32",
+    "ne_entangle_aos_w32", "ne_op_permute_inner_check_w32",
     "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
     "ne_abft_encode", "ne_abft_encode_limbs", "ne_abft_encode_conv", "ne_op_conv_limbs_plain", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
@@ -100,6 +101,8 @@ _SIGS = {
     "ne_disentangle_check_w32": [_PCFG, Streams, _I64, _I32, Streams, _VP, _VP, _VP],
     "ne_recover_w32": [_PCFG, Streams, _I64, _I32, Streams, _VP],
     "ne_inject_sweep_w32": [_PCFG, Streams, _I64, _I32, _VP, _VP, _VP],
+    "ne_entangle_aos_w32": [_PCFG, Streams, _I64, _VP, _VP, _VP],
+    "ne_op_permute_inner_check_w32": [_PCFG, _VP, _VP, _I64, _VP, _I64, _I64, _I32, Streams, Streams, _VP, _VP, _VP],
     "ne_conv_geometry": [_I64, _I32, _I32, C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I64)],
     "ne_entangle_limbs_conv": [_PCFG, Streams, _I64, _I32, _I32, _I32, _I32, _I32, _VP, _VP, _VP],
     "ne_conv_prep_taps": [_VP, _I32, _I32, _I32, _VP, _VP, _VP],
@@ -374,6 +377,21 @@ def ne_disentangle_check_w32(cfg: Config, delta, r: int, d_out, bitmap: torch.Te
 def ne_recover_w32(cfg: Config, delta, r: int, d_out) -> None:
     n = next(t for t in delta if t is not None).numel()
     _call("ne_recover_w32", C.byref(cfg), _streams(delta, torch.int32), n, r, _streams(d_out, torch.int32), _stream())
+
+
+def ne_entangle_aos_w32(cfg: Config, c, x_aos: torch.Tensor, diag=None) -> None:
+    """w = 32 AoS containers: x_aos[n*M + m] = eps_m[n] (int32)."""
+    _call("ne_entangle_aos_w32", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), _ptr(x_aos, torch.int32),
+          _ptr(diag, torch.int64), _stream())
+
+
+def ne_op_permute_inner_check_w32(cfg: Config, x_aos: torch.Tensor, v: torch.Tensor, block: int, r: int, d_out,
+                                  perm: torch.Tensor | None = None, delta_out=None, bitmap: torch.Tensor | None = None,
+                                  diag=None) -> None:
+    n = x_aos.numel() // cfg.M
+    _call("ne_op_permute_inner_check_w32", C.byref(cfg), _ptr(x_aos, torch.int32), _ptr(perm, torch.int32), n,
+          _ptr(v, torch.int32), v.numel(), block, r, _streams(delta_out or [], torch.int32),
+          _streams(d_out, torch.int32), _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _stream())
 
 
 def ne_inject_sweep_w32(cfg: Config, delta, window: int, r: int, flagwords: torch.Tensor, dhat: torch.Tensor) -> None:

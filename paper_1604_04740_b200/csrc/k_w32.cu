@@ -292,6 +292,190 @@ k_inject_sweep_w32(const __grid_constant__ ne_cstreams32 e, int M_rt, int l, int
   }
 }
 
+
+// ---- C4 class at w = 32 (NEXT-3: permute + inner where the range allows) ----
+// AoS containers x_aos[p * M + m] (int32): with M = 4 one position is 16
+// bytes, one 128-bit load in the random gather (half the w = 64 AoS bytes).
+template <int MT, bool V4 = false>
+__global__ void __launch_bounds__(kThreads)
+k_entangle_aos_w32(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n,
+                   int32_t* __restrict__ x_aos, ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  int bad = 0;
+  long long first = LLONG_MAX;
+  if (MT == 4 && V4) {
+    // 4 positions per thread: one 128-bit load per stream, four 128-bit stores
+    const int64_t nq = n / 4;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+      int32_t cv[4][4];  // [stream][position]
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int4 t = __ldcs(reinterpret_cast<const int4*>(c.s[m]) + q);
+        cv[m][0] = t.x; cv[m][1] = t.y; cv[m][2] = t.z; cv[m][3] = t.w;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (cv[m][u] > hi || cv[m][u] < -hi) {
+            ++bad;
+            const long long idx = (long long)m * n + 4 * q + u;
+            first = idx < first ? idx : first;
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t e[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) e[m] = (uint32_t)cv[m][u] + ((uint32_t)cv[(m + 3) & 3][u] << l);
+        __stcs(reinterpret_cast<uint4*>(x_aos) + 4 * q + u, make_uint4(e[0], e[1], e[2], e[3]));
+      }
+    }
+    if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+    return;
+  }
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    int32_t cv[MA];
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+      if (MT == 0 && m >= M) break;
+      cv[m] = __ldcs(c.s[m] + p);
+      if (cv[m] > hi || cv[m] < -hi) {
+        ++bad;
+        const long long idx = (long long)m * n + p;
+        first = idx < first ? idx : first;
+      }
+    }
+    uint32_t e[MA];
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {  // Eq. 15: eps_m = c_m + 2^l c_{m-1}, mod 2^32
+      if (MT == 0 && m >= M) break;
+      e[m] = (uint32_t)cv[m] + ((uint32_t)cv[m == 0 ? M - 1 : m - 1] << l);
+    }
+    if (MT == 4) {
+      *reinterpret_cast<uint4*>(x_aos + p * 4) = make_uint4(e[0], e[1], e[2], e[3]);
+    } else {
+#pragma unroll
+      for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+        if (MT == 0 && m >= M) break;
+        x_aos[p * M + m] = (int32_t)e[m];
+      }
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// permutation gather + blocked inner product + disentangle/check, w = 32:
+// one warp per output block, a CTA of 8 warps owns 32 blocks (one bitmap
+// word); sums wrap mod 2^32 (the w-bit container arithmetic); the check runs
+// Eqs. 16-19 + 21 with int64 temporaries (disentangle_rot32).
+constexpr int kPiBlocks = 32, kPiWarps = 8, kPiU = 8;
+
+template <int MT>
+__global__ void __launch_bounds__(kPiWarps * 32)
+k_pinner_w32(const int32_t* __restrict__ x_aos, int M_rt, int l, const int32_t* __restrict__ perm, int64_t n,
+             const int32_t* __restrict__ v, int64_t vlen, int64_t block, const __grid_constant__ ne_streams32 delta_out,
+             const __grid_constant__ ne_streams32 d_rot, int r, uint32_t* __restrict__ bitmap,
+             ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nb = (n + block - 1) / block;
+  __shared__ uint32_t s_flags;
+  if (threadIdx.x == 0) s_flags = 0;
+  __syncthreads();
+  const int64_t b_first = (int64_t)blockIdx.x * kPiBlocks;
+  int nflag = 0;
+  long long first = LLONG_MAX;
+  for (int bi = warp; bi < kPiBlocks; bi += kPiWarps) {
+    const int64_t b = b_first + bi;
+    if (b >= nb) break;
+    const int64_t p_begin = b * block;
+    const int64_t p_end = p_begin + block < n ? p_begin + block : n;
+    uint32_t acc[MA];
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) acc[m] = 0;
+    for (int64_t p0 = p_begin + lane; p0 < p_end; p0 += 32 * kPiU) {
+      int64_t idx[kPiU];
+      uint32_t coef[kPiU];
+#pragma unroll
+      for (int u = 0; u < kPiU; ++u) {
+        const int64_t p = p0 + 32 * u;
+        const bool ok = p < p_end;
+        idx[u] = ok ? (perm ? (int64_t)__ldcs(perm + p) : p) : -1;
+        coef[u] = ok ? (uint32_t)__ldg(v + (vlen == block ? p - p_begin : p % vlen)) : 0u;
+      }
+      if (MT == 4) {
+        uint32_t q[kPiU][4];
+#pragma unroll
+        for (int u = 0; u < kPiU; ++u) {
+          if (idx[u] >= 0) {
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(q[u][0]), "=r"(q[u][1]), "=r"(q[u][2]), "=r"(q[u][3])
+                         : "l"(x_aos + idx[u] * 4));
+          } else {
+            q[u][0] = q[u][1] = q[u][2] = q[u][3] = 0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kPiU; ++u)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) acc[m] += q[u][m] * coef[u];
+      } else {
+#pragma unroll
+        for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+          if (MT == 0 && m >= M) break;
+          uint32_t val[kPiU];
+#pragma unroll
+          for (int u = 0; u < kPiU; ++u) val[u] = idx[u] >= 0 ? (uint32_t)__ldcs(x_aos + idx[u] * M + m) : 0u;
+#pragma unroll
+          for (int u = 0; u < kPiU; ++u) acc[m] += val[u] * coef[u];
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+      if (MT == 0 && m >= M) break;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], o);
+    }
+    if (lane == 0) {
+      if (delta_out.s[0]) {
+#pragma unroll
+        for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m) {
+          if (MT == 0 && m >= M) break;
+          delta_out.s[m][b] = (int32_t)acc[m];
+        }
+      }
+      int64_t e[MA];  // rotated frame: e[j] = delta_{(r+j) mod M}, the w-bit words sign-extended
+      int32_t d[MA];
+#pragma unroll
+      for (int j = 0; j < (MT > 0 ? MT : NE_MAX_M); ++j) {
+        if (MT == 0 && j >= M) break;
+        int src = r + j;
+        if (src >= M) src -= M;
+        uint32_t a = 0;
+#pragma unroll
+        for (int m = 0; m < (MT > 0 ? MT : NE_MAX_M); ++m)
+          if (m == src) a = acc[m];
+        e[j] = (int64_t)(int32_t)a;
+      }
+      const bool f = disentangle_rot32<MT>(e, M, l, d, true);
+#pragma unroll
+      for (int j = 0; j < (MT > 0 ? MT : NE_MAX_M); ++j) {
+        if (MT == 0 && j >= M) break;
+        d_rot.s[j][b] = d[j];
+      }
+      if (f) {
+        atomicOr(&s_flags, 1u << bi);
+        ++nflag;
+        first = b < first ? b : first;
+      }
+    }
+  }
+  if (diag) diag_add(&diag->fault_positions, &diag->first_fault, nflag, first);
+  __syncthreads();
+  if (threadIdx.x == 0 && bitmap && b_first < nb) bitmap[blockIdx.x] = s_flags;
+}
+
 }  // namespace ne
 
 using namespace ne;
@@ -431,5 +615,48 @@ extern "C" ne_status ne_inject_sweep_w32(const ne_config* cfg, ne_cstreams32 del
   const int64_t trials = (int64_t)cfg->M * window * 32;
   NE_W32_M(cfg->M, k_inject_sweep_w32, grid_for(trials * 32, kThreads), cs(stream), rotate(delta, cfg->M, r), cfg->M,
            cfg->l, r, window, flagwords, dhat);
+  return launch_status();
+}
+
+extern "C" ne_status ne_entangle_aos_w32(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, int32_t* x_aos,
+                                         ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg32(cfg);
+  if (st != NE_OK) return st;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || !ok32(c, cfg->M) || !x_aos || !aligned16(x_aos)) return NE_EINVAL;
+  cudaStream_t s = cs(stream);
+  if (cfg->M == 4 && n_total % 4 == 0) {  // streams 16-B aligned (ok32): vectorised form
+    k_entangle_aos_w32<4, true><<<grid_for(n_total / 4, kThreads), kThreads, 0, s>>>(c, 4, cfg->l, range_hi(cfg),
+                                                                                     n_total, x_aos, diag);
+    return launch_status();
+  }
+  const int grid = grid_for(n_total, kThreads);
+  NE_W32_M(cfg->M, k_entangle_aos_w32, grid, s, c, cfg->M, cfg->l, range_hi(cfg), n_total, x_aos, diag);
+  return launch_status();
+}
+
+extern "C" ne_status ne_op_permute_inner_check_w32(const ne_config* cfg, const int32_t* x_aos, const int32_t* perm,
+                                                   int64_t n_total, const int32_t* v, int64_t vlen, int64_t block,
+                                                   int32_t r, ne_streams32 delta_out, ne_streams32 d_out,
+                                                   uint32_t* bitmap, ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg32(cfg);
+  if (st != NE_OK) return st;
+  const int M = cfg->M;
+  if (r < 0 || r >= M) return NE_EINDEX;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || n_total > INT32_MAX || block < 1 || vlen < 1 || !v || !x_aos || !aligned16(x_aos) ||
+      !ok32(d_out, M))
+    return NE_EINVAL;
+  if (delta_out.s[0] && !ok32(delta_out, M)) return NE_EINVAL;
+  const int64_t nb = (n_total + block - 1) / block;
+  const int grid = (int)((nb + kPiBlocks - 1) / kPiBlocks);
+  const ne_streams32 drot = rotate(d_out, M, r);
+  cudaStream_t s = cs(stream);
+  switch (M) {
+    case 3: k_pinner_w32<3><<<grid, kPiWarps * 32, 0, s>>>(x_aos, M, cfg->l, perm, n_total, v, vlen, block, delta_out, drot, r, bitmap, diag); break;
+    case 4: k_pinner_w32<4><<<grid, kPiWarps * 32, 0, s>>>(x_aos, M, cfg->l, perm, n_total, v, vlen, block, delta_out, drot, r, bitmap, diag); break;
+    case 8: k_pinner_w32<8><<<grid, kPiWarps * 32, 0, s>>>(x_aos, M, cfg->l, perm, n_total, v, vlen, block, delta_out, drot, r, bitmap, diag); break;
+    default: k_pinner_w32<0><<<grid, kPiWarps * 32, 0, s>>>(x_aos, M, cfg->l, perm, n_total, v, vlen, block, delta_out, drot, r, bitmap, diag); break;
+  }
   return launch_status();
 }

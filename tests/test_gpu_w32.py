@@ -7,7 +7,7 @@ import pytest
 import torch
 
 import paper_1604_04740_b200 as ne
-from _gpu import bitmap_to_flags, to_np, to_streams
+from _gpu import bitmap_to_flags, dev, to_np, to_streams
 
 pytestmark = pytest.mark.gpu
 
@@ -200,3 +200,89 @@ def test_w32_entangle_sets(O, M, sets, N):
     ne.ne_entangle_sets_w32(cfg, to_streams(c), sets, eps, diag)
     d = ne.diag_read(diag)
     assert d["range_violations"] == 1 and d["first_bad"] == (M + 2) * N + 7
+
+
+# ------------------------------------------------------------------ C4 class at w = 32
+@pytest.mark.parametrize("M,N", [(4, 4096 + 3), (4, 4096), (4, 65536 + 4), (3, 1000), (8, 515), (5, 129)])
+def test_w32_entangle_aos(O, M, N):
+    """x_aos[n*M + m] = eps_m[n] (Eq. 15 mod 2^32), range violations named."""
+    cfg, ocfg = ne.ne_config_for(M, 32), O.config_for(M, 32)
+    hi = ne.ne_dynamic_range(cfg)
+    c = gen(O, 30, 1, M, N, -hi, hi + 1)
+    c[:, 0], c[:, 1] = hi, -hi
+    x = torch.empty(N * M, dtype=torch.int32, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_aos_w32(cfg, to_streams(c), x, diag)
+    assert (x.view(N, M).cpu().numpy().T.astype(np.int64) == O.entangle(ocfg, c)).all()
+    assert ne.diag_read(diag)["range_violations"] == 0
+    c[M - 1, N - 1] = hi + 1
+    ne.ne_entangle_aos_w32(cfg, to_streams(c), x, diag)
+    d = ne.diag_read(diag)
+    assert d["range_violations"] == 1 and d["first_bad"] == (M - 1) * N + N - 1
+
+
+@pytest.mark.parametrize("M", [4, 3, 8, 5])
+@pytest.mark.parametrize("gather", [True, False])
+@pytest.mark.parametrize("vlen_eq_block", [True, False])
+def test_w32_permute_inner_check(O, M, gather, vlen_eq_block):
+    """Gather + blocked inner product + disentangle/check in w = 32 AoS
+    containers: block sums (mod 2^32), d_hat, bitmap and diag equal the
+    oracle's, and d_hat equals the plain inner products of the permuted c."""
+    cfg, ocfg = ne.ne_config_for(M, 32), O.config_for(M, 32)
+    hi = ne.ne_dynamic_range(cfg)
+    B = 256
+    vlen = B if vlen_eq_block else 96
+    N = B * 37 + 100
+    vb = 16
+    cb = max(1, hi // (B * vb))          # every block sum inside the dynamic range
+    c = gen(O, 31, 1, M, N, -cb, cb + 1)
+    v = O.gen_uniform(31, 7, 0, -vb, vb + 1, vlen)
+    perm = O.gen_perm(31, 6, N)
+    E = O.entangle(ocfg, c)
+    x = dev(E.T.copy(), torch.int32).reshape(-1)
+    nb = (N + B - 1) // B
+    d_out = [torch.empty(nb, dtype=torch.int32, device="cuda") for _ in range(M)]
+    delta = [torch.empty(nb, dtype=torch.int32, device="cuda") for _ in range(M)]
+    bm = torch.full(((nb + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+    diag = ne.diag_new()
+    r = 1 % M
+    ne.ne_op_permute_inner_check_w32(cfg, x, dev(v, torch.int32), B, r, d_out,
+                                     perm=dev(perm, torch.int32) if gather else None, delta_out=delta, bitmap=bm,
+                                     diag=diag)
+    p = perm if gather else np.arange(N)
+    odelta = O.op_inner(ocfg, O.op_permute(E, p), v, B)
+    assert (to_np(delta) == odelta).all()
+    od, oflags, onf = O.disentangle_check(ocfg, odelta, r)
+    assert (to_np(d_out) == od).all()
+    assert (od == O.op_inner(O.config_for(M, 64), c[:, p], v, B)).all()
+    assert (bitmap_to_flags(bm, nb) == oflags).all() and onf == 0
+    assert ne.diag_read(diag)["fault_positions"] == 0
+
+
+def test_w32_permute_inner_detects_storage_fault(O):
+    """Single-stream faults in stored w = 32 words are flagged in their blocks;
+    d_hat and flags equal the oracle's on the corrupted containers."""
+    M, B = 4, 1024
+    N = B * 64
+    cfg, ocfg = ne.ne_config_for(M, 32), O.config_for(M, 32)
+    c = gen(O, 32, 1, M, N, -64, 64)
+    v = O.gen_uniform(32, 7, 0, -64, 64, B)
+    perm = O.gen_perm(32, 6, N)
+    x = O.entangle(ocfg, c).T.copy()
+    hit = [(5, 2, 1 << 20), (40000 % N, 0, 1), (N - 1, 3, 1 << 31)]
+    for pos, s, mask in hit:
+        x[pos, s] = O.wrap(ocfg, int(x[pos, s]) ^ mask)
+    nb = N // B
+    d_out = [torch.empty(nb, dtype=torch.int32, device="cuda") for _ in range(M)]
+    bm = torch.empty(nb // 32, dtype=torch.int32, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_op_permute_inner_check_w32(cfg, dev(x, torch.int32).reshape(-1), dev(v, torch.int32), B, 0, d_out,
+                                     perm=dev(perm, torch.int32), bitmap=bm, diag=diag)
+    inv = np.argsort(perm)
+    blocks = sorted({int(inv[pos]) // B for pos, _, _ in hit})
+    flags = bitmap_to_flags(bm, nb)
+    assert list(np.flatnonzero(flags)) == blocks
+    odelta = O.op_inner(ocfg, O.op_permute(np.ascontiguousarray(x.T), perm), v, B)
+    od, oflags, _ = O.disentangle_check(ocfg, odelta, 0)
+    assert (to_np(d_out) == od).all() and (oflags == flags).all()
+    assert ne.diag_read(diag)["fault_positions"] == len(blocks)
