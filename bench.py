@@ -1235,6 +1235,13 @@ def run_ours(args, rank, world, local_rank):
         rec_ok = bool(torch.equal(W.drec[r_last], W.delta[r_last]))
     else:
         rec_ok = all(bool(torch.equal(a, b)) for a, b in zip(W.drec, W.dout))
+    if world > 1:
+        # every rank's fault / range counters and recovery verdict (all_reduce of the counters)
+        t = torch.tensor([dg["range_violations"], dg["fault_positions"], 0 if rec_ok else 1], device="cuda",
+                         dtype=torch.int64)
+        dist.all_reduce(t)
+        dg = dict(dg, range_violations=int(t[0].item()), fault_positions=int(t[1].item()))
+        rec_ok = int(t[2].item()) == 0
 
     # end to end through host buffers: pinned H2D inputs, D2H results, every
     # step, pipelined over three CUDA streams (Workload.e2e_pipeline)
