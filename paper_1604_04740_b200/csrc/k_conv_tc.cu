@@ -66,6 +66,10 @@ k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l,
       pos[u] = p;
       if (++p == n) p = 0;
     }
+    // which of the 4 t are counted by the range assertion (t in [s0, s0 + N))
+    bool tin[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tin[u] = 4 * q + u >= s0 && 4 * q + u < s0 + n;
     // streams in order with only the previous one live (registers: the M = 8
     // instantiation stays at full occupancy); c_{M-1} first, the "previous"
     // stream of stream 0 (circulant Eq. 14)
@@ -77,31 +81,42 @@ k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l,
 #pragma unroll
       for (int u = 0; u < 4; ++u) cur[u] = __ldg(c.s[m] + pos[u]);
       uint32_t w[4] = {0, 0, 0, 0};
+      unsigned badm = 0;  // bit u: position u out of range / not representable
+      if (pair) {
+        // the two-digit base-2^l plan in 32-bit arithmetic (as k_entangle_pair):
+        // d0 = sext_b(c), d1 = c_prev + (c >> b) + bit_{b-1}(c); packed 4 bytes at a time
+        int32_t d0[4], d1[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t cc = cur[u];
-        bool ok;
-        if (pair) {  // the two-digit base-2^l plan in 32-bit arithmetic (as k_entangle_pair)
-          const int32_t c32 = cur[u];
-          const int32_t d0 = (int32_t)((uint32_t)c32 << (32 - b)) >> (32 - b);
-          const int32_t d1 = prv[u] + (c32 >> b) + ((c32 >> (b - 1)) & 1);
-          ok = ((uint32_t)(d0 + 128) | (uint32_t)(d1 + 128)) <= 255u;
-          w[0] |= (uint32_t)(uint8_t)d0 << (8 * u);
-          w[1] |= (uint32_t)(uint8_t)d1 << (8 * u);
-        } else {
+        for (int u = 0; u < 4; ++u) {
+          d0[u] = (int32_t)((uint32_t)cur[u] << (32 - b)) >> (32 - b);
+          d1[u] = prv[u] + (cur[u] >> b) + ((cur[u] >> (b - 1)) & 1);
+          const bool out = ((uint32_t)(d0[u] + 128) | (uint32_t)(d1[u] + 128)) > 255u ||
+                           (hi < INT32_MAX && (cur[u] > hi || cur[u] < -hi));
+          badm |= (unsigned)out << u;
+        }
+        w[0] = __byte_perm(__byte_perm(d0[0], d0[1], 0x0040), __byte_perm(d0[2], d0[3], 0x0040), 0x5410);
+        w[1] = __byte_perm(__byte_perm(d1[0], d1[1], 0x0040), __byte_perm(d1[2], d1[3], 0x0040), 0x5410);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t cc = cur[u];
           const int64_t x = (int64_t)((uint64_t)cc + ((uint64_t)(int64_t)prv[u] << l));
           int8_t d[4];
-          ok = digits_b(x, b, L, d);
+          const bool ok = digits_b(x, b, L, d);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             if (j < L) w[j] |= (uint32_t)(uint8_t)d[j] << (8 * u);
+          badm |= (unsigned)(cc > hi || cc < -hi || !ok) << u;
         }
-        const int64_t t = 4 * q + u;
-        if (t >= s0 && t < s0 + n && (cc > hi || cc < -hi || !ok)) {
-          ++bad;
-          const long long idx = (long long)m * n + pos[u];
-          first = idx < first ? idx : first;
-        }
+      }
+      if (badm) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (((badm >> u) & 1) && tin[u]) {
+            ++bad;
+            const long long idx = (long long)m * n + pos[u];
+            first = idx < first ? idx : first;
+          }
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
