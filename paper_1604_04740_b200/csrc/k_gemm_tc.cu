@@ -14,13 +14,20 @@
 //
 // A CTA computes 128 x BN tiles of one stream at a time: the L limb
 // accumulators live side by side in TMEM (L * BN <= 512 columns).  Roles:
-//   warp 0 lane 0 : TMA producer  (cp.async.bulk.tensor, 64B swizzle, multicast, mbarrier complete_tx)
+//   warp 0 lane 0 : TMA producer  (cp.async.bulk.tensor, 64B or 128B swizzle, multicast, mbarrier complete_tx)
 //   warp 1 lane 0 : MMA issuer    (tcgen05.mma.cta_group::1.kind::i8, commit -> mbarrier)
 //   warp 2        : TMEM allocator (tcgen05.alloc / dealloc)
 //   warps 4..11   : epilogue      (tcgen05.ld 32x32b -> int64 recombine -> swizzled smem -> TMA store);
-//                   warp w reads TMEM lane quarter w%4, column half (w-4)/4
-// smem: STAGES x {L limb tiles 128 x 64 B, one B tile BN x 64 B} (64B swizzle),
-// 1024-B aligned; clusters of 2 CTAs along N multicast the limb tiles.
+//                   warp w reads TMEM lane quarter w%4, column half (w-4)/4; the TMEM load of
+//                   the next 16-column chunk is in flight while the current one is staged
+//   warps 12..19  : checkers (CHK > 0 only: the fused disentangle + check)
+// smem: STAGES x {L limb tiles 128 x BK, one B tile BN x BK} (BK = 64 or 128 bytes of K,
+// swizzle of the same width), 1024-B aligned; clusters of 2 CTAs along N multicast
+// the limb tiles (or along M the B tile, Toeplitz mode).  Output modes: one
+// tensor map per stream, or per destination row block (Geo::dest_rows, the C5
+// fused exchange).  DESIGN.md §7 has the measured per-tile timeline: with one
+// TMEM accumulator set (L * BN = 512) the ~4.5 us drain of each 256 KB int64
+// tile through the SM's store port is not overlapped.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
