@@ -1188,3 +1188,24 @@ def test_exhaustive_single_bit_injection_other_M(O, M, r, W):
         od, of = O.disentangle_one(ocfg, col, r)
         assert of == 1 and int(fw[t]) == (1 << n), (s, n, bit)
         assert (dh[t] == od).all(), (s, n, bit)
+
+
+def test_diag_reset_and_accumulation(O):
+    """ne_diag accumulates over calls (counts add, first_* keep the minimum)
+    until ne_diag_reset restores {0, INT64_MAX, 0, INT64_MAX}."""
+    M, N = 3, 4096
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    d = torch.full((4,), 7, dtype=torch.int64, device="cuda")
+    ne.ne_diag_reset(d)
+    assert d.cpu().tolist() == [0, 2 ** 63 - 1, 0, 2 ** 63 - 1]
+    c = gen(O, 70, 1, M, N, -100, 100)
+    D = O.entangle(ocfg, c)
+    out = empty_streams(M, N)
+    for pos in (900, 300):
+        Dc = D.copy()
+        Dc[1, pos] ^= 1 << 9
+        ne.ne_disentangle_check(cfg, to_streams(Dc, torch.int64), 0, out, None, d)
+    r = ne.diag_read(d)
+    assert r["fault_positions"] == 2 and r["first_fault"] == 300 and r["range_violations"] == 0
+    ne.ne_diag_reset(d)
+    assert ne.diag_read(d) == {"range_violations": 0, "first_bad": None, "fault_positions": 0, "first_fault": None}
