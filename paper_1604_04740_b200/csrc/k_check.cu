@@ -112,7 +112,14 @@ k_disentangle3x4(const __grid_constant__ ne_cstreams e, int l, int64_t n, const 
   int nflag = 0;
   long long first = LLONG_MAX;
   const int64_t nq_w = (nq + 31) & ~(int64_t)31;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nq_w; v += stride) {
+  // The check walks the positions from the end (grid-stride sweeps in reverse):
+  // the op that produced delta finished with its last tiles, which are still in
+  // L2; the recovery pass then walks forward into what the check touched last.
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nsweep = (nq_w + stride - 1) / stride;
+  for (int64_t it = 0; it < nsweep; ++it) {
+    const int64_t v = (CHECK ? nsweep - 1 - it : it) * stride + tid;
+    if (v >= nq_w) continue;  // warp-uniform: nq_w and stride are multiples of 32
     const int64_t n0 = 4 * v;
     bool f[4] = {false, false, false, false};
     if (v < nq) {
