@@ -112,6 +112,51 @@ k_prep_b(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __restr
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
+// B -> Bt for full tiles of 128 k x 64 columns (K % 128 == 0, cols % 64 == 0):
+// each thread packs 4 consecutive k of 4 columns per task (4 x 128-bit loads,
+// 16 threads per 256-byte row segment), the [64][33]-word shared tile is
+// transposed so that 8 threads store one full 128-byte line of a Bt row.
+__global__ void __launch_bounds__(256)
+k_prep_b128(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __restrict__ Bt,
+            ne_diag* __restrict__ diag) {
+  __shared__ uint32_t W[64][33];
+  const int64_t k0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 64;
+  int bad = 0;
+  long long first = LLONG_MAX;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int task = it * 256 + threadIdx.x;
+    const int c4 = task & 15, kq = task >> 4;  // 16 column quads x 32 k quads
+    const int64_t c = c0 + 4 * c4;
+    int32_t v[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t k = k0 + 4 * kq + r;
+      const int4 w = __ldcs(reinterpret_cast<const int4*>(B + k * cols + c));
+      v[r][0] = w.x; v[r][1] = w.y; v[r][2] = w.z; v[r][3] = w.w;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if ((uint32_t)(v[r][i] + 128) > 255u) {
+          ++bad;
+          const long long idx = (long long)(k * cols + c + i);
+          first = idx < first ? idx : first;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      W[4 * c4 + i][kq] = __byte_perm(__byte_perm(v[0][i], v[1][i], 0x0040), __byte_perm(v[2][i], v[3][i], 0x0040), 0x5410);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int u = it * 256 + threadIdx.x;  // 64 rows x 8 chunks of 16 bytes
+    const int cc = u >> 3, j = u & 7;
+    __stcs(reinterpret_cast<uint4*>(Bt + (c0 + cc) * K + k0 + 16 * j),
+           make_uint4(W[cc][4 * j], W[cc][4 * j + 1], W[cc][4 * j + 2], W[cc][4 * j + 3]));
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
 }  // namespace ne
 
 using namespace ne;
@@ -132,6 +177,10 @@ extern "C" ne_status ne_gemm_workspace(const ne_config* cfg, int64_t rows, int64
 extern "C" ne_status ne_gemm_prep_b(const int32_t* B, int64_t K, int64_t cols, int8_t* Bt, ne_diag* diag,
                                     ne_stream_t stream) {
   if (!B || !Bt || K <= 0 || cols <= 0 || K % 16 != 0 || !aligned16(Bt) || !aligned16(B)) return NE_EINVAL;
+  if (K % 128 == 0 && cols % 64 == 0) {
+    k_prep_b128<<<dim3((unsigned)(cols / 64), (unsigned)(K / 128)), 256, 0, cs(stream)>>>(B, K, cols, Bt, diag);
+    return launch_status();
+  }
   dim3 grid((unsigned)((cols + 127) / 128), (unsigned)((K + 63) / 64));
   k_prep_b<<<grid, 256, 0, cs(stream)>>>(B, K, cols, Bt, diag);
   return launch_status();
