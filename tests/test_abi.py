@@ -172,3 +172,33 @@ def test_sass_has_tcgen05_tma_and_tmem(L):
     sass = os.popen(f"/usr/local/cuda/bin/cuobjdump -sass {ne.LIB} 2>/dev/null").read()
     for op in ("UTCIMMA", "UTCBAR", "UTCATOMSWS", "LDTM", "UTMALDG", "UTMASTG"):
         assert op in sass, op
+
+
+def test_empty_inputs_are_no_ops(L):
+    """n_total = 0 is a valid, empty problem for every streaming entry point:
+    NE_OK before any pointer is inspected or any kernel is enqueued (no device
+    is needed, NULL buffers are fine)."""
+    c64, c32 = ne.ne_config_for(3), ne.ne_config_for(3, 32)
+    S = ne.Streams()        # all NULL
+    N = None
+    B = ctypes.byref
+    calls = {
+        "ne_entangle": (B(c64), S, 0, S, N, N),
+        "ne_entangle_sets": (B(c64), S, 2, 0, S, N, N),
+        "ne_entangle_aos": (B(c64), S, 0, N, N, N),
+        "ne_entangle_w32": (B(c32), S, 0, S, N, N),
+        "ne_entangle_aos_w32": (B(c32), S, 0, N, N, N),
+        "ne_op_scale": (B(c64), S, 0, 3, N, N),
+        "ne_op_add": (B(c64), S, S, 0, 1, N),
+        "ne_op_scale_add": (B(c64), S, 0, 3, N, S, 1, N),
+        "ne_op_scale_add_w32": (B(c32), S, 0, 3, N, N, 1, N),
+        "ne_disentangle_check": (B(c64), S, 0, 0, S, N, N, N),
+        "ne_disentangle_check_w32": (B(c32), S, 0, 0, S, N, N, N),
+        "ne_op_permute": (B(c64), S, N, 0, S, N),
+        "ne_op_inner": (B(c64), S, 0, N, 1, 1, S, N),
+        "ne_op_permute_inner_check": (B(c64), S, N, 1, N, 0, N, 1, 1, 0, S, S, N, N, N),
+        "ne_op_permute_inner_check_w32": (B(c32), N, N, 0, N, 1, 1, 0, S, S, N, N, N),
+        "ne_entangle_shared": (B(c64), N, N, 0, N),
+    }
+    for name, args in calls.items():
+        assert getattr(L, name)(*args) == 0, name
