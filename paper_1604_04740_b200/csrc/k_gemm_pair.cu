@@ -1,0 +1,304 @@
+// k_gemm_pair.cu — the entangled GEMM on CTA pairs with limb-major passes
+// (experiment).  Same exact limb product as k_gemm_tc.cu (C_m = sum_i
+// 2^(b i) D_{m,i} B, int8 x int8 -> int32 in TMEM, int64 recombination), with
+// one 256 x 256 output tile per pair of SMs (tcgen05.mma.cta_group::2, M = 256,
+// N = 256): each CTA streams its own 128 rows of A and HALF of the B columns,
+// so an SM receives A + B/2 per MAC.  Each tile runs two passes over K — limb 1,
+// then limb 0 — into the two halves of TMEM; the epilogue holds the finished
+// limb-1 accumulators in registers and releases that half at once, so the next
+// tile's limb-1 pass runs while this tile's limb 0 drains through the store
+// port (the drain is hidden, as in a double-buffered kernel).
+//
+// Pair protocol (as SM100 2-SM kernels): both CTAs' TMA loads complete on the
+// LEADER's full[s] (peer bit of the barrier address cleared); the leader alone
+// issues the MMAs; its commits are multicast to both CTAs' empty[s] /
+// tmem_full; both CTAs' epilogue warps arrive on the leader's tmem_empty[p]
+// (mapa + remote arrive).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "ne_internal.cuh"
+#include "tc_common.cuh"
+
+namespace ne {
+namespace tc {
+
+template <int STAGES, int SW>
+struct CfgP {
+  static constexpr int L = 2, BN = 256;
+  static constexpr int BK = SW;
+  static constexpr int kATile = BM * BK;          // this CTA's 128 rows of one limb
+  static constexpr int kBHalf = (BN / 2) * BK;    // this CTA's half of the B tile
+  static constexpr int kStage = kATile + kBHalf;
+  static constexpr int kStageOut = 32 * 16 * 8;
+  static constexpr int kOutBufs = (size_t)STAGES * kStage + 2 * 8 * kStageOut + 1536 <= 232448 ? 2 : 1;
+  static constexpr size_t kSmem = (size_t)STAGES * kStage + kOutBufs * 8 * kStageOut + 1024 + 256;
+};
+
+constexpr int kEpiP = 8;
+constexpr int kThreadsPair = 128 + 32 * kEpiP;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the leader's copy
+
+__device__ __forceinline__ void tma_load_pair(const CUtensorMap* map, uint64_t* bar, void* dst, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n\t"
+      ".reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t"
+      "}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int STAGES, int SW>
+__global__ void __launch_bounds__(kThreadsPair, 1)
+k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+            const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
+            int raster) {
+  using CF = CfgP<STAGES, SW>;
+  constexpr int BK = CF::BK, BN = CF::BN;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* stage_out = smem + STAGES * CF::kStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + CF::kOutBufs * 8 * CF::kStageOut);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;  // [1]
+  uint64_t* tmem_empty = tmem_full + 1;  // [2]: limb-1 half, limb-0 half (the leader's copy is used)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int KB = (int)(K / BK);
+  const int64_t n_rt = rows / (2 * BM), n_ct = cols / BN;
+  const int64_t n_work = (int64_t)M * n_rt * n_ct;
+  const int64_t pid = blockIdx.x / 2, npair = gridDim.x / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tmem_full[0], 1);
+    mbar_init(&tmem_empty[0], 2 * kEpiP);
+    mbar_init(&tmem_empty[1], 2 * kEpiP);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+      uint32_t it = 0;
+      for (int64_t w = pid; w < n_work; w += npair) {
+        const int m = (int)(w / (n_rt * n_ct));
+        const int64_t rem = w % (n_rt * n_ct);
+        const int64_t rt = raster ? rem % n_rt : rem / n_ct, ct = raster ? rem / n_rt : rem % n_ct;
+        const int64_t row0 = rt * 2 * BM + crank * BM;
+        const int64_t bcol0 = ct * BN + crank * (BN / 2);
+        for (int pass = 0; pass < 2; ++pass) {
+          const int li = 1 - pass;
+          for (int kb = 0; kb < KB; ++kb, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+            unsigned char* st = smem + s * CF::kStage;
+            if (leader) mbar_expect_tx(&full[s], (uint32_t)(2 * CF::kStage));
+            tma_load_pair(&mapA, &full[s], st, kb * BK, (int32_t)(((int64_t)m * 2 + li) * rows + row0));
+            tma_load_pair(&mapB, &full[s], st + CF::kATile, kb * BK, (int32_t)bcol0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
+      uint32_t it = 0, tile = 0;
+      for (int64_t w = pid; w < n_work; w += npair, ++tile) {
+        for (int pass = 0; pass < 2; ++pass) {
+          const int li = 1 - pass;
+          mbar_wait(&tmem_empty[pass], (tile & 1) ^ 1);  // both CTAs freed this half
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          for (int kb = 0; kb < KB; ++kb, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(&full[s], (it / STAGES) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sa = smem_u32(smem + s * CF::kStage);
+            const uint32_t sb = sa + CF::kATile;
+#pragma unroll
+            for (int ks = 0; ks < BK / UMMA_K; ++ks)
+              mma_pair(tmem_base + li * BN, umma_desc<SW>(sa + ks * UMMA_K), umma_desc<SW>(sb + ks * UMMA_K), idesc,
+                       (kb | ks) != 0);
+            commit_pair(&empty[s]);
+          }
+        }
+        commit_pair(&tmem_full[0]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    const uint32_t tl = tmem_base + ((uint32_t)(32 * q) << 16);
+    unsigned char* my_out = stage_out + ew * CF::kOutBufs * CF::kStageOut;
+    constexpr int kNch = BN / 2 / 16;
+    uint32_t tile = 0, buf = 0;
+    for (int64_t w = pid; w < n_work; w += npair, ++tile) {
+      const int m = (int)(w / (n_rt * n_ct));
+      const int64_t rem = w % (n_rt * n_ct);
+      const int64_t rt = raster ? rem % n_rt : rem / n_ct, ct = raster ? rem / n_rt : rem % n_ct;
+      const int64_t row0 = rt * 2 * BM + crank * BM;
+      const int64_t col0 = ct * BN;
+      mbar_wait(&tmem_full[0], tile & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int cb = half * (BN / 2);
+      // hold limb 1 of this warp's columns, release that half for the next tile
+      uint32_t hld[kNch][16];
+#pragma unroll
+      for (int ci = 0; ci < kNch; ++ci) tmem_ld16(tl + BN + cb + 16 * ci, hld[ci]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int ci = 0; ci < kNch; ++ci)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(hld[ci][j]));
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) arrive_leader(&tmem_empty[0]);
+#pragma unroll
+      for (int ci = 0; ci < kNch; ++ci) {
+        const int c = cb + 16 * ci;
+        uint32_t v0[16];
+        tmem_ld16(tl + c, v0);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(v0[j]));
+        if (ci + 1 == kNch) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) arrive_leader(&tmem_empty[1]);
+        }
+        if (lane == 0) {
+          if (CF::kOutBufs == 2)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncwarp();
+        unsigned char* box = my_out + buf * CF::kStageOut;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int64_t a0 = (int64_t)(int32_t)v0[2 * k] + ((int64_t)(int32_t)hld[ci][2 * k] << limb_bits);
+          const int64_t a1 = (int64_t)(int32_t)v0[2 * k + 1] + ((int64_t)(int32_t)hld[ci][2 * k + 1] << limb_bits);
+          *reinterpret_cast<longlong2*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) = make_longlong2(a0, a1);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  reinterpret_cast<uint64_t>(&outm.m[m])),
+              "r"((int32_t)(col0 + c)), "r"((int32_t)(row0 + 32 * q)), "r"(smem_u32(box))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        buf = (buf + 1) % CF::kOutBufs;
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u));
+  }
+}
+
+template <int STAGES, int SW>
+static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
+                          int limb_bits, const ne_streams& C, cudaStream_t s) {
+  using CF = CfgP<STAGES, SW>;
+  if (rows % (2 * BM) != 0 || cols % CF::BN != 0 || K % CF::BK != 0 || M > 8) return NE_ENOTSUP;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, planes, (uint64_t)K, (uint64_t)M * 2 * rows, SW, BM)) return NE_ECUDA;
+  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, CF::BN / 2)) return NE_ECUDA;
+  OutMaps om;
+  for (int m = 0; m < M; ++m)
+    if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)rows)) return NE_ECUDA;
+  auto kern = k_gemm_pair<STAGES, SW>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) != cudaSuccess)
+    return NE_ECUDA;
+  const int64_t n_work = (int64_t)M * (rows / (2 * BM)) * (cols / CF::BN);
+  cudaLaunchConfig_t lc = {};
+  lc.blockDim = dim3(kThreadsPair);
+  lc.dynamicSmemBytes = CF::kSmem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int64_t npairs = num_sms() / 2;
+  lc.gridDim = dim3((unsigned)(npairs * 2));
+  int active = 0;
+  if (cudaOccupancyMaxActiveClusters(&active, kern, &lc) == cudaSuccess && active > 0) {
+    if (active < npairs) npairs = active;
+  } else {
+    cudaGetLastError();
+  }
+  if (npairs > n_work) npairs = n_work;
+  lc.gridDim = dim3((unsigned)(npairs * 2));
+  // B panel larger than ~1/3 of L2: row tiles fastest (consecutive pairs share a B panel)
+  const int raster = (uint64_t)cols * (uint64_t)K > (48ull << 20) ? 1 : 0;
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster) != cudaSuccess) return NE_ECUDA;
+  return launch_status();
+}
+
+}  // namespace tc
+
+// 2 limbs, 256 x 256 pair tiles, limb-major passes; NE_ENOTSUP otherwise.
+ne_status launch_gemm_pair(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+                           int64_t K, const ne_streams& C, cudaStream_t s) {
+  if (L != 2 || b > 31) return NE_ENOTSUP;
+  if (K % 128 == 0) return tc::run_pair<6, 128>(planes, Bt, rows, cols, K, M, b, C, s);
+  return NE_ENOTSUP;
+}
+
+}  // namespace ne

@@ -690,8 +690,22 @@ void gemm_trace(long long* buf, int max_clusters) {
   tc::g_max_clusters = max_clusters;
 }
 
+ne_status launch_gemm_pair(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+                           int64_t K, const ne_streams& C, cudaStream_t s);
+
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s) {
+  // Two digits, mid-length K: the CTA-pair kernel with limb-major passes
+  // (k_gemm_pair.cu) hides the int64 drain behind the next tile's first pass
+  // (C3 GEMM 0.293 -> 0.277 ms).  Measured slower for short K (the paper's
+  // N = 200 / 2000 shapes: the per-pass fill costs more than the drain) and for
+  // C5's K = 16384 (the drain is ~6 % of a tile there), so those keep the
+  // single-CTA kernel.  The debug trace hook covers the single-CTA kernel only.
+  if (L == 2 && b <= 31 && K >= 4096 && K <= 8192 && K % 128 == 0 && rows % 256 == 0 && cols % 256 == 0 &&
+      tc::g_trace == nullptr) {
+    const ne_status st = launch_gemm_pair(M, L, b, planes, Bt, rows, cols, K, C, s);
+    if (st != NE_ENOTSUP) return st;
+  }
   return gemm_tc_dispatch<0>(M, L, b, planes, Bt, rows, cols, K, C, s, nullptr);
 }
 

@@ -1,0 +1,8 @@
+# Experiment: CTA-pair GEMM with limb-major passes (NE_GEMM_PAIR=1, k_gemm_pair.cu).
+cd $GRAFT_REPO_ROOT
+export PYTHONPATH=.
+NE_GEMM_PAIR=1 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "gemm_tc_i8 or pair_digits or zero_padded or c3_full or int32_limb or scatter" 2>&1 | tail -2
+for P in 0 1 0 1; do
+  if [ $P = 0 ]; then unset NE_GEMM_PAIR; else export NE_GEMM_PAIR=1; fi
+  timeout 300 python bench.py --workload c3 --steps 30 --warmup 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('pair=$P c3', d['ms_per_step'], d['stages_ms']['gemm'], d['eager_stages_ms']['gemm'], d['correctness'])"
+done

@@ -446,6 +446,30 @@ def test_gemm_tc_i8(O, M, L, bound, rows, cols, K):
     assert ne.diag_read(diag)["fault_positions"] == 0
 
 
+@pytest.mark.parametrize("M,bound,R,Cc,K", [(3, 127, 256, 512, 4096), (4, 127, 256, 256, 4096),
+                                            (8, 32, 256, 256, 8192), (3, 64, 512, 256, 6144)])
+def test_gemm_pair_limb_major(O, M, bound, R, Cc, K):
+    """Two-digit GEMMs with 4096 <= K <= 8192 run on the CTA-pair kernel with
+    limb-major passes (k_gemm_pair.cu: 256 x 256 pair tiles, cta_group::2, the
+    limb-1 accumulators held in registers while limb 0 drains): bit-exact
+    against the oracle for every pair plan base (l = 22, 16, 8), several work
+    items per pair and both passes, and the digits of every stream."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L, b = ne.ne_gemm_limb_plan(cfg, bound)
+    assert L == 2 and b == cfg.l
+    A = gen(O, 80, 4, M, R * K, -bound, bound + 1)
+    A[:, 0], A[:, -1] = bound, -bound
+    B = O.gen_uniform(80, 5, 0, -128, 128, K * Cc)
+    planes = torch.empty(M * L * R * K, dtype=torch.int8, device="cuda")
+    ne.ne_entangle_limbs(cfg, to_streams(A), L, planes, limb_bits=b)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    out = empty_streams(M, R * Cc)
+    ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, limb_bits=b)
+    ref = O.op_gemm(ocfg, O.entangle(ocfg, A).reshape(M, R, K), B.reshape(K, Cc)).reshape(M, -1)
+    assert (to_np(out) == ref).all()
+
+
 @pytest.mark.parametrize("max_clusters", [1, 3])
 def test_gemm_capped_persistent_grid_and_trace(O, max_clusters):
     """The persistent scheduler with a capped grid (every CTA walks many work
