@@ -80,7 +80,7 @@ template <int STAGES, int SW>
 __global__ void __launch_bounds__(kThreadsPair, 1)
 k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
             const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
-            int raster) {
+            int raster, int64_t a_plane_rows, int toeplitz) {
   using CF = CfgP<STAGES, SW>;
   constexpr int BK = CF::BK, BN = CF::BN;
   extern __shared__ unsigned char smem_raw[];
@@ -138,7 +138,11 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
             mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
             unsigned char* st = smem + s * CF::kStage;
             if (leader) mbar_expect_tx(&full[s], (uint32_t)(2 * CF::kStage));
-            tma_load_pair(&mapA, &full[s], st, kb * BK, (int32_t)(((int64_t)m * 2 + li) * rows + row0));
+            // Toeplitz mode (circular conv, k_conv_tc.cu): K-chunk kb of window row b is column
+            // (kb BK) mod W of row b + (kb BK) / W of the [plane_rows][W] view of the extended plane
+            const int32_t kc = toeplitz ? (int32_t)(((int64_t)kb * BK) % toeplitz) : kb * BK;
+            const int64_t radd = toeplitz ? ((int64_t)kb * BK) / toeplitz : 0;
+            tma_load_pair(&mapA, &full[s], st, kc, (int32_t)(((int64_t)m * 2 + li) * a_plane_rows + row0 + radd));
             tma_load_pair(&mapB, &full[s], st + CF::kATile, kb * BK, (int32_t)bcol0);
           }
         }
@@ -249,17 +253,24 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
   }
 }
 
+// plain GEMM: a_plane_rows = out_rows = rows, toeplitz = 0; Toeplitz conv:
+// a_plane_rows = rows of the [plane_rows][W] plane view, toeplitz = W = cols
+// = 256, out_rows = output blocks (rows past it are clipped by the store)
 template <int STAGES, int SW>
 static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
-                          int limb_bits, const ne_streams& C, cudaStream_t s) {
+                          int limb_bits, const ne_streams& C, cudaStream_t s, int64_t a_plane_rows = 0,
+                          int toeplitz = 0, int64_t out_rows = 0) {
   using CF = CfgP<STAGES, SW>;
   if (rows % (2 * BM) != 0 || cols % CF::BN != 0 || K % CF::BK != 0 || M > 8) return NE_ENOTSUP;
+  if (a_plane_rows == 0) a_plane_rows = rows;
+  if (out_rows == 0) out_rows = rows;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, planes, (uint64_t)K, (uint64_t)M * 2 * rows, SW, BM)) return NE_ECUDA;
+  if (!make_map(&ma, planes, toeplitz ? (uint64_t)toeplitz : (uint64_t)K, (uint64_t)M * 2 * a_plane_rows, SW, BM))
+    return NE_ECUDA;
   if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, CF::BN / 2)) return NE_ECUDA;
   OutMaps om;
   for (int m = 0; m < M; ++m)
-    if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)rows)) return NE_ECUDA;
+    if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows)) return NE_ECUDA;
   auto kern = k_gemm_pair<STAGES, SW>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) != cudaSuccess)
     return NE_ECUDA;
@@ -286,12 +297,22 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   if (npairs > n_work) npairs = n_work;
   lc.gridDim = dim3((unsigned)(npairs * 2));
   // B panel larger than ~1/3 of L2: row tiles fastest (consecutive pairs share a B panel)
-  const int raster = (uint64_t)cols * (uint64_t)K > (48ull << 20) ? 1 : 0;
-  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster) != cudaSuccess) return NE_ECUDA;
+  const int raster = !toeplitz && (uint64_t)cols * (uint64_t)K > (48ull << 20) ? 1 : 0;
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz) !=
+      cudaSuccess)
+    return NE_ECUDA;
   return launch_status();
 }
 
 }  // namespace tc
+
+// Toeplitz conv with 256-output blocks and 2 limbs on the pair kernel (C2P).
+ne_status launch_conv_pair(int M, int b, const int8_t* planes, int64_t plane_rows, const int8_t* Gt, int64_t Kpad,
+                           int64_t nblocks, const ne_streams& C, cudaStream_t s) {
+  if (b > 31 || Kpad % 128 != 0) return NE_ENOTSUP;
+  const int64_t rows = (nblocks + 255) / 256 * 256;
+  return tc::run_pair<6, 128>(planes, Gt, rows, 256, Kpad, M, b, C, s, plane_rows, 256, nblocks);
+}
 
 // 2 limbs, 256 x 256 pair tiles, limb-major passes; NE_ENOTSUP otherwise.
 ne_status launch_gemm_pair(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,

@@ -732,8 +732,18 @@ ne_status launch_gemm_tc_scatter(int L, int b, const int8_t* planes, const int8_
 //   W = 256 (L <= 2): the C3 GEMM configuration (128 x 256 tiles, 64-byte K
 //     stages, 5 stages) — the A windows are reused by 256 columns instead of
 //     128, halving the A stream per MAC
+ne_status launch_conv_pair(int M, int b, const int8_t* planes, int64_t plane_rows, const int8_t* Gt, int64_t Kpad,
+                           int64_t nblocks, const ne_streams& C, cudaStream_t s);
+
 ne_status launch_conv_tc(int M, int L, int b, int W, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
                          int64_t Kpad, int64_t nblocks, const ne_streams& C, cudaStream_t s) {
+  // long kernels (Kpad >= 2048) with 256-output blocks and two digits: the
+  // CTA-pair limb-major kernel (C2P M = 8, T = 4500: conv 0.080 -> 0.072 ms);
+  // at T = 1000 it is neutral and at T = 300 slower (pipeline fill per pass)
+  if (W == 256 && L == 2 && Kpad >= 2048 && tc::g_trace == nullptr) {
+    const ne_status st = launch_conv_pair(M, b, planes, plane_rows, Gt, Kpad, nblocks, C, s);
+    if (st != NE_ENOTSUP) return st;
+  }
   const tc::Geo geo{plane_rows, nblocks, W, 1, 0};
   const int64_t rows = (nblocks + 255) / 256 * 256;
   if (Kpad % 128 != 0) return NE_EINVAL;

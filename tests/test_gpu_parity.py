@@ -957,7 +957,9 @@ def test_gemm_limbs_check_fused(O, M, plan, bound, rows, cols, K, r):
     (5, 4096, 64, 1, 100, None), (3, 20000, 1000, 0, 127, None), (8, 70000, 700, 1, 100, 128),
     (3, 70000 + 5, 64, 0, 127, 256), (4, 600, 300, 1, 100, 256),
     # shift s0 mod N = 1, 2 (mod 4) for the vector-load entangle path
-    (3, 4096, 2, 0, 127, None), (4, 8192, 67, 0, 100, None), (3, 100, 302, 0, 127, None)])
+    (3, 4096, 2, 0, 127, None), (4, 8192, 67, 0, 100, None), (3, 100, 302, 0, 127, None),
+    # Kpad >= 2048 at W = 256: the CTA-pair limb-major kernel (several pair row tiles, correlation, M = 4)
+    (3, 70000 + 3, 2500, 1, 127, None), (4, 140000, 3000, 0, 100, None)])
 def test_conv_tensor_core(O, M, N, T, correlate, bound, block):
     """ne_op_conv_limbs (tcgen05 Toeplitz GEMM + partial-block tail) equals the
     oracle's circular convolution / correlation of the entangled streams,
