@@ -80,7 +80,7 @@ template <int STAGES, int SW>
 __global__ void __launch_bounds__(kThreadsPair, 1)
 k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
             const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
-            int raster, int64_t a_plane_rows, int toeplitz) {
+            int raster, int64_t a_plane_rows, int toeplitz, int kcb) {
   using CF = CfgP<STAGES, SW>;
   constexpr int BK = CF::BK, BN = CF::BN;
   extern __shared__ unsigned char smem_raw[];
@@ -88,8 +88,8 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
   unsigned char* stage_out = smem + STAGES * CF::kStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_out + CF::kOutBufs * 8 * CF::kStageOut);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;  // [1]
-  uint64_t* tmem_empty = tmem_full + 1;  // [2]: limb-1 half, limb-0 half (the leader's copy is used)
+  uint64_t* tmem_full = empty + STAGES;  // [2]: limb 1 complete, limb 0 complete
+  uint64_t* tmem_empty = tmem_full + 2;  // [2]: limb-1 half, limb-0 half free (the leader's copy is used)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -106,6 +106,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       mbar_init(&empty[s], 1);
     }
     mbar_init(&tmem_full[0], 1);
+    mbar_init(&tmem_full[1], 1);
     mbar_init(&tmem_empty[0], 2 * kEpiP);
     mbar_init(&tmem_empty[1], 2 * kEpiP);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -131,9 +132,12 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
         const int64_t rt = raster ? rem % n_rt : rem / n_ct, ct = raster ? rem / n_rt : rem % n_ct;
         const int64_t row0 = rt * 2 * BM + crank * BM;
         const int64_t bcol0 = ct * BN + crank * (BN / 2);
+        // K in chunks of kcb blocks, each chunk limb 1 then limb 0 (its B chunk is
+        // still in L2 for the second pass); kcb = KB: one pass per limb
+        for (int c0 = 0; c0 < KB; c0 += kcb)
         for (int pass = 0; pass < 2; ++pass) {
           const int li = 1 - pass;
-          for (int kb = 0; kb < KB; ++kb, ++it) {
+          for (int kb = c0; kb < KB && kb < c0 + kcb; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
             unsigned char* st = smem + s * CF::kStage;
@@ -153,11 +157,14 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
       uint32_t it = 0, tile = 0;
       for (int64_t w = pid; w < n_work; w += npair, ++tile) {
+        for (int c0 = 0; c0 < KB; c0 += kcb)
         for (int pass = 0; pass < 2; ++pass) {
           const int li = 1 - pass;
-          mbar_wait(&tmem_empty[pass], (tile & 1) ^ 1);  // both CTAs freed this half
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          for (int kb = 0; kb < KB; ++kb, ++it) {
+          if (c0 == 0) {
+            mbar_wait(&tmem_empty[pass], (tile & 1) ^ 1);  // both CTAs freed this half
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          }
+          for (int kb = c0; kb < KB && kb < c0 + kcb; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&full[s], (it / STAGES) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -169,8 +176,8 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
                        (kb | ks) != 0);
             commit_pair(&empty[s]);
           }
+          if (c0 + kcb >= KB) commit_pair(&tmem_full[pass]);  // limb li complete
         }
-        commit_pair(&tmem_full[0]);
       }
     }
   } else if (warp >= 4) {
@@ -202,6 +209,8 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) arrive_leader(&tmem_empty[0]);
+      mbar_wait(&tmem_full[1], tile & 1);  // limb 0 complete
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int ci = 0; ci < kNch; ++ci) {
         const int c = cb + 16 * ci;
@@ -298,7 +307,8 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   lc.gridDim = dim3((unsigned)(npairs * 2));
   // B panel larger than ~1/3 of L2: row tiles fastest (consecutive pairs share a B panel)
   const int raster = !toeplitz && (uint64_t)cols * (uint64_t)K > (48ull << 20) ? 1 : 0;
-  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz) !=
+  const int kcb = (int)(K / CF::BK) < 4096 / CF::BK ? (int)(K / CF::BK) : 4096 / CF::BK;  // 4096-deep K chunks
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz, kcb) !=
       cudaSuccess)
     return NE_ECUDA;
   return launch_status();
