@@ -307,7 +307,9 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   lc.gridDim = dim3((unsigned)(npairs * 2));
   // B panel larger than ~1/3 of L2: row tiles fastest (consecutive pairs share a B panel)
   const int raster = !toeplitz && (uint64_t)cols * (uint64_t)K > (48ull << 20) ? 1 : 0;
-  const int kcb = (int)(K / CF::BK) < 4096 / CF::BK ? (int)(K / CF::BK) : 4096 / CF::BK;  // 4096-deep K chunks
+  // whole-K passes up to K = 8192 (B chunks of one pass stay in L2 at these
+  // sizes); 4096-deep chunks beyond
+  const int kcb = K <= 8192 ? (int)(K / CF::BK) : 4096 / CF::BK;
   if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz, kcb) !=
       cudaSuccess)
     return NE_ECUDA;
