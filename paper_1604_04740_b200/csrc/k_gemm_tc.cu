@@ -701,8 +701,11 @@ ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t
   // N = 200 / 2000 shapes: the per-pass fill costs more than the drain) and for
   // C5's K = 16384 (the drain is ~6 % of a tile there), so those keep the
   // single-CTA kernel.  The debug trace hook covers the single-CTA kernel only.
-  if (L == 2 && b <= 31 && K >= 4096 && K <= 8192 && K % 128 == 0 && rows % 256 == 0 && cols % 256 == 0 &&
-      tc::g_trace == nullptr) {
+  // (K = 2048 pays only with several waves of pair tiles: the paper's M = 8,
+  // N = 2000 shape 0.086 -> 0.082 ms, M = 3 0.039 -> 0.041 ms; K <= 1024 never)
+  const int64_t pair_tiles = (int64_t)M * (rows / 256) * (cols / 256);
+  if (L == 2 && b <= 31 && (K >= 4096 || (K >= 2048 && pair_tiles >= 256)) && K <= 8192 && K % 128 == 0 &&
+      rows % 256 == 0 && cols % 256 == 0 && tc::g_trace == nullptr) {
     const ne_status st = launch_gemm_pair(M, L, b, planes, Bt, rows, cols, K, C, s);
     if (st != NE_ENOTSUP) return st;
   }
