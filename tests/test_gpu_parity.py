@@ -470,6 +470,28 @@ def test_gemm_pair_limb_major(O, M, bound, R, Cc, K):
     assert (to_np(out) == ref).all()
 
 
+def test_gemm_pair_short_k_many_tiles_sampled(O):
+    """K = 2048 with >= 256 pair tiles also runs on the pair kernel (the
+    paper's M = 8, N = 2000 shape class): rows sampled from every 256-row pair
+    tile of every stream equal the oracle's products."""
+    M, R, Cc, K = 8, 2048, 1024, 2048
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L, b = ne.ne_gemm_limb_plan(cfg, 32)
+    A = gen(O, 81, 4, M, R * K, -32, 32)
+    B = O.gen_uniform(81, 5, 0, -32, 32, K * Cc)
+    planes = torch.empty(M * L * R * K, dtype=torch.int8, device="cuda")
+    ne.ne_entangle_limbs(cfg, to_streams(A), L, planes, limb_bits=b)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    out = empty_streams(M, R * Cc)
+    ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, limb_bits=b)
+    rows = np.arange(0, R, 128) + np.arange(R // 128) % 128   # one row per 128-row half of every pair tile
+    E = O.entangle(ocfg, A).reshape(M, R, K)[:, rows]
+    ref = O.op_gemm(ocfg, E, B.reshape(K, Cc))
+    got = np.stack([out[m].view(R, Cc)[torch.from_numpy(rows).cuda()].cpu().numpy() for m in range(M)])
+    assert (got == ref).all()
+
+
 @pytest.mark.parametrize("max_clusters", [1, 3])
 def test_gemm_capped_persistent_grid_and_trace(O, max_clusters):
     """The persistent scheduler with a capped grid (every CTA walks many work
