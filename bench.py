@@ -347,49 +347,94 @@ class C3Gemm(Workload):
                          if self.fuse else
                          "entangle(limbs)+prep_B+GEMM+disentangle/check(r=0)+recover(r=step mod 3)")}
 
-    def plain_times(self, reps=5):
-        """GEMM on plain A: (i) same tcgen05 kernel with the same L limbs,
-        (ii) the narrowest native form (1 int8 limb); ms per call."""
+    def plain_times(self, reps=10):
+        """The paper's comparison (F5) with matched scopes, each
+        pipeline captured as one CUDA graph and replayed like the timed step:
+          no-fault entangled: entangle(limbs) + prep_B + GEMM + disentangle/check
+          plain, same kernel: int32 -> int8 planes (L digit planes, the upper
+            ones 0) + prep_B + the same tcgen05 GEMM kernel and plan
+          plain, native:      int32 -> one int8 plane + prep_B + the 1-digit
+            tcgen05 GEMM (the narrowest exact plain form)
+        and the fail-stop cost (recovery alone) separately.  Also cuBLASLt's
+        int8 x int8 -> int32 GEMM on the same multiply-adds (torch._int_mm) as
+        a library context number (int32 output, no int64 recombination)."""
         torch, ne = self.torch, self.ne
         if self.algo != "tc" or self.scheme != "entangled":
             return {}
-        M, R, K = self.M, self.rows, self.K
+        M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
+        cfg = self.cfg
         out = {}
-        for tag, L in (("same_kernel_L%d" % self.L, self.L), ("native_L1", 1)):  # plain A: digit 0 = A, rest 0
-            planes = torch.zeros(M * L * R * K, dtype=torch.int8, device="cuda")
-            pv = planes.view(M, L, R * K)
-            for m in range(M):
-                pv[m, 0].copy_(self.A[m].to(torch.int8))  # |A| < 64: one digit, the rest 0
-            ne.ne_op_gemm_limbs(self.cfg, planes, L, self.Bt, R, self.cols, K, self.delta)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(reps):
-                ne.ne_op_gemm_limbs(self.cfg, planes, L, self.Bt, R, self.cols, K, self.delta)
-            e1.record()
-            torch.cuda.synchronize()
-            out[tag] = e0.elapsed_time(e1) / reps
+        st = dict(self.stages(0))
+        out["entangled_nofault"] = (self._time(lambda: (st["entangle"](), st["prep_b"](), st["gemm"](),
+                                                        st["check"]()), reps),
+                                    "entangle(limbs)+prep_B+GEMM+disentangle/check")
+        out["failstop_recover"] = (self._time(st["recover"], reps), "recover(one stream lost)")
+        for tag, Lp, b in (("plain_same_kernel", L, self.limb_bits), ("plain_native_L1", 1, 8)):
+            planes = torch.empty(M * Lp * R * K, dtype=torch.int8, device="cuda")
+            kern = ne.ne_gemm_kernel_for(cfg, Lp, b, R, Cc, K)
+
+            def run(planes=planes, Lp=Lp, b=b):
+                ne.ne_to_limbs(self.A, Lp, planes, self.diag)
+                ne.ne_gemm_prep_b(self.B, K, Cc, self.Bt, self.diag)
+                ne.ne_op_gemm_limbs(cfg, planes, Lp, self.Bt, R, Cc, K, self.delta, b)
+            out[tag] = (self._time(run, reps), f"int32->int8 planes (L={Lp})+prep_B+GEMM(L={Lp}, {kern} kernel)")
+            out[tag + "_gemm_only"] = (self._time(
+                lambda planes=planes, Lp=Lp, b=b: ne.ne_op_gemm_limbs(cfg, planes, Lp, self.Bt, R, Cc, K,
+                                                                      self.delta, b), reps),
+                f"GEMM(L={Lp}) alone")
             del planes
+        try:  # library context: cuBLASLt int8 GEMM, int32 out, the same M x rows x cols x K multiply-adds
+            a8 = torch.randint(-64, 64, (M * R, K), dtype=torch.int8, device="cuda")
+            b8 = torch.randint(-64, 64, (K, Cc), dtype=torch.int8, device="cuda")
+            out["context_cublaslt_int8"] = (self._time(lambda: torch._int_mm(a8, b8), reps),
+                                            "torch._int_mm (cuBLASLt) int8 x int8 -> int32, one (M*rows) x K x cols GEMM")
+            del a8, b8
+        except Exception as e:  # noqa: BLE001 — context only
+            out["context_cublaslt_int8"] = (None, f"unavailable: {type(e).__name__}")
         return out
 
     # ---- CPU oracle on a bounded sample (rows of every stream)
+    def sample_rows(self, rows_sample):
+        """One row per 256-row pair band (C3: 16 bands), its 32-row TMEM lane
+        group cycling through all 8 (both CTA halves, every epilogue quarter);
+        the paper shapes: the first rows of the true (unpadded) operand."""
+        if self.true_shape is not None:
+            return np.arange(rows_sample)
+        band = self.rows // rows_sample
+        return np.array([band * i + 32 * (i % 8) % band + (7 * i) % 32 for i in range(rows_sample)])
+
     def oracle_sample(self, rows_sample):
         import oracle as O
 
         M, K, Cc = self.M, self.K, self.cols
         if self.true_shape is not None:
             _, Cc, K = self.true_shape
+        rows = self.sample_rows(rows_sample)
         ocfg = O.config_for(M, 64)
-        A = np.stack([O.gen_uniform(self.seed, 4, m, -64, 64, rows_sample * K) for m in range(M)])
+        A = np.stack([np.concatenate([O.gen_uniform(self.seed, 4, m, -64, 64, K, int(r) * K) for r in rows])
+                      for m in range(M)])
         B = O.gen_uniform(self.seed, 5, 0, -64, 64, K * Cc).reshape(K, Cc)
         t0 = time.perf_counter()
         E = O.entangle(ocfg, A)
-        D = O.op_gemm(ocfg, E.reshape(M, rows_sample, K), B).reshape(M, -1)
+        D = O.op_gemm(ocfg, E.reshape(M, len(rows), K), B).reshape(M, -1)
         d, flags, nf = O.disentangle_check(ocfg, D, 0)
         O.recover(ocfg, [None] + [D[m] for m in range(1, M)], 0)
         dt = time.perf_counter() - t0
-        return dt, 2 * M * rows_sample * Cc * K / 1e9, f"{rows_sample} of {self.rows} rows of each of the " \
-                                                       f"M={M} streams, full K and cols (same seeded inputs)"
+        self._oref = (rows, D.reshape(M, len(rows), Cc), d.reshape(M, len(rows), Cc))
+        return dt, 2 * M * len(rows) * Cc * K / 1e9, \
+            f"{len(rows)} of {self.rows} rows of each of the M={M} streams (one per 256-row band, all 8 TMEM " \
+            f"lane groups), full K and cols (same seeded inputs)"
+
+    def oracle_compare(self):
+        """The oracle's delta and d_hat of the sampled rows vs the timed run's."""
+        if getattr(self, "_oref", None) is None or self.scheme != "entangled":
+            return None
+        rows, D, d = self._oref
+        idx = self.torch.from_numpy(rows).cuda()
+        ct = D.shape[-1]
+        got_d = np.stack([t.view(self.rows, self.cols)[idx, :ct].cpu().numpy() for t in self.delta])
+        got = np.stack([t.view(self.rows, self.cols)[idx, :ct].cpu().numpy() for t in self.dout])
+        return bool((got_d == D).all() and (got == d).all())
 
 
 class C4PermInner(Workload):
@@ -517,7 +562,9 @@ class C4PermInner(Workload):
         e1.record()
         torch.cuda.synchronize()
         del plain
-        return {"same_kernel_plain_int64": e0.elapsed_time(e1) / reps}
+        return {"plain_same_kernel": (e0.elapsed_time(e1) / reps,
+                                      "gather+inner (+check, skipped on plain data) on plain int64 AoS containers, "
+                                      "inputs already widened")}
 
     def oracle_sample(self, blocks):
         import oracle as O
@@ -531,10 +578,20 @@ class C4PermInner(Workload):
                       for m in range(4)])
         eps = O.entangle(ocfg, c)
         delta = O.op_inner(ocfg, eps, v, B)
-        O.disentangle_check(ocfg, delta, 0)
+        d, _, _ = O.disentangle_check(ocfg, delta, 0)
         dt = time.perf_counter() - t0
+        self._oref = (delta, d)
         return dt, blocks * B * (84 if self.w == 64 else 52) / 1e9, \
             f"{blocks} output blocks of 1024 gathered positions (of {n // B})"
+
+    def oracle_compare(self):
+        if getattr(self, "_oref", None) is None:
+            return None
+        D, d = self._oref
+        nb = D.shape[1]
+        got_d = np.stack([t[:nb].to(self.torch.int64).cpu().numpy() for t in self.delta])
+        got = np.stack([t[:nb].to(self.torch.int64).cpu().numpy() for t in self.dout])
+        return bool((got_d == D).all() and (got == d).all())
 
 
 class C2Conv(Workload):
@@ -674,9 +731,10 @@ class C2Conv(Workload):
         if self.algo != "tc":
             x64 = [c.to(torch.int64) for c in self.c]
             o64 = [torch.empty_like(x) for x in x64]
-            return {"same_kernel_plain_int64": self._time(lambda: ne.ne_op_conv(self.cfg, x64, self.g, o64), reps)}
+            return {"plain_same_kernel": (self._time(lambda: ne.ne_op_conv(self.cfg, x64, self.g, o64), reps),
+                                          "direct conv kernel on plain int64 streams, inputs already widened")}
         M, out = self.M, {}
-        for tag, L in (("same_kernel_L%d" % self.L, self.L), ("native_L1", 1)):
+        for tag, L in (("plain_same_kernel", self.L), ("plain_native_L1", 1)):
             planes = torch.zeros(M * L * self.plen, dtype=torch.int8, device="cuda")
             pv = planes.view(M, L, self.plen)
             s0 = self.T - 1
@@ -692,7 +750,8 @@ class C2Conv(Workload):
                                     self.block)
             e1.record()
             torch.cuda.synchronize()
-            out[tag] = e0.elapsed_time(e1) / reps
+            out[tag] = (e0.elapsed_time(e1) / reps, f"Toeplitz conv GEMM (L={L}) on plain digit planes (planes "
+                                                    f"prepared outside the timing)")
             del planes
         return out
 
@@ -710,16 +769,28 @@ class C2Conv(Workload):
             t0 = time.perf_counter()
             eps = O.entangle(ocfg, c)
             d = O.op_conv(ocfg, eps, g)
-            O.disentangle_check(ocfg, d, 0)
+            dh, _, _ = O.disentangle_check(ocfg, d, 0)
             dt = time.perf_counter() - t0
+            # positions T-1 .. N'-1 of the N' prefix never wrap: they equal the full-size outputs
+            self._oref = (self.T - 1, d[:, self.T - 1:], dh[:, self.T - 1:])
             return dt, 2 * M * n2 * self.T / 1e9, f"one full pass at N'={n2} (M={M}, T={self.T}, same distributions)"
         t0 = time.perf_counter()
         for _ in range(reps):
             eps = O.entangle(ocfg, c)
             d = O.op_conv(ocfg, eps, g)
-            O.disentangle_check(ocfg, d, 0)
+            dh, _, _ = O.disentangle_check(ocfg, d, 0)
         dt = time.perf_counter() - t0
+        self._oref = (0, d, dh)
         return dt, reps * self.work_per_step(), f"{reps} full C2 passes"
+
+    def oracle_compare(self):
+        if getattr(self, "_oref", None) is None or self.scheme != "entangled":
+            return None
+        lo, D, d = self._oref
+        hi = lo + D.shape[1]
+        got_d = np.stack([t[lo:hi].cpu().numpy() for t in self.delta])
+        got = np.stack([t[lo:hi].cpu().numpy() for t in self.dout])
+        return bool((got_d == D).all() and (got == d).all())
 
 
 class C1Chain(Workload):
@@ -818,13 +889,15 @@ class C1Chain(Workload):
         torch, ne = self.torch, self.ne
         cfg32 = ne.ne_config_for(3, 32)
         x32 = [c.clone() for c in self.c]
-        native = self._time(lambda: ne.ne_op_scale_add_w32(cfg32, x32, 37, None, self.a, 1), reps)
+        native = (self._time(lambda: ne.ne_op_scale_add_w32(cfg32, x32, 37, None, self.a, 1), reps),
+                  "scale+add kernel in place on the plain int32 inputs (w = 32 kernel)")
         if self.w == 32:
-            return {"same_kernel_plain_int32": native}
+            return {"plain_same_kernel": native}
         x64 = [c.to(torch.int64) for c in self.c]
         a64 = [a.to(torch.int64) for a in self.a]
-        same = self._time(lambda: ne.ne_op_scale_add(self.cfg, x64, 37, a64), reps)
-        return {"same_kernel_plain_int64": same, "native_int32": native}
+        same = (self._time(lambda: ne.ne_op_scale_add(self.cfg, x64, 37, a64), reps),
+                "the same scale+add kernel on plain int64 containers (inputs already widened)")
+        return {"plain_same_kernel": same, "plain_native_int32": native}
 
     def oracle_sample(self, reps):
         import oracle as O
@@ -836,9 +909,20 @@ class C1Chain(Workload):
         t0 = time.perf_counter()
         for _ in range(reps):
             d = O.op_add(ocfg, O.op_scale(ocfg, O.entangle(ocfg, c), 37), O.entangle(ocfg, a))
-            O.disentangle_check(ocfg, d, 0)
+            dh, _, _ = O.disentangle_check(ocfg, d, 0)
         dt = time.perf_counter() - t0
+        self._oref = (d, dh)
         return dt, reps * ns / 1e9, f"{reps} full C1 passes (w={self.w})" + ("" if ns == self.n else f" at N'={ns}")
+
+    def oracle_compare(self):
+        """delta (left in eps by the in-place op) and d_hat of the timed run vs the oracle."""
+        if getattr(self, "_oref", None) is None:
+            return None
+        D, d = self._oref
+        ns = d.shape[1]
+        got = np.stack([t[:ns].to(self.torch.int64).cpu().numpy() for t in self.dout])
+        got_d = np.stack([t[:ns].to(self.torch.int64).cpu().numpy() for t in self.eps])
+        return bool((got == d).all() and (got_d == D).all())
 
 
 WORKLOADS = {"c1": C1Chain, "c2": C2Conv, "c2p": C2Conv, "c3": C3Gemm, "c3p": C3Gemm, "c4": C4PermInner, "c5": None}
@@ -921,9 +1005,10 @@ class ClockSampler:
 
 
 # ====================================================================== runs
-def c5_oracle_sample(plan, ncols):
+def c5_oracle_sample(plan, ncols, keep=None):
     """Row 0 of every stream, the first `ncols` output columns, through the
-    oracle: entangle, GEMM, disentangle + check, recovery without plan.kill."""
+    oracle: entangle, GEMM, disentangle + check, recovery without plan.kill.
+    keep (a dict, optional) receives the oracle's d_hat of those positions."""
     import oracle as O
 
     M, K, b = plan.M, plan.K, plan.bound
@@ -933,9 +1018,11 @@ def c5_oracle_sample(plan, ncols):
     t0 = time.perf_counter()
     E = O.entangle(ocfg, A0)
     D = O.op_gemm(ocfg, E.reshape(M, 1, K), B).reshape(M, -1)
-    O.disentangle_check(ocfg, D, 0)
+    d, _, _ = O.disentangle_check(ocfg, D, 0)
     O.recover(ocfg, [None if m == (plan.kill or 0) else D[m] for m in range(M)], plan.kill or 0)
     dt = time.perf_counter() - t0
+    if keep is not None:
+        keep["d"] = d
     return dt, 2 * M * ncols * K / 1e9, f"row 0 of each of the {M} stream blocks, first {ncols} of {plan.cols} columns"
 
 
@@ -1091,11 +1178,27 @@ def run_c5(args, rank, world, local_rank):
     }
     if fs is not None:
         line["failstop"] = fs
+    import oracle as O
+
+    n = ORACLE_SAMPLE["c5"][0]
+    keep = {}
+    O.set_threads(1)
+    dt, work, what = c5_oracle_sample(plan, n, keep)
     if world == 1:
-        n = ORACLE_SAMPLE["c5"][0]
-        dt, work, what = c5_oracle_sample(plan, n)
+        nt = O.max_threads()
+        O.set_threads(nt)
+        dt2, work2, _ = c5_oracle_sample(plan, n)
+        O.set_threads(1)
         line["cpu_baseline"] = {"value": round(work / dt, 6), "unit": "Gop/s", "cores": 1, "kind": "oracle",
-                                "sample": what, "seconds": round(dt, 3), "cpu": _cpu_model()}
+                                "sample": what, "seconds": round(dt, 3), "cpu": _cpu_model(),
+                                "all_cores": {"value": round(work2 / dt2, 6), "cores": nt, "seconds": round(dt2, 3),
+                                              "how": "the oracle's GEMM outer loop split over nproc threads"}}
+    # rank 0's checked slice starts at position 0: row 0 of every stream, first n columns
+    lo, dchk = res["check_slice"]
+    line["correctness"]["oracle_rows_equal"] = bool(
+        lo == 0 and all(t.numel() >= n for t in dchk)
+        and (np.stack([t[:n].cpu().numpy() for t in dchk]) == keep["d"]).all())
+    line["correctness"]["oracle_sample"] = what
     return line
 
 
@@ -1243,6 +1346,17 @@ def run_ours(args, rank, world, local_rank):
         dg = dict(dg, range_violations=int(t[0].item()), fault_positions=int(t[1].item()))
         rec_ok = int(t[2].item()) == 0
 
+    # the oracle on a bounded sample of this rank's inputs (the cpu_baseline
+    # leg), and the timed run's outputs (delta and d_hat of the last timed
+    # step) compared with it at the sampled positions — before any later
+    # measurement reuses the output buffers
+    cb = cpu_baseline(args.workload, W)
+    oracle_ok = W.oracle_compare()
+    if world > 1:
+        t = torch.tensor([0 if oracle_ok is False else 1], device="cuda", dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        oracle_ok = None if oracle_ok is None else bool(t.item())
+
     # end to end through host buffers: pinned H2D inputs, D2H results, every
     # step, pipelined over three CUDA streams (Workload.e2e_pipeline)
     e2e_steps = max(4, min(args.steps, 20))
@@ -1311,21 +1425,60 @@ def run_ours(args, rank, world, local_rank):
                         "recover_equals_check": rec_ok},
     }
     if plain:
-        line["plain_ms"] = {k: round(v, 4) for k, v in plain.items()}
-        op_stage = "gemm" if "gemm" in stage_ms else dom
-        line["overhead_pct"] = {f"step_vs_{k}": round((ms_per_step / v - 1) * 100, 2) for k, v in plain.items()}
-        line["overhead_pct"]["op_stage"] = op_stage
+        line["overhead"] = overhead_block(W, plain)
+        line["overhead_pct"] = line["overhead"]["pct"]
     line["timed_host_s"] = round(t_host1 - t_host0, 4)
     if world == 1:
-        line["cpu_baseline"] = cpu_baseline(args.workload, W)
+        line["cpu_baseline"] = cb
+    line["correctness"]["oracle_rows_equal"] = oracle_ok   # every rank's sample (min over ranks)
+    line["correctness"]["oracle_sample"] = cb["sample"] + ("" if world == 1 else " (per rank)")
     return line
 
 
+def overhead_block(W, plain, reps=10):
+    """% overhead vs plain (BASELINE metric; the paper's comparison, F5,
+    P:1118-1130) with the scopes stated: the no-fault entangled pipeline (every
+    stage but recovery) against each plain pipeline, and the fail-stop
+    recovery as its own cost.  Every pipeline is one CUDA graph replayed
+    `reps` times (Workload._time), the same launch path on both sides."""
+    st = W.stages(0)
+    names = [n for n, _ in st if n != "recover"]
+    nf = plain.pop("entangled_nofault", None) or (
+        W._time(lambda: [f() for n, f in st if n != "recover"], reps), "+".join(names))
+    rec = plain.pop("failstop_recover", None) or (W._time(dict(st)["recover"], reps), "recover(one stream lost)")
+    pct = {}
+    for k, (ms, _) in plain.items():
+        if ms and not k.startswith("context") and not k.endswith("_gemm_only"):
+            pct[f"nofault_vs_{k}"] = round((nf[0] / ms - 1) * 100, 2)
+    pct["failstop_recover_vs_nofault"] = round(rec[0] / nf[0] * 100, 2)
+    return {"entangled_nofault": {"ms": round(nf[0], 4), "scope": nf[1]},
+            "failstop_recover": {"ms": round(rec[0], 4), "scope": rec[1]},
+            "plain": {k: {"ms": None if ms is None else round(ms, 4), "scope": sc} for k, (ms, sc) in plain.items()},
+            "pct": pct,
+            "timing": f"each pipeline one CUDA graph, {reps} back-to-back replays (CUDA events)"}
+
+
 def cpu_baseline(workload, W):
+    """The oracle as it stands, on one host core, on a bounded sample of the
+    workload; for the GEMM configs also with its GEMM's outer loop split over
+    every host core, the thread count stated."""
+    import oracle as O
+
     n, _ = ORACLE_SAMPLE[workload]
+    O.set_threads(1)
     dt, work, what = W.oracle_sample(n)
-    return {"value": round(work / dt, 6), "unit": W.metric_unit, "cores": 1, "kind": "oracle",
-            "sample": what, "seconds": round(dt, 3), "cpu": _cpu_model()}
+    out = {"value": round(work / dt, 6), "unit": W.metric_unit, "cores": 1, "kind": "oracle",
+           "sample": what, "seconds": round(dt, 3), "cpu": _cpu_model()}
+    if workload in ("c3", "c3p"):
+        nt = O.max_threads()
+        O.set_threads(nt)
+        saved = getattr(W, "_oref", None)
+        dt2, work2, _ = W.oracle_sample(n)
+        W._oref = saved
+        O.set_threads(1)
+        out["all_cores"] = {"value": round(work2 / dt2, 6), "cores": nt, "seconds": round(dt2, 3),
+                            "how": "the oracle's GEMM outer loop split over nproc threads (same results)"}
+    return out
 
 
 def _cpu_model():
@@ -1426,6 +1579,62 @@ def run_reference(args):
     return line
 
 
+# the other BASELINE configs, measured in the same default run (compact lines
+# under "configs"): C1 at its stated N and the HBM-bound 2^27 sweep, C2, C4,
+# C5 (one GPU: all 8 streams local; N GPUs: one stream per rank)
+CONFIG_SET = (
+    ("C1", dict(workload="c1", steps=50)),
+    ("C1_n2e27", dict(workload="c1", n=1 << 27, steps=10)),
+    ("C2", dict(workload="c2", steps=50)),
+    ("C4", dict(workload="c4", steps=5)),
+    ("C5", dict(workload="c5", steps=5)),
+)
+_SUB_DEFAULTS = dict(algo="tc", limbs="plan", scheme="entangled", fuse=None, conv=None, taps=4500, streams=8,
+                     kdim=2000, w=64, layout="aos", n=None, failstop="simulated", exchange="auto", graph=1)
+
+
+def compact(line):
+    """The fields of a sub-config line that the configs block keeps."""
+    keep = ("value", "unit", "ms_per_step", "steps", "scaling", "dtype", "stages_ms", "gpu_launches",
+            "overhead_pct", "correctness")
+    out = {k: line[k] for k in keep if k in line}
+    out["workload"] = line["config"]["workload"]
+    if "roofline" in line:
+        out["roofline"] = {k: line["roofline"].get(k) for k in ("bound", "kernel", "achieved", "peak", "unit", "frac",
+                                                                  "traffic")}
+    if "e2e" in line:
+        out["e2e"] = {k: line["e2e"].get(k) for k in ("value", "unit", "ms_per_step", "h2d_bytes_per_step",
+                                                      "d2h_bytes_per_step")}
+    if "cpu_baseline" in line:
+        cb = line["cpu_baseline"]
+        out["cpu_baseline"] = {k: cb.get(k) for k in ("value", "unit", "cores", "sample", "all_cores") if k in cb}
+    if "clocks" in line:
+        out["clocks"] = line["clocks"]
+    return out
+
+
+def run_configs(args, rank, world, local_rank):
+    import argparse as _ap
+    import gc
+
+    import torch
+
+    out = {}
+    for name, over in CONFIG_SET:
+        sub = _ap.Namespace(**dict(vars(args), **_SUB_DEFAULTS, **over))
+        sub.warmup = max(3, min(args.warmup, 5))
+        t0 = time.perf_counter()
+        try:
+            ln = run_c5(sub, rank, world, local_rank) if sub.workload == "c5" else run_ours(sub, rank, world, local_rank)
+            if ln is not None:
+                out[name] = dict(compact(ln), wall_s=round(time.perf_counter() - t0, 1))
+        except Exception as e:  # noqa: BLE001 — one config failing must not hide the others; reported
+            out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1458,6 +1667,9 @@ def main():
                     help="c5: position-major exchange fused into the GEMM epilogue (symmetric memory) or an NCCL "
                          "all_to_all after it; auto = fused when N > 1")
     ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
+    ap.add_argument("--configs", type=int, default=1,
+                    help="default workload (c3) only: also measure C1, C1 at 2^27, C2, C4 and C5 in the same run and "
+                         "report them under \"configs\" (0: the C3 line alone)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -1486,6 +1698,18 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_c5(args, rank, world, local_rank) if args.workload == "c5" else run_ours(args, rank, world, local_rank)
+    default_run = args.workload == "c3" and all(getattr(args, k) == v for k, v in _SUB_DEFAULTS.items()
+                                                  if k not in ("taps", "streams", "kdim"))
+    if args.configs and default_run:
+        import gc
+
+        import torch
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        cfgs = run_configs(args, rank, world, local_rank)
+        if line is not None:
+            line["configs"] = cfgs
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -82,6 +82,8 @@ typedef struct {
 } ne_diag;
 
 typedef enum { NE_GEMM_TC_I8 = 0, NE_GEMM_IMAD64 = 1 } ne_gemm_algo;
+/* which tensor-core kernel a limb GEMM launch runs (ne_gemm_kernel_for) */
+typedef enum { NE_GEMM_KERNEL_CTA = 0, NE_GEMM_KERNEL_PAIR = 1 } ne_gemm_kernel;
 typedef enum { NE_OP_SCALE = 0, NE_OP_ADD = 1, NE_OP_LINEAR = 2, NE_OP_PERMUTE = 3 } ne_op_kind;
 
 /* ======================================================== a0: host only === */
@@ -314,12 +316,25 @@ ne_status ne_op_gemm_limbs_scatter(const ne_config* cfg, const int8_t* planes_m,
                                    const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams dests,
                                    int32_t ndest, int64_t* C_local, ne_stream_t stream);
 
+/* Which tcgen05 kernel ne_op_gemm_limbs / ne_op_gemm (TC) launches for this
+ * shape and digit plan (host-only query, no GPU needed; the same gate the
+ * launch uses): *kernel = NE_GEMM_KERNEL_PAIR for the CTA-pair limb-major
+ * kernel (k_gemm_pair: L = 2, base 2^b with b <= 31, 4096 <= K <= 8192 or
+ * K >= 2048 with >= 256 pair tiles, rows and cols multiples of 256, M <= 8),
+ * else NE_GEMM_KERNEL_CTA (k_gemm_tc, single-CTA tiles).  The gemm trace hook
+ * (ne_gemm_trace), when on, forces the single-CTA kernel.  Errors as
+ * ne_op_gemm_limbs (NE_ENOTSUP for shapes the tensor-core path refuses). */
+ne_status ne_gemm_kernel_for(const ne_config* cfg, int32_t L, int32_t limb_bits, int64_t rows, int64_t cols,
+                             int64_t K, int32_t* kernel);
+
 /* Debug hook (not on the hot path): every later tensor-core GEMM / Toeplitz
  * conv launch in this process records, for CTA c and its t-th tile (t < 32),
  * the %globaltimer value when the tile's accumulators are complete and when
  * its epilogue has staged the last chunk, at buf[(c * 32 + t) * 2 + {0, 1}]
  * (device memory of grid x 64 int64, zeroed by the caller).  max_clusters > 0
- * caps the persistent grid (0: occupancy-sized).  buf = NULL, max_clusters = 0
+ * caps the persistent grid (0: occupancy-sized) — of the CTA-pair kernel too
+ * (in pairs), which runs only while buf is NULL (the trace records the
+ * single-CTA kernel).  buf = NULL, max_clusters = 0
  * turn it off.  Not thread-safe; NE_EINVAL if max_clusters < 0. */
 ne_status ne_gemm_trace(long long* buf, int32_t max_clusters);
 

@@ -26,7 +26,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_SO) or any(os.path.getmtime(s) > os.path.getmtime(_SO) for s in srcs):
         cc = os.environ.get("CC", "gcc")
         subprocess.check_call(
-            [cc, "-O2", "-std=gnu11", "-Wall", "-fPIC", "-shared", "-o", _SO,
+            [cc, "-O2", "-std=gnu11", "-Wall", "-fPIC", "-pthread", "-shared", "-o", _SO,
              os.path.join(_HERE, "ne_oracle.c"), os.path.join(_HERE, "or_selftest.c")])
     return _SO
 
@@ -63,6 +63,8 @@ def lib():
             "or_op_outer": (None, [_PCFG, _P64, C.c_int64, C.c_int64, _P64, C.c_int64, _P64]),
             "or_op_conv": (None, [_PCFG, _P64, C.c_int64, C.c_int64, _P64, C.c_int64, C.c_int32, _P64]),
             "or_op_gemm": (None, [_PCFG, _P64, C.c_int64, C.c_int64, _P64, C.c_int64, _P64]),
+            "or_set_threads": (None, [C.c_int32]),
+            "or_max_threads": (C.c_int32, []),
             "or_op_permute": (None, [_P64, C.c_int64, C.c_int64, _P64, _P64]),
             "or_disentangle_one": (C.c_int32, [_PCFG, _P64, C.c_int32, _P64, C.c_int32]),
             "or_disentangle_check": (C.c_int64, [_PCFG, _P64, C.c_int64, C.c_int32, _P64, _PU8]),
@@ -209,6 +211,15 @@ def op_gemm(cfg: Config, A, B) -> np.ndarray:
     out = np.empty((A2.shape[0], cols), dtype=np.int64)
     lib().or_op_gemm(C.byref(cfg), _p(A2), A2.shape[0], K, _p(B), cols, _p(out))
     return out.reshape(*lead, cols)
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of op_gemm (1 = the single-core baseline)."""
+    lib().or_set_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(lib().or_max_threads())
 
 
 def op_permute(x, perm) -> np.ndarray:

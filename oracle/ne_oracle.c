@@ -16,7 +16,9 @@
  */
 #include "ne_oracle.h"
 
+#include <pthread.h>
 #include <stddef.h>
+#include <unistd.h>
 
 #include "../gen/ne_gen.h"
 
@@ -195,14 +197,52 @@ void or_op_conv(const or_config* cfg, const int64_t* x, int64_t rows, int64_t N,
 
 /* integer matrix product (reading R13): C = A B with A the
  * rows_total x K stack of the stream sub-blocks, B K x cols. Naive triple loop. */
-void or_op_gemm(const or_config* cfg, const int64_t* A, int64_t rows_total, int64_t K,
-                const int64_t* B, int64_t cols, int64_t* C) {
-  for (int64_t i = 0; i < rows_total; ++i)
+static void gemm_rows(const or_config* cfg, const int64_t* A, int64_t i0, int64_t i1, int64_t K,
+                      const int64_t* B, int64_t cols, int64_t* C) {
+  for (int64_t i = i0; i < i1; ++i)
     for (int64_t j = 0; j < cols; ++j) {
       int64_t acc = 0;
       for (int64_t k = 0; k < K; ++k) acc = wadd(cfg, acc, wmul(cfg, A[i * K + k], B[k * cols + j]));
       C[i * cols + j] = acc;
     }
+}
+
+/* The outer loop may be split over threads (SURVEY §8(c) allows parallelising
+ * the big GEMMs' outer loops): rows are independent and every C[i][j] is the
+ * same single accumulation in the same order, so the result does not depend
+ * on the thread count (or_set_threads; 1 = the single-core baseline). */
+static int32_t g_threads = 1;
+void or_set_threads(int32_t n) { g_threads = n > 0 ? n : 1; }
+int32_t or_max_threads(void) { return (int32_t)sysconf(_SC_NPROCESSORS_ONLN); }
+
+typedef struct {
+  const or_config* cfg;
+  const int64_t *A, *B;
+  int64_t i0, i1, K, cols;
+  int64_t* C;
+} gemm_job;
+
+static void* gemm_job_run(void* p) {
+  const gemm_job* j = (const gemm_job*)p;
+  gemm_rows(j->cfg, j->A, j->i0, j->i1, j->K, j->B, j->cols, j->C);
+  return NULL;
+}
+
+void or_op_gemm(const or_config* cfg, const int64_t* A, int64_t rows_total, int64_t K,
+                const int64_t* B, int64_t cols, int64_t* C) {
+  int64_t T = g_threads < rows_total ? g_threads : rows_total;
+  if (T <= 1) {
+    gemm_rows(cfg, A, 0, rows_total, K, B, cols, C);
+    return;
+  }
+  if (T > 256) T = 256;
+  pthread_t th[256];
+  gemm_job jobs[256];
+  for (int64_t t = 0; t < T; ++t) {
+    jobs[t] = (gemm_job){cfg, A, B, t * rows_total / T, (t + 1) * rows_total / T, K, cols, C};
+    pthread_create(&th[t], NULL, gemm_job_run, &jobs[t]);
+  }
+  for (int64_t t = 0; t < T; ++t) pthread_join(th[t], NULL);
 }
 
 /* permutation (bijection I -> G, reading R11): out_m[i] = x_m[perm[i]] */
@@ -369,3 +409,4 @@ void or_gen_perm(uint64_t seed, uint32_t tag, int64_t n, int64_t offset, int64_t
   uint64_t key = ne_gen_key(seed, tag, 0);
   for (int64_t i = 0; i < count; ++i) out[i] = (int64_t)ne_gen_perm(key, (uint64_t)n, (uint64_t)(offset + i));
 }
+

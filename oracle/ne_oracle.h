@@ -62,6 +62,9 @@ void or_op_outer(const or_config* cfg, const int64_t* x, int64_t rows, int64_t N
                  const int64_t* h, int64_t N2, int64_t* out);
 void or_op_conv(const or_config* cfg, const int64_t* x, int64_t rows, int64_t N,
                 const int64_t* g, int64_t T, int32_t correlate, int64_t* out);
+/* threads of or_op_gemm's outer loop (results independent of the count) */
+void or_set_threads(int32_t n);
+int32_t or_max_threads(void);
 void or_op_gemm(const or_config* cfg, const int64_t* A, int64_t rows_total, int64_t K,
                 const int64_t* B, int64_t cols, int64_t* C);
 void or_op_permute(const int64_t* x, int64_t rows, int64_t N, const int64_t* perm,

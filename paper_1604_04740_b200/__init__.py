@@ -33,7 +33,7 @@ EXPORTS = (
     "ne_entangle_limbs_stream", "ne_op_gemm_limbs_stream",
     "ne_op_scale", "ne_op_add", "ne_op_scale_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
-    "ne_gemm_check_workspace", "ne_op_gemm_limbs_check", "ne_gemm_trace", "ne_op_gemm_limbs_scatter",
+    "ne_gemm_check_workspace", "ne_op_gemm_limbs_check", "ne_gemm_trace", "ne_gemm_kernel_for", "ne_op_gemm_limbs_scatter",
     "ne_conv_geometry", "ne_entangle_limbs_conv", "ne_conv_prep_taps", "ne_op_conv_limbs",
     "ne_op_scale_add_check", "ne_op_conv_check", "ne_op_scale_add_check_w32",
     "ne_entangle_w32", "ne_op_scale_add_w32", "ne_disentangle_check_w32", "ne_recover_w32", "ne_inject_sweep_w32",
@@ -109,6 +109,7 @@ _SIGS = {
     "ne_op_conv_limbs": [_PCFG, _VP, _I32, _I32, _I32, _VP, _I64, _I32, _I32, Streams, _VP],
     "ne_gemm_check_workspace": [_I64, _I64, C.POINTER(_SZ)],
     "ne_gemm_trace": [_VP, _I32],
+    "ne_gemm_kernel_for": [_PCFG, _I32, _I32, _I64, _I64, _I64, C.POINTER(_I32)],
     "ne_op_gemm_limbs_scatter": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _I32, _VP, _VP],
     "ne_op_gemm_limbs_check": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _I32, Streams, _VP, _VP, _VP,
                                _VP],
@@ -446,6 +447,16 @@ def ne_op_gemm_limbs_scatter(cfg: Config, planes_m: torch.Tensor, L: int, Bt: to
     or peer memory) and, if given, in full into `local`."""
     _call("ne_op_gemm_limbs_scatter", C.byref(cfg), _ptr(planes_m, torch.int8), L, limb_bits, _ptr(Bt, torch.int8),
           rows, cols, K, _streams(dests, torch.int64), len(dests), _ptr(local, torch.int64), _stream())
+
+
+GEMM_KERNELS = {0: "cta", 1: "pair"}
+
+
+def ne_gemm_kernel_for(cfg: Config, L: int, limb_bits: int, rows: int, cols: int, K: int) -> str:
+    """Which tcgen05 kernel a limb GEMM of this shape/plan launches: "pair" or "cta"."""
+    k = _I32()
+    _call("ne_gemm_kernel_for", C.byref(cfg), L, limb_bits, rows, cols, K, C.byref(k))
+    return GEMM_KERNELS[k.value]
 
 
 def ne_gemm_trace(buf: torch.Tensor | None, max_clusters: int = 0) -> None:

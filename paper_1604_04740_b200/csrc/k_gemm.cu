@@ -13,6 +13,7 @@ void launch_gemm_imad64(int M, const ne_cstreams& A, const int32_t* B, const ne_
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s);
 void gemm_trace(long long* buf, int max_clusters);
+bool gemm_pair_gate(int M, int L, int b, int64_t rows, int64_t cols, int64_t K);
 ne_status launch_gemm_tc_scatter(int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                                  int64_t K, const ne_streams& dests, int ndest, int64_t* local, cudaStream_t s);
 ne_status launch_gemm_tc_check(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows,
@@ -197,6 +198,16 @@ extern "C" ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes
     if (!C.s[m] || !aligned16(C.s[m])) return NE_EINVAL;
   if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
   return launch_gemm_tc(cfg->M, L, limb_bits, planes, Bt, rows, cols, K, C, cs(stream));
+}
+
+extern "C" ne_status ne_gemm_kernel_for(const ne_config* cfg, int32_t L, int32_t limb_bits, int64_t rows,
+                                        int64_t cols, int64_t K, int32_t* kernel) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (!kernel || L < 1 || L > 4 || limb_bits < 8 || limb_bits > 63) return NE_EINVAL;
+  if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
+  *kernel = gemm_pair_gate(cfg->M, L, limb_bits, rows, cols, K) ? NE_GEMM_KERNEL_PAIR : NE_GEMM_KERNEL_CTA;
+  return NE_OK;
 }
 
 extern "C" ne_status ne_gemm_trace(long long* buf, int32_t max_clusters) {

@@ -1,5 +1,5 @@
 // k_gemm_pair.cu — the entangled GEMM on CTA pairs with limb-major passes
-// (experiment).  Same exact limb product as k_gemm_tc.cu (C_m = sum_i
+// (the C3 / C2P default for two-digit operands).  Same exact limb product as k_gemm_tc.cu (C_m = sum_i
 // 2^(b i) D_{m,i} B, int8 x int8 -> int32 in TMEM, int64 recombination), with
 // one 256 x 256 output tile per pair of SMs (tcgen05.mma.cta_group::2, M = 256,
 // N = 256): each CTA streams its own 128 rows of A and HALF of the B columns,
@@ -21,11 +21,12 @@
 #include "tc_common.cuh"
 
 namespace ne {
+int gemm_max_clusters();  // ne_gemm_trace's grid cap (debug / tests), k_gemm_tc.cu
 namespace tc {
 
 template <int STAGES, int SW>
 struct CfgP {
-  static constexpr int L = 2, BN = 256;
+  static constexpr int BN = 256;
   static constexpr int BK = SW;
   static constexpr int kATile = BM * BK;          // this CTA's 128 rows of one limb
   static constexpr int kBHalf = (BN / 2) * BK;    // this CTA's half of the B tile
@@ -76,11 +77,16 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
       : "memory");
 }
 
-template <int STAGES, int SW>
+// L = 2: the limb-major passes above.  L = 1 (one int8 digit: the plain
+// baselines, the ABFT data GEMM): one pass per tile, the two TMEM halves
+// double-buffer whole tiles (tile t accumulates in half t & 1), so the drain
+// of tile t overlaps the MMAs of tile t + 1.
+template <int L, int STAGES, int SW>
 __global__ void __launch_bounds__(kThreadsPair, 1)
 k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
             const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
             int raster, int64_t a_plane_rows, int toeplitz, int kcb) {
+  static_assert(L == 1 || L == 2, "one or two digit planes");
   using CF = CfgP<STAGES, SW>;
   constexpr int BK = CF::BK, BN = CF::BN;
   extern __shared__ unsigned char smem_raw[];
@@ -135,8 +141,8 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
         // K in chunks of kcb blocks, each chunk limb 1 then limb 0 (its B chunk is
         // still in L2 for the second pass); kcb = KB: one pass per limb
         for (int c0 = 0; c0 < KB; c0 += kcb)
-        for (int pass = 0; pass < 2; ++pass) {
-          const int li = 1 - pass;
+        for (int pass = 0; pass < L; ++pass) {
+          const int li = L - 1 - pass;
           for (int kb = c0; kb < KB && kb < c0 + kcb; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -146,7 +152,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
             // (kb BK) mod W of row b + (kb BK) / W of the [plane_rows][W] view of the extended plane
             const int32_t kc = toeplitz ? (int32_t)(((int64_t)kb * BK) % toeplitz) : kb * BK;
             const int64_t radd = toeplitz ? ((int64_t)kb * BK) / toeplitz : 0;
-            tma_load_pair(&mapA, &full[s], st, kc, (int32_t)(((int64_t)m * 2 + li) * a_plane_rows + row0 + radd));
+            tma_load_pair(&mapA, &full[s], st, kc, (int32_t)(((int64_t)m * L + li) * a_plane_rows + row0 + radd));
             tma_load_pair(&mapB, &full[s], st + CF::kATile, kb * BK, (int32_t)bcol0);
           }
         }
@@ -158,10 +164,13 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       uint32_t it = 0, tile = 0;
       for (int64_t w = pid; w < n_work; w += npair, ++tile) {
         for (int c0 = 0; c0 < KB; c0 += kcb)
-        for (int pass = 0; pass < 2; ++pass) {
-          const int li = 1 - pass;
+        for (int pass = 0; pass < L; ++pass) {
+          // L = 2: limb li into TMEM half li; L = 1: the tile into half tile & 1
+          const int li = L == 2 ? 1 - pass : (int)(tile & 1);
+          const int hb = L == 2 ? pass : li;                   // barrier pair of that half
+          const uint32_t ph = L == 2 ? (tile & 1) : ((tile >> 1) & 1);
           if (c0 == 0) {
-            mbar_wait(&tmem_empty[pass], (tile & 1) ^ 1);  // both CTAs freed this half
+            mbar_wait(&tmem_empty[hb], ph ^ 1);  // both CTAs freed this half
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           }
           for (int kb = c0; kb < KB && kb < c0 + kcb; ++kb, ++it) {
@@ -176,7 +185,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
                        (kb | ks) != 0);
             commit_pair(&empty[s]);
           }
-          if (c0 + kcb >= KB) commit_pair(&tmem_full[pass]);  // limb li complete
+          if (c0 + kcb >= KB) commit_pair(&tmem_full[hb]);  // limb li (L = 1: the tile) complete
         }
       }
     }
@@ -194,9 +203,54 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       const int64_t rt = raster ? rem % n_rt : rem / n_ct, ct = raster ? rem / n_rt : rem % n_ct;
       const int64_t row0 = rt * 2 * BM + crank * BM;
       const int64_t col0 = ct * BN;
+      const int cb = half * (BN / 2);
+      if constexpr (L == 1) {
+        const int hb = (int)(tile & 1);
+        mbar_wait(&tmem_full[hb], (tile >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint32_t vv[2][16];
+        tmem_ld16(tl + hb * BN + cb, vv[0]);
+#pragma unroll
+        for (int ci = 0; ci < kNch; ++ci) {
+          uint32_t(&v0)[16] = vv[ci & 1];
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(v0[j]));
+          if (ci + 1 < kNch) {
+            tmem_ld16(tl + hb * BN + cb + 16 * (ci + 1), vv[(ci + 1) & 1]);
+          } else {
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) arrive_leader(&tmem_empty[hb]);
+          }
+          if (lane == 0) {
+            if (CF::kOutBufs == 2)
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          __syncwarp();
+          unsigned char* box = my_out + buf * CF::kStageOut;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<longlong2*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) =
+                make_longlong2((int64_t)(int32_t)v0[2 * k], (int64_t)(int32_t)v0[2 * k + 1]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&outm.m[m])),
+                "r"((int32_t)(col0 + cb + 16 * ci)), "r"((int32_t)(row0 + 32 * q)), "r"(smem_u32(box))
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          buf = (buf + 1) % CF::kOutBufs;
+        }
+        continue;
+      }
       mbar_wait(&tmem_full[0], tile & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int cb = half * (BN / 2);
       // hold limb 1 of this warp's columns, release that half for the next tile
       uint32_t hld[kNch][16];
 #pragma unroll
@@ -265,7 +319,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
 // plain GEMM: a_plane_rows = out_rows = rows, toeplitz = 0; Toeplitz conv:
 // a_plane_rows = rows of the [plane_rows][W] plane view, toeplitz = W = cols
 // = 256, out_rows = output blocks (rows past it are clipped by the store)
-template <int STAGES, int SW>
+template <int L, int STAGES, int SW>
 static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
                           int limb_bits, const ne_streams& C, cudaStream_t s, int64_t a_plane_rows = 0,
                           int toeplitz = 0, int64_t out_rows = 0) {
@@ -274,13 +328,13 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   if (a_plane_rows == 0) a_plane_rows = rows;
   if (out_rows == 0) out_rows = rows;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, planes, toeplitz ? (uint64_t)toeplitz : (uint64_t)K, (uint64_t)M * 2 * a_plane_rows, SW, BM))
+  if (!make_map(&ma, planes, toeplitz ? (uint64_t)toeplitz : (uint64_t)K, (uint64_t)M * L * a_plane_rows, SW, BM))
     return NE_ECUDA;
   if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, CF::BN / 2)) return NE_ECUDA;
   OutMaps om;
   for (int m = 0; m < M; ++m)
     if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows)) return NE_ECUDA;
-  auto kern = k_gemm_pair<STAGES, SW>;
+  auto kern = k_gemm_pair<L, STAGES, SW>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) != cudaSuccess)
     return NE_ECUDA;
   const int64_t n_work = (int64_t)M * (rows / (2 * BM)) * (cols / CF::BN);
@@ -304,12 +358,13 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
     cudaGetLastError();
   }
   if (npairs > n_work) npairs = n_work;
+  if (gemm_max_clusters() > 0 && npairs > gemm_max_clusters()) npairs = gemm_max_clusters();
   lc.gridDim = dim3((unsigned)(npairs * 2));
   // B panel larger than ~1/3 of L2: row tiles fastest (consecutive pairs share a B panel)
   const int raster = !toeplitz && (uint64_t)cols * (uint64_t)K > (48ull << 20) ? 1 : 0;
   // whole-K passes up to K = 8192 (B chunks of one pass stay in L2 at these
   // sizes); 4096-deep chunks beyond
-  const int kcb = K <= 8192 ? (int)(K / CF::BK) : 4096 / CF::BK;
+  const int kcb = (L == 1 || K <= 8192) ? (int)(K / CF::BK) : 4096 / CF::BK;
   if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz, kcb) !=
       cudaSuccess)
     return NE_ECUDA;
@@ -323,14 +378,16 @@ ne_status launch_conv_pair(int M, int b, const int8_t* planes, int64_t plane_row
                            int64_t nblocks, const ne_streams& C, cudaStream_t s) {
   if (b > 31 || Kpad % 128 != 0) return NE_ENOTSUP;
   const int64_t rows = (nblocks + 255) / 256 * 256;
-  return tc::run_pair<6, 128>(planes, Gt, rows, 256, Kpad, M, b, C, s, plane_rows, 256, nblocks);
+  return tc::run_pair<2, 6, 128>(planes, Gt, rows, 256, Kpad, M, b, C, s, plane_rows, 256, nblocks);
 }
 
-// 2 limbs, 256 x 256 pair tiles, limb-major passes; NE_ENOTSUP otherwise.
+// 256 x 256 pair tiles: 2 limbs in limb-major passes, or 1 limb with
+// double-buffered tiles; NE_ENOTSUP otherwise.
 ne_status launch_gemm_pair(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                            int64_t K, const ne_streams& C, cudaStream_t s) {
-  if (L != 2 || b > 31) return NE_ENOTSUP;
-  if (K % 128 == 0) return tc::run_pair<6, 128>(planes, Bt, rows, cols, K, M, b, C, s);
+  if (K % 128 != 0 || b > 31) return NE_ENOTSUP;
+  if (L == 2) return tc::run_pair<2, 6, 128>(planes, Bt, rows, cols, K, M, b, C, s);
+  if (L == 1) return tc::run_pair<1, 6, 128>(planes, Bt, rows, cols, K, M, b, C, s);
   return NE_ENOTSUP;
 }
 

@@ -690,8 +690,21 @@ void gemm_trace(long long* buf, int max_clusters) {
   tc::g_max_clusters = max_clusters;
 }
 
+int gemm_max_clusters() { return tc::g_max_clusters; }
+
 ne_status launch_gemm_pair(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                            int64_t K, const ne_streams& C, cudaStream_t s);
+
+// The CTA-pair gate of launch_gemm_tc (also answered by ne_gemm_kernel_for).
+bool gemm_pair_gate(int M, int L, int b, int64_t rows, int64_t cols, int64_t K) {
+  const int64_t pair_tiles = (int64_t)M * (rows / 256) * (cols / 256);
+  if (K % 128 != 0 || rows % 256 != 0 || cols % 256 != 0 || M > 8 || b > 31) return false;
+  // one digit (plain baselines, ABFT data): double-buffered 256 x 256 pair
+  // tiles, each SM receiving A + B/2 per MAC (the single-CTA L = 1 tile needs
+  // A + B and is bound by the SM's inbound operand rate)
+  if (L == 1) return K >= 1024 && pair_tiles >= 64;
+  return L == 2 && (K >= 4096 || (K >= 2048 && pair_tiles >= 256)) && K <= 8192;
+}
 
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s) {
@@ -703,9 +716,7 @@ ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t
   // single-CTA kernel.  The debug trace hook covers the single-CTA kernel only.
   // (K = 2048 pays only with several waves of pair tiles: the paper's M = 8,
   // N = 2000 shape 0.086 -> 0.082 ms, M = 3 0.039 -> 0.041 ms; K <= 1024 never)
-  const int64_t pair_tiles = (int64_t)M * (rows / 256) * (cols / 256);
-  if (L == 2 && b <= 31 && (K >= 4096 || (K >= 2048 && pair_tiles >= 256)) && K <= 8192 && K % 128 == 0 &&
-      rows % 256 == 0 && cols % 256 == 0 && tc::g_trace == nullptr) {
+  if (gemm_pair_gate(M, L, b, rows, cols, K) && tc::g_trace == nullptr) {
     const ne_status st = launch_gemm_pair(M, L, b, planes, Bt, rows, cols, K, C, s);
     if (st != NE_ENOTSUP) return st;
   }
@@ -740,10 +751,11 @@ ne_status launch_conv_pair(int M, int b, const int8_t* planes, int64_t plane_row
 
 ne_status launch_conv_tc(int M, int L, int b, int W, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
                          int64_t Kpad, int64_t nblocks, const ne_streams& C, cudaStream_t s) {
-  // long kernels (Kpad >= 2048) with 256-output blocks and two digits: the
-  // CTA-pair limb-major kernel (C2P M = 8, T = 4500: conv 0.080 -> 0.072 ms);
-  // at T = 1000 it is neutral and at T = 300 slower (pipeline fill per pass)
-  if (W == 256 && L == 2 && Kpad >= 2048 && tc::g_trace == nullptr) {
+  // long kernels (2048 <= Kpad <= 8192, as the GEMM gate) with 256-output
+  // blocks and two digits: the CTA-pair limb-major kernel (C2P M = 8, T = 4500:
+  // conv 0.080 -> 0.072 ms); at T = 1000 it is neutral and at T = 300 slower
+  // (pipeline fill per pass); longer kernels keep the single-CTA kernel
+  if (W == 256 && L == 2 && Kpad >= 2048 && Kpad <= 8192 && tc::g_trace == nullptr) {
     const ne_status st = launch_conv_pair(M, b, planes, plane_rows, Gt, Kpad, nblocks, C, s);
     if (st != NE_ENOTSUP) return st;
   }

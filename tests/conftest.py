@@ -30,4 +30,5 @@ def O():
     import oracle
 
     oracle.lib()
+    oracle.set_threads(oracle.max_threads())  # the GEMM's outer loop split over host cores (same results)
     return oracle

@@ -118,6 +118,24 @@ def test_gemm_limb_plan():
     assert ne.ne_gemm_limb_plan(ne.ne_config_for(4), 1000) == (4, 8)
 
 
+def test_gemm_kernel_for_names_the_timed_kernels():
+    """The dispatch query (host-only) names the kernel each launch runs: the
+    C3 bench plan (base 2^22, L = 2, 4096^3) runs on the CTA-pair kernel, the
+    base-256 plan and short-K / odd shapes on the single-CTA kernel."""
+    c3 = ne.ne_config_for(3)
+    L, b = ne.ne_gemm_limb_plan(c3, 64)
+    assert ne.ne_gemm_kernel_for(c3, L, b, 4096, 4096, 4096) == "pair"
+    assert ne.ne_gemm_kernel_for(c3, 4, 8, 4096, 4096, 4096) == "cta"
+    assert ne.ne_gemm_kernel_for(c3, L, b, 256, 512, 4096) == "pair"       # smoke()'s pair GEMM
+    assert ne.ne_gemm_kernel_for(c3, L, b, 2048, 1280, 2048) == "cta"      # C3P M = 3, N = 2000: 30 pair tiles
+    c8 = ne.ne_config_for(8)
+    assert ne.ne_gemm_kernel_for(c8, 2, 8, 2048, 16384, 16384) == "cta"    # C5: K > 8192
+    assert ne.ne_gemm_kernel_for(c8, 2, 8, 2048, 1024, 2048) == "pair"     # 256 pair tiles at K = 2048
+    assert ne.ne_gemm_kernel_for(c3, L, b, 384, 512, 4096) == "cta"        # rows not a multiple of 256
+    with pytest.raises(ne.NeError):
+        ne.ne_gemm_kernel_for(c3, L, b, 100, 512, 4096)
+
+
 def test_argument_validation_of_the_newer_entry_points(L):
     """Errors are returned before any device work (fake, 16-B aligned device
     addresses are never dereferenced): stream-set counts, conv block widths,

@@ -452,11 +452,13 @@ def test_gemm_pair_limb_major(O, M, bound, R, Cc, K):
     """Two-digit GEMMs with 4096 <= K <= 8192 run on the CTA-pair kernel with
     limb-major passes (k_gemm_pair.cu: 256 x 256 pair tiles, cta_group::2, the
     limb-1 accumulators held in registers while limb 0 drains): bit-exact
-    against the oracle for every pair plan base (l = 22, 16, 8), several work
-    items per pair and both passes, and the digits of every stream."""
+    against the oracle, in full, for every pair plan base (l = 22, 16, 8) and
+    both passes, and the digits of every stream (one tile per pair at these
+    sizes; the multi-tile path is test_gemm_pair_multi_tile_full)."""
     cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
     L, b = ne.ne_gemm_limb_plan(cfg, bound)
     assert L == 2 and b == cfg.l
+    assert ne.ne_gemm_kernel_for(cfg, L, b, R, Cc, K) == "pair"
     A = gen(O, 80, 4, M, R * K, -bound, bound + 1)
     A[:, 0], A[:, -1] = bound, -bound
     B = O.gen_uniform(80, 5, 0, -128, 128, K * Cc)
@@ -468,6 +470,42 @@ def test_gemm_pair_limb_major(O, M, bound, R, Cc, K):
     ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, limb_bits=b)
     ref = O.op_gemm(ocfg, O.entangle(ocfg, A).reshape(M, R, K), B.reshape(K, Cc)).reshape(M, -1)
     assert (to_np(out) == ref).all()
+
+
+def test_gemm_pair_multi_tile(O):
+    """The pair kernel's multi-tile path (several pair tiles per SM pair: the
+    limb-1 hold in registers, the early tmem_empty release, barrier phase
+    flips across tiles), with the persistent grid capped (ne_gemm_trace with
+    no buffer) at 1 and 2 pairs so a pair walks 6-12 tiles of 3 streams:
+    rows in every 32-lane group of both 128-row halves vs the oracle, and the
+    whole output by a Freivalds identity (x in [-2, 2): |E (B x)| < 2^62)."""
+    M, R, Cc, K = 3, 256, 1024, 4096
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L, b = ne.ne_gemm_limb_plan(cfg, 127)
+    assert ne.ne_gemm_kernel_for(cfg, L, b, R, Cc, K) == "pair"
+    A = gen(O, 82, 4, M, R * K, -127, 128)
+    B = O.gen_uniform(82, 5, 0, -128, 128, K * Cc)
+    planes = torch.empty(M * L * R * K, dtype=torch.int8, device="cuda")
+    ne.ne_entangle_limbs(cfg, to_streams(A), L, planes, limb_bits=b)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    E = O.entangle(ocfg, A).reshape(M, R, K)
+    rows = _band_rows(R, 128, seed=5)
+    ref = O.op_gemm(ocfg, E[:, rows], B.reshape(K, Cc))
+    x = np.random.default_rng(2).integers(-2, 2, size=Cc)
+    bx = B.reshape(K, Cc) @ x
+    for cap in (1, 2):
+        out = empty_streams(M, R * Cc)
+        ne.ne_gemm_trace(None, cap)
+        try:
+            ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, limb_bits=b)
+            torch.cuda.synchronize()
+        finally:
+            ne.ne_gemm_trace(None, 0)
+        got = np.stack([out[m].view(R, Cc)[torch.from_numpy(rows).cuda()].cpu().numpy() for m in range(M)])
+        assert (got == ref).all(), cap
+        for m in range(M):
+            assert (out[m].cpu().numpy().reshape(R, Cc) @ x == E[m] @ bx).all(), (cap, m)
 
 
 def test_gemm_pair_short_k_many_tiles_sampled(O):
@@ -485,11 +523,17 @@ def test_gemm_pair_short_k_many_tiles_sampled(O):
     ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
     out = empty_streams(M, R * Cc)
     ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, limb_bits=b)
-    rows = np.arange(0, R, 128) + np.arange(R // 128) % 128   # one row per 128-row half of every pair tile
-    E = O.entangle(ocfg, A).reshape(M, R, K)[:, rows]
-    ref = O.op_gemm(ocfg, E, B.reshape(K, Cc))
+    assert ne.ne_gemm_kernel_for(cfg, L, b, R, Cc, K) == "pair"
+    rows = _band_rows(R, 128)   # every 32-lane group (epilogue warp quarter) of every 128-row half
+    E = O.entangle(ocfg, A).reshape(M, R, K)
+    ref = O.op_gemm(ocfg, E[:, rows], B.reshape(K, Cc))
     got = np.stack([out[m].view(R, Cc)[torch.from_numpy(rows).cuda()].cpu().numpy() for m in range(M)])
     assert (got == ref).all()
+    # the whole output: Freivalds with x in [-2^8, 2^8) (|E (B x)| <= 2^11 * 2^13 * 2^24 < 2^63)
+    x = np.random.default_rng(1).integers(-2 ** 8, 2 ** 8, size=Cc)
+    bx = B.reshape(K, Cc) @ x
+    for m in range(M):
+        assert (out[m].cpu().numpy().reshape(R, Cc) @ x == E[m] @ bx).all(), m
 
 
 @pytest.mark.parametrize("max_clusters", [1, 3])
@@ -652,13 +696,47 @@ def test_c5_fused_exchange_single_gpu(O, symmetric):
 
 
 # ------------------------------------------------------------------ BASELINE full sizes, bench launch config
-def test_c3_full_size_sampled(O):
-    """C3 at full size through the exact calls bench.py times: sampled rows vs
-    the oracle (delta, d_hat, recovery), every position unflagged, and a
-    Freivalds identity d_hat x == A (B x) over the whole output (exact in int64)."""
+def _band_rows(R, band=256, seed=0):
+    """One row in every 32-row TMEM lane group of every `band`-row pair band:
+    rows band*i + 32*q + j(i, q), so every epilogue warp quarter (q) of every
+    pair tile row band is compared."""
+    return np.array([band * i + 32 * q + (7 * i + 11 * q + seed) % 32
+                     for i in range(R // band) for q in range(band // 32)])
+
+
+def _band_rows_cyclic(R, band=256):
+    """One row per `band`-row pair band, its 32-row lane group (CTA half and
+    TMEM quarter) cycling with the band index: all 8 groups are covered
+    every 8 bands."""
+    return np.array([band * i + 32 * (i % (band // 32)) + (7 * i) % 32 for i in range(R // band)])
+
+
+def _freivalds(O, got, A_rows, Bh, x):
+    """got (R x C int64) == A (B x) for the test vector x (exact in int64:
+    callers size x so that no product wraps)."""
+    return (got @ x == A_rows @ (Bh @ x)).all()
+
+
+@pytest.mark.parametrize("plan", ["pair", "base256"])
+def test_c3_full_size_sampled(O, plan):
+    """C3 at full size through the calls bench.py times.  plan "pair" is the
+    bench default (ne_gemm_limb_plan: L = 2 digits in base 2^22), which the
+    dispatch query confirms runs on the CTA-pair kernel (768 pair tiles over
+    the SM pairs, many tiles per pair); "base256" is the L = 4 single-CTA
+    path.  Checked against the oracle: one row in every 256-row band of
+    every stream, its 32-row lane group cycling through all 8 (delta, d_hat);
+    recovery of every r equal to d_hat in full; the whole d_hat by two Freivalds identities d_hat x == A_m (B x) (exact in
+    int64), and the whole delta as the entanglement of d_hat (Eq. 15 on the
+    oracle side), so every output position of every stream is covered."""
     M, n = 3, 4096
     cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
-    L = ne.ne_gemm_limbs_for(cfg, 64)
+    if plan == "pair":
+        L, b = ne.ne_gemm_limb_plan(cfg, 64)
+        assert (L, b) == (2, 22)
+    else:
+        L, b = ne.ne_gemm_limbs_for(cfg, 64), 8
+        assert L == 4
+    assert ne.ne_gemm_kernel_for(cfg, L, b, n, n, n) == ("pair" if plan == "pair" else "cta")
     A = [torch.empty(n * n, dtype=torch.int32, device="cuda") for _ in range(M)]
     for m in range(M):
         ne.ne_gen_uniform_i32(2, 4, m, -64, 64, A[m])
@@ -666,31 +744,39 @@ def test_c3_full_size_sampled(O):
     ne.ne_gen_uniform_i32(2, 5, 0, -64, 64, B)
     planes = torch.empty(M * L * n * n, dtype=torch.int8, device="cuda")
     Bt = torch.empty(n * n, dtype=torch.int8, device="cuda")
-    delta, dout, drec = empty_streams(M, n * n), empty_streams(M, n * n), empty_streams(M, n * n)
+    delta, dout = empty_streams(M, n * n), empty_streams(M, n * n)
     diag = ne.diag_new()
-    ne.ne_entangle_limbs(cfg, A, L, planes, diag)
+    ne.ne_entangle_limbs(cfg, A, L, planes, diag, b)
     ne.ne_gemm_prep_b(B, n, n, Bt, diag)
-    ne.ne_op_gemm_limbs(cfg, planes, L, Bt, n, n, n, delta)
-    ne.ne_disentangle_check(cfg, delta, 0, dout, None, diag)
-    ne.ne_recover(cfg, [delta[0], None, delta[2]], 1, drec)
+    ne.ne_op_gemm_limbs(cfg, planes, L, Bt, n, n, n, delta, b)
+    bm = torch.empty(n * n // 32, dtype=torch.int32, device="cuda")
+    ne.ne_disentangle_check(cfg, delta, 0, dout, bm, diag)
     d = ne.diag_read(diag)
-    assert d["range_violations"] == 0 and d["fault_positions"] == 0
+    assert d["range_violations"] == 0 and d["fault_positions"] == 0 and int(bm.abs().sum()) == 0
+    del planes, Bt
     Bh = O.gen_uniform(2, 5, 0, -64, 64, n * n).reshape(n, n)
-    for row in (0, 1, 2047, 4095):
-        Arow = np.stack([O.gen_uniform(2, 4, m, -64, 64, n, row * n) for m in range(M)])
-        E = O.entangle(ocfg, Arow)
-        dref = O.op_gemm(ocfg, E.reshape(M, 1, n), Bh).reshape(M, n)
-        sl = slice(row * n, (row + 1) * n)
-        assert (np.stack([t[sl].cpu().numpy() for t in delta]) == dref).all()
-        plain = O.op_gemm(ocfg, Arow.reshape(M, 1, n), Bh).reshape(M, n)
-        assert (np.stack([t[sl].cpu().numpy() for t in dout]) == plain).all()
-        assert (np.stack([t[sl].cpu().numpy() for t in drec]) == plain).all()
+    rows = _band_rows_cyclic(n)
+    Ar = np.stack([np.stack([O.gen_uniform(2, 4, m, -64, 64, n, int(r) * n) for r in rows]) for m in range(M)])
+    dref = O.op_gemm(ocfg, O.entangle(ocfg, Ar.reshape(M, -1)).reshape(M, len(rows), n), Bh)
+    plain, _, nf = O.disentangle_check(ocfg, dref.reshape(M, -1), 0)
+    assert nf == 0
+    plain = plain.reshape(M, len(rows), n)
+    ridx = torch.from_numpy(rows).cuda()
+    assert (np.stack([t.view(n, n)[ridx].cpu().numpy() for t in delta]) == dref).all()
+    assert (np.stack([t.view(n, n)[ridx].cpu().numpy() for t in dout]) == plain).all()
+    for r in range(M):
+        drec = empty_streams(M, n * n)
+        ne.ne_recover(cfg, [None if m == r else delta[m] for m in range(M)], r, drec)
+        assert all(torch.equal(x, y) for x, y in zip(drec, dout)), r
+        del drec
     rng = np.random.default_rng(0)
-    x = rng.integers(-2 ** 20, 2 ** 20, size=n)
-    Bx = Bh @ x
+    X = [rng.integers(-2 ** 20, 2 ** 20, size=n) for _ in range(2)]   # |A(Bx)| <= 2^12 * 2^6 * 2^38 < 2^63
+    DH = to_np(dout)
     for m in range(M):
-        Am = torch.stack([A[m]]).cpu().numpy().astype(np.int64).reshape(n, n)
-        assert (dout[m].cpu().numpy().reshape(n, n) @ x == Am @ Bx).all()
+        Am = A[m].cpu().numpy().astype(np.int64).reshape(n, n)
+        for x in X:
+            assert _freivalds(O, DH[m].reshape(n, n), Am, Bh, x), m
+    assert (to_np(delta) == O.entangle(ocfg, DH)).all()
 
 
 def test_c4_full_size_sampled(O):
@@ -732,24 +818,51 @@ def test_c4_full_size_sampled(O):
         assert (DH[:, b] == O.op_inner(ocfg, cb, vh, Bk)[:, 0]).all()
 
 
-def test_c5_full_size_single_gpu_sampled(O):
-    """C5 at full size on one GPU (8 streams local): no flags, recovery of
-    stream 3 equals the checked outputs, sampled entries vs the oracle."""
-    from paper_1604_04740_b200.dist import C5Plan, GpuBackend, c5_run
+def test_c5_full_size_single_gpu_protocol(O):
+    """C5 at full size on one GPU (all 8 streams local), SURVEY §8(c) parity
+    protocol 5: no position flagged; sampled entries of rows in every
+    128-row tile band vs the oracle; two Freivalds identities d_hat_m x ==
+    A_m (B x) over the WHOLE checked output of every stream (x in
+    [-2^20, 2^20): |B x| <= 2^39, |A (B x)| <= 2^58, exact in int64); and the
+    fail-stop of EVERY stream r = 0..7 recovered from the other 7 equals the
+    checked d_hat in full (Props 1/3)."""
+    import dataclasses
+
+    from paper_1604_04740_b200.dist import C5Plan, GpuBackend, c5_setup, c5_step
 
     plan = C5Plan()
-    res = c5_run(GpuBackend(plan.M, plan.bound), plan)
+    M, K, cols, R = plan.M, plan.K, plan.cols, plan.rows
+    be = GpuBackend(M, plan.bound)
+    inp = c5_setup(be, plan)
+    res = c5_step(be, plan, inp, verify=True)
     assert res["flagged"] == 0 and res["checksum_ok"] is True
     _, d = res["check_slice"]
-    M, K, cols = plan.M, plan.K, plan.cols
+    assert all(t.numel() == R * cols for t in d)
+    chk = [t.clone() for t in d]
+    for r in range(M):
+        rr = c5_step(be, dataclasses.replace(plan, kill=r), inp, verify=False)
+        _, drec = rr["recover_slice"]
+        assert all(torch.equal(x, y) for x, y in zip(drec, chk)), r
+    # whole-output Freivalds per stream
+    Bh = O.gen_uniform(plan.seed, 5, 0, -32, 32, K * cols).reshape(K, cols)
+    rng = np.random.default_rng(5)
+    X = [rng.integers(-2 ** 20, 2 ** 20, size=cols) for _ in range(2)]
+    BX = [Bh @ x for x in X]
+    for m in range(M):
+        Am = O.gen_uniform(plan.seed, 4, m, -32, 32, R * K).reshape(R, K)
+        Dm = chk[m].cpu().numpy().reshape(R, cols)
+        for x, bx in zip(X, BX):
+            assert (Dm @ x == Am @ bx).all(), m
+        del Am, Dm
+    # sampled entries vs the oracle's own product
     cols_s = np.array([0, 1, 777, 8191, 16383])
-    Bs = np.stack([O.gen_uniform(plan.seed, 5, 0, -32, 32, 1, int(k) * cols + int(j)) [0]
-                   for k in range(K) for j in cols_s]).reshape(K, len(cols_s))
-    for row in (0, plan.rows - 1):
-        Arow = np.stack([O.gen_uniform(plan.seed, 4, m, -32, 32, K, row * K) for m in range(M)])
+    Bs = Bh[:, cols_s]
+    rows = np.arange(0, R, 128) + (np.arange(R // 128) * 37) % 128
+    for row in rows[::4]:
+        Arow = np.stack([O.gen_uniform(plan.seed, 4, m, -32, 32, K, int(row) * K) for m in range(M)])
         plain = O.op_gemm(O.config_for(M, 64), Arow.reshape(M, 1, K), Bs).reshape(M, -1)
-        got = np.stack([d[m][row * cols + cols_s].cpu().numpy() for m in range(M)])
-        assert (got == plain).all()
+        got = np.stack([chk[m][int(row) * cols + cols_s].cpu().numpy() for m in range(M)])
+        assert (got == plain).all(), row
 
 
 # ------------------------------------------------------------------ ABFT comparison baseline (NEXT-1)
