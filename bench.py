@@ -159,10 +159,19 @@ class Workload:
 
     def _time(self, fn, reps):
         """ms per call of fn, captured once in a CUDA graph and replayed: the
-        same launch path as the timed step, so plain and entangled compare."""
+        same launch path as the timed step, so plain and entangled compare
+        (eager launches when the step holds a collective, as the timed run)."""
         torch = self.torch
         fn()
         torch.cuda.synchronize()
+        if getattr(self, "eager_only", False):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / reps
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             fn()
@@ -176,8 +185,26 @@ class Workload:
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps
 
-    def work_per_step(self):  # metric units per step (before /time)
+    def work_per_step(self):  # metric units per step of THIS rank (before /time)
         raise NotImplementedError
+
+    # ---- multi-GPU: "strong" partitions the stated problem
+    # over the ranks (value = the whole problem / max-over-ranks time);
+    # "weak" runs one independent replica per rank (per-rank seeds)
+    partitioned = False
+    has_collective = False   # a collective inside the step (timed eagerly: not graph-captured)
+    partition_note = "single GPU: the whole problem on one rank"
+
+    def setup_partition(self, rank, world, scaling, seed):
+        self.rank, self.world = rank, world
+        self.partitioned = scaling == "strong" and world > 1
+        return seed + 1000 * rank if (scaling == "weak" and world > 1) else seed
+
+    def job_work(self):
+        """Metric units of the whole job per step (all ranks)."""
+        if self.partitioned:
+            return self.global_work()
+        return self.work_per_step() * getattr(self, "world", 1)
 
     def stage_info(self):  # stage -> (bound, algorithmic amount per launch, unit)
         raise NotImplementedError
@@ -193,9 +220,10 @@ class C3Gemm(Workload):
     E2E_OUT = ("dout",)
 
     def __init__(self, rank, n=4096, seed=2, algo="tc", scheme="entangled", limbs="plan", fuse=True,
-                 paper_shape=None):
+                 paper_shape=None, world=1, scaling="strong"):
         import torch
         import paper_1604_04740_b200 as ne
+        from paper_1604_04740_b200.dist import part_range
 
         self.ne, self.torch = ne, torch
         self.M, self.rows, self.cols, self.K = 3, n, n, n
@@ -208,7 +236,19 @@ class C3Gemm(Workload):
             self.M, self.true_shape = Mp, (Rt, Ct, Kt)
             self.rows, self.cols, self.K = -(-Rt // 128) * 128, -(-Ct // 256) * 256, -(-Kt // 128) * 128
             self.name = f"C3P_M{Mp}_N{Kt}"
-        self.seed = seed + 1000 * rank
+        if scaling == "strong" and world > 1 and (paper_shape is not None or self.rows % (256 * world)):
+            scaling = "weak"
+            self.partition_note = "replicas (the row split needs whole 256-row pair bands per rank)"
+        self.seed = self.setup_partition(rank, world, scaling, seed)
+        self.rows_global, self.r0 = self.rows, 0
+        if self.partitioned:
+            # rows of every A_m split over the ranks (all M streams per rank: the check stays local);
+            # B replicated, generated from the seed on every rank outside the timing
+            self.r0, r1 = part_range(self.rows, world, rank, 256)
+            self.rows = r1 - self.r0
+            self.partition_note = (f"rows [{self.r0}, {r1}) of every A_m (all M = {self.M} streams) on rank {rank} "
+                                   f"of {world}; B replicated (regenerated from the seed, untimed); no collective in "
+                                   "the step, counters all-reduced after it")
         self.cfg = ne.ne_config_for(self.M)
         if limbs == "base256":
             self.L, self.limb_bits = ne.ne_gemm_limbs_for(self.cfg, 64), 8
@@ -223,7 +263,7 @@ class C3Gemm(Workload):
         if self.true_shape is None:
             self.A = [torch.empty(R * K, dtype=torch.int32, device=dev) for _ in range(M)]
             for m in range(M):
-                ne.ne_gen_uniform_i32(self.seed, 4, m, -64, 64, self.A[m])
+                ne.ne_gen_uniform_i32(self.seed, 4, m, -64, 64, self.A[m], self.r0 * K)
             self.B = torch.empty(K * Cc, dtype=torch.int32, device=dev)
             ne.ne_gen_uniform_i32(self.seed, 5, 0, -64, 64, self.B)
         else:
@@ -244,7 +284,7 @@ class C3Gemm(Workload):
         self.drec = [torch.empty(R * Cc, dtype=torch.int64, device=dev) for _ in range(M)]
         self.bitmap = torch.empty(R * Cc // 32, dtype=torch.int32, device=dev)
         self.diag = ne.diag_new()
-        if algo == "imad":
+        if algo in ("imad", "imad64"):
             self.eps = [torch.empty(R * K, dtype=torch.int64, device=dev) for _ in range(M)]
         self.launches_per_step = 4 if self.fuse else 5
         self.counters = torch.zeros(ne.ne_gemm_check_workspace(R, Cc) // 4, dtype=torch.int32, device=dev)
@@ -274,11 +314,14 @@ class C3Gemm(Workload):
                 ("check", lambda: ne.ne_abft_check(cfg, self.delta, self.e, self.bitmap, self.diag)),
                 ("recover", lambda: ne.ne_abft_recover(cfg, rr, self.e, r, self.drec[r])),
             ]
-        if self.algo == "imad":
+        if self.algo in ("imad", "imad64"):
+            # CUDA-core comparison point: one IMAD.WIDE (32 x 32 -> 64) per MAC — C3's entangled
+            # operand fits int32 (|eps| <= 64 (2^22 + 1)) — or the any-operand 64-bit form
+            ia = ne.NE_GEMM_IMAD32W if self.algo == "imad" else ne.NE_GEMM_IMAD64
             return [
                 ("entangle", lambda: ne.ne_entangle(cfg, self.A, self.eps, self.diag)),
                 ("gemm", lambda: ne.ne_op_gemm(cfg, self.eps, self.B, self.rows, self.cols, self.K, self.delta,
-                                               algo=ne.NE_GEMM_IMAD64)),
+                                               algo=ia, diag=self.diag)),
                 ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
                 ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
             ]
@@ -305,6 +348,9 @@ class C3Gemm(Workload):
     def work_per_step(self):
         R, Cc, K = self.true_shape or (self.rows, self.cols, self.K)
         return 2 * self.M * R * Cc * K / 1e9  # G int64-equivalent ops (true shape)
+
+    def global_work(self):
+        return 2 * self.M * self.rows_global * self.cols * self.K / 1e9
 
     def stage_info(self):
         M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
@@ -400,8 +446,8 @@ class C3Gemm(Workload):
         the paper shapes: the first rows of the true (unpadded) operand."""
         if self.true_shape is not None:
             return np.arange(rows_sample)
-        band = self.rows // rows_sample
-        return np.array([band * i + 32 * (i % 8) % band + (7 * i) % 32 for i in range(rows_sample)])
+        band = max(32, self.rows // rows_sample)
+        return np.array([(band * i + 32 * (i % 8) % band + (7 * i) % 32) % self.rows for i in range(rows_sample)])
 
     def oracle_sample(self, rows_sample):
         import oracle as O
@@ -411,8 +457,8 @@ class C3Gemm(Workload):
             _, Cc, K = self.true_shape
         rows = self.sample_rows(rows_sample)
         ocfg = O.config_for(M, 64)
-        A = np.stack([np.concatenate([O.gen_uniform(self.seed, 4, m, -64, 64, K, int(r) * K) for r in rows])
-                      for m in range(M)])
+        A = np.stack([np.concatenate([O.gen_uniform(self.seed, 4, m, -64, 64, K, (self.r0 + int(r)) * K)
+                                      for r in rows]) for m in range(M)])
         B = O.gen_uniform(self.seed, 5, 0, -64, 64, K * Cc).reshape(K, Cc)
         t0 = time.perf_counter()
         E = O.entangle(ocfg, A)
@@ -448,12 +494,19 @@ class C4PermInner(Workload):
     E2E_IN = ("c",)
     E2E_OUT = ("dout",)
 
-    def __init__(self, rank, n=1 << 28, seed=3, layout="aos", w=64):
+    def __init__(self, rank, n=1 << 28, seed=3, layout="aos", w=64, world=1, scaling="strong"):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
         self.M, self.n, self.B, self.layout, self.w = 4, n, 1024, layout, w
+        self.b0 = 0   # first output block this rank checks
+        if scaling == "strong" and world > 1 and (layout != "aos" or w != 64):
+            scaling = "weak"
+            self.partition_note = "replicas (the stream placement is built for the default w = 64 layout)"
+        if scaling == "strong" and world > 1:
+            self._init_placement(rank, world, seed)
+            return
         if layout != "aos":
             self.name = "C4_soa"
         # w = 32 containers (NEXT-3): C4's own range (block sums up to 2^34) does
@@ -485,7 +538,83 @@ class C4PermInner(Workload):
         self.diag = ne.diag_new()
         self.launches_per_step = 3
 
+    def _init_placement(self, rank, world, seed):
+        """one entangled stream per GPU (streams m = rank mod
+        world when world <= M; at world = 2M each stream on 2 GPUs, each
+        computing half of its output blocks).  The global permutation stays
+        local to a stream (every rank holds pi and its streams' eps in full:
+        no all-to-all over 2^28 elements); c_{m-1} for Eq. 15 is regenerated
+        from the seed.  After the gathers, an all_gather of the per-stream
+        block sums (M x 2^18 int64) gives every rank all M streams of every
+        block, and rank r checks and recovers its own range of blocks."""
+        import torch
+        from paper_1604_04740_b200.dist import c4_payload, part_range
+
+        ne, n, M = self.ne, self.n, self.M
+        self.seed = self.setup_partition(rank, world, "strong", seed)
+        self.cfg = ne.ne_config_for(M, 64)
+        self.vr = 1 << 12
+        self.nb = n // self.B
+        self.items = c4_payload(M, world, rank, self.nb)
+        self.owned = sorted({m for m, _, _ in self.items})
+        need = sorted(set(self.owned) | {(m - 1) % M for m in self.owned})
+        dev = "cuda"
+        self.cgen = {}
+        for m in need:
+            t = torch.empty(n, dtype=torch.int32, device=dev)
+            ne.ne_gen_uniform_i32(self.seed, 1, m, -self.vr, self.vr, t)
+            self.cgen[m] = t
+        self.c = [self.cgen[m] for m in need]   # the step's inputs (e2e H2D), read through self.c by the step
+        self.cidx = {m: i for i, m in enumerate(need)}
+        self.perm = torch.empty(n, dtype=torch.int32, device=dev)
+        ne.ne_gen_perm_i32(self.seed, 6, self.perm)
+        self.v = torch.empty(self.B, dtype=torch.int32, device=dev)
+        ne.ne_gen_uniform_i32(self.seed, 7, 0, -self.vr, self.vr, self.v)
+        self.eps_s = {m: torch.empty(n, dtype=torch.int64, device=dev) for m in self.owned}
+        self.pay = [torch.empty(hi - lo, dtype=torch.int64, device=dev) for _, lo, hi in self.items]
+        self.b0, b1 = part_range(self.nb, world, rank, 32)
+        nc = b1 - self.b0
+        self.delta = [torch.zeros(nc, dtype=torch.int64, device=dev) for _ in range(M)]
+        self.dout = [torch.empty(nc, dtype=torch.int64, device=dev) for _ in range(M)]
+        self.drec = [torch.empty(nc, dtype=torch.int64, device=dev) for _ in range(M)]
+        self.bitmap = torch.empty((nc + 31) // 32, dtype=torch.int32, device=dev)
+        self.diag = ne.diag_new()
+        self.partitioned, self.has_collective = True, True
+        self.placement = True
+        self.launches_per_step = len(self.owned) + len(self.items) + 2
+        self.partition_note = (f"stream placement: rank {rank} of {world} entangles stream(s) {self.owned} and gathers "
+                               f"+ inner-products block range(s) {[(m, lo, hi) for m, lo, hi in self.items]}; "
+                               f"all_gather of the M x {self.nb} block sums; checks/recovers blocks "
+                               f"[{self.b0}, {b1})")
+
+    def _placement_stages(self, i):
+        from paper_1604_04740_b200.dist import c4_allgather
+
+        ne, cfg, M, B = self.ne, self.cfg, self.M, self.B
+        r = i % M
+        nc = self.dout[0].numel()
+
+        def entangle():
+            for m in self.owned:
+                ne.ne_entangle_stream(cfg, m, self.c[self.cidx[m]], self.c[self.cidx[(m - 1) % M]], self.eps_s[m],
+                                      self.diag)
+
+        def gather_inner():
+            for (m, lo, hi), out in zip(self.items, self.pay):
+                ne.ne_op_permute_inner_stream(cfg, self.eps_s[m], self.perm, self.v, B, lo, hi - lo, out)
+
+        def exchange():
+            full = c4_allgather(self.pay, M, self.nb)
+            self.delta = [t[self.b0:self.b0 + nc] for t in full]
+
+        return [("entangle", entangle), ("permute_inner", gather_inner), ("allgather", exchange),
+                ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
+                ("recover", lambda: ne.ne_recover(cfg, [None if m == r else self.delta[m] for m in range(M)], r,
+                                                  self.drec))]
+
     def stages(self, i):
+        if getattr(self, "placement", False):
+            return self._placement_stages(i)
         ne, cfg = self.ne, self.cfg
         r = i % 4
         part = [None if m == r else self.delta[m] for m in range(4)]
@@ -518,8 +647,19 @@ class C4PermInner(Workload):
             return self.n * (32 + 20) / 1e9
         return self.n * (48 + 36) / 1e9
 
+    def global_work(self):  # the whole C4 problem's algorithmic bytes (the single-GPU AoS accounting)
+        return self.n * (48 + 36) / 1e9
+
     def stage_info(self):
         n, nb = self.n, self.nb
+        if getattr(self, "placement", False):
+            npos = sum(hi - lo for _, lo, hi in self.items) * self.B
+            nc = self.dout[0].numel()
+            return {"entangle": ("hbm", len(self.owned) * n * 16 / 1e9, "GB"),
+                    "permute_inner": ("hbm", npos * 12 / 1e9, "GB"),
+                    "allgather": ("nvlink", self.M * nb * 8 / 1e9, "GB"),
+                    "check": ("hbm", nc * self.M * 16 / 1e9, "GB"),
+                    "recover": ("hbm", nc * 7 * 8 / 1e9, "GB")}
         if self.w == 32:
             return {"entangle": ("hbm", n * 32 / 1e9, "GB"),
                     "permute_inner_check": ("hbm", (n * 20 + nb * 4 * 8) / 1e9, "GB"),
@@ -548,7 +688,7 @@ class C4PermInner(Workload):
         """Same gather + inner kernel on plain (unentangled) data in the same
         int64 AoS containers, no check: the paper's conventional routine."""
         torch, ne = self.torch, self.ne
-        if self.layout != "aos" or self.w != 64:
+        if self.layout != "aos" or self.w != 64 or getattr(self, "placement", False):
             return {}
         plain = torch.stack([x.to(torch.int64) for x in self.c], dim=1).reshape(-1).contiguous()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -572,7 +712,7 @@ class C4PermInner(Workload):
         ocfg = O.config_for(4, self.w)
         n, B, vr = self.n, self.B, self.vr
         t0 = time.perf_counter()
-        idx = O.gen_perm(self.seed, 6, n, blocks * B, 0)
+        idx = O.gen_perm(self.seed, 6, n, blocks * B, self.b0 * B)
         v = O.gen_uniform(self.seed, 7, 0, -vr, vr, B)
         c = np.stack([np.concatenate([O.gen_uniform(self.seed, 1, m, -vr, vr, 1, int(p)) for p in idx])
                       for m in range(4)])
@@ -606,9 +746,11 @@ class C2Conv(Workload):
     E2E_IN = ("c", "g")
     E2E_OUT = ("dout",)
 
-    def __init__(self, rank, n=65536, taps=64, seed=1, M=3, algo="tc", paper=False, fuse=True, scheme="entangled"):
+    def __init__(self, rank, n=65536, taps=64, seed=1, M=3, algo="tc", paper=False, fuse=True, scheme="entangled",
+                 world=1, scaling="strong"):
         import torch
         import paper_1604_04740_b200 as ne
+        from paper_1604_04740_b200.dist import HALO, part_range
 
         self.ne, self.torch = ne, torch
         self.M, self.n, self.T, self.algo, self.paper = M, n, taps, algo, paper
@@ -616,15 +758,38 @@ class C2Conv(Workload):
         self.fuse = fuse and algo == "direct"  # the direct conv kernel carries the fused check
         if paper:
             self.name = "C2P"
-        self.seed = seed + 1000 * rank
+        if scaling == "strong" and world > 1 and not (algo == "direct" and self.fuse and taps - 1 <= HALO):
+            scaling = "weak"   # only the direct fused conv has the halo partition; the others run replicas
+            self.partition_note = "replicas (the halo partition exists for the direct fused conv only)"
+        self.seed = self.setup_partition(rank, world, scaling, seed)
+        self.n_global, self.lo, self.halo = n, 0, 0
+        if self.partitioned:
+            # contiguous position ranges + a circular halo of HALO >= T - 1 positions from rank - 1
+            self.lo, hi = part_range(n, world, rank, 32)
+            self.n = n = hi - self.lo
+            self.halo = HALO
+            self.has_collective = True
+            self.partition_note = (f"positions [{self.lo}, {hi}) of all M streams on rank {rank} of {world}, plus a "
+                                   f"halo of the previous rank's last {HALO} entangled positions per stream "
+                                   f"(send/recv, {HALO * M * 8} B per rank and step); the conv runs over the "
+                                   f"extended range and its own positions are exact (T - 1 = {taps - 1} <= {HALO})")
         self.cfg = ne.ne_config_for(M)
         self.c = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(M)]
         for m in range(M):
-            ne.ne_gen_uniform_i32(self.seed, 1, m, -128, 128, self.c[m])
+            ne.ne_gen_uniform_i32(self.seed, 1, m, -128, 128, self.c[m], self.lo)
         self.g = torch.empty(taps, dtype=torch.int32, device="cuda")
         ne.ne_gen_uniform_i32(self.seed, 3, 0, -128, 128, self.g)
-        mk = lambda: [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(M)]  # noqa: E731
-        self.delta, self.dout, self.drec = mk(), mk(), mk()
+        H = self.halo
+        mk = lambda: [torch.empty(H + n, dtype=torch.int64, device="cuda") for _ in range(M)]  # noqa: E731
+        if H:
+            # extended buffers: [halo | own positions]; the own part starts 8 H = 512 B in (16-B aligned)
+            self.eps_ext, self.delta_ext, self.dout_ext = mk(), mk(), mk()
+            self.delta = [t[H:] for t in self.delta_ext]
+            self.dout = [t[H:] for t in self.dout_ext]
+            self.drec = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(M)]
+            self.E2E_OUT = ("dout_ext",)
+        else:
+            self.delta, self.dout, self.drec = mk(), mk(), mk()
         if algo == "tc":
             # c in [-128, 127] (U[-128, 128)): exactly the int8 range, so eps = c_m + 2^l c_{m-1}
             # is its two int8 halves (the pair plan; |c| <= 127 in the plan's symmetric terms
@@ -641,10 +806,12 @@ class C2Conv(Workload):
                 self.e = torch.empty(n, dtype=torch.int64, device="cuda")
             self.Gt = torch.empty(self.block * self.kpad, dtype=torch.int8, device="cuda")
             self.launches_per_step = 5 + (1 if n % 128 else 0)
+        elif H:
+            self.launches_per_step = 3   # + the halo send/recv (NCCL)
         else:
             self.eps = mk()
             self.launches_per_step = 3 if self.fuse else 4
-        self.bitmap = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+        self.bitmap = torch.empty((H + n + 31) // 32, dtype=torch.int32, device="cuda")
         self.diag = ne.diag_new()
 
     def stages(self, i):
@@ -670,6 +837,15 @@ class C2Conv(Workload):
                     ("prep_g", lambda: ne.ne_conv_prep_taps(self.g, 0, self.Gt, self.diag, self.block)),
                     ("conv", lambda: ne.ne_op_conv_limbs(cfg, self.planes, self.L, self.Gt, self.n, self.T, 0,
                                                          self.delta, self.limb_bits, self.block))] + tail
+        if self.halo:
+            from paper_1604_04740_b200.dist import halo_exchange
+
+            H = self.halo
+            return [("entangle", lambda: ne.ne_entangle(cfg, self.c, [t[H:] for t in self.eps_ext], self.diag)),
+                    ("halo", lambda: halo_exchange(self.eps_ext, H, self.n)),
+                    ("conv_check", lambda: ne.ne_op_conv_check(cfg, self.eps_ext, self.g, self.delta_ext, 0,
+                                                               self.dout_ext, self.bitmap, self.diag)),
+                    tail[1]]
         if self.fuse:
             return [("entangle", lambda: ne.ne_entangle(cfg, self.c, self.eps, self.diag)),
                     ("conv_check", lambda: ne.ne_op_conv_check(cfg, self.eps, self.g, self.delta, 0, self.dout,
@@ -680,6 +856,9 @@ class C2Conv(Workload):
 
     def work_per_step(self):
         return 2 * self.M * self.n * self.T / 1e9
+
+    def global_work(self):
+        return 2 * self.M * self.n_global * self.T / 1e9
 
     def stage_info(self):
         n, M, T = self.n, self.M, self.T
@@ -760,7 +939,7 @@ class C2Conv(Workload):
 
         M = self.M
         ocfg = O.config_for(M, 64)
-        c = np.stack([O.gen_uniform(self.seed, 1, m, -128, 128, self.n) for m in range(M)])
+        c = np.stack([O.gen_uniform(self.seed, 1, m, -128, 128, self.n_global) for m in range(M)])
         g = O.gen_uniform(self.seed, 3, 0, -128, 128, self.T)
         if self.paper:
             # bounded sample: the same pipeline at N' = 16384 (same M, taps, distributions)
@@ -780,13 +959,15 @@ class C2Conv(Workload):
             d = O.op_conv(ocfg, eps, g)
             dh, _, _ = O.disentangle_check(ocfg, d, 0)
         dt = time.perf_counter() - t0
-        self._oref = (0, d, dh)
-        return dt, reps * self.work_per_step(), f"{reps} full C2 passes"
+        a, b = self.lo, self.lo + self.n   # this rank's positions (all of them on one GPU)
+        self._oref = (a, d[:, a:b], dh[:, a:b])
+        return dt, reps * self.global_work(), f"{reps} full C2 passes"
 
     def oracle_compare(self):
         if getattr(self, "_oref", None) is None or self.scheme != "entangled":
             return None
-        lo, D, d = self._oref
+        glo, D, d = self._oref   # global position of the first compared output
+        lo = glo - self.lo
         hi = lo + D.shape[1]
         got_d = np.stack([t[lo:hi].cpu().numpy() for t in self.delta])
         got = np.stack([t[lo:hi].cpu().numpy() for t in self.dout])
@@ -805,23 +986,31 @@ class C1Chain(Workload):
     E2E_IN = ("c", "a")
     E2E_OUT = ("dout",)
 
-    def __init__(self, rank, n=4096, seed=0, w=64, fuse=True):
+    def __init__(self, rank, n=4096, seed=0, w=64, fuse=True, world=1, scaling="strong"):
         import torch
         import paper_1604_04740_b200 as ne
+        from paper_1604_04740_b200.dist import part_range
 
         self.ne, self.torch = ne, torch
         self.M, self.n, self.w, self.fuse = 3, n, w, fuse
         if (n, w) != (4096, 64):
             self.name = f"C1_w{w}_n{n}"  # traffic.json key of the sweep lines
-        self.seed = seed + 1000 * rank
+        self.seed = self.setup_partition(rank, world, scaling, seed)
+        self.n_global, self.lo = n, 0
+        if self.partitioned:
+            # contiguous position ranges, all M streams of a range on this rank (whole bitmap words)
+            self.lo, hi = part_range(n, world, rank, 32)
+            self.n = n = hi - self.lo
+            self.partition_note = (f"positions [{self.lo}, {hi}) of all M streams on rank {rank} of {world}; "
+                                   "a1-a5 local, counters all-reduced after the step")
         self.cfg = ne.ne_config_for(3, w)
         dt = torch.int64 if w == 64 else torch.int32
         mk32 = lambda: [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3)]  # noqa: E731
         mk = lambda: [torch.empty(n, dtype=dt, device="cuda") for _ in range(3)]  # noqa: E731
         self.c, self.a = mk32(), mk32()
         for m in range(3):
-            ne.ne_gen_uniform_i32(self.seed, 1, m, -1024, 1024, self.c[m])
-            ne.ne_gen_uniform_i32(self.seed, 2, m, -1024, 1024, self.a[m])
+            ne.ne_gen_uniform_i32(self.seed, 1, m, -1024, 1024, self.c[m], self.lo)
+            ne.ne_gen_uniform_i32(self.seed, 2, m, -1024, 1024, self.a[m], self.lo)
         self.eps, self.alpha, self.dout, self.drec = mk(), mk(), mk(), mk()
         self.bitmap = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
         self.diag = ne.diag_new()
@@ -862,6 +1051,9 @@ class C1Chain(Workload):
 
     def work_per_step(self):
         return self.n / 1e9
+
+    def global_work(self):
+        return self.n_global / 1e9
 
     def stage_info(self):
         n, B = self.n, self.w // 8
@@ -904,8 +1096,8 @@ class C1Chain(Workload):
 
         ocfg = O.config_for(3, self.w)
         ns = min(self.n, 1 << 16)
-        c = np.stack([O.gen_uniform(self.seed, 1, m, -1024, 1024, ns) for m in range(3)])
-        a = np.stack([O.gen_uniform(self.seed, 2, m, -1024, 1024, ns) for m in range(3)])
+        c = np.stack([O.gen_uniform(self.seed, 1, m, -1024, 1024, ns, self.lo) for m in range(3)])
+        a = np.stack([O.gen_uniform(self.seed, 2, m, -1024, 1024, ns, self.lo) for m in range(3)])
         t0 = time.perf_counter()
         for _ in range(reps):
             d = O.op_add(ocfg, O.op_scale(ocfg, O.entangle(ocfg, c), 37), O.entangle(ocfg, a))
@@ -930,21 +1122,22 @@ ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c2p": (1, 1), "c3": (16, 2), "
                  "c5": (4096, 512)}  # (cpu_baseline, per reference-arm step)
 
 
-def make_workload(args, rank):
+def make_workload(args, rank, world=1):
+    kw = dict(world=world, scaling=args.scaling)
     if args.workload == "c3":
-        return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=bool(args.fuse or 0))
+        return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=bool(args.fuse or 0), **kw)
     if args.workload == "c3p":
         return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=bool(args.fuse or 0),
-                      paper_shape=(args.streams, 2000, 1200, args.kdim))
+                      paper_shape=(args.streams, 2000, 1200, args.kdim), **kw)
     if args.workload == "c2":
-        return C2Conv(rank, algo=args.conv or "direct", fuse=bool(args.fuse if args.fuse is not None else 1))
+        return C2Conv(rank, algo=args.conv or "direct", fuse=bool(args.fuse if args.fuse is not None else 1), **kw)
     if args.workload == "c2p":
         return C2Conv(rank, n=10 ** 6, taps=args.taps, M=args.streams, algo=args.conv or "tc", paper=True,
-                      scheme=args.scheme)
+                      scheme=args.scheme, **kw)
     if args.workload == "c4":
-        return C4PermInner(rank, layout=args.layout, w=args.w)
+        return C4PermInner(rank, layout=args.layout, w=args.w, **kw)
     if args.workload == "c1":
-        return C1Chain(rank, n=args.n or 4096, w=args.w, fuse=bool(args.fuse if args.fuse is not None else 1))
+        return C1Chain(rank, n=args.n or 4096, w=args.w, fuse=bool(args.fuse if args.fuse is not None else 1), **kw)
     return WORKLOADS[args.workload](rank)
 
 
@@ -1135,7 +1328,8 @@ def run_c5(args, rank, world, local_rank):
         fs = {"real": True, "dead_rank": plan.kill, "view": rf["view"],
               "detect_s_host": round(time.perf_counter() - t0, 3),
               "stages_ms": {k: round(v, 3) for k, v in st.items()},
-              "recovered_stream": rf.get("recovered_stream"), "new_world": rf.get("new_world")}
+              "recovered_stream": rf.get("recovered_stream"), "new_world": rf.get("new_world"),
+              "reform": rf.get("reform")}
         rank = dist.get_rank()
     if rank != 0:
         return None
@@ -1239,8 +1433,12 @@ def run_ours(args, rank, world, local_rank):
 
     ne.lib()
     torch.cuda.set_device(local_rank)
-    W = make_workload(args, rank)
+    W = make_workload(args, rank, world)
     torch.cuda.synchronize()
+    # a step with a collective inside (C2 halo, C4 all_gather at N > 1) is
+    # timed as eager launches: the collective is not captured into the graph
+    use_graph = bool(args.graph) and not (world > 1 and W.has_collective)
+    W.eager_only = not use_graph
 
     def barrier():
         if world > 1:
@@ -1276,7 +1474,7 @@ def run_ours(args, rank, world, local_rank):
                 for j, nm in enumerate(names)}
     eager_ms = total_ms / args.steps
     flush_l2 = W.e2e_bytes() < (512 << 20)
-    if args.graph:
+    if use_graph:
         # the same steps captured once per recovered stream r and replayed: removes
         # the per-call host launch overhead of launch-bound configs (C1, C2)
         graphs = []
@@ -1317,7 +1515,7 @@ def run_ours(args, rank, world, local_rank):
             total_ms = g0.elapsed_time(g1)
     clk.stop()
     eager_stage_ms = stage_ms
-    if args.graph:
+    if use_graph:
         # per-stage device time inside the replayed step: the same per-r graphs
         # captured again with event-record nodes between the stages (separate
         # graphs, so the timed replays above carry no extra nodes); each replay
@@ -1328,7 +1526,7 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = W.work_per_step() * world / (ms_per_step / 1e3)
+    value = W.job_work() / (ms_per_step / 1e3)   # the whole job (all ranks) per max-over-ranks step time
 
     # correctness sentinel of the timed run: no range violation, no flagged position
     dg = ne.diag_read(W.diag)
@@ -1369,12 +1567,19 @@ def run_ours(args, rank, world, local_rank):
         e2e_ms = float(t.item())
 
     plain = W.plain_times()
+    # every rank runs the overhead pipelines (a partitioned step may hold a collective)
+    ovh = overhead_block(W, plain) if plain else None
+    if world > 1 and ovh is not None:
+        t = torch.tensor([ovh["entangled_nofault"]["ms"], ovh["failstop_recover"]["ms"]], device="cuda",
+                         dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ovh["entangled_nofault"]["ms"], ovh["failstop_recover"]["ms"] = round(float(t[0]), 4), round(float(t[1]), 4)
     if rank != 0:
         return None
 
     peaks, peak_src = load_peaks()
     info = W.stage_info()
-    dom = max(stage_ms, key=stage_ms.get)
+    dom = max((k for k in stage_ms if info.get(k, ("",))[0] in ("hbm", "tensor", "alu")), key=stage_ms.get)
     bound, amount, unit = info[dom]
     achieved = amount / (stage_ms[dom] / 1e3)
     if bound == "hbm":
@@ -1397,13 +1602,14 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if W.partitioned else "weak",
         "vs_baseline": None,
         "dtype": "int32" if getattr(W, "w", 64) == 32 else "int64",  # the containers' arithmetic (w bits)
         "data": "synthetic (counter-based splitmix64 generator, gen/ne_gen.h; no dataset)",
-        "config": dict(W.config(), **({"l2": "working set < L2: a 512 MB write flushes L2 before every timed "
+        "config": dict(W.config(), partition=W.partition_note if world > 1 else None,
+                       **({"l2": "working set < L2: a 512 MB write flushes L2 before every timed "
                                                    "step, outside that step's CUDA events (per-step timing)"}
-                                             if flush_l2 and args.graph else {})),
+                                             if flush_l2 and use_graph else {})),
         "roofline": {"bound": bound, "kernel": dom, "achieved": round(achieved, 2), "peak": round(peak, 1),
                      "unit": runit, "frac": round(achieved / peak, 4), "traffic": traffic,
                      "traffic_unit": "GB per launch, ncu dram__bytes_read.sum + dram__bytes_write.sum "
@@ -1411,11 +1617,12 @@ def run_ours(args, rank, world, local_rank):
                      "algorithmic_per_launch": f"{amount:.4g} {unit}", "peak_source": peak_note},
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "stages_timing": ("device time of each stage inside the replayed step graph (event-record nodes, median)"
-                          if args.graph else "eager launches, CUDA events between stages"),
+                          if use_graph else "eager launches, CUDA events between stages"),
         "eager_stages_ms": {k: round(v, 4) for k, v in eager_stage_ms.items()},
-        "launch": "CUDA graph replay (one graph per recovered stream r)" if args.graph else "eager",
+        "launch": "CUDA graph replay (one graph per recovered stream r)" if use_graph else
+                  ("eager (the step contains a collective)" if args.graph else "eager"),
         "eager_ms_per_step": round(eager_ms, 4),
-        "e2e": {"value": round(W.work_per_step() * world / (e2e_ms / 1e3), 3), "unit": W.metric_unit,
+        "e2e": {"value": round(W.job_work() / (e2e_ms / 1e3), 3), "unit": W.metric_unit,
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "pipelined": "H2D / compute / D2H on three streams, two buffer slots" if W.E2E_PIPELINE
                 else "no (one stream; the step is smaller than the enqueue cost of a pipeline)"},
@@ -1424,9 +1631,9 @@ def run_ours(args, rank, world, local_rank):
         "correctness": {"range_violations": dg["range_violations"], "flagged_positions": dg["fault_positions"],
                         "recover_equals_check": rec_ok},
     }
-    if plain:
-        line["overhead"] = overhead_block(W, plain)
-        line["overhead_pct"] = line["overhead"]["pct"]
+    if ovh is not None:
+        line["overhead"] = ovh
+        line["overhead_pct"] = ovh["pct"]
     line["timed_host_s"] = round(t_host1 - t_host0, 4)
     if world == 1:
         line["cpu_baseline"] = cb
@@ -1590,7 +1797,8 @@ CONFIG_SET = (
     ("C5", dict(workload="c5", steps=5)),
 )
 _SUB_DEFAULTS = dict(algo="tc", limbs="plan", scheme="entangled", fuse=None, conv=None, taps=4500, streams=8,
-                     kdim=2000, w=64, layout="aos", n=None, failstop="simulated", exchange="auto", graph=1)
+                     kdim=2000, w=64, layout="aos", n=None, failstop="simulated", exchange="auto", graph=1,
+                     scaling="strong")
 
 
 def compact(line):
@@ -1621,7 +1829,7 @@ def run_configs(args, rank, world, local_rank):
 
     out = {}
     for name, over in CONFIG_SET:
-        sub = _ap.Namespace(**dict(vars(args), **_SUB_DEFAULTS, **over))
+        sub = _ap.Namespace(**{**vars(args), **_SUB_DEFAULTS, **over})
         sub.warmup = max(3, min(args.warmup, 5))
         t0 = time.perf_counter()
         try:
@@ -1641,7 +1849,9 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
-    ap.add_argument("--algo", default="tc", choices=["tc", "imad"])
+    ap.add_argument("--algo", default="tc", choices=["tc", "imad", "imad64"],
+                    help="c3 GEMM: tcgen05 int8 digits (default); CUDA-core IMAD.WIDE 32 x 32 -> 64 (imad, C3's "
+                         "operand fits int32); CUDA-core 64-bit form for any operand (imad64)")
     ap.add_argument("--limbs", default="plan", choices=["plan", "base256"],
                     help="c3: GEMM operand digits: cheapest exact plan (default) or balanced base 256")
     ap.add_argument("--scheme", default="entangled", choices=["entangled", "abft"],
@@ -1667,6 +1877,10 @@ def main():
                     help="c5: position-major exchange fused into the GEMM epilogue (symmetric memory) or an NCCL "
                          "all_to_all after it; auto = fused when N > 1")
     ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: partition the stated problem over the ranks (SURVEY 8(e): C1 position ranges, C2 "
+                         "ranges + halo, C3 row ranges, C4 stream placement; default) or run one independent replica "
+                         "per rank")
     ap.add_argument("--configs", type=int, default=1,
                     help="default workload (c3) only: also measure C1, C1 at 2^27, C2, C4 and C5 in the same run and "
                          "report them under \"configs\" (0: the C3 line alone)")

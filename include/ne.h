@@ -81,7 +81,11 @@ typedef struct {
   long long first_fault;               /* min flagged position                   */
 } ne_diag;
 
-typedef enum { NE_GEMM_TC_I8 = 0, NE_GEMM_IMAD64 = 1 } ne_gemm_algo;
+/* GEMM algorithms: the tcgen05 int8-digit path; CUDA-core 64 x 32-bit
+ * multiply-adds for any int64 A (IMAD64); CUDA-core 32 x 32 -> 64-bit
+ * IMAD.WIDE when every A entry fits int32 (IMAD32W; an entry that does not
+ * is a range violation in diag). */
+typedef enum { NE_GEMM_TC_I8 = 0, NE_GEMM_IMAD64 = 1, NE_GEMM_IMAD32W = 2 } ne_gemm_algo;
 /* which tensor-core kernel a limb GEMM launch runs (ne_gemm_kernel_for) */
 typedef enum { NE_GEMM_KERNEL_CTA = 0, NE_GEMM_KERNEL_PAIR = 1 } ne_gemm_kernel;
 typedef enum { NE_OP_SCALE = 0, NE_OP_ADD = 1, NE_OP_LINEAR = 2, NE_OP_PERMUTE = 3 } ne_op_kind;
@@ -207,6 +211,21 @@ ne_status ne_op_conv_check(const ne_config* cfg, ne_cstreams x, int64_t n_total,
 ne_status ne_op_inner(const ne_config* cfg, ne_cstreams x, int64_t n_total, const int32_t* v,
                       int64_t vlen, int64_t block, ne_streams out, ne_stream_t stream);
 
+/* One stream of the fused permutation + blocked inner product (the C4
+ * stream-per-GPU placement; bijection P:253-258, reading R11;
+ * inner product Eq. 2, reading R14): for output blocks b in
+ * [b_begin, b_begin + b_count),
+ *   out_m[b - b_begin] = sum_{i in block b} x_m[perm[i]] * v[i mod vlen]
+ * (wrap mod 2^64; ragged last block).  x_m: one int64 entangled stream of
+ * n_total (<= INT32_MAX) positions, 16-B aligned; perm: n_total int32
+ * indices (a bijection, unchecked); out_m: b_count int64.  The caller
+ * gathers the M streams' block sums (all_gather) and runs
+ * ne_disentangle_check on them.  Errors: NE_EINVAL for a block range outside
+ * [0, ceil(n_total / block)). */
+ne_status ne_op_permute_inner_stream(const ne_config* cfg, const int64_t* x_m, const int32_t* perm, int64_t n_total,
+                                     const int32_t* v, int64_t vlen, int64_t block, int64_t b_begin,
+                                     int64_t b_count, int64_t* out_m, ne_stream_t stream);
+
 /* Outer product (x) (Eq. 2): out_m[i*n2 + j] = x_m[i] * h[j]. */
 ne_status ne_op_outer(const ne_config* cfg, ne_cstreams x, int64_t n1, const int32_t* h,
                       int64_t n2, ne_streams out, ne_stream_t stream);
@@ -257,17 +276,68 @@ ne_status ne_op_permute(const ne_config* cfg, ne_cstreams x, const int32_t* perm
 /* Integer matrix product (reading R13): C_m = A_m * B for every
  * stream m, A_m rows x K (entangled, int64), B K x cols (plain int32, shared
  * kernel g, unmodified), C_m rows x cols int64.  algo NE_GEMM_IMAD64 runs on
- * the CUDA cores; NE_GEMM_TC_I8 splits A_m into L balanced base-2^limb_bits
- * int8 digit planes (ne_gemm_limb_plan) and B into one int8 plane and runs
- * tcgen05.mma kind::i8 with exact int32 limb accumulators, recombined in
- * int64.  ws: workspace
- * of ne_gemm_workspace() bytes (TC only).  Entries of B outside [-128,127]
- * or of A_m outside the L-limb range count in diag.range_violations (TC). */
+ * the CUDA cores; NE_GEMM_TC_I8 splits A_m into L (1..8) balanced
+ * base-2^limb_bits int8 digit planes (ne_gemm_limb_plan / ne_gemm_plan_for;
+ * limb_bits * (L - 1) <= 63) and B into LB (1..5) balanced base-256 digit
+ * planes, and runs tcgen05.mma kind::i8 with exact int32 digit accumulators,
+ * recombined in int64 (wrap mod 2^64, exact for certified results;
+ * DESIGN.md §7): L = 8 and LB = 5 cover every int64 operand and every int32
+ * B, so no certified operand range is refused.  ws: workspace of
+ * ne_gemm_workspace() bytes (TC only).  Entries of B outside the LB-digit
+ * range or of A_m outside the L-limb range count in diag.range_violations
+ * (TC). */
 ne_status ne_gemm_workspace(const ne_config* cfg, int64_t rows, int64_t cols, int64_t K,
-                            int32_t L, size_t* bytes);
+                            int32_t L, int32_t LB, size_t* bytes);
 ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int64_t rows,
-                     int64_t cols, int64_t K, ne_gemm_algo algo, int32_t L, int32_t limb_bits,
+                     int64_t cols, int64_t K, ne_gemm_algo algo, int32_t L, int32_t limb_bits, int32_t LB,
                      ne_streams C, void* ws, size_t ws_bytes, ne_diag* diag, ne_stream_t stream);
+
+/* ---- General digit plans of the tensor-core GEMM (the full certified range).
+ * An entangled operand eps_m = c_m + 2^l c_{m-1} (Eq. 15) and the shared B are
+ * held as int8 digit planes: eps_m = sum_{i<LA} 2^a_shift[i] D_{m,i} and
+ * B = sum_{j<LB} 2^(8j) B_j, so C_m = sum_i sum_j 2^(a_shift[i] + 8j)
+ * (D_{m,i} B_j), each product an exact int8 x int8 -> int32 tensor-core GEMM
+ * (K < 131072), recombined in int64.
+ *   kind NE_PLAN_EPS:   LA digits of eps in base 2^digit_bits (a_shift[i] =
+ *                       digit_bits * i): the two-digit plan (digit_bits = l,
+ *                       |c| <= 127) or balanced base 256 (ne_entangle_limbs).
+ *   kind NE_PLAN_SPLIT: c_m and c_{m-1} each in D = LA / 2 balanced base-256
+ *                       digits, at bit weights 0, 8, .. and l, l + 8, ..
+ *                       (2 ceil-digits(|c|) planes; stream m's planes carry
+ *                       only stream m's operand, so a fault in one stream's
+ *                       product still corrupts that delta_m alone, Props 2/4).
+ * planes: [(m*LA + i)*rows*K] int8 (K contiguous); Bt: [(j*cols + col)*K]. */
+typedef enum { NE_PLAN_EPS = 0, NE_PLAN_SPLIT = 1 } ne_plan_kind;
+typedef struct {
+  int32_t kind;        /* ne_plan_kind */
+  int32_t LA;          /* A digit planes per stream, 1..8 */
+  int32_t digit_bits;  /* NE_PLAN_EPS: the digit base 2^digit_bits; NE_PLAN_SPLIT: 8 */
+  int32_t LB;          /* B digit planes, 1..5 (balanced base 256) */
+  int32_t a_shift[8];  /* bit weight of A plane i */
+} ne_gemm_plan;
+
+/* The cheapest exact plan for |c| <= a_bound (the plain inputs of the
+ * entangled operand) and |B| <= b_bound (both <= INT32_MAX): fewest A planes,
+ * the two-digit plan first, then the split plan when it needs fewer planes
+ * than base-256 digits of eps.  Certification of the product (K a b <= hi) is
+ * ne_certify's job.  Host-only. */
+ne_status ne_gemm_plan_for(const ne_config* cfg, int64_t a_bound, int64_t b_bound, ne_gemm_plan* plan);
+/* a0 + a1 into the plan's digit planes (Eq. 15; |c| <= hi and the digit
+ * range asserted per value, violations named m*n_total + n).  n_total % 16 == 0. */
+ne_status ne_entangle_plan(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, const ne_gemm_plan* plan,
+                           int8_t* planes, ne_diag* diag, ne_stream_t stream);
+/* B (K x cols int32, row-major) -> LB balanced base-256 digit planes
+ * Bt[(j*cols + col)*K + k]; a value LB digits cannot hold is a range
+ * violation naming k*cols + col.  K % 16 == 0, LB in [1, 5]. */
+ne_status ne_gemm_prep_b_planes(const int32_t* B, int64_t K, int64_t cols, int32_t LB, int8_t* Bt, ne_diag* diag,
+                                ne_stream_t stream);
+/* C_m = sum_i sum_j 2^(a_shift[i] + 8j) D_{m,i} B_j for every stream: A planes
+ * in groups of <= 4 TMEM accumulators, one tcgen05 launch per (group, B
+ * plane), the first storing C and the others adding into it (TMA reduce-add,
+ * u64 wrap).  A plain plan (LB = 1, <= 4 digits of one base) runs as
+ * ne_op_gemm_limbs (CTA-pair kernel included).  Shapes as ne_op_gemm_limbs. */
+ne_status ne_op_gemm_plan(const ne_config* cfg, const int8_t* planes, const ne_gemm_plan* plan, const int8_t* Bt,
+                          int64_t rows, int64_t cols, int64_t K, ne_streams C, ne_stream_t stream);
 
 /* The tensor-core GEMM on operands already in limb form: planes from
  * ne_entangle_limbs (M*L planes of rows x K int8, K contiguous) and Bt from

@@ -17,7 +17,11 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "liboracle.so")
+# NE_ORACLE_UBSAN=1: the same sources built with -fsanitize=undefined and
+# -fno-sanitize-recover=all (any undefined behaviour aborts the process); the
+# CPU suite runs the oracle pins against it (tests/test_oracle_ubsan.py)
+UBSAN = os.environ.get("NE_ORACLE_UBSAN") == "1"
+_SO = os.path.join(_HERE, "liboracle_ubsan.so" if UBSAN else "liboracle.so")
 
 
 def build(force: bool = False) -> str:
@@ -25,9 +29,15 @@ def build(force: bool = False) -> str:
     srcs.append(os.path.join(_HERE, "..", "gen", "ne_gen.h"))
     if force or not os.path.exists(_SO) or any(os.path.getmtime(s) > os.path.getmtime(_SO) for s in srcs):
         cc = os.environ.get("CC", "gcc")
-        subprocess.check_call(
-            [cc, "-O2", "-std=gnu11", "-Wall", "-fPIC", "-pthread", "-shared", "-o", _SO,
-             os.path.join(_HERE, "ne_oracle.c"), os.path.join(_HERE, "or_selftest.c")])
+        flags = ["-O2", "-std=gnu11", "-Wall", "-fPIC", "-pthread"]
+        if UBSAN:   # the system gcc carries libubsan
+            cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else cc
+            flags = ["-O1", "-g", "-std=gnu11", "-Wall", "-fPIC", "-pthread", "-fsanitize=undefined",
+                     "-fno-sanitize-recover=all"]
+        tmp = _SO + f".{os.getpid()}.tmp"
+        subprocess.check_call([cc, *flags, "-shared", "-o", tmp, os.path.join(_HERE, "ne_oracle.c"),
+                               os.path.join(_HERE, "or_selftest.c")])
+        os.replace(tmp, _SO)
     return _SO
 
 

@@ -23,7 +23,7 @@ from ._build import LIB, build  # noqa: F401  (build() is what __graft_entry__.b
 NE_MAX_M = 32
 STATUS = {0: "NE_OK", 1: "NE_EINVAL", 2: "NE_ECONFIG", 3: "NE_ERANGE", 4: "NE_EINDEX",
           5: "NE_EUNRECOVERABLE", 6: "NE_ECUDA", 7: "NE_ENOTSUP"}
-NE_GEMM_TC_I8, NE_GEMM_IMAD64 = 0, 1
+NE_GEMM_TC_I8, NE_GEMM_IMAD64, NE_GEMM_IMAD32W = 0, 1, 2
 NE_OP_SCALE, NE_OP_ADD, NE_OP_LINEAR, NE_OP_PERMUTE = 0, 1, 2, 3
 
 # every symbol include/ne.h and include/ne_gendev.h declare (checked by tests)
@@ -33,12 +33,13 @@ EXPORTS = (
     "ne_entangle_limbs_stream", "ne_op_gemm_limbs_stream",
     "ne_op_scale", "ne_op_add", "ne_op_scale_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
+    "ne_gemm_plan_for", "ne_entangle_plan", "ne_gemm_prep_b_planes", "ne_op_gemm_plan",
     "ne_gemm_check_workspace", "ne_op_gemm_limbs_check", "ne_gemm_trace", "ne_gemm_kernel_for", "ne_op_gemm_limbs_scatter",
     "ne_conv_geometry", "ne_entangle_limbs_conv", "ne_conv_prep_taps", "ne_op_conv_limbs",
     "ne_op_scale_add_check", "ne_op_conv_check", "ne_op_scale_add_check_w32",
     "ne_entangle_w32", "ne_op_scale_add_w32", "ne_disentangle_check_w32", "ne_recover_w32", "ne_inject_sweep_w32",
     "ne_entangle_aos_w32", "ne_op_permute_inner_check_w32",
-    "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check",
+    "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check", "ne_op_permute_inner_stream",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
     "ne_abft_encode", "ne_abft_encode_limbs", "ne_abft_encode_conv", "ne_op_conv_limbs_plain", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
 )
@@ -55,6 +56,15 @@ class Config(C.Structure):
 
     def __repr__(self) -> str:
         return f"ne_config(M={self.M}, w={self.w}, l={self.l}, k={self.k})"
+
+
+class GemmPlan(C.Structure):  # ne_gemm_plan
+    _fields_ = [("kind", C.c_int32), ("LA", C.c_int32), ("digit_bits", C.c_int32), ("LB", C.c_int32),
+                ("a_shift", C.c_int32 * 8)]
+
+    def __repr__(self) -> str:
+        return (f"ne_gemm_plan(kind={'split' if self.kind else 'eps'}, LA={self.LA}, digit_bits={self.digit_bits}, "
+                f"LB={self.LB}, a_shift={list(self.a_shift)[:self.LA]})")
 
 
 class Streams(C.Structure):  # ne_streams / ne_cstreams / ne_cstreams32 (same ABI)
@@ -89,8 +99,12 @@ _SIGS = {
     "ne_op_outer": [_PCFG, Streams, _I64, _VP, _I64, Streams, _VP],
     "ne_op_conv": [_PCFG, Streams, _I64, _VP, _I32, _I32, Streams, _VP],
     "ne_op_permute": [_PCFG, Streams, _VP, _I64, Streams, _VP],
-    "ne_gemm_workspace": [_PCFG, _I64, _I64, _I64, _I32, C.POINTER(_SZ)],
-    "ne_op_gemm": [_PCFG, Streams, _VP, _I64, _I64, _I64, C.c_int, _I32, _I32, Streams, _VP, _SZ, _VP, _VP],
+    "ne_gemm_workspace": [_PCFG, _I64, _I64, _I64, _I32, _I32, C.POINTER(_SZ)],
+    "ne_op_gemm": [_PCFG, Streams, _VP, _I64, _I64, _I64, C.c_int, _I32, _I32, _I32, Streams, _VP, _SZ, _VP, _VP],
+    "ne_gemm_plan_for": [_PCFG, _I64, _I64, C.POINTER(GemmPlan)],
+    "ne_entangle_plan": [_PCFG, Streams, _I64, C.POINTER(GemmPlan), _VP, _VP, _VP],
+    "ne_gemm_prep_b_planes": [_VP, _I64, _I64, _I32, _VP, _VP, _VP],
+    "ne_op_gemm_plan": [_PCFG, _VP, C.POINTER(GemmPlan), _VP, _I64, _I64, _I64, Streams, _VP],
     "ne_gemm_prep_b": [_VP, _I64, _I64, _VP, _VP, _VP],
     "ne_op_gemm_limbs": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _VP],
     "ne_op_scale_add_check": [_PCFG, Streams, _I64, _I64, _VP, Streams, _I32, _I32, Streams, _VP, _VP, _VP],
@@ -117,6 +131,7 @@ _SIGS = {
     "ne_recover": [_PCFG, Streams, _I64, _I32, Streams, _VP],
     "ne_op_permute_inner_check": [_PCFG, Streams, _VP, _I32, _VP, _I64, _VP, _I64, _I64, _I32,
                                   Streams, Streams, _VP, _VP, _VP],
+    "ne_op_permute_inner_stream": [_PCFG, _VP, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _VP, _VP],
     "ne_inject": [_VP, _I64, _U64, _VP],
     "ne_abft_encode_conv": [_PCFG, Streams, _I64, _I32, _I32, _I32, _VP, _I32, _VP, _VP, _VP],
     "ne_op_conv_limbs_plain": [_I32, _VP, _I32, _I32, _I32, _VP, _I64, _I32, _I32, Streams, _VP],
@@ -313,17 +328,39 @@ def ne_op_permute(cfg: Config, x, perm: torch.Tensor, out) -> None:
           _streams(out, torch.int64), _stream())
 
 
-def ne_gemm_workspace(cfg: Config, rows: int, cols: int, K: int, L: int) -> int:
+def ne_gemm_workspace(cfg: Config, rows: int, cols: int, K: int, L: int, LB: int = 1) -> int:
     b = C.c_size_t()
-    _call("ne_gemm_workspace", C.byref(cfg), rows, cols, K, L, C.byref(b))
+    _call("ne_gemm_workspace", C.byref(cfg), rows, cols, K, L, LB, C.byref(b))
     return b.value
 
 
 def ne_op_gemm(cfg: Config, A, B: torch.Tensor, rows: int, cols: int, K: int, out, algo: int = NE_GEMM_TC_I8,
-               L: int = 4, ws: torch.Tensor | None = None, diag=None, limb_bits: int = 8) -> None:
+               L: int = 4, ws: torch.Tensor | None = None, diag=None, limb_bits: int = 8, LB: int = 1) -> None:
     _call("ne_op_gemm", C.byref(cfg), _streams(A, torch.int64), _ptr(B, torch.int32), rows, cols, K, algo, L, limb_bits,
-          _streams(out, torch.int64), _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
+          LB, _streams(out, torch.int64), _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
           _ptr(diag, torch.int64), _stream())
+
+
+def ne_gemm_plan_for(cfg: Config, a_bound: int, b_bound: int) -> GemmPlan:
+    p = GemmPlan()
+    _call("ne_gemm_plan_for", C.byref(cfg), a_bound, b_bound, C.byref(p))
+    return p
+
+
+def ne_entangle_plan(cfg: Config, c, plan: GemmPlan, planes: torch.Tensor, diag=None) -> None:
+    _call("ne_entangle_plan", C.byref(cfg), _streams(c, torch.int32), c[0].numel(), C.byref(plan),
+          _ptr(planes, torch.int8), _ptr(diag, torch.int64), _stream())
+
+
+def ne_gemm_prep_b_planes(B: torch.Tensor, K: int, cols: int, LB: int, Bt: torch.Tensor, diag=None) -> None:
+    _call("ne_gemm_prep_b_planes", _ptr(B, torch.int32), K, cols, LB, _ptr(Bt, torch.int8), _ptr(diag, torch.int64),
+          _stream())
+
+
+def ne_op_gemm_plan(cfg: Config, planes: torch.Tensor, plan: GemmPlan, Bt: torch.Tensor, rows: int, cols: int,
+                    K: int, out) -> None:
+    _call("ne_op_gemm_plan", C.byref(cfg), _ptr(planes, torch.int8), C.byref(plan), _ptr(Bt, torch.int8), rows, cols,
+          K, _streams(out, torch.int64), _stream())
 
 
 def ne_gemm_prep_b(B: torch.Tensor, K: int, cols: int, Bt: torch.Tensor, diag=None) -> None:
@@ -485,6 +522,13 @@ def ne_op_permute_inner_check(cfg: Config, v: torch.Tensor, block: int, r: int, 
     _call("ne_op_permute_inner_check", C.byref(cfg), xs, _ptr(x_aos, torch.int64), int(x_aos is not None),
           _ptr(perm, torch.int32), n, _ptr(v, torch.int32), v.numel(), block, r, do, _streams(d_out, torch.int64),
           _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _stream())
+
+
+def ne_op_permute_inner_stream(cfg: Config, x_m: torch.Tensor, perm: torch.Tensor, v: torch.Tensor, block: int,
+                               b_begin: int, b_count: int, out_m: torch.Tensor) -> None:
+    """One stream's gather + blocked inner product over blocks [b_begin, b_begin + b_count)."""
+    _call("ne_op_permute_inner_stream", C.byref(cfg), _ptr(x_m, torch.int64), _ptr(perm, torch.int32), x_m.numel(),
+          _ptr(v, torch.int32), v.numel(), block, b_begin, b_count, _ptr(out_m, torch.int64), _stream())
 
 
 # ------------------------------------------------------------------ ABFT comparison baseline (Eqs. 3-6)

@@ -10,6 +10,8 @@ namespace ne {
 
 void launch_gemm_imad64(int M, const ne_cstreams& A, const int32_t* B, const ne_streams& C, int64_t rows,
                         int64_t cols, int64_t K, cudaStream_t s);
+void launch_gemm_imad32w(int M, const ne_cstreams& A, const int32_t* B, const ne_streams& C, int64_t rows,
+                         int64_t cols, int64_t K, ne_diag* diag, cudaStream_t s);
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s);
 void gemm_trace(long long* buf, int max_clusters);
@@ -158,20 +160,161 @@ k_prep_b128(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __re
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
+// B (K x cols int32) -> LB balanced base-256 digit planes Bt[j][cols][K]
+// (digit j = byte j of y = B + sum_{i<LB} 128 * 256^i, xor 0x80): the multi-
+// plane int8 operand of a wide-range GEMM plan.  Tiles of 128 k x 64 columns
+// as k_prep_b128 (K % 128 == 0, cols % 64 == 0), one [64][33]-word shared tile
+// per plane; a value LB digits cannot hold is a range violation.
+template <int LB>
+__global__ void __launch_bounds__(256)
+k_prep_b_planes(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __restrict__ Bt,
+                ne_diag* __restrict__ diag) {
+  __shared__ uint32_t W[LB][64][33];
+  constexpr int64_t bias = (int64_t)(0x8080808080808080ull >> (64 - 8 * LB));
+  constexpr int64_t span = (int64_t)1 << (8 * LB);
+  const int64_t k0 = (int64_t)blockIdx.y * 128, c0 = (int64_t)blockIdx.x * 64;
+  int bad = 0;
+  long long first = LLONG_MAX;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+    const int task = it * 256 + threadIdx.x;
+    const int c4 = task & 15, kq = task >> 4;
+    const int64_t c = c0 + 4 * c4;
+    int64_t y[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t k = k0 + 4 * kq + r;
+      const int4 w = __ldcs(reinterpret_cast<const int4*>(B + k * cols + c));
+      const int32_t v[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        y[r][i] = (int64_t)v[i] + bias;
+        if (y[r][i] < 0 || y[r][i] >= span) {
+          ++bad;
+          const long long idx = (long long)(k * cols + c + i);
+          first = idx < first ? idx : first;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < LB; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t d[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) d[r] = (uint32_t)(((y[r][i] >> (8 * j)) & 0xff) ^ 0x80);
+        W[j][4 * c4 + i][kq] = d[0] | (d[1] << 8) | (d[2] << 16) | (d[3] << 24);
+      }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < LB; ++j)
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int u = it * 256 + threadIdx.x;
+      const int cc = u >> 3, q = u & 7;
+      __stcs(reinterpret_cast<uint4*>(Bt + ((int64_t)j * cols + c0 + cc) * K + k0 + 16 * q),
+             make_uint4(W[j][cc][4 * q], W[j][cc][4 * q + 1], W[j][cc][4 * q + 2], W[j][cc][4 * q + 3]));
+    }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+// any shape (K % 16 == 0): one thread per element, byte stores (edge shapes)
+__global__ void k_prep_b_planes_any(const int32_t* __restrict__ B, int64_t K, int64_t cols, int LB,
+                                    int8_t* __restrict__ Bt, ne_diag* __restrict__ diag) {
+  const int64_t bias = (int64_t)(0x8080808080808080ull >> (64 - 8 * LB));
+  const int64_t span = (int64_t)1 << (8 * LB);
+  int bad = 0;
+  long long first = LLONG_MAX;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K * cols; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / cols, c = e % cols;
+    const int64_t y = (int64_t)B[e] + bias;
+    if (y < 0 || y >= span) {
+      ++bad;
+      first = e < first ? e : first;
+    }
+    for (int j = 0; j < LB; ++j) Bt[((int64_t)j * cols + c) * K + k] = (int8_t)(uint8_t)(((y >> (8 * j)) & 0xff) ^ 0x80);
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+ne_status launch_gemm_planes(int M, const int8_t* planes, int LA, const int32_t* a_shift, const int8_t* Bt, int LB,
+                             int64_t rows, int64_t cols, int64_t K, const ne_streams& C, cudaStream_t s);
+
 }  // namespace ne
 
 using namespace ne;
+
+// balanced base-256 digits needed for |x| <= bound (digits in [-128, 127])
+static int digits256(int64_t bound) {
+  __int128 cap = 0, p = 1;
+  for (int L = 1; L <= 8; ++L) {
+    cap += 127 * p;
+    p *= 256;
+    if (bound <= cap) return L;
+  }
+  return 9;
+}
+
+extern "C" ne_status ne_gemm_plan_for(const ne_config* cfg, int64_t a_bound, int64_t b_bound, ne_gemm_plan* plan) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (!plan || a_bound < 0 || b_bound < 0 || a_bound > INT32_MAX || b_bound > INT32_MAX) return NE_EINVAL;
+  ne_gemm_plan p{};
+  p.LB = digits256(b_bound);                 // <= 5 for |B| < 2^31
+  const int l = cfg->l;
+  const int Le = ne_gemm_limbs_for(cfg, a_bound);   // base-256 digits of eps = c_m + 2^l c_{m-1}
+  const int D = digits256(a_bound);
+  if (a_bound <= 127 && l >= 8 && l <= 31) {  // the two-digit plan: the digits are c_m and c_{m-1}
+    p.kind = NE_PLAN_EPS;
+    p.LA = 2;
+    p.digit_bits = l;
+  } else if (D <= 4 && 2 * D < Le) {          // split: c_m and c_{m-1} in D digits each, at 0 and l
+    p.kind = NE_PLAN_SPLIT;
+    p.LA = 2 * D;
+    p.digit_bits = 8;
+  } else {                                    // base-256 digits of eps
+    p.kind = NE_PLAN_EPS;
+    p.LA = Le;
+    p.digit_bits = 8;
+  }
+  if (p.LA > 8) return NE_ERANGE;
+  for (int i = 0; i < p.LA; ++i)
+    p.a_shift[i] = p.kind == NE_PLAN_SPLIT ? (i < p.LA / 2 ? 8 * i : l + 8 * (i - p.LA / 2)) : p.digit_bits * i;
+  *plan = p;
+  return NE_OK;
+}
+
+extern "C" ne_status ne_gemm_prep_b_planes(const int32_t* B, int64_t K, int64_t cols, int32_t LB, int8_t* Bt,
+                                           ne_diag* diag, ne_stream_t stream) {
+  if (!B || !Bt || K <= 0 || cols <= 0 || K % 16 != 0 || LB < 1 || LB > 5 || !aligned16(Bt) || !aligned16(B))
+    return NE_EINVAL;
+  cudaStream_t s = cs(stream);
+  if (K % 128 == 0 && cols % 64 == 0) {
+    const dim3 grid((unsigned)(cols / 64), (unsigned)(K / 128));
+    switch (LB) {
+      case 1: k_prep_b_planes<1><<<grid, 256, 0, s>>>(B, K, cols, Bt, diag); break;
+      case 2: k_prep_b_planes<2><<<grid, 256, 0, s>>>(B, K, cols, Bt, diag); break;
+      case 3: k_prep_b_planes<3><<<grid, 256, 0, s>>>(B, K, cols, Bt, diag); break;
+      case 4: k_prep_b_planes<4><<<grid, 256, 0, s>>>(B, K, cols, Bt, diag); break;
+      default: k_prep_b_planes<5><<<grid, 256, 0, s>>>(B, K, cols, Bt, diag); break;
+    }
+    return launch_status();
+  }
+  k_prep_b_planes_any<<<grid_for(K * cols, 256), 256, 0, s>>>(B, K, cols, LB, Bt, diag);
+  return launch_status();
+}
 
 static bool tc_shape_ok(int64_t rows, int64_t cols, int64_t K) {
   return rows > 0 && cols > 0 && K > 0 && rows % 128 == 0 && cols % 128 == 0 && K % 128 == 0 && K < 131072;  // K * 2^14 < 2^31
 }
 
 extern "C" ne_status ne_gemm_workspace(const ne_config* cfg, int64_t rows, int64_t cols, int64_t K, int32_t L,
-                                       size_t* bytes) {
+                                       int32_t LB, size_t* bytes) {
   ne_status st = validate_cfg(cfg);
   if (st != NE_OK) return st;
-  if (!bytes || L < 1 || L > 8) return NE_EINVAL;
-  *bytes = (size_t)cfg->M * L * rows * K + (size_t)cols * K + 1024;
+  if (!bytes || L < 1 || L > 8 || LB < 1 || LB > 5) return NE_EINVAL;
+  *bytes = (size_t)cfg->M * L * rows * K + (size_t)LB * cols * K + 1024;
   return NE_OK;
 }
 
@@ -198,6 +341,20 @@ extern "C" ne_status ne_op_gemm_limbs(const ne_config* cfg, const int8_t* planes
     if (!C.s[m] || !aligned16(C.s[m])) return NE_EINVAL;
   if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
   return launch_gemm_tc(cfg->M, L, limb_bits, planes, Bt, rows, cols, K, C, cs(stream));
+}
+
+extern "C" ne_status ne_op_gemm_plan(const ne_config* cfg, const int8_t* planes, const ne_gemm_plan* plan,
+                                     const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, ne_streams C,
+                                     ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (!plan || !planes || !Bt || plan->LA < 1 || plan->LA > 8 || plan->LB < 1 || plan->LB > 5 ||
+      !aligned16(planes) || !aligned16(Bt))
+    return NE_EINVAL;
+  for (int m = 0; m < cfg->M; ++m)
+    if (!C.s[m] || !aligned16(C.s[m])) return NE_EINVAL;
+  if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
+  return launch_gemm_planes(cfg->M, planes, plan->LA, plan->a_shift, Bt, plan->LB, rows, cols, K, C, cs(stream));
 }
 
 extern "C" ne_status ne_gemm_kernel_for(const ne_config* cfg, int32_t L, int32_t limb_bits, int64_t rows,
@@ -276,8 +433,8 @@ extern "C" ne_status ne_op_gemm_limbs_scatter(const ne_config* cfg, const int8_t
 }
 
 extern "C" ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int64_t rows, int64_t cols,
-                                int64_t K, ne_gemm_algo algo, int32_t L, int32_t limb_bits, ne_streams C, void* ws,
-                                size_t ws_bytes, ne_diag* diag, ne_stream_t stream) {
+                                int64_t K, ne_gemm_algo algo, int32_t L, int32_t limb_bits, int32_t LB, ne_streams C,
+                                void* ws, size_t ws_bytes, ne_diag* diag, ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);
   if (st != NE_OK) return st;
   const int M = cfg->M;
@@ -290,11 +447,21 @@ extern "C" ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32
     launch_gemm_imad64(M, A, B, C, rows, cols, K, s);
     return launch_status();
   }
+  if (algo == NE_GEMM_IMAD32W) {
+    if (rows % 128 || cols % 128 || K % 16 || K == 0) {  // tile-aligned shapes only: the any-shape 64-bit form
+      launch_gemm_imad64(M, A, B, C, rows, cols, K, s);
+      return launch_status();
+    }
+    if (!aligned16(B)) return NE_EINVAL;
+    launch_gemm_imad32w(M, A, B, C, rows, cols, K, diag, s);
+    return launch_status();
+  }
   if (algo != NE_GEMM_TC_I8) return NE_EINVAL;
-  if (!tc_shape_ok(rows, cols, K) || L < 1 || L > 4) return NE_ENOTSUP;
-  if (limb_bits < 8 || limb_bits > 63) return NE_EINVAL;
+  if (L < 1 || L > 8 || LB < 1 || LB > 5 || limb_bits < 8 || limb_bits > 63 || limb_bits * (L - 1) > 63)
+    return NE_EINVAL;
+  if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
   size_t need = 0;
-  ne_gemm_workspace(cfg, rows, cols, K, L, &need);
+  ne_gemm_workspace(cfg, rows, cols, K, L, LB, &need);
   if (!ws || ws_bytes < need || !aligned16(ws)) return NE_EINVAL;
   int8_t* planes = static_cast<int8_t*>(ws);
   int8_t* Bt = planes + (size_t)M * L * rows * K;
@@ -307,6 +474,13 @@ extern "C" ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32
     default: k_split_limbs<0><<<grid, kThreads, 0, s>>>(A, M, n, L, limb_bits, planes, diag); break;
   }
   if ((st = launch_status()) != NE_OK) return st;
-  if ((st = ne_gemm_prep_b(B, K, cols, Bt, diag, stream)) != NE_OK) return st;
-  return launch_gemm_tc(M, L, limb_bits, planes, Bt, rows, cols, K, C, s);
+  if (LB == 1) {
+    if ((st = ne_gemm_prep_b(B, K, cols, Bt, diag, stream)) != NE_OK) return st;
+    if (L <= 4) return launch_gemm_tc(M, L, limb_bits, planes, Bt, rows, cols, K, C, s);
+  } else if ((st = ne_gemm_prep_b_planes(B, K, cols, LB, Bt, diag, stream)) != NE_OK) {
+    return st;
+  }
+  int32_t sh[8];
+  for (int i = 0; i < L; ++i) sh[i] = limb_bits * i;
+  return launch_gemm_planes(M, planes, L, sh, Bt, LB, rows, cols, K, C, s);
 }

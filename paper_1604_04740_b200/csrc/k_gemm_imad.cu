@@ -6,6 +6,8 @@
 // for the tcgen05 int8-limb kernel (k_gemm_tc.cu).
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include "ne_internal.cuh"
 
 namespace ne {
@@ -65,6 +67,118 @@ k_gemm_imad64(const __grid_constant__ ne_cstreams A, const int32_t* __restrict__
       if (gc < cols) Cm[gr * cols + gc] = (int64_t)acc[i][j];
     }
   }
+}
+
+// 32 x 32 -> 64-bit form (NE_GEMM_IMAD32W): when every entangled A entry
+// fits int32 (the C3 operand: |eps| <= 64 (2^22 + 1) < 2^31) each MAC is one
+// IMAD.WIDE (mad.wide.s32: 32 x 32 -> 64-bit product + 64-bit accumulator,
+// wrap mod 2^64 — the same value as the int64 form).  CTA tile 128 x 128,
+// K-step 16, 256 threads, 8 x 8 outputs per thread in two 4-row x two
+// 4-column quadrants (conflict-free 128-bit shared loads), the next K-step's
+// global loads in registers while the current one is multiplied.  rows and
+// cols multiples of 128, K of 16 (else the IMAD64 kernel runs).  An A entry
+// outside int32 is a range violation (diag), its product undefined.
+constexpr int kWM = 128, kWN = 128, kWK = 16;
+
+__device__ __forceinline__ int64_t mad_wide(int32_t a, int32_t b, int64_t c) {
+  int64_t d;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+
+__global__ void __launch_bounds__(256)
+k_gemm_imad32w(const __grid_constant__ ne_cstreams A, const int32_t* __restrict__ B,
+               const __grid_constant__ ne_streams C, int64_t rows, int64_t cols, int64_t K,
+               ne_diag* __restrict__ diag) {
+  __shared__ __align__(16) int32_t As[2][kWK][kWM];
+  __shared__ __align__(16) int32_t Bs[2][kWK][kWN];
+  const int m = blockIdx.z;
+  const int64_t row0 = (int64_t)blockIdx.y * kWM, col0 = (int64_t)blockIdx.x * kWN;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t* __restrict__ Am = A.s[m];
+  int bad = 0;
+  long long first = LLONG_MAX;
+  // global -> register staging: A 128 x 16 int64 (8 per thread), B 16 x 128 int32 (8 per thread)
+  // entry u of this thread: A row (tid / 16) + 16 u, k tid % 16; B k (tid / 128) + 2 u, col tid % 128
+  // (rows, cols multiples of 128 and K of 16: no bounds checks)
+  const int64_t* pa = Am + (row0 + (threadIdx.x >> 4)) * K + (threadIdx.x & 15);
+  const int32_t* pb = B + (int64_t)(threadIdx.x >> 7) * cols + col0 + (threadIdx.x & 127);
+  int32_t ra[8], rb[8];
+  auto load = [&](int64_t k0) {
+    uint32_t badm = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t x = __ldg(pa + 16 * u * K + k0);
+      ra[u] = (int32_t)x;
+      badm |= (uint32_t)(x != (int64_t)ra[u]) << u;
+      rb[u] = __ldg(pb + (k0 + 2 * u) * cols);
+    }
+    if (badm) {  // an entry outside int32: range violation naming m * rows * K + row * K + k
+      for (int u = 0; u < 8; ++u)
+        if (badm >> u & 1) {
+          ++bad;
+          const long long idx = ((long long)m * rows + row0 + (threadIdx.x >> 4) + 16 * u) * K + k0 + (threadIdx.x & 15);
+          first = idx < first ? idx : first;
+        }
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = threadIdx.x + 256 * u;
+      As[buf][t & 15][t >> 4] = ra[u];
+      Bs[buf][t >> 7][t & 127] = rb[u];
+    }
+  };
+  int64_t acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = 0; k0 < K; k0 += kWK) {
+    const bool more = k0 + kWK < K;
+    if (more) load(k0 + kWK);
+#pragma unroll
+    for (int kk = 0; kk < kWK; ++kk) {
+      const int4 a0 = *reinterpret_cast<const int4*>(&As[buf][kk][ty * 4]);
+      const int4 a1 = *reinterpret_cast<const int4*>(&As[buf][kk][64 + ty * 4]);
+      const int4 b0 = *reinterpret_cast<const int4*>(&Bs[buf][kk][tx * 4]);
+      const int4 b1 = *reinterpret_cast<const int4*>(&Bs[buf][kk][64 + tx * 4]);
+      const int32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const int32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = mad_wide(a[i], b[j], acc[i][j]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  int64_t* __restrict__ Cm = C.s[m];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t gr = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t gc = col0 + h * 64 + tx * 4;
+      *reinterpret_cast<longlong2*>(Cm + gr * cols + gc) = make_longlong2(acc[i][4 * h], acc[i][4 * h + 1]);
+      *reinterpret_cast<longlong2*>(Cm + gr * cols + gc + 2) = make_longlong2(acc[i][4 * h + 2], acc[i][4 * h + 3]);
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+void launch_gemm_imad32w(int M, const ne_cstreams& A, const int32_t* B, const ne_streams& C, int64_t rows,
+                         int64_t cols, int64_t K, ne_diag* diag, cudaStream_t s) {
+  dim3 grid((unsigned)((cols + kWN - 1) / kWN), (unsigned)((rows + kWM - 1) / kWM), (unsigned)M);
+  k_gemm_imad32w<<<grid, 256, 0, s>>>(A, B, C, rows, cols, K, diag);
 }
 
 void launch_gemm_imad64(int M, const ne_cstreams& A, const int32_t* B, const ne_streams& C, int64_t rows,

@@ -110,6 +110,30 @@ struct Geo {
   int dest_local;
 };
 
+// Digit plan of one launch (ne_op_gemm_planes; the default is the plain
+// L-digit base-2^b product): accumulator i holds A plane a0 + i (of a_total
+// planes per stream) times the B plane whose rows start at b_row0 of the
+// [LB * cols][K] B-plane stack, and carries bit weight sh[i] in the int64
+// recombination.  accumulate: the epilogue adds its tile into C with a TMA
+// reduce-add (u64, wrap mod 2^64) instead of storing it — the later launches
+// of a multi-launch plan (more than 4 A planes, or several B planes).
+struct Plan {
+  int sh[4];
+  int small;      // every sh[i] <= 30: 32 x 32 -> 64-bit multiply-adds
+  int a_total;
+  int a0;
+  int64_t b_row0;
+  int accumulate;
+};
+
+__host__ __device__ inline Plan plain_plan(int L, int b) {
+  Plan p{};
+  for (int i = 0; i < 4; ++i) p.sh[i] = i < L ? b * i : 0;
+  p.small = b * (L - 1) <= 30;
+  p.a_total = L;
+  return p;
+}
+
 // Debug hook (ne_gemm_trace): per CTA and tile t < 32, %globaltimer when the
 // tile's accumulators are complete and when its last chunk is staged.
 struct DbgArgs {
@@ -250,8 +274,8 @@ __device__ __forceinline__ void decode_work(int64_t w, int M, int64_t n_rt, int6
 template <int L, int BN, int STAGES, int SW, int CL, int CHK>
 __global__ void __launch_bounds__(threads_for<CHK>(), 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-          const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
-          const __grid_constant__ ChkArgs chk, const Geo geo, const DbgArgs dbg) {
+          const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M,
+          const __grid_constant__ ChkArgs chk, const Geo geo, const DbgArgs dbg, const Plan pl) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
   constexpr int BK = CF::BK;
   static_assert(L * BN <= 512, "TMEM holds 512 columns");
@@ -329,23 +353,24 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
           if (mb) {
 #pragma unroll
             for (int i = 0; i < L; ++i) {
-              const int32_t grow = (int32_t)(((int64_t)m * L + i) * geo.a_plane_rows + row0 + radd);
+              const int32_t grow =
+                  (int32_t)(((int64_t)m * pl.a_total + pl.a0 + i) * geo.a_plane_rows + row0 + radd);
               tma_load_2d(&mapA, &full[s], st + i * CF::kATile, kc, grow);
             }
             tma_load_2d_mc(&mapB, &full[s], st + L * CF::kATile + crank * (BN / CL) * BK, kb * BK,
-                           (int32_t)(col0 + crank * (BN / CL)), cmask);
+                           (int32_t)(pl.b_row0 + col0 + crank * (BN / CL)), cmask);
           } else {
 #pragma unroll
             for (int i = 0; i < L; ++i) {
               unsigned char* dst = st + i * CF::kATile + crank * CF::kARows * BK;
-              const int32_t grow =
-                  (int32_t)(((int64_t)m * L + i) * geo.a_plane_rows + row0 + crank * CF::kARows + radd);
+              const int32_t grow = (int32_t)(((int64_t)m * pl.a_total + pl.a0 + i) * geo.a_plane_rows + row0 +
+                                             crank * CF::kARows + radd);
               if (CL > 1)
                 tma_load_2d_mc(&mapA, &full[s], dst, kc, grow, cmask);
               else
                 tma_load_2d(&mapA, &full[s], dst, kc, grow);
             }
-            tma_load_2d(&mapB, &full[s], st + L * CF::kATile, kb * BK, (int32_t)col0);
+            tma_load_2d(&mapB, &full[s], st + L * CF::kATile, kb * BK, (int32_t)(pl.b_row0 + col0));
           }
         }
       }
@@ -426,13 +451,14 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
         __syncwarp();
         unsigned char* box = my_out + buf * CF::kStageOut;
         // row `lane` of the box, 16-byte chunk k stored at chunk k ^ (row & 7) (128B swizzle)
-        if (limb_bits * (L - 1) <= 30) {  // sum_i v_i 2^(b i) as 32 x 32 -> 64-bit multiply-adds
+        if (pl.small) {  // sum_i v_i 2^sh_i as 32 x 32 -> 64-bit multiply-adds
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            int64_t a0 = (int32_t)v[0][2 * k], a1 = (int32_t)v[0][2 * k + 1];
+            int64_t a0 = (int64_t)(int32_t)v[0][2 * k] * (1 << pl.sh[0]);
+            int64_t a1 = (int64_t)(int32_t)v[0][2 * k + 1] * (1 << pl.sh[0]);
 #pragma unroll
             for (int i = 1; i < L; ++i) {
-              const int32_t sc = 1 << (limb_bits * i);
+              const int32_t sc = 1 << pl.sh[i];
               a0 += (int64_t)(int32_t)v[i][2 * k] * sc;
               a1 += (int64_t)(int32_t)v[i][2 * k + 1] * sc;
             }
@@ -444,8 +470,8 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
             uint64_t a0 = 0, a1 = 0;
 #pragma unroll
             for (int i = 0; i < L; ++i) {
-              a0 += (uint64_t)(int64_t)(int32_t)v[i][2 * k] << (limb_bits * i);
-              a1 += (uint64_t)(int64_t)(int32_t)v[i][2 * k + 1] << (limb_bits * i);
+              a0 += (uint64_t)(int64_t)(int32_t)v[i][2 * k] << pl.sh[i];
+              a1 += (uint64_t)(int64_t)(int32_t)v[i][2 * k + 1] << pl.sh[i];
             }
             *reinterpret_cast<ulonglong2*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) = make_ulonglong2(a0, a1);
           }
@@ -455,6 +481,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
         if (lane == 0) {
           const int dj = geo.dest_rows > 0 ? (int)(row0 / geo.dest_rows) : m;  // destination map
           const int64_t drow = geo.dest_rows > 0 ? row0 - dj * geo.dest_rows : row0;
+          if (pl.accumulate)  // C += tile (u64 maps: wrap mod 2^64, exact for certified sums)
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                    reinterpret_cast<uint64_t>(&outm.m[dj])),
+                "r"((int32_t)(col0 + c)), "r"((int32_t)(drow + 32 * q)), "r"(smem_u32(box))
+                : "memory");
+          else
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                   reinterpret_cast<uint64_t>(&outm.m[dj])),
@@ -581,8 +614,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUte
 template <int L, int BN, int STAGES, int SW, int CL, int CHK = 0>
 static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
                      int limb_bits, const ne_streams& C, cudaStream_t s, const ChkArgs* chk = nullptr,
-                     const Geo* geo_in = nullptr) {
+                     const Geo* geo_in = nullptr, const Plan* plan_in = nullptr, int LB = 1) {
   using CF = Cfg<L, BN, STAGES, SW, CL>;
+  const Plan pl = plan_in ? *plan_in : plain_plan(L, limb_bits);
   if (cols % BN != 0 || K % CF::BK != 0) return NE_ENOTSUP;
   // B panel larger than ~1/3 of L2: rasterise along rows (see Geo)
   const int raster = (CHK == 0 && (uint64_t)cols * (uint64_t)K > (48ull << 20)) ? 1 : 0;
@@ -591,10 +625,10 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   if (mcb && rows % (BM * CL) != 0) return NE_ENOTSUP;
   if (!mcb && cols % (BN * CL) != 0) return NE_ENOTSUP;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, planes, geo.toeplitz ? (uint64_t)geo.toeplitz : (uint64_t)K, (uint64_t)M * L * geo.a_plane_rows, SW,
-                mcb ? BM : CF::kARows))
+  if (!make_map(&ma, planes, geo.toeplitz ? (uint64_t)geo.toeplitz : (uint64_t)K,
+                (uint64_t)M * pl.a_total * geo.a_plane_rows, SW, mcb ? BM : CF::kARows))
     return NE_ECUDA;
-  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, mcb ? BN / CL : BN)) return NE_ECUDA;
+  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols * LB, SW, mcb ? BN / CL : BN)) return NE_ECUDA;
   if (M > 8) return NE_ENOTSUP;
   OutMaps om;
   if (geo.dest_rows > 0) {  // C.s[j]: destination j's [dest_rows][cols] block
@@ -605,7 +639,8 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
     if (geo.dest_local && !make_out_map(&om.m[8], C.s[8], (uint64_t)cols, (uint64_t)rows)) return NE_ECUDA;
   } else {
     for (int m = 0; m < M; ++m)
-      if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)geo.out_rows)) return NE_ECUDA;
+      if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)geo.out_rows, pl.accumulate != 0))
+        return NE_ECUDA;
   }
   auto kern = k_gemm_tc<L, BN, STAGES, SW, CL, CHK>;
   ChkArgs ca{};
@@ -640,7 +675,7 @@ static ne_status run(const int8_t* planes, const int8_t* Bt, int64_t rows, int64
   if (g_max_clusters > 0 && nclusters > g_max_clusters) nclusters = g_max_clusters;
   lc.gridDim = dim3((unsigned)(nclusters * CL));
   const DbgArgs dbg{g_trace};
-  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, ca, geo, dbg) != cudaSuccess)
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, ca, geo, dbg, pl) != cudaSuccess)
     return NE_ECUDA;
   return launch_status();
 }
@@ -721,6 +756,66 @@ ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t
     if (st != NE_ENOTSUP) return st;
   }
   return gemm_tc_dispatch<0>(M, L, b, planes, Bt, rows, cols, K, C, s, nullptr);
+}
+
+// One launch of a general digit plan: Lsub <= 4 A planes (accumulators) x
+// one B plane, tile shapes as gemm_tc_dispatch.
+static ne_status run_plan(int M, int Lsub, const int8_t* planes, const int8_t* Bt, int LB, int64_t rows,
+                          int64_t cols, int64_t K, const ne_streams& C, cudaStream_t s, const tc::Plan& pl) {
+  const bool c512 = cols % 512 == 0, c256 = cols % 256 == 0;
+  switch (Lsub) {
+    case 1:
+      if (c512) return tc::run<1, 256, 6, 64, 2>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+      if (c256) return tc::run<1, 256, 6, 64, 1>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+      return tc::run<1, 128, 8, 64, 1>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+    case 2:
+      if (c512) return tc::run<2, 256, 5, 64, 2>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+      if (c256) return tc::run<2, 256, 5, 64, 1>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+      return tc::run<2, 128, 6, 64, 1>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+    case 3:
+      if (c256) return tc::run<3, 128, 5, 64, 2>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+      return tc::run<3, 128, 5, 64, 1>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+    case 4:
+      if (c256) return tc::run<4, 128, 4, 64, 2>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+      return tc::run<4, 128, 4, 64, 1>(planes, Bt, rows, cols, K, M, 8, C, s, nullptr, nullptr, &pl, LB);
+    default: return NE_ENOTSUP;
+  }
+}
+
+// The general exact product C_m = sum_{i<LA} sum_{j<LB} 2^(a_shift[i] + 8 j)
+// (D_{m,i} B_j): A planes in groups of <= 4 accumulators, one launch per
+// (group, B plane); the first launch stores C, the others add into it (TMA
+// reduce-add, wrap mod 2^64, exact for certified results).  A plain
+// L <= 4 base-2^b plan with one B plane takes launch_gemm_tc (incl. the
+// CTA-pair kernel).
+ne_status launch_gemm_planes(int M, const int8_t* planes, int LA, const int32_t* a_shift, const int8_t* Bt, int LB,
+                             int64_t rows, int64_t cols, int64_t K, const ne_streams& C, cudaStream_t s) {
+  if (LA < 1 || LA > 8 || LB < 1 || LB > 4) return NE_EINVAL;
+  bool uniform = LA <= 4 && LB == 1;
+  const int b = LA > 1 ? a_shift[1] - a_shift[0] : 8;
+  for (int i = 0; i < LA && uniform; ++i) uniform = a_shift[i] == b * i;
+  if (uniform && b >= 8 && b <= 63) return launch_gemm_tc(M, LA, b, planes, Bt, rows, cols, K, C, s);
+  bool first = true;
+  for (int j = 0; j < LB; ++j)
+    for (int g = 0; g < LA; g += 4) {
+      tc::Plan pl{};
+      const int Lsub = LA - g < 4 ? LA - g : 4;
+      int mx = 0;
+      for (int i = 0; i < Lsub; ++i) {
+        pl.sh[i] = a_shift[g + i] + 8 * j;
+        if (pl.sh[i] < 0 || pl.sh[i] > 63) return NE_EINVAL;
+        mx = pl.sh[i] > mx ? pl.sh[i] : mx;
+      }
+      pl.small = mx <= 30;
+      pl.a_total = LA;
+      pl.a0 = g;
+      pl.b_row0 = (int64_t)j * cols;
+      pl.accumulate = first ? 0 : 1;
+      const ne_status st = run_plan(M, Lsub, planes, Bt, LB, rows, cols, K, C, s, pl);
+      if (st != NE_OK) return st;
+      first = false;
+    }
+  return NE_OK;
 }
 
 // One stream's GEMM (M = 1) with row block j of the output stored to dests[j]

@@ -167,6 +167,63 @@ static void launch_pinner(int M, bool vb, int grid, cudaStream_t s, const ne_cst
   }
 }
 
+// One stream's permutation + blocked inner product over output blocks
+// [b_begin, b_begin + b_count): out_m[b - b_begin] = sum_{i in block b}
+// x_m[perm[i]] v[i mod vlen] (wrap mod 2^64).  A warp per block, 8 gathers in
+// flight per lane; the C4 stream-per-GPU placement.
+template <bool VB>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+k_pinner_stream(const int64_t* __restrict__ x, const int32_t* __restrict__ perm, int64_t n,
+                const int32_t* __restrict__ v, int64_t vlen, int64_t block, int64_t b_begin, int64_t b_count,
+                int64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t j = (int64_t)blockIdx.x * kWarpsPerCta + warp; j < b_count; j += (int64_t)gridDim.x * kWarpsPerCta) {
+    const int64_t b = b_begin + j;
+    const int64_t p_begin = b * block;
+    const int64_t p_end = p_begin + block < n ? p_begin + block : n;
+    uint64_t acc = 0;
+    for (int64_t p0 = p_begin + lane; p0 < p_end; p0 += 32 * kU) {
+      int64_t idx[kU];
+      uint64_t coef[kU], val[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t p = p0 + 32 * u;
+        const bool ok = p < p_end;
+        idx[u] = ok ? (int64_t)__ldcs(perm + p) : -1;
+        coef[u] = ok ? (uint64_t)(int64_t)__ldg(v + (VB ? (p - p_begin) : (p % vlen))) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) val[u] = idx[u] >= 0 ? (uint64_t)__ldcs(x + idx[u]) : 0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) acc += val[u] * coef[u];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[j] = (int64_t)acc;
+  }
+}
+
+extern "C" ne_status ne_op_permute_inner_stream(const ne_config* cfg, const int64_t* x_m, const int32_t* perm,
+                                                int64_t n_total, const int32_t* v, int64_t vlen, int64_t block,
+                                                int64_t b_begin, int64_t b_count, int64_t* out_m,
+                                                ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (n_total < 0 || n_total > INT32_MAX || block < 1 || vlen < 1 || !v || b_begin < 0 || b_count < 0) return NE_EINVAL;
+  const int64_t nb = (n_total + block - 1) / block;
+  if (b_begin + b_count > nb) return NE_EINVAL;
+  if (b_count == 0) return NE_OK;
+  if (!x_m || !perm || !out_m || !aligned16(x_m)) return NE_EINVAL;
+  const int grid = grid_for(b_count, kWarpsPerCta, 8);
+  if (vlen == block)
+    k_pinner_stream<true><<<grid, kWarpsPerCta * 32, 0, cs(stream)>>>(x_m, perm, n_total, v, vlen, block, b_begin,
+                                                                       b_count, out_m);
+  else
+    k_pinner_stream<false><<<grid, kWarpsPerCta * 32, 0, cs(stream)>>>(x_m, perm, n_total, v, vlen, block, b_begin,
+                                                                        b_count, out_m);
+  return launch_status();
+}
+
 extern "C" ne_status ne_op_inner(const ne_config* cfg, ne_cstreams x, int64_t n_total, const int32_t* v,
                                  int64_t vlen, int64_t block, ne_streams out, ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);

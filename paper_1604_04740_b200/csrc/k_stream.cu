@@ -770,6 +770,89 @@ extern "C" ne_status ne_entangle_limbs_stream(const ne_config* cfg, int32_t m, c
   return launch_status();
 }
 
+// The split ("mixed-radix") digit plan of the GEMM operand:
+// eps_m = c_m + 2^l c_{m-1} held as 2D int8 planes — the D balanced base-256
+// digits of c_m (bit weights 0, 8, ..) and the D digits of c_{m-1} (weights
+// l, l + 8, ..): planes[(m*2D + i)*n + idx].  Stream m's planes hold only
+// stream m's operand (stream-local: a fault in stream m's product still
+// corrupts delta_m alone, Props 2/4).  4 positions per thread; a value the D
+// digits cannot hold, or |c| > hi, is a range violation naming m*n + idx.
+template <int MT, int D>
+__global__ void __launch_bounds__(kThreads)
+k_entangle_split(const __grid_constant__ ne_cstreams32 c, int M_rt, int64_t hi, int64_t n,
+                 int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
+  constexpr int MA = MT > 0 ? MT : NE_MAX_M;
+  const int M = MT > 0 ? MT : M_rt;
+  constexpr int64_t bias = (int64_t)(0x8080808080808080ull >> (64 - 8 * D));
+  constexpr int64_t span = (int64_t)1 << (8 * D);
+  int bad = 0;
+  long long first = LLONG_MAX;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n / 4; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = 4 * v;
+    int4 q[MA];
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) q[m] = __ldcs(reinterpret_cast<const int4*>(c.s[m] + n0));
+#pragma unroll
+    for (int m = 0; m < (MT > 0 ? MT : M); ++m) {
+      const int4 cur = q[m], prv = q[m == 0 ? M - 1 : m - 1];
+      const int32_t cc[4] = {cur.x, cur.y, cur.z, cur.w}, pp[4] = {prv.x, prv.y, prv.z, prv.w};
+      uint32_t w[2 * D];
+#pragma unroll
+      for (int j = 0; j < 2 * D; ++j) w[j] = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t ylo = (int64_t)cc[i] + bias, yhi = (int64_t)pp[i] + bias;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          w[j] |= (uint32_t)(((ylo >> (8 * j)) & 0xff) ^ 0x80) << (8 * i);
+          w[D + j] |= (uint32_t)(((yhi >> (8 * j)) & 0xff) ^ 0x80) << (8 * i);
+        }
+        // c_m's digits are checked here; c_{m-1}'s by stream m-1 (the same value)
+        if (cc[i] > hi || cc[i] < -hi || ylo < 0 || ylo >= span) {
+          ++bad;
+          const long long idx = (long long)m * n + n0 + i;
+          first = idx < first ? idx : first;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2 * D; ++j)
+        __stcs(reinterpret_cast<unsigned int*>(planes + ((int64_t)m * 2 * D + j) * n + n0), w[j]);
+    }
+  }
+  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
+}
+
+extern "C" ne_status ne_entangle_plan(const ne_config* cfg, ne_cstreams32 c, int64_t n_total, const ne_gemm_plan* plan,
+                                      int8_t* planes, ne_diag* diag, ne_stream_t stream) {
+  ne_status st = validate_cfg(cfg);
+  if (st != NE_OK) return st;
+  if (!plan) return NE_EINVAL;
+  if (plan->kind == NE_PLAN_EPS) return ne_entangle_limbs(cfg, c, n_total, plan->LA, plan->digit_bits, planes, diag, stream);
+  if (plan->kind != NE_PLAN_SPLIT || plan->LA < 2 || plan->LA > 8 || plan->LA % 2) return NE_EINVAL;
+  if (n_total == 0) return NE_OK;
+  if (n_total < 0 || n_total % 16 != 0 || !streams_ok32(c, cfg->M) || !planes || !aligned16(planes)) return NE_EINVAL;
+  const int64_t hi = range_hi(cfg);
+  const int grid = grid_for(n_total / 4, kThreads);
+  cudaStream_t s = cs(stream);
+#define NE_SPLIT(MV, DV) k_entangle_split<MV, DV><<<grid, kThreads, 0, s>>>(c, cfg->M, hi, n_total, planes, diag)
+#define NE_SPLIT_D(MV)            \
+  switch (plan->LA / 2) {          \
+    case 1: NE_SPLIT(MV, 1); break; \
+    case 2: NE_SPLIT(MV, 2); break; \
+    case 3: NE_SPLIT(MV, 3); break; \
+    default: NE_SPLIT(MV, 4); break; \
+  }
+  switch (cfg->M) {
+    case 3: NE_SPLIT_D(3); break;
+    case 4: NE_SPLIT_D(4); break;
+    case 8: NE_SPLIT_D(8); break;
+    default: NE_SPLIT_D(0); break;
+  }
+#undef NE_SPLIT_D
+#undef NE_SPLIT
+  return launch_status();
+}
+
 extern "C" ne_status ne_entangle_shared(const ne_config* cfg, const int32_t* g, int64_t* g_ent,
                                         int64_t n_total, ne_stream_t stream) {
   ne_status st = validate_cfg(cfg);

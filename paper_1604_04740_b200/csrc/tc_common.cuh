@@ -148,14 +148,17 @@ static inline EncodeTiledFn encode_fn() {
 }
 
 // 2-D int8 tensor [outer][inner] (inner contiguous), box {SW, box_outer}, SW-byte swizzle
-static inline bool make_out_map(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows) {
+// (u64 = true: the reduce-add maps of accumulating launches — the same bytes,
+// added with wrap mod 2^64)
+static inline bool make_out_map(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, bool u64 = false) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 8};
   cuuint32_t box[2] = {16, 32};
   cuuint32_t estr[2] = {1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+  return fn(map, u64 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<void*>(base),
+            dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

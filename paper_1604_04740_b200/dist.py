@@ -1,4 +1,6 @@
-"""Multi-GPU orchestration of the hot path (BASELINE configs[4]).
+"""Multi-GPU orchestration of the hot path (BASELINE configs[4]),
+and the partition helpers of C1-C4 (position ranges, the C2 halo exchange,
+row ranges, the C4 stream placement and its all_gather).
 
 C5 — "M = 8 streams, one per GPU on 8xB200: entangled GEMM 16384^3 int32 in
 [-32, 32), rows sharded; kill one rank's output, recover all streams from the
@@ -24,10 +26,10 @@ c5_step_failstop is the REAL fail-stop (NEXT-4, world == M): the rank holding
 stream plan.kill terminates its process right after its GEMM (os._exit), the
 survivors detect it by heartbeat keys in the rendezvous store (a missing key
 after `timeout_s` = a dead rank; the first published view wins via
-compare_set, so every survivor adopts the same one), tear down the old
-communicator (it includes the dead peer), form a new world of the survivors
-on a fresh store prefix, exchange the M-1 surviving outputs there and recover
-all M streams (Props 1/3).  With no failure the same step runs the check.
+compare_set, so every survivor adopts the same one), shrink the communicator
+to the survivors (NCCL: ncclCommShrink with NCCL_SHRINK_ABORT via torch's
+shrink_group; gloo: a new world on a fresh store prefix), exchange the M-1
+surviving outputs there and recover all M streams (Props 1/3).  With no failure the same step runs the check.
 The store must outlive any single rank (torchrun's agent store, or a
 TCPStore the launcher hosts); the process that hosts it must not be killed.
 
@@ -190,6 +192,124 @@ class SymmWindow:
             self.hdl.barrier(channel=0)
 
 
+# ---------------------------------------------------------------- C1-C4 partitions (SURVEY §8(e))
+# C1: contiguous position ranges, all M streams of a range on one rank (a1-a5
+#     local; the counters are all-reduced after the step).
+# C2: contiguous position ranges plus a circular halo of the previous rank's
+#     last HALO >= T - 1 entangled positions (one send/recv per stream).
+# C3: row ranges of every A_m (all M streams per rank, so the check stays
+#     local), B replicated (regenerated from the seed, untimed).
+# C4: one entangled stream per rank (world <= M: stream m on rank m mod world;
+#     world = k M: stream r // k on rank r, block part r mod k), an all_gather
+#     of the per-stream block sums, then each rank checks its block range.
+HALO = 64  # >= T - 1 = 63 (C2), even: the rank's own range starts 16-B aligned
+
+
+def part_range(n: int, parts: int, j: int, align: int = 1) -> tuple[int, int]:
+    """[lo, hi) of part j when [0, n) is split into `parts` contiguous ranges
+    whose boundaries are multiples of `align` (n itself need not be)."""
+    units = -(-n // align)
+    lo = min(n, j * units // parts * align)
+    hi = min(n, (j + 1) * units // parts * align)
+    return lo, hi
+
+
+def _coll_tensor(t: torch.Tensor, group=None) -> torch.Tensor:
+    """gloo collectives take CPU tensors (the NE_BENCH_SHARE_GPU test hook and
+    the CPU tests); NCCL takes the CUDA tensor itself."""
+    if t.is_cuda and dist.get_backend(group) != "nccl":
+        return t.cpu()
+    return t
+
+
+def halo_exchange(ext: Sequence[torch.Tensor], H: int, L: int, group=None) -> None:
+    """ext[m] holds positions [lo - H, hi) of stream m (H + L entries, the
+    rank's own L from index H).  Fill ext[m][:H] with the previous rank's last
+    H positions (circularly: rank 0 receives the last rank's) — one send and
+    one receive per stream; with one rank, the stream's own tail."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if L < H:
+        raise ValueError(f"halo of {H} positions needs >= {H} positions per rank (got {L})")
+    if world == 1:
+        for t in ext:
+            t[:H].copy_(t[L:L + H])
+        return
+    rank = dist.get_rank(group)
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+    if group is not None:
+        nxt, prv = dist.get_global_rank(group, nxt), dist.get_global_rank(group, prv)
+    sends = [_coll_tensor(t[L:L + H].contiguous(), group) for t in ext]
+    recvs = [torch.empty_like(x) for x in sends]
+    ops = []
+    for snd, rcv in zip(sends, recvs):
+        ops.append(dist.P2POp(dist.isend, snd, nxt, group))
+        ops.append(dist.P2POp(dist.irecv, rcv, prv, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    for t, rcv in zip(ext, recvs):
+        t[:H].copy_(rcv)
+
+
+def c4_placement(M: int, world: int, rank: int) -> list[tuple[int, int, int]]:
+    """(stream m, block part, parts) items of `rank`: world <= M: every stream
+    m with m mod world == rank, whole (1 part); world = k M: stream rank // k,
+    part rank mod k of k (each stream on k GPUs, each computing its share of
+    the output blocks)."""
+    if world <= M:
+        return [(m, 0, 1) for m in range(M) if m % world == rank]
+    if world % M:
+        raise ValueError(f"C4 placement needs world <= M or a multiple of M (M={M}, world={world})")
+    k = world // M
+    return [(rank // k, rank % k, k)]
+
+
+def c4_payload(M: int, world: int, rank: int, nb: int) -> list[tuple[int, int, int]]:
+    """(m, b_lo, b_hi) block ranges of rank's block sums, in payload order."""
+    return [(m, *part_range(nb, k, j)) for m, j, k in c4_placement(M, world, rank)]
+
+
+def c4_allgather(local: Sequence[torch.Tensor], M: int, nb: int, group=None) -> list[torch.Tensor]:
+    """all_gather of every rank's block sums (its c4_payload items, in order):
+    returns the M full streams of nb block sums on every rank.  Payloads are
+    padded to the largest one; with the placements above every stream ends up
+    contiguous in the gathered buffer, so the streams are views of it."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lay = [c4_payload(M, world, r, nb) for r in range(world)]
+    width = max(sum(hi - lo for _, lo, hi in it) for it in lay)
+    mine = torch.cat(list(local)) if local else torch.empty(0, dtype=torch.int64)
+    dev = mine.device
+    if mine.numel() < width:
+        mine = torch.cat([mine, torch.zeros(width - mine.numel(), dtype=torch.int64, device=dev)])
+    if world == 1:
+        full = mine
+    else:
+        snd = _coll_tensor(mine, group)
+        full = torch.empty(world * width, dtype=torch.int64, device=snd.device)
+        dist.all_gather_into_tensor(full, snd, group=group)
+        full = full.to(dev)
+    pieces = {m: [] for m in range(M)}
+    for r, it in enumerate(lay):
+        off = r * width
+        for m, lo, hi in it:
+            pieces[m].append((lo, off, hi - lo))
+            off += hi - lo
+    out = []
+    for m in range(M):
+        ps = sorted(pieces[m])
+        lo0, off0, _ = ps[0]
+        contiguous = lo0 == 0 and all(ps[i][1] == off0 + ps[i][0] for i in range(len(ps))) and \
+            sum(c for _, _, c in ps) == nb
+        if contiguous:
+            out.append(full[off0:off0 + nb])
+        else:
+            t = torch.empty(nb, dtype=torch.int64, device=dev)
+            for lo, off, c in ps:
+                t[lo:lo + c] = full[off:off + c]
+            out.append(t)
+    return out
+
+
 # ---------------------------------------------------------------- host logic
 def owned_streams(M: int, world: int, rank: int) -> list[int]:
     """Stream m lives on rank m mod world (one stream per GPU when world == M)."""
@@ -226,8 +346,10 @@ def position_major_exchange(local: dict[int, torch.Tensor], M: int, members: lis
     recv_sizes = [(hi - lo) * c for c in counts]
     dev = next(iter(local.values())).device if local else _dev(group)
     send = torch.cat(send_chunks) if send_chunks else torch.empty(0, dtype=torch.int64, device=dev)
-    recv = torch.empty(sum(recv_sizes), dtype=torch.int64, device=dev)
+    send = _coll_tensor(send, group)   # gloo (CPU tests, the share-GPU bench hook): staged through host memory
+    recv = torch.empty(sum(recv_sizes), dtype=torch.int64, device=send.device)
     dist.all_to_all_single(recv, send, recv_sizes, send_sizes, group=group)
+    recv = recv.to(dev)
     out, off = {}, 0
     for src_ids, c in zip(ids, counts):
         for m in src_ids[:c]:
@@ -418,14 +540,28 @@ def detect_alive(store, epoch: int, world: int, rank: int, timeout_s: float) -> 
     return [int(x) for x in agreed.split(",") if x != ""]
 
 
-def reform_world(store, epoch: int, view: list[int], rank: int, backend_name: str) -> None:
-    """Replace the default process group (which includes the dead peer) by a
-    new one over the survivors in `view`, on a fresh store prefix."""
-    if dist.is_initialized():
-        dist.destroy_process_group()
-    prefix = dist.PrefixStore(f"ne/world/{epoch}", store)
-    dist.init_process_group(backend_name, store=prefix, rank=view.index(rank), world_size=len(view),
-                            timeout=timedelta(seconds=120))
+def reform_world(store, epoch: int, view: list[int], rank: int, backend_name: str, dead: Sequence[int] = (),
+                 api=dist) -> str:
+    """Replace the default process group (which includes the dead peer) by one
+    over the survivors in `view` (new ranks = positions in `view`).
+
+    NCCL: NCCL's own survivor path — ncclCommShrink of the parent
+    communicator with NCCL_SHRINK_ABORT (torch's shrink_group with
+    SHRINK_ABORT): the dead rank's outstanding operations are aborted and the
+    survivors' communicator is derived from the parent's (no new bootstrap
+    through the store); torch makes it the new default group and aborts the
+    parent.  Other backends (gloo: the CPU tests) have no shrink: the old
+    group is destroyed and a new world is formed on a fresh store prefix.
+    Returns "shrink" or "reinit"."""
+    if backend_name == "nccl" and hasattr(api, "shrink_group"):
+        api.shrink_group(sorted(dead), shrink_flags=api.distributed_c10d.SHRINK_ABORT)
+        return "shrink"
+    if api.is_initialized():
+        api.destroy_process_group()
+    prefix = api.PrefixStore(f"ne/world/{epoch}", store)
+    api.init_process_group(backend_name, store=prefix, rank=view.index(rank), world_size=len(view),
+                           timeout=timedelta(seconds=120))
+    return "reinit"
 
 
 def c5_step_failstop(backend, plan: C5Plan, inp: dict, store, epoch: int = 0, timeout_s: float = 10.0,
@@ -461,7 +597,7 @@ def c5_step_failstop(backend, plan: C5Plan, inp: dict, store, epoch: int = 0, ti
     if len(dead) > 1:
         raise RuntimeError(f"unrecoverable: {len(dead)} streams lost (S:113)")
     r = dead[0]  # stream r == rank r
-    reform_world(store, epoch, view, rank, backend_name)
+    how = reform_world(store, epoch, view, rank, backend_name, dead)
     backend.mark("reform")
     members = list(range(len(view)))
     me = view.index(rank)
@@ -470,7 +606,7 @@ def c5_step_failstop(backend, plan: C5Plan, inp: dict, store, epoch: int = 0, ti
     d_rec = backend.recover([None if j == r else sl2[j] for j in range(M)], r)
     backend.mark("exchange_recover")
     result.update(flagged=None, recovered_stream=r, recover_slice=(lo2, d_rec), new_rank=me,
-                  new_world=len(members))
+                  new_world=len(members), reform=how)
     return result
 
 

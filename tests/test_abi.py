@@ -132,8 +132,33 @@ def test_gemm_kernel_for_names_the_timed_kernels():
     assert ne.ne_gemm_kernel_for(c8, 2, 8, 2048, 16384, 16384) == "cta"    # C5: K > 8192
     assert ne.ne_gemm_kernel_for(c8, 2, 8, 2048, 1024, 2048) == "pair"     # 256 pair tiles at K = 2048
     assert ne.ne_gemm_kernel_for(c3, L, b, 384, 512, 4096) == "cta"        # rows not a multiple of 256
+    assert ne.ne_gemm_kernel_for(c3, 1, 8, 4096, 4096, 4096) == "pair"     # one digit: plain baselines, ABFT data
+    assert ne.ne_gemm_kernel_for(c3, 1, 8, 512, 512, 4096) == "cta"        # 12 pair tiles: too few
     with pytest.raises(ne.NeError):
         ne.ne_gemm_kernel_for(c3, L, b, 100, 512, 4096)
+
+
+def test_gemm_plan_for():
+    """The digit plan of the wide-range tensor-core GEMM: the two-digit plan
+    for |c| <= 127, the split (mixed-radix) plan when 2 x digits(|c|) is
+    fewer planes than base-256 digits of eps, else base 256 of eps; B in
+    balanced base-256 digits."""
+    c3, c4, c8 = ne.ne_config_for(3), ne.ne_config_for(4), ne.ne_config_for(8)
+
+    def plan(cfg, a, b):
+        p = ne.ne_gemm_plan_for(cfg, a, b)
+        return ("split" if p.kind else "eps", p.LA, p.digit_bits, p.LB, list(p.a_shift)[:p.LA])
+
+    assert plan(c3, 64, 64) == ("eps", 2, 22, 1, [0, 22])
+    assert plan(c3, 128, 127) == ("eps", 4, 8, 1, [0, 8, 16, 24])
+    assert plan(c3, 1 << 10, 128) == ("split", 4, 8, 2, [0, 8, 22, 30])
+    assert plan(c3, 1 << 15, 1 << 15) == ("eps", 5, 8, 3, [0, 8, 16, 24, 32])
+    assert plan(c3, 1 << 20, 127) == ("eps", 6, 8, 1, [0, 8, 16, 24, 32, 40])
+    assert plan(c8, 32, 32) == ("eps", 2, 8, 1, [0, 8])
+    assert plan(c4, 1000, 2 ** 31 - 1)[3] == 5      # every int32 B: 5 balanced digits
+    assert plan(c4, 2 ** 31 - 1, 1)[1] <= 8          # every int32 c: at most 8 planes
+    with pytest.raises(ne.NeError):
+        ne.ne_gemm_plan_for(c3, -1, 1)
 
 
 def test_argument_validation_of_the_newer_entry_points(L):

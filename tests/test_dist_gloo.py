@@ -226,3 +226,58 @@ def test_c5_real_failstop_no_failure_runs_the_check():
     out = _run_failstop(8, dict(SMALL, kill=None))
     for rank, key, ok, view, new_rank, flagged, covered in out:
         assert key == "check_slice" and ok and flagged == 0 and view == list(range(8))
+
+
+class _FakeDist:
+    """Records the calls reform_world makes (no communicator is touched)."""
+
+    class distributed_c10d:
+        SHRINK_ABORT, SHRINK_DEFAULT = 1, 0
+
+    def __init__(self, with_shrink=True):
+        self.calls = []
+        if with_shrink:
+            self.shrink_group = lambda ranks, shrink_flags=0: self.calls.append(("shrink_group", ranks, shrink_flags))
+
+    def is_initialized(self):
+        self.calls.append(("is_initialized",))
+        return True
+
+    def destroy_process_group(self):
+        self.calls.append(("destroy_process_group",))
+
+    def PrefixStore(self, prefix, store):  # noqa: N802 (mirrors torch.distributed)
+        self.calls.append(("PrefixStore", prefix))
+        return (prefix, store)
+
+    def init_process_group(self, backend, store, rank, world_size, timeout):
+        self.calls.append(("init_process_group", backend, rank, world_size))
+
+
+def test_failstop_reform_uses_nccl_shrink_with_abort():
+    """f4: on NCCL the survivors take NCCL's own fault path — one
+    shrink_group(dead, SHRINK_ABORT) (ncclCommShrink with NCCL_SHRINK_ABORT:
+    the parent's pending work aborted, the survivors' communicator derived
+    from it) and nothing else; no destroy / re-bootstrap.  Without shrink
+    support (gloo) the old world is destroyed and re-formed on a fresh store
+    prefix with the survivors' new ranks."""
+    from paper_1604_04740_b200.dist import reform_world
+
+    api = _FakeDist()
+    view = [0, 1, 2, 4, 5, 6, 7]
+    assert reform_world("store", 1, view, 5, "nccl", dead=[3], api=api) == "shrink"
+    assert api.calls == [("shrink_group", [3], 1)]
+    api = _FakeDist(with_shrink=False)
+    assert reform_world("store", 1, view, 5, "nccl", dead=[3], api=api) == "reinit"
+    api = _FakeDist()
+    assert reform_world("store", 2, view, 5, "gloo", dead=[3], api=api) == "reinit"
+    assert api.calls == [("is_initialized",), ("destroy_process_group",), ("PrefixStore", "ne/world/2"),
+                         ("init_process_group", "gloo", 4, 7)]
+
+
+def test_torch_exposes_nccl_shrink():
+    """The NCCL survivor path needs torch's shrink_group and the NCCL
+    backend's shrink (ncclCommShrink, NCCL >= 2.27; torch bundles 2.28)."""
+    assert hasattr(dist, "shrink_group") and hasattr(dist.distributed_c10d, "SHRINK_ABORT")
+    assert hasattr(torch._C._distributed_c10d, "ProcessGroupNCCL")
+    assert hasattr(torch._C._distributed_c10d.ProcessGroupNCCL, "shrink")

@@ -412,6 +412,41 @@ def test_gemm_imad64(O, rows, cols, K):
     assert (to_np(out) == ref).all()
 
 
+@pytest.mark.parametrize("rows,cols,K", [(128, 128, 16), (256, 384, 4096), (100, 37, 129)])
+def test_gemm_imad32w(O, rows, cols, K):
+    """The CUDA-core comparison point with one IMAD.WIDE per MAC (every
+    entangled entry fits int32, C3's operand): equal to the oracle; a shape
+    that is not tile-aligned runs the 64-bit form, same result."""
+    M = 3
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    A = np.stack([O.gen_uniform(3, 4, m, -64, 64, rows * K) for m in range(M)])
+    B = O.gen_uniform(3, 5, 0, -2 ** 31, 2 ** 31 - 1, K * cols)
+    E = O.entangle(ocfg, A)
+    out = empty_streams(M, rows * cols)
+    diag = ne.diag_new()
+    ne.ne_op_gemm(cfg, to_streams(E, torch.int64), dev(B, torch.int32), rows, cols, K, out,
+                  algo=ne.NE_GEMM_IMAD32W, diag=diag)
+    assert ne.diag_read(diag)["range_violations"] == 0
+    ref = O.op_gemm(ocfg, E.reshape(M, rows, K), B.reshape(K, cols)).reshape(M, -1)
+    assert (to_np(out) == ref).all()
+
+
+def test_gemm_imad32w_range_violation(O):
+    """An entangled entry outside int32 is named in diag (the 64-bit form is
+    the one for such operands)."""
+    M, rows, cols, K = 3, 128, 128, 32
+    cfg = ne.ne_config_for(M)
+    E = np.zeros((M, rows * K), dtype=np.int64)
+    E[1, 5 * K + 7] = 2 ** 31
+    E[2, 3] = -2 ** 31 - 1
+    out = empty_streams(M, rows * cols)
+    diag = ne.diag_new()
+    ne.ne_op_gemm(cfg, to_streams(E, torch.int64), torch.ones(K * cols, dtype=torch.int32, device="cuda"), rows,
+                  cols, K, out, algo=ne.NE_GEMM_IMAD32W, diag=diag)
+    d = ne.diag_read(diag)
+    assert d["range_violations"] == 2 and d["first_bad"] == 1 * rows * K + 5 * K + 7
+
+
 @pytest.mark.parametrize("M,L,bound,rows,cols,K", [
     (3, 4, 64, 128, 128, 128), (3, 4, 64, 256, 384, 512), (8, 2, 32, 128, 256, 256),
     (4, 4, 1000, 128, 128, 1024), (3, 3, 1, 128, 128, 256), (3, 1, 0, 128, 256, 128), (8, 2, 32, 256, 128, 128)])
@@ -508,6 +543,41 @@ def test_gemm_pair_multi_tile(O):
             assert (out[m].cpu().numpy().reshape(R, Cc) @ x == E[m] @ bx).all(), (cap, m)
 
 
+@pytest.mark.parametrize("cap", [0, 3])
+def test_gemm_pair_one_digit(O, cap):
+    """One int8 digit (plain data: the overhead baselines, ABFT's data GEMM)
+    runs on the pair kernel's double-buffered mode (tile t in TMEM half
+    t & 1): M = 4 streams of 1024 x 1024 at K = 2048 = 64 pair tiles, with
+    the full grid and with the grid capped at 3 pairs (21-22 tiles each,
+    both halves reused many times).  Sampled rows in every 32-lane group of
+    128-row half (cycling) vs the oracle, whole output by Freivalds."""
+    M, R, Cc, K = 4, 1024, 1024, 2048
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    assert ne.ne_gemm_kernel_for(cfg, 1, 8, R, Cc, K) == "pair"
+    A = gen(O, 83, 4, M, R * K, -128, 128)
+    B = O.gen_uniform(83, 5, 0, -128, 128, K * Cc)
+    planes = torch.empty(M * R * K, dtype=torch.int8, device="cuda")
+    ne.ne_to_limbs(to_streams(A), 1, planes)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    out = empty_streams(M, R * Cc)
+    ne.ne_gemm_trace(None, cap)
+    try:
+        ne.ne_op_gemm_limbs(cfg, planes, 1, Bt, R, Cc, K, out, limb_bits=8)
+        torch.cuda.synchronize()
+    finally:
+        ne.ne_gemm_trace(None, 0)
+    A3 = A.reshape(M, R, K)
+    rows = _band_rows_cyclic(R, 128)
+    ref = O.op_gemm(ocfg, A3[:, rows], B.reshape(K, Cc))
+    got = np.stack([out[m].view(R, Cc)[torch.from_numpy(rows).cuda()].cpu().numpy() for m in range(M)])
+    assert (got == ref).all()
+    x = np.random.default_rng(4).integers(-2 ** 16, 2 ** 16, size=Cc)   # |A (B x)| <= 2^11 2^7 2^34 < 2^63
+    bx = B.reshape(K, Cc) @ x
+    for m in range(M):
+        assert (out[m].cpu().numpy().reshape(R, Cc) @ x == A3[m] @ bx).all(), m
+
+
 def test_gemm_pair_short_k_many_tiles_sampled(O):
     """K = 2048 with >= 256 pair tiles also runs on the pair kernel (the
     paper's M = 8, N = 2000 shape class): rows sampled from every 256-row pair
@@ -571,6 +641,68 @@ def test_gemm_capped_persistent_grid_and_trace(O, max_clusters):
             assert r[2] <= r[0] <= r[1]          # MMA start <= accumulators full <= epilogue end
             if i:
                 assert rows[i - 1][0] <= r[2]   # single TMEM set: next tile starts after the previous is full
+
+
+@pytest.mark.parametrize("M,a,b,R,Cc,K", [
+    (3, 128, 127, 256, 512, 256),          # base-256 eps, 4 planes (one launch, the L = 4 kernel)
+    (3, 1 << 10, 127, 256, 512, 384),      # split plan: c_m, c_{m-1} in 2 digits each at 0, 8, l, l + 8
+    (3, 1 << 10, 128, 256, 512, 256),      # split plan x 2 B planes: reduce-add launches
+    (3, 1 << 15, 1 << 15, 128, 256, 256),  # 5 eps planes (4 + 1 accumulators) x 3 B planes = 6 launches
+    (4, 1 << 20, 1 << 15, 128, 256, 128),
+    (8, 1 << 20, 1 << 10, 128, 384, 128),  # l = 8: eps digits overlap byte-aligned
+])
+def test_gemm_wide_range_plans(O, M, a, b, R, Cc, K):
+    """The tensor-core GEMM over the certified operand range (missing in
+    round 1): ne_gemm_plan_for's plan, the operand entangled into its digit
+    planes, B into its digit planes, the multi-launch product — delta equal
+    to the oracle's E B (mod 2^64 on both sides), the planes equal to the
+    operands' digit expansions, and d_hat equal to the plain product when the
+    product is certified (K a b <= hi)."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    plan = ne.ne_gemm_plan_for(cfg, a, b)
+    A = gen(O, 90, 4, M, R * K, -a, a + 1)
+    A[:, 0], A[:, 1] = a, -a
+    B = O.gen_uniform(90, 5, 0, -b, b + 1, K * Cc)
+    B[0], B[1] = b, -b
+    planes = torch.empty(M * plan.LA * R * K, dtype=torch.int8, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_entangle_plan(cfg, to_streams(A), plan, planes, diag)
+    Bt = torch.empty(plan.LB * Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b_planes(dev(B, torch.int32), K, Cc, plan.LB, Bt, diag)
+    assert ne.diag_read(diag)["range_violations"] == 0
+    E = O.entangle(ocfg, A)
+    p = planes.cpu().numpy().astype(np.int64).reshape(M, plan.LA, R * K)
+    assert (sum(p[:, i] << plan.a_shift[i] for i in range(plan.LA)) == E).all()
+    q = Bt.cpu().numpy().astype(np.int64).reshape(plan.LB, Cc, K)
+    assert (sum(q[j] << (8 * j) for j in range(plan.LB)).T.reshape(-1) == B).all()
+    out = empty_streams(M, R * Cc)
+    ne.ne_op_gemm_plan(cfg, planes, plan, Bt, R, Cc, K, out)
+    ref = O.op_gemm(ocfg, E.reshape(M, R, K), B.reshape(K, Cc)).reshape(M, -1)
+    assert (to_np(out) == ref).all()
+    if K * a * b <= O.dynamic_range(ocfg):
+        d = empty_streams(M, R * Cc)
+        ne.ne_disentangle_check(cfg, out, 0, d, None, diag)
+        assert ne.diag_read(diag)["fault_positions"] == 0
+        assert (to_np(d) == (A.reshape(M, R, K) @ B.reshape(K, Cc)).reshape(M, -1)).all()
+
+
+def test_gemm_full_int64_operand_range(O):
+    """ne_op_gemm (TC) over the widest operands: entangled A of full-range
+    int32 inputs (8 base-256 digit planes) times full-range int32 B (5 digit
+    planes): 16 tcgen05 launches accumulating into delta, equal to the
+    oracle's wrapped int64 product (no operand range is refused)."""
+    M, R, Cc, K = 3, 128, 256, 128
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    A = gen(O, 91, 4, M, R * K, -2 ** 31, 2 ** 31 - 1)
+    B = O.gen_uniform(91, 5, 0, -2 ** 31, 2 ** 31 - 1, K * Cc)
+    E = O.entangle(ocfg, A)
+    ws = torch.empty(ne.ne_gemm_workspace(cfg, R, Cc, K, 8, 5), dtype=torch.int8, device="cuda")
+    out = empty_streams(M, R * Cc)
+    diag = ne.diag_new()
+    ne.ne_op_gemm(cfg, to_streams(E, torch.int64), dev(B, torch.int32), R, Cc, K, out, L=8, ws=ws, diag=diag, LB=5)
+    assert ne.diag_read(diag)["range_violations"] == 0
+    ref = O.op_gemm(ocfg, E.reshape(M, R, K), B.reshape(K, Cc)).reshape(M, -1)
+    assert (to_np(out) == ref).all()
 
 
 # ------------------------------------------------------------------ one-stream-per-GPU entry points (C5)
