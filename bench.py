@@ -255,6 +255,8 @@ class C3Gemm(Workload):
         else:  # the cheapest exact plan: base 2^l, 2 limbs (|A| < 128)
             self.L, self.limb_bits = ne.ne_gemm_limb_plan(self.cfg, 64)
         self.algo = algo
+        if algo != "tc":
+            self.name = f"{self.name}_{algo}"   # traffic.json key of the CUDA-core lines
         self.scheme = scheme
         # disentangle + check fused into the GEMM epilogue (ne_op_gemm_limbs_check)
         self.fuse = bool(fuse) and algo == "tc" and scheme == "entangled"
@@ -415,20 +417,36 @@ class C3Gemm(Workload):
                                                         st["check"]()), reps),
                                     "entangle(limbs)+prep_B+GEMM+disentangle/check")
         out["failstop_recover"] = (self._time(st["recover"], reps), "recover(one stream lost)")
-        for tag, Lp, b in (("plain_same_kernel", L, self.limb_bits), ("plain_native_L1", 1, 8)):
+        scratch = [torch.empty(R * Cc, dtype=torch.int64, device="cuda") for _ in range(M)]
+        for tag, Lp, b in (("plain_same_kernel", L, self.limb_bits), ("plain_L1_int64_out", 1, 8)):
             planes = torch.empty(M * Lp * R * K, dtype=torch.int8, device="cuda")
             kern = ne.ne_gemm_kernel_for(cfg, Lp, b, R, Cc, K)
 
             def run(planes=planes, Lp=Lp, b=b):
                 ne.ne_to_limbs(self.A, Lp, planes, self.diag)
                 ne.ne_gemm_prep_b(self.B, K, Cc, self.Bt, self.diag)
-                ne.ne_op_gemm_limbs(cfg, planes, Lp, self.Bt, R, Cc, K, self.delta, b)
-            out[tag] = (self._time(run, reps), f"int32->int8 planes (L={Lp})+prep_B+GEMM(L={Lp}, {kern} kernel)")
+                ne.ne_op_gemm_limbs(cfg, planes, Lp, self.Bt, R, Cc, K, scratch, b)
+            out[tag] = (self._time(run, reps), f"int32->int8 planes (L={Lp})+prep_B+GEMM(L={Lp}, {kern} kernel, "
+                                               f"int64 out)")
             out[tag + "_gemm_only"] = (self._time(
-                lambda planes=planes, Lp=Lp, b=b: ne.ne_op_gemm_limbs(cfg, planes, Lp, self.Bt, R, Cc, K,
-                                                                      self.delta, b), reps),
-                f"GEMM(L={Lp}) alone")
+                lambda planes=planes, Lp=Lp, b=b: ne.ne_op_gemm_limbs(cfg, planes, Lp, self.Bt, R, Cc, K, scratch, b),
+                reps), f"GEMM(L={Lp}) alone")
             del planes
+        # the narrowest native form: one int8 digit, int32 products (what a plain int8 GEMM returns)
+        if R % 256 == 0 and Cc % 256 == 0:
+            p1 = torch.empty(M * R * K, dtype=torch.int8, device="cuda")
+            o32 = [torch.empty(R * Cc, dtype=torch.int32, device="cuda") for _ in range(M)]
+
+            def run1():
+                ne.ne_to_limbs(self.A, 1, p1, self.diag)
+                ne.ne_gemm_prep_b(self.B, K, Cc, self.Bt, self.diag)
+                ne.ne_op_gemm_plain_i32(p1, self.Bt, R, Cc, K, o32)
+            out["plain_native_L1"] = (self._time(run1, reps), "int32->int8 plane (L=1)+prep_B+GEMM(L=1, pair kernel, "
+                                                               "int32 out)")
+            out["plain_native_L1_gemm_only"] = (self._time(lambda: ne.ne_op_gemm_plain_i32(p1, self.Bt, R, Cc, K, o32),
+                                                           reps), "GEMM(L=1, int32 out) alone")
+            del p1, o32
+        del scratch
         try:  # library context: cuBLASLt int8 GEMM, int32 out, the same M x rows x cols x K multiply-adds
             a8 = torch.randint(-64, 64, (M * R, K), dtype=torch.int8, device="cuda")
             b8 = torch.randint(-64, 64, (K, Cc), dtype=torch.int8, device="cuda")
@@ -649,6 +667,22 @@ class C4PermInner(Workload):
 
     def global_work(self):  # the whole C4 problem's algorithmic bytes (the single-GPU AoS accounting)
         return self.n * (48 + 36) / 1e9
+
+    def extra_roofline(self, dom, ms, peaks):
+        """The gather's own floor (profiles/r02_c4_floor.md): every random
+        32-B sector read costs one 128-B DRAM line fill on B200 (4 sectors per
+        L2 request, unchanged by any cache hint or fetch-granularity limit),
+        so the fused gather + inner + check moves >= 128 B + its 4-B index per
+        gathered position."""
+        if dom != "permute_inner_check" or self.layout != "aos" or getattr(self, "placement", False):
+            return None
+        per = 128 + 4
+        gb = self.n * per / 1e9
+        ach = gb / (ms / 1e3)
+        return {"bytes_per_position": per, "bytes_per_launch_GB": round(gb, 3), "achieved": round(ach, 1),
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
+                "floor_ms": round(gb / peaks["hbm_gbs"] * 1e3, 3),
+                "evidence": "profiles/r02_c4_floor.md (ncu: 4 DRAM sectors per random 32-B load)"}
 
     def stage_info(self):
         n, nb = self.n, self.nb
@@ -1146,55 +1180,68 @@ METRIC = "entangled LSB Gop/s (or GB/s) at 1/2/4/8 B200, % roofline, % overhead 
 
 # ====================================================================== clocks
 class ClockSampler:
-    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock, power and clock-event reasons sampled through NVML every
+    `period_s` (default 2 ms) on a background thread while the timed region
+    runs, so the record covers the kernels that dominate it (the GEMM of a
+    0.6 ms step included); nvidia-smi -lms 20 as the fallback."""
 
-    def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, index, period_s=0.002):
+        self.index, self.period = index, period_s
+        self.rows, self.max_mhz, self.source = [], None, None
+        self._stop = None
+        self._thr = None
 
     def start(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            reasons = [(nm, getattr(N, attr, 0)) for nm, attr in self.REASONS]
+            getr = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+        except Exception:  # noqa: BLE001 — no NVML: no clock record
+            self.source = "unavailable"
+            return
+        self.source = f"NVML every {self.period * 1e3:.0f} ms"
+        self._stop = threading.Event()
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                    pw = N.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    rs = getr(h)
+                    self.rows.append((sm, pw, [nm for nm, bit in reasons if bit and rs & bit]))
+                except Exception:  # noqa: BLE001
+                    pass
+                self._stop.wait(self.period)
+
+        self._thr = threading.Thread(target=loop, daemon=True)
+        self._thr.start()
 
     def stop(self):
-        if self.proc is None:
-            return
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-            out, _ = self.proc.communicate()
-        self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if self._thr is not None:
+            self._stop.set()
+            self._thr.join(timeout=2)
 
     def summary(self):
-        rows = []
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                rows.append((float(f[1]), float(f[2]), f[5], f[6], f[7], f[8]))
-            except ValueError:
-                continue
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        loaded = [r for r in rows if r[0] > 500] or rows
-        reasons = set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for r in loaded:
-            for nm, v in zip(names, r[2:]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": sorted(reasons), "samples": len(loaded)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0, "source": self.source}
+        loaded = [r for r in self.rows if r[0] > 500] or self.rows
+        reasons = sorted({x for r in loaded for x in r[2]})
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_min_mhz": min(r[0] for r in loaded),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(loaded),
+                "power_w_max": round(max(r[1] for r in loaded), 1), "source": self.source}
 
 
 # ====================================================================== runs
@@ -1265,7 +1312,6 @@ def run_c5(args, rank, world, local_rank):
     stage_tot, ok, flagged = {}, True, 0
     clk = ClockSampler(local_rank)
     clk.start()
-    time.sleep(0.05)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
@@ -1455,7 +1501,6 @@ def run_ours(args, rank, world, local_rank):
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)] for _ in range(args.steps)]
     clk = ClockSampler(local_rank)
     clk.start()
-    time.sleep(0.05)
     barrier()
     torch.cuda.synchronize()
     t_host0 = time.perf_counter()
@@ -1489,6 +1534,9 @@ def run_ours(args, rank, world, local_rank):
             graphs[i % nrot].replay()
         torch.cuda.synchronize()
         barrier()
+        clk.stop()   # the clock record covers the timed graph replays (the reported number)
+        clk = ClockSampler(local_rank)
+        clk.start()
         if flush_l2:
             # working set smaller than L2: every timed step starts cold — a 512 MB
             # write evicts the previous step's data, outside the step's own events
@@ -1593,6 +1641,7 @@ def run_ours(args, rank, world, local_rank):
         peak_note = "IMAD pipe: 64 lanes/clk/SM x 148 SMs x max SM clock (DESIGN.md)"
     tr = load_traffic().get(f"{W.name}:{dom}")
     traffic = tr["GB"] if tr else None
+    xr = W.extra_roofline(dom, stage_ms[dom], peaks) if hasattr(W, "extra_roofline") else None
     line = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -1614,7 +1663,8 @@ def run_ours(args, rank, world, local_rank):
                      "unit": runit, "frac": round(achieved / peak, 4), "traffic": traffic,
                      "traffic_unit": "GB per launch, ncu dram__bytes_read.sum + dram__bytes_write.sum "
                                      "(profiles/traffic.json)" if tr else None,
-                     "algorithmic_per_launch": f"{amount:.4g} {unit}", "peak_source": peak_note},
+                     "algorithmic_per_launch": f"{amount:.4g} {unit}", "peak_source": peak_note,
+                     **({"random_access_floor": xr} if xr else {})},
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "stages_timing": ("device time of each stage inside the replayed step graph (event-record nodes, median)"
                           if use_graph else "eager launches, CUDA events between stages"),
@@ -1809,7 +1859,8 @@ def compact(line):
     out["workload"] = line["config"]["workload"]
     if "roofline" in line:
         out["roofline"] = {k: line["roofline"].get(k) for k in ("bound", "kernel", "achieved", "peak", "unit", "frac",
-                                                                  "traffic")}
+                                                                  "traffic", "random_access_floor")
+                           if k in line["roofline"]}
     if "e2e" in line:
         out["e2e"] = {k: line["e2e"].get(k) for k in ("value", "unit", "ms_per_step", "h2d_bytes_per_step",
                                                       "d2h_bytes_per_step")}

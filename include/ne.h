@@ -292,6 +292,16 @@ ne_status ne_op_gemm(const ne_config* cfg, ne_cstreams A, const int32_t* B, int6
                      int64_t cols, int64_t K, ne_gemm_algo algo, int32_t L, int32_t limb_bits, int32_t LB,
                      ne_streams C, void* ws, size_t ws_bytes, ne_diag* diag, ne_stream_t stream);
 
+/* The plain (unentangled) GEMM with int32 products — the narrowest native
+ * baseline of the "% overhead vs plain" comparison (no
+ * entanglement involved): C_m = D_m B for m < count (<= 8), D_m one int8
+ * plane per stream (ne_to_limbs with L = 1) [rows][K], Bt from
+ * ne_gemm_prep_b, C_m int32 [rows][cols] (exact while K * 2^14 < 2^31).  The
+ * CTA-pair kernel with double-buffered TMEM; rows and cols multiples of 256,
+ * K of 128 (else NE_ENOTSUP). */
+ne_status ne_op_gemm_plain_i32(int32_t count, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
+                               int64_t K, ne_streams32 C, ne_stream_t stream);
+
 /* ---- General digit plans of the tensor-core GEMM (the full certified range).
  * An entangled operand eps_m = c_m + 2^l c_{m-1} (Eq. 15) and the shared B are
  * held as int8 digit planes: eps_m = sum_{i<LA} 2^a_shift[i] D_{m,i} and

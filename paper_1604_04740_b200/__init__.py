@@ -33,7 +33,7 @@ EXPORTS = (
     "ne_entangle_limbs_stream", "ne_op_gemm_limbs_stream",
     "ne_op_scale", "ne_op_add", "ne_op_scale_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
-    "ne_gemm_plan_for", "ne_entangle_plan", "ne_gemm_prep_b_planes", "ne_op_gemm_plan",
+    "ne_gemm_plan_for", "ne_entangle_plan", "ne_gemm_prep_b_planes", "ne_op_gemm_plan", "ne_op_gemm_plain_i32",
     "ne_gemm_check_workspace", "ne_op_gemm_limbs_check", "ne_gemm_trace", "ne_gemm_kernel_for", "ne_op_gemm_limbs_scatter",
     "ne_conv_geometry", "ne_entangle_limbs_conv", "ne_conv_prep_taps", "ne_op_conv_limbs",
     "ne_op_scale_add_check", "ne_op_conv_check", "ne_op_scale_add_check_w32",
@@ -105,6 +105,7 @@ _SIGS = {
     "ne_entangle_plan": [_PCFG, Streams, _I64, C.POINTER(GemmPlan), _VP, _VP, _VP],
     "ne_gemm_prep_b_planes": [_VP, _I64, _I64, _I32, _VP, _VP, _VP],
     "ne_op_gemm_plan": [_PCFG, _VP, C.POINTER(GemmPlan), _VP, _I64, _I64, _I64, Streams, _VP],
+    "ne_op_gemm_plain_i32": [_I32, _VP, _VP, _I64, _I64, _I64, Streams, _VP],
     "ne_gemm_prep_b": [_VP, _I64, _I64, _VP, _VP, _VP],
     "ne_op_gemm_limbs": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _VP],
     "ne_op_scale_add_check": [_PCFG, Streams, _I64, _I64, _VP, Streams, _I32, _I32, Streams, _VP, _VP, _VP],
@@ -339,6 +340,12 @@ def ne_op_gemm(cfg: Config, A, B: torch.Tensor, rows: int, cols: int, K: int, ou
     _call("ne_op_gemm", C.byref(cfg), _streams(A, torch.int64), _ptr(B, torch.int32), rows, cols, K, algo, L, limb_bits,
           LB, _streams(out, torch.int64), _ptr(ws), 0 if ws is None else ws.numel() * ws.element_size(),
           _ptr(diag, torch.int64), _stream())
+
+
+def ne_op_gemm_plain_i32(planes: torch.Tensor, Bt: torch.Tensor, rows: int, cols: int, K: int, out) -> None:
+    """Plain one-digit GEMM with int32 products (the narrowest native baseline)."""
+    _call("ne_op_gemm_plain_i32", len(out), _ptr(planes, torch.int8), _ptr(Bt, torch.int8), rows, cols, K,
+          _streams(out, torch.int32), _stream())
 
 
 def ne_gemm_plan_for(cfg: Config, a_bound: int, b_bound: int) -> GemmPlan:

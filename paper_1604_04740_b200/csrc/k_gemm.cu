@@ -240,6 +240,8 @@ __global__ void k_prep_b_planes_any(const int32_t* __restrict__ B, int64_t K, in
 
 ne_status launch_gemm_planes(int M, const int8_t* planes, int LA, const int32_t* a_shift, const int8_t* Bt, int LB,
                              int64_t rows, int64_t cols, int64_t K, const ne_streams& C, cudaStream_t s);
+ne_status launch_gemm_pair_i32(int M, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K,
+                               const ne_streams& C, cudaStream_t s);
 
 }  // namespace ne
 
@@ -355,6 +357,17 @@ extern "C" ne_status ne_op_gemm_plan(const ne_config* cfg, const int8_t* planes,
     if (!C.s[m] || !aligned16(C.s[m])) return NE_EINVAL;
   if (!tc_shape_ok(rows, cols, K)) return NE_ENOTSUP;
   return launch_gemm_planes(cfg->M, planes, plan->LA, plan->a_shift, Bt, plan->LB, rows, cols, K, C, cs(stream));
+}
+
+extern "C" ne_status ne_op_gemm_plain_i32(int32_t count, const int8_t* planes, const int8_t* Bt, int64_t rows,
+                                          int64_t cols, int64_t K, ne_streams32 C, ne_stream_t stream) {
+  if (count < 1 || count > 8 || !planes || !Bt || !aligned16(planes) || !aligned16(Bt)) return NE_EINVAL;
+  for (int m = 0; m < count; ++m)
+    if (!C.s[m] || !aligned16(C.s[m])) return NE_EINVAL;
+  if (!tc_shape_ok(rows, cols, K) || rows % 256 || cols % 256) return NE_ENOTSUP;
+  ne_streams Cs{};
+  for (int m = 0; m < count; ++m) Cs.s[m] = reinterpret_cast<int64_t*>(C.s[m]);
+  return launch_gemm_pair_i32(count, planes, Bt, rows, cols, K, Cs, cs(stream));
 }
 
 extern "C" ne_status ne_gemm_kernel_for(const ne_config* cfg, int32_t L, int32_t limb_bits, int64_t rows,

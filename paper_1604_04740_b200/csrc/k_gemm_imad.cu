@@ -78,7 +78,7 @@ k_gemm_imad64(const __grid_constant__ ne_cstreams A, const int32_t* __restrict__
 // global loads in registers while the current one is multiplied.  rows and
 // cols multiples of 128, K of 16 (else the IMAD64 kernel runs).  An A entry
 // outside int32 is a range violation (diag), its product undefined.
-constexpr int kWM = 128, kWN = 128, kWK = 16;
+constexpr int kWK = 16;
 
 __device__ __forceinline__ int64_t mad_wide(int32_t a, int32_t b, int64_t c) {
   int64_t d;
@@ -86,35 +86,39 @@ __device__ __forceinline__ int64_t mad_wide(int32_t a, int32_t b, int64_t c) {
   return d;
 }
 
+// TM x TN outputs per thread (two TM/2-row x two TN/2-column quadrants of the
+// CTA tile 16 TM x 16 TN), 256 threads
+template <int TM, int TN>
 __global__ void __launch_bounds__(256)
 k_gemm_imad32w(const __grid_constant__ ne_cstreams A, const int32_t* __restrict__ B,
                const __grid_constant__ ne_streams C, int64_t rows, int64_t cols, int64_t K,
                ne_diag* __restrict__ diag) {
-  __shared__ __align__(16) int32_t As[2][kWK][kWM];
-  __shared__ __align__(16) int32_t Bs[2][kWK][kWN];
+  constexpr int BMc = 16 * TM, BNc = 16 * TN, HM = TM / 2, HN = TN / 2;
+  __shared__ __align__(16) int32_t As[2][kWK][BMc];
+  __shared__ __align__(16) int32_t Bs[2][kWK][BNc];
   const int m = blockIdx.z;
-  const int64_t row0 = (int64_t)blockIdx.y * kWM, col0 = (int64_t)blockIdx.x * kWN;
+  const int64_t row0 = (int64_t)blockIdx.y * BMc, col0 = (int64_t)blockIdx.x * BNc;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int64_t* __restrict__ Am = A.s[m];
   int bad = 0;
   long long first = LLONG_MAX;
-  // global -> register staging: A 128 x 16 int64 (8 per thread), B 16 x 128 int32 (8 per thread)
-  // entry u of this thread: A row (tid / 16) + 16 u, k tid % 16; B k (tid / 128) + 2 u, col tid % 128
-  // (rows, cols multiples of 128 and K of 16: no bounds checks)
+  // A entry u (u < TM): row tid / 16 + 16 u, k tid % 16; B entry u (u < TN): k tid / BNc + (256 / BNc) u,
+  // col tid % BNc (rows, cols multiples of the tile and K of 16: no bounds checks)
   const int64_t* pa = Am + (row0 + (threadIdx.x >> 4)) * K + (threadIdx.x & 15);
-  const int32_t* pb = B + (int64_t)(threadIdx.x >> 7) * cols + col0 + (threadIdx.x & 127);
-  int32_t ra[8], rb[8];
+  const int32_t* pb = B + (int64_t)(threadIdx.x / BNc) * cols + col0 + (threadIdx.x % BNc);
+  int32_t ra[TM], rb[TN];
   auto load = [&](int64_t k0) {
     uint32_t badm = 0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < TM; ++u) {
       const int64_t x = __ldg(pa + 16 * u * K + k0);
       ra[u] = (int32_t)x;
       badm |= (uint32_t)(x != (int64_t)ra[u]) << u;
-      rb[u] = __ldg(pb + (k0 + 2 * u) * cols);
     }
+#pragma unroll
+    for (int u = 0; u < TN; ++u) rb[u] = __ldg(pb + (k0 + (256 / BNc) * u) * cols);
     if (badm) {  // an entry outside int32: range violation naming m * rows * K + row * K + k
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < TM; ++u)
         if (badm >> u & 1) {
           ++bad;
           const long long idx = ((long long)m * rows + row0 + (threadIdx.x >> 4) + 16 * u) * K + k0 + (threadIdx.x & 15);
@@ -124,17 +128,21 @@ k_gemm_imad32w(const __grid_constant__ ne_cstreams A, const int32_t* __restrict_
   };
   auto store = [&](int buf) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < TM; ++u) {
       const int t = threadIdx.x + 256 * u;
       As[buf][t & 15][t >> 4] = ra[u];
-      Bs[buf][t >> 7][t & 127] = rb[u];
+    }
+#pragma unroll
+    for (int u = 0; u < TN; ++u) {
+      const int t = threadIdx.x + 256 * u;
+      Bs[buf][t / BNc][t % BNc] = rb[u];
     }
   };
-  int64_t acc[8][8];
+  int64_t acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0;
   load(0);
   store(0);
   __syncthreads();
@@ -144,16 +152,21 @@ k_gemm_imad32w(const __grid_constant__ ne_cstreams A, const int32_t* __restrict_
     if (more) load(k0 + kWK);
 #pragma unroll
     for (int kk = 0; kk < kWK; ++kk) {
-      const int4 a0 = *reinterpret_cast<const int4*>(&As[buf][kk][ty * 4]);
-      const int4 a1 = *reinterpret_cast<const int4*>(&As[buf][kk][64 + ty * 4]);
-      const int4 b0 = *reinterpret_cast<const int4*>(&Bs[buf][kk][tx * 4]);
-      const int4 b1 = *reinterpret_cast<const int4*>(&Bs[buf][kk][64 + tx * 4]);
-      const int32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const int32_t b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      int32_t a[TM], b[TN];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < HM; ++i) {
+        a[i] = As[buf][kk][ty * HM + i];
+        a[HM + i] = As[buf][kk][BMc / 2 + ty * HM + i];
+      }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = mad_wide(a[i], b[j], acc[i][j]);
+      for (int j = 0; j < HN; ++j) {
+        b[j] = Bs[buf][kk][tx * HN + j];
+        b[HN + j] = Bs[buf][kk][BNc / 2 + tx * HN + j];
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = mad_wide(a[i], b[j], acc[i][j]);
     }
     if (more) {
       store(buf ^ 1);
@@ -163,22 +176,31 @@ k_gemm_imad32w(const __grid_constant__ ne_cstreams A, const int32_t* __restrict_
   }
   int64_t* __restrict__ Cm = C.s[m];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t gr = row0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+  for (int i = 0; i < TM; ++i) {
+    const int64_t gr = row0 + (i < HM ? ty * HM + i : BMc / 2 + ty * HM + i - HM);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t gc = col0 + h * 64 + tx * 4;
-      *reinterpret_cast<longlong2*>(Cm + gr * cols + gc) = make_longlong2(acc[i][4 * h], acc[i][4 * h + 1]);
-      *reinterpret_cast<longlong2*>(Cm + gr * cols + gc + 2) = make_longlong2(acc[i][4 * h + 2], acc[i][4 * h + 3]);
+      const int64_t gc = col0 + h * (BNc / 2) + tx * HN;
+#pragma unroll
+      for (int j = 0; j < HN; j += 2)
+        *reinterpret_cast<longlong2*>(Cm + gr * cols + gc + j) = make_longlong2(acc[i][h * HN + j], acc[i][h * HN + j + 1]);
     }
   }
   if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
 }
 
+#ifndef NE_IMAD_TM
+#define NE_IMAD_TM 8
+#endif
+#ifndef NE_IMAD_TN
+#define NE_IMAD_TN 8
+#endif
+constexpr int kWM = 16 * NE_IMAD_TM, kWN = 16 * NE_IMAD_TN;
+
 void launch_gemm_imad32w(int M, const ne_cstreams& A, const int32_t* B, const ne_streams& C, int64_t rows,
                          int64_t cols, int64_t K, ne_diag* diag, cudaStream_t s) {
-  dim3 grid((unsigned)((cols + kWN - 1) / kWN), (unsigned)((rows + kWM - 1) / kWM), (unsigned)M);
-  k_gemm_imad32w<<<grid, 256, 0, s>>>(A, B, C, rows, cols, K, diag);
+  dim3 grid((unsigned)(cols / kWN), (unsigned)(rows / kWM), (unsigned)M);
+  k_gemm_imad32w<NE_IMAD_TM, NE_IMAD_TN><<<grid, 256, 0, s>>>(A, B, C, rows, cols, K, diag);
 }
 
 void launch_gemm_imad64(int M, const ne_cstreams& A, const int32_t* B, const ne_streams& C, int64_t rows,

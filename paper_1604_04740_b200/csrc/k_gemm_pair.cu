@@ -17,12 +17,30 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "ne_internal.cuh"
 #include "tc_common.cuh"
 
 namespace ne {
 int gemm_max_clusters();  // ne_gemm_trace's grid cap (debug / tests), k_gemm_tc.cu
 namespace tc {
+
+// one epilogue box [32 rows x 16 int64] to C: a TMA store, or a TMA
+// reduce-add (u64 maps, wrap mod 2^64) when several K parts add into C
+__device__ __forceinline__ void store_box(const CUtensorMap* map, int64_t c0, int64_t r0, unsigned char* box,
+                                          bool add) {
+  if (add)
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"((int32_t)c0), "r"((int32_t)r0), "r"(smem_u32(box))
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"((int32_t)c0), "r"((int32_t)r0), "r"(smem_u32(box))
+                 : "memory");
+}
 
 template <int STAGES, int SW>
 struct CfgP {
@@ -81,11 +99,11 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
 // baselines, the ABFT data GEMM): one pass per tile, the two TMEM halves
 // double-buffer whole tiles (tile t accumulates in half t & 1), so the drain
 // of tile t overlaps the MMAs of tile t + 1.
-template <int L, int STAGES, int SW>
+template <int L, int STAGES, int SW, bool OUT32 = false>
 __global__ void __launch_bounds__(kThreadsPair, 1)
 k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
             const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
-            int raster, int64_t a_plane_rows, int toeplitz, int kcb) {
+            int raster, int64_t a_plane_rows, int toeplitz, int kcb, int64_t n_whole, int ksplit) {
   static_assert(L == 1 || L == 2, "one or two digit planes");
   using CF = CfgP<STAGES, SW>;
   constexpr int BK = CF::BK, BN = CF::BN;
@@ -103,8 +121,32 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
   const bool leader = crank == 0;
   const int KB = (int)(K / BK);
   const int64_t n_rt = rows / (2 * BM), n_ct = cols / BN;
-  const int64_t n_work = (int64_t)M * n_rt * n_ct;
+  // Work items: tiles 0 .. n_whole - 1 whole (stored); the remaining n_split
+  // tiles each in ksplit K parts, item n_whole + j = (part j / n_split, tile
+  // n_whole + j mod n_split), every part added into the zeroed C (TMA
+  // reduce-add, u64): split-K for grids that would leave SM pairs idle
+  // (n_whole = 0), or a split last wave (the tiles past the last full wave
+  // in two K halves, so the pairs finish within half a tile of each other)
+  const int64_t n_tiles = (int64_t)M * n_rt * n_ct;
+  const int64_t n_split = n_tiles - n_whole;
+  const int64_t n_work = n_whole + n_split * ksplit;
   const int64_t pid = blockIdx.x / 2, npair = gridDim.x / 2;
+  auto decode = [&](int64_t w, int& m, int64_t& rt, int64_t& ct, int& kb0, int& kb1, bool& add) {
+    int kp = 0;
+    int64_t t = w;
+    add = w >= n_whole;
+    if (add) {
+      kp = (int)((w - n_whole) / n_split);
+      t = n_whole + (w - n_whole) % n_split;
+    }
+    const int parts = add ? ksplit : 1;
+    m = (int)(t / (n_rt * n_ct));
+    const int64_t rem = t % (n_rt * n_ct);
+    rt = raster ? rem % n_rt : rem / n_ct;
+    ct = raster ? rem / n_rt : rem % n_ct;
+    kb0 = (int)((int64_t)kp * KB / parts);
+    kb1 = (int)((int64_t)(kp + 1) * KB / parts);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -133,17 +175,18 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
       uint32_t it = 0;
       for (int64_t w = pid; w < n_work; w += npair) {
-        const int m = (int)(w / (n_rt * n_ct));
-        const int64_t rem = w % (n_rt * n_ct);
-        const int64_t rt = raster ? rem % n_rt : rem / n_ct, ct = raster ? rem / n_rt : rem % n_ct;
+        int m, kb0, kb1;
+        int64_t rt, ct;
+        bool add;
+        decode(w, m, rt, ct, kb0, kb1, add);
         const int64_t row0 = rt * 2 * BM + crank * BM;
         const int64_t bcol0 = ct * BN + crank * (BN / 2);
         // K in chunks of kcb blocks, each chunk limb 1 then limb 0 (its B chunk is
         // still in L2 for the second pass); kcb = KB: one pass per limb
-        for (int c0 = 0; c0 < KB; c0 += kcb)
+        for (int c0 = kb0; c0 < kb1; c0 += kcb)
         for (int pass = 0; pass < L; ++pass) {
           const int li = L - 1 - pass;
-          for (int kb = c0; kb < KB && kb < c0 + kcb; ++kb, ++it) {
+          for (int kb = c0; kb < kb1 && kb < c0 + kcb; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
             unsigned char* st = smem + s * CF::kStage;
@@ -163,17 +206,21 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
       uint32_t it = 0, tile = 0;
       for (int64_t w = pid; w < n_work; w += npair, ++tile) {
-        for (int c0 = 0; c0 < KB; c0 += kcb)
+        int m, kb0, kb1;
+        int64_t rt, ct;
+        bool add;
+        decode(w, m, rt, ct, kb0, kb1, add);
+        for (int c0 = kb0; c0 < kb1; c0 += kcb)
         for (int pass = 0; pass < L; ++pass) {
           // L = 2: limb li into TMEM half li; L = 1: the tile into half tile & 1
           const int li = L == 2 ? 1 - pass : (int)(tile & 1);
           const int hb = L == 2 ? pass : li;                   // barrier pair of that half
           const uint32_t ph = L == 2 ? (tile & 1) : ((tile >> 1) & 1);
-          if (c0 == 0) {
+          if (c0 == kb0) {
             mbar_wait(&tmem_empty[hb], ph ^ 1);  // both CTAs freed this half
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           }
-          for (int kb = c0; kb < KB && kb < c0 + kcb; ++kb, ++it) {
+          for (int kb = c0; kb < kb1 && kb < c0 + kcb; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&full[s], (it / STAGES) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -182,10 +229,10 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
 #pragma unroll
             for (int ks = 0; ks < BK / UMMA_K; ++ks)
               mma_pair(tmem_base + li * BN, umma_desc<SW>(sa + ks * UMMA_K), umma_desc<SW>(sb + ks * UMMA_K), idesc,
-                       (kb | ks) != 0);
+                       (kb != kb0 || ks != 0) ? 1u : 0u);
             commit_pair(&empty[s]);
           }
-          if (c0 + kcb >= KB) commit_pair(&tmem_full[hb]);  // limb li (L = 1: the tile) complete
+          if (c0 + kcb >= kb1) commit_pair(&tmem_full[hb]);  // limb li (L = 1: the tile) complete
         }
       }
     }
@@ -198,13 +245,57 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
     constexpr int kNch = BN / 2 / 16;
     uint32_t tile = 0, buf = 0;
     for (int64_t w = pid; w < n_work; w += npair, ++tile) {
-      const int m = (int)(w / (n_rt * n_ct));
-      const int64_t rem = w % (n_rt * n_ct);
-      const int64_t rt = raster ? rem % n_rt : rem / n_ct, ct = raster ? rem / n_rt : rem % n_ct;
+      int m, kb0, kb1;
+      int64_t rt, ct;
+      bool add;
+      decode(w, m, rt, ct, kb0, kb1, add);
       const int64_t row0 = rt * 2 * BM + crank * BM;
       const int64_t col0 = ct * BN;
       const int cb = half * (BN / 2);
-      if constexpr (L == 1) {
+      if constexpr (L == 1 && OUT32) {
+        // plain int32 products (the narrowest native baseline): two 16-column TMEM
+        // chunks per [32 rows x 32 int32] box, 128B swizzle, TMA store (never split)
+        const int hb = (int)(tile & 1);
+        mbar_wait(&tmem_full[hb], (tile >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int ci = 0; ci < kNch; ci += 2) {
+          uint32_t va[16], vb[16];
+          tmem_ld16(tl + hb * BN + cb + 16 * ci, va);
+          tmem_ld16(tl + hb * BN + cb + 16 * (ci + 1), vb);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(va[j]), "+r"(vb[j]));
+          if (ci + 2 == kNch) {
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) arrive_leader(&tmem_empty[hb]);
+          }
+          if (lane == 0) {
+            if (CF::kOutBufs == 2)
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          __syncwarp();
+          unsigned char* box = my_out + buf * CF::kStageOut;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            *reinterpret_cast<uint4*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) =
+                make_uint4(va[4 * k], va[4 * k + 1], va[4 * k + 2], va[4 * k + 3]);
+            *reinterpret_cast<uint4*>(box + lane * 128 + (((k + 4) ^ (lane & 7)) * 16)) =
+                make_uint4(vb[4 * k], vb[4 * k + 1], vb[4 * k + 2], vb[4 * k + 3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            store_box(&outm.m[m], col0 + cb + 16 * ci, row0 + 32 * q, box, false);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          buf = (buf + 1) % CF::kOutBufs;
+        }
+        continue;
+      } else if constexpr (L == 1) {
         const int hb = (int)(tile & 1);
         mbar_wait(&tmem_full[hb], (tile >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -238,11 +329,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            asm volatile(
-                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                    reinterpret_cast<uint64_t>(&outm.m[m])),
-                "r"((int32_t)(col0 + cb + 16 * ci)), "r"((int32_t)(row0 + 32 * q)), "r"(smem_u32(box))
-                : "memory");
+            store_box(&outm.m[m], col0 + cb + 16 * ci, row0 + 32 * q, box, add);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
           buf = (buf + 1) % CF::kOutBufs;
@@ -295,11 +382,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          asm volatile(
-              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                  reinterpret_cast<uint64_t>(&outm.m[m])),
-              "r"((int32_t)(col0 + c)), "r"((int32_t)(row0 + 32 * q)), "r"(smem_u32(box))
-              : "memory");
+          store_box(&outm.m[m], col0 + c, row0 + 32 * q, box, add);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         buf = (buf + 1) % CF::kOutBufs;
@@ -319,7 +402,21 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
 // plain GEMM: a_plane_rows = out_rows = rows, toeplitz = 0; Toeplitz conv:
 // a_plane_rows = rows of the [plane_rows][W] plane view, toeplitz = W = cols
 // = 256, out_rows = output blocks (rows past it are clipped by the store)
-template <int L, int STAGES, int SW>
+// K parts of a grid that would leave SM pairs idle: the split (1..4) with the
+// best wave efficiency, kept only when it raises that efficiency by >= 15 %
+// and every part keeps >= 8 K blocks (each part pays a pipeline fill)
+static int pick_ksplit(int64_t n_tiles, int64_t npairs, int KB) {
+  auto eff = [&](int s) {
+    const int64_t items = n_tiles * s;
+    return (double)items / (double)(npairs * ((items + npairs - 1) / npairs));
+  };
+  int best = 1;
+  for (int sp = 2; sp <= 4; ++sp)
+    if (KB / sp >= 8 && eff(sp) > eff(best) * 1.15) best = sp;
+  return best;
+}
+
+template <int L, int STAGES, int SW, bool OUT32 = false>
 static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
                           int limb_bits, const ne_streams& C, cudaStream_t s, int64_t a_plane_rows = 0,
                           int toeplitz = 0, int64_t out_rows = 0) {
@@ -327,17 +424,9 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   if (rows % (2 * BM) != 0 || cols % CF::BN != 0 || K % CF::BK != 0 || M > 8) return NE_ENOTSUP;
   if (a_plane_rows == 0) a_plane_rows = rows;
   if (out_rows == 0) out_rows = rows;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, planes, toeplitz ? (uint64_t)toeplitz : (uint64_t)K, (uint64_t)M * L * a_plane_rows, SW, BM))
-    return NE_ECUDA;
-  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, CF::BN / 2)) return NE_ECUDA;
-  OutMaps om;
-  for (int m = 0; m < M; ++m)
-    if (!make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows)) return NE_ECUDA;
-  auto kern = k_gemm_pair<L, STAGES, SW>;
+  auto kern = k_gemm_pair<L, STAGES, SW, OUT32>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) != cudaSuccess)
     return NE_ECUDA;
-  const int64_t n_work = (int64_t)M * (rows / (2 * BM)) * (cols / CF::BN);
   cudaLaunchConfig_t lc = {};
   lc.blockDim = dim3(kThreadsPair);
   lc.dynamicSmemBytes = CF::kSmem;
@@ -349,6 +438,7 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   at[0].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
+  // persistent grid: one pair per two SMs, capped by how many pairs can be resident
   int64_t npairs = num_sms() / 2;
   lc.gridDim = dim3((unsigned)(npairs * 2));
   int active = 0;
@@ -357,16 +447,81 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   } else {
     cudaGetLastError();
   }
-  if (npairs > n_work) npairs = n_work;
   if (gemm_max_clusters() > 0 && npairs > gemm_max_clusters()) npairs = gemm_max_clusters();
+
+  // schedule: split-K for grids that would leave pairs idle, else a split last wave
+  const int64_t n_rt = rows / (2 * BM), n_ct = cols / CF::BN;
+  const int64_t n_tiles = (int64_t)M * n_rt * n_ct;
+  const int KBt = (int)(K / CF::BK);
+  int ksplit = (gemm_max_clusters() > 0 || OUT32) ? 1 : pick_ksplit(n_tiles, npairs, KBt);
+  int64_t n_whole = n_tiles;
+  if (ksplit > 1) {
+    n_whole = 0;
+  } else if (gemm_max_clusters() == 0 && !OUT32 && n_tiles > npairs && KBt >= 16) {
+    // the tiles past the last full wave, when they fill at most half of it,
+    // run as two K halves each (the pairs then finish within half a tile)
+    const int64_t tail = n_tiles % npairs;
+    if (tail > 0 && 2 * tail <= npairs) {
+      n_whole = n_tiles - tail;
+      ksplit = 2;
+    }
+  }
+#ifdef NE_PAIR_NO_SPLIT  // experiments (scripts/r02/ab.py): whole tiles only
+  ksplit = 1;
+  n_whole = n_tiles;
+#endif
+#ifdef NE_PAIR_NO_TAIL  // experiments: split-K for small grids, no split last wave
+  if (n_whole > 0) {
+    ksplit = 1;
+    n_whole = n_tiles;
+  }
+#endif
+  const bool adds = n_whole < n_tiles;
+  const int64_t n_work = n_whole + (n_tiles - n_whole) * ksplit;
+  if (npairs > n_work) npairs = n_work;
   lc.gridDim = dim3((unsigned)(npairs * 2));
   // B panel larger than ~1/3 of L2: row tiles fastest (consecutive pairs share a B panel)
   const int raster = !toeplitz && (uint64_t)cols * (uint64_t)K > (48ull << 20) ? 1 : 0;
+
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, planes, toeplitz ? (uint64_t)toeplitz : (uint64_t)K, (uint64_t)M * L * a_plane_rows, SW, BM))
+    return NE_ECUDA;
+  if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, CF::BN / 2)) return NE_ECUDA;
+  OutMaps om;
+  for (int m = 0; m < M; ++m) {
+    if (OUT32 ? !make_out_map32(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows)
+              : !make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows, adds))
+      return NE_ECUDA;
+    if (n_whole == 0 && cudaMemsetAsync(C.s[m], 0, (size_t)out_rows * cols * 8, s) != cudaSuccess) return NE_ECUDA;
+  }
+  if (adds && n_whole > 0) {
+    // zero the split tiles' output regions: runs of tiles sharing a row band
+    // (raster 0) or a column band (raster 1) are one 2-D memset each
+    int64_t t = n_whole;
+    while (t < n_tiles) {
+      const int m = (int)(t / (n_rt * n_ct));
+      const int64_t rem = t % (n_rt * n_ct);
+      const int64_t rt = raster ? rem % n_rt : rem / n_ct, ct = raster ? rem / n_rt : rem % n_ct;
+      int64_t run = 1;
+      while (t + run < n_tiles && (t + run) / (n_rt * n_ct) == m &&
+             (raster ? ((t + run) % (n_rt * n_ct)) / n_rt == ct : ((t + run) % (n_rt * n_ct)) / n_ct == rt))
+        ++run;
+      const int64_t r0 = rt * 2 * BM, c0 = ct * CF::BN;
+      if (r0 < out_rows) {
+        const int64_t h = raster ? (std::min)(run * 2 * BM, out_rows - r0) : (std::min)((int64_t)2 * BM, out_rows - r0);
+        const int64_t wcols = raster ? CF::BN : run * CF::BN;
+        if (cudaMemset2DAsync(C.s[m] + r0 * cols + c0, (size_t)cols * 8, 0, (size_t)wcols * 8, (size_t)h, s) !=
+            cudaSuccess)
+          return NE_ECUDA;
+      }
+      t += run;
+    }
+  }
   // whole-K passes up to K = 8192 (B chunks of one pass stay in L2 at these
   // sizes); 4096-deep chunks beyond
   const int kcb = (L == 1 || K <= 8192) ? (int)(K / CF::BK) : 4096 / CF::BK;
-  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz, kcb) !=
-      cudaSuccess)
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz, kcb,
+                         n_whole, ksplit) != cudaSuccess)
     return NE_ECUDA;
   return launch_status();
 }
@@ -379,6 +534,14 @@ ne_status launch_conv_pair(int M, int b, const int8_t* planes, int64_t plane_row
   if (b > 31 || Kpad % 128 != 0) return NE_ENOTSUP;
   const int64_t rows = (nblocks + 255) / 256 * 256;
   return tc::run_pair<2, 6, 128>(planes, Gt, rows, 256, Kpad, M, b, C, s, plane_rows, 256, nblocks);
+}
+
+// The plain (unentangled) one-digit GEMM with int32 products: the narrowest
+// native baseline of the overhead comparison.  C.s[m] point to int32 buffers.
+ne_status launch_gemm_pair_i32(int M, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K,
+                               const ne_streams& C, cudaStream_t s) {
+  if (K % 128 != 0) return NE_ENOTSUP;
+  return tc::run_pair<1, 6, 128, true>(planes, Bt, rows, cols, K, M, 8, C, s);
 }
 
 // 256 x 256 pair tiles: 2 limbs in limb-major passes, or 1 limb with

@@ -790,20 +790,25 @@ static ne_status run_plan(int M, int Lsub, const int8_t* planes, const int8_t* B
 // CTA-pair kernel).
 ne_status launch_gemm_planes(int M, const int8_t* planes, int LA, const int32_t* a_shift, const int8_t* Bt, int LB,
                              int64_t rows, int64_t cols, int64_t K, const ne_streams& C, cudaStream_t s) {
-  if (LA < 1 || LA > 8 || LB < 1 || LB > 4) return NE_EINVAL;
+  if (LA < 1 || LA > 8 || LB < 1 || LB > 5) return NE_EINVAL;
   bool uniform = LA <= 4 && LB == 1;
   const int b = LA > 1 ? a_shift[1] - a_shift[0] : 8;
   for (int i = 0; i < LA && uniform; ++i) uniform = a_shift[i] == b * i;
   if (uniform && b >= 8 && b <= 63) return launch_gemm_tc(M, LA, b, planes, Bt, rows, cols, K, C, s);
   bool first = true;
+  for (int i = 0; i < LA; ++i)
+    if (a_shift[i] < 0 || a_shift[i] > 63) return NE_EINVAL;
   for (int j = 0; j < LB; ++j)
     for (int g = 0; g < LA; g += 4) {
       tc::Plan pl{};
-      const int Lsub = LA - g < 4 ? LA - g : 4;
+      // products of bit weight >= 64 vanish mod 2^64 (the results wrap there):
+      // an accumulator group starting beyond that is skipped
+      if (a_shift[g] + 8 * j >= 64) continue;
+      int Lsub = LA - g < 4 ? LA - g : 4;
+      while (a_shift[g + Lsub - 1] + 8 * j >= 64) --Lsub;
       int mx = 0;
       for (int i = 0; i < Lsub; ++i) {
         pl.sh[i] = a_shift[g + i] + 8 * j;
-        if (pl.sh[i] < 0 || pl.sh[i] > 63) return NE_EINVAL;
         mx = pl.sh[i] > mx ? pl.sh[i] : mx;
       }
       pl.small = mx <= 30;

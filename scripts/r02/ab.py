@@ -1,0 +1,120 @@
+"""A/B timing of libne build variants on one box (experiments only).
+
+    python scripts/r02/ab.py --variant old:-DNE_CONV_ENTANGLE_OLD --variant new: --case conv_entangle
+
+Each variant is compiled (the _build flags + its -D flags) into
+/tmp/ne_ab/<name>/libne.so; each case is then timed in a fresh process per
+variant with CUDA events (median of reps), alternating variants 3 times."""
+import argparse
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+
+def build(name, flags):
+    import paper_1604_04740_b200._build as B
+
+    out = f"/tmp/ne_ab/{name}"
+    os.makedirs(out, exist_ok=True)
+    objs = []
+    procs = []
+    for src in sorted(glob.glob(os.path.join(B.CSRC, "*.cu"))):
+        obj = os.path.join(out, os.path.basename(src) + ".o")
+        procs.append(subprocess.Popen([B.NVCC, *B.ARCH, *B.FLAGS, *flags, "-c", src, "-o", obj]))
+        objs.append(obj)
+    assert all(p.wait() == 0 for p in procs)
+    lib = os.path.join(out, "libne.so")
+    subprocess.check_call([B.NVCC, *B.ARCH, "-shared", "-o", lib, *objs])
+    return lib
+
+
+CASES = {
+    "conv_entangle": """
+M, N, T = {M}, 10 ** 6, {T}
+cfg = ne.ne_config_for(M)
+L, b = ne.ne_gemm_limb_plan(cfg, 127)
+bw, kp, plen = ne.ne_conv_geometry(N, T, L)
+c = [torch.randint(-128, 128, (N,), dtype=torch.int32, device='cuda') for _ in range(M)]
+planes = torch.empty(M * L * plen, dtype=torch.int8, device='cuda')
+f = lambda: ne.ne_entangle_limbs_conv(cfg, c, T, 0, L, planes, None, b, bw)
+""",
+    "conv_gemm": """
+M, N, T = {M}, 10 ** 6, {T}
+cfg = ne.ne_config_for(M)
+L, b = ne.ne_gemm_limb_plan(cfg, 127)
+bw, kp, plen = ne.ne_conv_geometry(N, T, L)
+c = [torch.randint(-128, 128, (N,), dtype=torch.int32, device='cuda') for _ in range(M)]
+planes = torch.empty(M * L * plen, dtype=torch.int8, device='cuda')
+g = torch.randint(-128, 128, (T,), dtype=torch.int32, device='cuda')
+Gt = torch.empty(bw * kp, dtype=torch.int8, device='cuda')
+ne.ne_entangle_limbs_conv(cfg, c, T, 0, L, planes, None, b, bw)
+ne.ne_conv_prep_taps(g, 0, Gt, None, bw)
+out = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
+f = lambda: ne.ne_op_conv_limbs(cfg, planes, L, Gt, N, T, 0, out, b, bw)
+""",
+    "c3_gemm": """
+M, n = 3, 4096
+cfg = ne.ne_config_for(M)
+L, b = ne.ne_gemm_limb_plan(cfg, 64)
+A = [torch.randint(-64, 64, (n * n,), dtype=torch.int32, device='cuda') for _ in range(M)]
+planes = torch.empty(M * L * n * n, dtype=torch.int8, device='cuda')
+ne.ne_entangle_limbs(cfg, A, L, planes, None, b)
+Bt = torch.randint(-64, 64, (n * n,), dtype=torch.int8, device='cuda')
+out = [torch.empty(n * n, dtype=torch.int64, device='cuda') for _ in range(M)]
+f = lambda: ne.ne_op_gemm_limbs(cfg, planes, L, Bt, n, n, n, out, b)
+""",
+}
+
+TIMER = """
+import sys, statistics, torch
+sys.path.insert(0, {root!r})
+import paper_1604_04740_b200 as ne
+ne.LIB = {lib!r}
+ne.lib()
+{setup}
+for _ in range(5): f()
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    f()
+ts = []
+for _ in range({reps}):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+print(statistics.median(ts))
+"""
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--variant", action="append", required=True, help="name:flags (space separated)")
+    ap.add_argument("--case", required=True)
+    ap.add_argument("--M", type=int, default=8)
+    ap.add_argument("--T", type=int, default=4500)
+    ap.add_argument("--reps", type=int, default=50)
+    a = ap.parse_args()
+    libs = {}
+    for v in a.variant:
+        name, flags = v.split(":", 1)
+        libs[name] = build(name, flags.split())
+    setup = CASES[a.case].format(M=a.M, T=a.T)
+    res = {k: [] for k in libs}
+    for _ in range(3):
+        for name, lib in libs.items():
+            code = TIMER.format(root=ROOT, lib=lib, setup=setup, reps=a.reps)
+            r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+            if r.returncode:
+                print(name, "failed:", r.stderr[-2000:])
+                continue
+            res[name].append(float(r.stdout.strip().splitlines()[-1]))
+    for name, v in res.items():
+        print(f"{a.case} M={a.M} T={a.T} {name}: " + " ".join(f"{x * 1e3:.1f}" for x in v) + " us")
+
+
+if __name__ == "__main__":
+    main()

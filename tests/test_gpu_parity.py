@@ -543,6 +543,23 @@ def test_gemm_pair_multi_tile(O):
             assert (out[m].cpu().numpy().reshape(R, Cc) @ x == E[m] @ bx).all(), (cap, m)
 
 
+def test_gemm_plain_i32(O):
+    """The narrowest native baseline (plain one-digit GEMM, int32 products):
+    every entry equal to A_m B (numpy on the same seeded inputs, exact: |A B|
+    <= 1024 * 128 * 128 < 2^31), M = 3 streams of 256 x 512 at K = 1024."""
+    M, R, Cc, K = 3, 256, 512, 1024
+    A = gen(O, 84, 4, M, R * K, -128, 128)
+    B = O.gen_uniform(84, 5, 0, -128, 128, K * Cc)
+    planes = torch.empty(M * R * K, dtype=torch.int8, device="cuda")
+    ne.ne_to_limbs(to_streams(A), 1, planes)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    out = [torch.full((R * Cc,), 7, dtype=torch.int32, device="cuda") for _ in range(M)]
+    ne.ne_op_gemm_plain_i32(planes, Bt, R, Cc, K, out)
+    ref = O.op_gemm(O.config_for(3, 64), A.reshape(M, R, K), B.reshape(K, Cc)).reshape(M, -1)
+    assert (to_np(out) == ref).all()
+
+
 @pytest.mark.parametrize("cap", [0, 3])
 def test_gemm_pair_one_digit(O, cap):
     """One int8 digit (plain data: the overhead baselines, ABFT's data GEMM)
