@@ -258,91 +258,6 @@ k_conv_tail(const int8_t* __restrict__ planes, int M, int L, int b, int64_t plan
   }
 }
 
-// The two-digit plan (L = 2, b = l <= 31) with N % 4 == 0 and 16-B aligned
-// streams: every lane reads ONE aligned quad of each stream (a 128-bit load,
-// positions a .. a + 3 with a = p - p mod 4, p = (4 q - s0) mod N), forms its
-// two digit words, and the output quad t = 4q .. 4q + 3 (source positions
-// p .. p + 3, straddling this lane's and the next lane's quads when s0 mod 4
-// != 0) is cut from them with a funnel shift after one shuffle per word; lane
-// 31 digitises the following quad itself.  The range assertion sees the
-// same positions, counted once (t in [s0, s0 + N)), as k_entangle_conv_planes.
-template <int MT>
-__global__ void __launch_bounds__(kThreads)
-k_entangle_conv_pairq(const __grid_constant__ ne_cstreams32 c, int M_rt, int b, int64_t hi, int64_t n, int64_t s0,
-                      int64_t s0mod, int64_t plane_len, int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
-  const int M = MT > 0 ? MT : M_rt;
-  const int lane = threadIdx.x & 31;
-  const int r = (int)((4 - (s0mod & 3)) & 3);   // p mod 4, the same for every t = 4q
-  const int64_t nq = plane_len / 4;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  int bad = 0;
-  long long first = LLONG_MAX;
-  auto digits = [&](const int4 cur, const int4 prv, uint32_t& w0, uint32_t& w1, uint32_t& badm) {
-    const int32_t cc[4] = {cur.x, cur.y, cur.z, cur.w}, pp[4] = {prv.x, prv.y, prv.z, prv.w};
-    int32_t d0[4], d1[4];
-    badm = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      d0[u] = (int32_t)((uint32_t)cc[u] << (32 - b)) >> (32 - b);
-      d1[u] = pp[u] + (cc[u] >> b) + ((cc[u] >> (b - 1)) & 1);
-      const bool out = ((uint32_t)(d0[u] + 128) | (uint32_t)(d1[u] + 128)) > 255u ||
-                       (hi < INT32_MAX && (cc[u] > hi || cc[u] < -hi));
-      badm |= (uint32_t)out << u;
-    }
-    w0 = __byte_perm(__byte_perm(d0[0], d0[1], 0x0040), __byte_perm(d0[2], d0[3], 0x0040), 0x5410);
-    w1 = __byte_perm(__byte_perm(d1[0], d1[1], 0x0040), __byte_perm(d1[2], d1[3], 0x0040), 0x5410);
-  };
-  for (int64_t wq = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); wq * 32 < nq; wq += nwarps) {
-    const int64_t q = wq * 32 + lane;
-    int64_t p = 4 * q - s0mod;      // source position of t = 4q (mod n; t - s0mod < plane_len)
-    while (p < 0) p += n;
-    while (p >= n) p -= n;
-    int64_t a = p - r;              // this lane's aligned quad
-    if (a < 0) a += n;
-    int64_t an = a + 4;             // lane 31: the next quad, digitised here
-    if (an >= n) an -= n;
-    bool tin[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) tin[u] = 4 * q + u >= s0 && 4 * q + u < s0 + n && q < nq;
-    int4 prv = __ldg(reinterpret_cast<const int4*>(c.s[M - 1] + a));
-    int4 prvn = lane == 31 ? __ldg(reinterpret_cast<const int4*>(c.s[M - 1] + an)) : make_int4(0, 0, 0, 0);
-#pragma unroll 1
-    for (int m = 0; m < M; ++m) {
-      const int4 cur = __ldg(reinterpret_cast<const int4*>(c.s[m] + a));
-      uint32_t w0, w1, bm;
-      digits(cur, prv, w0, w1, bm);
-      uint32_t x0 = __shfl_down_sync(0xffffffffu, w0, 1);
-      uint32_t x1 = __shfl_down_sync(0xffffffffu, w1, 1);
-      uint32_t xb = __shfl_down_sync(0xffffffffu, bm, 1);
-      int4 curn = make_int4(0, 0, 0, 0);
-      if (lane == 31) {
-        curn = __ldg(reinterpret_cast<const int4*>(c.s[m] + an));
-        digits(curn, prvn, x0, x1, xb);
-        prvn = curn;
-      }
-      const uint32_t o0 = __funnelshift_r(w0, x0, 8 * r), o1 = __funnelshift_r(w1, x1, 8 * r);
-      const uint32_t ob = ((bm | (xb << 4)) >> r) & 0xfu;   // the four stored positions' violations
-      if (ob) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (((ob >> u) & 1) && tin[u]) {
-            ++bad;
-            int64_t pu = p + u;
-            if (pu >= n) pu -= n;
-            const long long idx = (long long)m * n + pu;
-            first = idx < first ? idx : first;
-          }
-      }
-      if (q < nq) {
-        __stcs(reinterpret_cast<unsigned int*>(planes + ((int64_t)m * 2) * plane_len + 4 * q), o0);
-        __stcs(reinterpret_cast<unsigned int*>(planes + ((int64_t)m * 2 + 1) * plane_len + 4 * q), o1);
-      }
-      prv = cur;
-    }
-  }
-  if (diag) diag_add(&diag->range_violations, &diag->first_bad, bad, first);
-}
-
 }  // namespace ne
 
 using namespace ne;
@@ -372,21 +287,6 @@ extern "C" ne_status ne_entangle_limbs_conv(const ne_config* cfg, ne_cstreams32 
   const int grid = grid_for(plen / 4, kThreads);
   cudaStream_t s = cs(stream);
   const int64_t hi = range_hi(cfg);
-  bool a16 = n_total % 4 == 0;
-  for (int m = 0; m < cfg->M; ++m) a16 &= aligned16(c.s[m]);
-#ifdef NE_CONV_ENTANGLE_OLD  // experiments (scripts/r02/ab.py): the per-position kernel only
-  a16 = false;
-#endif
-  if (L == 2 && limb_bits == cfg->l && limb_bits <= 31 && a16) {
-    const int gq = grid_for(plen / 4, kThreads);
-    switch (cfg->M) {
-      case 3: k_entangle_conv_pairq<3><<<gq, kThreads, 0, s>>>(c, 3, limb_bits, hi, n_total, s0, s0m, plen, planes, diag); break;
-      case 4: k_entangle_conv_pairq<4><<<gq, kThreads, 0, s>>>(c, 4, limb_bits, hi, n_total, s0, s0m, plen, planes, diag); break;
-      case 8: k_entangle_conv_pairq<8><<<gq, kThreads, 0, s>>>(c, 8, limb_bits, hi, n_total, s0, s0m, plen, planes, diag); break;
-      default: k_entangle_conv_pairq<0><<<gq, kThreads, 0, s>>>(c, cfg->M, limb_bits, hi, n_total, s0, s0m, plen, planes, diag); break;
-    }
-    return launch_status();
-  }
   switch (cfg->M) {
     case 3: k_entangle_conv_planes<3><<<grid, kThreads, 0, s>>>(c, 3, cfg->l, hi, n_total, s0, s0m, plen, L, limb_bits, planes, diag); break;
     case 4: k_entangle_conv_planes<4><<<grid, kThreads, 0, s>>>(c, 4, cfg->l, hi, n_total, s0, s0m, plen, L, limb_bits, planes, diag); break;

@@ -79,6 +79,10 @@ k_gemm_imad64(const __grid_constant__ ne_cstreams A, const int32_t* __restrict__
 // cols multiples of 128, K of 16 (else the IMAD64 kernel runs).  An A entry
 // outside int32 is a range violation (diag), its product undefined.
 constexpr int kWK = 16;
+#ifndef NE_IMAD_KUNROLL
+#define NE_IMAD_KUNROLL 16
+#endif
+constexpr int kKUnroll = NE_IMAD_KUNROLL;
 
 __device__ __forceinline__ int64_t mad_wide(int32_t a, int32_t b, int64_t c) {
   int64_t d;
@@ -150,7 +154,10 @@ k_gemm_imad32w(const __grid_constant__ ne_cstreams A, const int32_t* __restrict_
   for (int64_t k0 = 0; k0 < K; k0 += kWK) {
     const bool more = k0 + kWK < K;
     if (more) load(k0 + kWK);
-#pragma unroll
+    // (fully unrolled: ptxas pairs two products of one accumulator into
+    // IMAD.WIDE x 2 + a 3-input 64-bit add; one k per iteration keeps pure
+    // IMAD.WIDE chains but measured slower: 16.4 vs 19.0 MAC/clk/SM)
+#pragma unroll kKUnroll
     for (int kk = 0; kk < kWK; ++kk) {
       int32_t a[TM], b[TN];
 #pragma unroll

@@ -404,7 +404,9 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
 // = 256, out_rows = output blocks (rows past it are clipped by the store)
 // K parts of a grid that would leave SM pairs idle: the split (1..4) with the
 // best wave efficiency, kept only when it raises that efficiency by >= 15 %
-// and every part keeps >= 8 K blocks (each part pays a pipeline fill)
+// and every part keeps >= 16 K blocks (each part pays a pipeline fill and a
+// reduce-add of its tile: the C2P M = 3, T = 4500 conv measured 41.9 us whole
+// vs 47.5 us in 3 parts of 12-13 blocks, scripts/r02/ab.py)
 static int pick_ksplit(int64_t n_tiles, int64_t npairs, int KB) {
   auto eff = [&](int s) {
     const int64_t items = n_tiles * s;
@@ -412,7 +414,7 @@ static int pick_ksplit(int64_t n_tiles, int64_t npairs, int KB) {
   };
   int best = 1;
   for (int sp = 2; sp <= 4; ++sp)
-    if (KB / sp >= 8 && eff(sp) > eff(best) * 1.15) best = sp;
+    if (KB / sp >= 16 && eff(sp) > eff(best) * 1.15) best = sp;
   return best;
 }
 

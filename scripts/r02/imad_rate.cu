@@ -1,6 +1,8 @@
 // Issue rate of the integer multiply-adds on B200 CUDA cores: IMAD (32-bit),
-// IMAD.WIDE (32 x 32 + 64 -> 64), per SM per clock, with 16 independent
-// accumulator chains per thread (latency hidden), all SMs busy.
+// IMAD.WIDE (32 x 32 + 64 -> 64), per SM per clock, 16 independent
+// accumulator chains per thread.  The multiplier changes every iteration
+// (an xorshift on the ALU pipe) so the products cannot be hoisted out of the
+// loop (the first version of this benchmark let ptxas do exactly that).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o imad_rate imad_rate.cu
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -12,14 +14,18 @@ __global__ void __launch_bounds__(256) k_rate(int iters, int32_t a, int32_t b, i
   int32_t acc32[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) { acc[i] = threadIdx.x + i; acc32[i] = threadIdx.x + i; }
-  int32_t x = a + threadIdx.x, y = b ^ blockIdx.x;
+  uint32_t r = a + threadIdx.x * 2654435761u + blockIdx.x;
+  const int32_t y = b ^ blockIdx.x;
   for (int it = 0; it < iters; ++it) {
+    r ^= r << 13;
+    r ^= r >> 17;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
+      const int32_t x = (int32_t)(r + i);
       if (KIND == 0) {
-        asm volatile("mad.lo.s32 %0, %1, %2, %0;" : "+r"(acc32[i]) : "r"(x), "r"(y + i));
+        asm volatile("mad.lo.s32 %0, %1, %2, %0;" : "+r"(acc32[i]) : "r"(x), "r"(y));
       } else {
-        asm volatile("mad.wide.s32 %0, %1, %2, %0;" : "+l"(acc[i]) : "r"(x), "r"(y + i));
+        asm volatile("mad.wide.s32 %0, %1, %2, %0;" : "+l"(acc[i]) : "r"(x), "r"(y));
       }
     }
   }

@@ -14,8 +14,7 @@ a reset).  Instead (SURVEY §5's sanitizer line, done with our own checks):
 
 The kernels: k_gemm_pair (two digits, one digit, split-K), k_gemm_tc (L = 4,
 2; fused check; scatter; multi-launch plans with reduce-add), the entangle
-kernels (limbs, pair, split, stream, AoS, conv planes incl. the shuffle
-form), k_prep_b / k_prep_b_planes, k_disentangle / k_disentangle3x4 + bitmap,
+kernels (limbs, pair, split, stream, AoS, conv planes), k_prep_b / k_prep_b_planes, k_disentangle / k_disentangle3x4 + bitmap,
 recovery, k_pinner and k_pinner_stream, the direct and Toeplitz convs."""
 import numpy as np
 import pytest
