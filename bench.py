@@ -1637,8 +1637,12 @@ def run_ours(args, rank, world, local_rank):
         peak, runit = peaks["bf16_tflops"] * 2.0, "TOP/s"
         peak_note = f"int8 dense = 2 x bf16 burst ({peaks['bf16_tflops']} TFLOP/s, {peak_src}) x nominal 4.5/2.25"
     else:
-        peak, runit = 64 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, "TMAC/s"
-        peak_note = "IMAD pipe: 64 lanes/clk/SM x 148 SMs x max SM clock (DESIGN.md)"
+        # an exact MAC into a 64-bit accumulator is one IMAD.WIDE (32 x 32 + 64); IMAD.WIDE issues on
+        # the fmaheavy pipe at 32 lanes/clk/SM (ncu on the IMAD.WIDE GEMM: fmaheavy 60.4 % busy at
+        # 19.0 MAC/clk/SM; the 32-bit IMAD's 64 lanes/clk/SM is quoted in the note)
+        peak, runit = 32 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12, "TMAC/s"
+        peak_note = ("IMAD.WIDE pipe: 32 lanes/clk/SM x 148 SMs x max SM clock (profiles/r02_ncu_summary.md; "
+                     "32-bit IMAD: 64 lanes/clk/SM = 2x this)")
     tr = load_traffic().get(f"{W.name}:{dom}")
     traffic = tr["GB"] if tr else None
     xr = W.extra_roofline(dom, stage_ms[dom], peaks) if hasattr(W, "extra_roofline") else None
