@@ -1764,7 +1764,7 @@ def run_reference(args):
     if args.workload in ("c3", "c3p"):
         W.M, W.rows, W.cols, W.K, W.seed, W.algo, W.L, W.limb_bits, W.scheme = \
             3, 4096, 4096, 4096, 2, "tc", 2, 22, "entangled"
-        W.true_shape, W.fuse = None, False
+        W.true_shape, W.fuse, W.r0, W.rows_global = None, False, 0, 4096
         if args.workload == "c3p":
             W.M, W.true_shape = args.streams, (2000, 1200, args.kdim)
             W.rows, W.cols, W.K = 2048, 1280, -(-args.kdim // 128) * 128
@@ -1774,7 +1774,7 @@ def run_reference(args):
             l, k = 22, 20
         W.cfg = _Cfg
     elif args.workload == "c4":
-        W.M, W.n, W.B, W.seed, W.layout, W.w = 4, 1 << 28, 1024, 3, args.layout, args.w
+        W.M, W.n, W.B, W.seed, W.layout, W.w, W.b0 = 4, 1 << 28, 1024, 3, args.layout, args.w, 0
         W.vr = (1 << 12) if args.w == 64 else 64
 
         class _Cfg:
@@ -1802,6 +1802,7 @@ def run_reference(args):
     elif args.workload in ("c2", "c2p"):
         paper = args.workload == "c2p"
         W.M, W.n, W.T, W.seed = (args.streams, 10 ** 6, args.taps, 1) if paper else (3, 65536, 64, 1)
+        W.n_global, W.lo, W.halo = W.n, 0, 0
         W.algo, W.paper, W.name = args.conv or ("tc" if paper else "direct"), paper, "C2P" if paper else "C2"
         W.fuse = W.algo == "direct" and bool(args.fuse if args.fuse is not None else 1)
         W.scheme = args.scheme if W.algo == "tc" else "entangled"
@@ -1814,6 +1815,7 @@ def run_reference(args):
         W.cfg = _Cfg
     else:
         W.M, W.n, W.seed, W.w = 3, args.n or 4096, 0, args.w
+        W.n_global, W.lo = W.n, 0
         W.fuse = bool(args.fuse if args.fuse is not None else 1)
 
         class _Cfg:
