@@ -125,8 +125,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
   // tiles each in ksplit K parts, item n_whole + j = (part j / n_split, tile
   // n_whole + j mod n_split), every part added into the zeroed C (TMA
   // reduce-add, u64): split-K for grids that would leave SM pairs idle
-  // (n_whole = 0), or a split last wave (the tiles past the last full wave
-  // in two K halves, so the pairs finish within half a tile of each other)
+  // (n_whole = 0; the host uses no other split at present)
   const int64_t n_tiles = (int64_t)M * n_rt * n_ct;
   const int64_t n_split = n_tiles - n_whole;
   const int64_t n_work = n_whole + n_split * ksplit;
@@ -451,7 +450,9 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   }
   if (gemm_max_clusters() > 0 && npairs > gemm_max_clusters()) npairs = gemm_max_clusters();
 
-  // schedule: split-K for grids that would leave pairs idle, else a split last wave
+  // schedule: split-K for grids that would leave pairs idle (a split last wave
+  // — the tiles past the last full wave in two K halves — was measured: no
+  // gain on C3, 0.084 -> 0.092 ms on the paper's M = 8, N = 2000 GEMM; removed)
   const int64_t n_rt = rows / (2 * BM), n_ct = cols / CF::BN;
   const int64_t n_tiles = (int64_t)M * n_rt * n_ct;
   const int KBt = (int)(K / CF::BK);
@@ -459,24 +460,10 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   int64_t n_whole = n_tiles;
   if (ksplit > 1) {
     n_whole = 0;
-  } else if (gemm_max_clusters() == 0 && !OUT32 && n_tiles > npairs && KBt >= 16) {
-    // the tiles past the last full wave, when they fill at most half of it,
-    // run as two K halves each (the pairs then finish within half a tile)
-    const int64_t tail = n_tiles % npairs;
-    if (tail > 0 && 2 * tail <= npairs) {
-      n_whole = n_tiles - tail;
-      ksplit = 2;
-    }
   }
 #ifdef NE_PAIR_NO_SPLIT  // experiments (scripts/r02/ab.py): whole tiles only
   ksplit = 1;
   n_whole = n_tiles;
-#endif
-#ifdef NE_PAIR_NO_TAIL  // experiments: split-K for small grids, no split last wave
-  if (n_whole > 0) {
-    ksplit = 1;
-    n_whole = n_tiles;
-  }
 #endif
   const bool adds = n_whole < n_tiles;
   const int64_t n_work = n_whole + (n_tiles - n_whole) * ksplit;
@@ -495,29 +482,6 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
               : !make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows, adds))
       return NE_ECUDA;
     if (n_whole == 0 && cudaMemsetAsync(C.s[m], 0, (size_t)out_rows * cols * 8, s) != cudaSuccess) return NE_ECUDA;
-  }
-  if (adds && n_whole > 0) {
-    // zero the split tiles' output regions: runs of tiles sharing a row band
-    // (raster 0) or a column band (raster 1) are one 2-D memset each
-    int64_t t = n_whole;
-    while (t < n_tiles) {
-      const int m = (int)(t / (n_rt * n_ct));
-      const int64_t rem = t % (n_rt * n_ct);
-      const int64_t rt = raster ? rem % n_rt : rem / n_ct, ct = raster ? rem / n_rt : rem % n_ct;
-      int64_t run = 1;
-      while (t + run < n_tiles && (t + run) / (n_rt * n_ct) == m &&
-             (raster ? ((t + run) % (n_rt * n_ct)) / n_rt == ct : ((t + run) % (n_rt * n_ct)) / n_ct == rt))
-        ++run;
-      const int64_t r0 = rt * 2 * BM, c0 = ct * CF::BN;
-      if (r0 < out_rows) {
-        const int64_t h = raster ? (std::min)(run * 2 * BM, out_rows - r0) : (std::min)((int64_t)2 * BM, out_rows - r0);
-        const int64_t wcols = raster ? CF::BN : run * CF::BN;
-        if (cudaMemset2DAsync(C.s[m] + r0 * cols + c0, (size_t)cols * 8, 0, (size_t)wcols * 8, (size_t)h, s) !=
-            cudaSuccess)
-          return NE_ECUDA;
-      }
-      t += run;
-    }
   }
   // whole-K passes up to K = 8192 (B chunks of one pass stay in L2 at these
   // sizes); 4096-deep chunks beyond

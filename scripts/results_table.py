@@ -1,6 +1,10 @@
-"""Print DESIGN.md §10's results table from profiles/r01_bench_*.json."""
+"""Print DESIGN.md §10's results table from profiles/<round>_bench_*.json.
+
+    python scripts/results_table.py [r02]
+"""
 import json
 import os
+import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LINES = [
@@ -16,7 +20,9 @@ LINES = [
     ("c2p_8_1000", "C2P M = 8, T = 1000"), ("c2p_3_100", "C2P M = 3, T = 100"),
     ("c2p_direct", "C2P direct, M = 8, T = 4500"), ("c4", "C4"), ("c4_soa", "C4 `--layout soa`"), ("c4_w32", "C4 shape, `--w 32` (7-bit inputs)"),
     ("c5", "C5 (N = 1 emulation)"), ("c5_fused", "C5 `--exchange fused` (N = 1)"),
+    ("c3_imad64", "C3 `--algo imad64`"), ("c2p_3_1000", "C2P M = 3, T = 1000"),
 ]
+RND = sys.argv[1] if len(sys.argv) > 1 else "r01"
 
 
 def fmt(v):
@@ -29,10 +35,11 @@ def fmt(v):
     return f"{v:.3g}"
 
 
-print("| line | value | ms/step | dominant kernel (bound) | achieved | frac | e2e value (ms/step) | oracle (1 core) |")
-print("|---|---|---|---|---|---|---|---|")
+print("| line | value | ms/step | dominant kernel (bound) | achieved | frac | e2e value (ms/step) | oracle (1 core) "
+      "| oracle rows equal |")
+print("|---|---|---|---|---|---|---|---|---|")
 for key, name in LINES:
-    p = os.path.join(ROOT, "profiles", f"r01_bench_{key}.json")
+    p = os.path.join(ROOT, "profiles", f"{RND}_bench_{key}.json")
     if not os.path.exists(p):
         continue
     d = json.loads(open(p).read())
@@ -42,4 +49,4 @@ for key, name in LINES:
     e2e = f"{fmt(e.get('value'))} ({fmt(e.get('ms_per_step'))})" if e.get("value") else "—"
     print(f"| {name} | {fmt(d['value'])} {d['unit']} | {d['ms_per_step']:.4g} | {r.get('kernel', '—').split(' (')[0]} "
           f"({r.get('bound')}) | {fmt(r.get('achieved'))} {r.get('unit', '')} | {100 * r.get('frac', 0):.1f} % | {e2e} | "
-          f"{fmt(cb.get('value'))} |")
+          f"{fmt(cb.get('value'))} | {(d.get('correctness') or {}).get('oracle_rows_equal', '—')} |")
