@@ -45,21 +45,38 @@ k_scale_add_check(const __grid_constant__ ne_streams x, const __grid_constant__ 
         fb = pair ? (uint64_t)(int64_t)g[n0 + 1] : 0;
       }
       int64_t da[MT], db[MT], ra[MT], rb[MT];
+      if (pair) {
+        // all 2M loads in flight before any store (the stores into x may
+        // alias later streams' loads as far as the compiler knows)
+        longlong2 u[MT], w[MT];
+#ifndef NE_SAC_SERIAL  // (experiments, scripts/r02/ab.py: the round-1 load-store order per stream)
+#pragma unroll
+        for (int j = 0; j < MT; ++j) {
+          u[j] = __ldcs(reinterpret_cast<const longlong2*>(x.s[j] + n0));
+          w[j] = __ldcs(reinterpret_cast<const longlong2*>(a.s[j] + n0));
+        }
+#endif
+#pragma unroll
+        for (int j = 0; j < MT; ++j) {
+#ifdef NE_SAC_SERIAL
+          u[j] = __ldcs(reinterpret_cast<const longlong2*>(x.s[j] + n0));
+          w[j] = __ldcs(reinterpret_cast<const longlong2*>(a.s[j] + n0));
+#endif
+          da[j] = (int64_t)((uint64_t)u[j].x * fa + sg * (uint64_t)w[j].x);
+          db[j] = (int64_t)((uint64_t)u[j].y * fb + sg * (uint64_t)w[j].y);
+          __stcs(reinterpret_cast<longlong2*>(x.s[j] + n0), make_longlong2(da[j], db[j]));
+        }
+      } else {
 #pragma unroll
       for (int j = 0; j < MT; ++j) {
         int64_t* p = x.s[j] + n0;
         const int64_t* q = a.s[j] + n0;
-        if (pair) {
-          const longlong2 u = __ldcs(reinterpret_cast<const longlong2*>(p));
-          const longlong2 w = __ldcs(reinterpret_cast<const longlong2*>(q));
-          da[j] = (int64_t)((uint64_t)u.x * fa + sg * (uint64_t)w.x);
-          db[j] = (int64_t)((uint64_t)u.y * fb + sg * (uint64_t)w.y);
-          __stcs(reinterpret_cast<longlong2*>(p), make_longlong2(da[j], db[j]));
-        } else {
+        {
           da[j] = (int64_t)((uint64_t)p[0] * fa + sg * (uint64_t)q[0]);
           db[j] = 0;
           p[0] = da[j];
         }
+      }
       }
       f0 = disentangle_rot<MT>(da, MT, l, ra, true);
       f1 = disentangle_rot<MT>(db, MT, l, rb, true) && pair;

@@ -56,6 +56,16 @@ ne.ne_conv_prep_taps(g, 0, Gt, None, bw)
 out = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
 f = lambda: ne.ne_op_conv_limbs(cfg, planes, L, Gt, N, T, 0, out, b, bw)
 """,
+    "c1_sac": """
+M, n = 3, 1 << 27
+cfg = ne.ne_config_for(M)
+c = [torch.randint(-1024, 1024, (n,), dtype=torch.int32, device='cuda') for _ in range(2 * M)]
+eps = [torch.empty(n, dtype=torch.int64, device='cuda') for _ in range(2 * M)]
+ne.ne_entangle_sets(cfg, c, 2, eps)
+d = [torch.empty(n, dtype=torch.int64, device='cuda') for _ in range(M)]
+bm = torch.empty(n // 32, dtype=torch.int32, device='cuda')
+f = lambda: ne.ne_op_scale_add_check(cfg, eps[:M], 1, eps[M:], 0, d, bm)
+""",
     "c3_gemm": """
 M, n = 3, 4096
 cfg = ne.ne_config_for(M)
