@@ -1479,6 +1479,36 @@ def graph_stage_ms(W, nrot, reps, flush_l2):
     return {nm: sorted(v)[len(v) // 2] for nm, v in times.items()}
 
 
+def event_pair_overhead_ms(W, reps, flush_l2):
+    """What an event-record pair adds to a bracketed interval inside the step
+    graph: the same capture with an EMPTY pair (nothing between the two
+    events) after the first stage; median over replays.  Reported next to
+    stages_ms (which are not corrected by it)."""
+    import torch
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if flush_l2 else None
+    e0 = torch.cuda.Event(enable_timing=True, external=True)
+    e1 = torch.cuda.Event(enable_timing=True, external=True)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for jj, (_, f) in enumerate(W.stages(0)):
+            f()
+            if jj == 0:
+                e0.record()
+                e1.record()
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.fill_(1)
+        g.replay()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    del g
+    return sorted(ts)[len(ts) // 2]
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -1577,6 +1607,9 @@ def run_ours(args, rank, world, local_rank):
         # graphs, so the timed replays above carry no extra nodes); each replay
         # is synchronised and read, L2 flushed before it when the timed run did
         stage_ms = graph_stage_ms(W, getattr(W, "M", 1), max(3, min(args.steps, 10)), flush_l2)
+        ev_overhead = event_pair_overhead_ms(W, max(3, min(args.steps, 10)), flush_l2)
+    else:
+        ev_overhead = None
     if world > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -1682,6 +1715,7 @@ def run_ours(args, rank, world, local_rank):
                           "that stage per capture, median)"
                           if use_graph else "eager launches, CUDA events between stages"),
         "eager_stages_ms": {k: round(v, 4) for k, v in eager_stage_ms.items()},
+        "stages_event_pair_ms": None if ev_overhead is None else round(ev_overhead, 4),
         "launch": "CUDA graph replay (one graph per recovered stream r)" if use_graph else
                   ("eager (the step contains a collective)" if args.graph else "eager"),
         "eager_ms_per_step": round(eager_ms, 4),

@@ -66,6 +66,17 @@ d = [torch.empty(n, dtype=torch.int64, device='cuda') for _ in range(M)]
 bm = torch.empty(n // 32, dtype=torch.int32, device='cuda')
 f = lambda: ne.ne_op_scale_add_check(cfg, eps[:M], 1, eps[M:], 0, d, bm)
 """,
+    "c3_gemm_rank8": """
+M, n, R = 3, 4096, 512   # C3's row split at N = 8: 96 pair tiles (split-K 2 by the heuristic)
+cfg = ne.ne_config_for(M)
+L, b = ne.ne_gemm_limb_plan(cfg, 64)
+A = [torch.randint(-64, 64, (R * n,), dtype=torch.int32, device='cuda') for _ in range(M)]
+planes = torch.empty(M * L * R * n, dtype=torch.int8, device='cuda')
+ne.ne_entangle_limbs(cfg, A, L, planes, None, b)
+Bt = torch.randint(-64, 64, (n * n,), dtype=torch.int8, device='cuda')
+out = [torch.empty(R * n, dtype=torch.int64, device='cuda') for _ in range(M)]
+f = lambda: ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, n, n, out, b)
+""",
     "c3_gemm": """
 M, n = 3, 4096
 cfg = ne.ne_config_for(M)
