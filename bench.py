@@ -220,7 +220,7 @@ class C3Gemm(Workload):
     E2E_OUT = ("dout",)
 
     def __init__(self, rank, n=4096, seed=2, algo="tc", scheme="entangled", limbs="plan", fuse=True,
-                 paper_shape=None, world=1, scaling="strong"):
+                 paper_shape=None, world=1, scaling="strong", abound=64, bbound=64):
         import torch
         import paper_1604_04740_b200 as ne
         from paper_1604_04740_b200.dist import part_range
@@ -250,7 +250,17 @@ class C3Gemm(Workload):
                                    f"of {world}; B replicated (regenerated from the seed, untimed); no collective in "
                                    "the step, counters all-reduced after it")
         self.cfg = ne.ne_config_for(self.M)
-        if limbs == "base256":
+        # operand ranges: C3's U[-64, 64) by default; wider ranges (--abound / --bbound) take the
+        # general digit plan of ne_gemm_plan_for (split or base-256 planes of A, B in base-256 planes)
+        self.abound, self.bbound = abound, bbound
+        self.wide = (abound, bbound) != (64, 64) and algo == "tc" and scheme == "entangled"
+        self.LB = 1
+        if self.wide:
+            self.plan = ne.ne_gemm_plan_for(self.cfg, abound, bbound)
+            self.L, self.limb_bits, self.LB = self.plan.LA, self.plan.digit_bits, self.plan.LB
+            self.name = f"C3_a{abound}_b{bbound}"
+            fuse = False
+        elif limbs == "base256":
             self.L, self.limb_bits = ne.ne_gemm_limbs_for(self.cfg, 64), 8
         else:  # the cheapest exact plan: base 2^l, 2 limbs (|A| < 128)
             self.L, self.limb_bits = ne.ne_gemm_limb_plan(self.cfg, 64)
@@ -265,9 +275,9 @@ class C3Gemm(Workload):
         if self.true_shape is None:
             self.A = [torch.empty(R * K, dtype=torch.int32, device=dev) for _ in range(M)]
             for m in range(M):
-                ne.ne_gen_uniform_i32(self.seed, 4, m, -64, 64, self.A[m], self.r0 * K)
+                ne.ne_gen_uniform_i32(self.seed, 4, m, -abound, abound, self.A[m], self.r0 * K)
             self.B = torch.empty(K * Cc, dtype=torch.int32, device=dev)
-            ne.ne_gen_uniform_i32(self.seed, 5, 0, -64, 64, self.B)
+            ne.ne_gen_uniform_i32(self.seed, 5, 0, -bbound, bbound, self.B)
         else:
             Rt, Ct, Kt = self.true_shape
             self.A = [torch.zeros(R * K, dtype=torch.int32, device=dev) for _ in range(M)]
@@ -280,7 +290,7 @@ class C3Gemm(Workload):
             ne.ne_gen_uniform_i32(self.seed, 5, 0, -64, 64, t)
             self.B.view(K, Cc)[:Kt, :Ct] = t.view(Kt, Ct)
         self.planes = torch.empty(M * L * R * K, dtype=torch.int8, device=dev)
-        self.Bt = torch.empty(Cc * K, dtype=torch.int8, device=dev)
+        self.Bt = torch.empty(self.LB * Cc * K, dtype=torch.int8, device=dev)
         self.delta = [torch.empty(R * Cc, dtype=torch.int64, device=dev) for _ in range(M)]
         self.dout = [torch.empty(R * Cc, dtype=torch.int64, device=dev) for _ in range(M)]
         self.drec = [torch.empty(R * Cc, dtype=torch.int64, device=dev) for _ in range(M)]
@@ -327,6 +337,15 @@ class C3Gemm(Workload):
                 ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
                 ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
             ]
+        if self.wide:
+            return [
+                ("entangle", lambda: ne.ne_entangle_plan(cfg, self.A, self.plan, self.planes, self.diag)),
+                ("prep_b", lambda: ne.ne_gemm_prep_b_planes(self.B, self.K, self.cols, self.LB, self.Bt, self.diag)),
+                ("gemm", lambda: ne.ne_op_gemm_plan(cfg, self.planes, self.plan, self.Bt, self.rows, self.cols, self.K,
+                                                    self.delta)),
+                ("check", lambda: ne.ne_disentangle_check(cfg, self.delta, 0, self.dout, self.bitmap, self.diag)),
+                ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
+            ]
         if self.fuse:
             return [
                 ("entangle", lambda: ne.ne_entangle_limbs(cfg, self.A, self.L, self.planes, self.diag,
@@ -364,11 +383,11 @@ class C3Gemm(Workload):
                     "check": ("hbm", (M + 1) * n * 8 / 1e9, "GB"),
                     "recover": ("hbm", (M + 1) * n * 8 / 1e9, "GB")}
         Rt, Ct, Kt = self.true_shape or (R, Cc, K)  # useful work only (the zero padding is not counted)
-        gemm = ("tensor", 2 * L * M * Rt * Ct * Kt / 1e12, "TOP") if self.algo == "tc" else \
+        gemm = ("tensor", 2 * L * self.LB * M * Rt * Ct * Kt / 1e12, "TOP") if self.algo == "tc" else \
             ("alu", M * Rt * Ct * Kt / 1e12, "TMAC")
         return {
             "entangle": ("hbm", M * R * K * (4 + (L if self.algo == "tc" else 8)) / 1e9, "GB"),
-            "prep_b": ("hbm", K * Cc * 5 / 1e9, "GB"),
+            "prep_b": ("hbm", K * Cc * (4 + self.LB) / 1e9, "GB"),
             "gemm": gemm,
             "gemm_check": gemm,  # fused: the tensor work bounds it; + M*n*8 B of d_hat written under it
             "check": ("hbm", (M * n * 16 + n / 8) / 1e9, "GB"),
@@ -378,6 +397,11 @@ class C3Gemm(Workload):
     def config(self):
         wl = ("C3 (BASELINE configs[2]): M=3 entangled GEMM A_m 4096x4096 int32 U[-64,64), "
               "shared B 4096x4096 U[-64,64), K=4096, int64 results")
+        if self.wide:
+            p = self.plan
+            wl = (f"C3 shape with wider operands: M=3 entangled GEMM A_m 4096x4096 int32 U[-{self.abound},"
+                  f"{self.abound}), shared B U[-{self.bbound},{self.bbound}), K=4096, int64 results; digit plan "
+                  f"{'split' if p.kind else 'eps'} LA={p.LA} (bit weights {list(p.a_shift)[:p.LA]}) x LB={p.LB}")
         if self.true_shape is not None:
             Rt, Ct, Kt = self.true_shape
             wl = (f"C3P (the paper's GEMM shape, P:1119-1121): M={self.M} subblocks of {Rt}x{Kt} int32 "
@@ -407,7 +431,7 @@ class C3Gemm(Workload):
         int8 x int8 -> int32 GEMM on the same multiply-adds (torch._int_mm) as
         a library context number (int32 output, no int64 recombination)."""
         torch, ne = self.torch, self.ne
-        if self.algo != "tc" or self.scheme != "entangled":
+        if self.algo != "tc" or self.scheme != "entangled" or self.wide:
             return {}
         M, R, Cc, K, L = self.M, self.rows, self.cols, self.K, self.L
         cfg = self.cfg
@@ -475,9 +499,10 @@ class C3Gemm(Workload):
             _, Cc, K = self.true_shape
         rows = self.sample_rows(rows_sample)
         ocfg = O.config_for(M, 64)
-        A = np.stack([np.concatenate([O.gen_uniform(self.seed, 4, m, -64, 64, K, (self.r0 + int(r)) * K)
+        ab, bb = getattr(self, "abound", 64), getattr(self, "bbound", 64)
+        A = np.stack([np.concatenate([O.gen_uniform(self.seed, 4, m, -ab, ab, K, (self.r0 + int(r)) * K)
                                       for r in rows]) for m in range(M)])
-        B = O.gen_uniform(self.seed, 5, 0, -64, 64, K * Cc).reshape(K, Cc)
+        B = O.gen_uniform(self.seed, 5, 0, -bb, bb, K * Cc).reshape(K, Cc)
         t0 = time.perf_counter()
         E = O.entangle(ocfg, A)
         D = O.op_gemm(ocfg, E.reshape(M, len(rows), K), B).reshape(M, -1)
@@ -1159,7 +1184,8 @@ ORACLE_SAMPLE = {"c1": (200, 20), "c2": (20, 2), "c2p": (1, 1), "c3": (16, 2), "
 def make_workload(args, rank, world=1):
     kw = dict(world=world, scaling=args.scaling)
     if args.workload == "c3":
-        return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=bool(args.fuse or 0), **kw)
+        return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=bool(args.fuse or 0),
+                      abound=args.abound, bbound=args.bbound, **kw)
     if args.workload == "c3p":
         return C3Gemm(rank, algo=args.algo, scheme=args.scheme, limbs=args.limbs, fuse=bool(args.fuse or 0),
                       paper_shape=(args.streams, 2000, 1200, args.kdim), **kw)
@@ -1808,6 +1834,7 @@ def run_reference(args):
         W.M, W.rows, W.cols, W.K, W.seed, W.algo, W.L, W.limb_bits, W.scheme = \
             3, 4096, 4096, 4096, 2, "tc", 2, 22, "entangled"
         W.true_shape, W.fuse, W.r0, W.rows_global = None, False, 0, 4096
+        W.abound, W.bbound, W.wide, W.LB = args.abound, args.bbound, False, 1
         if args.workload == "c3p":
             W.M, W.true_shape = args.streams, (2000, 1200, args.kdim)
             W.rows, W.cols, W.K = 2048, 1280, -(-args.kdim // 128) * 128
@@ -1897,7 +1924,7 @@ CONFIG_SET = (
 )
 _SUB_DEFAULTS = dict(algo="tc", limbs="plan", scheme="entangled", fuse=None, conv=None, taps=4500, streams=8,
                      kdim=2000, w=64, layout="aos", n=None, failstop="simulated", exchange="auto", graph=1,
-                     scaling="strong")
+                     scaling="strong", abound=64, bbound=64)
 
 
 def compact(line):
@@ -1965,6 +1992,10 @@ def main():
     ap.add_argument("--taps", type=int, default=4500, help="c2p: kernel taps (paper: 100-4500)")
     ap.add_argument("--streams", type=int, default=8, help="c2p / c3p: M (paper: 3 or 8)")
     ap.add_argument("--kdim", type=int, default=2000, help="c3p: N, the inner dimension (paper: 200-2000)")
+    ap.add_argument("--abound", type=int, default=64,
+                    help="c3: A_m ~ U[-abound, abound) (default 64 = configs[2]); wider ranges run the general digit "
+                         "plan (ne_gemm_plan_for)")
+    ap.add_argument("--bbound", type=int, default=64, help="c3: B ~ U[-bbound, bbound)")
     ap.add_argument("--w", type=int, default=64, choices=[64, 32], help="c1 / c4: container width (P:528-530)")
     ap.add_argument("--layout", default="aos", choices=["aos", "soa"], help="c4: entangled layout at rest")
     ap.add_argument("--n", type=int, default=None, help="c1: stream length (default 4096 = configs[0])")

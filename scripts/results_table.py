@@ -21,6 +21,8 @@ LINES = [
     ("c2p_direct", "C2P direct, M = 8, T = 4500"), ("c4", "C4"), ("c4_soa", "C4 `--layout soa`"), ("c4_w32", "C4 shape, `--w 32` (7-bit inputs)"),
     ("c5", "C5 (N = 1 emulation)"), ("c5_fused", "C5 `--exchange fused` (N = 1)"),
     ("c3_imad64", "C3 `--algo imad64`"), ("c2p_3_1000", "C2P M = 3, T = 1000"),
+    ("c3_a1023", "C3 shape, A in U[-1023, 1023) (split plan, 4 planes)"),
+    ("c3_a32767_b255", "C3 shape, A in U[-2^15+1, 2^15-1), B in U[-255, 255) (5 x 2 planes)"),
 ]
 RND = sys.argv[1] if len(sys.argv) > 1 else "r01"
 
