@@ -401,22 +401,6 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
 // plain GEMM: a_plane_rows = out_rows = rows, toeplitz = 0; Toeplitz conv:
 // a_plane_rows = rows of the [plane_rows][W] plane view, toeplitz = W = cols
 // = 256, out_rows = output blocks (rows past it are clipped by the store)
-// K parts of a grid that would leave SM pairs idle: the split (1..4) with the
-// best wave efficiency, kept only when it raises that efficiency by >= 15 %
-// and every part keeps >= 16 K blocks (each part pays a pipeline fill and a
-// reduce-add of its tile: the C2P M = 3, T = 4500 conv measured 41.9 us whole
-// vs 47.5 us in 3 parts of 12-13 blocks, scripts/r02/ab.py)
-static int pick_ksplit(int64_t n_tiles, int64_t npairs, int KB) {
-  auto eff = [&](int s) {
-    const int64_t items = n_tiles * s;
-    return (double)items / (double)(npairs * ((items + npairs - 1) / npairs));
-  };
-  int best = 1;
-  for (int sp = 2; sp <= 4; ++sp)
-    if (KB / sp >= 16 && eff(sp) > eff(best) * 1.15) best = sp;
-  return best;
-}
-
 template <int L, int STAGES, int SW, bool OUT32 = false>
 static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols, int64_t K, int M,
                           int limb_bits, const ne_streams& C, cudaStream_t s, int64_t a_plane_rows = 0,
@@ -450,21 +434,23 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   }
   if (gemm_max_clusters() > 0 && npairs > gemm_max_clusters()) npairs = gemm_max_clusters();
 
-  // schedule: split-K for grids that would leave pairs idle (a split last wave
-  // — the tiles past the last full wave in two K halves — was measured: no
-  // gain on C3, 0.084 -> 0.092 ms on the paper's M = 8, N = 2000 GEMM; removed)
+  // schedule: whole tiles.  The kernel can also run tiles in K parts that
+  // reduce-add into a zeroed C (n_whole < n_tiles, ksplit > 1); every
+  // schedule of that kind was A/B-measured slower on one box
+  // (scripts/r02/ab.py): split-K of under-filled grids (C3's N = 8 row split,
+  // 96 pair tiles: 67.1 vs 55.1 us; the C2P M = 3, T = 4500 conv: 47.5 vs
+  // 41.9 us) and a split last wave (C3: 274.3 vs 274.4 us; the paper's M = 8,
+  // N = 2000 GEMM: 0.092 vs 0.084 ms) — every extra part re-drains an int64
+  // tile through the SM's store port.  NE_PAIR_KSPLIT=<s> (compile time)
+  // splits every tile, for experiments.
   const int64_t n_rt = rows / (2 * BM), n_ct = cols / CF::BN;
   const int64_t n_tiles = (int64_t)M * n_rt * n_ct;
-  const int KBt = (int)(K / CF::BK);
-  int ksplit = (gemm_max_clusters() > 0 || OUT32) ? 1 : pick_ksplit(n_tiles, npairs, KBt);
-  int64_t n_whole = n_tiles;
-  if (ksplit > 1) {
-    n_whole = 0;
-  }
-#ifdef NE_PAIR_NO_SPLIT  // experiments (scripts/r02/ab.py): whole tiles only
-  ksplit = 1;
-  n_whole = n_tiles;
+#ifdef NE_PAIR_KSPLIT
+  const int ksplit = OUT32 ? 1 : NE_PAIR_KSPLIT;
+#else
+  const int ksplit = 1;
 #endif
+  const int64_t n_whole = ksplit > 1 ? 0 : n_tiles;
   const bool adds = n_whole < n_tiles;
   const int64_t n_work = n_whole + (n_tiles - n_whole) * ksplit;
   if (npairs > n_work) npairs = n_work;

@@ -7,12 +7,12 @@ a reset).  Instead (SURVEY §5's sanitizer line, done with our own checks):
   the guards must be byte-identical (a write one element past either end of
   any output — planes, delta, d_hat, bitmaps, block sums — is caught);
 * races and ordering bugs in the mbarrier / TMA / TMEM pipelines, the
-  cross-CTA counters of the fused check, the reduce-add split-K and the
-  multi-launch digit plans: launches are repeated with different
+  cross-CTA counters of the fused check and the reduce-add multi-launch
+  digit plans: launches are repeated with different
   persistent-grid caps (different tile-to-SM schedules) and must give
   bit-identical outputs, each equal to the oracle.
 
-The kernels: k_gemm_pair (two digits, one digit, split-K), k_gemm_tc (L = 4,
+The kernels: k_gemm_pair (two digits, one digit), k_gemm_tc (L = 4,
 2; fused check; scatter; multi-launch plans with reduce-add), the entangle
 kernels (limbs, pair, split, stream, AoS, conv planes), k_prep_b / k_prep_b_planes, k_disentangle / k_disentangle3x4 + bitmap,
 recovery, k_pinner and k_pinner_stream, the direct and Toeplitz convs."""
@@ -63,7 +63,7 @@ def gen(O, seed, tag, M, N, lo, hi):
 
 
 @pytest.mark.parametrize("M,L,bound,R,Cc,K", [
-    (3, 2, 127, 256, 512, 4096),    # pair kernel, split-K (6 tiles)
+    (3, 2, 127, 256, 512, 4096),    # pair kernel, 6 tiles
     (3, 2, 127, 1024, 1024, 4096),  # pair kernel, 48 tiles
     (4, 1, 127, 1024, 1024, 1024),  # pair kernel, one digit
     (3, 4, 500, 256, 256, 256),     # single CTA, L = 4
