@@ -41,6 +41,12 @@ static int64_t conv_plane_len(int64_t n, int64_t taps, int W) {
 
 // a1 into circularly extended digit planes: 4 consecutive t per thread, all M
 // streams in order (each c_m[n] read once per t, used by streams m and m+1).
+// Three restructurings were A/B-measured slower or equal on one box (C2P,
+// N = 10^6, T = 4500, M = 8 / 3: 18.0 / 10.2 us here): one aligned 128-bit
+// load per lane with a funnel shift across lanes (22.2 / 12.4), every
+// stream's loads issued before any store (18.2 / 9.9), one thread per
+// (stream, quad) (20.5 / 11.3).  The kernel costs ~6 us fixed + ~1.5 us per
+// stream: a launch-latency-dominated pass of 6 MB per stream.
 // The range assertion (a0) counts every position once: t in [s0, s0 + N).
 template <int MT>
 __global__ void __launch_bounds__(kThreads)
