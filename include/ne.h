@@ -398,10 +398,11 @@ ne_status ne_op_gemm_limbs_scatter(const ne_config* cfg, const int8_t* planes_m,
 
 /* Which tcgen05 kernel ne_op_gemm_limbs / ne_op_gemm (TC) launches for this
  * shape and digit plan (host-only query, no GPU needed; the same gate the
- * launch uses): *kernel = NE_GEMM_KERNEL_PAIR for the CTA-pair limb-major
- * kernel (k_gemm_pair: L = 2, base 2^b with b <= 31, 4096 <= K <= 8192 or
- * K >= 2048 with >= 256 pair tiles, rows and cols multiples of 256, M <= 8),
- * else NE_GEMM_KERNEL_CTA (k_gemm_tc, single-CTA tiles).  The gemm trace hook
+ * launch uses): *kernel = NE_GEMM_KERNEL_PAIR for the CTA-pair kernel
+ * (k_gemm_pair; rows and cols multiples of 256, K of 128, M <= 8, b <= 31):
+ * L = 2 limb-major passes when 4096 <= K <= 8192, or K >= 2048 with >= 256
+ * pair tiles; L = 1 double-buffered tiles when K >= 1024 with >= 64 pair
+ * tiles), else NE_GEMM_KERNEL_CTA (k_gemm_tc, single-CTA tiles).  The gemm trace hook
  * (ne_gemm_trace), when on, forces the single-CTA kernel.  Errors as
  * ne_op_gemm_limbs (NE_ENOTSUP for shapes the tensor-core path refuses). */
 ne_status ne_gemm_kernel_for(const ne_config* cfg, int32_t L, int32_t limb_bits, int64_t rows, int64_t cols,
