@@ -738,7 +738,11 @@ bool gemm_pair_gate(int M, int L, int b, int64_t rows, int64_t cols, int64_t K) 
   // tiles, each SM receiving A + B/2 per MAC (the single-CTA L = 1 tile needs
   // A + B and is bound by the SM's inbound operand rate)
   if (L == 1) return K >= 1024 && pair_tiles >= 64;
-  return L == 2 && (K >= 4096 || (K >= 2048 && pair_tiles >= 256)) && K <= 8192;
+#ifndef NE_PAIR_KMIN   // experiments (scripts/r02/ab.py): the smallest K the two-digit pair kernel takes
+#define NE_PAIR_KMIN 2048
+#define NE_PAIR_TILES_SHORTK 256
+#endif
+  return L == 2 && (K >= 4096 || (K >= NE_PAIR_KMIN && pair_tiles >= NE_PAIR_TILES_SHORTK)) && K <= 8192;
 }
 
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
@@ -855,7 +859,10 @@ ne_status launch_conv_tc(int M, int L, int b, int W, const int8_t* planes, int64
   // blocks and two digits: the CTA-pair limb-major kernel (C2P M = 8, T = 4500:
   // conv 0.080 -> 0.072 ms); at T = 1000 it is neutral and at T = 300 slower
   // (pipeline fill per pass); longer kernels keep the single-CTA kernel
-  if (W == 256 && L == 2 && Kpad >= 2048 && Kpad <= 8192 && tc::g_trace == nullptr) {
+#ifndef NE_CONV_PAIR_KMIN  // experiments (scripts/r02/ab.py)
+#define NE_CONV_PAIR_KMIN 2048
+#endif
+  if (W == 256 && L == 2 && Kpad >= NE_CONV_PAIR_KMIN && Kpad <= 8192 && tc::g_trace == nullptr) {
     const ne_status st = launch_conv_pair(M, b, planes, plane_rows, Gt, Kpad, nblocks, C, s);
     if (st != NE_ENOTSUP) return st;
   }

@@ -77,6 +77,17 @@ Bt = torch.randint(-64, 64, (n * n,), dtype=torch.int8, device='cuda')
 out = [torch.empty(R * n, dtype=torch.int64, device='cuda') for _ in range(M)]
 f = lambda: ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, n, n, out, b)
 """,
+    "c3p_gemm": """
+M, R, Cc, K = {M}, 2048, 1280, {T}   # the paper's GEMM shape, padded (rows 2000 -> 2048, cols 1200 -> 1280)
+cfg = ne.ne_config_for(M)
+L, b = ne.ne_gemm_limb_plan(cfg, 64)
+A = [torch.randint(-64, 64, (R * K,), dtype=torch.int32, device='cuda') for _ in range(M)]
+planes = torch.empty(M * L * R * K, dtype=torch.int8, device='cuda')
+ne.ne_entangle_limbs(cfg, A, L, planes, None, b)
+Bt = torch.randint(-64, 64, (Cc * K,), dtype=torch.int8, device='cuda')
+out = [torch.empty(R * Cc, dtype=torch.int64, device='cuda') for _ in range(M)]
+f = lambda: ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, b)
+""",
     "c3_gemm": """
 M, n = 3, 4096
 cfg = ne.ne_config_for(M)

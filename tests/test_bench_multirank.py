@@ -49,6 +49,17 @@ def test_bench_two_ranks_partitioned(wl, extra):
     assert line["value"] > 0 and line["e2e"]["value"] > 0
 
 
+@pytest.mark.parametrize("wl", ["c2", "c3", "c4"])
+def test_bench_four_ranks_partitioned(wl):
+    """World 4: C2's halo ring over 4 ranks, C3's 1024-row bands, C4 with one
+    stream per rank (the SURVEY §8(e) placement at N = 4)."""
+    line = _bench(["--workload", wl, "--steps", "3", "--warmup", "3"], nproc=4, timeout=900)
+    assert line["n_gpus"] == 4 and line["scaling"] == "strong"
+    c = line["correctness"]
+    assert c["range_violations"] == 0 and c["flagged_positions"] == 0 and c["recover_equals_check"] is True
+    assert c["oracle_rows_equal"] is True
+
+
 def test_bench_two_ranks_c5_and_weak_replicas():
     line = _bench(["--workload", "c5", "--steps", "2", "--warmup", "3", "--exchange", "nccl"])
     assert line["n_gpus"] == 2 and line["correctness"]["flagged_positions"] == 0
