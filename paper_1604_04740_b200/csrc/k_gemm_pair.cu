@@ -22,6 +22,10 @@
 #include "ne_internal.cuh"
 #include "tc_common.cuh"
 
+#ifndef NE_PAIR_STAGES  // K stages of 32 KB (6: one output staging buffer per epilogue warp; 5: two)
+#define NE_PAIR_STAGES 6
+#endif
+
 namespace ne {
 int gemm_max_clusters();  // ne_gemm_trace's grid cap (debug / tests), k_gemm_tc.cu
 namespace tc {
@@ -501,8 +505,8 @@ ne_status launch_gemm_pair_i32(int M, const int8_t* planes, const int8_t* Bt, in
 ne_status launch_gemm_pair(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                            int64_t K, const ne_streams& C, cudaStream_t s) {
   if (K % 128 != 0 || b > 31) return NE_ENOTSUP;
-  if (L == 2) return tc::run_pair<2, 6, 128>(planes, Bt, rows, cols, K, M, b, C, s);
-  if (L == 1) return tc::run_pair<1, 6, 128>(planes, Bt, rows, cols, K, M, b, C, s);
+  if (L == 2) return tc::run_pair<2, NE_PAIR_STAGES, 128>(planes, Bt, rows, cols, K, M, b, C, s);
+  if (L == 1) return tc::run_pair<1, NE_PAIR_STAGES, 128>(planes, Bt, rows, cols, K, M, b, C, s);
   return NE_ENOTSUP;
 }
 

@@ -855,12 +855,12 @@ ne_status launch_conv_pair(int M, int b, const int8_t* planes, int64_t plane_row
 
 ne_status launch_conv_tc(int M, int L, int b, int W, const int8_t* planes, int64_t plane_rows, const int8_t* Gt,
                          int64_t Kpad, int64_t nblocks, const ne_streams& C, cudaStream_t s) {
-  // long kernels (2048 <= Kpad <= 8192, as the GEMM gate) with 256-output
-  // blocks and two digits: the CTA-pair limb-major kernel (C2P M = 8, T = 4500:
-  // conv 0.080 -> 0.072 ms); at T = 1000 it is neutral and at T = 300 slower
-  // (pipeline fill per pass); longer kernels keep the single-CTA kernel
-#ifndef NE_CONV_PAIR_KMIN  // experiments (scripts/r02/ab.py)
-#define NE_CONV_PAIR_KMIN 2048
+  // long kernels (1024 <= Kpad <= 8192) with 256-output blocks and two
+  // digits: the CTA-pair limb-major kernel (C2P M = 8, T = 4500: conv 0.080 ->
+  // 0.072 ms; T = 1000: 35.9 -> 35.0 us); at T = 300 slower (pipeline fill
+  // per pass); longer kernels keep the single-CTA kernel
+#ifndef NE_CONV_PAIR_KMIN  // (r02 A/B, C2P M = 8, T = 1000 at Kpad = 1280: pair 35.0 vs single-CTA 35.9 us)
+#define NE_CONV_PAIR_KMIN 1024
 #endif
   if (W == 256 && L == 2 && Kpad >= NE_CONV_PAIR_KMIN && Kpad <= 8192 && tc::g_trace == nullptr) {
     const ne_status st = launch_conv_pair(M, b, planes, plane_rows, Gt, Kpad, nblocks, C, s);
