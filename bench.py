@@ -299,6 +299,10 @@ class C3Gemm(Workload):
         if algo in ("imad", "imad64"):
             self.eps = [torch.empty(R * K, dtype=torch.int64, device=dev) for _ in range(M)]
         self.launches_per_step = 4 if self.fuse else 5
+        if self.wide:   # the plan's GEMM is one launch per (group of <= 4 A planes, B plane)
+            self.launches_per_step = 4 + -(-self.L // 4) * self.LB
+        if algo in ("imad", "imad64"):   # entangle, GEMM, check, recover
+            self.launches_per_step = 4
         self.counters = torch.zeros(ne.ne_gemm_check_workspace(R, Cc) // 4, dtype=torch.int32, device=dev)
         if scheme == "abft":
             # the paper's comparison method on the same kernels: plain data (1 int8
