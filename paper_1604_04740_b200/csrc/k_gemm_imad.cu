@@ -98,7 +98,11 @@ k_gemm_imad32w(const __grid_constant__ ne_cstreams A, const int32_t* __restrict_
                const __grid_constant__ ne_streams C, int64_t rows, int64_t cols, int64_t K,
                ne_diag* __restrict__ diag) {
   constexpr int BMc = 16 * TM, BNc = 16 * TN, HM = TM / 2, HN = TN / 2;
-  __shared__ __align__(16) int32_t As[2][kWK][BMc];
+  // A is stored transposed (k-major): a row pad of 4 int32 spreads a warp's
+  // 16 k-rows over 8 banks (2-way) instead of one (16-way: ncu counted 755 M
+  // shared-store bank conflicts per C3 launch), keeping 16-B aligned rows for
+  // the 128-bit reads
+  __shared__ __align__(16) int32_t As[2][kWK][BMc + 4];
   __shared__ __align__(16) int32_t Bs[2][kWK][BNc];
   const int m = blockIdx.z;
   const int64_t row0 = (int64_t)blockIdx.y * BMc, col0 = (int64_t)blockIdx.x * BNc;
