@@ -2,8 +2,8 @@
 """bench.py — the entangle -> LSB op -> disentangle + check -> recover hot path
 of arXiv 1604.04740 on B200, through libne.so's C ABI.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c1|c2|c4]
-                    [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c2p|c3|c3p|c4|c5]
+                    [--impl ours|reference] [--scaling strong|weak] [--configs 0|1]
 
 One "step" is one pass of every §8(a) stage of the chosen BASELINE.json config
 over one batch of synthetic (seeded, counter-generated) input that is already
@@ -12,11 +12,17 @@ disentangle + reliability check, a6 fail-stop recovery of stream (step mod M).
 Default workload = configs[2] (C3), the largest single-GPU configuration by
 work: the M = 3 entangled 4096^3 integer GEMM on tcgen05 int8 limbs.
 
-Rank 0 prints ONE JSON line (contract in the task statement).  Under torchrun
-(N > 1) every rank runs its own independent instance (weak scaling, no
-data-path collective); timing is max over ranks of CUDA-event time.
-``--impl reference`` times the CPU oracle (oracle/, plain C, 1 core) on a
-bounded sample of the same workload; only rank 0 runs it.
+Rank 0 prints ONE JSON line (contract in the task statement).  The default
+run (C3) also measures C1, C1 at 2^27, C2, C4 and C5 and reports them under
+"configs".  Under torchrun (N > 1) every config is partitioned over the ranks
+as SURVEY §8(e) specifies (``--scaling strong``, the default: C1 position
+ranges, C2 ranges + a halo exchange, C3 row ranges, C4 one stream per GPU +
+an all_gather, C5 one stream per rank) or replicated (``--scaling weak``);
+timing is the max over ranks of CUDA-event time, value = the whole job's work
+per step / that time.  Every line compares its timed outputs with the oracle
+at sampled positions (correctness.oracle_rows_equal).  ``--impl reference``
+times the CPU oracle (oracle/, plain C, 1 core) on a bounded sample of the
+same workload; only rank 0 runs it.
 """
 from __future__ import annotations
 
