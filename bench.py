@@ -1444,6 +1444,10 @@ def run_c5(args, rank, world, local_rank):
                                      "(profiles/traffic.json) x streams on the rank",
                      "peak_source": f"int8 dense = 2 x bf16 burst ({peak_src})"},
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        **({"exchange_algbw_GBs": round(len(mine) * plan.rows * plan.cols * 8 * (world - 1) / world / 1e9
+                                        / (stage_ms["exchange"] / 1e3), 1),
+            "exchange_bytes_per_rank": len(mine) * plan.rows * plan.cols * 8 * (world - 1) // world}
+           if "exchange" in stage_ms else {}),
         "e2e": {"value": round(2 * plan.M * plan.rows * plan.cols * plan.K / 1e9 / (e2e_ms / 1e3), 3),
                 "unit": "Gop/s", "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},

@@ -478,9 +478,11 @@ def c5_step(backend, plan: C5Plan, inp: dict, survivor_groups=None, verify: bool
         backend.mark("entangle_gemm")
         # position-major exchange over all ranks, then the reliability check (r = 0)
         sl = position_major_exchange(deltas, M, members, rank, group=None)
+        if world > 1:
+            backend.mark("exchange")   # the all_to_all alone (its algbw is reported)
     lo, _ = chunk_bounds(rows * cols, world)[rank]
     d_chk, flagged = backend.check([sl[m] for m in range(M)], 0)
-    backend.mark("exchange_check")
+    backend.mark("check" if (exchange != "fused" and world > 1) else "exchange_check")
     total_flags = int(_sum_u64(flagged, None))
     cks_check = _sum_u64(position_checksum(d_chk, lo), None) if verify else None
 
