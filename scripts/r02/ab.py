@@ -1,6 +1,8 @@
 """A/B timing of libne build variants on one box (experiments only).
 
     python scripts/r02/ab.py --variant old:-DNE_CONV_ENTANGLE_OLD --variant new: --case conv_entangle
+    python scripts/r02/ab.py --variant base@HEAD: --variant new: --case c3_gemm   # after
+        git archive HEAD paper_1604_04740_b200/csrc include gen | tar -x -C .ab_src/HEAD  (here, before gpurun)
 
 Each variant is compiled (the _build flags + its -D flags) into
 /tmp/ne_ab/<name>/libne.so; each case is then timed in a fresh process per
@@ -22,9 +24,13 @@ def build(name, flags):
     os.makedirs(out, exist_ok=True)
     objs = []
     procs = []
-    for src in sorted(glob.glob(os.path.join(B.CSRC, "*.cu"))):
+    csrc, inc = B.CSRC, []
+    if "@" in name:  # sources of another revision, exported under .ab_src/<rev>
+        tree = os.path.join(ROOT, ".ab_src", name.split("@", 1)[1])
+        csrc, inc = os.path.join(tree, "paper_1604_04740_b200", "csrc"), ["-I", os.path.join(tree, "include")]
+    for src in sorted(glob.glob(os.path.join(csrc, "*.cu"))):
         obj = os.path.join(out, os.path.basename(src) + ".o")
-        procs.append(subprocess.Popen([B.NVCC, *B.ARCH, *B.FLAGS, *flags, "-c", src, "-o", obj]))
+        procs.append(subprocess.Popen([B.NVCC, *B.ARCH, *inc, *B.FLAGS, *flags, "-c", src, "-o", obj]))
         objs.append(obj)
     assert all(p.wait() == 0 for p in procs)
     lib = os.path.join(out, "libne.so")
@@ -104,9 +110,13 @@ f = lambda: ne.ne_op_gemm_limbs(cfg, planes, L, Bt, n, n, n, out, b)
 TIMER = """
 import sys, statistics, torch
 sys.path.insert(0, {root!r})
+import ctypes
 import paper_1604_04740_b200 as ne
 ne.LIB = {lib!r}
+_L = ctypes.CDLL(ne.LIB)
+ne._SIGS = {{k: v for k, v in ne._SIGS.items() if hasattr(_L, k)}}  # an older build lacks newer calls
 ne.lib()
+{pre}
 {setup}
 for _ in range(5): f()
 torch.cuda.synchronize()
@@ -129,16 +139,23 @@ def main():
     ap.add_argument("--M", type=int, default=8)
     ap.add_argument("--T", type=int, default=4500)
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--pre", default="", help="python run after loading (e.g. ne.ne_gemm_pair_split(1))")
     a = ap.parse_args()
-    libs = {}
+    libs, pres, built = {}, {}, {}
     for v in a.variant:
         name, flags = v.split(":", 1)
-        libs[name] = build(name, flags.split())
+        toks = flags.split()
+        cflags = [t for t in toks if not t.startswith("py:")]
+        pres[name] = "\n".join(t[3:] for t in toks if t.startswith("py:"))  # e.g. py:ne.ne_gemm_pair_split(1)
+        key = (name.split("@", 1)[1] if "@" in name else "", tuple(cflags))
+        if key not in built:
+            built[key] = build(name, cflags)
+        libs[name] = built[key]
     setup = CASES[a.case].format(M=a.M, T=a.T)
     res = {k: [] for k in libs}
     for _ in range(3):
         for name, lib in libs.items():
-            code = TIMER.format(root=ROOT, lib=lib, setup=setup, reps=a.reps)
+            code = TIMER.format(root=ROOT, lib=lib, setup=setup, reps=a.reps, pre="\n".join(x for x in (a.pre if "@" not in name else "", pres[name]) if x))
             r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
             if r.returncode:
                 print(name, "failed:", r.stderr[-2000:])

@@ -1,0 +1,3 @@
+O=gpurun_out/r02v4; mkdir -p $O
+timeout 600 python scripts/r02/split_diag.py > $O/diag.txt 2>&1; echo rc=$?
+cat $O/diag.txt | tail -30
