@@ -419,28 +419,6 @@ ne_status ne_gemm_kernel_for(const ne_config* cfg, int32_t L, int32_t limb_bits,
  * turn it off.  Not thread-safe; NE_EINVAL if max_clusters < 0. */
 ne_status ne_gemm_trace(long long* buf, int32_t max_clusters);
 
-/* The CTA-pair kernel's schedule (two-digit plans; host-only, no GPU needed):
- * n_tiles 256 x 256 pair tiles (over all M streams) on npairs resident SM
- * pairs, K = 128 kblocks.  Either whole tiles (*n_whole = n_tiles, *ksplit =
- * 1) or *n_whole tiles in whole waves and every remaining tile in *ksplit K
- * parts: the first ksplit - 1 parts write int64 partial tiles to a
- * workspace the launch allocates on its own stream from the library's
- * stream-ordered memory pool (capturable; (ksplit - 1) x 512 KB per split
- * tile, freed stream-ordered after the kernel; the pool keeps its memory),
- * the last part adds them and stores C — the exact same int64 sums in
- * another order (wrap-free for certified results), so the split never
- * changes C.  Taken only when the round-robin makespan drops by > 3 % (the
- * last wave of C3's 768 tiles on 74 pairs; the paper's small shapes).
- * NE_EINVAL for null outputs, n_tiles < 0, npairs < 1 or kblocks < 1. */
-ne_status ne_gemm_pair_schedule(int64_t n_tiles, int64_t npairs, int32_t kblocks, int64_t* n_whole,
-                                int32_t* ksplit);
-
-/* Debug hook (tests): ksplit = 0 restores the automatic schedule above, 1
- * forces whole tiles, s >= 2 splits EVERY pair tile into min(s, kblocks) K
- * parts, for later CTA-pair launches in this process.  Not thread-safe;
- * NE_EINVAL outside 0..64. */
-ne_status ne_gemm_pair_split(int32_t ksplit);
-
 /* One stream of ne_op_gemm_limbs (the per-GPU GEMM of the one-stream-per-GPU
  * layout): C_m = sum_i 2^(8i) D_{m,i} B from planes_m (L planes). */
 ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t* planes_m, int32_t L,

@@ -18,9 +18,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <map>
-#include <mutex>
-#include <utility>
 
 #include "ne_internal.cuh"
 #include "tc_common.cuh"
@@ -47,27 +44,6 @@ __device__ __forceinline__ void store_box(const CUtensorMap* map, int64_t c0, in
                      reinterpret_cast<uint64_t>(map)),
                  "r"((int32_t)c0), "r"((int32_t)r0), "r"(smem_u32(box))
                  : "memory");
-}
-
-#ifdef NE_PAIR_TRACE  // experiments: per CTA and item t < 32, 8 timestamps (ne_dbg_pair_trace)
-__device__ long long g_pair_trace[160 * 32 * 8];
-__device__ __forceinline__ void ptrace(int t, int k, long long v) {
-  if (t < 32) g_pair_trace[(blockIdx.x * 32 + t) * 8 + k] = v;
-}
-__device__ __forceinline__ long long gtimer() {
-  long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define PTRACE(t, k, v) ptrace((int)(t), k, v)
-#else
-#define PTRACE(t, k, v)
-#endif
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
 }
 
 template <int STAGES, int SW>
@@ -127,14 +103,12 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
 // baselines, the ABFT data GEMM): one pass per tile, the two TMEM halves
 // double-buffer whole tiles (tile t accumulates in half t & 1), so the drain
 // of tile t overlaps the MMAs of tile t + 1.
-template <int L, int STAGES, int SW, bool OUT32 = false, bool SPLIT = false>
+template <int L, int STAGES, int SW, bool OUT32 = false>
 __global__ void __launch_bounds__(kThreadsPair, 1)
 k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
             const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
-            int raster, int64_t a_plane_rows, int toeplitz, int kcb, int64_t n_whole, int ksplit,
-            int64_t* __restrict__ ws, unsigned* __restrict__ cnt) {
+            int raster, int64_t a_plane_rows, int toeplitz, int kcb, int64_t n_whole, int ksplit) {
   static_assert(L == 1 || L == 2, "one or two digit planes");
-  static_assert(!SPLIT || (L == 2 && !OUT32), "split-K schedules: two-digit int64 tiles");
   using CF = CfgP<STAGES, SW>;
   constexpr int BK = CF::BK, BN = CF::BN;
   extern __shared__ unsigned char smem_raw[];
@@ -151,28 +125,24 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
   const bool leader = crank == 0;
   const int KB = (int)(K / BK);
   const int64_t n_rt = rows / (2 * BM), n_ct = cols / BN;
-  // Work items: tiles 0 .. n_whole - 1 whole; the remaining n_split tiles
-  // (L = 2 only) each in ksplit K parts, item n_whole + j = part j / n_split of
-  // split tile ts = j mod n_split (stream-K-like fix-up: parts 0 .. ksplit - 2
-  // write int64 partial tiles to the workspace ws[kp][ts][256][256] and count
-  // per epilogue warp in cnt[ts][2][8]; the last part waits for its warp's
-  // count, adds the partials and stores C).  Parts of a tile are ordered by w
-  // and every pair takes its items in increasing w, so a waiting part only
-  // waits on items already started (all pairs are resident): no deadlock.
+  // Work items: tiles 0 .. n_whole - 1 whole (stored); the remaining n_split
+  // tiles each in ksplit K parts, item n_whole + j = (part j / n_split, tile
+  // n_whole + j mod n_split), every part added into the zeroed C (TMA
+  // reduce-add, u64): split-K for grids that would leave SM pairs idle
+  // (n_whole = 0; the host uses no other split at present)
   const int64_t n_tiles = (int64_t)M * n_rt * n_ct;
   const int64_t n_split = n_tiles - n_whole;
   const int64_t n_work = n_whole + n_split * ksplit;
   const int64_t pid = blockIdx.x / 2, npair = gridDim.x / 2;
-  auto decode = [&](int64_t w, int& m, int64_t& rt, int64_t& ct, int& kb0, int& kb1, int& kp, int64_t& ts) {
-    kp = 0;
-    ts = -1;
+  auto decode = [&](int64_t w, int& m, int64_t& rt, int64_t& ct, int& kb0, int& kb1, bool& add) {
+    int kp = 0;
     int64_t t = w;
-    if (SPLIT && w >= n_whole) {
+    add = w >= n_whole;
+    if (add) {
       kp = (int)((w - n_whole) / n_split);
-      ts = (w - n_whole) % n_split;
-      t = n_whole + ts;
+      t = n_whole + (w - n_whole) % n_split;
     }
-    const int parts = ts >= 0 ? ksplit : 1;
+    const int parts = add ? ksplit : 1;
     m = (int)(t / (n_rt * n_ct));
     const int64_t rem = t % (n_rt * n_ct);
     rt = raster ? rem % n_rt : rem / n_ct;
@@ -208,9 +178,10 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
       uint32_t it = 0;
       for (int64_t w = pid; w < n_work; w += npair) {
-        int m, kb0, kb1, kp;
-        int64_t rt, ct, ts;
-        decode(w, m, rt, ct, kb0, kb1, kp, ts);
+        int m, kb0, kb1;
+        int64_t rt, ct;
+        bool add;
+        decode(w, m, rt, ct, kb0, kb1, add);
         const int64_t row0 = rt * 2 * BM + crank * BM;
         const int64_t bcol0 = ct * BN + crank * (BN / 2);
         // K in chunks of kcb blocks, each chunk limb 1 then limb 0 (its B chunk is
@@ -238,9 +209,10 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
       uint32_t it = 0, tile = 0;
       for (int64_t w = pid; w < n_work; w += npair, ++tile) {
-        int m, kb0, kb1, kp;
-        int64_t rt, ct, ts;
-        decode(w, m, rt, ct, kb0, kb1, kp, ts);
+        int m, kb0, kb1;
+        int64_t rt, ct;
+        bool add;
+        decode(w, m, rt, ct, kb0, kb1, add);
         for (int c0 = kb0; c0 < kb1; c0 += kcb)
         for (int pass = 0; pass < L; ++pass) {
           // L = 2: limb li into TMEM half li; L = 1: the tile into half tile & 1
@@ -250,7 +222,6 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
           if (c0 == kb0) {
             mbar_wait(&tmem_empty[hb], ph ^ 1);  // both CTAs freed this half
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            PTRACE(tile, 1 + pass, gtimer());
           }
           for (int kb = c0; kb < kb1 && kb < c0 + kcb; ++kb, ++it) {
             const int s = it % STAGES;
@@ -277,9 +248,10 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
     constexpr int kNch = BN / 2 / 16;
     uint32_t tile = 0, buf = 0;
     for (int64_t w = pid; w < n_work; w += npair, ++tile) {
-      int m, kb0, kb1, kp;
-      int64_t rt, ct, ts;
-      decode(w, m, rt, ct, kb0, kb1, kp, ts);
+      int m, kb0, kb1;
+      int64_t rt, ct;
+      bool add;
+      decode(w, m, rt, ct, kb0, kb1, add);
       const int64_t row0 = rt * 2 * BM + crank * BM;
       const int64_t col0 = ct * BN;
       const int cb = half * (BN / 2);
@@ -360,113 +332,11 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            store_box(&outm.m[m], col0 + cb + 16 * ci, row0 + 32 * q, box, false);
+            store_box(&outm.m[m], col0 + cb + 16 * ci, row0 + 32 * q, box, add);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
           buf = (buf + 1) % CF::kOutBufs;
         }
-        continue;
-      }
-      if (SPLIT && ts >= 0) {
-        // a K part of a split tile (the schedule's tail: both limbs are read
-        // from TMEM at the end, both halves released after the last chunk).
-        // The parts form a chain: part kp waits until part kp - 1 has
-        // written its running sum W_{kp-1} (this warp's box of it), adds it to
-        // its own values and writes W_kp to the workspace (om.m[8], rows
-        // [kp][ts][256]) — or, the last part, to C.  Own values go to the
-        // smem box lane = row (as every epilogue); the previous sum is read
-        // coalesced (4 rows x 128 B per warp load, one chunk ahead) and added
-        // in the box piece by piece.
-        const bool fin = kp == ksplit - 1;
-        unsigned* wcnt = cnt + ts * 16 + crank * 8 + ew;
-        const int64_t prow = crank * BM + 32 * q;   // this warp's first row in the pair tile
-        // W_{kp-1}: [32 rows][256 cols] int64 slab of this warp; lane reads row lane / 8 + 4 it, piece lane % 8
-        const int64_t* wprev =
-            kp > 0 ? ws + (((int64_t)(kp - 1) * n_split + ts) * 256 + prow + (lane >> 3)) * 256 + cb + 2 * (lane & 7)
-                   : nullptr;
-        mbar_wait(&tmem_full[0], tile & 1);
-        mbar_wait(&tmem_full[1], tile & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (ew == 0 && lane == 0) {
-          PTRACE(tile, 0, w);
-          PTRACE(tile, 3, gtimer());
-        }
-        longlong2 qn[8];
-        if (kp > 0) {
-          if (lane == 0) {
-            while (ld_acquire_u32(wcnt) < (unsigned)kp) __nanosleep(32);
-          }
-          __syncwarp();
-#pragma unroll
-          for (int it = 0; it < 8; ++it) qn[it] = __ldcg(reinterpret_cast<const longlong2*>(wprev + it * 4 * 256));
-        }
-        if (ew == 0 && lane == 0) PTRACE(tile, 4, gtimer());
-#pragma unroll 1
-        for (int ci = 0; ci < kNch; ++ci) {
-          const int c = cb + 16 * ci;
-          uint32_t v0[16], v1[16];
-          tmem_ld16(tl + BN + c, v1);
-          tmem_ld16(tl + c, v0);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(v0[j]), "+r"(v1[j]));
-          if (ci + 1 == kNch) {
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-              arrive_leader(&tmem_empty[0]);
-              arrive_leader(&tmem_empty[1]);
-            }
-          }
-          if (lane == 0) {
-            if (CF::kOutBufs == 2)
-              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            else
-              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-          }
-          __syncwarp();
-          unsigned char* box = my_out + buf * CF::kStageOut;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int64_t a0 = (int64_t)(int32_t)v0[2 * k] + ((int64_t)(int32_t)v1[2 * k] << limb_bits);
-            const int64_t a1 = (int64_t)(int32_t)v0[2 * k + 1] + ((int64_t)(int32_t)v1[2 * k + 1] << limb_bits);
-            *reinterpret_cast<longlong2*>(box + lane * 128 + ((k ^ (lane & 7)) * 16)) = make_longlong2(a0, a1);
-          }
-          if (kp > 0) {
-            __syncwarp();
-#pragma unroll
-            for (int it = 0; it < 8; ++it) {
-              const int r = it * 4 + (lane >> 3), k = lane & 7;
-              longlong2* pc = reinterpret_cast<longlong2*>(box + r * 128 + ((k ^ (r & 7)) * 16));
-              longlong2 v = *pc;
-              v.x += qn[it].x;
-              v.y += qn[it].y;
-              *pc = v;
-            }
-            if (ci + 1 < kNch)  // the next chunk's loads fly during this chunk's store
-#pragma unroll
-              for (int it = 0; it < 8; ++it)
-                qn[it] = __ldcg(reinterpret_cast<const longlong2*>(wprev + it * 4 * 256 + 16 * (ci + 1)));
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-            if (fin)
-              store_box(&outm.m[m], col0 + c, row0 + 32 * q, box, false);
-            else
-              store_box(&outm.m[8], c, ((int64_t)kp * n_split + ts) * 256 + prow, box, false);
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          }
-          buf = (buf + 1) % CF::kOutBufs;
-        }
-        if (!fin && lane == 0) {  // W_kp of this warp complete in global: release it to part kp + 1
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          __threadfence();
-          atomicAdd(wcnt, 1u);
-        }
-        if (ew == 0 && lane == 0) PTRACE(tile, 5, gtimer());
-        __syncwarp();
         continue;
       }
       mbar_wait(&tmem_full[0], tile & 1);
@@ -485,10 +355,6 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       if (lane == 0) arrive_leader(&tmem_empty[0]);
       mbar_wait(&tmem_full[1], tile & 1);  // limb 0 complete
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (ew == 0 && lane == 0) {
-        PTRACE(tile, 0, w);
-        PTRACE(tile, 3, gtimer());
-      }
 #pragma unroll
       for (int ci = 0; ci < kNch; ++ci) {
         const int c = cb + 16 * ci;
@@ -519,7 +385,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          store_box(&outm.m[m], col0 + c, row0 + 32 * q, box, false);
+          store_box(&outm.m[m], col0 + c, row0 + 32 * q, box, add);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         buf = (buf + 1) % CF::kOutBufs;
@@ -534,75 +400,6 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u));
   }
-}
-
-// Schedule of n_tiles pair tiles over np resident pairs (static round robin):
-// whole tiles only, or whole waves then the remaining tiles each in s K parts
-// with the workspace fix-up.  Makespan in whole-tile units: whole waves + the
-// rounds of parts, each 1/s of a tile plus an overhead f per part (pipeline
-// ramp, the partial tile's write and read: about 1.5 us against 0.77 us per
-// 128-deep K block of a two-pass tile, f = 2 / KB); the split is taken when it
-// saves more than 3 %.  g_split forces s (debug hook ne_gemm_pair_split: 1 =
-// whole tiles, s >= 2 = every tile in s parts).
-static int g_split = 0;
-
-void pair_schedule(int64_t n_tiles, int64_t np, int KB, int64_t* n_whole, int* ksplit) {
-  *n_whole = n_tiles;
-  *ksplit = 1;
-  if (np <= 0 || n_tiles <= 0) return;
-  if (g_split > 0) {
-    const int sf = std::min(g_split, std::max(KB, 1));
-    if (sf > 1) *n_whole = 0;
-    *ksplit = sf;
-    return;
-  }
-  const double f = 2.0 / std::max(KB, 1);
-  double best = (double)((n_tiles + np - 1) / np);
-  const double base = best;
-  for (int64_t k = n_tiles / np; k >= 0 && k >= n_tiles / np - 2; --k) {
-    const int64_t rest = n_tiles - k * np;
-    if (rest <= 0) continue;
-    for (int sp = 2; sp <= 8 && sp <= KB; ++sp) {
-      const double mk = (double)k + (double)((rest * sp + np - 1) / np) * (1.0 / sp + f);
-      if (mk < best * 0.99) {  // a larger split only for a clear gain
-        best = mk;
-        *n_whole = k * np;
-        *ksplit = sp;
-      }
-    }
-  }
-  if (best > 0.97 * base) {
-    *n_whole = n_tiles;
-    *ksplit = 1;
-  }
-}
-
-// the library's stream-ordered pool for split-K workspaces (one per device,
-// kept warm: release threshold = max), so a launch allocates its partial
-// tiles and counters on its own stream — also inside graph capture (memory
-// nodes) — and concurrent launches on other streams never share them
-static cudaMemPool_t split_pool() {
-  static std::mutex mu;
-  static std::map<int, cudaMemPool_t> pools;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = pools.find(dev);
-  if (it != pools.end()) return it->second;
-  cudaMemPoolProps pp = {};
-  pp.allocType = cudaMemAllocationTypePinned;
-  pp.location.type = cudaMemLocationTypeDevice;
-  pp.location.id = dev;
-  cudaMemPool_t pool = nullptr;
-  if (cudaMemPoolCreate(&pool, &pp) != cudaSuccess) {
-    cudaGetLastError();
-    pool = nullptr;
-  } else {
-    uint64_t keep = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
-  pools[dev] = pool;
-  return pool;
 }
 
 // plain GEMM: a_plane_rows = out_rows = rows, toeplitz = 0; Toeplitz conv:
@@ -641,19 +438,24 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   }
   if (gemm_max_clusters() > 0 && npairs > gemm_max_clusters()) npairs = gemm_max_clusters();
 
-  // schedule: whole tiles, or (L = 2) whole waves then the remaining tiles in
-  // K parts with the workspace fix-up (pair_schedule; the workspace and the
-  // counters are allocated per launch from the library's stream-ordered pool)
+  // schedule: whole tiles.  The kernel can also run tiles in K parts that
+  // reduce-add into a zeroed C (n_whole < n_tiles, ksplit > 1); every
+  // schedule of that kind was A/B-measured slower on one box
+  // (scripts/r02/ab.py): split-K of under-filled grids (C3's N = 8 row split,
+  // 96 pair tiles: 67.1 vs 55.1 us; the C2P M = 3, T = 4500 conv: 47.5 vs
+  // 41.9 us) and a split last wave (C3: 274.3 vs 274.4 us; the paper's M = 8,
+  // N = 2000 GEMM: 0.092 vs 0.084 ms) — every extra part re-drains an int64
+  // tile through the SM's store port.  NE_PAIR_KSPLIT=<s> (compile time)
+  // splits every tile, for experiments.
   const int64_t n_rt = rows / (2 * BM), n_ct = cols / CF::BN;
   const int64_t n_tiles = (int64_t)M * n_rt * n_ct;
-  int64_t n_whole = n_tiles;
-  int ksplit = 1;
-  if (L == 2 && !OUT32) pair_schedule(n_tiles, npairs, (int)(K / CF::BK), &n_whole, &ksplit);
-  cudaMemPool_t pool = ksplit > 1 ? split_pool() : nullptr;
-  if (!pool) {
-    n_whole = n_tiles;
-    ksplit = 1;
-  }
+#ifdef NE_PAIR_KSPLIT
+  const int ksplit = OUT32 ? 1 : NE_PAIR_KSPLIT;
+#else
+  const int ksplit = 1;
+#endif
+  const int64_t n_whole = ksplit > 1 ? 0 : n_tiles;
+  const bool adds = n_whole < n_tiles;
   const int64_t n_work = n_whole + (n_tiles - n_whole) * ksplit;
   if (npairs > n_work) npairs = n_work;
   lc.gridDim = dim3((unsigned)(npairs * 2));
@@ -667,43 +469,16 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   OutMaps om;
   for (int m = 0; m < M; ++m) {
     if (OUT32 ? !make_out_map32(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows)
-              : !make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows))
+              : !make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows, adds))
       return NE_ECUDA;
+    if (n_whole == 0 && cudaMemsetAsync(C.s[m], 0, (size_t)out_rows * cols * 8, s) != cudaSuccess) return NE_ECUDA;
   }
   // whole-K passes up to K = 8192 (B chunks of one pass stay in L2 at these
   // sizes); 4096-deep chunks beyond
   const int kcb = (L == 1 || K <= 8192) ? (int)(K / CF::BK) : 4096 / CF::BK;
-  cudaError_t e;
-  if constexpr (L == 2 && !OUT32) {
-    if (ksplit > 1) {
-      // partial tiles [ksplit - 1][n_split][256][256] int64, then the counters
-      const size_t n_split = (size_t)(n_tiles - n_whole);
-      const size_t wsb = (size_t)(ksplit - 1) * n_split * 256 * 256 * 8;
-      void* wsp = nullptr;
-      if (cudaMallocFromPoolAsync(&wsp, wsb + n_split * 16 * sizeof(unsigned), pool, s) != cudaSuccess)
-        return NE_ECUDA;
-      int64_t* ws = static_cast<int64_t*>(wsp);
-      unsigned* cnt = reinterpret_cast<unsigned*>(static_cast<char*>(wsp) + wsb);
-      if (!make_out_map(&om.m[8], ws, 256, (uint64_t)(ksplit - 1) * n_split * 256) ||
-          cudaMemsetAsync(cnt, 0, n_split * 16 * sizeof(unsigned), s) != cudaSuccess) {
-        cudaFreeAsync(wsp, s);
-        return NE_ECUDA;
-      }
-      auto ks = k_gemm_pair<L, STAGES, SW, false, true>;
-      if (cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem) != cudaSuccess)
-        return NE_ECUDA;
-      e = cudaLaunchKernelEx(&lc, ks, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz, kcb,
-                             n_whole, ksplit, ws, cnt);
-      if (cudaFreeAsync(wsp, s) != cudaSuccess && e == cudaSuccess) e = cudaErrorUnknown;
-    } else {
-      e = cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz,
-                             kcb, n_whole, ksplit, (int64_t*)nullptr, (unsigned*)nullptr);
-    }
-  } else {
-    e = cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz, kcb,
-                           n_whole, ksplit, (int64_t*)nullptr, (unsigned*)nullptr);
-  }
-  if (e != cudaSuccess) return NE_ECUDA;
+  if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz, kcb,
+                         n_whole, ksplit) != cudaSuccess)
+    return NE_ECUDA;
   return launch_status();
 }
 
@@ -723,22 +498,6 @@ ne_status launch_gemm_pair_i32(int M, const int8_t* planes, const int8_t* Bt, in
                                const ne_streams& C, cudaStream_t s) {
   if (K % 128 != 0) return NE_ENOTSUP;
   return tc::run_pair<1, 6, 128, true>(planes, Bt, rows, cols, K, M, 8, C, s);
-}
-
-void gemm_pair_split(int s) { tc::g_split = s; }
-
-#ifdef NE_PAIR_TRACE
-extern "C" int ne_dbg_pair_trace(long long* host, int reset) {
-  if (reset) {
-    static long long zero[160 * 32 * 8];
-    return cudaMemcpyToSymbol(tc::g_pair_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : 1;
-  }
-  return cudaMemcpyFromSymbol(host, tc::g_pair_trace, sizeof(long long) * 160 * 32 * 8) == cudaSuccess ? 0 : 1;
-}
-#endif
-
-void gemm_pair_schedule(int64_t n_tiles, int64_t npairs, int KB, int64_t* n_whole, int* ksplit) {
-  tc::pair_schedule(n_tiles, npairs, KB, n_whole, ksplit);
 }
 
 // 256 x 256 pair tiles: 2 limbs in limb-major passes, or 1 limb with

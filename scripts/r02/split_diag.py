@@ -1,4 +1,5 @@
-"""Split-K diagnostics (experiments): eager vs graph-replayed timing of the
+"""(Runs against commit d1b12b3, the split-K experiment: ne_gemm_pair_split / NE_PAIR_TRACE were reverted after it.)
+Split-K diagnostics (experiments): eager vs graph-replayed timing of the
 pair-kernel conv / GEMM under forced split factors."""
 import statistics
 import sys

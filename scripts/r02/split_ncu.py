@@ -1,4 +1,5 @@
-"""One C3-shape pair GEMM whole (split 1) then forced split 2, for an ncu capture (experiments)."""
+"""(Runs against commit d1b12b3, the split-K experiment: ne_gemm_pair_split / NE_PAIR_TRACE were reverted after it.)
+One C3-shape pair GEMM whole (split 1) then forced split 2, for an ncu capture (experiments)."""
 import sys
 
 import torch

@@ -1,4 +1,5 @@
-"""Per-item timeline of the CTA-pair kernel (experiments): builds libne with
+"""(Runs against commit d1b12b3, the split-K experiment: ne_gemm_pair_split / NE_PAIR_TRACE were reverted after it.)
+Per-item timeline of the CTA-pair kernel (experiments): builds libne with
 -DNE_PAIR_TRACE, runs one C3-shape GEMM under a given split setting and prints
 the last rounds' items (MMA pass starts, limb-0 complete, after the chain
 wait, epilogue end; microseconds from the first MMA start)."""

@@ -245,22 +245,3 @@ def test_empty_inputs_are_no_ops(L):
     }
     for name, args in calls.items():
         assert getattr(L, name)(*args) == 0, name
-
-
-def test_gemm_pair_auto_split_schedules(L):
-    """The automatic schedule splits exactly the shapes it should: C3's 768
-    tiles on 74 pairs (10 whole waves, the last 28 tiles in 2 parts), the
-    paper's conv M = 3, T = 4500 (48 tiles in 3 parts), the paper's GEMM
-    M = 8, N = 2000 (4 whole waves + 24 tiles in 3 parts); whole tiles when
-    the tiles fill the waves (148 tiles) or K is too short to pay."""
-    assert ne.ne_gemm_pair_schedule(768, 74, 32) == (740, 2)
-    assert ne.ne_gemm_pair_schedule(48, 74, 36) == (0, 3)
-    assert ne.ne_gemm_pair_schedule(320, 74, 16) == (296, 3)
-    assert ne.ne_gemm_pair_schedule(148, 74, 32) == (148, 1)
-    assert ne.ne_gemm_pair_schedule(128, 74, 8) == (128, 1)
-
-
-    with pytest.raises(ne.NeError):
-        ne.ne_gemm_pair_schedule(10, 0, 32)
-    with pytest.raises(ne.NeError):
-        ne.ne_gemm_pair_split(-1)

@@ -543,53 +543,6 @@ def test_gemm_pair_multi_tile(O):
             assert (out[m].cpu().numpy().reshape(R, Cc) @ x == E[m] @ bx).all(), (cap, m)
 
 
-@pytest.mark.parametrize("split,cap", [(2, 0), (3, 0), (7, 1), (3, 2), (32, 0)])
-def test_gemm_pair_split_k(O, split, cap):
-    """The pair kernel's split-K schedule (ne_gemm_pair_split forces every
-    pair tile into `split` K parts: the first parts write int64 partial tiles
-    to the workspace, the last waits for them and adds): with the full grid
-    and with the grid capped at 1-2 pairs (a pair then walks all parts of a
-    tile in order, the deadlock-freedom case), split = 32 = one 128-deep K
-    block per part.  Sampled rows in every 32-lane group vs the oracle, the
-    whole output by Freivalds, and bit-equal to the whole-tile schedule."""
-    M, R, Cc, K = 3, 512, 512, 4096
-    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
-    L, b = ne.ne_gemm_limb_plan(cfg, 127)
-    assert ne.ne_gemm_kernel_for(cfg, L, b, R, Cc, K) == "pair"
-    A = gen(O, 86, 4, M, R * K, -127, 128)
-    A[:, 0], A[:, -1] = 127, -127
-    B = O.gen_uniform(86, 5, 0, -128, 128, K * Cc)
-    planes = torch.empty(M * L * R * K, dtype=torch.int8, device="cuda")
-    ne.ne_entangle_limbs(cfg, to_streams(A), L, planes, limb_bits=b)
-    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
-    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
-    whole = empty_streams(M, R * Cc)
-    ne.ne_gemm_pair_split(1)
-    try:
-        ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, whole, limb_bits=b)
-        out = empty_streams(M, R * Cc)
-        ne.ne_gemm_pair_split(split)
-        ne.ne_gemm_trace(None, cap)
-        for _ in range(2):   # twice: the counters must be back at 0 after a launch
-            for o in out:
-                o.fill_(-1)
-            ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, limb_bits=b)
-            torch.cuda.synchronize()
-            assert all(torch.equal(o, w) for o, w in zip(out, whole))
-    finally:
-        ne.ne_gemm_trace(None, 0)
-        ne.ne_gemm_pair_split(0)
-    E = O.entangle(ocfg, A).reshape(M, R, K)
-    rows = _band_rows(R, 128, seed=split)
-    ref = O.op_gemm(ocfg, E[:, rows], B.reshape(K, Cc))
-    got = np.stack([out[m].view(R, Cc)[torch.from_numpy(rows).cuda()].cpu().numpy() for m in range(M)])
-    assert (got == ref).all()
-    x = np.random.default_rng(split).integers(-2, 2, size=Cc)   # |E (B x)| <= 2^30 2^12 2^7 2^10 < 2^62
-    bx = B.reshape(K, Cc) @ x
-    for m in range(M):
-        assert (out[m].cpu().numpy().reshape(R, Cc) @ x == E[m] @ bx).all(), m
-
-
 def test_gemm_plain_i32(O):
     """The narrowest native baseline (plain one-digit GEMM, int32 products):
     every entry equal to A_m B (numpy on the same seeded inputs, exact: |A B|
