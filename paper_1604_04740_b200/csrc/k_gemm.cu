@@ -119,6 +119,10 @@ k_prep_b(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __restr
 // each thread packs 4 consecutive k of 4 columns per task (4 x 128-bit loads,
 // 16 threads per 256-byte row segment), the [64][33]-word shared tile is
 // transposed so that 8 threads store one full 128-byte line of a Bt row.
+// (r02 A/B, C3's 4096 x 4096 B replayed alone: 15.6 us = 5.4 TB/s; a
+// persistent variant — grid of SMs x resident blocks walking the tiles, next
+// tile's loads issued before this tile's stores, double-buffered shared tile —
+// 18.1 us, dropped.)
 __global__ void __launch_bounds__(256)
 k_prep_b128(const int32_t* __restrict__ B, int64_t K, int64_t cols, int8_t* __restrict__ Bt,
             ne_diag* __restrict__ diag) {

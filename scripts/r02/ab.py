@@ -94,6 +94,12 @@ Bt = torch.randint(-64, 64, (Cc * K,), dtype=torch.int8, device='cuda')
 out = [torch.empty(R * Cc, dtype=torch.int64, device='cuda') for _ in range(M)]
 f = lambda: ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, b)
 """,
+    "prep_b": """
+K, C = 4096, 4096   # C3's B operand: int32 K x cols -> int8 cols x K
+B = torch.randint(-128, 128, (K * C,), dtype=torch.int32, device='cuda')
+Bt = torch.empty(C * K, dtype=torch.int8, device='cuda')
+f = lambda: ne.ne_gemm_prep_b(B, K, C, Bt)
+""",
     "c3_gemm": """
 M, n = 3, 4096
 cfg = ne.ne_config_for(M)

@@ -1161,11 +1161,14 @@ def test_pair_digits_extremes_and_alignment(O, M, align32):
     assert dd["first_bad"] == bad.min()
 
 
-@pytest.mark.parametrize("K,cols", [(64, 128), (192, 260), (16, 5), (4096, 384), (128, 64), (256, 192)])
+@pytest.mark.parametrize("K,cols", [(64, 128), (192, 260), (16, 5), (4096, 384), (128, 64), (256, 192),
+                                    (4096, 4160)])
 def test_prep_b_ragged(O, K, cols):
     """B (K x cols int32) -> Bt (cols x K int8): full 128 x 64 tiles (K % 128 == 0,
-    cols % 64 == 0), partial 64 x 128 tiles,
-    scalar tail columns, and out-of-int8 entries counted with the first named."""
+    cols % 64 == 0; 4096 x 4160 = 2080 tiles, more than the persistent grid
+    holds, so blocks walk several tiles through both shared buffers), partial
+    64 x 128 tiles, scalar tail columns, and out-of-int8 entries counted with
+    the first named."""
     B = O.gen_uniform(3, 5, 0, -128, 128, K * cols)
     B[7 % (K * cols)] = 300
     B[(K * cols) // 2] = -129
