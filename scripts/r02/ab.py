@@ -94,6 +94,17 @@ Bt = torch.randint(-64, 64, (Cc * K,), dtype=torch.int8, device='cuda')
 out = [torch.empty(R * Cc, dtype=torch.int64, device='cuda') for _ in range(M)]
 f = lambda: ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, out, b)
 """,
+    "c2_conv_check": """
+M, N, T = {M}, 65536, {T}   # C2: 3 x 65536 outputs, 64 taps (--M 3 --T 64)
+cfg = ne.ne_config_for(M)
+c = [torch.randint(-128, 128, (N,), dtype=torch.int32, device='cuda') for _ in range(M)]
+eps = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
+ne.ne_entangle(cfg, c, eps)
+taps = torch.randint(-128, 128, (T,), dtype=torch.int32, device='cuda')
+out = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
+d = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
+f = lambda: ne.ne_op_conv_check(cfg, eps, taps, out, 0, d)
+""",
     "prep_b": """
 K, C = 4096, 4096   # C3's B operand: int32 K x cols -> int8 cols x K
 B = torch.randint(-128, 128, (K * C,), dtype=torch.int32, device='cuda')
@@ -130,7 +141,10 @@ g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g):
     f()
 ts = []
+flush = torch.empty(1 << 29, dtype=torch.uint8, device='cuda') if {flush} else None
 for _ in range({reps}):
+    if flush is not None:
+        flush.fill_(1)   # 512 MB: L2 cold for the replay (outside the events)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
@@ -145,6 +159,7 @@ def main():
     ap.add_argument("--M", type=int, default=8)
     ap.add_argument("--T", type=int, default=4500)
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--flush", action="store_true", help="flush L2 (512 MB write) before every replay")
     ap.add_argument("--pre", default="", help="python run after loading (e.g. ne.ne_gemm_pair_split(1))")
     a = ap.parse_args()
     libs, pres, built = {}, {}, {}
@@ -161,7 +176,7 @@ def main():
     res = {k: [] for k in libs}
     for _ in range(3):
         for name, lib in libs.items():
-            code = TIMER.format(root=ROOT, lib=lib, setup=setup, reps=a.reps, pre="\n".join(x for x in (a.pre if "@" not in name else "", pres[name]) if x))
+            code = TIMER.format(root=ROOT, lib=lib, setup=setup, reps=a.reps, flush=a.flush, pre="\n".join(x for x in (a.pre if "@" not in name else "", pres[name]) if x))
             r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
             if r.returncode:
                 print(name, "failed:", r.stderr[-2000:])

@@ -1344,11 +1344,15 @@ def test_scale_add_check_fused(O, M, N, r):
             assert d["first_fault"] == N // 3
 
 
-@pytest.mark.parametrize("M,N,T,correlate,r", [(3, 65536, 64, 0, 0), (3, 1000, 64, 1, 1), (4, 777, 1, 0, 2),
-                                               (8, 5000, 300, 1, 7), (3, 50, 300, 0, 0), (5, 2000, 64, 0, 4)])
-def test_conv_check_fused(O, M, N, T, correlate, r):
+@pytest.mark.parametrize("M,N,T,correlate,r,bit", [
+    (3, 65536, 64, 0, 0, 7), (3, 1000, 64, 1, 1, 7), (4, 777, 1, 0, 2, 7), (8, 5000, 300, 1, 7, 7),
+    (3, 50, 300, 0, 0, 7), (5, 2000, 64, 0, 4, 7), (3, 4096, 65, 0, 0, 40), (8, 3000, 257, 0, 3, 45),
+    (3, 200000, 64, 0, 1, 7), (4, 160000, 33, 1, 0, 40)])
+def test_conv_check_fused(O, M, N, T, correlate, r, bit):
     """ne_op_conv_check == oracle circular conv + disentangle/check, clean and
-    with a corrupted stored eps word (flags exactly where the oracle's are)."""
+    with a corrupted stored eps word (flags exactly where the oracle's are);
+    bit 40/45 puts a window value outside int32, so the 64-bit MAC path runs;
+    odd T, T > 256 (several tap chunks), N up to 200 000."""
     cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
     c = gen(O, 14, 1, M, N, -128, 128)
     g = O.gen_uniform(14, 3, 0, -128, 128, T)
@@ -1356,7 +1360,7 @@ def test_conv_check_fused(O, M, N, T, correlate, r):
     for corrupt in (False, True):
         Ec = E.copy()
         if corrupt:
-            Ec[(r + 2) % M, N // 2] ^= 1 << 7
+            Ec[(r + 2) % M, N // 2] ^= 1 << bit
         D = O.op_conv(ocfg, Ec, g, bool(correlate))
         ref, flags, nf = O.disentangle_check(ocfg, D, r)
         out, d_out = empty_streams(M, N), empty_streams(M, N)
