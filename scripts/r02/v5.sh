@@ -1,3 +1,4 @@
+# r02v5: split-K diagnostics after the chained fix-up + pair/conv parity (commit d1b12b3)
 O=gpurun_out/r02v5; mkdir -p $O
 timeout 600 python scripts/r02/split_diag.py > $O/diag.txt 2>&1; echo rc=$?
 cat $O/diag.txt | tail -30

@@ -1,3 +1,4 @@
+# r02x2: conv_check A/B (one thread per output vs stream-split), warm and flushed L2
 O=gpurun_out/r02x2; mkdir -p $O
 for fl in "" "--flush"; do
 for mt in "3 64" "8 64" "3 1000"; do set -- $mt
