@@ -1310,6 +1310,57 @@ def c5_traffic(streams):
     return round((g["GB"] + e["GB"]) * streams, 4)
 
 
+def c5_overhead(be, plan, inp, stage_ms, reps=3):
+    """% overhead vs plain for C5 (one GPU, all M streams local): the no-fault
+    entangled step (prep_B, entangle + GEMM of every stream, check; the step's
+    own stage events) against the plain pipeline of the same scope and launch
+    mode (prep_B, then per stream the int32 -> int8 plane and the one-digit
+    GEMM: int64 results, and the narrowest native form with int32 products);
+    recovery reported as its own cost."""
+    import torch
+
+    ne = be.ne
+    rows, cols, K, M = plan.rows, plan.cols, plan.K, plan.M
+    dev = torch.device("cuda")
+    plane = torch.empty(rows * K, dtype=torch.int8, device=dev)
+    Bt = torch.empty(cols * K, dtype=torch.int8, device=dev)
+    o64 = torch.empty(rows * cols, dtype=torch.int64, device=dev)
+    o32 = torch.empty(rows * cols, dtype=torch.int32, device=dev)
+
+    def run(kind):
+        ne.ne_gemm_prep_b(inp["B"], K, cols, Bt)
+        for m in range(M):
+            ne.ne_to_limbs([inp["A"][m][0]], 1, plane)
+            if kind == "L1_int64_out":
+                ne.ne_op_gemm_limbs_stream(be.cfg, plane, 1, Bt, rows, cols, K, o64, 8)
+            else:
+                ne.ne_op_gemm_plain_i32(plane, Bt, rows, cols, K, [o32])
+
+    plain = {}
+    for kind, scope in (("L1_int64_out", "prep_B + M x (int32 -> int8 plane + one-digit pair GEMM, int64 out)"),
+                        ("native_L1", "prep_B + M x (int32 -> int8 plane + one-digit pair GEMM, int32 products)")):
+        run(kind)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            run(kind)
+        e1.record()
+        torch.cuda.synchronize()
+        plain[kind] = (e0.elapsed_time(e1) / reps, scope)
+    nf_keys = [k for k in stage_ms if k in ("entangle_gemm", "exchange", "check", "exchange_check")]
+    nf = sum(stage_ms[k] for k in nf_keys)
+    rec = stage_ms.get("exchange_recover", 0.0)
+    pct = {f"nofault_vs_plain_{k}": round((nf / ms - 1) * 100, 2) for k, (ms, _) in plain.items()}
+    pct["failstop_recover_vs_nofault"] = round(rec / nf * 100, 2)
+    return {"entangled_nofault": {"ms": round(nf, 4), "scope": "prep_B + M x (entangle + GEMM) + check "
+                                                                  "(the timed step's stage events: " + "+".join(nf_keys) + ")"},
+            "failstop_recover": {"ms": round(rec, 4), "scope": "recover (stream plan.kill lost)"},
+            "plain": {k: {"ms": round(ms, 4), "scope": sc} for k, (ms, sc) in plain.items()},
+            "pct": pct,
+            "timing": f"eager launches on both sides (as the C5 step), {reps} back-to-back plain pipelines (CUDA events)"}
+
+
 def run_c5(args, rank, world, local_rank):
     """configs[4]: M = 8 entangled streams (one per GPU when N = 8; stream m on
     rank m mod N otherwise), GEMM 16384^3 int32 U[-32,32) rows sharded, position-
@@ -1458,6 +1509,10 @@ def run_c5(args, rank, world, local_rank):
     }
     if fs is not None:
         line["failstop"] = fs
+    if world == 1:
+        ovh = c5_overhead(be, plan, inp, stage_ms)
+        line["overhead"] = ovh
+        line["overhead_pct"] = ovh["pct"]
     import oracle as O
 
     n = ORACLE_SAMPLE["c5"][0]
