@@ -105,6 +105,14 @@ out = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
 d = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
 f = lambda: ne.ne_op_conv_check(cfg, eps, taps, out, 0, d)
 """,
+    "c3_entangle": """
+M, n = 3, 4096   # C3's operand: 3 x 4096^2 int32 -> two base-2^22 digit planes per stream
+cfg = ne.ne_config_for(M)
+L, b = ne.ne_gemm_limb_plan(cfg, 64)
+A = [torch.randint(-64, 64, (n * n,), dtype=torch.int32, device='cuda') for _ in range(M)]
+planes = torch.empty(M * L * n * n, dtype=torch.int8, device='cuda')
+f = lambda: ne.ne_entangle_limbs(cfg, A, L, planes, None, b)
+""",
     "prep_b": """
 K, C = 4096, 4096   # C3's B operand: int32 K x cols -> int8 cols x K
 B = torch.randint(-128, 128, (K * C,), dtype=torch.int32, device='cuda')
