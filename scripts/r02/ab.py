@@ -62,6 +62,22 @@ ne.ne_conv_prep_taps(g, 0, Gt, None, bw)
 out = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
 f = lambda: ne.ne_op_conv_limbs(cfg, planes, L, Gt, N, T, 0, out, b, bw)
 """,
+    "conv_gemm128": """
+M, N, T = {M}, 10 ** 6, {T}   # the paper's conv shape with 128-output blocks forced (single-CTA 128 x 128 tiles)
+cfg = ne.ne_config_for(M)
+L, b = ne.ne_gemm_limb_plan(cfg, 127)
+bw = 128
+kp = (T + bw - 1 + 127) // 128 * 128
+plen = (bw * ((N + bw - 1) // bw) + kp + bw - 1) // bw * bw
+c = [torch.randint(-128, 128, (N,), dtype=torch.int32, device='cuda') for _ in range(M)]
+planes = torch.empty(M * L * plen, dtype=torch.int8, device='cuda')
+taps = torch.randint(-128, 128, (T,), dtype=torch.int32, device='cuda')
+Gt = torch.empty(bw * kp, dtype=torch.int8, device='cuda')
+ne.ne_entangle_limbs_conv(cfg, c, T, 0, L, planes, None, b, bw)
+ne.ne_conv_prep_taps(taps, 0, Gt, None, bw)
+out = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
+f = lambda: ne.ne_op_conv_limbs(cfg, planes, L, Gt, N, T, 0, out, b, bw)
+""",
     "c1_sac": """
 M, n = 3, 1 << 27
 cfg = ne.ne_config_for(M)
