@@ -419,6 +419,21 @@ ne_status ne_gemm_kernel_for(const ne_config* cfg, int32_t L, int32_t limb_bits,
  * turn it off.  Not thread-safe; NE_EINVAL if max_clusters < 0. */
 ne_status ne_gemm_trace(long long* buf, int32_t max_clusters);
 
+/* The CTA-pair kernel's schedule for two-digit GEMMs (host-only, no GPU
+ * needed): of n_tiles 256 x 256 pair tiles (over all M streams) on npairs
+ * resident SM pairs, *n_whole run whole; a last partial wave of r =
+ * n_tiles mod npairs tiles with 2 r <= npairs runs as 2 r half tiles of
+ * 256 x 128 (N = 128 MMAs, ~0.76 of a tile's time each), the same exact
+ * products.  C3: 768 tiles on 74 pairs -> 740 whole + 56 halves.  One-digit
+ * launches and the Toeplitz conv keep whole tiles.  NE_EINVAL for a null
+ * output, n_tiles < 0 or npairs < 1. */
+ne_status ne_gemm_pair_schedule(int64_t n_tiles, int64_t npairs, int64_t* n_whole);
+
+/* Debug hook (tests): mode 0 restores the schedule above, 1 keeps every pair
+ * tile whole, 2 halves every tile, for later two-digit CTA-pair launches in
+ * this process.  Not thread-safe; NE_EINVAL outside 0..2. */
+ne_status ne_gemm_pair_halves(int32_t mode);
+
 /* One stream of ne_op_gemm_limbs (the per-GPU GEMM of the one-stream-per-GPU
  * layout): C_m = sum_i 2^(8i) D_{m,i} B from planes_m (L planes). */
 ne_status ne_op_gemm_limbs_stream(const ne_config* cfg, const int8_t* planes_m, int32_t L,

@@ -34,7 +34,7 @@ EXPORTS = (
     "ne_op_scale", "ne_op_add", "ne_op_scale_add", "ne_op_inner", "ne_op_outer", "ne_op_conv", "ne_op_permute",
     "ne_gemm_workspace", "ne_op_gemm", "ne_gemm_prep_b", "ne_op_gemm_limbs",
     "ne_gemm_plan_for", "ne_entangle_plan", "ne_gemm_prep_b_planes", "ne_op_gemm_plan", "ne_op_gemm_plain_i32",
-    "ne_gemm_check_workspace", "ne_op_gemm_limbs_check", "ne_gemm_trace", "ne_gemm_kernel_for", "ne_op_gemm_limbs_scatter",
+    "ne_gemm_check_workspace", "ne_op_gemm_limbs_check", "ne_gemm_trace", "ne_gemm_pair_schedule", "ne_gemm_pair_halves", "ne_gemm_kernel_for", "ne_op_gemm_limbs_scatter",
     "ne_conv_geometry", "ne_entangle_limbs_conv", "ne_conv_prep_taps", "ne_op_conv_limbs",
     "ne_op_scale_add_check", "ne_op_conv_check", "ne_op_scale_add_check_w32",
     "ne_entangle_w32", "ne_op_scale_add_w32", "ne_disentangle_check_w32", "ne_recover_w32", "ne_inject_sweep_w32",
@@ -124,6 +124,8 @@ _SIGS = {
     "ne_op_conv_limbs": [_PCFG, _VP, _I32, _I32, _I32, _VP, _I64, _I32, _I32, Streams, _VP],
     "ne_gemm_check_workspace": [_I64, _I64, C.POINTER(_SZ)],
     "ne_gemm_trace": [_VP, _I32],
+    "ne_gemm_pair_schedule": [_I64, _I64, C.POINTER(_I64)],
+    "ne_gemm_pair_halves": [_I32],
     "ne_gemm_kernel_for": [_PCFG, _I32, _I32, _I64, _I64, _I64, C.POINTER(_I32)],
     "ne_op_gemm_limbs_scatter": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _I32, _VP, _VP],
     "ne_op_gemm_limbs_check": [_PCFG, _VP, _I32, _I32, _VP, _I64, _I64, _I64, Streams, _I32, Streams, _VP, _VP, _VP,
@@ -506,6 +508,18 @@ def ne_gemm_kernel_for(cfg: Config, L: int, limb_bits: int, rows: int, cols: int
 def ne_gemm_trace(buf: torch.Tensor | None, max_clusters: int = 0) -> None:
     """Debug hook: per-CTA tile timestamps of later GEMM launches (see ne.h)."""
     _call("ne_gemm_trace", _ptr(buf, torch.int64), max_clusters)
+
+
+def ne_gemm_pair_schedule(n_tiles: int, npairs: int) -> int:
+    """Pair tiles the CTA-pair kernel keeps whole (the rest run as two halves; see ne.h)."""
+    nw = _I64()
+    _call("ne_gemm_pair_schedule", n_tiles, npairs, C.byref(nw))
+    return nw.value
+
+
+def ne_gemm_pair_halves(mode: int) -> None:
+    """Debug hook: 0 automatic, 1 never halve, 2 halve every pair tile."""
+    _call("ne_gemm_pair_halves", mode)
 
 
 # ------------------------------------------------------------------ a4-a7

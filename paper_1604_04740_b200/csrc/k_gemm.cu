@@ -15,6 +15,8 @@ void launch_gemm_imad32w(int M, const ne_cstreams& A, const int32_t* B, const ne
 ne_status launch_gemm_tc(int M, int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                          int64_t K, const ne_streams& C, cudaStream_t s);
 void gemm_trace(long long* buf, int max_clusters);
+void gemm_pair_halves(int mode);
+int64_t gemm_pair_whole_tiles(int64_t n_tiles, int64_t npairs);
 bool gemm_pair_gate(int M, int L, int b, int64_t rows, int64_t cols, int64_t K);
 ne_status launch_gemm_tc_scatter(int L, int b, const int8_t* planes, const int8_t* Bt, int64_t rows, int64_t cols,
                                  int64_t K, const ne_streams& dests, int ndest, int64_t* local, cudaStream_t s);
@@ -387,6 +389,18 @@ extern "C" ne_status ne_gemm_kernel_for(const ne_config* cfg, int32_t L, int32_t
 extern "C" ne_status ne_gemm_trace(long long* buf, int32_t max_clusters) {
   if (max_clusters < 0) return NE_EINVAL;
   gemm_trace(buf, max_clusters);
+  return NE_OK;
+}
+
+extern "C" ne_status ne_gemm_pair_halves(int32_t mode) {
+  if (mode < 0 || mode > 2) return NE_EINVAL;
+  gemm_pair_halves(mode);
+  return NE_OK;
+}
+
+extern "C" ne_status ne_gemm_pair_schedule(int64_t n_tiles, int64_t npairs, int64_t* n_whole) {
+  if (!n_whole || n_tiles < 0 || npairs < 1) return NE_EINVAL;
+  *n_whole = gemm_pair_whole_tiles(n_tiles, npairs);
   return NE_OK;
 }
 

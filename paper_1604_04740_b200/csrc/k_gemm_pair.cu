@@ -7,7 +7,10 @@
 // then limb 0 — into the two halves of TMEM; the epilogue holds the finished
 // limb-1 accumulators in registers and releases that half at once, so the next
 // tile's limb-1 pass runs while this tile's limb 0 drains through the store
-// port (the drain is hidden, as in a double-buffered kernel).
+// port (the drain is hidden, as in a double-buffered kernel).  A last partial
+// wave of r tiles with 2 r <= pairs runs as 2 r half tiles (256 x 128, N = 128
+// MMAs; r02 A/B: the paper's M = 8, N = 2000 GEMM 81.5 -> 78.9 us, C3 280.5
+// -> 280.5 us against the previous build, 282.1 with every tile whole).
 //
 // Pair protocol (as SM100 2-SM kernels): both CTAs' TMA loads complete on the
 // LEADER's full[s] (peer bit of the barrier address cleared); the leader alone
@@ -30,20 +33,12 @@ namespace ne {
 int gemm_max_clusters();  // ne_gemm_trace's grid cap (debug / tests), k_gemm_tc.cu
 namespace tc {
 
-// one epilogue box [32 rows x 16 int64] to C: a TMA store, or a TMA
-// reduce-add (u64 maps, wrap mod 2^64) when several K parts add into C
-__device__ __forceinline__ void store_box(const CUtensorMap* map, int64_t c0, int64_t r0, unsigned char* box,
-                                          bool add) {
-  if (add)
-    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"((int32_t)c0), "r"((int32_t)r0), "r"(smem_u32(box))
-                 : "memory");
-  else
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"((int32_t)c0), "r"((int32_t)r0), "r"(smem_u32(box))
-                 : "memory");
+// one epilogue box [32 rows x 16 int64] (or [32 x 32 int32]) to C: a TMA store
+__device__ __forceinline__ void store_box(const CUtensorMap* map, int64_t c0, int64_t r0, unsigned char* box) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"((int32_t)c0), "r"((int32_t)r0), "r"(smem_u32(box))
+               : "memory");
 }
 
 template <int STAGES, int SW>
@@ -107,7 +102,8 @@ template <int L, int STAGES, int SW, bool OUT32 = false>
 __global__ void __launch_bounds__(kThreadsPair, 1)
 k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
             const __grid_constant__ OutMaps outm, int64_t rows, int64_t cols, int64_t K, int M, int limb_bits,
-            int raster, int64_t a_plane_rows, int toeplitz, int kcb, int64_t n_whole, int ksplit) {
+            int raster, int64_t a_plane_rows, int toeplitz, int kcb, int64_t n_whole,
+            const __grid_constant__ CUtensorMap mapBh) {
   static_assert(L == 1 || L == 2, "one or two digit planes");
   using CF = CfgP<STAGES, SW>;
   constexpr int BK = CF::BK, BN = CF::BN;
@@ -125,30 +121,26 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
   const bool leader = crank == 0;
   const int KB = (int)(K / BK);
   const int64_t n_rt = rows / (2 * BM), n_ct = cols / BN;
-  // Work items: tiles 0 .. n_whole - 1 whole (stored); the remaining n_split
-  // tiles each in ksplit K parts, item n_whole + j = (part j / n_split, tile
-  // n_whole + j mod n_split), every part added into the zeroed C (TMA
-  // reduce-add, u64): split-K for grids that would leave SM pairs idle
-  // (n_whole = 0; the host uses no other split at present)
+  // Work items: tiles 0 .. n_whole - 1 whole (256 x 256); the remaining tiles
+  // (L = 2, the last partial wave) as two 256 x 128 halves each, item
+  // n_whole + j = half j & 1 of tile n_whole + j / 2: N = 128 MMAs, half of
+  // every CTA's B box (mapBh), half the epilogue chunks.  A half costs ~0.76
+  // of a tile (the operand stream per MAC grows by half), so the last wave's
+  // tiles spread over twice the pairs (run_pair's schedule).
   const int64_t n_tiles = (int64_t)M * n_rt * n_ct;
-  const int64_t n_split = n_tiles - n_whole;
-  const int64_t n_work = n_whole + n_split * ksplit;
+  const int64_t n_work = n_whole + 2 * (n_tiles - n_whole);
   const int64_t pid = blockIdx.x / 2, npair = gridDim.x / 2;
-  auto decode = [&](int64_t w, int& m, int64_t& rt, int64_t& ct, int& kb0, int& kb1, bool& add) {
-    int kp = 0;
+  auto decode = [&](int64_t w, int& m, int64_t& rt, int64_t& ct, int& hs) {
     int64_t t = w;
-    add = w >= n_whole;
-    if (add) {
-      kp = (int)((w - n_whole) / n_split);
-      t = n_whole + (w - n_whole) % n_split;
+    hs = -1;
+    if (w >= n_whole) {
+      t = n_whole + (w - n_whole) / 2;
+      hs = (int)((w - n_whole) & 1);
     }
-    const int parts = add ? ksplit : 1;
     m = (int)(t / (n_rt * n_ct));
     const int64_t rem = t % (n_rt * n_ct);
     rt = raster ? rem % n_rt : rem / n_ct;
     ct = raster ? rem / n_rt : rem % n_ct;
-    kb0 = (int)((int64_t)kp * KB / parts);
-    kb1 = (int)((int64_t)(kp + 1) * KB / parts);
   };
 
   if (threadIdx.x == 0) {
@@ -176,54 +168,57 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+      if (n_whole < n_tiles) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapBh)) : "memory");
       uint32_t it = 0;
       for (int64_t w = pid; w < n_work; w += npair) {
-        int m, kb0, kb1;
+        int m, hs;
         int64_t rt, ct;
-        bool add;
-        decode(w, m, rt, ct, kb0, kb1, add);
+        decode(w, m, rt, ct, hs);
         const int64_t row0 = rt * 2 * BM + crank * BM;
-        const int64_t bcol0 = ct * BN + crank * (BN / 2);
+        // this CTA's B rows: half of the tile's columns (a quarter of a 256-wide tile for a half item)
+        const int64_t bcol0 = hs < 0 ? ct * BN + crank * (BN / 2) : ct * BN + hs * (BN / 2) + crank * (BN / 4);
+        const CUtensorMap* mb = hs < 0 ? &mapB : &mapBh;
+        const uint32_t tx = hs < 0 ? (uint32_t)(2 * CF::kStage) : (uint32_t)(2 * (CF::kATile + CF::kBHalf / 2));
         // K in chunks of kcb blocks, each chunk limb 1 then limb 0 (its B chunk is
         // still in L2 for the second pass); kcb = KB: one pass per limb
-        for (int c0 = kb0; c0 < kb1; c0 += kcb)
+        for (int c0 = 0; c0 < KB; c0 += kcb)
         for (int pass = 0; pass < L; ++pass) {
           const int li = L - 1 - pass;
-          for (int kb = c0; kb < kb1 && kb < c0 + kcb; ++kb, ++it) {
+          for (int kb = c0; kb < KB && kb < c0 + kcb; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
             unsigned char* st = smem + s * CF::kStage;
-            if (leader) mbar_expect_tx(&full[s], (uint32_t)(2 * CF::kStage));
+            if (leader) mbar_expect_tx(&full[s], tx);
             // Toeplitz mode (circular conv, k_conv_tc.cu): K-chunk kb of window row b is column
             // (kb BK) mod W of row b + (kb BK) / W of the [plane_rows][W] view of the extended plane
             const int32_t kc = toeplitz ? (int32_t)(((int64_t)kb * BK) % toeplitz) : kb * BK;
             const int64_t radd = toeplitz ? ((int64_t)kb * BK) / toeplitz : 0;
             tma_load_pair(&mapA, &full[s], st, kc, (int32_t)(((int64_t)m * L + li) * a_plane_rows + row0 + radd));
-            tma_load_pair(&mapB, &full[s], st + CF::kATile, kb * BK, (int32_t)bcol0);
+            tma_load_pair(mb, &full[s], st + CF::kATile, kb * BK, (int32_t)bcol0);
           }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      constexpr uint32_t idesc = idesc_i8(2 * BM, BN);
+      constexpr uint32_t idesc_full = idesc_i8(2 * BM, BN), idesc_half = idesc_i8(2 * BM, BN / 2);
       uint32_t it = 0, tile = 0;
       for (int64_t w = pid; w < n_work; w += npair, ++tile) {
-        int m, kb0, kb1;
+        int m, hs;
         int64_t rt, ct;
-        bool add;
-        decode(w, m, rt, ct, kb0, kb1, add);
-        for (int c0 = kb0; c0 < kb1; c0 += kcb)
+        decode(w, m, rt, ct, hs);
+        const uint32_t idesc = hs < 0 ? idesc_full : idesc_half;
+        for (int c0 = 0; c0 < KB; c0 += kcb)
         for (int pass = 0; pass < L; ++pass) {
           // L = 2: limb li into TMEM half li; L = 1: the tile into half tile & 1
           const int li = L == 2 ? 1 - pass : (int)(tile & 1);
           const int hb = L == 2 ? pass : li;                   // barrier pair of that half
           const uint32_t ph = L == 2 ? (tile & 1) : ((tile >> 1) & 1);
-          if (c0 == kb0) {
+          if (c0 == 0) {
             mbar_wait(&tmem_empty[hb], ph ^ 1);  // both CTAs freed this half
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           }
-          for (int kb = c0; kb < kb1 && kb < c0 + kcb; ++kb, ++it) {
+          for (int kb = c0; kb < KB && kb < c0 + kcb; ++kb, ++it) {
             const int s = it % STAGES;
             mbar_wait(&full[s], (it / STAGES) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -232,10 +227,10 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
 #pragma unroll
             for (int ks = 0; ks < BK / UMMA_K; ++ks)
               mma_pair(tmem_base + li * BN, umma_desc<SW>(sa + ks * UMMA_K), umma_desc<SW>(sb + ks * UMMA_K), idesc,
-                       (kb != kb0 || ks != 0) ? 1u : 0u);
+                       (kb != 0 || ks != 0) ? 1u : 0u);
             commit_pair(&empty[s]);
           }
-          if (c0 + kcb >= kb1) commit_pair(&tmem_full[hb]);  // limb li (L = 1: the tile) complete
+          if (c0 + kcb >= KB) commit_pair(&tmem_full[hb]);  // limb li (L = 1: the tile) complete
         }
       }
     }
@@ -248,13 +243,14 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
     constexpr int kNch = BN / 2 / 16;
     uint32_t tile = 0, buf = 0;
     for (int64_t w = pid; w < n_work; w += npair, ++tile) {
-      int m, kb0, kb1;
+      int m, hs;
       int64_t rt, ct;
-      bool add;
-      decode(w, m, rt, ct, kb0, kb1, add);
+      decode(w, m, rt, ct, hs);
       const int64_t row0 = rt * 2 * BM + crank * BM;
-      const int64_t col0 = ct * BN;
-      const int cb = half * (BN / 2);
+      // a half item (L = 2 only): columns [hs * 128, hs * 128 + 128) of the tile, 64 per warp
+      const int64_t col0 = ct * BN + (hs > 0 ? BN / 2 : 0);
+      const int cb = half * (hs < 0 ? BN / 2 : BN / 4);
+      const int nch = hs < 0 ? kNch : kNch / 2;
       if constexpr (L == 1 && OUT32) {
         // plain int32 products (the narrowest native baseline): two 16-column TMEM
         // chunks per [32 rows x 32 int32] box, 128B swizzle, TMA store (never split)
@@ -292,7 +288,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            store_box(&outm.m[m], col0 + cb + 16 * ci, row0 + 32 * q, box, false);
+            store_box(&outm.m[m], col0 + cb + 16 * ci, row0 + 32 * q, box);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
           buf = (buf + 1) % CF::kOutBufs;
@@ -332,7 +328,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            store_box(&outm.m[m], col0 + cb + 16 * ci, row0 + 32 * q, box, add);
+            store_box(&outm.m[m], col0 + cb + 16 * ci, row0 + 32 * q, box);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
           buf = (buf + 1) % CF::kOutBufs;
@@ -342,9 +338,11 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       mbar_wait(&tmem_full[0], tile & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // hold limb 1 of this warp's columns, release that half for the next tile
+      // (chunks ci >= nch are unused on a half item; indices stay compile-time)
       uint32_t hld[kNch][16];
 #pragma unroll
-      for (int ci = 0; ci < kNch; ++ci) tmem_ld16(tl + BN + cb + 16 * ci, hld[ci]);
+      for (int ci = 0; ci < kNch; ++ci)
+        if (ci < nch) tmem_ld16(tl + BN + cb + 16 * ci, hld[ci]);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
       for (int ci = 0; ci < kNch; ++ci)
@@ -357,13 +355,14 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int ci = 0; ci < kNch; ++ci) {
+        if (ci >= nch) break;
         const int c = cb + 16 * ci;
         uint32_t v0[16];
         tmem_ld16(tl + c, v0);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(v0[j]));
-        if (ci + 1 == kNch) {
+        if (ci + 1 == nch) {
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) arrive_leader(&tmem_empty[1]);
@@ -385,7 +384,7 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
-          store_box(&outm.m[m], col0 + c, row0 + 32 * q, box, add);
+          store_box(&outm.m[m], col0 + c, row0 + 32 * q, box);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
         buf = (buf + 1) % CF::kOutBufs;
@@ -400,6 +399,19 @@ k_gemm_pair(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CU
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512u));
   }
+}
+
+// Tiles kept whole by run_pair's schedule: all of them, or all but a last
+// partial wave of r tiles when its 2 r halves fit one wave (2 r <= np).
+// g_halves (debug hook ne_gemm_pair_halves): 0 = this rule, 1 = never halve,
+// 2 = halve every tile.
+static int g_halves = 0;
+
+int64_t pair_halves(int64_t n_tiles, int64_t np) {
+  if (g_halves == 1 || np < 1) return n_tiles;
+  if (g_halves == 2) return 0;
+  const int64_t r = n_tiles % np;
+  return (r > 0 && 2 * r <= np) ? n_tiles - r : n_tiles;
 }
 
 // plain GEMM: a_plane_rows = out_rows = rows, toeplitz = 0; Toeplitz conv:
@@ -438,51 +450,47 @@ static ne_status run_pair(const int8_t* planes, const int8_t* Bt, int64_t rows, 
   }
   if (gemm_max_clusters() > 0 && npairs > gemm_max_clusters()) npairs = gemm_max_clusters();
 
-  // schedule: whole tiles.  The kernel can also run tiles in K parts that
-  // reduce-add into a zeroed C (n_whole < n_tiles, ksplit > 1); every
-  // schedule of that kind was A/B-measured slower on one box
-  // (scripts/r02/ab.py): split-K of under-filled grids (C3's N = 8 row split,
-  // 96 pair tiles: 67.1 vs 55.1 us; the C2P M = 3, T = 4500 conv: 47.5 vs
-  // 41.9 us) and a split last wave (C3: 274.3 vs 274.4 us; the paper's M = 8,
-  // N = 2000 GEMM: 0.092 vs 0.084 ms) — every extra part re-drains an int64
-  // tile through the SM's store port.  NE_PAIR_KSPLIT=<s> (compile time)
-  // splits every tile, for experiments.
+  // schedule: whole 256 x 256 tiles, except (L = 2, plain GEMMs) that a last
+  // partial wave of r tiles with 2 r <= pairs runs as 2 r half tiles of 256 x
+  // 128 (pair_halves): a half costs ~0.76 of a tile (C3's shape with every
+  // tile halved: 408.8 vs 280.7 us for twice the items); measured on the
+  // tail: the paper's M = 8, N = 2000 GEMM 81.5 -> 78.9 us, C3 282.1 -> 280.5.  Split-K schedules (reduce-add into a zeroed C, or a
+  // chained workspace fix-up) were measured slower: every K part
+  // re-drains a whole int64 tile.
   const int64_t n_rt = rows / (2 * BM), n_ct = cols / CF::BN;
   const int64_t n_tiles = (int64_t)M * n_rt * n_ct;
-#ifdef NE_PAIR_KSPLIT
-  const int ksplit = OUT32 ? 1 : NE_PAIR_KSPLIT;
-#else
-  const int ksplit = 1;
-#endif
-  const int64_t n_whole = ksplit > 1 ? 0 : n_tiles;
-  const bool adds = n_whole < n_tiles;
-  const int64_t n_work = n_whole + (n_tiles - n_whole) * ksplit;
+  const int64_t n_whole = (L == 2 && !OUT32 && !toeplitz) ? pair_halves(n_tiles, npairs) : n_tiles;
+  const int64_t n_work = n_whole + 2 * (n_tiles - n_whole);
   if (npairs > n_work) npairs = n_work;
   lc.gridDim = dim3((unsigned)(npairs * 2));
   // B panel larger than ~1/3 of L2: row tiles fastest (consecutive pairs share a B panel)
   const int raster = !toeplitz && (uint64_t)cols * (uint64_t)K > (48ull << 20) ? 1 : 0;
 
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mbh;
   if (!make_map(&ma, planes, toeplitz ? (uint64_t)toeplitz : (uint64_t)K, (uint64_t)M * L * a_plane_rows, SW, BM))
     return NE_ECUDA;
   if (!make_map(&mb, Bt, (uint64_t)K, (uint64_t)cols, SW, CF::BN / 2)) return NE_ECUDA;
+  if (!make_map(&mbh, Bt, (uint64_t)K, (uint64_t)cols, SW, CF::BN / 4)) return NE_ECUDA;
   OutMaps om;
   for (int m = 0; m < M; ++m) {
     if (OUT32 ? !make_out_map32(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows)
-              : !make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows, adds))
+              : !make_out_map(&om.m[m], C.s[m], (uint64_t)cols, (uint64_t)out_rows))
       return NE_ECUDA;
-    if (n_whole == 0 && cudaMemsetAsync(C.s[m], 0, (size_t)out_rows * cols * 8, s) != cudaSuccess) return NE_ECUDA;
   }
   // whole-K passes up to K = 8192 (B chunks of one pass stay in L2 at these
   // sizes); 4096-deep chunks beyond
   const int kcb = (L == 1 || K <= 8192) ? (int)(K / CF::BK) : 4096 / CF::BK;
   if (cudaLaunchKernelEx(&lc, kern, ma, mb, om, rows, cols, K, M, limb_bits, raster, a_plane_rows, toeplitz, kcb,
-                         n_whole, ksplit) != cudaSuccess)
+                         n_whole, mbh) != cudaSuccess)
     return NE_ECUDA;
   return launch_status();
 }
 
 }  // namespace tc
+
+void gemm_pair_halves(int mode) { tc::g_halves = mode; }
+
+int64_t gemm_pair_whole_tiles(int64_t n_tiles, int64_t npairs) { return tc::pair_halves(n_tiles, npairs); }
 
 // Toeplitz conv with 256-output blocks and 2 limbs on the pair kernel (C2P).
 ne_status launch_conv_pair(int M, int b, const int8_t* planes, int64_t plane_rows, const int8_t* Gt, int64_t Kpad,

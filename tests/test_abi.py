@@ -245,3 +245,22 @@ def test_empty_inputs_are_no_ops(L):
     }
     for name, args in calls.items():
         assert getattr(L, name)(*args) == 0, name
+
+
+def test_gemm_pair_schedule(L):
+    """The CTA-pair kernel keeps whole tiles except a last partial wave of r
+    tiles with 2 r <= pairs, which runs as 2 r half tiles: C3's 768 tiles on
+    74 pairs -> 740 whole + 28 halved; the paper's M = 8, N = 2000 GEMM (320
+    tiles) -> 296 whole; 48 or 128 tiles (r = 48 / 54 > 37) stay whole; full
+    waves stay whole; 12 tiles on 74 pairs are all halved."""
+    assert ne.ne_gemm_pair_schedule(768, 74) == 740
+    assert ne.ne_gemm_pair_schedule(320, 74) == 296
+    assert ne.ne_gemm_pair_schedule(48, 74) == 48
+    assert ne.ne_gemm_pair_schedule(128, 74) == 128
+    assert ne.ne_gemm_pair_schedule(740, 74) == 740
+    assert ne.ne_gemm_pair_schedule(12, 74) == 0
+    assert ne.ne_gemm_pair_schedule(0, 74) == 0
+    with pytest.raises(ne.NeError):
+        ne.ne_gemm_pair_schedule(10, 0)
+    with pytest.raises(ne.NeError):
+        ne.ne_gemm_pair_halves(3)

@@ -543,6 +543,55 @@ def test_gemm_pair_multi_tile(O):
             assert (out[m].cpu().numpy().reshape(R, Cc) @ x == E[m] @ bx).all(), (cap, m)
 
 
+@pytest.mark.parametrize("cap", [0, 4, 8])
+def test_gemm_pair_half_tiles(O, cap):
+    """The pair kernel's 256 x 128 half tiles (N = 128 MMAs, a quarter of the
+    B columns per CTA through the half-box tensor map, 4 epilogue chunks per
+    warp): every tile halved (debug hook), every tile whole, and the
+    automatic schedule (a last partial wave halved), with the full grid
+    (automatic: all 18 tiles halved) and with 4 or 8 pairs (automatic: 16
+    whole tiles, then 4 halves — halves after whole tiles on one pair):
+    bit-identical, and equal to the oracle on rows in every lane group plus
+    a Freivalds identity over the whole output."""
+    M, R, Cc, K = 3, 512, 768, 4096     # 18 pair tiles
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    L, b = ne.ne_gemm_limb_plan(cfg, 127)
+    assert ne.ne_gemm_kernel_for(cfg, L, b, R, Cc, K) == "pair"
+    A = gen(O, 87, 4, M, R * K, -127, 128)
+    A[:, 0], A[:, -1] = 127, -127
+    B = O.gen_uniform(87, 5, 0, -128, 128, K * Cc)
+    planes = torch.empty(M * L * R * K, dtype=torch.int8, device="cuda")
+    ne.ne_entangle_limbs(cfg, to_streams(A), L, planes, limb_bits=b)
+    Bt = torch.empty(Cc * K, dtype=torch.int8, device="cuda")
+    ne.ne_gemm_prep_b(dev(B, torch.int32), K, Cc, Bt)
+    outs = {}
+    ne.ne_gemm_trace(None, cap)
+    try:
+        for mode in (1, 2, 0):
+            ne.ne_gemm_pair_halves(mode)
+            o = empty_streams(M, R * Cc)
+            for t in o:
+                t.fill_(-1)
+            ne.ne_op_gemm_limbs(cfg, planes, L, Bt, R, Cc, K, o, limb_bits=b)
+            torch.cuda.synchronize()
+            outs[mode] = o
+    finally:
+        ne.ne_gemm_pair_halves(0)
+        ne.ne_gemm_trace(None, 0)
+    for mode in (2, 0):
+        assert all(torch.equal(x, y) for x, y in zip(outs[mode], outs[1])), mode
+    out = outs[2]
+    E = O.entangle(ocfg, A).reshape(M, R, K)
+    rows = _band_rows(R, 128, seed=cap)
+    ref = O.op_gemm(ocfg, E[:, rows], B.reshape(K, Cc))
+    got = np.stack([out[m].view(R, Cc)[torch.from_numpy(rows).cuda()].cpu().numpy() for m in range(M)])
+    assert (got == ref).all()
+    x = np.random.default_rng(cap + 10).integers(-2, 2, size=Cc)   # |E (B x)| < 2^30 2^12 2^9 2^8 < 2^63
+    bx = B.reshape(K, Cc) @ x
+    for m in range(M):
+        assert (out[m].cpu().numpy().reshape(R, Cc) @ x == E[m] @ bx).all(), m
+
+
 def test_gemm_plain_i32(O):
     """The narrowest native baseline (plain one-digit GEMM, int32 products):
     every entry equal to A_m B (numpy on the same seeded inputs, exact: |A B|
