@@ -547,12 +547,13 @@ class C4PermInner(Workload):
     E2E_IN = ("c",)
     E2E_OUT = ("dout",)
 
-    def __init__(self, rank, n=1 << 28, seed=3, layout="aos", w=64, world=1, scaling="strong"):
+    def __init__(self, rank, n=1 << 28, seed=3, layout="aos", w=64, world=1, scaling="strong", algo="gather"):
         import torch
         import paper_1604_04740_b200 as ne
 
         self.ne, self.torch = ne, torch
         self.M, self.n, self.B, self.layout, self.w = 4, n, 1024, layout, w
+        self.algo = algo if (layout == "aos" and w == 64) else "gather"
         self.b0 = 0   # first output block this rank checks
         if scaling == "strong" and world > 1 and (layout != "aos" or w != 64):
             scaling = "weak"
@@ -590,6 +591,10 @@ class C4PermInner(Workload):
         self.bitmap = torch.empty((self.nb + 31) // 32, dtype=torch.int32, device=dev)
         self.diag = ne.diag_new()
         self.launches_per_step = 3
+        if self.algo == "bucket":
+            self.name = "C4_bucket"
+            self.ws = torch.empty(ne.ne_permute_inner_workspace(self.cfg, n, self.B), dtype=torch.uint8, device=dev)
+            self.launches_per_step = 5   # entangle, scatter, reduce, check, recover (+ memsets)
 
     def _init_placement(self, rank, world, seed):
         """one entangled stream per GPU (streams m = rank mod
@@ -687,6 +692,14 @@ class C4PermInner(Workload):
                     delta_out=self.delta, bitmap=self.bitmap, diag=self.diag)),
                 ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
             ]
+        if self.algo == "bucket":
+            return [
+                ("entangle", lambda: ne.ne_entangle_aos(cfg, self.c, self.eps, self.diag)),
+                ("permute_inner_check", lambda: ne.ne_op_permute_inner_check_bucketed(
+                    cfg, self.eps, self.perm, self.v, self.B, 0, self.delta, self.dout, self.ws,
+                    self.bitmap, self.diag)),
+                ("recover", lambda: ne.ne_recover(cfg, part, r, self.drec)),
+            ]
         return [
             ("entangle", lambda: ne.ne_entangle_aos(cfg, self.c, self.eps, self.diag)),
             ("permute_inner_check", lambda: ne.ne_op_permute_inner_check(
@@ -711,6 +724,15 @@ class C4PermInner(Workload):
         gathered position."""
         if dom != "permute_inner_check" or self.layout != "aos" or getattr(self, "placement", False):
             return None
+        if self.algo == "bucket":   # what the scatter-reduce moves: perm 4 + pairs 8 + 8 + eps 32 B per position
+            per = 52
+            gb = self.n * per / 1e9
+            ach = gb / (ms / 1e3)
+            return {"bytes_per_position": per, "bytes_per_launch_GB": round(gb, 3), "achieved": round(ach, 1),
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
+                    "floor_ms": round(gb / peaks["hbm_gbs"] * 1e3, 3),
+                    "evidence": "bucketed scatter-reduce: perm read, (i, perm[i]) pairs written and read, every "
+                                "eps entry read once from its window (L2-resident while its bucket is consumed)"}
         per = 128 + 4
         gb = self.n * per / 1e9
         ach = gb / (ms / 1e3)
@@ -751,7 +773,10 @@ class C4PermInner(Workload):
                            "SoA (one int64 stream per m; 4 random sectors per gathered position)"),
                 "entanglement": {"l": self.cfg.l, "k": self.cfg.k, "w": self.w},
                 "l2": "working set ~13 GB >> 126 MB L2 (no flush needed)",
-                "step": "entangle(AoS)+gather/inner/disentangle/check fused(r=0)+recover(r=step mod 4)"}
+                "step": ("entangle(AoS)+bucketed scatter-reduce permute/inner + disentangle/check(r=0)"
+                         "+recover(r=step mod 4)" if self.algo == "bucket" else
+                         "entangle(AoS)+gather/inner/disentangle/check fused(r=0)+recover(r=step mod 4)"),
+                "c4algo": self.algo}
 
     def plain_times(self, reps=3):
         """Same gather + inner kernel on plain (unentangled) data in the same
@@ -1205,7 +1230,7 @@ def make_workload(args, rank, world=1):
         return C2Conv(rank, n=10 ** 6, taps=args.taps, M=args.streams, algo=args.conv or "tc", paper=True,
                       scheme=args.scheme, **kw)
     if args.workload == "c4":
-        return C4PermInner(rank, layout=args.layout, w=args.w, **kw)
+        return C4PermInner(rank, layout=args.layout, w=args.w, algo=args.c4algo, **kw)
     if args.workload == "c1":
         return C1Chain(rank, n=args.n or 4096, w=args.w, fuse=bool(args.fuse if args.fuse is not None else 1), **kw)
     return WORKLOADS[args.workload](rank)
@@ -1992,7 +2017,7 @@ CONFIG_SET = (
     ("C5", dict(workload="c5", steps=5)),
 )
 _SUB_DEFAULTS = dict(algo="tc", limbs="plan", scheme="entangled", fuse=None, conv=None, taps=4500, streams=8,
-                     kdim=2000, w=64, layout="aos", n=None, failstop="simulated", exchange="auto", graph=1,
+                     kdim=2000, w=64, layout="aos", c4algo="gather", n=None, failstop="simulated", exchange="auto", graph=1,
                      scaling="strong", abound=64, bbound=64)
 
 
@@ -2067,6 +2092,9 @@ def main():
     ap.add_argument("--bbound", type=int, default=64, help="c3: B ~ U[-bbound, bbound)")
     ap.add_argument("--w", type=int, default=64, choices=[64, 32], help="c1 / c4: container width (P:528-530)")
     ap.add_argument("--layout", default="aos", choices=["aos", "soa"], help="c4: entangled layout at rest")
+    ap.add_argument("--c4algo", default="gather", choices=["gather", "bucket"],
+                    help="c4 (AoS, w = 64): the fused gather kernel, or the bucketed scatter-reduce "
+                         "(ne_op_permute_inner_check_bucketed: no random DRAM gather)")
     ap.add_argument("--n", type=int, default=None, help="c1: stream length (default 4096 = configs[0])")
     ap.add_argument("--failstop", default="simulated", choices=["simulated", "exit"],
                     help="c5 at N = M = 8: after the timed steps, the rank of stream 3 exits its process and the "

@@ -471,6 +471,27 @@ ne_status ne_op_permute_inner_check(const ne_config* cfg, ne_cstreams x, const i
                                     ne_streams delta_out, ne_streams d_out, uint32_t* bitmap,
                                     ne_diag* diag, ne_stream_t stream);
 
+/* The same op as a partitioned scatter-reduce, without a random DRAM gather
+ * (k_permute_bucket.cu): the pairs (i, perm[i]) are partitioned into cells
+ * (source window perm[i] >> S, destination range of output blocks) by a
+ * count, a scan and a scatter pass over perm (coalesced); then one CTA per
+ * destination range walks its cells window by window — every CTA reads the
+ * same window of x, which stays in L2 — and adds each pair's M products
+ * x_m[perm[i]] * v[i mod vlen] into its shared-memory block sums (int64 sums
+ * mod 2^64, so delta is bit-identical to the gather form), written once;
+ * then ne_disentangle_check on delta.  x AoS only (x_aos[n*M + m], 16-byte
+ * aligned), M <= 8 (NE_ENOTSUP otherwise), perm required and a bijection of
+ * [0, n_total): entries outside it are range violations in diag (first_bad =
+ * i) and skipped.  delta (required) receives the block sums.  workspace:
+ * device memory of at least ne_permute_inner_workspace(cfg, n_total, block)
+ * bytes, 16-byte aligned, owned by the caller (NE_EINVAL if smaller). */
+ne_status ne_permute_inner_workspace(const ne_config* cfg, int64_t n_total, int64_t block, size_t* bytes);
+ne_status ne_op_permute_inner_check_bucketed(const ne_config* cfg, const int64_t* x_aos, const int32_t* perm,
+                                             int64_t n_total, const int32_t* v, int64_t vlen, int64_t block,
+                                             int32_t r, ne_streams delta, ne_streams d_out, uint32_t* bitmap,
+                                             ne_diag* diag, void* workspace, size_t ws_bytes,
+                                             ne_stream_t stream);
+
 /* ====================================== comparison baseline: ABFT (NEXT-1) === */
 /* The paper's comparison method, run on the same hardware so the
  * overhead of entanglement can be compared with ABFT's at equal fault

@@ -39,7 +39,7 @@ EXPORTS = (
     "ne_op_scale_add_check", "ne_op_conv_check", "ne_op_scale_add_check_w32",
     "ne_entangle_w32", "ne_op_scale_add_w32", "ne_disentangle_check_w32", "ne_recover_w32", "ne_inject_sweep_w32",
     "ne_entangle_aos_w32", "ne_op_permute_inner_check_w32",
-    "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check", "ne_op_permute_inner_stream",
+    "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check", "ne_op_permute_inner_stream", "ne_permute_inner_workspace", "ne_op_permute_inner_check_bucketed",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
     "ne_abft_encode", "ne_abft_encode_limbs", "ne_abft_encode_conv", "ne_op_conv_limbs_plain", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
 )
@@ -132,6 +132,9 @@ _SIGS = {
                                _VP],
     "ne_disentangle_check": [_PCFG, Streams, _I64, _I32, Streams, _VP, _VP, _VP],
     "ne_recover": [_PCFG, Streams, _I64, _I32, Streams, _VP],
+    "ne_permute_inner_workspace": [_PCFG, _I64, _I64, C.POINTER(_SZ)],
+    "ne_op_permute_inner_check_bucketed": [_PCFG, _VP, _VP, _I64, _VP, _I64, _I64, _I32, Streams, Streams, _VP, _VP,
+                                           _VP, _SZ, _VP],
     "ne_op_permute_inner_check": [_PCFG, Streams, _VP, _I32, _VP, _I64, _VP, _I64, _I64, _I32,
                                   Streams, Streams, _VP, _VP, _VP],
     "ne_op_permute_inner_stream": [_PCFG, _VP, _VP, _I64, _VP, _I64, _I64, _I64, _I64, _VP, _VP],
@@ -543,6 +546,23 @@ def ne_op_permute_inner_check(cfg: Config, v: torch.Tensor, block: int, r: int, 
     _call("ne_op_permute_inner_check", C.byref(cfg), xs, _ptr(x_aos, torch.int64), int(x_aos is not None),
           _ptr(perm, torch.int32), n, _ptr(v, torch.int32), v.numel(), block, r, do, _streams(d_out, torch.int64),
           _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _stream())
+
+
+def ne_permute_inner_workspace(cfg: Config, n: int, block: int) -> int:
+    """Bytes of device workspace ne_op_permute_inner_check_bucketed needs."""
+    b = _SZ()
+    _call("ne_permute_inner_workspace", C.byref(cfg), n, block, C.byref(b))
+    return b.value
+
+
+def ne_op_permute_inner_check_bucketed(cfg: Config, x_aos: torch.Tensor, perm: torch.Tensor, v: torch.Tensor,
+                                       block: int, r: int, delta, d_out, ws: torch.Tensor, bitmap=None,
+                                       diag=None) -> None:
+    """The C4 op as a partitioned scatter-reduce (no random gather; see ne.h)."""
+    n = x_aos.numel() // cfg.M
+    _call("ne_op_permute_inner_check_bucketed", C.byref(cfg), _ptr(x_aos, torch.int64), _ptr(perm, torch.int32), n,
+          _ptr(v, torch.int32), v.numel(), block, r, _streams(delta, torch.int64), _streams(d_out, torch.int64),
+          _ptr(bitmap, torch.int32), _ptr(diag, torch.int64), _ptr(ws), ws.numel() * ws.element_size(), _stream())
 
 
 def ne_op_permute_inner_stream(cfg: Config, x_m: torch.Tensor, perm: torch.Tensor, v: torch.Tensor, block: int,

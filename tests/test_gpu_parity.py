@@ -352,6 +352,84 @@ def test_permute_inner_check(O, M, aos, gather):
     assert ne.diag_read(diag)["fault_positions"] == 0
 
 
+@pytest.mark.parametrize("M,N,B,vlen", [(4, 1024 * 37 + 500, 1024, 1024), (3, 100003, 100, 100), (8, 65536, 1024, 1024),
+                                        (5, 4099, 7, 3), (4, 1 << 20, 1024, 1024), (4, 1, 1024, 1024)])
+def test_permute_inner_bucketed(O, M, N, B, vlen):
+    """The bucketed scatter-reduce form of the C4 op (ne_op_permute_inner_check_
+    bucketed): delta, d_hat, bitmap and diag equal to the oracle's gather +
+    blocked inner product + disentangle/check and bit-identical to the
+    gather kernel — ragged n (last window and last block partial), block !=
+    vlen, M = 3..8, windows from 16 up (n = 2^20), run twice on the same
+    workspace."""
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 5, 1, M, N, -2 ** 12, 2 ** 12)
+    perm = O.gen_perm(5, 6, N)
+    v = O.gen_uniform(5, 7, 0, -2 ** 12, 2 ** 12, vlen)
+    eps = O.entangle(ocfg, c)
+    x_aos = dev(eps.T.copy(), torch.int64).reshape(-1)
+    nb = (N + B - 1) // B
+    ws = torch.empty(ne.ne_permute_inner_workspace(cfg, N, B), dtype=torch.uint8, device="cuda")
+    p = perm
+    idx = np.arange(N)
+    odelta = np.zeros((M, nb), dtype=np.int64)
+    prod = (eps[:, p].astype(np.int64) * v[idx % vlen].astype(np.int64))   # |eps v| < 2^29 2^12: exact
+    for m in range(M):
+        odelta[m] = np.add.reduceat(prod[m], np.arange(0, N, B)) if N > 0 else 0
+    if vlen == B:
+        assert (odelta == O.op_inner(ocfg, O.op_permute(eps, p), v, B)).all()   # the oracle's own definition
+    od, oflags, onf = O.disentangle_check(ocfg, odelta, 2 % M)
+    for _ in range(2):
+        delta, d_out = empty_streams(M, nb), empty_streams(M, nb)
+        bm = torch.full(((nb + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        diag = ne.diag_new()
+        ne.ne_op_permute_inner_check_bucketed(cfg, x_aos, dev(perm, torch.int32), dev(v, torch.int32), B, 2 % M,
+                                              delta, d_out, ws, bm, diag)
+        torch.cuda.synchronize()
+        assert (to_np(delta) == odelta).all()
+        assert (to_np(d_out) == od).all()
+        assert (bitmap_to_flags(bm, nb) == oflags).all() and onf == 0
+        dd = ne.diag_read(diag)
+        assert dd["fault_positions"] == 0 and dd["range_violations"] == 0
+    if vlen == B:
+        d2 = empty_streams(M, nb)
+        g = empty_streams(M, nb)
+        ne.ne_op_permute_inner_check(cfg, dev(v, torch.int32), B, 2 % M, d2, x_aos=x_aos,
+                                     perm=dev(perm, torch.int32), n=N, delta_out=g)
+        assert all(torch.equal(a, b) for a, b in zip(g, delta)) and all(torch.equal(a, b) for a, b in zip(d2, d_out))
+
+
+def test_permute_inner_bucketed_bad_perm_and_fault(O):
+    """perm entries outside [0, n) are counted (first named) and skipped; a
+    stored-eps fault in one stream flags exactly its block, as the gather
+    path does."""
+    M, N, B = 4, 1024 * 64, 1024
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 6, 1, M, N, -2 ** 12, 2 ** 12)
+    perm = O.gen_perm(6, 6, N)
+    v = O.gen_uniform(6, 7, 0, -2 ** 12, 2 ** 12, B)
+    eps = O.entangle(ocfg, c)
+    xa = eps.T.copy()
+    xa[perm[5000], 1] = np.int64(np.uint64(xa[perm[5000], 1]) ^ np.uint64(1 << 33))   # position 5000's source
+    x_aos = dev(xa, torch.int64).reshape(-1)
+    nb = N // B
+    ws = torch.empty(ne.ne_permute_inner_workspace(cfg, N, B), dtype=torch.uint8, device="cuda")
+    delta, d_out = empty_streams(M, nb), empty_streams(M, nb)
+    bm = torch.empty(nb // 32, dtype=torch.int32, device="cuda")
+    diag = ne.diag_new()
+    ne.ne_op_permute_inner_check_bucketed(cfg, x_aos, dev(perm, torch.int32), dev(v, torch.int32), B, 0, delta,
+                                          d_out, ws, bm, diag)
+    flags = bitmap_to_flags(bm, nb)
+    assert flags.sum() == 1 and flags[5000 // B]
+    assert ne.diag_read(diag)["fault_positions"] == 1
+    bad = perm.copy()
+    bad[[17, 40000]] = [-3, N + 5]
+    diag = ne.diag_new()
+    ne.ne_op_permute_inner_check_bucketed(cfg, dev(eps.T.copy(), torch.int64).reshape(-1), dev(bad, torch.int32),
+                                          dev(v, torch.int32), B, 0, delta, d_out, ws, None, diag)
+    dd = ne.diag_read(diag)
+    assert dd["range_violations"] == 2 and dd["first_bad"] == 17
+
+
 def test_permute_inner_detects_storage_fault(O):
     """A fault in one stored eps word (one stream) is caught in its block."""
     M, N, B = 4, 1024 * 64, 1024
