@@ -547,7 +547,7 @@ class C4PermInner(Workload):
     E2E_IN = ("c",)
     E2E_OUT = ("dout",)
 
-    def __init__(self, rank, n=1 << 28, seed=3, layout="aos", w=64, world=1, scaling="strong", algo="gather"):
+    def __init__(self, rank, n=1 << 28, seed=3, layout="aos", w=64, world=1, scaling="strong", algo="bucket"):
         import torch
         import paper_1604_04740_b200 as ne
 
@@ -591,8 +591,9 @@ class C4PermInner(Workload):
         self.bitmap = torch.empty((self.nb + 31) // 32, dtype=torch.int32, device=dev)
         self.diag = ne.diag_new()
         self.launches_per_step = 3
+        if self.algo == "gather" and layout == "aos" and w == 64:
+            self.name = "C4_gather"   # traffic.json key of the gather-kernel line
         if self.algo == "bucket":
-            self.name = "C4_bucket"
             self.ws = torch.empty(ne.ne_permute_inner_workspace(self.cfg, n, self.B), dtype=torch.uint8, device=dev)
             self.launches_per_step = 5   # entangle, scatter, reduce, check, recover (+ memsets)
 
@@ -786,19 +787,25 @@ class C4PermInner(Workload):
             return {}
         plain = torch.stack([x.to(torch.int64) for x in self.c], dim=1).reshape(-1).contiguous()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ne.ne_op_permute_inner_check(self.cfg, self.v, self.B, 0, self.drec, x_aos=plain, perm=self.perm,
-                                     n=self.n, delta_out=self.delta)
+        if self.algo == "bucket":
+            run = lambda: ne.ne_op_permute_inner_check_bucketed(  # noqa: E731
+                self.cfg, plain, self.perm, self.v, self.B, 0, self.delta, self.drec, self.ws)
+            what = ("partitioned scatter-reduce + inner (+check, meaningless on plain data) on plain int64 AoS "
+                    "containers, inputs already widened")
+        else:
+            run = lambda: ne.ne_op_permute_inner_check(  # noqa: E731
+                self.cfg, self.v, self.B, 0, self.drec, x_aos=plain, perm=self.perm, n=self.n, delta_out=self.delta)
+            what = ("gather+inner (+check, skipped on plain data) on plain int64 AoS containers, "
+                    "inputs already widened")
+        run()
         torch.cuda.synchronize()
         e0.record()
         for _ in range(reps):
-            ne.ne_op_permute_inner_check(self.cfg, self.v, self.B, 0, self.drec, x_aos=plain, perm=self.perm,
-                                         n=self.n, delta_out=self.delta)
+            run()
         e1.record()
         torch.cuda.synchronize()
         del plain
-        return {"plain_same_kernel": (e0.elapsed_time(e1) / reps,
-                                      "gather+inner (+check, skipped on plain data) on plain int64 AoS containers, "
-                                      "inputs already widened")}
+        return {"plain_same_kernel": (e0.elapsed_time(e1) / reps, what)}
 
     def oracle_sample(self, blocks):
         import oracle as O
@@ -2017,7 +2024,7 @@ CONFIG_SET = (
     ("C5", dict(workload="c5", steps=5)),
 )
 _SUB_DEFAULTS = dict(algo="tc", limbs="plan", scheme="entangled", fuse=None, conv=None, taps=4500, streams=8,
-                     kdim=2000, w=64, layout="aos", c4algo="gather", n=None, failstop="simulated", exchange="auto", graph=1,
+                     kdim=2000, w=64, layout="aos", c4algo="bucket", n=None, failstop="simulated", exchange="auto", graph=1,
                      scaling="strong", abound=64, bbound=64)
 
 
@@ -2092,9 +2099,9 @@ def main():
     ap.add_argument("--bbound", type=int, default=64, help="c3: B ~ U[-bbound, bbound)")
     ap.add_argument("--w", type=int, default=64, choices=[64, 32], help="c1 / c4: container width (P:528-530)")
     ap.add_argument("--layout", default="aos", choices=["aos", "soa"], help="c4: entangled layout at rest")
-    ap.add_argument("--c4algo", default="gather", choices=["gather", "bucket"],
-                    help="c4 (AoS, w = 64): the fused gather kernel, or the bucketed scatter-reduce "
-                         "(ne_op_permute_inner_check_bucketed: no random DRAM gather)")
+    ap.add_argument("--c4algo", default="bucket", choices=["gather", "bucket"],
+                    help="c4 (AoS, w = 64): the partitioned scatter-reduce (ne_op_permute_inner_check_bucketed: "
+                         "no random DRAM gather; default), or the fused gather kernel")
     ap.add_argument("--n", type=int, default=None, help="c1: stream length (default 4096 = configs[0])")
     ap.add_argument("--failstop", default="simulated", choices=["simulated", "exit"],
                     help="c5 at N = M = 8: after the timed steps, the rank of stream 3 exits its process and the "

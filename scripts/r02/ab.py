@@ -78,6 +78,25 @@ ne.ne_conv_prep_taps(taps, 0, Gt, None, bw)
 out = [torch.empty(N, dtype=torch.int64, device='cuda') for _ in range(M)]
 f = lambda: ne.ne_op_conv_limbs(cfg, planes, L, Gt, N, T, 0, out, b, bw)
 """,
+    "c4_permute": """
+M, n, B = 4, 1 << 28, 1024   # C4's permute + inner + check stage (--T 1: the partitioned scatter-reduce)
+cfg = ne.ne_config_for(M)
+c = [torch.randint(-4096, 4096, (n,), dtype=torch.int32, device='cuda') for _ in range(M)]
+eps = torch.empty(n * M, dtype=torch.int64, device='cuda')
+ne.ne_entangle_aos(cfg, c, eps)
+del c
+perm = torch.empty(n, dtype=torch.int32, device='cuda')
+ne.ne_gen_perm_i32(3, 6, perm)
+v = torch.randint(-4096, 4096, (B,), dtype=torch.int32, device='cuda')
+nb = n // B
+delta = [torch.empty(nb, dtype=torch.int64, device='cuda') for _ in range(M)]
+dout = [torch.empty(nb, dtype=torch.int64, device='cuda') for _ in range(M)]
+if {T} == 1:
+    ws = torch.empty(ne.ne_permute_inner_workspace(cfg, n, B), dtype=torch.uint8, device='cuda')
+    f = lambda: ne.ne_op_permute_inner_check_bucketed(cfg, eps, perm, v, B, 0, delta, dout, ws)
+else:
+    f = lambda: ne.ne_op_permute_inner_check(cfg, v, B, 0, dout, x_aos=eps, perm=perm, n=n, delta_out=delta)
+""",
     "c1_sac": """
 M, n = 3, 1 << 27
 cfg = ne.ne_config_for(M)

@@ -353,14 +353,15 @@ def test_permute_inner_check(O, M, aos, gather):
 
 
 @pytest.mark.parametrize("M,N,B,vlen", [(4, 1024 * 37 + 500, 1024, 1024), (3, 100003, 100, 100), (8, 65536, 1024, 1024),
-                                        (5, 4099, 7, 3), (4, 1 << 20, 1024, 1024), (4, 1, 1024, 1024)])
+                                        (5, 4099, 7, 3), (4, 1 << 20, 1024, 1024), (4, 1, 1024, 1024),
+                                        (4, 70000, 4096, 4096)])
 def test_permute_inner_bucketed(O, M, N, B, vlen):
     """The bucketed scatter-reduce form of the C4 op (ne_op_permute_inner_check_
     bucketed): delta, d_hat, bitmap and diag equal to the oracle's gather +
     blocked inner product + disentangle/check and bit-identical to the
     gather kernel — ragged n (last window and last block partial), block !=
-    vlen, M = 3..8, windows from 16 up (n = 2^20), run twice on the same
-    workspace."""
+    vlen, M = 3..8, windows from 16 up (n = 2^20), blocks above 2048 (the
+    shared sums' 64-bit path), run twice on the same workspace."""
     cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
     c = gen(O, 5, 1, M, N, -2 ** 12, 2 ** 12)
     perm = O.gen_perm(5, 6, N)
@@ -396,6 +397,35 @@ def test_permute_inner_bucketed(O, M, N, B, vlen):
         ne.ne_op_permute_inner_check(cfg, dev(v, torch.int32), B, 2 % M, d2, x_aos=x_aos,
                                      perm=dev(perm, torch.int32), n=N, delta_out=g)
         assert all(torch.equal(a, b) for a, b in zip(g, delta)) and all(torch.equal(a, b) for a, b in zip(d2, d_out))
+
+
+@pytest.mark.parametrize("kind", ["identity", "reverse", "local"])
+def test_permute_inner_bucketed_skewed_perm(O, kind):
+    """Permutations far from random fill some cells past their capacity (a
+    random permutation's mean + 8 sigma): those pairs take the overflow list
+    (global 64-bit reductions after the reduce pass) — identity, reversal and
+    a shuffle inside 4096-position windows, against the oracle."""
+    M, N, B = 4, 1 << 18, 1024
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = gen(O, 8, 1, M, N, -2 ** 12, 2 ** 12)
+    v = O.gen_uniform(8, 7, 0, -2 ** 12, 2 ** 12, B)
+    if kind == "identity":
+        perm = np.arange(N, dtype=np.int32)
+    elif kind == "reverse":
+        perm = np.arange(N - 1, -1, -1, dtype=np.int32)
+    else:
+        perm = np.concatenate([w0 + O.gen_perm(8, 9 + w0 // 4096, 4096) for w0 in range(0, N, 4096)]).astype(np.int32)
+    eps = O.entangle(ocfg, c)
+    nb = N // B
+    odelta = O.op_inner(ocfg, O.op_permute(eps, perm), v, B)
+    od, _, _ = O.disentangle_check(ocfg, odelta, 0)
+    ws = torch.empty(ne.ne_permute_inner_workspace(cfg, N, B), dtype=torch.uint8, device="cuda")
+    delta, d_out = empty_streams(M, nb), empty_streams(M, nb)
+    diag = ne.diag_new()
+    ne.ne_op_permute_inner_check_bucketed(cfg, dev(eps.T.copy(), torch.int64).reshape(-1), dev(perm, torch.int32),
+                                          dev(v, torch.int32), B, 0, delta, d_out, ws, None, diag)
+    assert (to_np(delta) == odelta).all() and (to_np(d_out) == od).all()
+    assert ne.diag_read(diag)["fault_positions"] == 0
 
 
 def test_permute_inner_bucketed_bad_perm_and_fault(O):
