@@ -22,6 +22,7 @@ run c1_w32 --workload c1 --w 32
 run c1_n2e27 --workload c1 --n 134217728
 run c1_w32_n2e27 --workload c1 --w 32 --n 134217728
 run c4 --workload c4
+run c4_gather --workload c4 --c4algo gather
 run c4_soa --workload c4 --layout soa --steps 10
 run c4_w32 --workload c4 --w 32
 run c5 --workload c5 --steps 10

@@ -155,3 +155,36 @@ def test_fuzz_gemm_then_check_and_recover(O, seed):
         rec = empty_streams(M, R * Cc)
         ne.ne_recover(cfg, [None if m == rr else delta[m] for m in range(M)], rr, rec)
         assert (to_np(rec) == plain).all(), rr
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_permute_inner_bucketed(O, seed):
+    """The partitioned scatter-reduce form of the C4 op over seeded n, M,
+    block, vlen and value ranges (wide values take its 64-bit path): delta and
+    d_hat equal to the oracle's gather + blocked inner product + check."""
+    r = np.random.default_rng(7000 + seed)
+    M = int(r.choice([3, 4, 5, 8]))
+    N = int(r.integers(1, 300000))
+    B = int(r.choice([1, 7, 64, 1000, 1024, 3000]))
+    vlen = B if r.integers(0, 2) else int(r.integers(1, 2000))
+    lim = int(r.choice([2 ** 5, 2 ** 12, 2 ** 20]))
+    cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
+    c = np.stack([O.gen_uniform(8000 + seed, 1, m, -lim, lim, N) for m in range(M)])
+    perm = O.gen_perm(8000 + seed, 6, N)
+    v = O.gen_uniform(8000 + seed, 7, 0, -lim, lim, vlen)
+    eps = O.entangle(ocfg, c)
+    nb = (N + B - 1) // B
+    # the oracle's definition, term by term (products mod 2^64 as the int64 sums of the op)
+    xs = np.ascontiguousarray(eps[:, perm].astype(np.int64)).view(np.uint64)
+    vs = np.ascontiguousarray(v[np.arange(N) % vlen].astype(np.int64)).view(np.uint64)
+    prod = xs * vs
+    odelta = np.ascontiguousarray(np.stack([np.add.reduceat(prod[m], np.arange(0, N, B)) for m in range(M)]))
+    odelta = odelta.view(np.int64)
+    od, _, _ = O.disentangle_check(ocfg, odelta, seed % M)
+    ws = torch.empty(ne.ne_permute_inner_workspace(cfg, N, B), dtype=torch.uint8, device="cuda")
+    delta, d_out = empty_streams(M, nb), empty_streams(M, nb)
+    ne.ne_op_permute_inner_check_bucketed(cfg, dev(eps.T.copy(), torch.int64).reshape(-1), dev(perm, torch.int32),
+                                          dev(v, torch.int32), B, seed % M, delta, d_out, ws)
+    torch.cuda.synchronize()
+    assert (to_np(delta) == odelta).all(), (M, N, B, vlen, lim)
+    assert (to_np(d_out) == od).all()
