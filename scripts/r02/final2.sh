@@ -1,5 +1,5 @@
 # r02 final (2): every bench line of the round after the half-tile schedule (profiles/r02_bench_*.json via gpurun_out/r02zz/), then the C3 launch list and ncu captures of the pair GEMM (C3, C3P M = 8)
-O=gpurun_out/r02zz; mkdir -p $O
+O=gpurun_out/r02zz2; mkdir -p $O
 run() { name=$1; shift; timeout 600 python bench.py --configs 0 "$@" > $O/b_$name.json 2> $O/b_$name.err; echo $name rc=$?; }
 timeout 900 python bench.py > $O/b_default.json 2> $O/b_default.err; echo default rc=$?
 run c3 --workload c3
