@@ -1946,6 +1946,7 @@ def run_reference(args):
         W.cfg = _Cfg
     elif args.workload == "c4":
         W.M, W.n, W.B, W.seed, W.layout, W.w, W.b0 = 4, 1 << 28, 1024, 3, args.layout, args.w, 0
+        W.algo = args.c4algo if (args.layout == "aos" and args.w == 64) else "gather"
         W.vr = (1 << 12) if args.w == 64 else 64
 
         class _Cfg:
