@@ -559,6 +559,7 @@ class C4PermInner(Workload):
             scaling = "weak"
             self.partition_note = "replicas (the stream placement is built for the default w = 64 layout)"
         if scaling == "strong" and world > 1:
+            self.algo = "gather"   # the placement gathers per stream (ne_op_permute_inner_stream)
             self._init_placement(rank, world, seed)
             return
         if layout != "aos":
