@@ -486,6 +486,22 @@ ne_status ne_op_permute_inner_check(const ne_config* cfg, ne_cstreams x, const i
  * device memory of at least ne_permute_inner_workspace(cfg, n_total, block)
  * bytes, 16-byte aligned, owned by the caller (NE_EINVAL if smaller). */
 ne_status ne_permute_inner_workspace(const ne_config* cfg, int64_t n_total, int64_t block, size_t* bytes);
+
+/* The plan ne_op_permute_inner_check_bucketed runs for (cfg->M, n_total,
+ * block); host only, no device work.  mode 1 = owned runs (the C4 default:
+ * block a power of two dividing the 4096-position scatter chunk, at least 2
+ * positions per run-index entry): a chunk's slice of a cell is sorted by
+ * (window, output block), a pair is packed in 32 bits ((i mod block) << S |
+ * perm[i] mod 2^S), one 32-bit run-index entry per (cell, block) holds the
+ * run's offset and length, and reduce thread t owns blocks t, t + T, ... of
+ * its range and sums their runs in registers — no atomics; mode 0 = 8-byte
+ * pairs and shared-memory block sums (two 32-bit shared atomics per
+ * product).  Outputs (each nullable): S (2^S entries of x per window), nwin
+ * windows, nrange destination ranges (= reduce CTAs), rb output blocks per
+ * range, cap pair slots per cell, index_bytes (run index; 0 in mode 0).
+ * NE_EINVAL for n_total < 0 or > INT32_MAX or block < 1. */
+ne_status ne_permute_inner_plan(const ne_config* cfg, int64_t n_total, int64_t block, int32_t* mode, int32_t* S,
+                                int32_t* nwin, int32_t* nrange, int64_t* rb, int64_t* cap, int64_t* index_bytes);
 ne_status ne_op_permute_inner_check_bucketed(const ne_config* cfg, const int64_t* x_aos, const int32_t* perm,
                                              int64_t n_total, const int32_t* v, int64_t vlen, int64_t block,
                                              int32_t r, ne_streams delta, ne_streams d_out, uint32_t* bitmap,

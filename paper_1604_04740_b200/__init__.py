@@ -39,7 +39,7 @@ EXPORTS = (
     "ne_op_scale_add_check", "ne_op_conv_check", "ne_op_scale_add_check_w32",
     "ne_entangle_w32", "ne_op_scale_add_w32", "ne_disentangle_check_w32", "ne_recover_w32", "ne_inject_sweep_w32",
     "ne_entangle_aos_w32", "ne_op_permute_inner_check_w32",
-    "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check", "ne_op_permute_inner_stream", "ne_permute_inner_workspace", "ne_op_permute_inner_check_bucketed",
+    "ne_disentangle_check", "ne_recover", "ne_op_permute_inner_check", "ne_op_permute_inner_stream", "ne_permute_inner_workspace", "ne_permute_inner_plan", "ne_op_permute_inner_check_bucketed",
     "ne_inject", "ne_inject_sweep", "ne_gen_uniform_i32", "ne_gen_perm_i32",
     "ne_abft_encode", "ne_abft_encode_limbs", "ne_abft_encode_conv", "ne_op_conv_limbs_plain", "ne_to_limbs", "ne_abft_check", "ne_abft_recover",
 )
@@ -133,6 +133,8 @@ _SIGS = {
     "ne_disentangle_check": [_PCFG, Streams, _I64, _I32, Streams, _VP, _VP, _VP],
     "ne_recover": [_PCFG, Streams, _I64, _I32, Streams, _VP],
     "ne_permute_inner_workspace": [_PCFG, _I64, _I64, C.POINTER(_SZ)],
+    "ne_permute_inner_plan": [_PCFG, _I64, _I64, C.POINTER(_I32), C.POINTER(_I32), C.POINTER(_I32),
+                              C.POINTER(_I32), C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64)],
     "ne_op_permute_inner_check_bucketed": [_PCFG, _VP, _VP, _I64, _VP, _I64, _I64, _I32, Streams, Streams, _VP, _VP,
                                            _VP, _SZ, _VP],
     "ne_op_permute_inner_check": [_PCFG, Streams, _VP, _I32, _VP, _I64, _VP, _I64, _I64, _I32,
@@ -553,6 +555,17 @@ def ne_permute_inner_workspace(cfg: Config, n: int, block: int) -> int:
     b = _SZ()
     _call("ne_permute_inner_workspace", C.byref(cfg), n, block, C.byref(b))
     return b.value
+
+
+def ne_permute_inner_plan(cfg: Config, n: int, block: int) -> dict:
+    """The plan (mode 1 = owned runs, 0 = shared-memory block sums) and geometry
+    ne_op_permute_inner_check_bucketed runs for this (M, n, block); host only."""
+    mode, S, nwin, nrange = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+    rb, cap, ib = C.c_int64(), C.c_int64(), C.c_int64()
+    _call("ne_permute_inner_plan", C.byref(cfg), n, block, C.byref(mode), C.byref(S), C.byref(nwin),
+          C.byref(nrange), C.byref(rb), C.byref(cap), C.byref(ib))
+    return {"mode": mode.value, "S": S.value, "nwin": nwin.value, "nrange": nrange.value, "rb": rb.value,
+            "cap": cap.value, "index_bytes": ib.value}
 
 
 def ne_op_permute_inner_check_bucketed(cfg: Config, x_aos: torch.Tensor, perm: torch.Tensor, v: torch.Tensor,

@@ -264,3 +264,29 @@ def test_gemm_pair_schedule(L):
         ne.ne_gemm_pair_schedule(10, 0)
     with pytest.raises(ne.NeError):
         ne.ne_gemm_pair_halves(3)
+
+
+def test_permute_inner_plan():
+    """ne_permute_inner_plan (host only): the C4 config (M = 4, n = 2^28,
+    blocks of 1024) runs the owned-run mode with 64 MB windows and one reduce
+    CTA per SM; blocks that do not tile the 4096-position scatter chunk take
+    the shared-atomic mode; the workspace holds the 32-bit pairs, the run
+    index and the overflow list."""
+    cfg = ne.ne_config_for(4)
+    p = ne.ne_permute_inner_plan(cfg, 1 << 28, 1024)
+    assert p["mode"] == 1 and p["S"] == 21 and p["nwin"] == 128
+    assert p["nrange"] <= 148 and p["rb"] % 4 == 0 and p["rb"] * p["nrange"] >= (1 << 18)
+    cells = p["nwin"] * p["nrange"]
+    assert p["index_bytes"] == cells * p["rb"] * 4
+    assert cells * p["cap"] >= 1 << 28 and p["cap"] < 65536
+    ws = ne.ne_permute_inner_workspace(cfg, 1 << 28, 1024)
+    assert ws >= cells * p["cap"] * 4 + p["index_bytes"] + (1 << 28) * 8
+    for M, n, B in [(4, 100003, 100), (5, 4099, 7), (4, 1 << 20, 3000)]:
+        q = ne.ne_permute_inner_plan(ne.ne_config_for(M), n, B)
+        assert q["mode"] == 0 and q["index_bytes"] == 0
+    for M, n, B in [(8, 65536, 1024), (4, 70000, 4096), (3, 1, 1024), (8, 1 << 28, 1024)]:
+        assert ne.ne_permute_inner_plan(ne.ne_config_for(M), n, B)["mode"] == 1
+    assert ne.ne_permute_inner_plan(ne.ne_config_for(8), 1 << 28, 1024)["nrange"] <= 148
+    for n, B in [(-1, 1024), (1 << 31, 1024), (10, 0)]:
+        with pytest.raises(ne.NeError):
+            ne.ne_permute_inner_plan(cfg, n, B)
