@@ -726,15 +726,21 @@ class C4PermInner(Workload):
         gathered position."""
         if dom != "permute_inner_check" or self.layout != "aos" or getattr(self, "placement", False):
             return None
-        if self.algo == "bucket":   # what the scatter-reduce moves: perm 4 + pairs 8 + 8 + eps 32 B per position
-            per = 52
+        if self.algo == "bucket":   # what the scatter-reduce moves per position (ne_permute_inner_plan)
+            plan = self.ne.ne_permute_inner_plan(self.cfg, self.n, self.B)
+            if plan["mode"] == 1:   # perm 4 + 32-bit pairs written and read 4 + 4 + eps 32 + run index written and read
+                per = 44 + 2 * plan["index_bytes"] / self.n
+                how = ("owned-run scatter-reduce: perm read, 32-bit pairs written and read, the run index written "
+                       "and read, every eps entry read once from its window (L2-resident while its cells are reduced)")
+            else:                   # perm 4 + 8-byte pairs written and read 8 + 8 + eps 32
+                per = 52
+                how = ("bucketed scatter-reduce: perm read, (i, perm[i]) pairs written and read, every eps entry "
+                       "read once from its window (L2-resident while its bucket is consumed)")
             gb = self.n * per / 1e9
             ach = gb / (ms / 1e3)
-            return {"bytes_per_position": per, "bytes_per_launch_GB": round(gb, 3), "achieved": round(ach, 1),
+            return {"bytes_per_position": round(per, 3), "bytes_per_launch_GB": round(gb, 3), "achieved": round(ach, 1),
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ach / peaks["hbm_gbs"], 4),
-                    "floor_ms": round(gb / peaks["hbm_gbs"] * 1e3, 3),
-                    "evidence": "bucketed scatter-reduce: perm read, (i, perm[i]) pairs written and read, every "
-                                "eps entry read once from its window (L2-resident while its bucket is consumed)"}
+                    "floor_ms": round(gb / peaks["hbm_gbs"] * 1e3, 3), "plan": plan, "evidence": how}
         per = 128 + 4
         gb = self.n * per / 1e9
         ach = gb / (ms / 1e3)

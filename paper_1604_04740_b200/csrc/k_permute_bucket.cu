@@ -26,6 +26,11 @@
 // Measured (profiles/r02_c4_bucket.md, r02c_ncu_summary.md): C4 stage 5.20 ms
 // vs 5.80 ms for the gather kernel; every line of x fetched once (10.8 GB for
 // pairs + x against 35.2 GB); the reduce bound by its shared atomics.
+// Owned-run mode (mode 1 of ne_permute_inner_plan, the C4 default; below
+// k_pb_overflow): chunk slices sorted by (window, block) so each block's
+// pairs form one run per cell, 32-bit pairs, a run index per (cell, block),
+// and a reduce without atomics — each block owned by one thread, cells staged
+// in shared memory by TMA, x gathered through L2 only: C4 stage 3.9 ms.
 // Every sum is an int64 sum mod 2^64, so delta is bit-identical to the gather
 // order (wrap-free for certified results).
 #include <cuda_runtime.h>
@@ -500,94 +505,6 @@ __device__ __forceinline__ void pb_load_x(const int64_t* xe, int M, uint64_t* c)
   }
 }
 
-// reduce thread t owns blocks q = t + 2 j T and q + T of its range (two runs
-// per window walked together: their loads are independent); block sums live
-// in shared memory, touched by their owner only
-template <int MT>
-__global__ void __launch_bounds__(kPoMaxThreads, 1)
-k_pb_reduce_own_direct(const int64_t* __restrict__ x_aos, int M_rt, const uint32_t* __restrict__ pairs,
-                const uint32_t* __restrict__ index, int64_t cap, unsigned* __restrict__ done, int nwin, int nrange,
-                int64_t rb, int32_t block, int S, const int32_t* __restrict__ v, int32_t vlen, int64_t nb,
-                int lockstep, ne_streams delta) {
-  constexpr int MA = MT > 0 ? MT : 8;  // M <= 8 (host check)
-  constexpr int UN = MA <= 4 ? 4 : 2;  // pairs in flight per thread
-  const int M = MT > 0 ? MT : M_rt;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* acc = reinterpret_cast<uint64_t*>(smem);  // [rb][M]
-  const int d = blockIdx.x;
-  const int T = blockDim.x;
-  const int64_t b0 = (int64_t)d * rb;
-  const int rbl = (int)min(rb, nb - b0);
-  const uint32_t smask = (uint32_t)((1ull << S) - 1);
-  for (int q = threadIdx.x; q < rbl; q += T)
-    for (int m = 0; m < M; ++m) acc[(int64_t)q * M + m] = 0;
-  for (int w = 0; w < nwin; ++w) {
-    if (lockstep && w >= 2) {  // as k_pb_reduce: at most ~3 windows of x in flight
-      if (threadIdx.x == 0) {
-        for (int spin = 0; spin < (1 << 20) && *(volatile unsigned*)(done + w - 2) < (unsigned)nrange; ++spin)
-          __nanosleep(100);
-      }
-      __syncthreads();
-    }
-    const int64_t cell = (int64_t)w * nrange + d;
-    const uint32_t* pc = pairs + cell * cap;
-    const int64_t* xw = x_aos + ((int64_t)w << S) * M;
-    for (int q = threadIdx.x; q < rbl; q += 2 * T) {
-      const int q1 = q + T;
-      const uint32_t e0 = __ldcs(index + cell * rb + q);
-      const uint32_t e1 = q1 < rbl ? __ldcs(index + cell * rb + q1) : 0u;
-      const int c0 = (int)(e0 >> 16), c1 = (int)(e1 >> 16);
-      const uint32_t* p0 = pc + (e0 & 0xFFFFu);
-      const uint32_t* p1 = pc + (e1 & 0xFFFFu);
-      // first v index of each block: (block start) mod vlen
-      const uint32_t vb0 = (uint32_t)(((b0 + q) * block) % vlen), vb1 = (uint32_t)(((b0 + q1) * block) % vlen);
-      uint64_t s0[MA], s1[MA];
-#pragma unroll
-      for (int m = 0; m < MA; ++m) s0[m] = s1[m] = 0;
-      const int ct = c0 + c1;  // the two runs as one list: element k < c0 is p0[k], else p1[k - c0]
-      for (int k0 = 0; k0 < ct; k0 += UN) {
-        uint32_t pr[UN];
-#pragma unroll
-        for (int u = 0; u < UN; ++u) {
-          const int k = k0 + u;
-          pr[u] = k < ct ? __ldcs(k < c0 ? p0 + k : p1 + (k - c0)) : 0u;
-        }
-        uint64_t c[UN][MA];
-        uint64_t wg[UN];
-#pragma unroll
-        for (int u = 0; u < UN; ++u) {
-          const int k = k0 + u;
-          if (k >= ct) continue;
-          uint32_t vi = (k < c0 ? vb0 : vb1) + (pr[u] >> S);
-          if (vi >= (uint32_t)vlen) vi %= (uint32_t)vlen;
-          wg[u] = (uint64_t)(int64_t)__ldg(v + vi);
-          pb_load_x<MT>(xw + (int64_t)(pr[u] & smask) * M, M, c[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < UN; ++u) {
-          const int k = k0 + u;
-          if (k >= ct) continue;
-          const bool first = k < c0;
-#pragma unroll
-          for (int m = 0; m < MA; ++m) {
-            if (MT == 0 && m >= M) break;
-            const uint64_t p = c[u][m] * wg[u];
-            if (first) s0[m] += p; else s1[m] += p;
-          }
-        }
-      }
-      if (c0)
-        for (int m = 0; m < M; ++m) acc[(int64_t)q * M + m] += s0[m];
-      if (c1)
-        for (int m = 0; m < M; ++m) acc[(int64_t)q1 * M + m] += s1[m];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(done + w, 1u);
-  }
-  for (int q = threadIdx.x; q < rbl; q += T)
-    for (int m = 0; m < M; ++m) delta.s[m][b0 + q] = (int64_t)acc[(int64_t)q * M + m];
-}
-
 // 1-D bulk copy global -> shared (TMA), completing on an mbarrier
 __device__ __forceinline__ void po_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -666,7 +583,6 @@ k_pb_reduce_own(const int64_t* __restrict__ x_aos, int M_rt, const uint32_t* __r
     const uint32_t* pc = stg + (w & 1) * stride;
     const uint32_t* ic = pc + cap;
     const int64_t* xw = x_aos + ((int64_t)w << S) * M;
-#ifndef NE_PO_FLAT
     for (int q = threadIdx.x; q < rbl; q += R * T) {
       int cum[R];
       int po[R];
@@ -728,64 +644,6 @@ k_pb_reduce_own(const int64_t* __restrict__ x_aos, int M_rt, const uint32_t* __r
           for (int m = 0; m < M; ++m) acc[(int64_t)qj * M + m] += s[j][m];
       }
     }
-#else
-    // the thread's runs (blocks q = t, t + T, ...) as one list, UN elements
-    // in flight across run boundaries; a run's sum stays in registers until
-    // the next element belongs to another block
-    {
-      int q = threadIdx.x;
-      uint32_t e = q < rbl ? ic[q] : 0u;
-      int cj = (int)(e >> 16), kk = 0;
-      const uint32_t* pj = pc + (e & 0xFFFFu);
-      int cur = q;
-      uint64_t s[MA];
-#pragma unroll
-      for (int m = 0; m < MA; ++m) s[m] = 0;
-      while (q < rbl) {
-        uint32_t pr[UN];
-        int qq[UN];
-#pragma unroll
-        for (int u = 0; u < UN; ++u) {
-          while (kk == cj && q < rbl) {  // next owned block with a non-empty run
-            q += T;
-            e = q < rbl ? ic[q] : 0u;
-            cj = (int)(e >> 16);
-            kk = 0;
-            pj = pc + (e & 0xFFFFu);
-          }
-          qq[u] = q < rbl ? q : -1;
-          pr[u] = q < rbl ? pj[kk++] : 0u;
-        }
-        uint64_t c[UN][MA];
-        uint64_t wg[UN];
-#pragma unroll
-        for (int u = 0; u < UN; ++u) {
-          if (qq[u] < 0) continue;
-          uint32_t vi = vbs[qq[u]] + (pr[u] >> S);
-          if (vi >= (uint32_t)vlen) vi %= (uint32_t)vlen;
-          wg[u] = (uint64_t)(int64_t)__ldg(v + vi);
-          pb_load_x<MT>(xw + (int64_t)(pr[u] & smask) * M, M, c[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < UN; ++u) {
-          if (qq[u] < 0) continue;
-          if (qq[u] != cur) {
-            for (int m = 0; m < M; ++m) acc[(int64_t)cur * M + m] += s[m];
-#pragma unroll
-            for (int m = 0; m < MA; ++m) s[m] = 0;
-            cur = qq[u];
-          }
-#pragma unroll
-          for (int m = 0; m < MA; ++m) {
-            if (MT == 0 && m >= M) break;
-            s[m] += c[u][m] * wg[u];
-          }
-        }
-      }
-      if (cur < rbl)
-        for (int m = 0; m < M; ++m) acc[(int64_t)cur * M + m] += s[m];
-    }
-#endif
     __syncthreads();  // buffer w & 1 consumed
     if (threadIdx.x == 0) {
       atomicAdd(done + w, 1u);
@@ -834,21 +692,12 @@ static ne_status pb_run_own(const ne_config* cfg, const PbGeo& g, int M, const i
     per_sm = 0;
   }
   const int lockstep = g.nrange <= (int64_t)per_sm * num_sms() ? 1 : 0;
-#ifdef NE_PO_DIRECT  // A/B: the unstaged reduce (pairs and index read from global memory)
-#define NE_PO_RED(MV)                                                                                            \
-  cudaFuncSetAttribute(k_pb_reduce_own_direct<MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);       \
-  k_pb_reduce_own_direct<MV><<<g.nrange, g.rthreads, (size_t)g.rb * M * 8, s>>>(                                \
-      x_aos, M, pairs, index, g.cap, done, g.nwin, g.nrange, g.rb, (int32_t)block, g.S, v, (int32_t)vlen, nb,    \
-      lockstep, delta);                                                                                          \
-  k_pb_overflow<MV><<<num_sms(), 256, 0, s>>>(x_aos, M, ov, ovn, (int32_t)block, v, (int32_t)vlen, delta)
-#else
 #define NE_PO_RED(MV)                                                                                            \
   cudaFuncSetAttribute(k_pb_reduce_own<MV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);              \
   k_pb_reduce_own<MV><<<g.nrange, g.rthreads, rsm, s>>>(x_aos, M, pairs, index, fill, g.cap, done, g.nwin,       \
                                                         g.nrange, g.rb, (int32_t)block, g.S, v, (int32_t)vlen,   \
                                                         nb, lockstep, n_total, delta);                           \
   k_pb_overflow<MV><<<num_sms(), 256, 0, s>>>(x_aos, M, ov, ovn, (int32_t)block, v, (int32_t)vlen, delta)
-#endif
   switch (M) {
     case 4: NE_PO_RED(4); break;
     case 3: NE_PO_RED(3); break;

@@ -61,10 +61,11 @@ def launches(path):
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     agg = collections.OrderedDict()
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
-            continue
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
+            continue   # launch lists with DRAM bytes as well: the durations only
         name = re.sub(r"\(.*", "", r[ki])
         agg.setdefault(name, []).append(float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1))
     return agg
