@@ -66,6 +66,41 @@ class Workload:
     def stages(self, i):  # -> list of (stage_name, callable)
         raise NotImplementedError
 
+    # independent stages run side by side inside the timed step: {side stage: the stage it runs beside}
+    # (the side stage on a second stream, forked before and joined after the main one; the stage
+    # timings keep every stage on its own)
+    concurrent: dict = {}
+    overlap = True
+
+    def run_step(self, i):
+        st = self.stages(i)
+        fns = dict(st)
+        par = self.concurrent if self.overlap else {}
+        beside = {}
+        for side, mains in par.items():
+            main = next((m for m in (mains if isinstance(mains, tuple) else (mains,)) if m in fns), None)
+            if side in fns and main is not None:
+                beside[main] = side
+        sides = set(beside.values())
+        torch = self.torch
+        for nm, f in st:
+            if nm in sides:
+                continue
+            if nm not in beside:
+                f()
+                continue
+            cur = torch.cuda.current_stream()
+            if getattr(self, "_side", None) is None:
+                self._side = torch.cuda.Stream()
+            fork, join = torch.cuda.Event(), torch.cuda.Event()
+            fork.record(cur)
+            self._side.wait_event(fork)
+            with torch.cuda.stream(self._side):
+                fns[beside[nm]]()
+            f()
+            join.record(self._side)
+            cur.wait_event(join)
+
     # ---- end to end (pinned host inputs -> device -> result -> pinned host),
     # pipelined across steps: step i's H2D, compute and D2H run on three CUDA
     # streams over two device buffer slots, so the copies of one step overlap
@@ -102,8 +137,7 @@ class Workload:
         for i in range(steps):
             for d, h in zip(dev_in, h_in):
                 d.copy_(h, non_blocking=True)
-            for _, f in self.stages(i):
-                f()
+            self.run_step(i)
             for h, d in zip(h_out, dev_out):
                 h.copy_(d, non_blocking=True)
         t1.record()
@@ -146,8 +180,7 @@ class Workload:
                     s_cmp.wait_event(ev_out[i - nslots])  # D2H i-nslots done reading slot k's results
                 for n in names:
                     setattr(self, n, sl[n])
-                for _, f in self.stages(i):
-                    f()
+                self.run_step(i)
                 ev_cmp[i].record(s_cmp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(ev_cmp[i])
@@ -217,6 +250,8 @@ class Workload:
 
 
 class C3Gemm(Workload):
+    # B's digit planes do not depend on A's entangle (or ABFT's encode), nor the fail-stop recovery on the check
+    concurrent = {"prep_b": ("entangle", "encode"), "recover": "check"}
     """configs[2]: M=3 entangled GEMM, A_m 4096x4096 int32 in [-64,64), shared B
     4096x4096 in [-64,64), K = 4096, int64 results; tcgen05 int8 limbs (L = 4)."""
 
@@ -437,7 +472,8 @@ class C3Gemm(Workload):
             ones 0) + prep_B + the same tcgen05 GEMM kernel and plan
           plain, native:      int32 -> one int8 plane + prep_B + the 1-digit
             tcgen05 GEMM (the narrowest exact plain form)
-        and the fail-stop cost (recovery alone) separately.  Also cuBLASLt's
+        and the fail-stop cost (recovery alone) separately; both sides strictly in
+        order (no side stream, unlike the timed step).  Also cuBLASLt's
         int8 x int8 -> int32 GEMM on the same multiply-adds (torch._int_mm) as
         a library context number (int32 output, no int64 recombination)."""
         torch, ne = self.torch, self.ne
@@ -843,6 +879,8 @@ class C4PermInner(Workload):
 
 
 class C2Conv(Workload):
+    # the Toeplitz tap matrix does not depend on the entangle (or ABFT's encode), nor the recovery on the check
+    concurrent = {"prep_g": ("entangle", "encode"), "recover": "check"}
     """configs[1]: M=3 streams of 65536 int32 U[-128,128), circular convolution
     with a shared 64-tap kernel U[-128,128), entangled int64.  algo "tc": the
     Toeplitz GEMM on tcgen05 over extended digit planes (k_conv_tc.cu);
@@ -1652,6 +1690,7 @@ def run_ours(args, rank, world, local_rank):
     ne.lib()
     torch.cuda.set_device(local_rank)
     W = make_workload(args, rank, world)
+    W.overlap = bool(args.overlap)
     torch.cuda.synchronize()
     # a step with a collective inside (C2 halo, C4 all_gather at N > 1) is
     # timed as eager launches: the collective is not captured into the graph
@@ -1699,8 +1738,7 @@ def run_ours(args, rank, world, local_rank):
         for i in range(nrot):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                for _, f in W.stages(i):
-                    f()
+                W.run_step(i)
             graphs.append(g)
         for i in range(args.warmup):
             graphs[i % nrot].replay()
@@ -1850,8 +1888,11 @@ def run_ours(args, rank, world, local_rank):
                           if use_graph else "eager launches, CUDA events between stages"),
         "eager_stages_ms": {k: round(v, 4) for k, v in eager_stage_ms.items()},
         "stages_event_pair_ms": None if ev_overhead is None else round(ev_overhead, 4),
-        "launch": "CUDA graph replay (one graph per recovered stream r)" if use_graph else
-                  ("eager (the step contains a collective)" if args.graph else "eager"),
+        "launch": ("CUDA graph replay (one graph per recovered stream r)" if use_graph else
+                   ("eager (the step contains a collective)" if args.graph else "eager")) +
+                  ("; side by side on a second stream: " + ", ".join(
+                      f"{s} with {'/'.join(m) if isinstance(m, tuple) else m}" for s, m in W.concurrent.items())
+                   if W.overlap and W.concurrent else ""),
         "eager_ms_per_step": round(eager_ms, 4),
         "e2e": {"value": round(W.job_work() / (e2e_ms / 1e3), 3), "unit": W.metric_unit,
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -2120,6 +2161,9 @@ def main():
                     help="c5: position-major exchange fused into the GEMM epilogue (symmetric memory) or an NCCL "
                          "all_to_all after it; auto = fused when N > 1")
     ap.add_argument("--graph", type=int, default=1, help="time CUDA-graph replays of the step (default) or eager")
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="run independent stages of the step side by side on a second stream (C3: prep_b with "
+                         "entangle, recover with check); 0 = strictly in order")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="N > 1: partition the stated problem over the ranks (SURVEY 8(e): C1 position ranges, C2 "
                          "ranges + halo, C3 row ranges, C4 stream placement; default) or run one independent replica "
