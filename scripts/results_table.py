@@ -8,7 +8,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LINES = [
-    ("c3", "C3 (default)"), ("c3_abft", "C3 `--scheme abft`"), ("c3_base256", "C3 `--limbs base256`"),
+    ("c3", "C3 (default)"), ("c3_inorder", "C3 `--overlap 0` (stages strictly in order)"), ("c3_abft", "C3 `--scheme abft`"), ("c3_base256", "C3 `--limbs base256`"),
     ("c3_fused", "C3 `--fuse 1`"), ("c3_imad", "C3 `--algo imad`"),
     ("c3p_3_2000", "C3P M = 3, N = 2000 (paper shape)"), ("c3p_8_2000", "C3P M = 8, N = 2000 (paper shape)"),
     ("c3p_3_200", "C3P M = 3, N = 200 (paper shape)"), ("c3p_8_200", "C3P M = 8, N = 200 (paper shape)"),
@@ -18,7 +18,7 @@ LINES = [
     ("c2p_8_4500", "C2P M = 8, T = 4500"), ("c2p_3_4500", "C2P M = 3, T = 4500"),
     ("c2p_8_4500_abft", "C2P M = 8, T = 4500 `--scheme abft`"), ("c2p_3_4500_abft", "C2P M = 3, T = 4500 `--scheme abft`"),
     ("c2p_8_1000", "C2P M = 8, T = 1000"), ("c2p_3_100", "C2P M = 3, T = 100"),
-    ("c2p_direct", "C2P direct, M = 8, T = 4500"), ("c4", "C4 (partitioned scatter-reduce)"), ("c4_gather", "C4 `--c4algo gather`"), ("c4_soa", "C4 `--layout soa` (gather)"), ("c4_w32", "C4 shape, `--w 32` (7-bit inputs)"),
+    ("c2p_direct", "C2P direct, M = 8, T = 4500"), ("c4", "C4 (partitioned scatter-reduce, owned runs)"), ("c4_gather", "C4 `--c4algo gather`"), ("c4_soa", "C4 `--layout soa` (gather)"), ("c4_w32", "C4 shape, `--w 32` (7-bit inputs)"),
     ("c5", "C5 (N = 1 emulation)"), ("c5_fused", "C5 `--exchange fused` (N = 1)"),
     ("c3_imad64", "C3 `--algo imad64`"), ("c2p_3_1000", "C2P M = 3, T = 1000"),
     ("c3_a1023", "C3 shape, A in U[-1023, 1023) (split plan, 4 planes)"),
