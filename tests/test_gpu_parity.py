@@ -1087,7 +1087,10 @@ def test_c3_full_size_sampled(O, plan):
 
 def test_c4_full_size_sampled(O):
     """C4 at full size (M = 4, 2^28 positions): sampled output blocks vs the
-    oracle recomputed from the generator at the permuted positions."""
+    oracle recomputed from the generator at the permuted positions, for the
+    fused gather kernel and for the op bench.py times (the partitioned
+    scatter-reduce in its owned-run mode), whose delta, d_hat and bitmap
+    equal the gather's in full."""
     M, n, Bk = 4, 1 << 28, 1024
     cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
     c = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(M)]
@@ -1111,6 +1114,17 @@ def test_c4_full_size_sampled(O):
     d = ne.diag_read(diag)
     assert d["range_violations"] == 0 and d["fault_positions"] == 0 and int(bm.abs().sum()) == 0
     assert all(torch.equal(a, b) for a, b in zip(dout, drec))
+    # the timed form: partitioned scatter-reduce, owned runs (mode 1), the bench's r = 0
+    assert ne.ne_permute_inner_plan(cfg, n, Bk)["mode"] == 1
+    ws = torch.empty(ne.ne_permute_inner_workspace(cfg, n, Bk), dtype=torch.uint8, device="cuda")
+    delta2, dout2 = empty_streams(M, nb), empty_streams(M, nb)
+    bm2 = torch.full((nb // 32,), -1, dtype=torch.int32, device="cuda")
+    diag2 = ne.diag_new()
+    ne.ne_op_permute_inner_check_bucketed(cfg, eps, perm, v, Bk, 0, delta2, dout2, ws, bm2, diag2)
+    del ws
+    d2 = ne.diag_read(diag2)
+    assert d2["range_violations"] == 0 and d2["fault_positions"] == 0 and int(bm2.abs().sum()) == 0
+    assert all(torch.equal(a, b) for a, b in zip(delta, delta2)) and all(torch.equal(a, b) for a, b in zip(dout, dout2))
     vh = O.gen_uniform(3, 7, 0, -(1 << 12), 1 << 12, Bk)
     D, DH = to_np(delta), to_np(dout)
     for b in (0, 1, 12345, nb // 2 + 7, nb - 1):
