@@ -48,8 +48,11 @@ static int64_t conv_plane_len(int64_t n, int64_t taps, int W) {
 // (stream, quad) (20.5 / 11.3).  The kernel costs ~6 us fixed + ~1.5 us per
 // stream: a launch-latency-dominated pass of 6 MB per stream.
 // The range assertion (a0) counts every position once: t in [s0, s0 + N).
+#ifndef NE_CP_MINB  // >= 4 CTAs per SM (<= 64 registers): r02 A/B (scripts/r02/z41.sh), M = 8 / 3:
+#define NE_CP_MINB 4  // 1 (76 regs) 18.2 / 11.1 us, 4 (58) 17.6 / 10.0, 6 (40, spills) 18.6 / 11.5, 8 (32) 20.1 / 12.0
+#endif
 template <int MT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, NE_CP_MINB)
 k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64_t hi, int64_t n, int64_t s0,
                        int64_t s0mod, int64_t plane_len, int L, int b, int8_t* __restrict__ planes,
                        ne_diag* __restrict__ diag) {
