@@ -218,8 +218,11 @@ __device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
 
+#ifndef NE_EP_MINB  // r02 A/B (scripts/r02/z42.sh, L2 flushed): 1 (64 regs) 57.3 us, 5 (48, spills) 61.4, 6 (40) 67.6
+#define NE_EP_MINB 1
+#endif
 template <int MT, bool V256>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, NE_EP_MINB)
 k_entangle_pair(const __grid_constant__ ne_cstreams32 c, int M_rt, int b, int64_t hi, int64_t n,
                 int8_t* __restrict__ planes, ne_diag* __restrict__ diag) {
   constexpr int MA = MT > 0 ? MT : NE_MAX_M;
