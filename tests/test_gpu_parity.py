@@ -354,14 +354,19 @@ def test_permute_inner_check(O, M, aos, gather):
 
 @pytest.mark.parametrize("M,N,B,vlen", [(4, 1024 * 37 + 500, 1024, 1024), (3, 100003, 100, 100), (8, 65536, 1024, 1024),
                                         (5, 4099, 7, 3), (4, 1 << 20, 1024, 1024), (4, 1, 1024, 1024),
-                                        (4, 70000, 4096, 4096)])
+                                        (4, 70000, 4096, 4096), (4, 300001, 2048, 2048), (3, (1 << 19) + 77, 512, 300),
+                                        (8, 200003, 256, 256), (5, 1 << 21, 1024, 1000),
+                                        (4, 100000, 3000, 3000)])
 def test_permute_inner_bucketed(O, M, N, B, vlen):
     """The bucketed scatter-reduce form of the C4 op (ne_op_permute_inner_check_
     bucketed): delta, d_hat, bitmap and diag equal to the oracle's gather +
     blocked inner product + disentangle/check and bit-identical to the
     gather kernel — ragged n (last window and last block partial), block !=
-    vlen, M = 3..8, windows from 16 up (n = 2^20), blocks above 2048 (the
-    shared sums' 64-bit path), run twice on the same workspace."""
+    vlen, M = 3..8, windows from 16 up (n = 2^21), a block above 2048 in
+    the shared-sum plan (3000: its 64-bit path), both plans (owned runs for power-of-two
+    blocks 256-4096 — one, two and four blocks per scatter chunk, the
+    16-byte and the scalar run-index stores — shared-memory sums for
+    blocks 7, 100 and 3000), run twice on the same workspace."""
     cfg, ocfg = ne.ne_config_for(M), O.config_for(M, 64)
     c = gen(O, 5, 1, M, N, -2 ** 12, 2 ** 12)
     perm = O.gen_perm(5, 6, N)
