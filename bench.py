@@ -1897,7 +1897,10 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": round(W.job_work() / (e2e_ms / 1e3), 3), "unit": W.metric_unit,
                 "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "pipelined": "H2D / compute / D2H on three streams, two buffer slots" if W.E2E_PIPELINE
-                else "no (one stream; the step is smaller than the enqueue cost of a pipeline)"},
+                else "no (one stream; the step is smaller than the enqueue cost of a pipeline)",
+                # what the copies alone ask of the host link per step (PCIe; H2D and D2H run concurrently
+                # when pipelined): the e2e number is link-bound when these approach the link's rate
+                "link_GBs": {"h2d": round(h2d / 1e9 / (e2e_ms / 1e3), 2), "d2h": round(d2h / 1e9 / (e2e_ms / 1e3), 2)}},
         "gpu_launches": W.launches_per_step * args.steps,
         "clocks": clk.summary(),
         "correctness": {"range_violations": dg["range_violations"], "flagged_positions": dg["fault_positions"],
