@@ -1859,6 +1859,7 @@ def run_ours(args, rank, world, local_rank):
     tr = load_traffic().get(f"{W.name}:{dom}")
     traffic = tr["GB"] if tr else None
     xr = W.extra_roofline(dom, stage_ms[dom], peaks) if hasattr(W, "extra_roofline") else None
+    srf = step_roofline(W, list(stage_ms), info, peaks, ms_per_step)
     line = {
         "metric": METRIC,
         "value": round(value, 3),
@@ -1882,6 +1883,7 @@ def run_ours(args, rank, world, local_rank):
                                      "(profiles/traffic.json)" if tr else None,
                      "algorithmic_per_launch": f"{amount:.4g} {unit}", "peak_source": peak_note,
                      **({"random_access_floor": xr} if xr else {})},
+        "step_roofline": srf,
         "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "stages_timing": ("device time of each stage inside the replayed step graph (one event-record pair around "
                           "that stage per capture, median)"
@@ -2099,6 +2101,46 @@ def compact(line):
     if "clocks" in line:
         out["clocks"] = line["clocks"]
     return out
+
+
+def step_roofline(W, names, info, peaks, ms_per_step):
+    """The whole step against the sum of its stages' own rooflines: each stage's
+    algorithmic amount (W.stage_info) at its bound's peak; stages the timed step
+    runs side by side (W.concurrent) share the HBM when both are HBM-bound (their
+    bytes add) and otherwise overlap (the longer counts).  frac = floor / step."""
+    rate = {"hbm": peaks["hbm_gbs"], "tensor": peaks["bf16_tflops"] * 2.0,
+            "alu": 32 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12}
+    par = W.concurrent if W.overlap else {}
+    side_of = {}
+    for side, mains in par.items():
+        main = next((m for m in (mains if isinstance(mains, tuple) else (mains,)) if m in names), None)
+        if side in names and main is not None:
+            side_of[main] = side
+    sides = set(side_of.values())
+    floor, per, missing = 0.0, {}, []
+    for nm in names:
+        if nm in sides:
+            continue
+        group = [nm] + ([side_of[nm]] if nm in side_of else [])
+        parts = []
+        for g in group:
+            if g not in info or info[g][0] not in rate:
+                missing.append(g)
+                continue
+            b, amount, _ = info[g]
+            parts.append((b, amount, amount / rate[b] * 1e3))
+            per[g] = round(amount / rate[b] * 1e3, 4)
+        if not parts:
+            continue
+        if len(parts) > 1 and all(b == "hbm" for b, _, _ in parts):
+            floor += sum(a for _, a, _ in parts) / rate["hbm"] * 1e3
+        else:
+            floor += max(t for _, _, t in parts)
+    return {"floor_ms": round(floor, 4), "frac": round(floor / ms_per_step, 4) if ms_per_step else None,
+            "stage_floor_ms": per, "unaccounted": missing,
+            "basis": "each stage's algorithmic bytes / ops at its roofline's peak (HBM copy bandwidth, int8 tensor, "
+                     "IMAD.WIDE pipe); stages run side by side share the HBM when both are HBM-bound"}
+
 
 
 def run_configs(args, rank, world, local_rank):

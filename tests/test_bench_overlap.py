@@ -92,3 +92,21 @@ def test_in_order_without_overlap_or_partner():
     W, log = _workload(bench.C2Conv.concurrent, ["entangle", "conv_check", "recover"])
     W.run_step(0)
     assert _runs(log) == [("main", "entangle"), ("main", "conv_check"), ("main", "recover")]
+
+
+def test_step_roofline_sums_stage_floors():
+    """step_roofline: C3's stages at their own peaks, the side-by-side HBM
+    pairs (entangle + prep_b, check + recover) sharing the HBM."""
+    W = bench.Workload()
+    W.concurrent, W.overlap = bench.C3Gemm.concurrent, True
+    info = {"entangle": ("hbm", 0.302, "GB"), "prep_b": ("hbm", 0.084, "GB"), "gemm": ("tensor", 0.8246, "TOP"),
+            "check": ("hbm", 0.807, "GB"), "recover": ("hbm", 0.671, "GB")}
+    peaks = {"hbm_gbs": 6544.0, "bf16_tflops": 1623.3}
+    names = ["entangle", "prep_b", "gemm", "check", "recover"]
+    r = bench.step_roofline(W, names, info, peaks, 0.565)
+    want = (0.302 + 0.084) / 6544 * 1e3 + 0.8246 / 3246.6 * 1e3 + (0.807 + 0.671) / 6544 * 1e3
+    assert abs(r["floor_ms"] - want) < 1e-3 and abs(r["frac"] - want / 0.565) < 1e-3 and r["unaccounted"] == []
+    W.overlap = False   # in order: the same sum (every pair here is HBM-bound)
+    assert abs(bench.step_roofline(W, names, info, peaks, 0.565)["floor_ms"] - want) < 1e-3
+    r = bench.step_roofline(W, names + ["halo"], info, peaks, 0.565)
+    assert r["unaccounted"] == ["halo"]
