@@ -473,13 +473,16 @@ ne_status ne_op_permute_inner_check(const ne_config* cfg, ne_cstreams x, const i
 
 /* The same op as a partitioned scatter-reduce, without a random DRAM gather
  * (k_permute_bucket.cu): the pairs (i, perm[i]) are partitioned into cells
- * (source window perm[i] >> S, destination range of output blocks) by a
- * count, a scan and a scatter pass over perm (coalesced); then one CTA per
- * destination range walks its cells window by window — every CTA reads the
- * same window of x, which stays in L2 — and adds each pair's M products
- * x_m[perm[i]] * v[i mod vlen] into its shared-memory block sums (int64 sums
- * mod 2^64, so delta is bit-identical to the gather form), written once;
- * then ne_disentangle_check on delta.  x AoS only (x_aos[n*M + m], 16-byte
+ * (source window perm[i] >> S, destination range of output blocks) by one
+ * scatter pass over perm (coalesced; a chunk's pairs sorted in shared
+ * memory); then one CTA per destination range walks its cells window by
+ * window — every CTA reads the same window of x, which stays in L2 — and
+ * adds each pair's M products x_m[perm[i]] * v[i mod vlen] into its block
+ * sums (int64 sums mod 2^64, so delta is bit-identical to the gather form),
+ * written once; then ne_disentangle_check on delta.  Two plans (which one:
+ * ne_permute_inner_plan): owned runs (each block's pairs one run per cell,
+ * each block summed by one thread, no atomics; power-of-two blocks dividing
+ * 4096) or shared-memory block sums with 32-bit shared atomics.  x AoS only (x_aos[n*M + m], 16-byte
  * aligned), M <= 8 (NE_ENOTSUP otherwise), perm required and a bijection of
  * [0, n_total): entries outside it are range violations in diag (first_bad =
  * i) and skipped.  delta (required) receives the block sums.  workspace:
