@@ -1,0 +1,9 @@
+# r02z48: end-of-session validation of HEAD: whole GPU suite, smoke, default bench line, reference arm
+O=gpurun_out/r02z48; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo build rc=$?
+timeout 2400 python -m pytest tests -m gpu -q > $O/gpu_tests.log 2>&1; echo tests rc=$?
+tail -2 $O/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke rc=$?
+timeout 900 python bench.py > $O/b_default.json 2> $O/b_default.err; echo default rc=$?
+timeout 600 python bench.py --impl reference > $O/b_ref.json 2> $O/b_ref.err; echo ref rc=$?
+python -c "import json; d=json.load(open('$O/b_default.json')); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['step_roofline']['frac'], d['correctness']['oracle_rows_equal'], {k: c.get('value') for k, c in d['configs'].items()})"
