@@ -108,7 +108,11 @@ k_scale_add_check(const __grid_constant__ ne_streams x, const __grid_constant__ 
 // over thread groups — 256 x M threads per block, one stream per thread, two
 // accumulators — to raise occupancy at C2's 256 blocks measured slower: C2
 // 10.0 -> 15.8 us, M = 3 T = 1000 54.7 -> 134.6 us; the per-output form
-// shares each tap load over M MACs.)
+// shares each tap load over M MACs.  Late r02: 64 threads x 4 consecutive
+// outputs per tile with the window sliding through registers (a quarter of
+// the shared loads) measured slower too — C2 9.9 -> 14.3 us, M = 8 19.0 ->
+// 34.2, T = 300 22.2 -> 34.6 (scripts/r02/z49.sh): the tile's window load,
+// spread over 4x fewer threads, is what the kernel waits on.)
 constexpr int kTCc = 256;
 
 template <int MT, int P>
