@@ -146,15 +146,43 @@ k_conv_check(const __grid_constant__ ne_cstreams x, const __grid_constant__ ne_s
     base %= N;
     if (base < 0) base += N;
     int fits = 1;
+#ifndef NE_CONV_WLOAD2  // r02 A/B (scripts/r02/z50.sh): C2 10.1 -> 9.9 us, M = 8 18.8 -> 18.0, T = 300 equal
+#define NE_CONV_WLOAD2 1
+#endif
+    if (NE_CONV_WLOAD2 && wlen <= 512) {
+      // every stream's (at most two) window values loaded before any is stored: one load latency
+      int64_t v[MT][2];
 #pragma unroll
-    for (int m = 0; m < MT; ++m) {
-      for (int q = threadIdx.x; q < wlen; q += 256) {
-        int64_t idx = base + q;
-        if (idx >= N) idx %= N;
-        const int64_t val = __ldg(x.s[m] + idx);
-        xs[m * WS + q] = val;
-        xs32[m * WS + q] = (int32_t)val;
-        fits &= (val == (int64_t)(int32_t)val);
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int q = threadIdx.x + 256 * k;
+          int64_t idx = base + q;
+          if (idx >= N) idx %= N;
+          v[m][k] = q < wlen ? __ldg(x.s[m] + idx) : 0;
+        }
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int q = threadIdx.x + 256 * k;
+          if (q < wlen) {
+            xs[m * WS + q] = v[m][k];
+            xs32[m * WS + q] = (int32_t)v[m][k];
+            fits &= (v[m][k] == (int64_t)(int32_t)v[m][k]);
+          }
+        }
+    } else {
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        for (int q = threadIdx.x; q < wlen; q += 256) {
+          int64_t idx = base + q;
+          if (idx >= N) idx %= N;
+          const int64_t val = __ldg(x.s[m] + idx);
+          xs[m * WS + q] = val;
+          xs32[m * WS + q] = (int32_t)val;
+          fits &= (val == (int64_t)(int32_t)val);
+        }
       }
     }
     fits = __syncthreads_and(fits);
