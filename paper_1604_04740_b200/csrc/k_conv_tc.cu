@@ -45,7 +45,9 @@ static int64_t conv_plane_len(int64_t n, int64_t taps, int W) {
 // N = 10^6, T = 4500, M = 8 / 3: 18.0 / 10.2 us here): one aligned 128-bit
 // load per lane with a funnel shift across lanes (22.2 / 12.4), every
 // stream's loads issued before any store (18.2 / 9.9), one thread per
-// (stream, quad) (20.5 / 11.3).  The kernel costs ~6 us fixed + ~1.5 us per
+// (stream, quad) (20.5 / 11.3); r02z52 (base 16.5 / 10.2 that box): stream
+// m + 1's loads issued before stream m is digitised 18.5 / 10.5, a one-wave
+// grid of 148 x 4 CTAs 18.7 / 10.5, both 20.6 / 12.1.  The kernel costs ~6 us fixed + ~1.5 us per
 // stream: a launch-latency-dominated pass of 6 MB per stream.
 // The range assertion (a0) counts every position once: t in [s0, s0 + N).
 #ifndef NE_CP_PF
