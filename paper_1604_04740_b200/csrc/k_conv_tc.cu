@@ -50,12 +50,6 @@ static int64_t conv_plane_len(int64_t n, int64_t taps, int W) {
 // grid of 148 x 4 CTAs 18.7 / 10.5, both 20.6 / 12.1.  The kernel costs ~6 us fixed + ~1.5 us per
 // stream: a launch-latency-dominated pass of 6 MB per stream.
 // The range assertion (a0) counts every position once: t in [s0, s0 + N).
-#ifndef NE_CP_PF
-#define NE_CP_PF 0
-#endif
-#ifndef NE_CP_GRID  // 1: one wave of resident CTAs (148 SMs x NE_CP_MINB), grid-stride over quads
-#define NE_CP_GRID 0
-#endif
 #ifndef NE_CP_MINB  // >= 4 CTAs per SM (<= 64 registers): r02 A/B (scripts/r02/z41.sh), M = 8 / 3:
 #define NE_CP_MINB 4  // 1 (76 regs) 18.2 / 11.1 us, 4 (58) 17.6 / 10.0, 6 (40, spills) 18.6 / 11.5, 8 (32) 20.1 / 12.0
 #endif
@@ -93,26 +87,10 @@ k_entangle_conv_planes(const __grid_constant__ ne_cstreams32 c, int M_rt, int l,
     int32_t prv[4], cur[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) prv[u] = __ldg(c.s[M - 1] + pos[u]);
-#if NE_CP_PF
-    // one stream ahead: stream m + 1's loads are in flight while stream m is
-    // digitised and stored (two load latencies overlap instead of M in series)
-    int32_t nxt[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) nxt[u] = __ldg(c.s[0] + pos[u]);
-#endif
 #pragma unroll 1
     for (int m = 0; m < M; ++m) {
-#if NE_CP_PF
-#pragma unroll
-      for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
-      if (m + 1 < M) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) nxt[u] = __ldg(c.s[m + 1] + pos[u]);
-      }
-#else
 #pragma unroll
       for (int u = 0; u < 4; ++u) cur[u] = __ldg(c.s[m] + pos[u]);
-#endif
       uint32_t w[4] = {0, 0, 0, 0};
       unsigned badm = 0;  // bit u: position u out of range / not representable
       if (pair) {
@@ -317,8 +295,7 @@ extern "C" ne_status ne_entangle_limbs_conv(const ne_config* cfg, ne_cstreams32 
   const int64_t plen = conv_plane_len(n_total, taps, block);
   const int64_t s0 = correlate ? 0 : (int64_t)taps - 1;
   const int64_t s0m = s0 % n_total;
-  int grid = grid_for(plen / 4, kThreads);
-  if (NE_CP_GRID) grid = grid < 148 * NE_CP_MINB ? grid : 148 * NE_CP_MINB;
+  const int grid = grid_for(plen / 4, kThreads);
   cudaStream_t s = cs(stream);
   const int64_t hi = range_hi(cfg);
   switch (cfg->M) {
