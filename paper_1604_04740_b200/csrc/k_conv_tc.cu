@@ -47,7 +47,9 @@ static int64_t conv_plane_len(int64_t n, int64_t taps, int W) {
 // stream's loads issued before any store (18.2 / 9.9), one thread per
 // (stream, quad) (20.5 / 11.3); r02z52 (base 16.5 / 10.2 that box): stream
 // m + 1's loads issued before stream m is digitised 18.5 / 10.5, a one-wave
-// grid of 148 x 4 CTAs 18.7 / 10.5, both 20.6 / 12.1.  The kernel costs ~6 us fixed + ~1.5 us per
+// grid of 148 x 4 CTAs 18.7 / 10.5, both 20.6 / 12.1.  r02z54: warp-coalesced loads (lane
+// loads t0 + lane + 32 u, digit bytes re-packed through a per-warp shared
+// row) 18.6 / 10.7 vs 16.6 / 10.3 (parity green, dropped).  The kernel costs ~6 us fixed + ~1.5 us per
 // stream: a launch-latency-dominated pass of 6 MB per stream.
 // The range assertion (a0) counts every position once: t in [s0, s0 + N).
 #ifndef NE_CP_MINB  // >= 4 CTAs per SM (<= 64 registers): r02 A/B (scripts/r02/z41.sh), M = 8 / 3:
