@@ -213,7 +213,11 @@ k_entangle_limbs(const __grid_constant__ ne_cstreams32 c, int M_rt, int l, int64
 // -2^31.  Range failures (|c| > hi, digit out of int8) take a slow path.
 // (r02 A/B, C3's 3 x 4096^2 operand, L2 flushed: 55.3 us = 5.46 TB/s; 16
 // positions per thread with 128-bit plane stores 57.3 us — fewer resident
-// threads for the same bytes in flight.)
+// threads for the same bytes in flight.)  The plane stores stay evict-first:
+// ordinary stores of the planes and of prep_b's Bt, so the GEMM would find
+// part of them in L2, took the C3 step from 0.5614 to 0.566-0.575 ms (three
+// alternating default lines, r02z55: GEMM 0.283-0.289 vs 0.287-0.295 ms, the
+// entangle 0.061 vs 0.058 ms).
 __device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32_t d) {
   return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
 }
